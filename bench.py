@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Benchmark: enhanced-DPSO particle-iterations/s at N=1000 viewpoints.
+
+One "step" = one generation of the whole swarm (update -> mutation every
+3rd generation -> gbest select -> 2-opt when gbest stalled -> finalize),
+i.e. P particle-iterations, on synthetic input resident in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c2|c1|c3|c4|c5]
+
+Default workload = BASELINE.json configs[1] (the metric's N=1000 case):
+random-Euclidean N=1000 extended TSP (conftest.py:27-31 generator,
+default_rng(1000)), swarm P=1024, paper defaults (w=1, phi1=phi2=0.4,
+mutation every 3 gens, 2-opt on stall), numpy-exact PCG64 streams.
+
+Timing: W untimed warm-up generations, then K generations each bracketed by
+CUDA events on the launching stream, with an L2 flush (256 MiB write)
+between timed generations, outside the events; barrier + synchronize around
+the timed region; max over ranks.  Multi-GPU: island model (one swarm per
+rank, gbest exchanged over NCCL every --exchange-every generations;
+"scaling": "weak").  ``--impl reference`` times the oracle port of the
+reference CPU algorithm (oracle/dpso_oracle.py) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle-iterations/sec at N=1000 viewpoints"
+UNIT = "particle-iterations/s"
+
+CONFIGS = {
+    "c1": dict(n=15, P=32, G=100, matrix="wall",
+               workload="C1: pkg/scenes/wall.json (N=15) via the reference "
+                        "pipeline, P=32, G=100, boustrophedon seed"),
+    "c2": dict(n=1000, P=1024, G=500, matrix="euclid",
+               workload="C2: synthetic N=1000 extended TSP (random Euclidean,"
+                        " default_rng(1000)), swarm P=1024, 500-generation "
+                        "schedule, enhanced DPSO (paper defaults)"),
+    "c3": dict(n=500, P=16384, G=100, matrix="grid",
+               workload="C3: bridge-sized synthetic instance N=500 (integer "
+                        "grid costs, many ties), swarm P=16384"),
+    "c4": dict(n=2000, P=65536, G=50, matrix="euclid",
+               workload="C4: synthetic N=2000 extended TSP, P=65536"),
+    "c5": dict(n=10000, P=65536, G=20, matrix="euclid", ee=False,
+               workload="C5: synthetic N=10000, P=65536 per GPU, islands, "
+                        "use_edge_exchange=False"),
+}
+
+
+def make_matrix(cfg):
+    import numpy as np
+    n = cfg["n"]
+    if cfg["matrix"] == "wall":
+        with open(os.path.join(ROOT, "tests", "golden",
+                               "golden_e2e.json")) as fh:
+            g = json.load(fh)
+        return np.array(g["matrices"]["wall"], dtype=float), \
+            g["seed_tours"]["wall"]
+    rng = np.random.default_rng(1000)
+    if cfg["matrix"] == "grid":
+        side = int(math.ceil(math.sqrt(n)))
+        idx = np.arange(n)
+        pts = np.stack([idx % side, idx // side], 1).astype(float)
+        d = np.abs(pts[:, None, :] - pts[None, :, :]).sum(-1)
+        return d, None
+    pts = rng.random((n, 2)) * 10.0
+    c = np.sqrt(((pts[:, None, :] - pts[None, :, :]) ** 2).sum(-1))
+    np.fill_diagonal(c, 0.0)
+    return c, None
+
+
+def solver_params(cfg, P, G, seed):
+    return dict(n_particles=P, max_generations=G, stall_generations=G,
+                use_edge_exchange=cfg.get("ee", True), random_state=seed)
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,"
+              "clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [],
+                    "samples": 0}
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap")
+        reasons = sorted({names[i] for _, _, fl in rows
+                          for i, f in enumerate(fl) if f.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows),
+                "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------ cpu baseline
+def cpu_sample(cost, cfg, P_cpu=32, budget_s=12.0, max_gens=12, warm=1,
+               seed=0, seed_tour=None):
+    """Oracle port of the reference (single thread) on a bounded sample:
+    P_cpu particles of the same matrix; returns (rate, gens, seconds)."""
+    from oracle.dpso_oracle import OracleSolver
+    s = OracleSolver(**solver_params(cfg, P_cpu, 10 ** 6, seed),
+                     seed_tour=seed_tour)
+    s.start(cost)
+    for _ in range(warm):
+        s.generation()
+    t0 = time.perf_counter()
+    g = 0
+    while g < max_gens:
+        s.generation()
+        g += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return P_cpu * g / dt, g, dt
+
+
+def _ref_worker(args):
+    cfg_name, steps, warmup, seed = args
+    cfg = CONFIGS[cfg_name]
+    cost, seed_tour = make_matrix(cfg)
+    from oracle.dpso_oracle import OracleSolver
+    s = OracleSolver(**solver_params(cfg, 32, 10 ** 6, seed),
+                     seed_tour=seed_tour)
+    s.start(cost)
+    for _ in range(warmup):
+        s.generation()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        s.generation()
+    return 32 * steps, time.perf_counter() - t0
+
+
+def run_reference(args, cfg_name, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    steps = args.steps
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(cores) as pool:
+        res = pool.map(_ref_worker, [(cfg_name, steps, args.warmup, 100 + i)
+                                     for i in range(cores)])
+    wall = time.perf_counter() - t0
+    work = sum(r[0] for r in res)
+    tmax = max(r[1] for r in res)
+    value = work / tmax
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tmax / steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": config_dict(cfg_name, cfg, args),
+        "cpu_baseline": {
+            "value": value, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": (f"{cores} concurrent processes of the oracle port "
+                       f"(oracle/dpso_oracle.py, single-threaded Python+numpy"
+                       f" like the reference), each a 32-particle swarm on "
+                       f"the same matrix, {args.warmup} warm-up + {steps} "
+                       f"timed generations; one step = one generation of "
+                       f"each 32-particle sample (wall {wall:.1f}s)")},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(cfg_name, cfg, args):
+    return {"workload": cfg["workload"], "config": cfg_name, "n": cfg["n"],
+            "particles_per_gpu": cfg["P"], "global_particles":
+                cfg["P"] * args.gpus,
+            "generation_schedule": cfg["G"],
+            "parallelism": f"islands{args.gpus}" if args.gpus > 1 else "1gpu",
+            "exchange_every": args.exchange_every if args.gpus > 1 else None,
+            "rng": "numpy-pcg64-exact",
+            "l2": "flushed between timed steps (256 MiB write)"}
+
+
+# --------------------------------------------------------------- our arm
+def kernels_per_generation(cfg):
+    k = 2 + 1  # begin, update, select
+    k += 7  # mutation pipeline (no-op kernels on non-mutating generations)
+    if cfg.get("ee", True):
+        k += 3  # 2-opt scan, apply, finalize
+    return k
+
+
+def run_ours(args, cfg_name, cfg):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    from paper_1706_04399_b200 import DiscreteSwarmSolver
+    from paper_1706_04399_b200.islands import IslandExchange
+    from paper_1706_04399_b200.solver import numpy_stream_states
+
+    cost, seed_tour = make_matrix(cfg)
+    n, P = cost.shape[0], cfg["P"]
+    W, K = args.warmup, args.steps
+    G = W + K + args.profile_gens + 1
+    params = solver_params(cfg, P, G, 1000 + rank)
+    if seed_tour is not None:
+        params["seed_tour"] = seed_tour
+    solver = DiscreteSwarmSolver(**params)
+    seed_body, n_seed = solver._seed(n)
+    ctx = solver._make_context(cost)
+    ctx.set_streams(numpy_stream_states(params["random_state"], P + 2))
+    ctx.init(seed_body, n_seed)
+    ex = IslandExchange(ctx, n) if world > 1 else None
+
+    ctx.step(W)
+    torch.cuda.synchronize()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(K):
+            flush.fill_(k & 0xFF)
+            ev[k][0].record(stream)
+            ctx.step(1)
+            ev[k][1].record(stream)
+            if ex is not None and (k + 1) % args.exchange_every == 0:
+                torch.cuda.synchronize()
+                ex.exchange()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    value = P * K * world / (total_ms / 1e3)
+
+    # live per-phase kernel timing for the roofline (CUDA events on the
+    # launching stream, same generations continued)
+    c0 = ctx.ctl()
+    prof_gens = args.profile_gens
+    phase_ms, cnt = ctx.step_timed(prof_gens)
+    fired = cnt - c0["two_opt_count"]
+    names = ["update", "mutation", "select", "two_opt_scan", "two_opt_apply",
+             "finalize"]
+    phases = {k: v / prof_gens for k, v in zip(names, phase_ms)}
+    ctx.close()
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except Exception:
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    scan_bytes = P * 4.0 * n * (n - 1)  # 8 B x n(n-1)/2 unique pair entries
+    upd_bytes = P * 26.0 * n           # update 16n + fitness 10n
+    if cfg.get("ee", True) and fired > 0:
+        dom, dur_ms, alg = "two_opt_scan", phase_ms[3] / fired, scan_bytes
+    else:
+        dom, dur_ms, alg = "update", phase_ms[0] / prof_gens, upd_bytes
+    achieved = alg / (dur_ms / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            tr = json.load(fh)
+        key = f"{cfg_name}:{dom}"
+        if key in tr:
+            traffic = tr[key]
+    except Exception:
+        pass
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": total_ms / K,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": config_dict(cfg_name, cfg, args),
+        "gpu_launches": kernels_per_generation(cfg) * K,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved,
+                     "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": traffic,
+                     "algorithmic_bytes_per_launch": alg,
+                     "avg_launch_ms": dur_ms,
+                     "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json"
+                                    "); the cost matrix is L2-resident, so "
+                                    "this kernel is L2-gather bound"},
+        "phase_ms_per_gen": phases,
+        "two_opt_fired": f"{fired}/{prof_gens}",
+    }
+    # clocks
+    line["clocks"] = clk.summary()
+
+    # e2e through the public API with host buffers (H2D of the matrix and
+    # RNG states, D2H of tour + convergence inside the timed region)
+    if not args.no_e2e:
+        Ge = cfg["G"]
+        ep = solver_params(cfg, P, Ge, 7)
+        if seed_tour is not None:
+            ep["seed_tour"] = seed_tour
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s = DiscreteSwarmSolver(**ep).fit(cost)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        gens = s.n_generations_
+        h2d = cost.nbytes + (P + 2) * 48 + (2 * n if seed_tour else 0)
+        d2h = 4 * (n + 1) + 8 * (gens + 1)
+        line["e2e"] = {"value": P * gens / dt, "unit": UNIT,
+                       "h2d_bytes_per_step": h2d / gens,
+                       "d2h_bytes_per_step": d2h / gens,
+                       "generations": gens, "wall_s": dt,
+                       "api": "DiscreteSwarmSolver.fit(host numpy matrix)"}
+
+    if not args.no_cpu_baseline and world == 1:
+        rate, g, dt = cpu_sample(cost, cfg, seed_tour=seed_tour)
+        line["cpu_baseline"] = {
+            "value": rate, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": (f"oracle port (oracle/dpso_oracle.py) of the reference"
+                       f" solve, 32-particle swarm on the same matrix, 1 warm"
+                       f"-up + {g} timed generations ({dt:.1f}s), 1 thread")}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--exchange-every", type=int, default=10)
+    ap.add_argument("--profile-gens", type=int, default=6)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, args.config, cfg)
+    else:
+        run_ours(args, args.config, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,153 @@
+/*
+ * dpso.h — C ABI of the B200-native enhanced discrete PSO solve path.
+ *
+ * This is the drop-in boundary for the reference's DPSO solve call
+ * (`DiscreteSwarmSolver.fit`, /root/reference/pkg/src/inspectour/solver.py:262-335,
+ * and `solve_matrix`, solver.py:352-356).  The reference is pure Python, so
+ * its "FFI" is the estimator API; the Python host layer
+ * (paper_1706_04399_b200/solver.py) binds these symbols with ctypes, and
+ * INTEGRATION.md shows that binding.  Plain pointers and sizes only.
+ *
+ * Memory ownership: the caller allocates one device workspace of
+ * dpso_workspace_size() bytes (e.g. a torch uint8 tensor) and the device
+ * cost matrix; the library never allocates large device memory itself
+ * (only a private stream, events and a CUDA graph).  Host arrays are
+ * ordinary pageable or pinned buffers.
+ *
+ * Return codes: 0 ok, 1 invalid argument (Python: ValueError, same messages
+ * as solver.py:139-172 where tests match them), 2 CUDA error (RuntimeError),
+ * 3 NCCL/island error (RuntimeError).  dpso_last_error() is thread-local.
+ */
+#ifndef DPSO_H_
+#define DPSO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DPSO_OK 0
+#define DPSO_EINVAL 1
+#define DPSO_ECUDA 2
+#define DPSO_ECOMM 3
+
+#define DPSO_RNG_NUMPY 0  /* PCG64 streams exactly as numpy: bit-exact runs  */
+#define DPSO_RNG_PHILOX 1 /* counter-based Philox4x32-10: fully parallel     */
+
+/* Constructor parameters of DiscreteSwarmSolver (solver.py:118-135). */
+typedef struct dpso_params {
+  int32_t n_particles;       /* >= 3 */
+  double inertia;            /* w in [0, 1] */
+  double cognitive;          /* phi1 in [0, 1] */
+  double social;             /* phi2 in [0, 1] */
+  int32_t max_generations;   /* >= 1 */
+  int32_t stall_generations; /* >= 1 */
+  int32_t mutation_period;   /* >= 1 */
+  double seed_fraction;      /* [0, 1] */
+  int32_t use_mutation;
+  int32_t use_edge_exchange;
+  int32_t parallel; /* accepted for API parity; results are identical */
+  int32_t rng_mode; /* DPSO_RNG_NUMPY | DPSO_RNG_PHILOX */
+  uint64_t philox_seed;
+} dpso_params;
+
+typedef struct dpso_ctx dpso_ctx;
+
+/* --- swarm solve (replaces DiscreteSwarmSolver.fit, solver.py:262-335) --- */
+
+/* Bytes of device workspace needed for n nodes. */
+int dpso_workspace_size(const dpso_params* prm, int32_t n, size_t* bytes);
+
+/* Bind a context to a caller-owned workspace and CUDA stream (may be NULL =
+ * legacy default stream; the library orders its private stream after it). */
+int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
+                size_t workspace_bytes, void* cuda_stream, dpso_ctx** out);
+
+/* Device cost matrix, row-major fp64, leading dimension ld >= n (elements).
+ * The caller owns it and must keep it alive while the context runs. */
+int dpso_set_cost(dpso_ctx* ctx, const double* dev_cost, int64_t ld);
+
+/* RNG streams for DPSO_RNG_NUMPY: (n_particles + 2) records of 6 uint64
+ * {state_hi, state_lo, inc_hi, inc_lo, has_uint32, uinteger}, in the order
+ * of SeedSequence(random_state).spawn(P + 2) (solver.py:278-282):
+ * [0] = init stream, [1] = mutation stream, [2..] = particle streams. */
+int dpso_set_streams(dpso_ctx* ctx, const uint64_t* host_states);
+
+/* _init_swarm (solver.py:166-188).  seed_body: NULL or n node ids (the open
+ * seed tour, already validated by the caller); n_seed as in solver.py:173. */
+int dpso_init(dpso_ctx* ctx, const int32_t* host_seed_body, int32_t n_seed);
+
+/* Run generations until max_generations or the stall break.  Blocks the
+ * calling thread; returns the number of generations run. */
+int dpso_run(dpso_ctx* ctx, int32_t* gens_run);
+
+/* Run exactly `gens` more generations (or fewer if the stall break fires);
+ * no host synchronisation.  Used by the benchmark to time single steps. */
+int dpso_step(dpso_ctx* ctx, int32_t gens);
+
+/* Like dpso_step, but launches each phase directly with CUDA events between
+ * phases and accumulates their device time (ms) into phase_ms[6]:
+ * begin+update, mutation, select, 2-opt scan, 2-opt apply, finalize.
+ * *two_opt_count = generations so far in which the 2-opt pass ran. */
+int dpso_step_timed(dpso_ctx* ctx, int32_t gens, double* phase_ms,
+                    int32_t* two_opt_count);
+
+/* Control record: out[6] = {gen, stall, done, gens_run, two_opt_count,
+ * n_mutation_events}; *gbest_fit = current global best fitness. */
+int dpso_ctl(dpso_ctx* ctx, int32_t* out, double* gbest_fit);
+
+/* Results: closed best tour (n + 1 ints), best fitness, convergence trace
+ * (capacity max_generations + 1; *n_conv = generations_run + 1). */
+int dpso_result(dpso_ctx* ctx, int32_t* host_tour, double* host_fitness,
+                double* host_convergence, int32_t* n_conv);
+
+/* Copy the full swarm state to host (parity tests): x, pbest as P*n int32;
+ * fit, pfit as P doubles; vmap as P*n int32 (identity when inertia < 1). */
+int dpso_get_state(dpso_ctx* ctx, int32_t* x, int32_t* pbest, double* fit,
+                   double* pfit, int32_t* vmap, int32_t* gbest,
+                   double* gbest_fit);
+int dpso_set_state(dpso_ctx* ctx, const int32_t* x, const int32_t* pbest,
+                   const double* fit, const double* pfit, const int32_t* vmap,
+                   const int32_t* gbest, double gbest_fit);
+
+/* Island exchange (multi-GPU): overwrite gbest when `fitness` is strictly
+ * better; the host layer moves the 16-byte records and tours with NCCL. */
+int dpso_offer_gbest(dpso_ctx* ctx, const int32_t* host_tour, double fitness);
+
+void dpso_destroy(dpso_ctx* ctx);
+const char* dpso_last_error(void);
+
+/* --- kernel-level entry points (the reference's private helpers) ------- */
+
+/* _tour_cost (solver.py:48-54) for `count` open tours of n nodes (device
+ * int32, row-major), written to dev_out.  Sequential reference order. */
+int dpso_tour_cost_batch(const double* dev_cost, int64_t ld, int32_t n,
+                         const int32_t* dev_tours, int32_t count,
+                         double* dev_out, void* cuda_stream);
+
+/* _best_exchange (solver.py:88-106) for `count` tours: best 2-opt move with
+ * first-index tie break; tours are rewritten in place when the move is
+ * strictly improving (< -1e-12), dev_delta gets the delta or 0.0. */
+int dpso_best_exchange_batch(const double* dev_cost, int64_t ld, int32_t n,
+                             int32_t* dev_tours, int32_t count,
+                             double* dev_delta, void* cuda_stream);
+
+/* Nearest-neighbour construction of baselines.py:110-116 (from `start`,
+ * ties to the smallest index); host_tour gets n ids. */
+int dpso_nn_tour(const double* dev_cost, int64_t ld, int32_t n, int32_t start,
+                 int32_t* host_tour, void* cuda_stream);
+
+/* nearest_neighbor_two_opt (baselines.py:103-123): NN tour then
+ * best-improvement 2-opt to a fixed point, all on the device. */
+int dpso_nn_two_opt(const double* dev_cost, int64_t ld, int32_t n,
+                    int32_t* host_tour, double* host_cost, void* cuda_stream);
+
+/* Build/version string. */
+const char* dpso_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DPSO_H_ */

@@ -1,0 +1,17 @@
+"""B200-native enhanced discrete PSO solve path (arXiv 1706.04399).
+
+Drop-in for the reference's DPSO solve call (``inspectour.solver``):
+``DiscreteSwarmSolver``, ``SolveReport``, ``solve_matrix``; plus the device
+versions of the helpers the reference's baselines and tests use.
+"""
+from .solver import DiscreteSwarmSolver, SolveReport, solve_matrix
+from .kernels import (best_exchange_batch, nearest_neighbor_tour,
+                      nearest_neighbor_two_opt, tour_cost_batch)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "DiscreteSwarmSolver", "SolveReport", "solve_matrix",
+    "best_exchange_batch", "nearest_neighbor_tour",
+    "nearest_neighbor_two_opt", "tour_cost_batch",
+]

@@ -1,0 +1,730 @@
+// C ABI (include/dpso.h): context lifecycle, workspace layout, the
+// device-resident generation loop and the kernel-level entry points.
+//
+// One generation (solver.py:292-328) is a fixed sequence of launches that all
+// read their control flags from device memory (DevCtl), so it is captured
+// once into a CUDA graph and replayed; data-dependent branches (mutation
+// period, 2-opt trigger, stall break) are flags checked at kernel entry.  The
+// host polls `done` once per batch of generations.
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "dpso_internal.cuh"
+
+using namespace dpso;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  std::string m = std::string(where) + ": " + cudaGetErrorString(e);
+  return fail(DPSO_ECUDA, m);
+}
+
+#define CK(call)                                        \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+struct Layout {
+  size_t off_ctl, off_streams, off_mut_start, off_x, off_pbest, off_vmap,
+      off_vel, off_vel_len, off_fit, off_pfit, off_dcache, off_gbest,
+      off_conv, off_tores, off_chunk_row, off_rank, off_hash, off_flag,
+      off_sidx, off_order, off_surv, off_keep, off_ev_slot, off_ev_k,
+      off_ev_cursor, off_init_cursor, off_seed, total;
+  int64_t vel_cap;
+  int chunks;
+};
+
+int64_t vel_capacity(const dpso_params* p, int n) {
+  if (p->inertia >= 1.0) return 0;
+  double cap = (2.0 * n + 1.0) / (1.0 - p->inertia) + 8.0;
+  if (cap > 64.0 * n + 64) cap = 64.0 * n + 64;  // bound memory; overflow flagged
+  return (int64_t)cap;
+}
+
+Layout make_layout(const dpso_params* prm, int n) {
+  Layout L;
+  const int64_t P = prm->n_particles;
+  const int64_t np = round_up(n, 8);
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o = round_up(o + bytes, 256);
+    return at;
+  };
+  L.chunks = two_opt_pick_chunks(n, (int32_t)P);
+  L.vel_cap = vel_capacity(prm, n);
+  L.off_ctl = take(sizeof(DevCtl));
+  L.off_streams = take(sizeof(PcgState) * (P + 2));
+  L.off_mut_start = take(sizeof(PcgState));
+  L.off_x = take(2 * P * np);
+  L.off_pbest = take(2 * P * np);
+  L.off_vmap = take(prm->inertia == 1.0 ? 2 * P * np : 0);
+  L.off_vel = take(L.vel_cap ? 4 * P * (L.vel_cap + 2 * (int64_t)n) : 0);
+  L.off_vel_len = take(4 * P);
+  L.off_fit = take(8 * P);
+  L.off_pfit = take(8 * P);
+  L.off_dcache = take(8 * P * np);
+  L.off_gbest = take(2 * np);
+  L.off_conv = take(8 * ((int64_t)prm->max_generations + 1));
+  L.off_tores = take(sizeof(TwoOptRes) * P * L.chunks);
+  L.off_chunk_row = take(4 * (L.chunks + 1));
+  L.off_rank = take(4 * P);
+  L.off_hash = take(8 * P);
+  L.off_flag = take(4 * P);
+  L.off_sidx = take(4 * P);
+  L.off_order = take(4 * P);
+  L.off_surv = take(4 * P);
+  L.off_keep = take(4 * P);
+  L.off_ev_slot = take(4 * P);
+  L.off_ev_k = take(4 * P);
+  L.off_ev_cursor = take(8 * P);
+  L.off_init_cursor = take(8 * P);
+  L.off_seed = take(2 * np);
+  L.total = o;
+  return L;
+}
+
+int check_params(const dpso_params* p, int n) {
+  // messages follow solver.py:139-153
+  if (!p) return fail(DPSO_EINVAL, "params is NULL");
+  if (p->n_particles < 3) return fail(DPSO_EINVAL, "n_particles must be >= 3");
+  const char* names[3] = {"inertia", "cognitive", "social"};
+  double vals[3] = {p->inertia, p->cognitive, p->social};
+  for (int i = 0; i < 3; ++i)
+    if (!(vals[i] >= 0.0 && vals[i] <= 1.0)) {
+      char buf[128];
+      snprintf(buf, sizeof buf, "%s must be in [0, 1], got %g", names[i],
+               vals[i]);
+      return fail(DPSO_EINVAL, buf);
+    }
+  if (p->max_generations < 1)
+    return fail(DPSO_EINVAL, "max_generations must be >= 1");
+  if (p->stall_generations < 1)
+    return fail(DPSO_EINVAL, "stall_generations must be >= 1");
+  if (p->mutation_period < 1)
+    return fail(DPSO_EINVAL, "mutation_period must be >= 1");
+  if (!(p->seed_fraction >= 0.0 && p->seed_fraction <= 1.0))
+    return fail(DPSO_EINVAL, "seed_fraction must be in [0, 1]");
+  if (n < 2 || n > kMaxN)
+    return fail(DPSO_EINVAL, "n must be in [2, 65535] for the device path");
+  if (p->rng_mode != DPSO_RNG_NUMPY && p->rng_mode != DPSO_RNG_PHILOX)
+    return fail(DPSO_EINVAL, "unknown rng_mode");
+  return DPSO_OK;
+}
+
+}  // namespace
+
+struct dpso_ctx {
+  dpso_params prm;
+  int n;
+  Layout L;
+  unsigned char* ws;
+  cudaStream_t user;
+  cudaStream_t stream;
+  cudaEvent_t ev;
+  cudaGraphExec_t graph;
+  bool have_cost, have_streams, initialized;
+  SwarmView v;
+  DevCtl* host_ctl;  // pinned
+};
+
+static int sync_in(dpso_ctx* c) {
+  CK(cudaEventRecord(c->ev, c->user));
+  CK(cudaStreamWaitEvent(c->stream, c->ev, 0));
+  return DPSO_OK;
+}
+static int sync_out(dpso_ctx* c) {
+  CK(cudaEventRecord(c->ev, c->stream));
+  CK(cudaStreamWaitEvent(c->user, c->ev, 0));
+  return DPSO_OK;
+}
+
+static cudaError_t enqueue_generation(const SwarmView& v, cudaStream_t s) {
+  cudaError_t e = launch_gen_begin(v, s);
+  if (e) return e;
+  if ((e = launch_update(v, s))) return e;
+  if (v.use_mutation && (e = launch_mutation(v, s))) return e;
+  if (v.use_edge_exchange) {
+    if ((e = launch_select(v, false, s))) return e;
+    if ((e = launch_two_opt(v, s))) return e;
+    if ((e = launch_finalize(v, s))) return e;
+  } else {
+    if ((e = launch_select(v, true, s))) return e;
+  }
+  return cudaSuccess;
+}
+
+extern "C" {
+
+const char* dpso_last_error(void) { return g_err.c_str(); }
+
+const char* dpso_version(void) {
+  return "paper_1706_04399_b200 dpso 0.1.0 (sm_100a)";
+}
+
+int dpso_workspace_size(const dpso_params* prm, int32_t n, size_t* bytes) {
+  int rc = check_params(prm, n);
+  if (rc) return rc;
+  *bytes = make_layout(prm, n).total;
+  return DPSO_OK;
+}
+
+int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
+                size_t workspace_bytes, void* cuda_stream, dpso_ctx** out) {
+  int rc = check_params(prm, n);
+  if (rc) return rc;
+  if (prm->rng_mode == DPSO_RNG_PHILOX)
+    return fail(DPSO_EINVAL, "rng_mode philox is not available in this build");
+  Layout L = make_layout(prm, n);
+  if (!dev_workspace || workspace_bytes < L.total)
+    return fail(DPSO_EINVAL, "workspace too small");
+  dpso_ctx* c = new dpso_ctx();
+  c->prm = *prm;
+  c->n = n;
+  c->L = L;
+  c->ws = (unsigned char*)dev_workspace;
+  c->user = (cudaStream_t)cuda_stream;
+  c->graph = nullptr;
+  c->have_cost = c->have_streams = c->initialized = false;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e) {
+    delete c;
+    return cuda_fail(e, "cudaStreamCreate");
+  }
+  cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming);
+  cudaMallocHost(&c->host_ctl, sizeof(DevCtl));
+  SwarmView& v = c->v;
+  memset(&v, 0, sizeof v);
+  v.n = n;
+  v.np = (int32_t)round_up(n, 8);
+  v.P = prm->n_particles;
+  v.max_generations = prm->max_generations;
+  v.stall_generations = prm->stall_generations;
+  v.mutation_period = prm->mutation_period;
+  v.use_mutation = prm->use_mutation ? 1 : 0;
+  v.use_edge_exchange = prm->use_edge_exchange ? 1 : 0;
+  v.rng_mode = prm->rng_mode;
+  v.philox_seed = prm->philox_seed;
+  v.inertia = prm->inertia;
+  v.cognitive = prm->cognitive;
+  v.social = prm->social;
+  unsigned char* w = c->ws;
+  v.ctl = (DevCtl*)(w + L.off_ctl);
+  v.streams = (PcgState*)(w + L.off_streams);
+  v.mut_start = (PcgState*)(w + L.off_mut_start);
+  v.x = (uint16_t*)(w + L.off_x);
+  v.pbest = (uint16_t*)(w + L.off_pbest);
+  v.vmap = prm->inertia == 1.0 ? (uint16_t*)(w + L.off_vmap) : nullptr;
+  v.vel = L.vel_cap ? (uint32_t*)(w + L.off_vel) : nullptr;
+  v.vel_len = (int32_t*)(w + L.off_vel_len);
+  v.vel_cap = L.vel_cap;
+  v.fit = (double*)(w + L.off_fit);
+  v.pfit = (double*)(w + L.off_pfit);
+  v.dcache = (double*)(w + L.off_dcache);
+  v.gbest = (uint16_t*)(w + L.off_gbest);
+  v.conv = (double*)(w + L.off_conv);
+  v.tores = (TwoOptRes*)(w + L.off_tores);
+  v.chunks = L.chunks;
+  v.chunk_row = (int32_t*)(w + L.off_chunk_row);
+  v.rank = (int32_t*)(w + L.off_rank);
+  v.hash = (uint64_t*)(w + L.off_hash);
+  v.flag = (int32_t*)(w + L.off_flag);
+  v.sidx = (int32_t*)(w + L.off_sidx);
+  v.order = (int32_t*)(w + L.off_order);
+  v.surv_list = (int32_t*)(w + L.off_surv);
+  v.keep = (int32_t*)(w + L.off_keep);
+  v.ev_slot = (int32_t*)(w + L.off_ev_slot);
+  v.ev_k = (int32_t*)(w + L.off_ev_k);
+  v.ev_cursor = (uint64_t*)(w + L.off_ev_cursor);
+  v.init_cursor = (uint64_t*)(w + L.off_init_cursor);
+  std::vector<int32_t> rows(L.chunks + 1);
+  two_opt_chunk_rows(n, L.chunks, rows.data());
+  if ((rc = sync_in(c))) {
+    dpso_destroy(c);
+    return rc;
+  }
+  e = cudaMemcpyAsync(v.chunk_row, rows.data(), 4 * rows.size(),
+                      cudaMemcpyHostToDevice, c->stream);
+  if (!e) e = cudaMemsetAsync(v.ctl, 0, sizeof(DevCtl), c->stream);
+  if (!e) e = cudaStreamSynchronize(c->stream);
+  if (e) {
+    dpso_destroy(c);
+    return cuda_fail(e, "dpso_create");
+  }
+  *out = c;
+  return DPSO_OK;
+}
+
+int dpso_set_cost(dpso_ctx* c, const double* dev_cost, int64_t ld) {
+  if (!c || !dev_cost) return fail(DPSO_EINVAL, "null argument");
+  if (ld < round_up(c->n, 2) || (ld & 1) || ((uintptr_t)dev_cost & 15))
+    return fail(DPSO_EINVAL,
+                "cost matrix needs an even ld >= n (padded) and 16-B "
+                "alignment");
+  c->v.cost = dev_cost;
+  c->v.ld = ld;
+  c->have_cost = true;
+  if (c->graph) {
+    cudaGraphExecDestroy(c->graph);
+    c->graph = nullptr;
+  }
+  return DPSO_OK;
+}
+
+int dpso_set_streams(dpso_ctx* c, const uint64_t* host_states) {
+  if (!c || !host_states) return fail(DPSO_EINVAL, "null argument");
+  const int64_t P = c->prm.n_particles;
+  int rc = sync_in(c);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(c->v.streams, host_states, sizeof(PcgState) * (P + 2),
+                     cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->have_streams = true;
+  return DPSO_OK;
+}
+
+int dpso_init(dpso_ctx* c, const int32_t* seed_body, int32_t n_seed) {
+  if (!c) return fail(DPSO_EINVAL, "null context");
+  if (!c->have_cost) return fail(DPSO_EINVAL, "cost matrix not set");
+  if (!c->have_streams) return fail(DPSO_EINVAL, "rng streams not set");
+  const int n = c->n;
+  if (n_seed < 0 || n_seed > c->prm.n_particles)
+    return fail(DPSO_EINVAL, "n_seed out of range");
+  if (n_seed > 0 && !seed_body)
+    return fail(DPSO_EINVAL, "seed_tour is not a tour over the matrix");
+  uint16_t* dseed = (uint16_t*)(c->ws + c->L.off_seed);
+  if (n_seed > 0) {
+    std::vector<uint16_t> s(n);
+    std::vector<char> seen(n, 0);
+    for (int i = 0; i < n; ++i) {
+      int32_t val = seed_body[i];
+      if (val < 0 || val >= n || seen[val])
+        return fail(DPSO_EINVAL, "seed_tour is not a tour over the matrix");
+      seen[val] = 1;
+      s[i] = (uint16_t)val;
+    }
+    int rc = sync_in(c);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(dseed, s.data(), 2 * n, cudaMemcpyHostToDevice,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  int rc = sync_in(c);
+  if (rc) return rc;
+  CK(launch_init(c->v, dseed, n_seed, c->stream));
+  CK(launch_init_best(c->v, c->stream));
+  c->initialized = true;
+  return sync_out(c);
+}
+
+static int ensure_graph(dpso_ctx* c) {
+  if (c->graph) return DPSO_OK;
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  cudaError_t e = enqueue_generation(c->v, c->stream);
+  cudaError_t e2 = cudaStreamEndCapture(c->stream, &g);
+  if (e) return cuda_fail(e, "capture generation");
+  if (e2) return cuda_fail(e2, "cudaStreamEndCapture");
+  e = cudaGraphInstantiate(&c->graph, g, 0);
+  cudaGraphDestroy(g);
+  if (e) return cuda_fail(e, "cudaGraphInstantiate");
+  return DPSO_OK;
+}
+
+int dpso_step(dpso_ctx* c, int32_t gens) {
+  if (!c || !c->initialized) return fail(DPSO_EINVAL, "context not initialized");
+  int rc = ensure_graph(c);
+  if (rc) return rc;
+  if ((rc = sync_in(c))) return rc;
+  for (int g = 0; g < gens; ++g) CK(cudaGraphLaunch(c->graph, c->stream));
+  return sync_out(c);
+}
+
+int dpso_step_timed(dpso_ctx* c, int32_t gens, double* phase_ms,
+                    int32_t* two_opt_count) {
+  // Same launches as one graph replay, issued directly with CUDA events
+  // between phases: [0] begin+update [1] mutation [2] select
+  // [3] 2-opt scan [4] 2-opt apply [5] finalize.
+  if (!c || !c->initialized) return fail(DPSO_EINVAL, "context not initialized");
+  int rc = sync_in(c);
+  if (rc) return rc;
+  const SwarmView& v = c->v;
+  cudaEvent_t ev[7];
+  for (int i = 0; i < 7; ++i) CK(cudaEventCreate(&ev[i]));
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  for (int g = 0; g < gens; ++g) {
+    cudaStream_t s = c->stream;
+    CK(cudaEventRecord(ev[0], s));
+    CK(launch_gen_begin(v, s));
+    CK(launch_update(v, s));
+    CK(cudaEventRecord(ev[1], s));
+    if (v.use_mutation) CK(launch_mutation(v, s));
+    CK(cudaEventRecord(ev[2], s));
+    CK(launch_select(v, !v.use_edge_exchange, s));
+    CK(cudaEventRecord(ev[3], s));
+    if (v.use_edge_exchange) CK(launch_two_opt(v, s, 1));
+    CK(cudaEventRecord(ev[4], s));
+    if (v.use_edge_exchange) CK(launch_two_opt(v, s, 2));
+    CK(cudaEventRecord(ev[5], s));
+    if (v.use_edge_exchange) CK(launch_finalize(v, s));
+    CK(cudaEventRecord(ev[6], s));
+    CK(cudaEventSynchronize(ev[6]));
+    for (int i = 0; i < 6; ++i) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+      acc[i] += ms;
+    }
+  }
+  for (int i = 0; i < 7; ++i) cudaEventDestroy(ev[i]);
+  if (phase_ms)
+    for (int i = 0; i < 6; ++i) phase_ms[i] = acc[i];
+  if (two_opt_count) {
+    DevCtl h;
+    CK(cudaMemcpy(&h, c->v.ctl, sizeof h, cudaMemcpyDeviceToHost));
+    *two_opt_count = h.two_opt_count;
+  }
+  return sync_out(c);
+}
+
+int dpso_ctl(dpso_ctx* c, int32_t* out /* gen, stall, done, gens_run,
+                                           two_opt_count, n_events */,
+             double* gbest_fit) {
+  if (!c) return fail(DPSO_EINVAL, "null context");
+  int rc = sync_in(c);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(c->stream));
+  DevCtl h;
+  CK(cudaMemcpy(&h, c->v.ctl, sizeof h, cudaMemcpyDeviceToHost));
+  if (out) {
+    out[0] = h.gen;
+    out[1] = h.stall;
+    out[2] = h.done;
+    out[3] = h.gens_run;
+    out[4] = h.two_opt_count;
+    out[5] = h.n_events;
+  }
+  if (gbest_fit) *gbest_fit = h.gbest_fit;
+  return DPSO_OK;
+}
+
+int dpso_run(dpso_ctx* c, int32_t* gens_run) {
+  if (!c || !c->initialized) return fail(DPSO_EINVAL, "context not initialized");
+  int rc = ensure_graph(c);
+  if (rc) return rc;
+  if ((rc = sync_in(c))) return rc;
+  int launched = 0;
+  const int G = c->prm.max_generations;
+  int batch = 4;
+  while (launched < G) {
+    const int b = std::min(batch, G - launched);
+    for (int g = 0; g < b; ++g) CK(cudaGraphLaunch(c->graph, c->stream));
+    launched += b;
+    CK(cudaMemcpyAsync(c->host_ctl, c->v.ctl, sizeof(DevCtl),
+                       cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->host_ctl->done) break;
+    if (batch < 64) batch *= 2;
+  }
+  CK(cudaMemcpyAsync(c->host_ctl, c->v.ctl, sizeof(DevCtl),
+                     cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->host_ctl->vel_overflow)
+    return fail(DPSO_ECUDA, "velocity list capacity exceeded (inertia too "
+                            "close to 1 for the device list bound)");
+  if (gens_run) *gens_run = c->host_ctl->gens_run;
+  return sync_out(c);
+}
+
+int dpso_result(dpso_ctx* c, int32_t* tour, double* fitness, double* conv,
+                int32_t* n_conv) {
+  if (!c || !c->initialized) return fail(DPSO_EINVAL, "context not initialized");
+  const int n = c->n;
+  int rc = sync_in(c);
+  if (rc) return rc;
+  std::vector<uint16_t> g(n);
+  CK(cudaMemcpyAsync(c->host_ctl, c->v.ctl, sizeof(DevCtl),
+                     cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(g.data(), c->v.gbest, 2 * n, cudaMemcpyDeviceToHost,
+                     c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  const int gens = c->host_ctl->gens_run;
+  if (conv)
+    CK(cudaMemcpy(conv, c->v.conv, sizeof(double) * (gens + 1),
+                  cudaMemcpyDeviceToHost));
+  if (n_conv) *n_conv = gens + 1;
+  if (tour) {
+    for (int i = 0; i < n; ++i) tour[i] = g[i];
+    tour[n] = g[0];
+  }
+  if (fitness) *fitness = c->host_ctl->gbest_fit;
+  return DPSO_OK;
+}
+
+int dpso_get_state(dpso_ctx* c, int32_t* x, int32_t* pbest, double* fit,
+                   double* pfit, int32_t* vmap, int32_t* gbest,
+                   double* gbest_fit) {
+  if (!c) return fail(DPSO_EINVAL, "null context");
+  const int64_t P = c->prm.n_particles, n = c->n, np = c->v.np;
+  int rc = sync_in(c);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(c->stream));
+  std::vector<uint16_t> buf(P * np);
+  auto rows = [&](const uint16_t* src, int32_t* dst) -> int {
+    if (!dst) return DPSO_OK;
+    if (!src) {
+      for (int64_t p = 0; p < P; ++p)
+        for (int64_t i = 0; i < n; ++i) dst[p * n + i] = (int32_t)i;
+      return DPSO_OK;
+    }
+    CK(cudaMemcpy(buf.data(), src, 2 * P * np, cudaMemcpyDeviceToHost));
+    for (int64_t p = 0; p < P; ++p)
+      for (int64_t i = 0; i < n; ++i) dst[p * n + i] = buf[p * np + i];
+    return DPSO_OK;
+  };
+  if ((rc = rows(c->v.x, x))) return rc;
+  if ((rc = rows(c->v.pbest, pbest))) return rc;
+  if ((rc = rows(c->v.vmap, vmap))) return rc;
+  if (fit) CK(cudaMemcpy(fit, c->v.fit, 8 * P, cudaMemcpyDeviceToHost));
+  if (pfit) CK(cudaMemcpy(pfit, c->v.pfit, 8 * P, cudaMemcpyDeviceToHost));
+  if (gbest) {
+    std::vector<uint16_t> g(n);
+    CK(cudaMemcpy(g.data(), c->v.gbest, 2 * n, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i) gbest[i] = g[i];
+  }
+  if (gbest_fit) {
+    DevCtl h;
+    CK(cudaMemcpy(&h, c->v.ctl, sizeof h, cudaMemcpyDeviceToHost));
+    *gbest_fit = h.gbest_fit;
+  }
+  return DPSO_OK;
+}
+
+int dpso_set_state(dpso_ctx* c, const int32_t* x, const int32_t* pbest,
+                   const double* fit, const double* pfit, const int32_t* vmap,
+                   const int32_t* gbest, double gbest_fit) {
+  if (!c) return fail(DPSO_EINVAL, "null context");
+  const int64_t P = c->prm.n_particles, n = c->n, np = c->v.np;
+  int rc = sync_in(c);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(c->stream));
+  std::vector<uint16_t> buf(P * np, 0);
+  auto put = [&](uint16_t* dst, const int32_t* src) -> int {
+    if (!dst || !src) return DPSO_OK;
+    for (int64_t p = 0; p < P; ++p)
+      for (int64_t i = 0; i < n; ++i) buf[p * np + i] = (uint16_t)src[p * n + i];
+    CK(cudaMemcpy(dst, buf.data(), 2 * P * np, cudaMemcpyHostToDevice));
+    return DPSO_OK;
+  };
+  if ((rc = put(c->v.x, x))) return rc;
+  if ((rc = put(c->v.pbest, pbest))) return rc;
+  if ((rc = put(c->v.vmap, vmap))) return rc;
+  if (fit) CK(cudaMemcpy(c->v.fit, fit, 8 * P, cudaMemcpyHostToDevice));
+  if (pfit) CK(cudaMemcpy(c->v.pfit, pfit, 8 * P, cudaMemcpyHostToDevice));
+  if (gbest) {
+    std::vector<uint16_t> g(n);
+    for (int i = 0; i < n; ++i) g[i] = (uint16_t)gbest[i];
+    CK(cudaMemcpy(c->v.gbest, g.data(), 2 * n, cudaMemcpyHostToDevice));
+    DevCtl h;
+    CK(cudaMemcpy(&h, c->v.ctl, sizeof h, cudaMemcpyDeviceToHost));
+    h.gbest_fit = gbest_fit;
+    CK(cudaMemcpy(c->v.ctl, &h, sizeof h, cudaMemcpyHostToDevice));
+  }
+  // refresh the edge-cost cache for the new positions
+  CK(launch_tour_cost_rows(c->v.cost, c->v.ld, c->n, c->v.x, np,
+                           c->prm.n_particles, c->v.fit, c->v.dcache,
+                           c->stream));
+  if (fit) CK(cudaMemcpyAsync(c->v.fit, fit, 8 * P, cudaMemcpyHostToDevice,
+                              c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->initialized = true;
+  return DPSO_OK;
+}
+
+int dpso_offer_gbest(dpso_ctx* c, const int32_t* tour, double fitness) {
+  if (!c || !tour) return fail(DPSO_EINVAL, "null argument");
+  const int n = c->n;
+  int rc = sync_in(c);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(c->host_ctl, c->v.ctl, sizeof(DevCtl),
+                     cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (!(fitness < c->host_ctl->gbest_fit)) return DPSO_OK;
+  std::vector<uint16_t> g(n);
+  for (int i = 0; i < n; ++i) g[i] = (uint16_t)tour[i];
+  CK(cudaMemcpy(c->v.gbest, g.data(), 2 * n, cudaMemcpyHostToDevice));
+  c->host_ctl->gbest_fit = fitness;
+  CK(cudaMemcpy(&c->v.ctl->gbest_fit, &fitness, sizeof(double),
+                cudaMemcpyHostToDevice));
+  return DPSO_OK;
+}
+
+void dpso_destroy(dpso_ctx* c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  if (c->ev) cudaEventDestroy(c->ev);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->host_ctl) cudaFreeHost(c->host_ctl);
+  delete c;
+}
+
+// ---- kernel-level entry points -------------------------------------------
+
+static int to_u16_tours(const int32_t* dev_tours, int32_t n, int32_t count,
+                        uint16_t* dst, int64_t np, cudaStream_t s);
+
+int dpso_tour_cost_batch(const double* dev_cost, int64_t ld, int32_t n,
+                         const int32_t* dev_tours, int32_t count,
+                         double* dev_out, void* cuda_stream) {
+  if (!dev_cost || !dev_tours || !dev_out || n < 1 || n > kMaxN || count < 0)
+    return fail(DPSO_EINVAL, "bad arguments");
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  const int64_t np = round_up(n, 8);
+  uint16_t* t16 = nullptr;
+  CK(cudaMallocAsync(&t16, 2 * np * (int64_t)std::max(count, 1), s));
+  int rc = to_u16_tours(dev_tours, n, count, t16, np, s);
+  if (rc) return rc;
+  CK(launch_tour_cost_rows(dev_cost, ld, n, t16, np, count, dev_out, nullptr,
+                           s));
+  CK(cudaFreeAsync(t16, s));
+  return DPSO_OK;
+}
+
+__global__ void k_i32_to_u16(const int32_t* src, int n, int count,
+                             uint16_t* dst, int64_t np) {
+  const int64_t t = blockIdx.x;
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    dst[t * np + i] = (uint16_t)src[t * n + i];
+}
+__global__ void k_u16_to_i32(const uint16_t* src, int n, int count,
+                             int32_t* dst, int64_t np) {
+  const int64_t t = blockIdx.x;
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    dst[t * n + i] = (int32_t)src[t * np + i];
+}
+
+static int to_u16_tours(const int32_t* dev_tours, int32_t n, int32_t count,
+                        uint16_t* dst, int64_t np, cudaStream_t s) {
+  if (count > 0) k_i32_to_u16<<<count, 256, 0, s>>>(dev_tours, n, count, dst, np);
+  CK(cudaGetLastError());
+  return DPSO_OK;
+}
+
+int dpso_best_exchange_batch(const double* dev_cost, int64_t ld, int32_t n,
+                             int32_t* dev_tours, int32_t count,
+                             double* dev_delta, void* cuda_stream) {
+  if (!dev_cost || !dev_tours || !dev_delta || n < 1 || n > kMaxN ||
+      count < 0)
+    return fail(DPSO_EINVAL, "bad arguments");
+  if (ld < round_up(n, 2) || (ld & 1) || ((uintptr_t)dev_cost & 15))
+    return fail(DPSO_EINVAL, "cost matrix needs an even ld >= n and 16-B "
+                             "alignment");
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  const int64_t np = round_up(n, 8);
+  const int chunks = two_opt_pick_chunks(n, std::max(count, 1));
+  std::vector<int32_t> rows(chunks + 1);
+  two_opt_chunk_rows(n, chunks, rows.data());
+  const int64_t cnt = std::max(count, 1);
+  size_t bytes = round_up(2 * np * cnt, 256) + round_up(8 * np * cnt, 256) +
+                 round_up(sizeof(TwoOptRes) * chunks * cnt, 256) +
+                 round_up(4 * (chunks + 1), 256) + round_up(8 * cnt, 256);
+  unsigned char* tmp = nullptr;
+  CK(cudaMallocAsync(&tmp, bytes, s));
+  uint16_t* t16 = (uint16_t*)tmp;
+  double* dc = (double*)(tmp + round_up(2 * np * cnt, 256));
+  TwoOptRes* res = (TwoOptRes*)((unsigned char*)dc + round_up(8 * np * cnt, 256));
+  int32_t* crow = (int32_t*)((unsigned char*)res +
+                             round_up(sizeof(TwoOptRes) * chunks * cnt, 256));
+  CK(cudaMemcpyAsync(crow, rows.data(), 4 * (chunks + 1),
+                     cudaMemcpyHostToDevice, s));
+  int rc = to_u16_tours(dev_tours, n, count, t16, np, s);
+  if (rc) return rc;
+  double* fsum = (double*)((unsigned char*)crow + round_up(4 * (chunks + 1), 256));
+  CK(launch_tour_cost_rows(dev_cost, ld, n, t16, np, count, fsum, dc, s));
+  CK(launch_two_opt_batch(dev_cost, ld, n, (int32_t)np, t16, dc, count, res,
+                          chunks, crow, dev_delta, s));
+  if (count > 0) k_u16_to_i32<<<count, 256, 0, s>>>(t16, n, count, dev_tours, np);
+  CK(cudaGetLastError());
+  CK(cudaFreeAsync(tmp, s));
+  return DPSO_OK;
+}
+
+int dpso_nn_tour(const double* dev_cost, int64_t ld, int32_t n, int32_t start,
+                 int32_t* host_tour, void* cuda_stream) {
+  if (!dev_cost || !host_tour || n < 1 || start < 0 || start >= n)
+    return fail(DPSO_EINVAL, "bad arguments");
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  int32_t* d = nullptr;
+  CK(cudaMallocAsync(&d, 4 * n, s));
+  CK(launch_nn(dev_cost, ld, n, start, d, s));
+  CK(cudaMemcpyAsync(host_tour, d, 4 * n, cudaMemcpyDeviceToHost, s));
+  CK(cudaFreeAsync(d, s));
+  CK(cudaStreamSynchronize(s));
+  return DPSO_OK;
+}
+
+int dpso_nn_two_opt(const double* dev_cost, int64_t ld, int32_t n,
+                    int32_t* host_tour, double* host_cost, void* cuda_stream) {
+  // baselines.py:103-123: NN from 0, total = sum of edges in order, then
+  // best-improvement 2-opt until delta == 0.0, total += delta each move.
+  if (!dev_cost || !host_tour || !host_cost || n < 1)
+    return fail(DPSO_EINVAL, "bad arguments");
+  if (n == 1) {
+    host_tour[0] = 0;
+    host_tour[1] = 0;
+    *host_cost = 0.0;
+    return DPSO_OK;
+  }
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  int32_t* d = nullptr;
+  double* dd = nullptr;
+  CK(cudaMallocAsync(&d, 4 * n, s));
+  CK(cudaMallocAsync(&dd, 8, s));
+  CK(launch_nn(dev_cost, ld, n, 0, d, s));
+  std::vector<int32_t> body(n);
+  CK(cudaMemcpyAsync(body.data(), d, 4 * n, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  std::vector<double> row(n);
+  double total = 0.0;
+  // sum(rows[a][b] for a, b in zip(body, body[1:] + body[:1])): Python sum
+  // starts from int 0 and adds in order
+  {
+    std::vector<double> edges(n);
+    for (int i = 0; i < n; ++i) {
+      int a = body[i], b = body[(i + 1) % n];
+      CK(cudaMemcpy(&edges[i], dev_cost + (size_t)a * ld + b, 8,
+                    cudaMemcpyDeviceToHost));
+    }
+    for (int i = 0; i < n; ++i) total += edges[i];
+  }
+  for (;;) {
+    int rc = dpso_best_exchange_batch(dev_cost, ld, n, d, 1, dd, s);
+    if (rc) return rc;
+    double delta;
+    CK(cudaMemcpyAsync(&delta, dd, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (delta == 0.0) break;
+    total += delta;
+  }
+  CK(cudaMemcpyAsync(host_tour, d, 4 * n, cudaMemcpyDeviceToHost, s));
+  CK(cudaFreeAsync(d, s));
+  CK(cudaFreeAsync(dd, s));
+  CK(cudaStreamSynchronize(s));
+  host_tour[n] = host_tour[0];
+  *host_cost = total;
+  return DPSO_OK;
+}
+
+}  // extern "C"

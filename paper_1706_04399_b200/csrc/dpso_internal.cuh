@@ -1,0 +1,140 @@
+// Internal declarations of the B200 DPSO solve path (not part of the ABI).
+//
+// HBM layout of one swarm (all in the caller-owned workspace, 256-B aligned
+// sections; NP = n rounded up to 8 so every u16 row is 16-B aligned):
+//   ctl      DevCtl                      generation/stall/flags (one record)
+//   streams  (P+2) x PcgState            numpy streams: init, mutation, particles
+//   x        P x NP  u16                 current open tour per particle
+//   pbest    P x NP  u16                 personal best tour
+//   vmap     P x NP  u16                 composed velocity permutation (w == 1)
+//   vel      P x (cap+2n) u32            transposition lists (w < 1 only)
+//   fit,pfit P f64                       fitness / personal-best fitness
+//   dcache   P x NP  f64                 edge costs d_i = C[x_i][x_{i+1}]
+//   gbest    NP u16, conv (G+1) f64      global best tour, convergence trace
+//   tores    P x chunks x TwoOptRes      2-opt partial argmins
+//   mutation scratch (ranks, hashes, lists, events) and init cursors.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/dpso.h"
+#include "pcg64.cuh"
+
+namespace dpso {
+
+constexpr int kMaxN = 65535;  // u16 node ids
+
+__host__ __device__ inline int64_t round_up(int64_t v, int64_t m) {
+  return (v + m - 1) / m * m;
+}
+
+struct DevCtl {
+  double gbest_fit;
+  int32_t gen;        // generation currently running (1-based), 0 after init
+  int32_t stall;
+  int32_t done;       // stall break or max_generations reached
+  int32_t gens_run;
+  int32_t improved;   // cand.fitness < gbest_fit after update(+mutation)
+  int32_t cand;
+  int32_t mutating;   // this generation mutates
+  int32_t two_opt_ran;
+  int32_t n_surv;
+  int32_t n_drop;
+  int32_t n_events;
+  int32_t collision;  // canonical-hash collision seen (diagnostic)
+  int32_t vel_overflow;
+  int32_t two_opt_count;  // generations in which the 2-opt pass ran
+  uint64_t mut_q;     // u32 draws consumed by the current mutation call
+};
+
+struct TwoOptRes {
+  double delta;
+  int32_t i, j;
+};
+
+// Everything a kernel needs, passed by value.
+struct SwarmView {
+  int32_t n, np, P;
+  int32_t max_generations, stall_generations, mutation_period;
+  int32_t use_mutation, use_edge_exchange;
+  int32_t rng_mode;
+  uint64_t philox_seed;
+  double inertia, cognitive, social;
+  const double* cost;
+  int64_t ld;
+  DevCtl* ctl;
+  PcgState* streams;   // [0] init, [1] mutation, [2+p] particle p
+  PcgState* mut_start; // copy of the mutation stream at call start
+  uint16_t* x;
+  uint16_t* pbest;
+  uint16_t* vmap;
+  uint32_t* vel;
+  int32_t* vel_len;
+  int64_t vel_cap;     // entries per particle list (excl. 2n scratch)
+  double* fit;
+  double* pfit;
+  double* dcache;
+  uint16_t* gbest;
+  double* conv;
+  TwoOptRes* tores;
+  int32_t chunks;      // 2-opt row chunks per particle
+  int32_t* chunk_row;  // chunks + 1 row boundaries
+  // mutation scratch
+  int32_t* rank;
+  uint64_t* hash;
+  int32_t* flag;       // 1 = dropped duplicate
+  int32_t* sidx;       // survivor / dropped index in rank order
+  int32_t* order;      // slot at each rank
+  int32_t* surv_list;
+  int32_t* keep;
+  int32_t* ev_slot;
+  int32_t* ev_k;
+  uint64_t* ev_cursor;
+  uint64_t* init_cursor;
+};
+
+// ---- kernel launchers (each .cu owns its kernels) -------------------------
+cudaError_t launch_gen_begin(const SwarmView& v, cudaStream_t s);
+cudaError_t launch_update(const SwarmView& v, cudaStream_t s);
+cudaError_t launch_mutation(const SwarmView& v, cudaStream_t s);
+cudaError_t launch_select(const SwarmView& v, bool finalize, cudaStream_t s);
+cudaError_t launch_two_opt(const SwarmView& v, cudaStream_t s, int parts = 3);
+cudaError_t launch_finalize(const SwarmView& v, cudaStream_t s);
+cudaError_t launch_init(const SwarmView& v, const uint16_t* dev_seed,
+                        int32_t n_seed, cudaStream_t s);
+cudaError_t launch_init_best(const SwarmView& v, cudaStream_t s);
+
+// generic batch kernels (kernel-level ABI and internal reuse)
+cudaError_t launch_tour_cost_rows(const double* cost, int64_t ld, int32_t n,
+                                  const uint16_t* tours, int64_t stride,
+                                  int32_t count, double* out, double* dcache,
+                                  cudaStream_t s);
+cudaError_t launch_two_opt_batch(const double* cost, int64_t ld, int32_t n,
+                                 int32_t np, uint16_t* tours,
+                                 const double* dcache, int32_t count,
+                                 TwoOptRes* res, int32_t chunks,
+                                 const int32_t* chunk_row, double* delta_out,
+                                 cudaStream_t s);
+cudaError_t launch_nn(const double* cost, int64_t ld, int32_t n, int32_t start,
+                      int32_t* out, cudaStream_t s);
+int two_opt_chunk_rows(int32_t n, int32_t chunks, int32_t* rows);
+int two_opt_pick_chunks(int32_t n, int32_t P);
+
+// Fitness in the reference's order (solver.py:48-54):
+// total = 0; total += d[n-1]; total += d[0]; ... total += d[n-2].
+__device__ __forceinline__ double seq_tour_sum(const double* d, int n) {
+  double total = 0.0;
+  total = __dadd_rn(total, d[n - 1]);
+  for (int i = 0; i < n - 1; ++i) total = __dadd_rn(total, d[i]);
+  return total;
+}
+
+// _prefix_len (solver.py:82-85) without FMA contraction.
+__device__ __forceinline__ int prefix_len(double c, int length) {
+  if (!(c > 0.0)) return 0;
+  double v = __dadd_rn(__dmul_rn(c, (double)length), 0.5);
+  int k = (int)v;  // truncation == Python int() for v >= 0
+  return k < length ? k : length;
+}
+
+}  // namespace dpso

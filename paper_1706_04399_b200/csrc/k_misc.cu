@@ -1,0 +1,475 @@
+// Generation control, gbest/stall bookkeeping, swarm init, batch fitness and
+// the nearest-neighbour construction.
+//
+//   k_gen_begin     gen += 1; mutation flag (solver.py:292-294, 304)
+//   k_select        first-index argmin of fitness, improved flag
+//                   (solver.py:307-308); optionally finalizes
+//   k_finalize      argmin again after 2-opt (solver.py:318-319), gbest copy
+//                   from the current position, stall, convergence, stall
+//                   break (solver.py:320-328)
+//   k_init_walk     one pass over the init stream recording where each
+//                   particle's draws start (solver.py:176-183)
+//   k_init_build    per particle: seed / one-swap seed / permutation(n),
+//                   fitness, pbest = self, vmap = identity (solver.py:37-45)
+//   k_init_best     initial gbest = first minimum (solver.py:284-287)
+//   k_tour_cost     _tour_cost (solver.py:48-54) for a batch of tours
+//   k_nn            nearest-neighbour construction (baselines.py:110-116)
+#include <float.h>
+
+#include "dpso_internal.cuh"
+
+namespace dpso {
+
+namespace {
+
+constexpr int kRed = 1024;
+
+// First-index argmin over fit[0..P) with strict < (Python min / solver.py:284,
+// 307): lexicographic (value, index) reduction.
+__device__ void block_argmin(const double* fit, int P, double* s_v, int* s_i,
+                             double* out_v, int* out_i) {
+  const int tid = threadIdx.x;
+  double bv = __longlong_as_double(0x7ff0000000000000ll);
+  int bi = 0x7fffffff;
+  for (int i = tid; i < P; i += blockDim.x) {
+    double f = fit[i];
+    if (bi == 0x7fffffff || f < bv) {
+      bv = f;
+      bi = i;
+    }
+  }
+  const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+    int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (v2 < bv || (!(bv < v2) && i2 < bi)) {
+      bv = v2;
+      bi = i2;
+    }
+  }
+  if (lane == 0) {
+    s_v[warp] = bv;
+    s_i[warp] = bi;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    bv = lane < nw ? s_v[lane] : __longlong_as_double(0x7ff0000000000000ll);
+    bi = lane < nw ? s_i[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+      int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (v2 < bv || (!(bv < v2) && i2 < bi)) {
+        bv = v2;
+        bi = i2;
+      }
+    }
+    if (lane == 0) {
+      *out_v = bv;
+      *out_i = bi;
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void k_gen_begin(SwarmView v) {
+  if (threadIdx.x != 0) return;
+  DevCtl* c = v.ctl;
+  if (c->done) return;
+  c->gen += 1;
+  c->mutating = v.use_mutation && (c->gen % v.mutation_period == 0);
+  c->two_opt_ran = 0;
+  c->improved = 0;
+}
+
+__global__ void __launch_bounds__(kRed) k_select(SwarmView v, int finalize) {
+  DevCtl* c = v.ctl;
+  if (c->done) return;
+  __shared__ double s_v[32];
+  __shared__ int s_i[32];
+  __shared__ double bv;
+  __shared__ int bi;
+  block_argmin(v.fit, v.P, s_v, s_i, &bv, &bi);
+  const int improved = bv < c->gbest_fit;
+  __syncthreads();
+  if (!finalize) {
+    if (threadIdx.x == 0) {
+      c->cand = bi;
+      c->improved = improved;
+    }
+    return;
+  }
+  if (improved) {
+    const uint16_t* src = v.x + (size_t)bi * v.np;
+    for (int i = threadIdx.x; i < v.n; i += blockDim.x) v.gbest[i] = src[i];
+  }
+  if (threadIdx.x == 0) {
+    c->cand = bi;
+    c->improved = improved;
+    if (improved) {
+      c->gbest_fit = bv;
+      c->stall = 0;
+    } else {
+      c->stall += 1;
+    }
+    v.conv[c->gen] = c->gbest_fit;
+    c->gens_run = c->gen;
+    if (c->stall >= v.stall_generations || c->gen >= v.max_generations)
+      c->done = 1;
+  }
+}
+
+__global__ void __launch_bounds__(kRed) k_finalize(SwarmView v) {
+  DevCtl* c = v.ctl;
+  if (c->done) return;
+  __shared__ double s_v[32];
+  __shared__ int s_i[32];
+  __shared__ double bv;
+  __shared__ int bi;
+  __shared__ int s_improved;
+  if (!c->improved) {
+    // 2-opt ran for every particle: recompute cand (solver.py:318-319)
+    block_argmin(v.fit, v.P, s_v, s_i, &bv, &bi);
+    if (threadIdx.x == 0) {
+      s_improved = bv < c->gbest_fit;
+      c->two_opt_ran = 1;
+      c->two_opt_count += 1;
+    }
+  } else {
+    if (threadIdx.x == 0) {
+      bi = c->cand;
+      bv = v.fit[bi];
+      s_improved = 1;
+    }
+  }
+  __syncthreads();
+  const int improved = s_improved;
+  if (improved) {
+    const uint16_t* src = v.x + (size_t)bi * v.np;
+    for (int i = threadIdx.x; i < v.n; i += blockDim.x) v.gbest[i] = src[i];
+  }
+  if (threadIdx.x == 0) {
+    c->cand = bi;
+    if (improved) {
+      c->gbest_fit = bv;
+      c->stall = 0;
+    } else {
+      c->stall += 1;
+    }
+    v.conv[c->gen] = c->gbest_fit;
+    c->gens_run = c->gen;
+    if (c->stall >= v.stall_generations || c->gen >= v.max_generations)
+      c->done = 1;
+  }
+}
+
+// ---- init (numpy streams) --------------------------------------------------
+
+// Counts next32() calls so each particle's first draw can be located.
+struct CountingPcg {
+  Pcg r;
+  uint64_t q;
+  __device__ uint32_t next32() {
+    ++q;
+    return r.next32();
+  }
+  __device__ uint32_t lemire32(uint32_t rng) {
+    const uint32_t rng_excl = rng + 1u;
+    uint64_t m = (uint64_t)next32() * rng_excl;
+    uint32_t leftover = (uint32_t)m;
+    if (leftover < rng_excl) {
+      const uint32_t threshold = (0xFFFFFFFFu - rng) % rng_excl;
+      while (leftover < threshold) {
+        m = (uint64_t)next32() * rng_excl;
+        leftover = (uint32_t)m;
+      }
+    }
+    return (uint32_t)(m >> 32);
+  }
+  __device__ uint32_t bounded(uint32_t rng) {
+    if (rng == 0) return 0;
+    if (rng == 0xFFFFFFFFu) return next32();
+    return lemire32(rng);
+  }
+  __device__ uint32_t interval(uint32_t mx) {
+    if (mx == 0) return 0;
+    uint32_t mask = mx;
+    mask |= mask >> 1;
+    mask |= mask >> 2;
+    mask |= mask >> 4;
+    mask |= mask >> 8;
+    mask |= mask >> 16;
+    uint32_t v;
+    while ((v = (next32() & mask)) > mx) {
+    }
+    return v;
+  }
+};
+
+__global__ void k_init_walk(SwarmView v, int n_seed) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int n = v.n;
+  *v.mut_start = v.streams[0];  // keep the start of the init stream
+  CountingPcg cr;
+  cr.r.load(v.streams[0]);
+  cr.q = 0;
+  for (int i = 0; i < v.P; ++i) {
+    v.init_cursor[i] = cr.q;
+    if (i < n_seed) {
+      if (i > 0 && n > 1) {
+        // choice(n, 2, replace=False): Floyd (2 draws) + shuffle (1 draw)
+        cr.bounded((uint32_t)(n - 2));
+        cr.bounded((uint32_t)(n - 1));
+        cr.bounded(1u);
+      }
+    } else {
+      for (int j = n - 1; j >= 1; --j) cr.interval((uint32_t)j);
+    }
+  }
+  cr.r.store(v.streams[0]);
+}
+
+__global__ void __launch_bounds__(128) k_init_build(SwarmView v,
+                                                    const uint16_t* seed,
+                                                    int n_seed) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = v.n, np = v.np, tid = threadIdx.x;
+  uint16_t* body = (uint16_t*)smem;
+  double* sd = (double*)(smem + round_up((int64_t)2 * np, 16));
+  __shared__ int s_flag;
+  for (int p = blockIdx.x; p < v.P; p += gridDim.x) {
+    if (p < n_seed) {
+      for (int i = tid; i < n; i += blockDim.x) body[i] = seed[i];
+    } else {
+      for (int i = tid; i < n; i += blockDim.x) body[i] = (uint16_t)i;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      Pcg r;
+      r.seek_u32(*v.mut_start, v.init_cursor[p]);
+      if (p < n_seed) {
+        if (p > 0 && n > 1) {
+          uint32_t v0 = r.bounded((uint32_t)(n - 2));
+          uint32_t v1 = r.bounded((uint32_t)(n - 1));
+          if (v1 == v0) v1 = (uint32_t)(n - 1);
+          uint32_t out[2] = {v0, v1};
+          uint32_t jj = r.bounded(1u);
+          uint32_t t = out[1];
+          out[1] = out[jj];
+          out[jj] = t;
+          uint16_t x = body[out[0]];
+          body[out[0]] = body[out[1]];
+          body[out[1]] = x;
+        }
+      } else {
+        for (int j = n - 1; j >= 1; --j) {
+          uint32_t jj = r.interval((uint32_t)j);
+          uint16_t x = body[j];
+          body[j] = body[jj];
+          body[jj] = x;
+        }
+      }
+    }
+    __syncthreads();
+    uint16_t* xg = v.x + (size_t)p * np;
+    uint16_t* pb = v.pbest + (size_t)p * np;
+    double* dg = v.dcache + (size_t)p * np;
+    for (int i = tid; i < n; i += blockDim.x) {
+      int a = body[i], b = body[i + 1 == n ? 0 : i + 1];
+      double d = v.cost[(size_t)a * v.ld + b];
+      sd[i] = d;
+      dg[i] = d;
+      xg[i] = (uint16_t)a;
+      pb[i] = (uint16_t)a;
+      if (v.vmap) v.vmap[(size_t)p * np + i] = (uint16_t)i;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double f = seq_tour_sum(sd, n);
+      v.fit[p] = f;
+      v.pfit[p] = f;
+      if (v.vel_len) v.vel_len[p] = 0;
+    }
+    __syncthreads();
+  }
+  (void)s_flag;
+}
+
+__global__ void __launch_bounds__(kRed) k_init_best(SwarmView v) {
+  __shared__ double s_v[32];
+  __shared__ int s_i[32];
+  __shared__ double bv;
+  __shared__ int bi;
+  block_argmin(v.fit, v.P, s_v, s_i, &bv, &bi);
+  const uint16_t* src = v.x + (size_t)bi * v.np;
+  for (int i = threadIdx.x; i < v.n; i += blockDim.x) v.gbest[i] = src[i];
+  if (threadIdx.x == 0) {
+    DevCtl* c = v.ctl;
+    c->gbest_fit = bv;
+    c->cand = bi;
+    c->gen = 0;
+    c->stall = 0;
+    c->done = 0;
+    c->gens_run = 0;
+    c->improved = 0;
+    c->mutating = 0;
+    c->two_opt_ran = 0;
+    c->collision = 0;
+    c->vel_overflow = 0;
+    c->two_opt_count = 0;
+    v.conv[0] = bv;
+  }
+}
+
+// One warp per tour.
+__global__ void __launch_bounds__(128) k_tour_cost(const double* cost,
+                                                   int64_t ld, int n,
+                                                   const uint16_t* tours,
+                                                   int64_t stride, int count,
+                                                   double* out,
+                                                   double* dcache) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * 4 + warp;
+  double* sd = (double*)smem + (size_t)warp * n;
+  if (t >= count) return;
+  const uint16_t* tour = tours + (size_t)t * stride;
+  for (int i = lane; i < n; i += 32) {
+    int a = tour[i], b = tour[i + 1 == n ? 0 : i + 1];
+    double d = cost[(size_t)a * ld + b];
+    sd[i] = d;
+    if (dcache) dcache[(size_t)t * stride + i] = d;
+  }
+  __syncwarp();
+  if (lane == 0) out[t] = seq_tour_sum(sd, n);
+}
+
+// Greedy nearest neighbour from `start` (baselines.py:110-116): n-1 steps,
+// each a CTA-wide argmin over unvisited nodes of row `cur` on (cost, index).
+__global__ void __launch_bounds__(1024) k_nn(const double* cost, int64_t ld,
+                                             int n, int start, int32_t* out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* visited = smem;
+  __shared__ double s_v[32];
+  __shared__ int s_i[32];
+  __shared__ int s_cur;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < n; i += blockDim.x) visited[i] = 0;
+  __syncthreads();
+  if (tid == 0) {
+    visited[start] = 1;
+    out[0] = start;
+    s_cur = start;
+  }
+  __syncthreads();
+  for (int step = 1; step < n; ++step) {
+    const double* row = cost + (size_t)s_cur * ld;
+    double bv = __longlong_as_double(0x7ff0000000000000ll);
+    int bi = 0x7fffffff;
+    for (int j = tid; j < n; j += blockDim.x) {
+      if (!visited[j]) {
+        double c = row[j];
+        if (bi == 0x7fffffff || c < bv) {
+          bv = c;
+          bi = j;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+      int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      bool take = (i2 != 0x7fffffff) &&
+                  (bi == 0x7fffffff || v2 < bv || (!(bv < v2) && i2 < bi));
+      if (take) {
+        bv = v2;
+        bi = i2;
+      }
+    }
+    if (lane == 0) {
+      s_v[warp] = bv;
+      s_i[warp] = bi;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const int nw = blockDim.x >> 5;
+      bv = lane < nw ? s_v[lane] : __longlong_as_double(0x7ff0000000000000ll);
+      bi = lane < nw ? s_i[lane] : 0x7fffffff;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+        int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+        bool take = (i2 != 0x7fffffff) &&
+                    (bi == 0x7fffffff || v2 < bv || (!(bv < v2) && i2 < bi));
+        if (take) {
+          bv = v2;
+          bi = i2;
+        }
+      }
+      if (lane == 0) {
+        visited[bi] = 1;
+        out[step] = bi;
+        s_cur = bi;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_gen_begin(const SwarmView& v, cudaStream_t s) {
+  k_gen_begin<<<1, 32, 0, s>>>(v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select(const SwarmView& v, bool finalize, cudaStream_t s) {
+  k_select<<<1, kRed, 0, s>>>(v, finalize ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const SwarmView& v, cudaStream_t s) {
+  k_finalize<<<1, kRed, 0, s>>>(v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init(const SwarmView& v, const uint16_t* dev_seed,
+                        int32_t n_seed, cudaStream_t s) {
+  k_init_walk<<<1, 32, 0, s>>>(v, n_seed);
+  size_t smem = round_up((int64_t)2 * v.np, 16) + (size_t)8 * v.np;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_init_build,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  k_init_build<<<v.P, 128, smem, s>>>(v, dev_seed, n_seed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_best(const SwarmView& v, cudaStream_t s) {
+  k_init_best<<<1, kRed, 0, s>>>(v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tour_cost_rows(const double* cost, int64_t ld, int32_t n,
+                                  const uint16_t* tours, int64_t stride,
+                                  int32_t count, double* out, double* dcache,
+                                  cudaStream_t s) {
+  size_t smem = (size_t)4 * n * sizeof(double);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_tour_cost,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  k_tour_cost<<<(count + 3) / 4, 128, smem, s>>>(cost, ld, n, tours, stride,
+                                                 count, out, dcache);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_nn(const double* cost, int64_t ld, int32_t n, int32_t start,
+                      int32_t* out, cudaStream_t s) {
+  k_nn<<<1, 1024, round_up(n, 16), s>>>(cost, ld, n, start, out);
+  return cudaGetLastError();
+}
+
+}  // namespace dpso

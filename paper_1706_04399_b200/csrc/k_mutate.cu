@@ -1,0 +1,462 @@
+// Random mutation with elitism and canonical-form dedupe (solver.py:222-258).
+//
+// Pipeline (all kernels no-op unless ctl->mutating):
+//   k_mut_hash   per particle: canonical rotation/direction (graph.py:106-115)
+//                and a 64-bit order-dependent hash of the canonical sequence
+//   k_mut_rank   rank in (fitness, slot) order by counting (solver.py:223-224)
+//   k_mut_dedupe a particle is a dropped duplicate iff an earlier-ranked one
+//                has the same canonical form (hash match + exact compare)
+//   k_mut_lists  survivors / dropped in rank order, keep = first ceil(S/3)
+//                survivors, events = non-kept slots in slot order
+//   k_mut_copy   dropped #r copies body+fitness of survivors[r % S]
+//   k_mut_walk   walks the single mutation stream: k = integers(1, k_hi+1),
+//                then the Floyd + shuffle draws of choice(n, 2k, False),
+//                checking Lemire rejections 1024 draws at a time, to find
+//                where every event's draws start
+//   k_mut_apply  one CTA per event: regenerate its draws from the stream
+//                (PCG64 jump-ahead), Floyd/tail-shuffle sampler, k disjoint
+//                swaps, fitness in reference order, pbest (solver.py:241-258)
+#include "dpso_internal.cuh"
+
+namespace dpso {
+
+namespace {
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// canonical element m (1 <= m < n) of tour t with 0 at position k
+__device__ __forceinline__ int canon_at(const uint16_t* t, int n, int k,
+                                        int rev, int m) {
+  int idx = rev ? (k - m + n) % n : (k + m) % n;
+  return t[idx];
+}
+
+__global__ void __launch_bounds__(128) k_mut_hash(SwarmView v,
+                                                  int32_t* canon) {
+  if (!v.ctl->mutating || v.ctl->done) return;
+  const int p = blockIdx.x, n = v.n, tid = threadIdx.x;
+  const uint16_t* t = v.x + (size_t)p * v.np;
+  __shared__ int s_k;
+  __shared__ unsigned long long s_h;
+  if (tid == 0) s_h = 0ull;
+  for (int i = tid; i < n; i += blockDim.x)
+    if (t[i] == 0) s_k = i;
+  __syncthreads();
+  const int k = s_k;
+  const int rev = (n > 2) && (t[(k - 1 + n) % n] < t[(k + 1) % n]);
+  uint64_t h = 0;
+  for (int m = 1 + tid; m < n; m += blockDim.x)
+    h += mix64(((uint64_t)m << 32) | (uint64_t)canon_at(t, n, k, rev, m));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  if ((tid & 31) == 0) atomicAdd(&s_h, (unsigned long long)h);
+  __syncthreads();
+  if (tid == 0) {
+    v.hash[p] = s_h;
+    canon[p] = k | (rev << 31);
+  }
+}
+
+constexpr int kTile = 2048;
+
+__global__ void __launch_bounds__(256) k_mut_rank(SwarmView v) {
+  if (!v.ctl->mutating || v.ctl->done) return;
+  __shared__ double s_f[kTile];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const double fi = i < v.P ? v.fit[i] : 0.0;
+  int cnt = 0;
+  for (int base = 0; base < v.P; base += kTile) {
+    const int m = min(kTile, v.P - base);
+    __syncthreads();
+    for (int u = threadIdx.x; u < m; u += blockDim.x) s_f[u] = v.fit[base + u];
+    __syncthreads();
+    if (i < v.P) {
+      for (int u = 0; u < m; ++u) {
+        const double f = s_f[u];
+        const int j = base + u;
+        cnt += (f < fi) || (f == fi && j < i);
+      }
+    }
+  }
+  if (i < v.P) {
+    v.rank[i] = cnt;
+    v.order[cnt] = i;
+  }
+}
+
+__device__ bool canon_equal(const SwarmView& v, const int32_t* canon, int a,
+                            int b) {
+  const int n = v.n;
+  const uint16_t* ta = v.x + (size_t)a * v.np;
+  const uint16_t* tb = v.x + (size_t)b * v.np;
+  const int ka = canon[a] & 0x7fffffff, ra = (int)((uint32_t)canon[a] >> 31);
+  const int kb = canon[b] & 0x7fffffff, rb = (int)((uint32_t)canon[b] >> 31);
+  for (int m = 1; m < n; ++m)
+    if (canon_at(ta, n, ka, ra, m) != canon_at(tb, n, kb, rb, m)) return false;
+  return true;
+}
+
+__global__ void __launch_bounds__(256) k_mut_dedupe(SwarmView v,
+                                                    const int32_t* canon) {
+  if (!v.ctl->mutating || v.ctl->done) return;
+  __shared__ unsigned long long s_h[kTile];
+  __shared__ int s_r[kTile];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t hi = i < v.P ? v.hash[i] : 0;
+  const int ri = i < v.P ? v.rank[i] : 0;
+  int dropped = 0;
+  for (int base = 0; base < v.P; base += kTile) {
+    const int m = min(kTile, v.P - base);
+    __syncthreads();
+    for (int u = threadIdx.x; u < m; u += blockDim.x) {
+      s_h[u] = v.hash[base + u];
+      s_r[u] = v.rank[base + u];
+    }
+    __syncthreads();
+    if (i < v.P && !dropped) {
+      for (int u = 0; u < m; ++u) {
+        if (s_h[u] == hi && s_r[u] < ri) {
+          if (canon_equal(v, canon, i, base + u)) {
+            dropped = 1;
+            break;
+          }
+          v.ctl->collision = 1;
+        }
+      }
+    }
+  }
+  if (i < v.P) v.flag[i] = dropped;
+}
+
+template <int T>
+__device__ int block_scan_excl(int val, int* s_w, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = val;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < T / 32 ? s_w[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < T / 32) s_w[lane] = w;
+  }
+  __syncthreads();
+  int base = warp ? s_w[warp - 1] : 0;
+  *total = s_w[T / 32 - 1];
+  __syncthreads();
+  return base + x - val;
+}
+
+__global__ void __launch_bounds__(1024) k_mut_lists(SwarmView v) {
+  if (!v.ctl->mutating || v.ctl->done) return;
+  __shared__ int s_w[32];
+  const int P = v.P, tid = threadIdx.x;
+  int surv_run = 0;
+  for (int base = 0; base < P; base += 1024) {
+    const int r = base + tid;
+    const int i = r < P ? v.order[r] : 0;
+    const int s = (r < P) ? !v.flag[i] : 0;
+    int tot;
+    const int ex = block_scan_excl<1024>(s, s_w, &tot);
+    if (r < P) {
+      if (s) {
+        v.sidx[i] = surv_run + ex;
+        v.surv_list[surv_run + ex] = i;
+      } else {
+        v.sidx[i] = r - (surv_run + ex);  // dropped index in rank order
+      }
+    }
+    surv_run += tot;
+  }
+  const int S = surv_run;
+  const int nkeep = (S + 2) / 3;  // ceil(S / 3)
+  __syncthreads();
+  int ev_run = 0;
+  for (int base = 0; base < P; base += 1024) {
+    const int i = base + tid;
+    int kp = 0;
+    if (i < P) {
+      kp = !v.flag[i] && v.sidx[i] < nkeep;
+      v.keep[i] = kp;
+    }
+    const int e = (i < P) && !kp;
+    int tot;
+    const int ex = block_scan_excl<1024>(e, s_w, &tot);
+    if (e) v.ev_slot[ev_run + ex] = i;
+    ev_run += tot;
+  }
+  if (tid == 0) {
+    v.ctl->n_surv = S;
+    v.ctl->n_drop = P - S;
+    v.ctl->n_events = ev_run;
+  }
+}
+
+__global__ void __launch_bounds__(128) k_mut_copy(SwarmView v) {
+  if (!v.ctl->mutating || v.ctl->done) return;
+  const int p = blockIdx.x;
+  if (!v.flag[p]) return;
+  const int S = v.ctl->n_surv;
+  const int src = v.surv_list[v.sidx[p] % S];
+  const uint16_t* a = v.x + (size_t)src * v.np;
+  uint16_t* b = v.x + (size_t)p * v.np;
+  for (int i = threadIdx.x; i < v.n; i += blockDim.x) b[i] = a[i];
+  if (threadIdx.x == 0) v.fit[p] = v.fit[src];
+}
+
+// ---- the sequential stream walk ------------------------------------------
+
+constexpr int kWalk = 1024;     // threads
+constexpr int kRing = 4096;     // u32 ring (fresh draws)
+constexpr int kHalf = kRing / 2;
+
+struct WalkShared {
+  uint32_t ring[kRing];
+  int64_t wbase;  // fresh index of ring window start
+  int64_t q;      // u32 draws consumed
+  int k;
+  int first;
+};
+
+__global__ void __launch_bounds__(kWalk) k_mut_walk(SwarmView v) {
+  if (!v.ctl->mutating || v.ctl->done) return;
+  __shared__ WalkShared sh;
+  const int tid = threadIdx.x;
+  const PcgState g = v.streams[1];
+  if (tid == 0) *v.mut_start = g;
+  const int64_t h = (int64_t)g.has_uint32;
+  const uint32_t ub = (uint32_t)g.uinteger;
+  const u128 S0 = {g.state_hi, g.state_lo}, inc = {g.inc_hi, g.inc_lo};
+  // thread state: output index (1-based) 1 + tid, then + kWalk per slide
+  u128 st = pcg_advance(S0, inc, 1 + (uint64_t)tid);
+  u128 A, C;
+  pcg_jump_coeffs(kWalk, inc, &A, &C);
+  {
+    uint64_t o = pcg_output(st);
+    sh.ring[2 * tid] = (uint32_t)o;
+    sh.ring[2 * tid + 1] = (uint32_t)(o >> 32);
+    st = add128(mul128(A, st), C);
+    o = pcg_output(st);
+    sh.ring[kHalf + 2 * tid] = (uint32_t)o;
+    sh.ring[kHalf + 2 * tid + 1] = (uint32_t)(o >> 32);
+  }
+  if (tid == 0) {
+    sh.wbase = 0;
+    sh.q = 0;
+  }
+  __syncthreads();
+
+  auto get = [&](int64_t q) -> uint32_t {
+    if (q < h) return ub;
+    return sh.ring[(q - h) & (kRing - 1)];
+  };
+  // make the ring cover fresh indices [f(q), f(q) + need)
+  auto ensure = [&](int64_t q, int need) {
+    for (;;) {
+      const int64_t f = q - h;
+      if (f + need <= sh.wbase + kRing) break;
+      __syncthreads();
+      const int64_t nb = sh.wbase + kHalf;  // new window start
+      st = add128(mul128(A, st), C);
+      const uint64_t o = pcg_output(st);
+      const int64_t fi = nb + kHalf + 2 * tid;  // fresh index of lo half
+      sh.ring[fi & (kRing - 1)] = (uint32_t)o;
+      sh.ring[(fi + 1) & (kRing - 1)] = (uint32_t)(o >> 32);
+      __syncthreads();
+      if (tid == 0) sh.wbase = nb;
+      __syncthreads();
+    }
+  };
+
+  const int n = v.n;
+  const int k_hi = max(2, n / 4);
+  const int E = v.ctl->n_events;
+  const bool tail = (n > 10000);
+  for (int e = 0; e < E; ++e) {
+    int64_t q = sh.q;
+    ensure(q, kHalf);
+    if (tid == 0) {
+      // integers(1, k_hi + 1): Lemire with rng = k_hi - 1 (>= 1)
+      const uint32_t rng = (uint32_t)(k_hi - 1);
+      uint32_t u;
+      do {
+        u = get(q);
+        ++q;
+      } while (lemire_rejects(u, rng));
+      const int kraw = (int)(((uint64_t)u * (rng + 1u)) >> 32) + 1;
+      const int k = min(kraw, n / 2);
+      sh.k = k;
+      sh.q = q;
+      v.ev_k[e] = k;
+      v.ev_cursor[e] = (uint64_t)q;
+    }
+    __syncthreads();
+    const int k = sh.k;
+    q = sh.q;
+    if (k < 1) continue;
+    const int size = 2 * k;
+    int F, jstart, D;
+    const bool use_tail = tail && size > n / 50;
+    if (use_tail) {
+      jstart = max(n - size, 1);  // bounds n-1 .. jstart, descending
+      F = n - jstart;
+      D = F;
+    } else {
+      jstart = max(n - size, 1);  // Floyd bounds jstart .. n-1 (j=0: no draw)
+      F = n - jstart;
+      D = F + size - 1;
+    }
+    int d0 = 0;
+    while (d0 < D) {
+      ensure(q, kWalk);
+      const int cnt = min(kWalk, D - d0);
+      if (tid == 0) sh.first = cnt;
+      __syncthreads();
+      if (tid < cnt) {
+        const int d = d0 + tid;
+        uint32_t rng;
+        if (use_tail)
+          rng = (uint32_t)(n - 1 - d);
+        else
+          rng = d < F ? (uint32_t)(jstart + d) : (uint32_t)(size - 1 - (d - F));
+        if (lemire_rejects(get(q + tid), rng)) atomicMin(&sh.first, tid);
+      }
+      __syncthreads();
+      const int first = sh.first;
+      if (first == cnt) {
+        q += cnt;
+        d0 += cnt;
+      } else {
+        q += first + 1;
+        d0 += first;
+      }
+      __syncthreads();
+    }
+    if (tid == 0) sh.q = q;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    Pcg r;
+    r.seek_u32(g, (uint64_t)sh.q);
+    r.store(v.streams[1]);
+    v.ctl->mut_q = (uint64_t)sh.q;
+  }
+}
+
+__global__ void __launch_bounds__(128) k_mut_apply(SwarmView v) {
+  if (!v.ctl->mutating || v.ctl->done) return;
+  const int e = blockIdx.x;
+  if (e >= v.ctl->n_events) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = v.n, np = v.np, tid = threadIdx.x;
+  const int p = v.ev_slot[e];
+  const int k = v.ev_k[e];
+  if (k < 1) return;
+  const int size = 2 * k;
+  uint16_t* idx = (uint16_t*)smem;                       // size (<= n)
+  double* sd = (double*)(smem + round_up(2 * (int64_t)np, 16));
+  uint32_t* bits = (uint32_t*)(sd + np);                 // n bits, or
+  uint16_t* arr = (uint16_t*)bits;                       // tail: arange(n)
+  const bool use_tail = (n > 10000) && size > n / 50;
+  if (use_tail) {
+    for (int i = tid; i < n; i += blockDim.x) arr[i] = (uint16_t)i;
+  } else {
+    for (int i = tid; i < (n + 31) / 32; i += blockDim.x) bits[i] = 0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    Pcg r;
+    r.seek_u32(*v.mut_start, v.ev_cursor[e]);
+    if (use_tail) {
+      const int first = max(n - size, 1);
+      for (int i = n - 1; i >= first; --i) {
+        uint32_t j = r.bounded((uint32_t)i);
+        uint16_t t = arr[i];
+        arr[i] = arr[j];
+        arr[j] = t;
+      }
+      for (int t = 0; t < size; ++t) idx[t] = arr[n - size + t];
+    } else {
+      for (int t = 0; t < size; ++t) {
+        const uint32_t j = (uint32_t)(n - size + t);
+        uint32_t val = r.bounded(j);
+        if (bits[val >> 5] & (1u << (val & 31))) val = j;
+        bits[val >> 5] |= 1u << (val & 31);
+        idx[t] = (uint16_t)val;
+      }
+      for (int i = size - 1; i >= 1; --i) {
+        uint32_t j = r.bounded((uint32_t)i);
+        uint16_t t = idx[i];
+        idx[i] = idx[j];
+        idx[j] = t;
+      }
+    }
+  }
+  __syncthreads();
+  uint16_t* body = v.x + (size_t)p * np;
+  // the k position pairs are disjoint (sampled without replacement)
+  for (int t = tid; t < k; t += blockDim.x) {
+    const int a = idx[2 * t], b = idx[2 * t + 1];
+    const uint16_t x = body[a];
+    body[a] = body[b];
+    body[b] = x;
+  }
+  __syncthreads();
+  double* dg = v.dcache + (size_t)p * np;
+  for (int i = tid; i < n; i += blockDim.x) {
+    const int a = body[i], b = body[i + 1 == n ? 0 : i + 1];
+    const double d = v.cost[(size_t)a * v.ld + b];
+    sd[i] = d;
+    dg[i] = d;
+  }
+  __syncthreads();
+  __shared__ int s_better;
+  if (tid == 0) {
+    const double f = seq_tour_sum(sd, n);
+    v.fit[p] = f;
+    s_better = f < v.pfit[p];
+    if (s_better) v.pfit[p] = f;
+  }
+  __syncthreads();
+  if (s_better) {
+    uint16_t* pb = v.pbest + (size_t)p * np;
+    for (int i = tid; i < n; i += blockDim.x) pb[i] = body[i];
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_mutation(const SwarmView& v, cudaStream_t s) {
+  const int P = v.P;
+  // canon info lives in the ev_k array until the walk overwrites it
+  int32_t* canon = v.ev_k;
+  k_mut_hash<<<P, 128, 0, s>>>(v, canon);
+  k_mut_rank<<<(P + 255) / 256, 256, 0, s>>>(v);
+  k_mut_dedupe<<<(P + 255) / 256, 256, 0, s>>>(v, canon);
+  k_mut_lists<<<1, 1024, 0, s>>>(v);
+  k_mut_copy<<<P, 128, 0, s>>>(v);
+  k_mut_walk<<<1, kWalk, 0, s>>>(v);
+  size_t smem = round_up(2 * (int64_t)v.np, 16) + (size_t)8 * v.np +
+                (v.n > 10000 ? (size_t)2 * v.np : round_up((v.n + 31) / 32 * 4, 16));
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_mut_apply,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  k_mut_apply<<<P, 128, smem, s>>>(v);
+  return cudaGetLastError();
+}
+
+}  // namespace dpso

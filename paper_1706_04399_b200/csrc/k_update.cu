@@ -1,0 +1,335 @@
+// Velocity / position update, fitness and pbest (solver.py:190-220).
+//
+// One CTA per particle.  For w == 1 (the paper default) the reference keeps
+// a composed velocity permutation vmap and moves x <- vmap o x after folding
+// the first k1 transpositions of the left-to-right repair x -> pbest and the
+// first k2 of x -> gbest into it (solver.py:196-212).  The repair is a
+// sequential scan in the reference; here it is computed data-parallel in
+// shared memory:
+//   pi(i)  = pos_x(T[i]);  emitting positions = non-maximal members of the
+//            non-trivial pi-cycles (cycle maxima by pointer jumping);
+//   t      = k-th emitting position (block scan);
+//   cur_t[q] = T[q] (q <= t) or T[r], r = first position > t on the backward
+//            pi-orbit of q (pointer jumping with threshold t);
+//   sigma(x[q]) = cur_t[q];  vmap' = sigma2 o sigma1 o vmap;  x' = vmap' o x.
+// Work is O(n log n) per particle with every thread busy; no transposition
+// list is ever materialised.  Fitness is then summed in the reference's
+// sequential order (closing edge first) so downstream decisions are exact.
+//
+// For w < 1 the reference keeps an explicit transposition list and replays
+// it (solver.py:213-216); that path runs the repair sequentially in one
+// thread per particle (k_update_seq) on a bounded per-particle ring.
+#include "dpso_internal.cuh"
+
+namespace dpso {
+
+namespace {
+
+template <int T>
+__device__ __forceinline__ int block_excl_scan(int val, int* s_warp,
+                                               int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = val;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < (T / 32) ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < (T / 32)) s_warp[lane] = w;  // inclusive per-warp totals
+  }
+  __syncthreads();
+  int base = warp > 0 ? s_warp[warp - 1] : 0;
+  *total = s_warp[T / 32 - 1];
+  __syncthreads();
+  return base + x - val;
+}
+
+// sigma (value permutation of the first prefix_len(c, L) repair
+// transpositions of x -> target) into sout[value].
+template <int T>
+__device__ void sigma_pass(const uint16_t* __restrict__ tgt_g, double c,
+                           int n, int R, const uint16_t* sx,
+                           const uint16_t* sposx, uint16_t* sT, uint16_t* sB,
+                           uint32_t* sW, uint16_t* sout, int* s_warp,
+                           int* s_misc) {
+  const int tid = threadIdx.x;
+  for (int i = tid; i < n; i += T) sT[i] = tgt_g[i];
+  __syncthreads();
+  // pi, its inverse (backward orbit), and (J, M) = (pi(p), p) for jumping
+  for (int i = tid; i < n; i += T) {
+    int pi = sposx[sT[i]];
+    sB[pi] = (uint16_t)i;
+    sW[i] = (uint32_t)pi | ((uint32_t)i << 16);
+  }
+  __syncthreads();
+  // cycle maxima: M(p) = max over 2^r orbit elements, J(p) = pi^(2^r)(p).
+  // (J, M) is one 32-bit word, so in-place jumping reads consistent pairs.
+  for (int r = 0; r < R; ++r) {
+    for (int p = tid; p < n; p += T) {
+      uint32_t w = sW[p];
+      uint32_t w2 = sW[w & 0xFFFFu];
+      uint32_t m = max(w >> 16, w2 >> 16);
+      sW[p] = (w2 & 0xFFFFu) | (m << 16);
+    }
+    __syncthreads();
+  }
+  // emitting = not the maximum of its cycle; contiguous chunk per thread
+  const int per = (n + T - 1) / T;
+  const int c0 = min(n, tid * per), c1 = min(n, c0 + per);
+  int cnt = 0;
+  for (int p = c0; p < c1; ++p) cnt += ((int)(sW[p] >> 16) != p);
+  int L;
+  int excl = block_excl_scan<T>(cnt, s_warp, &L);
+  const int k = prefix_len(c, L);
+  if (k == 0) {
+    for (int v = tid; v < n; v += T) sout[v] = (uint16_t)v;
+    __syncthreads();
+    return;
+  }
+  if (excl <= k - 1 && k - 1 < excl + cnt) {
+    int need = k - 1 - excl;
+    for (int p = c0; p < c1; ++p) {
+      if ((int)(sW[p] >> 16) != p) {
+        if (need == 0) {
+          s_misc[0] = p;
+          break;
+        }
+        --need;
+      }
+    }
+  }
+  __syncthreads();
+  const int t = s_misc[0];
+  // backward jumping to the first position > t: word = ptr | done << 16
+  for (int q = tid; q < n; q += T) {
+    uint32_t b = sB[q];
+    sW[q] = b | ((b > (uint32_t)t ? 1u : 0u) << 16);
+  }
+  __syncthreads();
+  for (int r = 0; r < 2 * R + 2; ++r) {
+    int pending = 0;
+    for (int q = tid; q < n; q += T) {
+      uint32_t w = sW[q];
+      if (!(w >> 16)) {
+        uint32_t w2 = sW[w & 0xFFFFu];
+        sW[q] = w2;
+        if (q > t && !(w2 >> 16)) pending = 1;
+      }
+    }
+    if (!__syncthreads_or(pending)) break;
+  }
+  for (int q = tid; q < n; q += T) {
+    uint16_t cur = (q <= t) ? sT[q] : sT[sW[q] & 0xFFFFu];
+    sout[sx[q]] = cur;
+  }
+  __syncthreads();
+}
+
+// x' is in sx; compute d_i, the sequential fitness, write x/dcache/fit and
+// update pbest (solver.py:217-220).  sd is an 8*np-byte scratch.
+template <int T>
+__device__ void finish_particle(const SwarmView& v, int p, const uint16_t* sx,
+                                double* sd, int* s_flag) {
+  const int n = v.n, np = v.np, tid = threadIdx.x;
+  uint16_t* xg = v.x + (size_t)p * np;
+  double* dg = v.dcache + (size_t)p * np;
+  for (int i = tid; i < n; i += T) {
+    int a = sx[i], b = sx[i + 1 == n ? 0 : i + 1];
+    double d = __ldg(v.cost + (size_t)a * v.ld + b);
+    sd[i] = d;
+    dg[i] = d;
+    xg[i] = (uint16_t)a;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double f = seq_tour_sum(sd, n);
+    v.fit[p] = f;
+    int better = f < v.pfit[p];
+    if (better) v.pfit[p] = f;
+    s_flag[0] = better;
+  }
+  __syncthreads();
+  if (s_flag[0]) {
+    uint16_t* pb = v.pbest + (size_t)p * np;
+    for (int i = tid; i < n; i += T) pb[i] = sx[i];
+  }
+  __syncthreads();
+}
+
+template <int T>
+__global__ void __launch_bounds__(T) k_update_w1(SwarmView v, int R) {
+  if (v.ctl->done) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = v.n, np = v.np, tid = threadIdx.x;
+  uint16_t* sx = (uint16_t*)smem;
+  uint16_t* sposx = sx + np;
+  uint16_t* ssig1 = sposx + np;
+  uint16_t* ssig2 = ssig1 + np;
+  uint16_t* sT = ssig2 + np;
+  uint16_t* sB = sT + np;
+  uint32_t* sW = (uint32_t*)(sB + np);
+  double* sd = (double*)sT;  // aliases sT, sB, sW (8*np bytes)
+  __shared__ int s_warp[32];
+  __shared__ int s_misc[4];
+  __shared__ double s_c[2];
+
+  for (int p = blockIdx.x; p < v.P; p += gridDim.x) {
+    const uint16_t* xg = v.x + (size_t)p * np;
+    for (int i = tid; i < n; i += T) sx[i] = xg[i];
+    __syncthreads();
+    for (int i = tid; i < n; i += T) sposx[sx[i]] = (uint16_t)i;
+    if (tid == 0) {
+      Pcg r;
+      r.load(v.streams[2 + p]);
+      double r1 = r.next_double();
+      double r2 = r.next_double();
+      r.store(v.streams[2 + p]);
+      s_c[0] = __dmul_rn(v.cognitive, r1);
+      s_c[1] = __dmul_rn(v.social, r2);
+    }
+    __syncthreads();
+    sigma_pass<T>(v.pbest + (size_t)p * np, s_c[0], n, R, sx, sposx, sT, sB,
+                  sW, ssig1, s_warp, s_misc);
+    sigma_pass<T>(v.gbest, s_c[1], n, R, sx, sposx, sT, sB, sW, ssig2, s_warp,
+                  s_misc);
+    // vmap' = sigma2 o sigma1 o vmap (solver.py:201-209), x' = vmap' o x
+    uint16_t* vm = v.vmap + (size_t)p * np;
+    for (int u = tid; u < n; u += T) sB[u] = ssig2[ssig1[vm[u]]];
+    __syncthreads();
+    for (int u = tid; u < n; u += T) vm[u] = sB[u];
+    for (int i = tid; i < n; i += T) sx[i] = sB[sx[i]];
+    __syncthreads();
+    finish_particle<T>(v, p, sx, sd, s_misc);
+  }
+}
+
+// ---- w < 1: explicit transposition lists (solver.py:213-216) -------------
+
+__device__ int repair_seq(const uint16_t* sx, const uint16_t* tgt, int n,
+                          uint16_t* cur, uint16_t* pos, uint32_t* out) {
+  for (int i = 0; i < n; ++i) {
+    cur[i] = sx[i];
+    pos[sx[i]] = (uint16_t)i;
+  }
+  int cnt = 0;
+  for (int i = 0; i < n; ++i) {
+    uint16_t want = tgt[i], have = cur[i];
+    if (have != want) {
+      int j = pos[want];
+      cur[j] = have;
+      pos[have] = (uint16_t)j;
+      out[cnt++] = (uint32_t)have | ((uint32_t)want << 16);
+    }
+  }
+  return cnt;
+}
+
+__global__ void __launch_bounds__(32) k_update_seq(SwarmView v) {
+  if (v.ctl->done) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = v.n, np = v.np, tid = threadIdx.x;
+  uint16_t* sx = (uint16_t*)smem;
+  uint16_t* scur = sx + np;
+  uint16_t* spos = scur + np;
+  uint16_t* sgt = spos + np;
+  double* sd = (double*)(sgt + np);
+  __shared__ int s_flag[2];
+  for (int p = blockIdx.x; p < v.P; p += gridDim.x) {
+    const uint16_t* xg = v.x + (size_t)p * np;
+    for (int i = tid; i < n; i += 32) sx[i] = xg[i];
+    __syncwarp();
+    if (tid == 0) {
+      Pcg r;
+      r.load(v.streams[2 + p]);
+      double r1 = r.next_double(), r2 = r.next_double();
+      r.store(v.streams[2 + p]);
+      double c1 = __dmul_rn(v.cognitive, r1), c2 = __dmul_rn(v.social, r2);
+      const int64_t stride = v.vel_cap + 2 * (int64_t)n;
+      uint32_t* lst = v.vel + (size_t)p * stride;
+      uint32_t* t1 = lst + v.vel_cap;
+      uint32_t* t2 = t1 + n;
+      const uint16_t* pb = v.pbest + (size_t)p * np;
+      for (int i = 0; i < n; ++i) sgt[i] = pb[i];
+      int L1 = repair_seq(sx, sgt, n, scur, spos, t1);
+      int k1 = prefix_len(c1, L1);
+      for (int i = 0; i < n; ++i) sgt[i] = v.gbest[i];
+      int L2 = repair_seq(sx, sgt, n, scur, spos, t2);
+      int k2 = prefix_len(c2, L2);
+      int len = v.vel_len[p];
+      int k0 = prefix_len(v.inertia, len);
+      if ((int64_t)k0 + k1 + k2 > v.vel_cap) {
+        v.ctl->vel_overflow = 1;
+        k0 = 0;
+      }
+      for (int e = 0; e < k1; ++e) lst[k0 + e] = t1[e];
+      for (int e = 0; e < k2; ++e) lst[k0 + k1 + e] = t2[e];
+      len = k0 + k1 + k2;
+      v.vel_len[p] = len;
+      // _apply_open (solver.py:72-79) on the whole new velocity
+      for (int i = 0; i < n; ++i) {
+        scur[i] = sx[i];
+        spos[sx[i]] = (uint16_t)i;
+      }
+      for (int e = 0; e < len; ++e) {
+        uint32_t ab = lst[e];
+        uint16_t a = ab & 0xFFFFu, b = ab >> 16;
+        uint16_t ia = spos[a], ib = spos[b];
+        scur[ia] = b;
+        scur[ib] = a;
+        spos[a] = ib;
+        spos[b] = ia;
+      }
+      for (int i = 0; i < n; ++i) sx[i] = scur[i];
+    }
+    __syncwarp();
+    finish_particle<32>(v, p, sx, sd, s_flag);
+  }
+}
+
+}  // namespace
+
+static int ceil_log2(int n) {
+  int r = 0;
+  while ((1 << r) < n) ++r;
+  return r;
+}
+
+cudaError_t launch_update(const SwarmView& v, cudaStream_t s) {
+  const int grid = v.P;
+  if (v.inertia == 1.0) {
+    size_t smem = (size_t)16 * v.np;
+    const int R = ceil_log2(v.n);
+    if (v.n <= 2048) {
+      auto k = k_update_w1<256>;
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+      k<<<grid, 256, smem, s>>>(v, R);
+    } else {
+      auto k = k_update_w1<512>;
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+      k<<<grid, 512, smem, s>>>(v, R);
+    }
+  } else {
+    size_t smem = (size_t)8 * v.np + (size_t)8 * v.np;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_update_seq,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+    k_update_seq<<<grid, 32, smem, s>>>(v);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace dpso

@@ -1,0 +1,324 @@
+"""Drop-in ``DiscreteSwarmSolver`` running the enhanced DPSO on a B200.
+
+Mirrors the reference estimator (``inspectour/solver.py:109-356``): same
+constructor parameters (stored verbatim, sklearn ``BaseEstimator``), same
+validation and error messages in ``fit`` (solver.py:139-172), same fitted
+attributes ``best_tour_``, ``best_fitness_``, ``convergence_``,
+``n_generations_``, ``report_``, and ``solve_matrix``.  With the default
+``rng="numpy"`` the device reproduces the reference's numpy PCG64 streams
+exactly (``SeedSequence(random_state).spawn(P + 2)``, solver.py:278-282), so a
+fit returns the reference's tour and convergence trace bit for bit.
+
+Extra keyword-only knobs (explicit parameters, as sklearn requires):
+``rng`` ("numpy" | "philox") and ``device`` (a CUDA device, default current).
+
+All compute runs in ``libdpso.so`` (hand-written sm_100a CUDA); PyTorch only
+provides device memory and the stream.  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+from sklearn.base import BaseEstimator
+
+from . import _lib
+
+
+@dataclass
+class SolveReport:
+    """solver.py:23-30."""
+    best_tour: tuple[int, ...]
+    best_fitness: float
+    convergence: list[float]
+    generations_run: int
+    wall_time: float
+    augmentation_flags: dict[str, bool] = field(default_factory=dict)
+
+
+_M64 = (1 << 64) - 1
+
+
+def numpy_stream_states(random_state, count: int) -> np.ndarray:
+    """PCG64 states of ``SeedSequence(random_state).spawn(count)`` as the
+    (count, 6) uint64 records ``dpso_set_streams`` expects."""
+    seqs = np.random.SeedSequence(random_state).spawn(count)
+    out = np.empty((count, 6), dtype=np.uint64)
+    for i, s in enumerate(seqs):
+        st = np.random.PCG64(s).state
+        a, b = st["state"]["state"], st["state"]["inc"]
+        out[i] = (a >> 64, a & _M64, b >> 64, b & _M64, st["has_uint32"],
+                  st["uinteger"])
+    return out
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "paper_1706_04399_b200 needs a CUDA (sm_100a) device; there is no "
+            "CPU fallback")
+    return torch
+
+
+def device_cost(X: np.ndarray, device=None):
+    """Upload an n x n fp64 matrix into a zero-padded (n, ld) device tensor
+    with ld = round_up(n, 8) (16-B aligned rows for the bulk row copies)."""
+    torch = _torch()
+    n = X.shape[0]
+    ld = (n + 7) // 8 * 8
+    dev = torch.device(device) if device is not None else torch.device(
+        "cuda", torch.cuda.current_device())
+    buf = torch.zeros((n, ld), dtype=torch.float64, device=dev)
+    buf[:, :n].copy_(torch.from_numpy(np.ascontiguousarray(X, dtype=float)))
+    return buf, ld
+
+
+class SwarmContext:
+    """Owns one device swarm (workspace tensor + ``dpso_ctx``)."""
+
+    def __init__(self, params: "_lib.DpsoParams", n: int, cost_tensor, ld,
+                 device=None):
+        torch = _torch()
+        self.lib = _lib.load()
+        self.torch = torch
+        self.params = params
+        self.n = n
+        self.device = cost_tensor.device
+        nbytes = ctypes.c_size_t(0)
+        _lib.check(self.lib.dpso_workspace_size(ctypes.byref(params), n,
+                                                ctypes.byref(nbytes)))
+        self.workspace = torch.empty(int(nbytes.value), dtype=torch.uint8,
+                                     device=self.device)
+        self.cost = cost_tensor
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.dpso_create(
+            ctypes.byref(params), n, self.workspace.data_ptr(),
+            int(nbytes.value), stream, ctypes.byref(h)))
+        self.h = h
+        _lib.check(self.lib.dpso_set_cost(h, cost_tensor.data_ptr(), ld))
+
+    def set_streams(self, states: np.ndarray) -> None:
+        states = np.ascontiguousarray(states, dtype=np.uint64)
+        _lib.check(self.lib.dpso_set_streams(
+            self.h, states.ctypes.data_as(ctypes.c_void_p)))
+
+    def init(self, seed_body, n_seed: int) -> None:
+        if seed_body is not None and n_seed > 0:
+            arr = np.ascontiguousarray(seed_body, dtype=np.int32)
+            ptr = arr.ctypes.data_as(ctypes.c_void_p)
+        else:
+            arr, ptr, n_seed = None, None, 0
+        _lib.check(self.lib.dpso_init(self.h, ptr, int(n_seed)))
+
+    def run(self) -> int:
+        g = ctypes.c_int32(0)
+        _lib.check(self.lib.dpso_run(self.h, ctypes.byref(g)))
+        return int(g.value)
+
+    def step(self, gens: int) -> None:
+        _lib.check(self.lib.dpso_step(self.h, int(gens)))
+
+    def step_timed(self, gens: int):
+        """Per-phase device ms over `gens` generations (dpso_step_timed)."""
+        ms = np.zeros(6, dtype=np.float64)
+        cnt = ctypes.c_int32(0)
+        _lib.check(self.lib.dpso_step_timed(
+            self.h, int(gens), ms.ctypes.data_as(ctypes.c_void_p),
+            ctypes.byref(cnt)))
+        return ms, int(cnt.value)
+
+    def ctl(self):
+        out = np.zeros(6, dtype=np.int32)
+        gf = ctypes.c_double(0.0)
+        _lib.check(self.lib.dpso_ctl(self.h, out.ctypes.data_as(
+            ctypes.c_void_p), ctypes.byref(gf)))
+        keys = ("gen", "stall", "done", "gens_run", "two_opt_count",
+                "n_events")
+        d = {k: int(v) for k, v in zip(keys, out)}
+        d["gbest_fit"] = float(gf.value)
+        return d
+
+    def result(self):
+        n = self.n
+        tour = np.empty(n + 1, dtype=np.int32)
+        fit = ctypes.c_double(0.0)
+        conv = np.empty(self.params.max_generations + 1, dtype=np.float64)
+        nconv = ctypes.c_int32(0)
+        _lib.check(self.lib.dpso_result(
+            self.h, tour.ctypes.data_as(ctypes.c_void_p), ctypes.byref(fit),
+            conv.ctypes.data_as(ctypes.c_void_p), ctypes.byref(nconv)))
+        return tour, float(fit.value), conv[:nconv.value]
+
+    def state(self):
+        P, n = self.params.n_particles, self.n
+        x = np.empty((P, n), np.int32)
+        pb = np.empty((P, n), np.int32)
+        vm = np.empty((P, n), np.int32)
+        fit = np.empty(P, np.float64)
+        pfit = np.empty(P, np.float64)
+        gb = np.empty(n, np.int32)
+        gf = ctypes.c_double(0.0)
+        ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        _lib.check(self.lib.dpso_get_state(self.h, ptr(x), ptr(pb), ptr(fit),
+                                           ptr(pfit), ptr(vm), ptr(gb),
+                                           ctypes.byref(gf)))
+        return {"x": x, "pbest": pb, "fit": fit, "pfit": pfit, "vmap": vm,
+                "gbest": gb, "gbest_fit": float(gf.value)}
+
+    def offer_gbest(self, tour, fitness: float) -> None:
+        arr = np.ascontiguousarray(tour, dtype=np.int32)
+        _lib.check(self.lib.dpso_offer_gbest(
+            self.h, arr.ctypes.data_as(ctypes.c_void_p), float(fitness)))
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.dpso_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DiscreteSwarmSolver(BaseEstimator):
+    """Discrete PSO tour optimizer over a cost matrix (GPU).
+
+    Parameters are those of the reference (solver.py:118-135) plus ``rng``
+    and ``device``.  ``fit(X)`` expects a square cost matrix and exposes
+    ``best_tour_``, ``best_fitness_``, ``convergence_``, ``n_generations_``
+    and ``report_`` afterwards.
+    """
+
+    def __init__(self, n_particles=100, inertia=1.0, cognitive=0.4,
+                 social=0.4, max_generations=200, stall_generations=30,
+                 mutation_period=3, seed_fraction=0.1, seed_tour=None,
+                 use_mutation=True, use_edge_exchange=True, parallel=False,
+                 random_state=None, rng="numpy", device=None):
+        self.n_particles = n_particles
+        self.inertia = inertia
+        self.cognitive = cognitive
+        self.social = social
+        self.max_generations = max_generations
+        self.stall_generations = stall_generations
+        self.mutation_period = mutation_period
+        self.seed_fraction = seed_fraction
+        self.seed_tour = seed_tour
+        self.use_mutation = use_mutation
+        self.use_edge_exchange = use_edge_exchange
+        self.parallel = parallel
+        self.random_state = random_state
+        self.rng = rng
+        self.device = device
+
+    # -- validation (solver.py:139-162) -------------------------------------
+    def _check_params(self):
+        if self.n_particles < 3:
+            raise ValueError("n_particles must be >= 3")
+        for name in ("inertia", "cognitive", "social"):
+            v = getattr(self, name)
+            if not 0.0 <= v <= 1.0:
+                raise ValueError(f"{name} must be in [0, 1], got {v}")
+        if self.max_generations < 1:
+            raise ValueError("max_generations must be >= 1")
+        if self.stall_generations < 1:
+            raise ValueError("stall_generations must be >= 1")
+        if self.mutation_period < 1:
+            raise ValueError("mutation_period must be >= 1")
+        if not 0.0 <= self.seed_fraction <= 1.0:
+            raise ValueError("seed_fraction must be in [0, 1]")
+        if self.rng not in _lib.RNG_MODES:
+            raise ValueError(f"rng must be one of {sorted(_lib.RNG_MODES)}")
+
+    @staticmethod
+    def _check_cost(X) -> np.ndarray:
+        X = np.asarray(X, dtype=float)
+        if X.ndim != 2 or X.shape[0] != X.shape[1]:
+            raise ValueError(f"cost matrix must be square, got {X.shape}")
+        if not np.isfinite(X).all():
+            raise ValueError("cost matrix must be finite")
+        return X
+
+    def _params(self) -> "_lib.DpsoParams":
+        return _lib.DpsoParams(
+            n_particles=int(self.n_particles), inertia=float(self.inertia),
+            cognitive=float(self.cognitive), social=float(self.social),
+            max_generations=int(self.max_generations),
+            stall_generations=int(self.stall_generations),
+            mutation_period=int(self.mutation_period),
+            seed_fraction=float(self.seed_fraction),
+            use_mutation=int(bool(self.use_mutation)),
+            use_edge_exchange=int(bool(self.use_edge_exchange)),
+            parallel=int(bool(self.parallel)),
+            rng_mode=_lib.RNG_MODES[self.rng],
+            philox_seed=0)
+
+    def _seed(self, n):
+        """solver.py:167-174."""
+        if self.seed_tour is not None and self.seed_fraction > 0:
+            seed_body = [int(v) for v in list(self.seed_tour[:-1])]
+            if sorted(seed_body) != list(range(n)):
+                raise ValueError("seed_tour is not a tour over the matrix")
+            n_seed = min(self.n_particles,
+                         int(self.seed_fraction * self.n_particles + 0.5))
+            return seed_body, n_seed
+        return None, 0
+
+    # -- main entry (solver.py:262-335) -------------------------------------
+    def fit(self, X, y=None):
+        self._check_params()
+        cost = self._check_cost(X)
+        n = cost.shape[0]
+        t0 = time.perf_counter()
+        flags = {
+            "init": self.seed_tour is not None and self.seed_fraction > 0,
+            "mutation": self.use_mutation,
+            "edge_exchange": self.use_edge_exchange,
+            "parallel": self.parallel,
+        }
+        if n == 1:
+            self._finish((0, 0), 0.0, [0.0], 1, t0, flags)
+            return self
+        seed_body, n_seed = self._seed(n)
+        ctx = self._make_context(cost)
+        try:
+            ctx.set_streams(numpy_stream_states(self.random_state,
+                                                self.n_particles + 2))
+            ctx.init(seed_body, n_seed)
+            gens = ctx.run()
+            tour, fit, conv = ctx.result()
+        finally:
+            ctx.close()
+        self._finish(tuple(int(v) for v in tour), fit,
+                     [float(c) for c in conv], gens, t0, flags)
+        return self
+
+    def _make_context(self, cost: np.ndarray) -> SwarmContext:
+        cost_t, ld = device_cost(cost, self.device)
+        return SwarmContext(self._params(), cost.shape[0], cost_t, ld)
+
+    def _finish(self, tour, fitness, convergence, generations, t0, flags):
+        self.best_tour_ = tuple(int(x) for x in tour)
+        self.best_fitness_ = float(fitness)
+        self.convergence_ = [float(c) for c in convergence]
+        self.n_generations_ = generations
+        self.report_ = SolveReport(
+            best_tour=self.best_tour_,
+            best_fitness=self.best_fitness_,
+            convergence=self.convergence_,
+            generations_run=generations,
+            wall_time=time.perf_counter() - t0,
+            augmentation_flags=flags,
+        )
+
+
+def solve_matrix(cost, **params) -> SolveReport:
+    """One-shot convenience wrapper (solver.py:352-356)."""
+    solver = DiscreteSwarmSolver(**params)
+    solver.fit(cost)
+    return solver.report_

@@ -1,0 +1,135 @@
+"""GPU parity: the CUDA path through the C ABI against the golden vectors of
+the reference and against the oracle, bit for bit (permutations, argmin
+choices, fitness bits — numpy-exact RNG streams make whole runs identical)."""
+import numpy as np
+import pytest
+
+from conftest import golden_matrix, golden_params, random_euclidean_matrix
+from oracle import dpso_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    from paper_1706_04399_b200.build import build
+    build()
+    import paper_1706_04399_b200 as pkg
+    return pkg
+
+
+def test_e2e_golden_runs(pkg, golden_e2e):
+    for case in golden_e2e["cases"]:
+        cost = golden_matrix(golden_e2e, case["instance"])
+        s = pkg.DiscreteSwarmSolver(**golden_params(golden_e2e, case)).fit(cost)
+        ctx = (case["instance"], case["params"])
+        assert list(s.best_tour_) == case["best_tour"], ctx
+        assert s.best_fitness_ == case["best_fitness"], ctx
+        assert s.convergence_ == case["convergence"], ctx
+        assert s.n_generations_ == case["n_generations"], ctx
+
+
+def test_best_exchange_golden(pkg, golden_kernels):
+    by_inst = {}
+    for rec in golden_kernels["best_exchange"]:
+        by_inst.setdefault(rec["instance"], []).append(rec)
+    for inst, recs in by_inst.items():
+        cost = golden_matrix(golden_kernels, inst)
+        tours = np.array([r["body"] for r in recs], dtype=np.int32)
+        new, delta = pkg.best_exchange_batch(cost, tours)
+        for r, nb, d in zip(recs, new, delta):
+            assert [int(v) for v in nb] == r["new_body"], inst
+            assert float(d) == r["delta"], inst
+        costs = pkg.tour_cost_batch(cost, tours)
+        assert [float(c) for c in costs] == [r["cost"] for r in recs]
+
+
+def test_best_exchange_vs_oracle_sizes(pkg):
+    rng = np.random.default_rng(3)
+    for n in (4, 5, 31, 32, 33, 64, 65, 127, 300, 513, 1000, 1500, 2049, 2500):
+        cost = random_euclidean_matrix(n, rng)
+        if n in (65, 513):  # integer costs: many ties
+            cost = np.floor(cost)
+        tours = np.array([rng.permutation(n) for _ in range(6)],
+                         dtype=np.int32)
+        new, delta = pkg.best_exchange_batch(cost, tours)
+        for t, nb, d in zip(tours, new, delta):
+            eb, ed = O.best_exchange([int(v) for v in t], cost)
+            assert [int(v) for v in nb] == [int(v) for v in eb], n
+            assert float(d) == ed, n
+
+
+def test_nn_two_opt_golden(pkg, golden_kernels):
+    for rec in golden_kernels["nn_two_opt"]:
+        cost = golden_matrix(golden_kernels, rec["instance"])
+        tour, total = pkg.nearest_neighbor_two_opt(cost)
+        assert list(tour) == rec["tour"], rec["instance"]
+        assert total == rec["cost"], rec["instance"]
+        nn = pkg.nearest_neighbor_tour(cost)
+        assert nn == O.nearest_neighbor_body(cost)
+
+
+@pytest.mark.parametrize("n,P,G,kw", [
+    (40, 30, 25, {}),
+    (40, 30, 25, {"mutation_period": 1}),
+    (97, 24, 12, {"inertia": 0.5}),
+    (130, 40, 10, {"seed_fraction": 0.3}),
+    (260, 33, 6, {}),
+    (200, 64, 8, {"use_edge_exchange": False, "mutation_period": 2}),
+])
+def test_per_generation_state_matches_oracle(pkg, n, P, G, kw):
+    from paper_1706_04399_b200.solver import numpy_stream_states
+    cost = random_euclidean_matrix(n, np.random.default_rng(n))
+    seed = list(range(n)) + [0]
+    params = dict(n_particles=P, max_generations=G, stall_generations=G,
+                  random_state=n + P, seed_tour=seed, **kw)
+    orc = O.OracleSolver(**params)
+    trace = []
+    orc.fit(cost, trace=trace)
+    gpu = pkg.DiscreteSwarmSolver(**params)
+    seed_body, n_seed = gpu._seed(n)
+    ctx = gpu._make_context(cost)
+    try:
+        ctx.set_streams(numpy_stream_states(params["random_state"], P + 2))
+        ctx.init(seed_body, n_seed)
+        for step, (_, st, gbest, gfit) in enumerate(trace):
+            if step > 0:
+                ctx.step(1)
+            g = ctx.state()
+            assert g["x"].tolist() == st.x, step
+            assert g["fit"].tolist() == st.fit, step
+            assert g["pbest"].tolist() == st.pbest, step
+            assert g["pfit"].tolist() == st.pfit, step
+            if gpu.inertia == 1.0:
+                assert g["vmap"].tolist() == st.vmap, step
+            assert g["gbest"].tolist() == gbest, step
+            assert g["gbest_fit"] == gfit, step
+    finally:
+        ctx.close()
+
+
+def test_full_size_properties(pkg):
+    # BASELINE config-2 size (N=1000, P=1024), a few generations: every tour
+    # stays a permutation, fitness equals the recomputed tour cost, the
+    # convergence trace is monotone.
+    n, P = 1000, 1024
+    cost = random_euclidean_matrix(n, np.random.default_rng(1000))
+    s = pkg.DiscreteSwarmSolver(n_particles=P, max_generations=6,
+                                stall_generations=6, random_state=0)
+    seed_body, n_seed = s._seed(n)
+    from paper_1706_04399_b200.solver import numpy_stream_states
+    ctx = s._make_context(cost)
+    try:
+        ctx.set_streams(numpy_stream_states(0, P + 2))
+        ctx.init(None, 0)
+        ctx.step(6)
+        st = ctx.state()
+        assert (np.sort(st["x"], axis=1) == np.arange(n)).all()
+        assert (np.sort(st["pbest"], axis=1) == np.arange(n)).all()
+        rec = pkg.tour_cost_batch(cost, st["x"])
+        assert np.allclose(rec, st["fit"], rtol=1e-9, atol=0)
+        tour, fit, conv = ctx.result()
+        assert all(b <= a for a, b in zip(conv, conv[1:]))
+        assert fit == conv[-1]
+    finally:
+        ctx.close()

@@ -1,0 +1,78 @@
+"""The C-ABI library builds for sm_100a, loads on a CPU host, and exports
+every symbol include/dpso.h declares (no compute calls without a GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import ROOT
+from paper_1706_04399_b200 import _lib
+from paper_1706_04399_b200.build import build
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build()
+    return _lib.load()
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "dpso.h")).read()
+    return sorted(set(re.findall(r"\b(dpso_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_exports_every_declared_symbol(lib):
+    decl = declared_symbols()
+    assert len(decl) >= 15
+    for name in decl:
+        assert hasattr(lib, name), name
+    assert set(decl) == set(_lib.EXPORTED)
+
+
+def test_version_and_param_validation(lib):
+    assert b"sm_100a" in lib.dpso_version()
+    p = _lib.DpsoParams(n_particles=2, inertia=1.0, cognitive=0.4,
+                        social=0.4, max_generations=10, stall_generations=5,
+                        mutation_period=3, seed_fraction=0.1, use_mutation=1,
+                        use_edge_exchange=1, parallel=0, rng_mode=0)
+    nb = ctypes.c_size_t(0)
+    rc = lib.dpso_workspace_size(ctypes.byref(p), 10, ctypes.byref(nb))
+    assert rc == _lib.DPSO_EINVAL
+    assert b"n_particles must be >= 3" in lib.dpso_last_error()
+    with pytest.raises(ValueError, match="n_particles"):
+        _lib.check(rc)
+    p.n_particles = 32
+    p.inertia = 1.5
+    rc = lib.dpso_workspace_size(ctypes.byref(p), 10, ctypes.byref(nb))
+    assert rc == _lib.DPSO_EINVAL and b"inertia" in lib.dpso_last_error()
+    p.inertia = 1.0
+    assert lib.dpso_workspace_size(ctypes.byref(p), 1000,
+                                   ctypes.byref(nb)) == 0
+    assert nb.value > 32 * 1000 * 2 * 3
+
+
+def test_sass_is_sm100a():
+    so = os.path.join(ROOT, "paper_1706_04399_b200", "libdpso.so")
+    out = os.popen(f"cuobjdump --list-elf {so} 2>&1").read()
+    assert "sm_100a" in out
+
+
+def test_estimator_api_cpu():
+    # construction / get_params / validation never touch the device
+    from paper_1706_04399_b200 import DiscreteSwarmSolver
+    s = DiscreteSwarmSolver(n_particles=10, random_state=5)
+    params = s.get_params()
+    assert params["n_particles"] == 10
+    assert DiscreteSwarmSolver(**params).get_params() == params
+    s.set_params(social=0.3)
+    assert s.social == 0.3
+    import numpy as np
+    with pytest.raises(ValueError):
+        DiscreteSwarmSolver().fit(np.zeros((3, 2)))
+    with pytest.raises(ValueError):
+        DiscreteSwarmSolver(n_particles=2).fit(np.zeros((3, 3)))
+    with pytest.raises(ValueError):
+        DiscreteSwarmSolver(mutation_period=0).fit(np.zeros((3, 3)))
+    r = DiscreteSwarmSolver(random_state=0).fit(np.zeros((1, 1)))
+    assert r.best_tour_ == (0, 0) and r.n_generations_ == 1
