@@ -98,14 +98,27 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        import threading
+        self.lines = []
+        self.proc = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200",
+                 "--format=csv,noheader,nounits", "-lms", "20",
                  "-i", str(self.index)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
-            self.proc = None
+            return self
+        first = threading.Event()
+
+        def pump():
+            for line in self.proc.stdout:
+                self.lines.append(line)
+                first.set()
+        self.thread = threading.Thread(target=pump, daemon=True)
+        self.thread.start()
+        first.wait(timeout=10.0)  # sampler is live before the timed region
+        self.skip = len(self.lines)
         return self
 
     def __exit__(self, *exc):
@@ -113,9 +126,11 @@ class ClockSampler:
         if self.proc is not None:
             self.proc.terminate()
             try:
-                self.out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+            self.thread.join(timeout=5)
+            self.out = "".join(self.lines[self.skip:])
 
     def summary(self):
         rows = []
@@ -395,7 +410,7 @@ def run_ours(args, cfg_name, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))

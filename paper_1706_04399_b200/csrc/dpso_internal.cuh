@@ -44,6 +44,8 @@ struct DevCtl {
   int32_t collision;  // canonical-hash collision seen (diagnostic)
   int32_t vel_overflow;
   int32_t two_opt_count;  // generations in which the 2-opt pass ran
+  int32_t mut_bad;        // first event whose sample needed a redraw
+  int32_t pad_;
   uint64_t mut_q;     // u32 draws consumed by the current mutation call
 };
 
@@ -90,6 +92,7 @@ struct SwarmView {
   int32_t* ev_slot;
   int32_t* ev_k;
   uint64_t* ev_cursor;
+  uint16_t* ev_idx;    // P x np sampled positions per mutation event
   uint64_t* init_cursor;
 };
 

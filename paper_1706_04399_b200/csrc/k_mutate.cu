@@ -9,13 +9,16 @@
 //   k_mut_lists  survivors / dropped in rank order, keep = first ceil(S/3)
 //                survivors, events = non-kept slots in slot order
 //   k_mut_copy   dropped #r copies body+fitness of survivors[r % S]
-//   k_mut_walk   walks the single mutation stream: k = integers(1, k_hi+1),
-//                then the Floyd + shuffle draws of choice(n, 2k, False),
-//                checking Lemire rejections 1024 draws at a time, to find
-//                where every event's draws start
-//   k_mut_apply  one CTA per event: regenerate its draws from the stream
-//                (PCG64 jump-ahead), Floyd/tail-shuffle sampler, k disjoint
-//                swaps, fitness in reference order, pbest (solver.py:241-258)
+//   k_mut_walk   chains k = integers(1, k_hi+1) through the single mutation
+//                stream to find where every event's draws start
+//   k_mut_sample one CTA per event: regenerate its draws (PCG64 jump-ahead),
+//                numpy's Floyd / tail-shuffle sampler, verify the draw count
+//   k_mut_fix    exact sequential re-walk from the first event that needed a
+//                Lemire redraw (rare), persistent stream state update
+//   k_mut_swap   k disjoint swaps, fitness in reference order, pbest
+//                (solver.py:241-258)
+#include <algorithm>
+
 #include "dpso_internal.cuh"
 
 namespace dpso {
@@ -218,194 +221,249 @@ __global__ void __launch_bounds__(128) k_mut_copy(SwarmView v) {
 }
 
 // ---- the sequential stream walk ------------------------------------------
+//
+// The mutation stream is ONE numpy PCG64 stream consumed in slot order, so
+// where event e's draws start depends on every earlier event's k.  The walk
+// is split: (1) k_mut_walk chains only the k-draws (one thread, reading a
+// shared-memory ring of the stream that the whole CTA refills by PCG jump-
+// ahead), assuming the Floyd/shuffle draws of each event need no Lemire
+// redraw; (2) k_mut_sample (one CTA per event) regenerates the event's draws
+// from its cursor, runs the exact numpy sampler and counts the u32 it
+// consumed - a mismatch means a redraw happened (probability ~1e-7 per draw
+// at n=1000); (3) k_mut_fix redoes the walk exactly and sequentially from the
+// first such event (rare path) and advances the persistent stream state;
+// (4) k_mut_swap applies the k disjoint swaps, fitness and pbest.
 
-constexpr int kWalk = 1024;     // threads
-constexpr int kRing = 4096;     // u32 ring (fresh draws)
-constexpr int kHalf = kRing / 2;
+constexpr int kWalk = 1024;          // threads
+constexpr int kRing = 16384;         // u32 in the ring (64 KiB dynamic smem)
+constexpr int kOutPerThread = kRing / 2 / kWalk;
 
-struct WalkShared {
-  uint32_t ring[kRing];
-  int64_t wbase;  // fresh index of ring window start
-  int64_t q;      // u32 draws consumed
-  int k;
-  int first;
-};
+// number of Floyd + shuffle draws of choice(n, 2k, replace=False) when no
+// Lemire redraw happens (numpy _generator.pyx: Floyd skips j == 0; n > 10000
+// with 2k > n // 50 uses the tail shuffle instead)
+__device__ __forceinline__ int sample_draws(int n, int k) {
+  const int size = 2 * k;
+  const int jstart = max(n - size, 1);
+  const int F = n - jstart;
+  if (n > 10000 && size > n / 50) return F;
+  return F + size - 1;
+}
 
 __global__ void __launch_bounds__(kWalk) k_mut_walk(SwarmView v) {
   if (!v.ctl->mutating || v.ctl->done) return;
-  __shared__ WalkShared sh;
+  extern __shared__ __align__(16) uint32_t ring[];
+  __shared__ int64_t s_q, s_wbase;
+  __shared__ int s_e;
   const int tid = threadIdx.x;
   const PcgState g = v.streams[1];
-  if (tid == 0) *v.mut_start = g;
+  if (tid == 0) {
+    *v.mut_start = g;
+    s_q = 0;
+    s_e = 0;
+    s_wbase = -(int64_t)kRing;  // force a fill
+    v.ctl->mut_bad = 0x7fffffff;
+  }
   const int64_t h = (int64_t)g.has_uint32;
   const uint32_t ub = (uint32_t)g.uinteger;
   const u128 S0 = {g.state_hi, g.state_lo}, inc = {g.inc_hi, g.inc_lo};
-  // thread state: output index (1-based) 1 + tid, then + kWalk per slide
-  u128 st = pcg_advance(S0, inc, 1 + (uint64_t)tid);
   u128 A, C;
   pcg_jump_coeffs(kWalk, inc, &A, &C);
-  {
-    uint64_t o = pcg_output(st);
-    sh.ring[2 * tid] = (uint32_t)o;
-    sh.ring[2 * tid + 1] = (uint32_t)(o >> 32);
-    st = add128(mul128(A, st), C);
-    o = pcg_output(st);
-    sh.ring[kHalf + 2 * tid] = (uint32_t)o;
-    sh.ring[kHalf + 2 * tid + 1] = (uint32_t)(o >> 32);
-  }
-  if (tid == 0) {
-    sh.wbase = 0;
-    sh.q = 0;
-  }
-  __syncthreads();
-
-  auto get = [&](int64_t q) -> uint32_t {
-    if (q < h) return ub;
-    return sh.ring[(q - h) & (kRing - 1)];
-  };
-  // make the ring cover fresh indices [f(q), f(q) + need)
-  auto ensure = [&](int64_t q, int need) {
-    for (;;) {
-      const int64_t f = q - h;
-      if (f + need <= sh.wbase + kRing) break;
-      __syncthreads();
-      const int64_t nb = sh.wbase + kHalf;  // new window start
-      st = add128(mul128(A, st), C);
-      const uint64_t o = pcg_output(st);
-      const int64_t fi = nb + kHalf + 2 * tid;  // fresh index of lo half
-      sh.ring[fi & (kRing - 1)] = (uint32_t)o;
-      sh.ring[(fi + 1) & (kRing - 1)] = (uint32_t)(o >> 32);
-      __syncthreads();
-      if (tid == 0) sh.wbase = nb;
-      __syncthreads();
-    }
-  };
-
   const int n = v.n;
   const int k_hi = max(2, n / 4);
+  const uint32_t rng_k = (uint32_t)(k_hi - 1);
   const int E = v.ctl->n_events;
-  const bool tail = (n > 10000);
-  for (int e = 0; e < E; ++e) {
-    int64_t q = sh.q;
-    ensure(q, kHalf);
+  __syncthreads();
+  for (;;) {
+    // refill so the ring starts at the chain position
+    const int64_t f = s_q - h;
+    if (f < 0 || f + 64 > s_wbase + kRing) {
+      const int64_t wb = f < 0 ? 0 : (f & ~(int64_t)1);
+      u128 st = pcg_advance(S0, inc, (uint64_t)(wb / 2 + 1 + tid));
+#pragma unroll
+      for (int r = 0; r < kOutPerThread; ++r) {
+        const uint64_t o = pcg_output(st);
+        const int idx = 2 * (tid + kWalk * r);
+        ring[idx] = (uint32_t)o;
+        ring[idx + 1] = (uint32_t)(o >> 32);
+        st = add128(mul128(A, st), C);
+      }
+      __syncthreads();
+      if (tid == 0) s_wbase = wb;
+      __syncthreads();
+    }
     if (tid == 0) {
-      // integers(1, k_hi + 1): Lemire with rng = k_hi - 1 (>= 1)
-      const uint32_t rng = (uint32_t)(k_hi - 1);
-      uint32_t u;
-      do {
-        u = get(q);
-        ++q;
-      } while (lemire_rejects(u, rng));
-      const int kraw = (int)(((uint64_t)u * (rng + 1u)) >> 32) + 1;
-      const int k = min(kraw, n / 2);
-      sh.k = k;
-      sh.q = q;
-      v.ev_k[e] = k;
-      v.ev_cursor[e] = (uint64_t)q;
+      int64_t q = s_q;
+      int e = s_e;
+      const int64_t wb = s_wbase;
+      while (e < E) {
+        if (q - h + 64 > wb + kRing) break;  // k-draw (+redraws) in ring
+        uint32_t u;
+        do {
+          u = q < h ? ub : ring[q - h - wb];
+          ++q;
+        } while (lemire_rejects(u, rng_k));
+        const int kraw = (int)(((uint64_t)u * (rng_k + 1u)) >> 32) + 1;
+        const int k = min(kraw, n / 2);
+        v.ev_k[e] = k;
+        v.ev_cursor[e] = (uint64_t)q;
+        if (k >= 1) q += sample_draws(n, k);
+        ++e;
+        if (q - h + 64 > wb + kRing) break;
+      }
+      s_q = q;
+      s_e = e;
     }
     __syncthreads();
-    const int k = sh.k;
-    q = sh.q;
-    if (k < 1) continue;
-    const int size = 2 * k;
-    int F, jstart, D;
-    const bool use_tail = tail && size > n / 50;
-    if (use_tail) {
-      jstart = max(n - size, 1);  // bounds n-1 .. jstart, descending
-      F = n - jstart;
-      D = F;
-    } else {
-      jstart = max(n - size, 1);  // Floyd bounds jstart .. n-1 (j=0: no draw)
-      F = n - jstart;
-      D = F + size - 1;
-    }
-    int d0 = 0;
-    while (d0 < D) {
-      ensure(q, kWalk);
-      const int cnt = min(kWalk, D - d0);
-      if (tid == 0) sh.first = cnt;
-      __syncthreads();
-      if (tid < cnt) {
-        const int d = d0 + tid;
-        uint32_t rng;
-        if (use_tail)
-          rng = (uint32_t)(n - 1 - d);
-        else
-          rng = d < F ? (uint32_t)(jstart + d) : (uint32_t)(size - 1 - (d - F));
-        if (lemire_rejects(get(q + tid), rng)) atomicMin(&sh.first, tid);
-      }
-      __syncthreads();
-      const int first = sh.first;
-      if (first == cnt) {
-        q += cnt;
-        d0 += cnt;
-      } else {
-        q += first + 1;
-        d0 += first;
-      }
-      __syncthreads();
-    }
-    if (tid == 0) sh.q = q;
-    __syncthreads();
+    if (s_e >= E) break;
   }
-  if (tid == 0) {
+  if (tid == 0) v.ctl->mut_q = (uint64_t)s_q;
+}
+
+// Numpy's choice(n, 2k, replace=False) from stream position `cur`: writes
+// the 2k sampled positions to idx; returns the number of u32 consumed.
+__device__ int64_t sample_event(const PcgState& start, uint64_t cur, int n,
+                                int k, uint16_t* idx, uint32_t* bits,
+                                uint16_t* arr) {
+  struct Counting {
     Pcg r;
-    r.seek_u32(g, (uint64_t)sh.q);
-    r.store(v.streams[1]);
-    v.ctl->mut_q = (uint64_t)sh.q;
+    int64_t q = 0;
+    __device__ uint32_t bounded(uint32_t rng) {
+      if (rng == 0) return 0;
+      const uint32_t rng_excl = rng + 1u;
+      ++q;
+      uint64_t m = (uint64_t)r.next32() * rng_excl;
+      uint32_t leftover = (uint32_t)m;
+      if (leftover < rng_excl) {
+        const uint32_t threshold = (0xFFFFFFFFu - rng) % rng_excl;
+        while (leftover < threshold) {
+          ++q;
+          m = (uint64_t)r.next32() * rng_excl;
+          leftover = (uint32_t)m;
+        }
+      }
+      return (uint32_t)(m >> 32);
+    }
+  } c;
+  c.r.seek_u32(start, cur);
+  const int size = 2 * k;
+  if (n > 10000 && size > n / 50) {
+    const int first = max(n - size, 1);
+    for (int i = n - 1; i >= first; --i) {
+      uint32_t j = c.bounded((uint32_t)i);
+      uint16_t t = arr[i];
+      arr[i] = arr[j];
+      arr[j] = t;
+    }
+    for (int t = 0; t < size; ++t) idx[t] = arr[n - size + t];
+  } else {
+    for (int t = 0; t < size; ++t) {
+      const uint32_t j = (uint32_t)(n - size + t);
+      uint32_t val = c.bounded(j);
+      if (bits[val >> 5] & (1u << (val & 31))) val = j;
+      bits[val >> 5] |= 1u << (val & 31);
+      idx[t] = (uint16_t)val;
+    }
+    for (int i = size - 1; i >= 1; --i) {
+      uint32_t j = c.bounded((uint32_t)i);
+      uint16_t t = idx[i];
+      idx[i] = idx[j];
+      idx[j] = t;
+    }
+  }
+  return c.q;
+}
+
+__device__ void clear_scratch(int n, bool tail, uint32_t* bits,
+                              uint16_t* arr) {
+  if (tail) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) arr[i] = (uint16_t)i;
+  } else {
+    for (int i = threadIdx.x; i < (n + 31) / 32; i += blockDim.x) bits[i] = 0;
   }
 }
 
-__global__ void __launch_bounds__(128) k_mut_apply(SwarmView v) {
+__global__ void __launch_bounds__(128) k_mut_sample(SwarmView v) {
+  if (!v.ctl->mutating || v.ctl->done) return;
+  const int e = blockIdx.x;
+  if (e >= v.ctl->n_events) return;
+  const int n = v.n, k = v.ev_k[e];
+  if (k < 1) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* bits = (uint32_t*)smem;
+  uint16_t* arr = (uint16_t*)smem;
+  const bool tail = (n > 10000) && 2 * k > n / 50;
+  clear_scratch(n, tail, bits, arr);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint16_t* idx = v.ev_idx + (size_t)e * v.np;
+    const int64_t used =
+        sample_event(*v.mut_start, v.ev_cursor[e], n, k, idx, bits, arr);
+    if (used != sample_draws(n, k)) atomicMin(&v.ctl->mut_bad, e);
+  }
+}
+
+// Rare path + stream bookkeeping: exact sequential re-walk from the first
+// event whose sample needed a Lemire redraw.
+__global__ void __launch_bounds__(32) k_mut_fix(SwarmView v) {
+  if (!v.ctl->mutating || v.ctl->done) return;
+  if (threadIdx.x != 0) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* bits = (uint32_t*)smem;
+  uint16_t* arr = (uint16_t*)smem;
+  const int n = v.n;
+  const int E = v.ctl->n_events;
+  const int bad = v.ctl->mut_bad;
+  uint64_t q = v.ctl->mut_q;
+  if (bad < E) {
+    const int k_hi = max(2, n / 4);
+    const uint32_t rng_k = (uint32_t)(k_hi - 1);
+    q = 0;
+    if (bad > 0) {
+      // the previous event was verified, so its draws ended where the
+      // speculative walk assumed
+      const int kp = v.ev_k[bad - 1];
+      q = v.ev_cursor[bad - 1] + (kp >= 1 ? sample_draws(n, kp) : 0);
+    }
+    for (int e = bad; e < E; ++e) {
+      Pcg r;
+      r.seek_u32(*v.mut_start, q);
+      uint32_t u;
+      do {
+        u = r.next32();
+        ++q;
+      } while (lemire_rejects(u, rng_k));
+      const int kraw = (int)(((uint64_t)u * (rng_k + 1u)) >> 32) + 1;
+      const int k = min(kraw, n / 2);
+      v.ev_k[e] = k;
+      v.ev_cursor[e] = q;
+      if (k < 1) continue;
+      const bool tail = (n > 10000) && 2 * k > n / 50;
+      if (tail) {
+        for (int i = 0; i < n; ++i) arr[i] = (uint16_t)i;
+      } else {
+        for (int i = 0; i < (n + 31) / 32; ++i) bits[i] = 0;
+      }
+      q += sample_event(*v.mut_start, q, n, k, v.ev_idx + (size_t)e * v.np,
+                        bits, arr);
+    }
+  }
+  Pcg r;
+  r.seek_u32(*v.mut_start, q);
+  r.store(v.streams[1]);
+  v.ctl->mut_q = q;
+}
+
+__global__ void __launch_bounds__(128) k_mut_swap(SwarmView v) {
   if (!v.ctl->mutating || v.ctl->done) return;
   const int e = blockIdx.x;
   if (e >= v.ctl->n_events) return;
   extern __shared__ __align__(16) unsigned char smem[];
+  double* sd = (double*)smem;
   const int n = v.n, np = v.np, tid = threadIdx.x;
   const int p = v.ev_slot[e];
   const int k = v.ev_k[e];
   if (k < 1) return;
-  const int size = 2 * k;
-  uint16_t* idx = (uint16_t*)smem;                       // size (<= n)
-  double* sd = (double*)(smem + round_up(2 * (int64_t)np, 16));
-  uint32_t* bits = (uint32_t*)(sd + np);                 // n bits, or
-  uint16_t* arr = (uint16_t*)bits;                       // tail: arange(n)
-  const bool use_tail = (n > 10000) && size > n / 50;
-  if (use_tail) {
-    for (int i = tid; i < n; i += blockDim.x) arr[i] = (uint16_t)i;
-  } else {
-    for (int i = tid; i < (n + 31) / 32; i += blockDim.x) bits[i] = 0;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    Pcg r;
-    r.seek_u32(*v.mut_start, v.ev_cursor[e]);
-    if (use_tail) {
-      const int first = max(n - size, 1);
-      for (int i = n - 1; i >= first; --i) {
-        uint32_t j = r.bounded((uint32_t)i);
-        uint16_t t = arr[i];
-        arr[i] = arr[j];
-        arr[j] = t;
-      }
-      for (int t = 0; t < size; ++t) idx[t] = arr[n - size + t];
-    } else {
-      for (int t = 0; t < size; ++t) {
-        const uint32_t j = (uint32_t)(n - size + t);
-        uint32_t val = r.bounded(j);
-        if (bits[val >> 5] & (1u << (val & 31))) val = j;
-        bits[val >> 5] |= 1u << (val & 31);
-        idx[t] = (uint16_t)val;
-      }
-      for (int i = size - 1; i >= 1; --i) {
-        uint32_t j = r.bounded((uint32_t)i);
-        uint16_t t = idx[i];
-        idx[i] = idx[j];
-        idx[j] = t;
-      }
-    }
-  }
-  __syncthreads();
+  const uint16_t* idx = v.ev_idx + (size_t)e * np;
   uint16_t* body = v.x + (size_t)p * np;
   // the k position pairs are disjoint (sampled without replacement)
   for (int t = tid; t < k; t += blockDim.x) {
@@ -448,14 +506,27 @@ cudaError_t launch_mutation(const SwarmView& v, cudaStream_t s) {
   k_mut_dedupe<<<(P + 255) / 256, 256, 0, s>>>(v, canon);
   k_mut_lists<<<1, 1024, 0, s>>>(v);
   k_mut_copy<<<P, 128, 0, s>>>(v);
-  k_mut_walk<<<1, kWalk, 0, s>>>(v);
-  size_t smem = round_up(2 * (int64_t)v.np, 16) + (size_t)8 * v.np +
-                (v.n > 10000 ? (size_t)2 * v.np : round_up((v.n + 31) / 32 * 4, 16));
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_mut_apply,
+  const size_t ring = (size_t)kRing * 4;
+  cudaFuncSetAttribute(k_mut_walk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)ring);
+  k_mut_walk<<<1, kWalk, ring, s>>>(v);
+  const size_t scratch =
+      std::max<size_t>(round_up((v.n + 31) / 32 * 4, 16), 2 * (size_t)v.np);
+  if (scratch > 48 * 1024) {
+    cudaFuncSetAttribute(k_mut_sample,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-  k_mut_apply<<<P, 128, smem, s>>>(v);
+                         (int)scratch);
+    cudaFuncSetAttribute(k_mut_fix,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)scratch);
+  }
+  k_mut_sample<<<P, 128, scratch, s>>>(v);
+  k_mut_fix<<<1, 32, scratch, s>>>(v);
+  const size_t sd = (size_t)8 * v.np;
+  if (sd > 48 * 1024)
+    cudaFuncSetAttribute(k_mut_swap,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sd);
+  k_mut_swap<<<P, 128, sd, s>>>(v);
   return cudaGetLastError();
 }
 

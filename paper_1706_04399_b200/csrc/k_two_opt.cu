@@ -19,13 +19,15 @@
 // argmin tie-break bit for bit.
 #include <float.h>
 
+#include <algorithm>
+
 #include "dpso_internal.cuh"
 
 namespace dpso {
 
 namespace {
 
-constexpr int kWarps = 4;  // warps (tasks) per CTA
+constexpr int kMaxWarps = 4;  // warps (tasks) per CTA, upper bound
 constexpr int kBufs = 3;   // row ring depth per warp
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -97,22 +99,26 @@ __device__ __forceinline__ bool res_less(double d1, int i1, int j1, double d2,
 
 // NPL > 0: lane-owned columns in registers (n <= 32*NPL).
 // NPL == 0: generic path, columns streamed from global/L1 per row.
-template <int NPL>
-__global__ void __launch_bounds__(kWarps * 32)
+// STAGE: cost rows staged in shared memory by bulk copies (false = read the
+// rows straight from global/L2, for n too large for a 3-row ring).
+constexpr int kGroup = 4;  // column blocks (of 32) per uniform skip test
+
+template <int NPL, bool STAGE>
+__global__ void __launch_bounds__(kMaxWarps * 32)
     k_two_opt_scan(ScanArgs a) {
   if (a.ctl && (a.ctl->done || a.ctl->improved)) return;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bars[kWarps][kBufs];
+  __shared__ __align__(8) uint64_t bars[kMaxWarps][kBufs];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int task = blockIdx.x * kWarps + warp;
+  const int task = blockIdx.x * (blockDim.x >> 5) + warp;
   const int p = task / a.chunks, c = task % a.chunks;
   if (p >= a.count) return;
   const int n = a.n;
   const int r0 = a.chunk_row[c], r1 = a.chunk_row[c + 1];
   TwoOptRes* out = a.res + (size_t)p * a.chunks + c;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
   if (r0 >= r1) {
-    if (lane == 0) *out = {__longlong_as_double(0x7ff0000000000000ll),
-                           0x7fffffff, 0x7fffffff};
+    if (lane == 0) *out = {kInf, 0x7fffffff, 0x7fffffff};
     return;
   }
   const uint16_t* tour = a.tours + (size_t)p * a.np;
@@ -120,11 +126,12 @@ __global__ void __launch_bounds__(kWarps * 32)
   unsigned char* wbase = smem + (size_t)warp * kBufs * a.buf_stride;
   uint64_t* wb = bars[warp];
 
-  uint32_t pk[NPL > 0 ? NPL : 1];
-  double dj[NPL > 0 ? NPL : 1];
+  constexpr int NR = NPL > 0 ? NPL : 1;
+  uint32_t pk[NR];
+  double dj[NR];
   if (NPL > 0) {
 #pragma unroll
-    for (int m = 0; m < (NPL > 0 ? NPL : 1); ++m) {
+    for (int m = 0; m < NR; ++m) {
       int j = lane + 32 * m;
       if (j < n) {
         uint32_t aj = tour[j], sj = tour[j + 1 == n ? 0 : j + 1];
@@ -138,7 +145,7 @@ __global__ void __launch_bounds__(kWarps * 32)
   }
 
   const int nrows = r1 - r0 + 1;  // cost rows a_r0 .. a_r1
-  if (lane == 0) {
+  if (STAGE && lane == 0) {
     for (int b = 0; b < kBufs; ++b) mbar_init(&wb[b], 1);
     fence_barrier_init();
     for (int q = 0; q < 2 && q < nrows; ++q) {
@@ -150,38 +157,58 @@ __global__ void __launch_bounds__(kWarps * 32)
   }
   __syncwarp();
 
-  double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  double best = kInf;
   int bi = 0x7fffffff, bj = 0x7fffffff;
 
   for (int i = r0; i < r1; ++i) {
     const int q = i - r0;
-    if (lane == 0 && q + 2 < nrows) {
-      const int b = (q + 2) % kBufs;
-      const int node = tour[r0 + q + 2];
-      fence_proxy_async();
-      mbar_expect_tx(&wb[b], a.row_bytes);
-      bulk_g2s(wbase + (size_t)b * a.buf_stride,
-               a.cost + (size_t)node * a.ld, a.row_bytes, &wb[b]);
+    const double* A;
+    const double* B;
+    if (STAGE) {
+      if (lane == 0 && q + 2 < nrows) {
+        const int b = (q + 2) % kBufs;
+        const int node = tour[r0 + q + 2];
+        fence_proxy_async();
+        mbar_expect_tx(&wb[b], a.row_bytes);
+        bulk_g2s(wbase + (size_t)b * a.buf_stride,
+                 a.cost + (size_t)node * a.ld, a.row_bytes, &wb[b]);
+      }
+      const int ba = q % kBufs, bb = (q + 1) % kBufs;
+      mbar_wait(&wb[ba], (uint32_t)((q / kBufs) & 1));
+      mbar_wait(&wb[bb], (uint32_t)(((q + 1) / kBufs) & 1));
+      A = (const double*)(wbase + (size_t)ba * a.buf_stride);
+      B = (const double*)(wbase + (size_t)bb * a.buf_stride);
+    } else {
+      A = a.cost + (size_t)tour[i] * a.ld;
+      B = a.cost + (size_t)tour[i + 1] * a.ld;
     }
-    const int ba = q % kBufs, bb = (q + 1) % kBufs;
-    mbar_wait(&wb[ba], (uint32_t)((q / kBufs) & 1));
-    mbar_wait(&wb[bb], (uint32_t)(((q + 1) / kBufs) & 1));
-    const double* A = (const double*)(wbase + (size_t)ba * a.buf_stride);
-    const double* B = (const double*)(wbase + (size_t)bb * a.buf_stride);
     const double di = dg[i];
+    // row-local first minimum over this lane's columns (ascending j)
+    double rbest = kInf;
+    int rj = 0x7fffffff;
     if (NPL > 0) {
 #pragma unroll
-      for (int m = 0; m < (NPL > 0 ? NPL : 1); ++m) {
-        if (32 * m + 31 > i) {
-          const int j = lane + 32 * m;
-          if (j > i && j < n) {
-            double t = __dadd_rn(A[pk[m] & 0xFFFFu], B[pk[m] >> 16]);
-            t = __dsub_rn(t, di);
-            t = __dsub_rn(t, dj[m]);
-            if (t < best) {
-              best = t;
-              bi = i;
-              bj = j;
+      for (int m0 = 0; m0 < NR; m0 += kGroup) {
+        if (32 * (m0 + kGroup) - 1 > i) {  // warp-uniform: group not dead
+          double av[kGroup], bv[kGroup];
+#pragma unroll
+          for (int g = 0; g < kGroup; ++g) {
+            if (m0 + g < NR) {
+              av[g] = A[pk[m0 + g] & 0xFFFFu];
+              bv[g] = B[pk[m0 + g] >> 16];
+            }
+          }
+#pragma unroll
+          for (int g = 0; g < kGroup; ++g) {
+            if (m0 + g < NR) {
+              const int j = lane + 32 * (m0 + g);
+              double t = __dadd_rn(av[g], bv[g]);
+              t = __dsub_rn(t, di);
+              t = __dsub_rn(t, dj[m0 + g]);
+              t = (j > i && j < n) ? t : kInf;
+              const bool lt = t < rbest;
+              rbest = lt ? t : rbest;
+              rj = lt ? j : rj;
             }
           }
         }
@@ -192,12 +219,15 @@ __global__ void __launch_bounds__(kWarps * 32)
         double t = __dadd_rn(A[aj], B[sj]);
         t = __dsub_rn(t, di);
         t = __dsub_rn(t, dg[j]);
-        if (t < best) {
-          best = t;
-          bi = i;
-          bj = j;
-        }
+        const bool lt = t < rbest;
+        rbest = lt ? t : rbest;
+        rj = lt ? j : rj;
       }
+    }
+    if (rbest < best) {
+      best = rbest;
+      bi = i;
+      bj = rj;
     }
     __syncwarp();
   }
@@ -286,19 +316,27 @@ __global__ void __launch_bounds__(128) k_two_opt_apply(ApplyArgs a) {
   }
 }
 
-template <int NPL>
-cudaError_t launch_scan_t(const ScanArgs& a, int blocks, size_t smem,
-                          cudaStream_t s) {
-  auto k = k_two_opt_scan<NPL>;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         227 * 1024);
-    configured = true;
+template <int NPL, bool STAGE>
+cudaError_t launch_scan_t(const ScanArgs& a, int warps, int blocks,
+                          size_t smem, cudaStream_t s) {
+  auto k = k_two_opt_scan<NPL, STAGE>;
+  static size_t configured = 48 * 1024;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(
+        k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
   }
-  k<<<blocks, kWarps * 32, smem, s>>>(a);
+  k<<<blocks, warps * 32, smem, s>>>(a);
   return cudaGetLastError();
 }
+
+// bytes of the per-warp row ring
+size_t ring_bytes(int n) {
+  return (size_t)kBufs * round_up((int64_t)round_up(n, 2) * 8, 128);
+}
+
+constexpr size_t kSmemBudget = 220 * 1024;
 
 }  // namespace
 
@@ -306,8 +344,8 @@ int two_opt_pick_chunks(int32_t n, int32_t P) {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  size_t per_warp = (size_t)kBufs * round_up((int64_t)round_up(n, 2) * 8, 128);
-  int warps_per_sm = (int)(200 * 1024 / per_warp);
+  size_t per_warp = ring_bytes(n);
+  int warps_per_sm = (int)(kSmemBudget / per_warp);
   if (warps_per_sm < 1) warps_per_sm = 1;
   if (warps_per_sm > 32) warps_per_sm = 32;
   int64_t slots = (int64_t)sms * warps_per_sm;
@@ -361,27 +399,35 @@ cudaError_t launch_two_opt_core(const double* cost, int64_t ld, int32_t n,
   a.ctl = ctl;
   a.row_bytes = (uint32_t)(round_up(n, 2) * 8);
   a.buf_stride = (uint32_t)round_up(a.row_bytes, 128);
-  const size_t smem = (size_t)kWarps * kBufs * a.buf_stride;
+  const size_t per_warp = ring_bytes(n);
+  const bool stage = per_warp <= kSmemBudget;
+  int warps = stage ? (int)std::min<size_t>(kMaxWarps, kSmemBudget / per_warp)
+                    : kMaxWarps;
+  const size_t smem = stage ? (size_t)warps * per_warp : 0;
   const int64_t tasks = (int64_t)count * chunks;
-  const int blocks = (int)((tasks + kWarps - 1) / kWarps);
+  const int blocks = (int)((tasks + warps - 1) / warps);
   cudaError_t e = cudaSuccess;
   if ((parts & 1) && n >= 4 && blocks > 0) {
+#define SCAN(NPL)                                                    \
+  (stage ? launch_scan_t<NPL, true>(a, warps, blocks, smem, s)       \
+         : launch_scan_t<NPL, false>(a, warps, blocks, smem, s))
     if (n <= 32)
-      e = launch_scan_t<1>(a, blocks, smem, s);
+      e = SCAN(1);
     else if (n <= 64)
-      e = launch_scan_t<2>(a, blocks, smem, s);
+      e = SCAN(2);
     else if (n <= 128)
-      e = launch_scan_t<4>(a, blocks, smem, s);
+      e = SCAN(4);
     else if (n <= 256)
-      e = launch_scan_t<8>(a, blocks, smem, s);
+      e = SCAN(8);
     else if (n <= 512)
-      e = launch_scan_t<16>(a, blocks, smem, s);
+      e = SCAN(16);
     else if (n <= 1024)
-      e = launch_scan_t<32>(a, blocks, smem, s);
+      e = SCAN(32);
     else if (n <= 2048)
-      e = launch_scan_t<64>(a, blocks, smem, s);
+      e = SCAN(64);
     else
-      e = launch_scan_t<0>(a, blocks, smem, s);
+      e = SCAN(0);
+#undef SCAN
     if (e != cudaSuccess) return e;
   }
   ApplyArgs b;
