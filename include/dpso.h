@@ -79,6 +79,12 @@ int dpso_set_streams(dpso_ctx* ctx, const uint64_t* host_states);
  * seed tour, already validated by the caller); n_seed as in solver.py:173. */
 int dpso_init(dpso_ctx* ctx, const int32_t* host_seed_body, int32_t n_seed);
 
+/* 2-opt scan mode chosen by dpso_set_cost from the matrix: 0 = fp64
+ * rows, 1 = exact fp32 (integer |C| < 2^22), 2 = fp32 filter + exact fp64
+ * re-evaluation of candidates (see k_two_opt.cu).  The environment variable
+ * DPSO_SCAN_MODE overrides it (testing). */
+int dpso_scan_mode(dpso_ctx* ctx);
+
 /* Run generations until max_generations or the stall break.  Blocks the
  * calling thread; returns the number of generations run. */
 int dpso_run(dpso_ctx* ctx, int32_t* gens_run);

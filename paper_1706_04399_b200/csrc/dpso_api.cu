@@ -7,6 +7,7 @@
 // period, 2-opt trigger, stall break) are flags checked at kernel entry.  The
 // host polls `done` once per batch of generations.
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
@@ -41,7 +42,8 @@ struct Layout {
       off_vel, off_vel_len, off_fit, off_pfit, off_dcache, off_gbest,
       off_conv, off_tores, off_chunk_row, off_rank, off_hash, off_flag,
       off_sidx, off_order, off_surv, off_keep, off_ev_slot, off_ev_k,
-      off_ev_cursor, off_ev_idx, off_init_cursor, off_seed, total;
+      off_ev_cursor, off_ev_idx, off_init_cursor, off_seed, off_cost32,
+      off_stats, total;
   int64_t vel_cap;
   int chunks;
 };
@@ -93,6 +95,8 @@ Layout make_layout(const dpso_params* prm, int n) {
   L.off_ev_idx = take(2 * P * np);
   L.off_init_cursor = take(8 * P);
   L.off_seed = take(2 * np);
+  L.off_cost32 = take(prm->use_edge_exchange ? 4 * (int64_t)n * np : 0);
+  L.off_stats = take(sizeof(CostStats));
   L.total = o;
   return L;
 }
@@ -277,6 +281,27 @@ int dpso_set_cost(dpso_ctx* c, const double* dev_cost, int64_t ld) {
                 "alignment");
   c->v.cost = dev_cost;
   c->v.ld = ld;
+  TwoOptPlan& pl = c->v.plan;
+  pl.cost = dev_cost;
+  pl.ld = ld;
+  pl.cost32 = nullptr;
+  pl.ld32 = c->v.np;
+  pl.mode = kScanFP64;
+  pl.thr = 0.f;
+  if (c->prm.use_edge_exchange) {
+    float* c32 = (float*)(c->ws + c->L.off_cost32);
+    CostStats* st = (CostStats*)(c->ws + c->L.off_stats);
+    int rc = sync_in(c);
+    if (rc) return rc;
+    CK(launch_cost_prep(dev_cost, ld, c->n, c32, c->v.np, st, c->stream));
+    CostStats h;
+    CK(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    pl.cost32 = c32;
+    pl.mode = two_opt_mode(h, c->n, &pl.thr);
+    if (getenv("DPSO_SCAN_MODE")) pl.mode = atoi(getenv("DPSO_SCAN_MODE"));
+    if (pl.mode == kScanFilter32 && pl.thr == 0.f) pl.mode = kScanFP64;
+  }
   c->have_cost = true;
   if (c->graph) {
     cudaGraphExecDestroy(c->graph);
@@ -284,6 +309,8 @@ int dpso_set_cost(dpso_ctx* c, const double* dev_cost, int64_t ld) {
   }
   return DPSO_OK;
 }
+
+int dpso_scan_mode(dpso_ctx* c) { return c ? c->v.plan.mode : -1; }
 
 int dpso_set_streams(dpso_ctx* c, const uint64_t* host_states) {
   if (!c || !host_states) return fail(DPSO_EINVAL, "null argument");
@@ -641,22 +668,42 @@ int dpso_best_exchange_batch(const double* dev_cost, int64_t ld, int32_t n,
   const int64_t cnt = std::max(count, 1);
   size_t bytes = round_up(2 * np * cnt, 256) + round_up(8 * np * cnt, 256) +
                  round_up(sizeof(TwoOptRes) * chunks * cnt, 256) +
-                 round_up(4 * (chunks + 1), 256) + round_up(8 * cnt, 256);
+                 round_up(4 * (chunks + 1), 256) + round_up(8 * cnt, 256) +
+                 round_up(4 * (int64_t)n * np, 256) + 256;
   unsigned char* tmp = nullptr;
   CK(cudaMallocAsync(&tmp, bytes, s));
-  uint16_t* t16 = (uint16_t*)tmp;
-  double* dc = (double*)(tmp + round_up(2 * np * cnt, 256));
-  TwoOptRes* res = (TwoOptRes*)((unsigned char*)dc + round_up(8 * np * cnt, 256));
-  int32_t* crow = (int32_t*)((unsigned char*)res +
-                             round_up(sizeof(TwoOptRes) * chunks * cnt, 256));
+  size_t o = 0;
+  auto take = [&](size_t b) {
+    unsigned char* p = tmp + o;
+    o += round_up(b, 256);
+    return p;
+  };
+  uint16_t* t16 = (uint16_t*)take(2 * np * cnt);
+  double* dc = (double*)take(8 * np * cnt);
+  TwoOptRes* res = (TwoOptRes*)take(sizeof(TwoOptRes) * chunks * cnt);
+  int32_t* crow = (int32_t*)take(4 * (chunks + 1));
+  double* fsum = (double*)take(8 * cnt);
+  float* c32 = (float*)take(4 * (int64_t)n * np);
+  CostStats* st = (CostStats*)take(sizeof(CostStats));
   CK(cudaMemcpyAsync(crow, rows.data(), 4 * (chunks + 1),
                      cudaMemcpyHostToDevice, s));
   int rc = to_u16_tours(dev_tours, n, count, t16, np, s);
   if (rc) return rc;
-  double* fsum = (double*)((unsigned char*)crow + round_up(4 * (chunks + 1), 256));
   CK(launch_tour_cost_rows(dev_cost, ld, n, t16, np, count, fsum, dc, s));
-  CK(launch_two_opt_batch(dev_cost, ld, n, (int32_t)np, t16, dc, count, res,
-                          chunks, crow, dev_delta, s));
+  TwoOptPlan pl;
+  pl.cost = dev_cost;
+  pl.ld = ld;
+  pl.cost32 = c32;
+  pl.ld32 = np;
+  CK(launch_cost_prep(dev_cost, ld, n, c32, np, st, s));
+  CostStats h;
+  CK(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  pl.mode = two_opt_mode(h, n, &pl.thr);
+  if (getenv("DPSO_SCAN_MODE")) pl.mode = atoi(getenv("DPSO_SCAN_MODE"));
+  if (pl.mode == kScanFilter32 && pl.thr == 0.f) pl.mode = kScanFP64;
+  CK(launch_two_opt_batch(pl, n, (int32_t)np, t16, dc, count, res, chunks,
+                          crow, dev_delta, s));
   if (count > 0) k_u16_to_i32<<<count, 256, 0, s>>>(t16, n, count, dev_tours, np);
   CK(cudaGetLastError());
   CK(cudaFreeAsync(tmp, s));
@@ -695,22 +742,11 @@ int dpso_nn_two_opt(const double* dev_cost, int64_t ld, int32_t n,
   CK(cudaMallocAsync(&d, 4 * n, s));
   CK(cudaMallocAsync(&dd, 8, s));
   CK(launch_nn(dev_cost, ld, n, 0, d, s));
-  std::vector<int32_t> body(n);
-  CK(cudaMemcpyAsync(body.data(), d, 4 * n, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  std::vector<double> row(n);
+  // total = sum(rows[a][b] for a, b in zip(body, body[1:] + body[:1]))
   double total = 0.0;
-  // sum(rows[a][b] for a, b in zip(body, body[1:] + body[:1])): Python sum
-  // starts from int 0 and adds in order
-  {
-    std::vector<double> edges(n);
-    for (int i = 0; i < n; ++i) {
-      int a = body[i], b = body[(i + 1) % n];
-      CK(cudaMemcpy(&edges[i], dev_cost + (size_t)a * ld + b, 8,
-                    cudaMemcpyDeviceToHost));
-    }
-    for (int i = 0; i < n; ++i) total += edges[i];
-  }
+  CK(launch_pysum_tour(dev_cost, ld, n, d, dd, s));
+  CK(cudaMemcpyAsync(&total, dd, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
   for (;;) {
     int rc = dpso_best_exchange_batch(dev_cost, ld, n, d, 1, dd, s);
     if (rc) return rc;

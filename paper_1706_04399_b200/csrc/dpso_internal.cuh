@@ -49,6 +49,26 @@ struct DevCtl {
   uint64_t mut_q;     // u32 draws consumed by the current mutation call
 };
 
+// 2-opt scan modes (k_two_opt.cu)
+constexpr int kScanFP64 = 0;
+constexpr int kScanExact32 = 1;
+constexpr int kScanFilter32 = 2;
+
+struct CostStats {
+  unsigned long long maxabs_bits;  // bits of max |C| (non-negative double)
+  int nonintegral;
+  int pad_;
+};
+
+struct TwoOptPlan {
+  const double* cost;
+  int64_t ld;
+  const float* cost32;  // fp32 copy (EXACT32 / FILTER32), may be null
+  int64_t ld32;
+  int mode;
+  float thr;  // FILTER32 candidate window (2 eps)
+};
+
 struct TwoOptRes {
   double delta;
   int32_t i, j;
@@ -78,6 +98,7 @@ struct SwarmView {
   double* dcache;
   uint16_t* gbest;
   double* conv;
+  TwoOptPlan plan;     // cost matrix views + 2-opt scan mode
   TwoOptRes* tores;
   int32_t chunks;      // 2-opt row chunks per particle
   int32_t* chunk_row;  // chunks + 1 row boundaries
@@ -112,14 +133,20 @@ cudaError_t launch_tour_cost_rows(const double* cost, int64_t ld, int32_t n,
                                   const uint16_t* tours, int64_t stride,
                                   int32_t count, double* out, double* dcache,
                                   cudaStream_t s);
-cudaError_t launch_two_opt_batch(const double* cost, int64_t ld, int32_t n,
-                                 int32_t np, uint16_t* tours,
-                                 const double* dcache, int32_t count,
-                                 TwoOptRes* res, int32_t chunks,
+cudaError_t launch_two_opt_batch(const TwoOptPlan& pl, int32_t n, int32_t np,
+                                 uint16_t* tours, const double* dcache,
+                                 int32_t count, TwoOptRes* res, int32_t chunks,
                                  const int32_t* chunk_row, double* delta_out,
                                  cudaStream_t s);
+cudaError_t launch_cost_prep(const double* cost, int64_t ld, int32_t n,
+                             float* cost32, int64_t ld32, CostStats* st,
+                             cudaStream_t s);
+int two_opt_mode(const CostStats& st, int n, float* thr);
 cudaError_t launch_nn(const double* cost, int64_t ld, int32_t n, int32_t start,
                       int32_t* out, cudaStream_t s);
+cudaError_t launch_pysum_tour(const double* cost, int64_t ld, int32_t n,
+                              const int32_t* body, double* out,
+                              cudaStream_t s);
 int two_opt_chunk_rows(int32_t n, int32_t chunks, int32_t* rows);
 int two_opt_pick_chunks(int32_t n, int32_t P);
 

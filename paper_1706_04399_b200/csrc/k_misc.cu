@@ -418,7 +418,40 @@ __global__ void __launch_bounds__(1024) k_nn(const double* cost, int64_t ld,
   }
 }
 
+// Python's builtin sum() over the closed tour's edges, as CPython 3.12+
+// evaluates it for floats (bltinmodule.c builtin_sum_impl: the int start 0 is
+// added to the first item, then Neumaier-compensated accumulation, and the
+// compensation is added at the end when it is non-zero and finite).  This is
+// what baselines.py:117 computes.
+__global__ void k_pysum_tour(const double* cost, int64_t ld, int n,
+                             const int32_t* body, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double f = 0.0, c = 0.0;
+  for (int k = 0; k < n; ++k) {
+    const double x = cost[(size_t)body[k] * ld + body[k + 1 == n ? 0 : k + 1]];
+    if (k == 0) {
+      f = x;  // int 0 + float x
+      continue;
+    }
+    const double t = __dadd_rn(f, x);
+    if (fabs(f) >= fabs(x))
+      c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x));
+    else
+      c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), f));
+    f = t;
+  }
+  if (c != 0.0 && isfinite(c)) f = __dadd_rn(f, c);
+  *out = f;
+}
+
 }  // namespace
+
+cudaError_t launch_pysum_tour(const double* cost, int64_t ld, int32_t n,
+                              const int32_t* body, double* out,
+                              cudaStream_t s) {
+  k_pysum_tour<<<1, 32, 0, s>>>(cost, ld, n, body, out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_gen_begin(const SwarmView& v, cudaStream_t s) {
   k_gen_begin<<<1, 32, 0, s>>>(v);

@@ -4,20 +4,38 @@
 // s = roll(a, -1), d_i = C[a_i, s_i]; the move is the first (row-major)
 // argmin; it is applied when delta < -1e-12 and fitness += delta.
 //
-// Layout on the device: one warp owns a task = (particle, band of pair rows
-// [r0, r1)).  The cost rows a_r0 .. a_r1 are streamed in order from L2 into a
-// 3-deep per-warp ring in shared memory with cp.async.bulk (TMA bulk copy,
-// mbarrier completion), so each cost row is read from L2 once per task and
-// used twice: as the A row of pair-row i and the B row of pair-row i-1.
-// Lane l owns the columns j = l + 32m; a_j, s_j (packed u16 pair) and d_j
-// live in registers for the whole task.  Row i then costs two shared-memory
-// gathers A[a_j], B[s_j] and three fp64 adds per pair in the reference's
-// exact expression order (no FMA contraction possible for add/sub).  Each lane
-// keeps its first strict minimum in (i, j) order; a warp shuffle reduction
-// on (delta, i, j) gives the band's first-index argmin, and the apply kernel
-// merges bands in row order (earlier band wins ties), reproducing numpy's
-// argmin tie-break bit for bit.
+// Work decomposition: one warp owns a task = (particle, band of pair rows
+// [r0, r1)); bands are cut so every task has ~equal pair count and there are
+// ~4 tasks per resident warp slot.  The cost rows a_r0 .. a_r1 are streamed
+// in tour order from L2 into a 3-deep per-warp ring in shared memory by
+// cp.async.bulk (TMA bulk copy, mbarrier completion): each row is read once
+// per task and used twice (A row of pair-row i, B row of pair-row i-1).
+// Lane l owns columns j = l + 32m; a_j, s_j (packed u16) and d_j stay in
+// registers for the whole task; a row costs two shared-memory gathers per
+// pair.  Columns are processed in groups of 4 blocks of 32 with a
+// warp-uniform skip of dead groups (j <= i), predicated masking inside, so
+// gathers of a group are in flight together.
+//
+// Three scan modes, chosen once per cost matrix (k_cost_prep):
+//   EXACT32  integer matrices with |C| < 2^22 (scene matrices): every fp32
+//            delta equals the fp64 delta exactly, so the fp32 scan IS the
+//            reference computation (half the L2 bytes and gathers of fp64).
+//   FILTER32 everything else: fp32 deltas with a rigorous bound
+//            |delta32 - delta64| <= eps (eps = 2^-18 max|C| >= 4x the
+//            worst-case rounding), each lane keeps the pairs within 2 eps of
+//            its running fp32 minimum; at the end the warp's candidates within
+//            2 eps of the warp minimum are re-evaluated in fp64 (exact
+//            reference arithmetic).  The true argmin and all its fp64 ties are
+//            provably among the candidates.  The structural pairs (i, i+1)
+//            and (0, n-1) - arithmetic no-ops whose fp64 residue the
+//            reference can still pick - are evaluated exactly from d.  A
+//            candidate-list overflow re-scans that task in fp64 (FP64 mode).
+//   FP64     the reference expression on fp64 rows (fallback and for
+//            matrices fp32 cannot represent).
+// Each lane keeps its first strict minimum in (i, j) order; warp shuffles
+// reduce (delta, i, j); the apply kernel merges bands in row order.
 #include <float.h>
+#include <string.h>
 
 #include <algorithm>
 
@@ -28,7 +46,10 @@ namespace dpso {
 namespace {
 
 constexpr int kMaxWarps = 4;  // warps (tasks) per CTA, upper bound
-constexpr int kBufs = 3;   // row ring depth per warp
+constexpr int kBufs = 3;      // row ring depth per warp
+constexpr int kGroup = 4;     // column blocks (of 32) per uniform skip test
+constexpr int kCand = 4;      // fp32 candidates kept per lane (FILTER32)
+constexpr int kOverflowTag = -2;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -80,6 +101,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 struct ScanArgs {
   const double* cost;
   int64_t ld;
+  const float* cost32;
+  int64_t ld32;
   int32_t n, np, count, chunks;
   const uint16_t* tours;   // count x np
   const double* dcache;    // count x np
@@ -88,6 +111,8 @@ struct ScanArgs {
   const DevCtl* ctl;       // nullable: skip when done or improved
   uint32_t row_bytes;      // bytes streamed per cost row (multiple of 16)
   uint32_t buf_stride;     // bytes between ring buffers
+  float thr;               // FILTER32: 2 * eps
+  int only_flagged;        // FP64 fallback: only tasks tagged kOverflowTag
 };
 
 __device__ __forceinline__ bool res_less(double d1, int i1, int j1, double d2,
@@ -97,15 +122,67 @@ __device__ __forceinline__ bool res_less(double d1, int i1, int j1, double d2,
   return (i1 < i2) || (i1 == i2 && j1 < j2);
 }
 
-// NPL > 0: lane-owned columns in registers (n <= 32*NPL).
-// NPL == 0: generic path, columns streamed from global/L1 per row.
-// STAGE: cost rows staged in shared memory by bulk copies (false = read the
-// rows straight from global/L2, for n too large for a 3-row ring).
-constexpr int kGroup = 4;  // column blocks (of 32) per uniform skip test
+__device__ __forceinline__ void warp_argmin(double& best, int& bi, int& bj) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double d2 = __shfl_xor_sync(0xffffffffu, best, o);
+    int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+    int j2 = __shfl_xor_sync(0xffffffffu, bj, o);
+    if (res_less(d2, i2, j2, best, bi, bj)) {
+      best = d2;
+      bi = i2;
+      bj = j2;
+    }
+  }
+}
 
+// Row ring: lane 0 issues bulk copies; all lanes wait on the mbarriers.
+template <typename T>
+struct RowRing {
+  unsigned char* base;
+  uint64_t* bars;
+  uint32_t row_bytes, stride;
+  const T* mat;
+  int64_t ld;
+  const uint16_t* tour;
+  int r0, nrows;
+
+  __device__ void start() {
+    if ((threadIdx.x & 31) == 0) {
+      for (int b = 0; b < kBufs; ++b) mbar_init(&bars[b], 1);
+      fence_barrier_init();
+      for (int q = 0; q < 2 && q < nrows; ++q) issue(q);
+    }
+    __syncwarp();
+  }
+  __device__ void issue(int q) {
+    const int b = q % kBufs;
+    const int node = tour[r0 + q];
+    mbar_expect_tx(&bars[b], row_bytes);
+    bulk_g2s(base + (size_t)b * stride, mat + (size_t)node * ld, row_bytes,
+             &bars[b]);
+  }
+  // rows q (A) and q+1 (B) ready; row q+2 requested
+  __device__ void advance(int q, const T** A, const T** B) {
+    if ((threadIdx.x & 31) == 0 && q + 2 < nrows) {
+      fence_proxy_async();
+      issue(q + 2);
+    }
+    const int ba = q % kBufs, bb = (q + 1) % kBufs;
+    mbar_wait(&bars[ba], (uint32_t)((q / kBufs) & 1));
+    mbar_wait(&bars[bb], (uint32_t)(((q + 1) / kBufs) & 1));
+    *A = (const T*)(base + (size_t)ba * stride);
+    *B = (const T*)(base + (size_t)bb * stride);
+  }
+};
+
+// ---- FP64 scan (reference arithmetic on fp64 rows) -------------------------
+// NPL > 0: lane-owned columns in registers (n <= 32*NPL); NPL == 0: columns
+// read from global/L1 per row.  STAGE: rows in the smem ring (false = read
+// the rows straight from global/L2, for n too large for the ring).
 template <int NPL, bool STAGE>
 __global__ void __launch_bounds__(kMaxWarps * 32)
-    k_two_opt_scan(ScanArgs a) {
+    k_two_opt_scan64(ScanArgs a) {
   if (a.ctl && (a.ctl->done || a.ctl->improved)) return;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bars[kMaxWarps][kBufs];
@@ -116,6 +193,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
   const int n = a.n;
   const int r0 = a.chunk_row[c], r1 = a.chunk_row[c + 1];
   TwoOptRes* out = a.res + (size_t)p * a.chunks + c;
+  if (a.only_flagged && out->i != kOverflowTag) return;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
   if (r0 >= r1) {
     if (lane == 0) *out = {kInf, 0x7fffffff, 0x7fffffff};
@@ -123,8 +201,6 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
   }
   const uint16_t* tour = a.tours + (size_t)p * a.np;
   const double* dg = a.dcache + (size_t)p * a.np;
-  unsigned char* wbase = smem + (size_t)warp * kBufs * a.buf_stride;
-  uint64_t* wb = bars[warp];
 
   constexpr int NR = NPL > 0 ? NPL : 1;
   uint32_t pk[NR];
@@ -143,47 +219,23 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
       }
     }
   }
-
-  const int nrows = r1 - r0 + 1;  // cost rows a_r0 .. a_r1
-  if (STAGE && lane == 0) {
-    for (int b = 0; b < kBufs; ++b) mbar_init(&wb[b], 1);
-    fence_barrier_init();
-    for (int q = 0; q < 2 && q < nrows; ++q) {
-      int node = tour[r0 + q];
-      mbar_expect_tx(&wb[q], a.row_bytes);
-      bulk_g2s(wbase + (size_t)q * a.buf_stride,
-               a.cost + (size_t)node * a.ld, a.row_bytes, &wb[q]);
-    }
-  }
-  __syncwarp();
+  RowRing<double> ring{smem + (size_t)warp * kBufs * a.buf_stride,
+                       bars[warp], a.row_bytes, a.buf_stride, a.cost, a.ld,
+                       tour, r0, r1 - r0 + 1};
+  if (STAGE) ring.start();
 
   double best = kInf;
   int bi = 0x7fffffff, bj = 0x7fffffff;
-
   for (int i = r0; i < r1; ++i) {
-    const int q = i - r0;
     const double* A;
     const double* B;
     if (STAGE) {
-      if (lane == 0 && q + 2 < nrows) {
-        const int b = (q + 2) % kBufs;
-        const int node = tour[r0 + q + 2];
-        fence_proxy_async();
-        mbar_expect_tx(&wb[b], a.row_bytes);
-        bulk_g2s(wbase + (size_t)b * a.buf_stride,
-                 a.cost + (size_t)node * a.ld, a.row_bytes, &wb[b]);
-      }
-      const int ba = q % kBufs, bb = (q + 1) % kBufs;
-      mbar_wait(&wb[ba], (uint32_t)((q / kBufs) & 1));
-      mbar_wait(&wb[bb], (uint32_t)(((q + 1) / kBufs) & 1));
-      A = (const double*)(wbase + (size_t)ba * a.buf_stride);
-      B = (const double*)(wbase + (size_t)bb * a.buf_stride);
+      ring.advance(i - r0, &A, &B);
     } else {
       A = a.cost + (size_t)tour[i] * a.ld;
       B = a.cost + (size_t)tour[i + 1] * a.ld;
     }
     const double di = dg[i];
-    // row-local first minimum over this lane's columns (ascending j)
     double rbest = kInf;
     int rj = 0x7fffffff;
     if (NPL > 0) {
@@ -231,18 +283,191 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
     }
     __syncwarp();
   }
+  warp_argmin(best, bi, bj);
+  if (lane == 0) *out = {best, bi, bj};
+}
+
+// ---- FP32 scan: EXACT32 (MODE 1) and FILTER32 (MODE 2) ---------------------
+template <int NPL, int MODE>
+__global__ void __launch_bounds__(kMaxWarps * 32)
+    k_two_opt_scan32(ScanArgs a) {
+  if (a.ctl && (a.ctl->done || a.ctl->improved)) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bars[kMaxWarps][kBufs];
+  __shared__ uint32_t s_cij[kMaxWarps][kCand][32];
+  __shared__ float s_cd[kMaxWarps][kCand][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int task = blockIdx.x * (blockDim.x >> 5) + warp;
+  const int p = task / a.chunks, c = task % a.chunks;
+  if (p >= a.count) return;
+  const int n = a.n;
+  const int r0 = a.chunk_row[c], r1 = a.chunk_row[c + 1];
+  TwoOptRes* out = a.res + (size_t)p * a.chunks + c;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  const float kInfF = __int_as_float(0x7f800000);
+  if (r0 >= r1) {
+    if (lane == 0) *out = {kInf, 0x7fffffff, 0x7fffffff};
+    return;
+  }
+  const uint16_t* tour = a.tours + (size_t)p * a.np;
+  const double* dg = a.dcache + (size_t)p * a.np;
+  // FILTER32 excludes the structural pairs (i, i+1) (and (0, n-1) below)
+  constexpr int kGap = MODE == 2 ? 1 : 0;
+
+  uint32_t pk[NPL];
+  float dj[NPL];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    double d2 = __shfl_xor_sync(0xffffffffu, best, o);
-    int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-    int j2 = __shfl_xor_sync(0xffffffffu, bj, o);
-    if (res_less(d2, i2, j2, best, bi, bj)) {
-      best = d2;
-      bi = i2;
-      bj = j2;
+  for (int m = 0; m < NPL; ++m) {
+    int j = lane + 32 * m;
+    if (j < n) {
+      uint32_t aj = tour[j], sj = tour[j + 1 == n ? 0 : j + 1];
+      pk[m] = aj | (sj << 16);
+      dj[m] = (float)dg[j];
+    } else {
+      pk[m] = 0;
+      dj[m] = 0.f;
     }
   }
-  if (lane == 0) *out = {best, bi, bj};
+  RowRing<float> ring{smem + (size_t)warp * kBufs * a.buf_stride, bars[warp],
+                      a.row_bytes, a.buf_stride, a.cost32, a.ld32, tour, r0,
+                      r1 - r0 + 1};
+  ring.start();
+
+  // EXACT32: running first minimum.  FILTER32: running fp32 minimum + list.
+  float best = kInfF;
+  int bi = 0x7fffffff, bj = 0x7fffffff;
+  float lim = kInfF;  // FILTER32: best + thr
+  int ncand = 0, overflow = 0;
+  for (int i = r0; i < r1; ++i) {
+    const float* A;
+    const float* B;
+    ring.advance(i - r0, &A, &B);
+    const float di = (float)dg[i];
+    // FILTER32: pair (0, n-1) is structural too
+    const int jlim = (MODE == 2 && i == 0) ? n - 1 : n;
+    float rbest = kInfF;
+    int rj = 0x7fffffff;
+#pragma unroll
+    for (int m0 = 0; m0 < NPL; m0 += kGroup) {
+      if (32 * (m0 + kGroup) - 1 > i + kGap) {  // warp-uniform
+        float av[kGroup], bv[kGroup];
+#pragma unroll
+        for (int g = 0; g < kGroup; ++g) {
+          if (m0 + g < NPL) {
+            av[g] = A[pk[m0 + g] & 0xFFFFu];
+            bv[g] = B[pk[m0 + g] >> 16];
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < kGroup; ++g) {
+          if (m0 + g < NPL) {
+            const int j = lane + 32 * (m0 + g);
+            float t = __fadd_rn(av[g], bv[g]);
+            t = __fsub_rn(t, di);
+            t = __fsub_rn(t, dj[m0 + g]);
+            t = (j > i + kGap && j < jlim) ? t : kInfF;
+            if (MODE == 1) {
+              const bool lt = t < rbest;
+              rbest = lt ? t : rbest;
+              rj = lt ? j : rj;
+            } else if (t <= lim) {  // rare: new minimum or near-tie
+              if (t < best) {
+                best = t;
+                lim = __fadd_ru(t, a.thr);
+                int w = 0;
+                for (int k = 0; k < ncand; ++k) {
+                  const float d = s_cd[warp][k][lane];
+                  if (d <= lim) {
+                    s_cd[warp][w][lane] = d;
+                    s_cij[warp][w][lane] = s_cij[warp][k][lane];
+                    ++w;
+                  }
+                }
+                ncand = w;
+              }
+              if (ncand < kCand) {
+                s_cd[warp][ncand][lane] = t;
+                s_cij[warp][ncand][lane] = ((uint32_t)i << 16) | (uint32_t)j;
+                ++ncand;
+              } else {
+                overflow = 1;
+              }
+            }
+          }
+        }
+      }
+    }
+    if (MODE == 1 && rbest < best) {
+      best = rbest;
+      bi = i;
+      bj = rj;
+    }
+    __syncwarp();
+  }
+  if (MODE == 1) {
+    double bd = best == kInfF ? kInf : (double)best;
+    warp_argmin(bd, bi, bj);
+    if (lane == 0) *out = {bd, bi, bj};
+    return;
+  }
+  // FILTER32: warp minimum, candidate re-evaluation in fp64
+  if (__any_sync(0xffffffffu, overflow)) {
+    if (lane == 0) *out = {kInf, kOverflowTag, kOverflowTag};
+    return;
+  }
+  float m = best;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+    m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const float keep = __fadd_ru(m, a.thr);
+  double bd = kInf;
+  int ei = 0x7fffffff, ej = 0x7fffffff;
+  for (int k = 0; k < ncand; ++k) {
+    if (s_cd[warp][k][lane] <= keep) {
+      const uint32_t ij = s_cij[warp][k][lane];
+      const int i = (int)(ij >> 16), j = (int)(ij & 0xFFFFu);
+      const int ai = tour[i], aj = tour[j];
+      const int si = tour[i + 1], sj = tour[j + 1 == n ? 0 : j + 1];
+      double t = __dadd_rn(a.cost[(size_t)ai * a.ld + aj],
+                           a.cost[(size_t)si * a.ld + sj]);
+      t = __dsub_rn(t, dg[i]);
+      t = __dsub_rn(t, dg[j]);
+      if (res_less(t, i, j, bd, ei, ej)) {
+        bd = t;
+        ei = i;
+        ej = j;
+      }
+    }
+  }
+  // structural pairs, exact from d: (i, i+1) has A = d_i, B = d_{i+1}
+  for (int i = r0 + lane; i < r1; i += 32) {
+    if (i + 1 < n) {
+      const double d0 = dg[i], d1 = dg[i + 1];
+      double t = __dadd_rn(d0, d1);
+      t = __dsub_rn(t, d0);
+      t = __dsub_rn(t, d1);
+      if (res_less(t, i, i + 1, bd, ei, ej)) {
+        bd = t;
+        ei = i;
+        ej = i + 1;
+      }
+    }
+  }
+  if (r0 == 0 && lane == 0 && n - 1 > 1) {  // (0, n-1): s_{n-1} = a_0
+    const int j = n - 1;
+    const int a0 = tour[0], aj = tour[j], s0 = tour[1], sj = tour[0];
+    double t = __dadd_rn(a.cost[(size_t)a0 * a.ld + aj],
+                         a.cost[(size_t)s0 * a.ld + sj]);
+    t = __dsub_rn(t, dg[0]);
+    t = __dsub_rn(t, dg[j]);
+    if (res_less(t, 0, j, bd, ei, ej)) {
+      bd = t;
+      ei = 0;
+      ej = j;
+    }
+  }
+  warp_argmin(bd, ei, ej);
+  if (lane == 0) *out = {bd, ei, ej};
 }
 
 struct ApplyArgs {
@@ -265,6 +490,7 @@ __global__ void __launch_bounds__(128) k_two_opt_apply(ApplyArgs a) {
   if (p >= a.count) return;
   __shared__ int s_move[3];
   __shared__ double s_delta;
+  __shared__ int s_better;
   const int tid = threadIdx.x;
   if (tid == 0) {
     double best = __longlong_as_double(0x7ff0000000000000ll);
@@ -295,13 +521,12 @@ __global__ void __launch_bounds__(128) k_two_opt_apply(ApplyArgs a) {
   }
   __syncthreads();
   if (a.cost) {
-    for (int k = max(i, 0) + tid; k <= j && k < a.n; k += blockDim.x) {
+    for (int k = i + tid; k <= j && k < a.n; k += blockDim.x) {
       int u = t[k], w = t[k + 1 == a.n ? 0 : k + 1];
       a.dcache[(size_t)p * a.np + k] = a.cost[(size_t)u * a.ld + w];
     }
   }
   if (a.fit) {
-    __shared__ int s_better;
     if (tid == 0) {
       double f = __dadd_rn(a.fit[p], s_delta);
       a.fit[p] = f;
@@ -316,10 +541,40 @@ __global__ void __launch_bounds__(128) k_two_opt_apply(ApplyArgs a) {
   }
 }
 
+// ---- cost-matrix preparation ------------------------------------------------
+// fp32 copy + statistics: max |C| (as the bits of a non-negative double,
+// which order like the values) and whether every entry is an integer.
+__global__ void k_cost_prep(const double* cost, int64_t ld, int n,
+                            float* cost32, int64_t ld32, CostStats* st) {
+  unsigned long long mx = 0;
+  int nonint = 0;
+  const int64_t total = (int64_t)n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / n, c = e % n;
+    const double v = cost[r * ld + c];
+    cost32[r * ld32 + c] = (float)v;
+    const unsigned long long b =
+        (unsigned long long)__double_as_longlong(fabs(v));
+    mx = b > mx ? b : mx;
+    nonint |= (v != rint(v));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long m2 = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = m2 > mx ? m2 : mx;
+    nonint |= __shfl_xor_sync(0xffffffffu, nonint, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&st->maxabs_bits, mx);
+    if (nonint) atomicOr(&st->nonintegral, 1);
+  }
+}
+
 template <int NPL, bool STAGE>
-cudaError_t launch_scan_t(const ScanArgs& a, int warps, int blocks,
-                          size_t smem, cudaStream_t s) {
-  auto k = k_two_opt_scan<NPL, STAGE>;
+cudaError_t launch_scan64_t(const ScanArgs& a, int warps, int blocks,
+                            size_t smem, cudaStream_t s) {
+  auto k = k_two_opt_scan64<NPL, STAGE>;
   static size_t configured = 48 * 1024;
   if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(
@@ -331,23 +586,75 @@ cudaError_t launch_scan_t(const ScanArgs& a, int warps, int blocks,
   return cudaGetLastError();
 }
 
-// bytes of the per-warp row ring
-size_t ring_bytes(int n) {
-  return (size_t)kBufs * round_up((int64_t)round_up(n, 2) * 8, 128);
+template <int NPL, int MODE>
+cudaError_t launch_scan32_t(const ScanArgs& a, int warps, int blocks,
+                            size_t smem, cudaStream_t s) {
+  auto k = k_two_opt_scan32<NPL, MODE>;
+  static size_t configured = 48 * 1024;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(
+        k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  k<<<blocks, warps * 32, smem, s>>>(a);
+  return cudaGetLastError();
 }
 
-constexpr size_t kSmemBudget = 220 * 1024;
+// bytes of one warp's row ring for element size `es`
+size_t ring_bytes(int n, int es) {
+  return (size_t)kBufs * round_up((int64_t)round_up(n, 16 / es) * es, 128);
+}
+
+constexpr size_t kSmemBudget = 200 * 1024;
+
+int npl_for(int n) {
+  if (n <= 32) return 1;
+  if (n <= 64) return 2;
+  if (n <= 128) return 4;
+  if (n <= 256) return 8;
+  if (n <= 512) return 16;
+  if (n <= 1024) return 32;
+  if (n <= 2048) return 64;
+  return 0;
+}
 
 }  // namespace
+
+int two_opt_mode(const CostStats& st, int n, float* thr) {
+  double mx;
+  memcpy(&mx, &st.maxabs_bits, sizeof mx);
+  *thr = 0.f;
+  if (npl_for(n) == 0) return kScanFP64;  // register layout needs n <= 2048
+  if (!(mx < 1e30)) return kScanFP64;     // fp32 range
+  if (!st.nonintegral && mx < 4194304.0) return kScanExact32;  // 2^22
+  if (mx < 1e-30) return kScanFP64;       // fp32 subnormal range
+  // eps = 2^-18 max|C| (>= 4x the worst-case fp32 rounding of a delta);
+  // candidates within 2 eps of the fp32 minimum are re-evaluated in fp64.
+  *thr = (float)(mx * (2.0 / 262144.0));
+  return kScanFilter32;
+}
+
+cudaError_t launch_cost_prep(const double* cost, int64_t ld, int32_t n,
+                             float* cost32, int64_t ld32, CostStats* st,
+                             cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(st, 0, sizeof(CostStats), s);
+  if (e) return e;
+  const int64_t total = (int64_t)n * n;
+  int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  if (blocks < 1) blocks = 1;
+  k_cost_prep<<<blocks, 256, 0, s>>>(cost, ld, n, cost32, ld32, st);
+  return cudaGetLastError();
+}
 
 int two_opt_pick_chunks(int32_t n, int32_t P) {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  size_t per_warp = ring_bytes(n);
+  size_t per_warp = ring_bytes(n, 4);
   int warps_per_sm = (int)(kSmemBudget / per_warp);
   if (warps_per_sm < 1) warps_per_sm = 1;
-  if (warps_per_sm > 32) warps_per_sm = 32;
+  if (warps_per_sm > 16) warps_per_sm = 16;
   int64_t slots = (int64_t)sms * warps_per_sm;
   int chunks = (int)((4 * slots + P - 1) / P);
   if (chunks < 1) chunks = 1;
@@ -377,17 +684,19 @@ int two_opt_chunk_rows(int32_t n, int32_t chunks, int32_t* rows) {
   return 0;
 }
 
-cudaError_t launch_two_opt_core(const double* cost, int64_t ld, int32_t n,
-                                int32_t np, uint16_t* tours,
-                                const double* dcache, int32_t count,
-                                TwoOptRes* res, int32_t chunks,
+cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
+                                uint16_t* tours, const double* dcache,
+                                int32_t count, TwoOptRes* res, int32_t chunks,
                                 const int32_t* chunk_row, const DevCtl* ctl,
                                 double* fit, double* pfit, uint16_t* pbest,
                                 double* delta_out, double* dcache_rw,
-                                cudaStream_t s, int parts = 3) {
+                                cudaStream_t s, int parts) {
   ScanArgs a;
-  a.cost = cost;
-  a.ld = ld;
+  memset(&a, 0, sizeof a);
+  a.cost = pl.cost;
+  a.ld = pl.ld;
+  a.cost32 = pl.cost32;
+  a.ld32 = pl.ld32;
   a.n = n;
   a.np = np;
   a.count = count;
@@ -397,39 +706,68 @@ cudaError_t launch_two_opt_core(const double* cost, int64_t ld, int32_t n,
   a.chunk_row = chunk_row;
   a.res = res;
   a.ctl = ctl;
-  a.row_bytes = (uint32_t)(round_up(n, 2) * 8);
-  a.buf_stride = (uint32_t)round_up(a.row_bytes, 128);
-  const size_t per_warp = ring_bytes(n);
-  const bool stage = per_warp <= kSmemBudget;
-  int warps = stage ? (int)std::min<size_t>(kMaxWarps, kSmemBudget / per_warp)
-                    : kMaxWarps;
-  const size_t smem = stage ? (size_t)warps * per_warp : 0;
+  a.thr = pl.thr;
   const int64_t tasks = (int64_t)count * chunks;
-  const int blocks = (int)((tasks + warps - 1) / warps);
   cudaError_t e = cudaSuccess;
-  if ((parts & 1) && n >= 4 && blocks > 0) {
-#define SCAN(NPL)                                                    \
-  (stage ? launch_scan_t<NPL, true>(a, warps, blocks, smem, s)       \
-         : launch_scan_t<NPL, false>(a, warps, blocks, smem, s))
-    if (n <= 32)
-      e = SCAN(1);
-    else if (n <= 64)
-      e = SCAN(2);
-    else if (n <= 128)
-      e = SCAN(4);
-    else if (n <= 256)
-      e = SCAN(8);
-    else if (n <= 512)
-      e = SCAN(16);
-    else if (n <= 1024)
-      e = SCAN(32);
-    else if (n <= 2048)
-      e = SCAN(64);
-    else
-      e = SCAN(0);
-#undef SCAN
+  const int npl = npl_for(n);
+  auto fp64_scan = [&](int only_flagged) -> cudaError_t {
+    a.only_flagged = only_flagged;
+    a.row_bytes = (uint32_t)(round_up(n, 2) * 8);
+    a.buf_stride = (uint32_t)round_up(a.row_bytes, 128);
+    const size_t per_warp = ring_bytes(n, 8);
+    const bool stage = per_warp <= kSmemBudget;
+    const int warps =
+        stage ? (int)std::min<size_t>(kMaxWarps, kSmemBudget / per_warp)
+              : kMaxWarps;
+    const size_t smem = stage ? (size_t)warps * per_warp : 0;
+    const int blocks = (int)((tasks + warps - 1) / warps);
+#define SCAN64(NPL)                                                 \
+  (stage ? launch_scan64_t<NPL, true>(a, warps, blocks, smem, s)    \
+         : launch_scan64_t<NPL, false>(a, warps, blocks, smem, s))
+    switch (npl) {
+      case 1: return SCAN64(1);
+      case 2: return SCAN64(2);
+      case 4: return SCAN64(4);
+      case 8: return SCAN64(8);
+      case 16: return SCAN64(16);
+      case 32: return SCAN64(32);
+      case 64: return SCAN64(64);
+      default: return SCAN64(0);
+    }
+#undef SCAN64
+  };
+  if ((parts & 1) && n >= 4 && tasks > 0) {
+    if (pl.mode == kScanFP64 || !pl.cost32) {
+      e = fp64_scan(0);
+    } else {
+      a.row_bytes = (uint32_t)(round_up(n, 4) * 4);
+      a.buf_stride = (uint32_t)round_up(a.row_bytes, 128);
+      const size_t per_warp = ring_bytes(n, 4);
+      const int warps =
+          (int)std::max<size_t>(1, std::min<size_t>(kMaxWarps,
+                                                    kSmemBudget / per_warp));
+      const size_t smem = (size_t)warps * per_warp;
+      const int blocks = (int)((tasks + warps - 1) / warps);
+#define SCAN32(NPL)                                                        \
+  (pl.mode == kScanExact32                                                 \
+       ? launch_scan32_t<NPL, 1>(a, warps, blocks, smem, s)                \
+       : launch_scan32_t<NPL, 2>(a, warps, blocks, smem, s))
+      switch (npl) {
+        case 1: e = SCAN32(1); break;
+        case 2: e = SCAN32(2); break;
+        case 4: e = SCAN32(4); break;
+        case 8: e = SCAN32(8); break;
+        case 16: e = SCAN32(16); break;
+        case 32: e = SCAN32(32); break;
+        default: e = SCAN32(64); break;
+      }
+#undef SCAN32
+      // FILTER32 candidate-list overflow: exact fp64 re-scan of those tasks
+      if (!e && pl.mode == kScanFilter32) e = fp64_scan(1);
+    }
     if (e != cudaSuccess) return e;
   }
+  if (!(parts & 2)) return cudaSuccess;
   ApplyArgs b;
   b.n = n;
   b.np = np;
@@ -442,10 +780,9 @@ cudaError_t launch_two_opt_core(const double* cost, int64_t ld, int32_t n,
   b.pbest = pbest;
   b.delta_out = delta_out;
   b.ctl = ctl;
-  b.cost = dcache_rw ? cost : nullptr;
-  b.ld = ld;
+  b.cost = dcache_rw ? pl.cost : nullptr;
+  b.ld = pl.ld;
   b.dcache = dcache_rw;
-  if (!(parts & 2)) return cudaSuccess;
   if (n < 4) {
     // _best_exchange returns (body, 0.0) for n < 4 (solver.py:91-93)
     if (delta_out) cudaMemsetAsync(delta_out, 0, sizeof(double) * count, s);
@@ -456,21 +793,19 @@ cudaError_t launch_two_opt_core(const double* cost, int64_t ld, int32_t n,
 }
 
 cudaError_t launch_two_opt(const SwarmView& v, cudaStream_t s, int parts) {
-  return launch_two_opt_core(v.cost, v.ld, v.n, v.np, v.x, v.dcache, v.P,
-                             v.tores, v.chunks, v.chunk_row, v.ctl, v.fit,
-                             v.pfit, v.pbest, nullptr, nullptr, s, parts);
+  return launch_two_opt_core(v.plan, v.n, v.np, v.x, v.dcache, v.P, v.tores,
+                             v.chunks, v.chunk_row, v.ctl, v.fit, v.pfit,
+                             v.pbest, nullptr, nullptr, s, parts);
 }
 
-cudaError_t launch_two_opt_batch(const double* cost, int64_t ld, int32_t n,
-                                 int32_t np, uint16_t* tours,
-                                 const double* dcache, int32_t count,
-                                 TwoOptRes* res, int32_t chunks,
+cudaError_t launch_two_opt_batch(const TwoOptPlan& pl, int32_t n, int32_t np,
+                                 uint16_t* tours, const double* dcache,
+                                 int32_t count, TwoOptRes* res, int32_t chunks,
                                  const int32_t* chunk_row, double* delta_out,
                                  cudaStream_t s) {
-  return launch_two_opt_core(cost, ld, n, np, tours, dcache, count, res,
-                             chunks, chunk_row, nullptr, nullptr, nullptr,
-                             nullptr, delta_out, const_cast<double*>(dcache),
-                             s);
+  return launch_two_opt_core(pl, n, np, tours, dcache, count, res, chunks,
+                             chunk_row, nullptr, nullptr, nullptr, nullptr,
+                             delta_out, const_cast<double*>(dcache), s, 3);
 }
 
 }  // namespace dpso

@@ -18,7 +18,7 @@ def pkg():
     return pkg
 
 
-def test_e2e_golden_runs(pkg, golden_e2e):
+def test_e2e_golden_runs(pkg, golden_e2e, scan_mode):
     for case in golden_e2e["cases"]:
         cost = golden_matrix(golden_e2e, case["instance"])
         s = pkg.DiscreteSwarmSolver(**golden_params(golden_e2e, case)).fit(cost)
@@ -44,19 +44,67 @@ def test_best_exchange_golden(pkg, golden_kernels):
         assert [float(c) for c in costs] == [r["cost"] for r in recs]
 
 
-def test_best_exchange_vs_oracle_sizes(pkg):
+SCAN_MODES = {"fp64": "0", "exact32": "1", "filter32": "2"}
+
+
+@pytest.fixture(params=[None, "fp64", "filter32"])
+def scan_mode(request, monkeypatch):
+    if request.param:
+        monkeypatch.setenv("DPSO_SCAN_MODE", SCAN_MODES[request.param])
+    return request.param
+
+
+def check_batch(pkg, cost, tours, tag):
+    new, delta = pkg.best_exchange_batch(cost, tours)
+    for t, nb, d in zip(tours, new, delta):
+        eb, ed = O.best_exchange([int(v) for v in t], cost)
+        assert [int(v) for v in nb] == [int(v) for v in eb], tag
+        assert float(d) == ed, tag
+
+
+def test_best_exchange_vs_oracle_sizes(pkg, scan_mode):
     rng = np.random.default_rng(3)
     for n in (4, 5, 31, 32, 33, 64, 65, 127, 300, 513, 1000, 1500, 2049, 2500):
         cost = random_euclidean_matrix(n, rng)
-        if n in (65, 513):  # integer costs: many ties
-            cost = np.floor(cost)
         tours = np.array([rng.permutation(n) for _ in range(6)],
                          dtype=np.int32)
-        new, delta = pkg.best_exchange_batch(cost, tours)
-        for t, nb, d in zip(tours, new, delta):
-            eb, ed = O.best_exchange([int(v) for v in t], cost)
-            assert [int(v) for v in nb] == [int(v) for v in eb], n
-            assert float(d) == ed, n
+        check_batch(pkg, cost, tours, (n, scan_mode))
+
+
+@pytest.mark.parametrize("mode", [None, "fp64", "exact32", "filter32"])
+def test_best_exchange_integer_ties(pkg, mode, monkeypatch):
+    # integer costs: many exact ties -> row-major first-index tie break
+    if mode:
+        monkeypatch.setenv("DPSO_SCAN_MODE", SCAN_MODES[mode])
+    rng = np.random.default_rng(8)
+    for n in (17, 65, 300, 513, 1100):
+        cost = np.floor(random_euclidean_matrix(n, rng))
+        tours = np.array([rng.permutation(n) for _ in range(5)],
+                         dtype=np.int32)
+        check_batch(pkg, cost, tours, (n, mode))
+
+
+def test_best_exchange_near_ties_and_converged(pkg, scan_mode):
+    rng = np.random.default_rng(11)
+    # a lattice with 1e-9 jitter: thousands of near-ties inside the fp32
+    # filter window -> candidate-list overflow -> fp64 re-scan of the task
+    side = 20
+    g = np.stack(np.meshgrid(np.arange(side), np.arange(side)), -1)
+    pts = g.reshape(-1, 2).astype(float) + rng.random((side * side, 2)) * 1e-9
+    cost = np.sqrt(((pts[:, None] - pts[None]) ** 2).sum(-1))
+    tours = np.array([rng.permutation(side * side) for _ in range(4)] +
+                     [np.arange(side * side)], dtype=np.int32)
+    check_batch(pkg, cost, tours, ("lattice", scan_mode))
+    # 2-opt-optimal tours: only the structural (i,i+1) residues are ~0
+    for n in (50, 200):
+        cost = random_euclidean_matrix(n, rng) * 1e4
+        tour, _ = O.nearest_neighbor_two_opt(cost)
+        body = np.array([tour[:-1]], dtype=np.int32)
+        check_batch(pkg, cost, body, ("converged", n, scan_mode))
+    # large values: fp64 residues of the no-op pairs exceed 1e-12
+    cost = random_euclidean_matrix(60, rng) * 1e9
+    tours = np.array([rng.permutation(60) for _ in range(4)], dtype=np.int32)
+    check_batch(pkg, cost, tours, ("big", scan_mode))
 
 
 def test_nn_two_opt_golden(pkg, golden_kernels):
