@@ -46,6 +46,9 @@ CONFIGS = {
                workload="C2: synthetic N=1000 extended TSP (random Euclidean,"
                         " default_rng(1000)), swarm P=1024, 500-generation "
                         "schedule, enhanced DPSO (paper defaults)"),
+    "c2i": dict(n=1000, P=1024, G=500, matrix="euclid_int",
+                workload="C2 with integer costs: floor(1000 x random-Euclidean "
+                         "N=1000), swarm P=1024 (scene-like integer matrix)"),
     "c3": dict(n=500, P=16384, G=100, matrix="grid",
                workload="C3: bridge-sized synthetic instance N=500 (integer "
                         "grid costs, many ties), swarm P=16384"),
@@ -76,6 +79,8 @@ def make_matrix(cfg):
     pts = rng.random((n, 2)) * 10.0
     c = np.sqrt(((pts[:, None, :] - pts[None, :, :]) ** 2).sum(-1))
     np.fill_diagonal(c, 0.0)
+    if cfg["matrix"] == "euclid_int":
+        c = np.floor(c * 1000.0)
     return c, None
 
 
@@ -418,10 +423,17 @@ def main():
     ap.add_argument("--profile-gens", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--scan-mode", choices=["auto", "fp64", "exact32",
+                                            "filter32"], default="auto",
+                    help="force the 2-opt scan mode (default: chosen from "
+                         "the matrix)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     cfg = CONFIGS[args.config]
+    if args.scan_mode != "auto":
+        os.environ["DPSO_SCAN_MODE"] = {"fp64": "0", "exact32": "1",
+                                        "filter32": "2"}[args.scan_mode]
     if args.impl == "reference":
         run_reference(args, args.config, cfg)
     else:

@@ -10,12 +10,28 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "dpso_internal.cuh"
 
 using namespace dpso;
+
+namespace dpso {
+cudaError_t set_dyn_smem(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> done;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = done.find(kernel);
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(
+      kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done[kernel] = bytes;
+  return e;
+}
+}  // namespace dpso
 
 namespace {
 
@@ -156,18 +172,27 @@ static int sync_out(dpso_ctx* c) {
   return DPSO_OK;
 }
 
+static const char* g_stage = "";
+
 static cudaError_t enqueue_generation(const SwarmView& v, cudaStream_t s) {
-  cudaError_t e = launch_gen_begin(v, s);
-  if (e) return e;
-  if ((e = launch_update(v, s))) return e;
-  if (v.use_mutation && (e = launch_mutation(v, s))) return e;
+  cudaError_t e;
+#define STAGE(name, call)      \
+  do {                         \
+    g_stage = name;            \
+    if ((e = (call))) return e; \
+  } while (0)
+  STAGE("gen_begin", launch_gen_begin(v, s));
+  STAGE("update", launch_update(v, s));
+  if (v.use_mutation) STAGE("mutation", launch_mutation(v, s));
   if (v.use_edge_exchange) {
-    if ((e = launch_select(v, false, s))) return e;
-    if ((e = launch_two_opt(v, s))) return e;
-    if ((e = launch_finalize(v, s))) return e;
+    STAGE("select", launch_select(v, false, s));
+    STAGE("two_opt", launch_two_opt(v, s));
+    STAGE("finalize", launch_finalize(v, s));
   } else {
-    if ((e = launch_select(v, true, s))) return e;
+    STAGE("select+finalize", launch_select(v, true, s));
   }
+#undef STAGE
+  g_stage = "";
   return cudaSuccess;
 }
 
@@ -364,7 +389,10 @@ static int ensure_graph(dpso_ctx* c) {
   CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   cudaError_t e = enqueue_generation(c->v, c->stream);
   cudaError_t e2 = cudaStreamEndCapture(c->stream, &g);
-  if (e) return cuda_fail(e, "capture generation");
+  if (e) {
+    std::string where = std::string("capture generation (") + g_stage + ")";
+    return cuda_fail(e, where.c_str());
+  }
   if (e2) return cuda_fail(e2, "cudaStreamEndCapture");
   e = cudaGraphInstantiate(&c->graph, g, 0);
   cudaGraphDestroy(g);

@@ -147,6 +147,9 @@ cudaError_t launch_nn(const double* cost, int64_t ld, int32_t n, int32_t start,
 cudaError_t launch_pysum_tour(const double* cost, int64_t ld, int32_t n,
                               const int32_t* body, double* out,
                               cudaStream_t s);
+// Opt a kernel in to `bytes` of dynamic shared memory (cached per kernel;
+// static shared memory counts against the same limit, so always opt in).
+cudaError_t set_dyn_smem(const void* kernel, size_t bytes);
 int two_opt_chunk_rows(int32_t n, int32_t chunks, int32_t* rows);
 int two_opt_pick_chunks(int32_t n, int32_t P);
 

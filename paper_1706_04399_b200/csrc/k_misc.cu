@@ -472,10 +472,7 @@ cudaError_t launch_init(const SwarmView& v, const uint16_t* dev_seed,
                         int32_t n_seed, cudaStream_t s) {
   k_init_walk<<<1, 32, 0, s>>>(v, n_seed);
   size_t smem = round_up((int64_t)2 * v.np, 16) + (size_t)8 * v.np;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_init_build,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+  set_dyn_smem((const void*)k_init_build, smem);
   k_init_build<<<v.P, 128, smem, s>>>(v, dev_seed, n_seed);
   return cudaGetLastError();
 }
@@ -490,10 +487,7 @@ cudaError_t launch_tour_cost_rows(const double* cost, int64_t ld, int32_t n,
                                   int32_t count, double* out, double* dcache,
                                   cudaStream_t s) {
   size_t smem = (size_t)4 * n * sizeof(double);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_tour_cost,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+  set_dyn_smem((const void*)k_tour_cost, smem);
   k_tour_cost<<<(count + 3) / 4, 128, smem, s>>>(cost, ld, n, tours, stride,
                                                  count, out, dcache);
   return cudaGetLastError();

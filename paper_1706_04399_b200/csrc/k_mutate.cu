@@ -507,25 +507,16 @@ cudaError_t launch_mutation(const SwarmView& v, cudaStream_t s) {
   k_mut_lists<<<1, 1024, 0, s>>>(v);
   k_mut_copy<<<P, 128, 0, s>>>(v);
   const size_t ring = (size_t)kRing * 4;
-  cudaFuncSetAttribute(k_mut_walk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)ring);
+  set_dyn_smem((const void*)k_mut_walk, ring);
   k_mut_walk<<<1, kWalk, ring, s>>>(v);
   const size_t scratch =
       std::max<size_t>(round_up((v.n + 31) / 32 * 4, 16), 2 * (size_t)v.np);
-  if (scratch > 48 * 1024) {
-    cudaFuncSetAttribute(k_mut_sample,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)scratch);
-    cudaFuncSetAttribute(k_mut_fix,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)scratch);
-  }
+  set_dyn_smem((const void*)k_mut_sample, scratch);
+  set_dyn_smem((const void*)k_mut_fix, scratch);
   k_mut_sample<<<P, 128, scratch, s>>>(v);
   k_mut_fix<<<1, 32, scratch, s>>>(v);
   const size_t sd = (size_t)8 * v.np;
-  if (sd > 48 * 1024)
-    cudaFuncSetAttribute(k_mut_swap,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sd);
+  set_dyn_smem((const void*)k_mut_swap, sd);
   k_mut_swap<<<P, 128, sd, s>>>(v);
   return cudaGetLastError();
 }

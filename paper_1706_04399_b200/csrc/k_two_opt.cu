@@ -288,6 +288,52 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
 }
 
 // ---- FP32 scan: EXACT32 (MODE 1) and FILTER32 (MODE 2) ---------------------
+// FILTER32 candidate bookkeeping, out of line (rarely taken; keeping it out
+// of the unrolled column loop keeps the kernel inside the instruction cache).
+// Per lane state lives in shared memory (stride 32 between words): st[0] =
+// running fp32 minimum, st[32] = candidate count, st[64] = overflow flag; cd/cij are this lane's
+// candidate slots (stride 32).  Returns the new window limit.
+__device__ __noinline__ float cand_group(float t0, float t1, float t2,
+                                         float t3, int i, int j0, float lim,
+                                         float thr, float* cd, uint32_t* cij,
+                                         float* st) {
+  float best = st[0];
+  int ncand = __float_as_int(st[32]);
+  int overflow = __float_as_int(st[64]);
+  const float tv[4] = {t0, t1, t2, t3};
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const float t = tv[g];
+    if (t <= lim) {
+      if (t < best) {
+        best = t;
+        lim = __fadd_ru(t, thr);
+        int w = 0;
+        for (int k = 0; k < ncand; ++k) {
+          const float d = cd[32 * k];
+          if (d <= lim) {
+            cd[32 * w] = d;
+            cij[32 * w] = cij[32 * k];
+            ++w;
+          }
+        }
+        ncand = w;
+      }
+      if (ncand < kCand) {
+        cd[32 * ncand] = t;
+        cij[32 * ncand] = ((uint32_t)i << 16) | (uint32_t)(j0 + 32 * g);
+        ++ncand;
+      } else {
+        overflow = 1;
+      }
+    }
+  }
+  st[0] = best;
+  st[32] = __int_as_float(ncand);
+  st[64] = __int_as_float(overflow);
+  return lim;
+}
+
 template <int NPL, int MODE>
 __global__ void __launch_bounds__(kMaxWarps * 32)
     k_two_opt_scan32(ScanArgs a) {
@@ -296,6 +342,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
   __shared__ __align__(8) uint64_t bars[kMaxWarps][kBufs];
   __shared__ uint32_t s_cij[kMaxWarps][kCand][32];
   __shared__ float s_cd[kMaxWarps][kCand][32];
+  __shared__ float s_st[kMaxWarps][3][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int task = blockIdx.x * (blockDim.x >> 5) + warp;
   const int p = task / a.chunks, c = task % a.chunks;
@@ -305,6 +352,11 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
   TwoOptRes* out = a.res + (size_t)p * a.chunks + c;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
   const float kInfF = __int_as_float(0x7f800000);
+  if (MODE == 2) {
+    s_st[warp][0][lane] = kInfF;
+    s_st[warp][1][lane] = __int_as_float(0);
+    s_st[warp][2][lane] = __int_as_float(0);
+  }
   if (r0 >= r1) {
     if (lane == 0) *out = {kInf, 0x7fffffff, 0x7fffffff};
     return;
@@ -333,11 +385,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
                       r1 - r0 + 1};
   ring.start();
 
-  // EXACT32: running first minimum.  FILTER32: running fp32 minimum + list.
+  // EXACT32: running first minimum.  FILTER32: window limit (state in smem).
   float best = kInfF;
   int bi = 0x7fffffff, bj = 0x7fffffff;
-  float lim = kInfF;  // FILTER32: best + thr
-  int ncand = 0, overflow = 0;
+  float lim = FLT_MAX;  // FILTER32: best + thr (finite: masked +inf never enters)
   for (int i = r0; i < r1; ++i) {
     const float* A;
     const float* B;
@@ -350,7 +401,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
 #pragma unroll
     for (int m0 = 0; m0 < NPL; m0 += kGroup) {
       if (32 * (m0 + kGroup) - 1 > i + kGap) {  // warp-uniform
-        float av[kGroup], bv[kGroup];
+        float av[kGroup], bv[kGroup], tv[kGroup];
 #pragma unroll
         for (int g = 0; g < kGroup; ++g) {
           if (m0 + g < NPL) {
@@ -360,6 +411,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
         }
 #pragma unroll
         for (int g = 0; g < kGroup; ++g) {
+          tv[g] = kInfF;
           if (m0 + g < NPL) {
             const int j = lane + 32 * (m0 + g);
             float t = __fadd_rn(av[g], bv[g]);
@@ -370,30 +422,19 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
               const bool lt = t < rbest;
               rbest = lt ? t : rbest;
               rj = lt ? j : rj;
-            } else if (t <= lim) {  // rare: new minimum or near-tie
-              if (t < best) {
-                best = t;
-                lim = __fadd_ru(t, a.thr);
-                int w = 0;
-                for (int k = 0; k < ncand; ++k) {
-                  const float d = s_cd[warp][k][lane];
-                  if (d <= lim) {
-                    s_cd[warp][w][lane] = d;
-                    s_cij[warp][w][lane] = s_cij[warp][k][lane];
-                    ++w;
-                  }
-                }
-                ncand = w;
-              }
-              if (ncand < kCand) {
-                s_cd[warp][ncand][lane] = t;
-                s_cij[warp][ncand][lane] = ((uint32_t)i << 16) | (uint32_t)j;
-                ++ncand;
-              } else {
-                overflow = 1;
-              }
+            } else {
+              tv[g] = t;
             }
           }
+        }
+        if (MODE == 2) {
+          bool hit = false;
+#pragma unroll
+          for (int g = 0; g < kGroup; ++g) hit |= tv[g] <= lim;
+          if (hit)
+            lim = cand_group(tv[0], tv[1], tv[2], tv[3], i, lane + 32 * m0,
+                             lim, a.thr, &s_cd[warp][0][lane],
+                             &s_cij[warp][0][lane], &s_st[warp][0][lane]);
         }
       }
     }
@@ -411,7 +452,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
     return;
   }
   // FILTER32: warp minimum, candidate re-evaluation in fp64
-  if (__any_sync(0xffffffffu, overflow)) {
+  best = s_st[warp][0][lane];
+  const int ncand = __float_as_int(s_st[warp][1][lane]);
+  if (__any_sync(0xffffffffu, __float_as_int(s_st[warp][2][lane]))) {
     if (lane == 0) *out = {kInf, kOverflowTag, kOverflowTag};
     return;
   }
@@ -575,13 +618,8 @@ template <int NPL, bool STAGE>
 cudaError_t launch_scan64_t(const ScanArgs& a, int warps, int blocks,
                             size_t smem, cudaStream_t s) {
   auto k = k_two_opt_scan64<NPL, STAGE>;
-  static size_t configured = 48 * 1024;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(
-        k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  cudaError_t e = set_dyn_smem((const void*)k, smem);
+  if (e != cudaSuccess) return e;
   k<<<blocks, warps * 32, smem, s>>>(a);
   return cudaGetLastError();
 }
@@ -590,13 +628,8 @@ template <int NPL, int MODE>
 cudaError_t launch_scan32_t(const ScanArgs& a, int warps, int blocks,
                             size_t smem, cudaStream_t s) {
   auto k = k_two_opt_scan32<NPL, MODE>;
-  static size_t configured = 48 * 1024;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(
-        k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  cudaError_t e = set_dyn_smem((const void*)k, smem);
+  if (e != cudaSuccess) return e;
   k<<<blocks, warps * 32, smem, s>>>(a);
   return cudaGetLastError();
 }

@@ -310,23 +310,16 @@ cudaError_t launch_update(const SwarmView& v, cudaStream_t s) {
     const int R = ceil_log2(v.n);
     if (v.n <= 2048) {
       auto k = k_update_w1<256>;
-      if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+      set_dyn_smem((const void*)k, smem);
       k<<<grid, 256, smem, s>>>(v, R);
     } else {
       auto k = k_update_w1<512>;
-      if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+      set_dyn_smem((const void*)k, smem);
       k<<<grid, 512, smem, s>>>(v, R);
     }
   } else {
     size_t smem = (size_t)8 * v.np + (size_t)8 * v.np;
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(k_update_seq,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
+    set_dyn_smem((const void*)k_update_seq, smem);
     k_update_seq<<<grid, 32, smem, s>>>(v);
   }
   return cudaGetLastError();
