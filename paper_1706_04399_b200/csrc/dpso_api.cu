@@ -154,7 +154,8 @@ struct dpso_ctx {
   unsigned char* ws;
   cudaStream_t user;
   cudaStream_t stream;
-  cudaEvent_t ev;
+  cudaStream_t stream2;  // fork for the mutation-stream walk
+  cudaEvent_t ev, ev_fork, ev_join;
   cudaGraphExec_t graph;
   bool have_cost, have_streams, initialized;
   SwarmView v;
@@ -174,7 +175,11 @@ static int sync_out(dpso_ctx* c) {
 
 static const char* g_stage = "";
 
-static cudaError_t enqueue_generation(const SwarmView& v, cudaStream_t s) {
+// One generation.  With mutation on, the mutation-stream walk runs on a
+// forked stream (s2) concurrently with the update and the dedupe pipeline.
+static cudaError_t enqueue_generation(const SwarmView& v, cudaStream_t s,
+                                      cudaStream_t s2, cudaEvent_t fork,
+                                      cudaEvent_t join) {
   cudaError_t e;
 #define STAGE(name, call)      \
   do {                         \
@@ -182,8 +187,18 @@ static cudaError_t enqueue_generation(const SwarmView& v, cudaStream_t s) {
     if ((e = (call))) return e; \
   } while (0)
   STAGE("gen_begin", launch_gen_begin(v, s));
+  if (v.use_mutation) {
+    STAGE("fork", cudaEventRecord(fork, s));
+    STAGE("fork", cudaStreamWaitEvent(s2, fork, 0));
+    STAGE("mutation_walk", launch_mutation_walk(v, s2));
+    STAGE("join", cudaEventRecord(join, s2));
+  }
   STAGE("update", launch_update(v, s));
-  if (v.use_mutation) STAGE("mutation", launch_mutation(v, s));
+  if (v.use_mutation) {
+    STAGE("mutation_pre", launch_mutation_pre(v, s));
+    STAGE("join", cudaStreamWaitEvent(s, join, 0));
+    STAGE("mutation_post", launch_mutation_post(v, s));
+  }
   if (v.use_edge_exchange) {
     STAGE("select", launch_select(v, false, s));
     STAGE("two_opt", launch_two_opt(v, s));
@@ -234,6 +249,9 @@ int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
     return cuda_fail(e, "cudaStreamCreate");
   }
   cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+  cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking);
   cudaMallocHost(&c->host_ctl, sizeof(DevCtl));
   SwarmView& v = c->v;
   memset(&v, 0, sizeof v);
@@ -387,7 +405,8 @@ static int ensure_graph(dpso_ctx* c) {
   if (c->graph) return DPSO_OK;
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-  cudaError_t e = enqueue_generation(c->v, c->stream);
+  cudaError_t e = enqueue_generation(c->v, c->stream, c->stream2, c->ev_fork,
+                                     c->ev_join);
   cudaError_t e2 = cudaStreamEndCapture(c->stream, &g);
   if (e) {
     std::string where = std::string("capture generation (") + g_stage + ")";
@@ -427,7 +446,15 @@ int dpso_step_timed(dpso_ctx* c, int32_t gens, double* phase_ms,
     CK(launch_gen_begin(v, s));
     CK(launch_update(v, s));
     CK(cudaEventRecord(ev[1], s));
-    if (v.use_mutation) CK(launch_mutation(v, s));
+    if (v.use_mutation) {
+      CK(cudaEventRecord(c->ev_fork, s));
+      CK(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
+      CK(launch_mutation_walk(v, c->stream2));
+      CK(cudaEventRecord(c->ev_join, c->stream2));
+      CK(launch_mutation_pre(v, s));
+      CK(cudaStreamWaitEvent(s, c->ev_join, 0));
+      CK(launch_mutation_post(v, s));
+    }
     CK(cudaEventRecord(ev[2], s));
     CK(launch_select(v, !v.use_edge_exchange, s));
     CK(cudaEventRecord(ev[3], s));
@@ -632,6 +659,9 @@ void dpso_destroy(dpso_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->graph) cudaGraphExecDestroy(c->graph);
   if (c->ev) cudaEventDestroy(c->ev);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->stream2) cudaStreamDestroy(c->stream2);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->host_ctl) cudaFreeHost(c->host_ctl);
   delete c;

@@ -121,6 +121,12 @@ struct SwarmView {
 cudaError_t launch_gen_begin(const SwarmView& v, cudaStream_t s);
 cudaError_t launch_update(const SwarmView& v, cudaStream_t s);
 cudaError_t launch_mutation(const SwarmView& v, cudaStream_t s);
+// the three parts of launch_mutation: the stream walk depends only on the
+// mutation stream and may run on a forked stream concurrently with the
+// update and launch_mutation_pre; launch_mutation_post must follow both.
+cudaError_t launch_mutation_walk(const SwarmView& v, cudaStream_t s);
+cudaError_t launch_mutation_pre(const SwarmView& v, cudaStream_t s);
+cudaError_t launch_mutation_post(const SwarmView& v, cudaStream_t s);
 cudaError_t launch_select(const SwarmView& v, bool finalize, cudaStream_t s);
 cudaError_t launch_two_opt(const SwarmView& v, cudaStream_t s, int parts = 3);
 cudaError_t launch_finalize(const SwarmView& v, cudaStream_t s);

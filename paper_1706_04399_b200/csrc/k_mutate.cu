@@ -1,22 +1,28 @@
 // Random mutation with elitism and canonical-form dedupe (solver.py:222-258).
 //
 // Pipeline (all kernels no-op unless ctl->mutating):
-//   k_mut_hash   per particle: canonical rotation/direction (graph.py:106-115)
-//                and a 64-bit order-dependent hash of the canonical sequence
-//   k_mut_rank   rank in (fitness, slot) order by counting (solver.py:223-224)
-//   k_mut_dedupe a particle is a dropped duplicate iff an earlier-ranked one
-//                has the same canonical form (hash match + exact compare)
-//   k_mut_lists  survivors / dropped in rank order, keep = first ceil(S/3)
-//                survivors, events = non-kept slots in slot order
-//   k_mut_copy   dropped #r copies body+fitness of survivors[r % S]
-//   k_mut_walk   chains k = integers(1, k_hi+1) through the single mutation
-//                stream to find where every event's draws start
-//   k_mut_sample one CTA per event: regenerate its draws (PCG64 jump-ahead),
-//                numpy's Floyd / tail-shuffle sampler, verify the draw count
-//   k_mut_fix    exact sequential re-walk from the first event that needed a
-//                Lemire redraw (rare), persistent stream state update
-//   k_mut_swap   k disjoint swaps, fitness in reference order, pbest
-//                (solver.py:241-258)
+//   k_mut_hash    per particle: canonical rotation/direction (graph.py:106-115)
+//                 and a 64-bit order-dependent hash of the canonical sequence
+//   k_mut_rank    rank in (fitness, slot) order by counting (solver.py:223-224)
+//   k_mut_dedupe  earliest-ranked particle with the same hash (candidate
+//                 duplicate source)
+//   k_mut_verify  one warp per candidate: exact canonical-form comparison
+//                 (a hash collision falls back to an exact search)
+//   k_mut_lists   survivors / dropped in rank order, keep = first ceil(S/3)
+//                 survivors, events = non-kept slots in slot order
+//   k_mut_copy    dropped #r copies body+fitness of survivors[r % S]
+//   k_mut_walk    chains k = integers(1, k_hi+1) through the single mutation
+//                 stream to find where every event's draws start.  The chain
+//                 depends only on the stream, not on the swarm, so it is
+//                 computed for all P potential events on a forked stream,
+//                 concurrently with update/hash/rank/dedupe/lists/copy
+//   k_mut_sample  one warp per event: regenerate its draws in parallel (PCG64
+//                 jump-ahead), check Lemire rejections in parallel, numpy's
+//                 Floyd sampler + shuffle (sequential, on precomputed values)
+//   k_mut_fix     exact sequential re-walk from the first event whose draws
+//                 needed a Lemire redraw (rare); persistent stream update
+//   k_mut_swap    k disjoint swaps, fitness in reference order, pbest
+//                 (solver.py:241-258)
 #include <algorithm>
 
 #include "dpso_internal.cuh"
@@ -92,27 +98,16 @@ __global__ void __launch_bounds__(256) k_mut_rank(SwarmView v) {
   }
 }
 
-__device__ bool canon_equal(const SwarmView& v, const int32_t* canon, int a,
-                            int b) {
-  const int n = v.n;
-  const uint16_t* ta = v.x + (size_t)a * v.np;
-  const uint16_t* tb = v.x + (size_t)b * v.np;
-  const int ka = canon[a] & 0x7fffffff, ra = (int)((uint32_t)canon[a] >> 31);
-  const int kb = canon[b] & 0x7fffffff, rb = (int)((uint32_t)canon[b] >> 31);
-  for (int m = 1; m < n; ++m)
-    if (canon_at(ta, n, ka, ra, m) != canon_at(tb, n, kb, rb, m)) return false;
-  return true;
-}
-
-__global__ void __launch_bounds__(256) k_mut_dedupe(SwarmView v,
-                                                    const int32_t* canon) {
+// Earliest-ranked particle with the same canonical hash and a lower rank
+// (-1: none) -> flag[i] holds that candidate + 1 until k_mut_verify.
+__global__ void __launch_bounds__(256) k_mut_dedupe(SwarmView v) {
   if (!v.ctl->mutating || v.ctl->done) return;
   __shared__ unsigned long long s_h[kTile];
   __shared__ int s_r[kTile];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t hi = i < v.P ? v.hash[i] : 0;
   const int ri = i < v.P ? v.rank[i] : 0;
-  int dropped = 0;
+  int cand = -1, crank = 0x7fffffff;
   for (int base = 0; base < v.P; base += kTile) {
     const int m = min(kTile, v.P - base);
     __syncthreads();
@@ -121,19 +116,54 @@ __global__ void __launch_bounds__(256) k_mut_dedupe(SwarmView v,
       s_r[u] = v.rank[base + u];
     }
     __syncthreads();
-    if (i < v.P && !dropped) {
+    if (i < v.P) {
       for (int u = 0; u < m; ++u) {
-        if (s_h[u] == hi && s_r[u] < ri) {
-          if (canon_equal(v, canon, i, base + u)) {
-            dropped = 1;
-            break;
-          }
-          v.ctl->collision = 1;
+        const int r = s_r[u];
+        if (s_h[u] == hi && r < ri && r < crank) {
+          crank = r;
+          cand = base + u;
         }
       }
     }
   }
-  if (i < v.P) v.flag[i] = dropped;
+  if (i < v.P) v.flag[i] = cand + 1;
+}
+
+__device__ bool warp_canon_equal(const SwarmView& v, const int32_t* canon,
+                                 int a, int b) {
+  const int n = v.n, lane = threadIdx.x & 31;
+  const uint16_t* ta = v.x + (size_t)a * v.np;
+  const uint16_t* tb = v.x + (size_t)b * v.np;
+  const int ka = canon[a] & 0x7fffffff, ra = (int)((uint32_t)canon[a] >> 31);
+  const int kb = canon[b] & 0x7fffffff, rb = (int)((uint32_t)canon[b] >> 31);
+  int diff = 0;
+  for (int m = 1 + lane; m < n; m += 32)
+    diff |= canon_at(ta, n, ka, ra, m) != canon_at(tb, n, kb, rb, m);
+  return !__any_sync(0xffffffffu, diff);
+}
+
+// One warp per particle: exact check of the hash candidate.  A particle is a
+// dropped duplicate iff an earlier-ranked particle has the same canonical
+// form (solver.py:227-233).  flag: 1 = dropped, 0 = survivor.
+__global__ void __launch_bounds__(128) k_mut_verify(SwarmView v,
+                                                    const int32_t* canon) {
+  if (!v.ctl->mutating || v.ctl->done) return;
+  const int i = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (i >= v.P) return;
+  const int cand = v.flag[i] - 1;
+  if (cand < 0) return;  // flag already 0
+  int dropped = warp_canon_equal(v, canon, i, cand);
+  if (!dropped) {
+    // 64-bit hash collision with a different tour: exact search over every
+    // earlier-ranked particle with the same hash (never seen in practice)
+    if ((threadIdx.x & 31) == 0) v.ctl->collision = 1;
+    const uint64_t hi = v.hash[i];
+    const int ri = v.rank[i];
+    for (int j = 0; j < v.P && !dropped; ++j)
+      if (j != cand && v.hash[j] == hi && v.rank[j] < ri)
+        dropped = warp_canon_equal(v, canon, i, j);
+  }
+  if ((threadIdx.x & 31) == 0) v.flag[i] = dropped;
 }
 
 template <int T>
@@ -225,14 +255,12 @@ __global__ void __launch_bounds__(128) k_mut_copy(SwarmView v) {
 // The mutation stream is ONE numpy PCG64 stream consumed in slot order, so
 // where event e's draws start depends on every earlier event's k.  The walk
 // is split: (1) k_mut_walk chains only the k-draws (one thread, reading a
-// shared-memory ring of the stream that the whole CTA refills by PCG jump-
-// ahead), assuming the Floyd/shuffle draws of each event need no Lemire
-// redraw; (2) k_mut_sample (one CTA per event) regenerates the event's draws
-// from its cursor, runs the exact numpy sampler and counts the u32 it
-// consumed - a mismatch means a redraw happened (probability ~1e-7 per draw
-// at n=1000); (3) k_mut_fix redoes the walk exactly and sequentially from the
-// first such event (rare path) and advances the persistent stream state;
-// (4) k_mut_swap applies the k disjoint swaps, fitness and pbest.
+// shared-memory ring of the stream that the whole CTA refills: every thread
+// holds the jump coefficients for its own offset, so a refill is one 128-bit
+// multiply-add per generated output), assuming the Floyd/shuffle draws of
+// each event need no Lemire redraw; (2) k_mut_sample verifies that
+// assumption per event; (3) k_mut_fix redoes the walk exactly and
+// sequentially from the first event that needed a redraw (rare path).
 
 constexpr int kWalk = 1024;          // threads
 constexpr int kRing = 16384;         // u32 in the ring (64 KiB dynamic smem)
@@ -254,6 +282,7 @@ __global__ void __launch_bounds__(kWalk) k_mut_walk(SwarmView v) {
   extern __shared__ __align__(16) uint32_t ring[];
   __shared__ int64_t s_q, s_wbase;
   __shared__ int s_e;
+  __shared__ uint64_t s_base[2];
   const int tid = threadIdx.x;
   const PcgState g = v.streams[1];
   if (tid == 0) {
@@ -266,19 +295,26 @@ __global__ void __launch_bounds__(kWalk) k_mut_walk(SwarmView v) {
   const int64_t h = (int64_t)g.has_uint32;
   const uint32_t ub = (uint32_t)g.uinteger;
   const u128 S0 = {g.state_hi, g.state_lo}, inc = {g.inc_hi, g.inc_lo};
-  u128 A, C;
+  u128 A, C, At, Ct;
   pcg_jump_coeffs(kWalk, inc, &A, &C);
+  pcg_jump_coeffs((uint64_t)tid, inc, &At, &Ct);
   const int n = v.n;
   const int k_hi = max(2, n / 4);
   const uint32_t rng_k = (uint32_t)(k_hi - 1);
-  const int E = v.ctl->n_events;
+  const int E = v.P;  // every potential event; k_mut_lists picks the first E
   __syncthreads();
   for (;;) {
     // refill so the ring starts at the chain position
     const int64_t f = s_q - h;
     if (f < 0 || f + 64 > s_wbase + kRing) {
       const int64_t wb = f < 0 ? 0 : (f & ~(int64_t)1);
-      u128 st = pcg_advance(S0, inc, (uint64_t)(wb / 2 + 1 + tid));
+      if (tid == 0) {
+        const u128 b = pcg_advance(S0, inc, (uint64_t)(wb / 2 + 1));
+        s_base[0] = b.hi;
+        s_base[1] = b.lo;
+      }
+      __syncthreads();
+      u128 st = add128(mul128(At, {s_base[0], s_base[1]}), Ct);
 #pragma unroll
       for (int r = 0; r < kOutPerThread; ++r) {
         const uint64_t o = pcg_output(st);
@@ -308,7 +344,6 @@ __global__ void __launch_bounds__(kWalk) k_mut_walk(SwarmView v) {
         v.ev_cursor[e] = (uint64_t)q;
         if (k >= 1) q += sample_draws(n, k);
         ++e;
-        if (q - h + 64 > wb + kRing) break;
       }
       s_q = q;
       s_e = e;
@@ -316,14 +351,13 @@ __global__ void __launch_bounds__(kWalk) k_mut_walk(SwarmView v) {
     __syncthreads();
     if (s_e >= E) break;
   }
-  if (tid == 0) v.ctl->mut_q = (uint64_t)s_q;
 }
 
-// Numpy's choice(n, 2k, replace=False) from stream position `cur`: writes
-// the 2k sampled positions to idx; returns the number of u32 consumed.
-__device__ int64_t sample_event(const PcgState& start, uint64_t cur, int n,
-                                int k, uint16_t* idx, uint32_t* bits,
-                                uint16_t* arr) {
+// Numpy's choice(n, 2k, replace=False) from stream position `cur`, one
+// thread: writes the 2k sampled positions to idx; returns the u32 consumed.
+__device__ int64_t sample_event_seq(const PcgState& start, uint64_t cur,
+                                    int n, int k, uint16_t* idx,
+                                    uint32_t* bits, uint16_t* arr) {
   struct Counting {
     Pcg r;
     int64_t q = 0;
@@ -373,37 +407,109 @@ __device__ int64_t sample_event(const PcgState& start, uint64_t cur, int n,
   return c.q;
 }
 
-__device__ void clear_scratch(int n, bool tail, uint32_t* bits,
-                              uint16_t* arr) {
-  if (tail) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) arr[i] = (uint16_t)i;
-  } else {
-    for (int i = threadIdx.x; i < (n + 31) / 32; i += blockDim.x) bits[i] = 0;
-  }
-}
+// One warp per event.  Shared memory per warp: draw values (u32, D+1) and
+// the n-bit Floyd bitmap (or arange(n) for the tail shuffle).
+constexpr int kSampleWarps = 4;
 
-__global__ void __launch_bounds__(128) k_mut_sample(SwarmView v) {
+__global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample(
+    SwarmView v, int vals_cap, int scratch_words) {
   if (!v.ctl->mutating || v.ctl->done) return;
-  const int e = blockIdx.x;
+  extern __shared__ __align__(16) uint32_t sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int e = blockIdx.x * (blockDim.x >> 5) + warp;
   if (e >= v.ctl->n_events) return;
   const int n = v.n, k = v.ev_k[e];
   if (k < 1) return;
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* bits = (uint32_t*)smem;
-  uint16_t* arr = (uint16_t*)smem;
-  const bool tail = (n > 10000) && 2 * k > n / 50;
-  clear_scratch(n, tail, bits, arr);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint16_t* idx = v.ev_idx + (size_t)e * v.np;
-    const int64_t used =
-        sample_event(*v.mut_start, v.ev_cursor[e], n, k, idx, bits, arr);
-    if (used != sample_draws(n, k)) atomicMin(&v.ctl->mut_bad, e);
+  uint32_t* vals = sm + (size_t)warp * (vals_cap + scratch_words);
+  uint32_t* bits = vals + vals_cap;
+  uint16_t* arr = (uint16_t*)bits;
+  uint16_t* idx = v.ev_idx + (size_t)e * v.np;
+  const int size = 2 * k;
+  const bool tail = (n > 10000) && size > n / 50;
+  const uint64_t cur = v.ev_cursor[e];
+  const int D = sample_draws(n, k);
+  if (tail || vals_cap == 0) {
+    // sequential sampler (tail shuffle, or n too large for a draw buffer)
+    if (tail) {
+      for (int i = lane; i < n; i += 32) arr[i] = (uint16_t)i;
+    } else {
+      for (int i = lane; i < (n + 31) / 32; i += 32) bits[i] = 0;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const int64_t used =
+          sample_event_seq(*v.mut_start, cur, n, k, idx, bits, arr);
+      if (used != D) atomicMin(&v.ctl->mut_bad, e);
+    }
+    return;
+  }
+  for (int i = lane; i < (n + 31) / 32; i += 32) bits[i] = 0;
+  // --- generate the event's D draws in parallel
+  const PcgState& g = *v.mut_start;
+  const int64_t h = (int64_t)g.has_uint32;
+  const u128 inc = {g.inc_hi, g.inc_lo};
+  // fresh index of the first draw; outputs counted from 1
+  const int64_t f0 = (int64_t)cur - h;  // >= 0: the k draw precedes cur
+  const int64_t m0 = f0 / 2 + 1;
+  const int skip = (int)(f0 & 1);  // first draw is the high half of m0
+  const int nout = (skip + D + 1) / 2;
+  u128 Al, Cl, A32, C32;
+  pcg_jump_coeffs((uint64_t)lane, inc, &Al, &Cl);
+  pcg_jump_coeffs(32, inc, &A32, &C32);
+  u128 base = {0, 0};
+  if (lane == 0)
+    base = pcg_advance({g.state_hi, g.state_lo}, inc, (uint64_t)m0);
+  base.hi = __shfl_sync(0xffffffffu, base.hi, 0);
+  base.lo = __shfl_sync(0xffffffffu, base.lo, 0);
+  u128 st = add128(mul128(Al, base), Cl);
+  for (int o = lane; o < nout; o += 32) {
+    const uint64_t out = pcg_output(st);
+    const int d0 = 2 * o - skip;  // draw index of the low half
+    if (d0 >= 0 && d0 < D) vals[d0] = (uint32_t)out;
+    if (d0 + 1 >= 0 && d0 + 1 < D) vals[d0 + 1] = (uint32_t)(out >> 32);
+    st = add128(mul128(A32, st), C32);
+  }
+  __syncwarp();
+  // --- rejection check and bounded values, in parallel
+  const int jstart = max(n - size, 1);
+  const int F = n - jstart;
+  int rej = 0;
+  for (int d = lane; d < D; d += 32) {
+    const uint32_t rng = d < F ? (uint32_t)(jstart + d)
+                               : (uint32_t)(size - 1 - (d - F));
+    const uint32_t u = vals[d];
+    rej |= lemire_rejects(u, rng);
+    vals[d] = (uint32_t)(((uint64_t)u * (rng + 1u)) >> 32);
+  }
+  if (__any_sync(0xffffffffu, rej)) {
+    // a redraw shifts every later draw: flag for the exact re-walk
+    if (lane == 0) atomicMin(&v.ctl->mut_bad, e);
+    return;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    // Floyd: j = n - 2k .. n-1 (j == 0 takes no draw and yields 0)
+    int d = 0;
+    for (int t = 0; t < size; ++t) {
+      const uint32_t j = (uint32_t)(n - size + t);
+      uint32_t val = j == 0 ? 0u : vals[d++];
+      if (bits[val >> 5] & (1u << (val & 31))) val = j;
+      bits[val >> 5] |= 1u << (val & 31);
+      idx[t] = (uint16_t)val;
+    }
+    // shuffle (numpy _shuffle_int): i = size-1 .. 1
+    for (int i = size - 1; i >= 1; --i) {
+      const uint32_t j = vals[d++];
+      const uint16_t t = idx[i];
+      idx[i] = idx[j];
+      idx[j] = t;
+    }
   }
 }
 
 // Rare path + stream bookkeeping: exact sequential re-walk from the first
-// event whose sample needed a Lemire redraw.
+// event whose sample needed a Lemire redraw, then advance the persistent
+// stream past the last event actually used.
 __global__ void __launch_bounds__(32) k_mut_fix(SwarmView v) {
   if (!v.ctl->mutating || v.ctl->done) return;
   if (threadIdx.x != 0) return;
@@ -413,11 +519,10 @@ __global__ void __launch_bounds__(32) k_mut_fix(SwarmView v) {
   const int n = v.n;
   const int E = v.ctl->n_events;
   const int bad = v.ctl->mut_bad;
-  uint64_t q = v.ctl->mut_q;
+  uint64_t q = 0;
   if (bad < E) {
     const int k_hi = max(2, n / 4);
     const uint32_t rng_k = (uint32_t)(k_hi - 1);
-    q = 0;
     if (bad > 0) {
       // the previous event was verified, so its draws ended where the
       // speculative walk assumed
@@ -443,9 +548,12 @@ __global__ void __launch_bounds__(32) k_mut_fix(SwarmView v) {
       } else {
         for (int i = 0; i < (n + 31) / 32; ++i) bits[i] = 0;
       }
-      q += sample_event(*v.mut_start, q, n, k, v.ev_idx + (size_t)e * v.np,
-                        bits, arr);
+      q += sample_event_seq(*v.mut_start, q, n, k,
+                            v.ev_idx + (size_t)e * v.np, bits, arr);
     }
+  } else if (E > 0) {
+    const int kl = v.ev_k[E - 1];
+    q = v.ev_cursor[E - 1] + (kl >= 1 ? sample_draws(n, kl) : 0);
   }
   Pcg r;
   r.seek_u32(*v.mut_start, q);
@@ -497,28 +605,60 @@ __global__ void __launch_bounds__(128) k_mut_swap(SwarmView v) {
 
 }  // namespace
 
-cudaError_t launch_mutation(const SwarmView& v, cudaStream_t s) {
-  const int P = v.P;
-  // canon info lives in the ev_k array until the walk overwrites it
-  int32_t* canon = v.ev_k;
-  k_mut_hash<<<P, 128, 0, s>>>(v, canon);
-  k_mut_rank<<<(P + 255) / 256, 256, 0, s>>>(v);
-  k_mut_dedupe<<<(P + 255) / 256, 256, 0, s>>>(v, canon);
-  k_mut_lists<<<1, 1024, 0, s>>>(v);
-  k_mut_copy<<<P, 128, 0, s>>>(v);
+cudaError_t launch_mutation_walk(const SwarmView& v, cudaStream_t s) {
   const size_t ring = (size_t)kRing * 4;
   set_dyn_smem((const void*)k_mut_walk, ring);
   k_mut_walk<<<1, kWalk, ring, s>>>(v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mutation_pre(const SwarmView& v, cudaStream_t s) {
+  const int P = v.P;
+  // canon info (k | rev << 31) lives in the rank-order scratch `keep` until
+  // k_mut_lists rewrites it
+  int32_t* canon = v.keep;
+  k_mut_hash<<<P, 128, 0, s>>>(v, canon);
+  k_mut_rank<<<(P + 255) / 256, 256, 0, s>>>(v);
+  k_mut_dedupe<<<(P + 255) / 256, 256, 0, s>>>(v);
+  k_mut_verify<<<(P + 3) / 4, 128, 0, s>>>(v, canon);
+  k_mut_lists<<<1, 1024, 0, s>>>(v);
+  k_mut_copy<<<P, 128, 0, s>>>(v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mutation_post(const SwarmView& v, cudaStream_t s) {
+  const int P = v.P;
+  const int n = v.n;
+  // per warp: draw values (<= 2n + 1 u32) + Floyd bitmap / tail arange;
+  // without room for the draw buffer the warp samples sequentially
+  const int scratch_words =
+      (int)round_up(std::max<int64_t>((n + 31) / 32, (n + 1) / 2), 4);
+  int vals_cap = (int)round_up(2 * (int64_t)n + 2, 4);
+  constexpr size_t kBudget = 200 * 1024;
+  if ((size_t)(vals_cap + scratch_words) * 4 > kBudget) vals_cap = 0;
+  const size_t per_warp = (size_t)(vals_cap + scratch_words) * 4;
+  const int warps =
+      (int)std::max<size_t>(1, std::min<size_t>(kSampleWarps,
+                                                kBudget / per_warp));
+  const size_t smem = (size_t)warps * per_warp;
+  set_dyn_smem((const void*)k_mut_sample, smem);
+  k_mut_sample<<<(P + warps - 1) / warps, warps * 32, smem, s>>>(
+      v, vals_cap, scratch_words);
   const size_t scratch =
-      std::max<size_t>(round_up((v.n + 31) / 32 * 4, 16), 2 * (size_t)v.np);
-  set_dyn_smem((const void*)k_mut_sample, scratch);
+      std::max<size_t>(round_up((n + 31) / 32 * 4, 16), 2 * (size_t)v.np);
   set_dyn_smem((const void*)k_mut_fix, scratch);
-  k_mut_sample<<<P, 128, scratch, s>>>(v);
   k_mut_fix<<<1, 32, scratch, s>>>(v);
   const size_t sd = (size_t)8 * v.np;
   set_dyn_smem((const void*)k_mut_swap, sd);
   k_mut_swap<<<P, 128, sd, s>>>(v);
   return cudaGetLastError();
+}
+
+cudaError_t launch_mutation(const SwarmView& v, cudaStream_t s) {
+  cudaError_t e = launch_mutation_walk(v, s);
+  if (!e) e = launch_mutation_pre(v, s);
+  if (!e) e = launch_mutation_post(v, s);
+  return e;
 }
 
 }  // namespace dpso
