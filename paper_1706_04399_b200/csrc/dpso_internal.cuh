@@ -113,7 +113,9 @@ struct SwarmView {
   int32_t* ev_slot;
   int32_t* ev_k;
   uint64_t* ev_cursor;
+  uint64_t* ev_end;     // stream position after each event's draws
   uint16_t* ev_idx;    // P x np sampled positions per mutation event
+  uint32_t* walk_ring; // global ring for the stream walk (large n only)
   uint64_t* init_cursor;
 };
 
@@ -125,6 +127,7 @@ cudaError_t launch_mutation(const SwarmView& v, cudaStream_t s);
 // mutation stream and may run on a forked stream concurrently with the
 // update and launch_mutation_pre; launch_mutation_post must follow both.
 cudaError_t launch_mutation_walk(const SwarmView& v, cudaStream_t s);
+int64_t walk_ring_bytes(int n);
 cudaError_t launch_mutation_pre(const SwarmView& v, cudaStream_t s);
 cudaError_t launch_mutation_post(const SwarmView& v, cudaStream_t s);
 cudaError_t launch_select(const SwarmView& v, bool finalize, cudaStream_t s);

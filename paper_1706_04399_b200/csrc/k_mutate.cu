@@ -263,8 +263,7 @@ __global__ void __launch_bounds__(128) k_mut_copy(SwarmView v) {
 // sequentially from the first event that needed a redraw (rare path).
 
 constexpr int kWalk = 1024;          // threads
-constexpr int kRing = 16384;         // u32 in the ring (64 KiB dynamic smem)
-constexpr int kOutPerThread = kRing / 2 / kWalk;
+constexpr int kRingSmem = 16384;     // u32 ring in shared memory (64 KiB)
 
 // number of Floyd + shuffle draws of choice(n, 2k, replace=False) when no
 // Lemire redraw happens (numpy _generator.pyx: Floyd skips j == 0; n > 10000
@@ -277,12 +276,37 @@ __device__ __forceinline__ int sample_draws(int n, int k) {
   return F + size - 1;
 }
 
+__device__ __forceinline__ uint32_t sample_bound(int n, int k, int d) {
+  const int size = 2 * k;
+  const int jstart = max(n - size, 1);
+  const int F = n - jstart;
+  if (n > 10000 && size > n / 50) return (uint32_t)(n - 1 - d);  // tail
+  return d < F ? (uint32_t)(jstart + d) : (uint32_t)(size - 1 - (d - F));
+}
+
+constexpr int kWinEvents = 256;  // events chained per ring window (max)
+
+// Ring size in u32 for n nodes: >= 4x the worst-case span of one event.
+__host__ __device__ inline int64_t walk_ring_size(int n) {
+  int64_t need = 4 * (64 + 2 * (int64_t)n);
+  int64_t r = kRingSmem;
+  while (r < need) r *= 2;
+  return r;
+}
+
 __global__ void __launch_bounds__(kWalk) k_mut_walk(SwarmView v) {
   if (!v.ctl->mutating || v.ctl->done) return;
-  extern __shared__ __align__(16) uint32_t ring[];
+  extern __shared__ __align__(16) uint32_t ring_smem[];
+  const int64_t kRing = walk_ring_size(v.n);
+  // large n: the ring lives in global memory (L2)
+  uint32_t* ring = kRing == kRingSmem ? ring_smem : v.walk_ring;
+  const int out_per_thread = (int)(kRing / 2 / kWalk);
   __shared__ int64_t s_q, s_wbase;
-  __shared__ int s_e;
+  __shared__ int s_e, s_e0;
   __shared__ uint64_t s_base[2];
+  __shared__ unsigned long long s_bad;  // (position << 16 | event offset)
+  __shared__ int s_ek[kWinEvents];
+  __shared__ int64_t s_ec[kWinEvents];
   const int tid = threadIdx.x;
   const PcgState g = v.streams[1];
   if (tid == 0) {
@@ -302,11 +326,15 @@ __global__ void __launch_bounds__(kWalk) k_mut_walk(SwarmView v) {
   const int k_hi = max(2, n / 4);
   const uint32_t rng_k = (uint32_t)(k_hi - 1);
   const int E = v.P;  // every potential event; k_mut_lists picks the first E
+  const int margin = 64 + sample_draws(n, n / 2);  // worst-case event span
   __syncthreads();
+  auto at = [&](int64_t q) -> uint32_t {
+    return q < h ? ub : ring[q - h - s_wbase];
+  };
   for (;;) {
     // refill so the ring starts at the chain position
     const int64_t f = s_q - h;
-    if (f < 0 || f + 64 > s_wbase + kRing) {
+    if (f < 0 || f + margin > s_wbase + kRing) {
       const int64_t wb = f < 0 ? 0 : (f & ~(int64_t)1);
       if (tid == 0) {
         const u128 b = pcg_advance(S0, inc, (uint64_t)(wb / 2 + 1));
@@ -315,8 +343,7 @@ __global__ void __launch_bounds__(kWalk) k_mut_walk(SwarmView v) {
       }
       __syncthreads();
       u128 st = add128(mul128(At, {s_base[0], s_base[1]}), Ct);
-#pragma unroll
-      for (int r = 0; r < kOutPerThread; ++r) {
+      for (int r = 0; r < out_per_thread; ++r) {
         const uint64_t o = pcg_output(st);
         const int idx = 2 * (tid + kWalk * r);
         ring[idx] = (uint32_t)o;
@@ -327,26 +354,82 @@ __global__ void __launch_bounds__(kWalk) k_mut_walk(SwarmView v) {
       if (tid == 0) s_wbase = wb;
       __syncthreads();
     }
+    // (1) chain k-draws of the events whose whole draw span is in the ring
     if (tid == 0) {
       int64_t q = s_q;
       int e = s_e;
-      const int64_t wb = s_wbase;
-      while (e < E) {
-        if (q - h + 64 > wb + kRing) break;  // k-draw (+redraws) in ring
+      s_e0 = e;
+      while (e < E && e - s_e0 < kWinEvents) {
+        if (q - h + margin > s_wbase + kRing) break;
         uint32_t u;
         do {
-          u = q < h ? ub : ring[q - h - wb];
+          u = at(q);
           ++q;
         } while (lemire_rejects(u, rng_k));
         const int kraw = (int)(((uint64_t)u * (rng_k + 1u)) >> 32) + 1;
         const int k = min(kraw, n / 2);
-        v.ev_k[e] = k;
-        v.ev_cursor[e] = (uint64_t)q;
+        s_ek[e - s_e0] = k;
+        s_ec[e - s_e0] = q;
         if (k >= 1) q += sample_draws(n, k);
         ++e;
       }
       s_q = q;
       s_e = e;
+      s_bad = ~0ull;
+    }
+    __syncthreads();
+    // (2) every draw of those events checked for a Lemire redraw, in parallel
+    const int e0 = s_e0, ne = s_e - s_e0;
+    for (int w = 0; w < ne; ++w) {
+      const int k = s_ek[w];
+      if (k < 1) continue;
+      const int D = sample_draws(n, k);
+      const int64_t c0 = s_ec[w];
+      for (int d = tid; d < D; d += kWalk)
+        if (lemire_rejects(at(c0 + d), sample_bound(n, k, d)))
+          atomicMin(&s_bad, ((unsigned long long)(c0 + d) << 16) | w);
+    }
+    __syncthreads();
+    // (3) commit up to the first event with a redraw, which thread 0
+    //     consumes exactly (redraws stay inside the ring margin)
+    if (tid == 0) {
+      int upto = ne;
+      if (s_bad != ~0ull) upto = (int)(s_bad & 0xFFFF);
+      for (int w = 0; w < upto; ++w) {
+        const int k = s_ek[w];
+        v.ev_k[e0 + w] = k;
+        v.ev_cursor[e0 + w] = (uint64_t)s_ec[w];
+        v.ev_end[e0 + w] = (uint64_t)(s_ec[w] + (k >= 1 ? sample_draws(n, k) : 0));
+      }
+      if (upto < ne) {
+        const int w = upto, k = s_ek[w];
+        int64_t q = s_ec[w];
+        const int D = sample_draws(n, k);
+        bool ok = true;
+        for (int d = 0; d < D && ok; ++d) {
+          const uint32_t rng = sample_bound(n, k, d);
+          if (rng == 0) continue;
+          for (;;) {
+            if (q - h - s_wbase >= kRing) {
+              ok = false;  // redraw run beyond the ring: exact re-walk
+              break;
+            }
+            if (!lemire_rejects(at(q), rng)) break;
+            ++q;
+          }
+          ++q;
+        }
+        if (ok) {
+          v.ev_k[e0 + w] = k;
+          v.ev_cursor[e0 + w] = (uint64_t)s_ec[w];
+          v.ev_end[e0 + w] = (uint64_t)q;
+          s_q = q;
+          s_e = e0 + w + 1;
+        } else {
+          v.ctl->mut_bad = e0 + w;  // k_mut_fix redoes events >= w exactly
+          s_e = E;
+        }
+      }
     }
     __syncthreads();
     if (s_e >= E) break;
@@ -436,11 +519,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample(
       for (int i = lane; i < (n + 31) / 32; i += 32) bits[i] = 0;
     }
     __syncwarp();
-    if (lane == 0) {
-      const int64_t used =
-          sample_event_seq(*v.mut_start, cur, n, k, idx, bits, arr);
-      if (used != D) atomicMin(&v.ctl->mut_bad, e);
-    }
+    if (lane == 0) sample_event_seq(*v.mut_start, cur, n, k, idx, bits, arr);
     return;
   }
   for (int i = lane; i < (n + 31) / 32; i += 32) bits[i] = 0;
@@ -482,8 +561,13 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample(
     vals[d] = (uint32_t)(((uint64_t)u * (rng + 1u)) >> 32);
   }
   if (__any_sync(0xffffffffu, rej)) {
-    // a redraw shifts every later draw: flag for the exact re-walk
-    if (lane == 0) atomicMin(&v.ctl->mut_bad, e);
+    // this event holds a Lemire redraw (the walk accounted for it): sample
+    // it exactly, sequentially
+    __syncwarp();
+    if (lane == 0) {
+      for (int i = 0; i < (n + 31) / 32; ++i) bits[i] = 0;
+      sample_event_seq(*v.mut_start, cur, n, k, idx, bits, arr);
+    }
     return;
   }
   __syncwarp();
@@ -508,8 +592,8 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample(
 }
 
 // Rare path + stream bookkeeping: exact sequential re-walk from the first
-// event whose sample needed a Lemire redraw, then advance the persistent
-// stream past the last event actually used.
+// event the walk could not resolve (a redraw run beyond the ring margin,
+// never seen), then advance the persistent stream past the last event used.
 __global__ void __launch_bounds__(32) k_mut_fix(SwarmView v) {
   if (!v.ctl->mutating || v.ctl->done) return;
   if (threadIdx.x != 0) return;
@@ -523,12 +607,7 @@ __global__ void __launch_bounds__(32) k_mut_fix(SwarmView v) {
   if (bad < E) {
     const int k_hi = max(2, n / 4);
     const uint32_t rng_k = (uint32_t)(k_hi - 1);
-    if (bad > 0) {
-      // the previous event was verified, so its draws ended where the
-      // speculative walk assumed
-      const int kp = v.ev_k[bad - 1];
-      q = v.ev_cursor[bad - 1] + (kp >= 1 ? sample_draws(n, kp) : 0);
-    }
+    if (bad > 0) q = v.ev_end[bad - 1];
     for (int e = bad; e < E; ++e) {
       Pcg r;
       r.seek_u32(*v.mut_start, q);
@@ -552,8 +631,7 @@ __global__ void __launch_bounds__(32) k_mut_fix(SwarmView v) {
                             v.ev_idx + (size_t)e * v.np, bits, arr);
     }
   } else if (E > 0) {
-    const int kl = v.ev_k[E - 1];
-    q = v.ev_cursor[E - 1] + (kl >= 1 ? sample_draws(n, kl) : 0);
+    q = v.ev_end[E - 1];
   }
   Pcg r;
   r.seek_u32(*v.mut_start, q);
@@ -605,8 +683,13 @@ __global__ void __launch_bounds__(128) k_mut_swap(SwarmView v) {
 
 }  // namespace
 
+int64_t walk_ring_bytes(int n) {
+  const int64_t r = walk_ring_size(n);
+  return r == kRingSmem ? 0 : 4 * r;  // global ring only when smem is short
+}
+
 cudaError_t launch_mutation_walk(const SwarmView& v, cudaStream_t s) {
-  const size_t ring = (size_t)kRing * 4;
+  const size_t ring = (size_t)kRingSmem * 4;
   set_dyn_smem((const void*)k_mut_walk, ring);
   k_mut_walk<<<1, kWalk, ring, s>>>(v);
   return cudaGetLastError();

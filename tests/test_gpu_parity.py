@@ -121,6 +121,14 @@ def test_nn_two_opt_golden(pkg, golden_kernels):
 
 
 @pytest.mark.parametrize("n,P,G,kw", [
+    # random_state 2923: the first mutation call's event 5 needs a Lemire
+    # redraw (found by scanning seeds with oracle/np_random.py) -> exercises
+    # the walk's redraw handling and the sampler's exact fallback
+    (1000, 30, 3, {"mutation_period": 1, "use_edge_exchange": False,
+                   "random_state": 2923}),
+    (1000, 30, 2, {"mutation_period": 1, "random_state": 6395}),
+    # n = 3000: the stream-walk ring no longer fits shared memory
+    (3000, 8, 3, {"mutation_period": 1, "use_edge_exchange": False}),
     (40, 30, 25, {}),
     (40, 30, 25, {"mutation_period": 1}),
     (97, 24, 12, {"inertia": 0.5}),
@@ -133,7 +141,8 @@ def test_per_generation_state_matches_oracle(pkg, n, P, G, kw):
     cost = random_euclidean_matrix(n, np.random.default_rng(n))
     seed = list(range(n)) + [0]
     params = dict(n_particles=P, max_generations=G, stall_generations=G,
-                  random_state=n + P, seed_tour=seed, **kw)
+                  random_state=n + P, seed_tour=seed)
+    params.update(kw)
     orc = O.OracleSolver(**params)
     trace = []
     orc.fit(cost, trace=trace)
