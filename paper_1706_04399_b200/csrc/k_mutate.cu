@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(128) k_mut_copy(SwarmView v) {
 // sequentially from the first event that needed a redraw (rare path).
 
 constexpr int kWalk = 1024;          // threads
-constexpr int kRingSmem = 16384;     // u32 ring in shared memory (64 KiB)
+constexpr int kRingSmem = 32768;     // u32 ring in shared memory (128 KiB)
 
 // number of Floyd + shuffle draws of choice(n, 2k, replace=False) when no
 // Lemire redraw happens (numpy _generator.pyx: Floyd skips j == 0; n > 10000
@@ -378,29 +378,39 @@ __global__ void __launch_bounds__(kWalk) k_mut_walk(SwarmView v) {
       s_bad = ~0ull;
     }
     __syncthreads();
-    // (2) every draw of those events checked for a Lemire redraw, in parallel
+    // (2) every draw of those events checked for a Lemire redraw: warp w
+    //     checks events w, w + 32, ... with its 32 lanes
     const int e0 = s_e0, ne = s_e - s_e0;
-    for (int w = 0; w < ne; ++w) {
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int w = warp; w < ne; w += kWalk / 32) {
       const int k = s_ek[w];
       if (k < 1) continue;
       const int D = sample_draws(n, k);
       const int64_t c0 = s_ec[w];
-      for (int d = tid; d < D; d += kWalk)
-        if (lemire_rejects(at(c0 + d), sample_bound(n, k, d)))
-          atomicMin(&s_bad, ((unsigned long long)(c0 + d) << 16) | w);
+      int bad = 0x7fffffff;
+      for (int d = lane; d < D; d += 32)
+        if (bad == 0x7fffffff &&
+            lemire_rejects(at(c0 + d), sample_bound(n, k, d)))
+          bad = d;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+        bad = min(bad, __shfl_xor_sync(0xffffffffu, bad, o));
+      if (lane == 0 && bad != 0x7fffffff)
+        atomicMin(&s_bad, ((unsigned long long)(c0 + bad) << 16) | w);
     }
     __syncthreads();
-    // (3) commit up to the first event with a redraw, which thread 0
-    //     consumes exactly (redraws stay inside the ring margin)
+    // (3) commit every event before the first one with a redraw (all warps),
+    //     then thread 0 consumes that event exactly (redraws stay inside the
+    //     ring margin) and the chain resumes after it
+    const int upto = s_bad == ~0ull ? ne : (int)(s_bad & 0xFFFF);
+    for (int w = tid; w < upto; w += kWalk) {
+      const int k = s_ek[w];
+      v.ev_k[e0 + w] = k;
+      v.ev_cursor[e0 + w] = (uint64_t)s_ec[w];
+      v.ev_end[e0 + w] =
+          (uint64_t)(s_ec[w] + (k >= 1 ? sample_draws(n, k) : 0));
+    }
     if (tid == 0) {
-      int upto = ne;
-      if (s_bad != ~0ull) upto = (int)(s_bad & 0xFFFF);
-      for (int w = 0; w < upto; ++w) {
-        const int k = s_ek[w];
-        v.ev_k[e0 + w] = k;
-        v.ev_cursor[e0 + w] = (uint64_t)s_ec[w];
-        v.ev_end[e0 + w] = (uint64_t)(s_ec[w] + (k >= 1 ? sample_draws(n, k) : 0));
-      }
       if (upto < ne) {
         const int w = upto, k = s_ek[w];
         int64_t q = s_ec[w];
