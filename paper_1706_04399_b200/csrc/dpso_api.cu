@@ -58,7 +58,7 @@ struct Layout {
       off_vel, off_vel_len, off_fit, off_pfit, off_dcache, off_gbest,
       off_conv, off_tores, off_chunk_row, off_rank, off_hash, off_flag,
       off_sidx, off_order, off_surv, off_keep, off_ev_slot, off_ev_k,
-      off_ev_cursor, off_ev_end, off_ev_idx, off_walk_ring, off_init_cursor, off_seed, off_cost32,
+      off_ev_cursor, off_ev_end, off_ev_idx, off_mstream, off_init_cursor, off_seed, off_cost32,
       off_stats, total;
   int64_t vel_cap;
   int chunks;
@@ -110,7 +110,7 @@ Layout make_layout(const dpso_params* prm, int n) {
   L.off_ev_cursor = take(8 * P);
   L.off_ev_end = take(8 * P);
   L.off_ev_idx = take(2 * P * np);
-  L.off_walk_ring = take(prm->use_mutation ? walk_ring_bytes(n) : 0);
+  L.off_mstream = take(prm->use_mutation ? 4 * mstream_words(n, P) : 0);
   L.off_init_cursor = take(8 * P);
   L.off_seed = take(2 * np);
   L.off_cost32 = take(prm->use_edge_exchange ? 4 * (int64_t)n * np : 0);
@@ -300,7 +300,8 @@ int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
   v.ev_cursor = (uint64_t*)(w + L.off_ev_cursor);
   v.ev_end = (uint64_t*)(w + L.off_ev_end);
   v.ev_idx = (uint16_t*)(w + L.off_ev_idx);
-  v.walk_ring = (uint32_t*)(w + L.off_walk_ring);
+  v.mstream = (uint32_t*)(w + L.off_mstream);
+  v.mstream_cap = prm->use_mutation ? mstream_words(n, v.P) : 0;
   v.init_cursor = (uint64_t*)(w + L.off_init_cursor);
   std::vector<int32_t> rows(L.chunks + 1);
   two_opt_chunk_rows(n, L.chunks, rows.data());

@@ -45,7 +45,9 @@ struct DevCtl {
   int32_t vel_overflow;
   int32_t two_opt_count;  // generations in which the 2-opt pass ran
   int32_t mut_bad;        // first event whose sample needed a redraw
-  int32_t pad_;
+  int32_t mut_round;      // last stream-walk round run this call
+  int32_t mut_from;       // first event of that round
+  int32_t mut_overflow;   // stream buffer too short (exact fallback)
   uint64_t mut_q;     // u32 draws consumed by the current mutation call
 };
 
@@ -115,7 +117,8 @@ struct SwarmView {
   uint64_t* ev_cursor;
   uint64_t* ev_end;     // stream position after each event's draws
   uint16_t* ev_idx;    // P x np sampled positions per mutation event
-  uint32_t* walk_ring; // global ring for the stream walk (large n only)
+  uint32_t* mstream;   // generated mutation-stream span (u32)
+  int64_t mstream_cap; // u32 capacity of mstream
   uint64_t* init_cursor;
 };
 
@@ -127,7 +130,7 @@ cudaError_t launch_mutation(const SwarmView& v, cudaStream_t s);
 // mutation stream and may run on a forked stream concurrently with the
 // update and launch_mutation_pre; launch_mutation_post must follow both.
 cudaError_t launch_mutation_walk(const SwarmView& v, cudaStream_t s);
-int64_t walk_ring_bytes(int n);
+int64_t mstream_words(int n, int P);
 cudaError_t launch_mutation_pre(const SwarmView& v, cudaStream_t s);
 cudaError_t launch_mutation_post(const SwarmView& v, cudaStream_t s);
 cudaError_t launch_select(const SwarmView& v, bool finalize, cudaStream_t s);

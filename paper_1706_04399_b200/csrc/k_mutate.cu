@@ -11,21 +11,14 @@
 //   k_mut_lists   survivors / dropped in rank order, keep = first ceil(S/3)
 //                 survivors, events = non-kept slots in slot order
 //   k_mut_copy    dropped #r copies body+fitness of survivors[r % S]
-//   k_mut_walk    chains k = integers(1, k_hi+1) through the single mutation
-//                 stream to find where every event's draws start.  The chain
-//                 depends only on the stream, not on the swarm, so it is
-//                 computed for all P potential events on a forked stream,
-//                 concurrently with update/hash/rank/dedupe/lists/copy
-//   k_mut_sample  one warp per event: regenerate its draws in parallel (PCG64
-//                 jump-ahead), check Lemire rejections in parallel, numpy's
-//                 Floyd sampler + shuffle (sequential, on precomputed values)
-//   k_mut_fix     exact sequential re-walk from the first event whose draws
-//                 needed a Lemire redraw (rare); persistent stream update
+//   k_mut_gen/k_mut_walk/k_mut_sample/k_mut_fix: the mutation stream (see
+//                 the section comment below)
 //   k_mut_swap    k disjoint swaps, fitness in reference order, pbest
 //                 (solver.py:241-258)
 #include <algorithm>
 
 #include "dpso_internal.cuh"
+#include "tma.cuh"
 
 namespace dpso {
 
@@ -250,27 +243,38 @@ __global__ void __launch_bounds__(128) k_mut_copy(SwarmView v) {
   if (threadIdx.x == 0) v.fit[p] = v.fit[src];
 }
 
-// ---- the sequential stream walk ------------------------------------------
+// ---- the mutation stream ----------------------------------------------------
 //
 // The mutation stream is ONE numpy PCG64 stream consumed in slot order, so
-// where event e's draws start depends on every earlier event's k.  The walk
-// is split: (1) k_mut_walk chains only the k-draws (one thread, reading a
-// shared-memory ring of the stream that the whole CTA refills: every thread
-// holds the jump coefficients for its own offset, so a refill is one 128-bit
-// multiply-add per generated output), assuming the Floyd/shuffle draws of
-// each event need no Lemire redraw; (2) k_mut_sample verifies that
-// assumption per event; (3) k_mut_fix redoes the walk exactly and
-// sequentially from the first event that needed a redraw (rare path).
+// where event e's draws start depends on every earlier event's k.  Steps:
+//   k_mut_gen     (grid-wide) writes the span of the stream this call can
+//                 use into an L2-resident buffer (fresh u32 index f ->
+//                 mstream[f]); every thread jumps to its own chunk.
+//   k_mut_walk    one thread chains the k-draws for all P potential events
+//                 through an 8-slot shared-memory ring of 16 KiB stream
+//                 segments fed by cp.async.bulk, assuming the events'
+//                 Floyd/shuffle draws need no Lemire redraw.  It only needs the
+//                 stream, so it runs on a forked stream concurrently with the
+//                 update and the dedupe pipeline.
+//   k_mut_sample  one warp per event reads its draws from the buffer, checks
+//                 them for redraws in parallel and runs numpy's Floyd sampler
+//                 + shuffle; an event that does contain a redraw is sampled
+//                 exactly (sequentially), its true end recorded, and the first
+//                 such event flagged.
+//   rounds 1, 2   k_mut_walk/k_mut_sample again from the event after the
+//                 flagged one (no-ops when nothing was flagged).
+//   k_mut_fix     exact sequential fallback after two flagged rounds (never
+//                 seen) and the persistent stream update.
 
-constexpr int kWalk = 1024;          // threads
-constexpr int kRingSmem = 32768;     // u32 ring in shared memory (128 KiB)
+constexpr int kSeg = 4096;   // u32 per ring segment (16 KiB)
+constexpr int kNSeg = 8;     // ring slots (128 KiB)
 
 // number of Floyd + shuffle draws of choice(n, 2k, replace=False) when no
 // Lemire redraw happens (numpy _generator.pyx: Floyd skips j == 0; n > 10000
 // with 2k > n // 50 uses the tail shuffle instead)
-__device__ __forceinline__ int sample_draws(int n, int k) {
+__host__ __device__ __forceinline__ int sample_draws(int n, int k) {
   const int size = 2 * k;
-  const int jstart = max(n - size, 1);
+  const int jstart = n - size > 1 ? n - size : 1;
   const int F = n - jstart;
   if (n > 10000 && size > n / 50) return F;
   return F + size - 1;
@@ -284,196 +288,147 @@ __device__ __forceinline__ uint32_t sample_bound(int n, int k, int d) {
   return d < F ? (uint32_t)(jstart + d) : (uint32_t)(size - 1 - (d - F));
 }
 
-constexpr int kWinEvents = 256;  // events chained per ring window (max)
+constexpr int kGenPer = 64;  // outputs per k_mut_gen thread
 
-// Ring size in u32 for n nodes: >= 4x the worst-case span of one event.
-__host__ __device__ inline int64_t walk_ring_size(int n) {
-  int64_t need = 4 * (64 + 2 * (int64_t)n);
-  int64_t r = kRingSmem;
-  while (r < need) r *= 2;
-  return r;
+__global__ void __launch_bounds__(256) k_mut_gen(SwarmView v) {
+  if (!v.ctl->mutating || v.ctl->done) return;
+  const PcgState g = v.streams[1];
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c == 0) {
+    *v.mut_start = g;
+    v.ctl->mut_bad = 0x7fffffff;
+    v.ctl->mut_round = 0;
+    v.ctl->mut_from = 0;
+  }
+  const int64_t outs = v.mstream_cap / 2;
+  const int64_t o0 = c * kGenPer;
+  if (o0 >= outs) return;
+  const u128 inc = {g.inc_hi, g.inc_lo};
+  u128 st = pcg_advance({g.state_hi, g.state_lo}, inc, (uint64_t)o0 + 1);
+  const u128 M = pcg_mult();
+  uint2* out = reinterpret_cast<uint2*>(v.mstream);
+  for (int r = 0; r < kGenPer && o0 + r < outs; ++r) {
+    const uint64_t o = pcg_output(st);
+    out[o0 + r] = make_uint2((uint32_t)o, (uint32_t)(o >> 32));
+    st = add128(mul128(st, M), inc);
+  }
 }
 
-__global__ void __launch_bounds__(kWalk) k_mut_walk(SwarmView v) {
-  if (!v.ctl->mutating || v.ctl->done) return;
-  extern __shared__ __align__(16) uint32_t ring_smem[];
-  const int64_t kRing = walk_ring_size(v.n);
-  // large n: the ring lives in global memory (L2)
-  uint32_t* ring = kRing == kRingSmem ? ring_smem : v.walk_ring;
-  const int out_per_thread = (int)(kRing / 2 / kWalk);
-  __shared__ int64_t s_q, s_wbase;
-  __shared__ int s_e, s_e0;
-  __shared__ uint64_t s_base[2];
-  __shared__ unsigned long long s_bad;  // (position << 16 | event offset)
-  __shared__ int s_ek[kWinEvents];
-  __shared__ int64_t s_ec[kWinEvents];
-  const int tid = threadIdx.x;
-  const PcgState g = v.streams[1];
-  if (tid == 0) {
-    *v.mut_start = g;
-    s_q = 0;
-    s_e = 0;
-    s_wbase = -(int64_t)kRing;  // force a fill
-    v.ctl->mut_bad = 0x7fffffff;
+// The stream as seen from a thread: u32 at position q (counting next32()
+// calls from the call's start, so q = 0 may be numpy's buffered half).
+struct StreamView {
+  const uint32_t* buf;
+  int64_t h, cap;
+  uint32_t ub;
+  __device__ __forceinline__ uint32_t at(int64_t q) const {
+    return q < h ? ub : buf[q - h];
   }
-  const int64_t h = (int64_t)g.has_uint32;
-  const uint32_t ub = (uint32_t)g.uinteger;
-  const u128 S0 = {g.state_hi, g.state_lo}, inc = {g.inc_hi, g.inc_lo};
-  u128 A, C, At, Ct;
-  pcg_jump_coeffs(kWalk, inc, &A, &C);
-  pcg_jump_coeffs((uint64_t)tid, inc, &At, &Ct);
+};
+
+// Chain of k-draws from (e0, q0) for events e0..e_end-1, one thread, ring of
+// stream segments in shared memory.  Returns false on buffer overflow.
+__device__ bool chain_events(const SwarmView& v, StreamView sv, int e0,
+                             int64_t q0, int e_end, uint32_t* ring,
+                             uint64_t* bars) {
   const int n = v.n;
   const int k_hi = max(2, n / 4);
   const uint32_t rng_k = (uint32_t)(k_hi - 1);
-  const int E = v.P;  // every potential event; k_mut_lists picks the first E
-  const int margin = 64 + sample_draws(n, n / 2);  // worst-case event span
-  __syncthreads();
-  auto at = [&](int64_t q) -> uint32_t {
-    return q < h ? ub : ring[q - h - s_wbase];
+  const int64_t nseg_total = (sv.cap + kSeg - 1) / kSeg;
+  const int64_t f0 = q0 - sv.h < 0 ? 0 : q0 - sv.h;
+  const int64_t s_first = f0 / kSeg;
+  int64_t next_issue = s_first;
+  for (int b = 0; b < kNSeg; ++b) mbar_init(&bars[b], 1);
+  fence_barrier_init();
+  auto issue = [&]() {
+    if (next_issue < nseg_total) {
+      const int slot = (int)(next_issue % kNSeg);
+      mbar_expect_tx(&bars[slot], kSeg * 4);
+      bulk_g2s(ring + (size_t)slot * kSeg, sv.buf + next_issue * kSeg,
+               kSeg * 4, &bars[slot]);
+    }
+    ++next_issue;
   };
-  for (;;) {
-    // refill so the ring starts at the chain position
-    const int64_t f = s_q - h;
-    if (f < 0 || f + margin > s_wbase + kRing) {
-      const int64_t wb = f < 0 ? 0 : (f & ~(int64_t)1);
-      if (tid == 0) {
-        const u128 b = pcg_advance(S0, inc, (uint64_t)(wb / 2 + 1));
-        s_base[0] = b.hi;
-        s_base[1] = b.lo;
-      }
-      __syncthreads();
-      u128 st = add128(mul128(At, {s_base[0], s_base[1]}), Ct);
-      for (int r = 0; r < out_per_thread; ++r) {
-        const uint64_t o = pcg_output(st);
-        const int idx = 2 * (tid + kWalk * r);
-        ring[idx] = (uint32_t)o;
-        ring[idx + 1] = (uint32_t)(o >> 32);
-        st = add128(mul128(A, st), C);
-      }
-      __syncthreads();
-      if (tid == 0) s_wbase = wb;
-      __syncthreads();
+  for (int b = 0; b < kNSeg; ++b) issue();
+  auto get = [&](int64_t q, uint32_t* out) -> bool {
+    if (q < sv.h) {
+      *out = sv.ub;
+      return true;
     }
-    // (1) chain k-draws of the events whose whole draw span is in the ring
-    if (tid == 0) {
-      int64_t q = s_q;
-      int e = s_e;
-      s_e0 = e;
-      while (e < E && e - s_e0 < kWinEvents) {
-        if (q - h + margin > s_wbase + kRing) break;
-        uint32_t u;
-        do {
-          u = at(q);
-          ++q;
-        } while (lemire_rejects(u, rng_k));
-        const int kraw = (int)(((uint64_t)u * (rng_k + 1u)) >> 32) + 1;
-        const int k = min(kraw, n / 2);
-        s_ek[e - s_e0] = k;
-        s_ec[e - s_e0] = q;
-        if (k >= 1) q += sample_draws(n, k);
-        ++e;
-      }
-      s_q = q;
-      s_e = e;
-      s_bad = ~0ull;
+    const int64_t f = q - sv.h;
+    const int64_t s = f / kSeg;
+    if (s >= nseg_total) return false;
+    while (s >= next_issue) {  // slide: the chain never looks back
+      fence_proxy_async();
+      issue();
     }
-    __syncthreads();
-    // (2) every draw of those events checked for a Lemire redraw: warp w
-    //     checks events w, w + 32, ... with its 32 lanes
-    const int e0 = s_e0, ne = s_e - s_e0;
-    const int lane = tid & 31, warp = tid >> 5;
-    for (int w = warp; w < ne; w += kWalk / 32) {
-      const int k = s_ek[w];
-      if (k < 1) continue;
-      const int D = sample_draws(n, k);
-      const int64_t c0 = s_ec[w];
-      int bad = 0x7fffffff;
-      for (int d = lane; d < D; d += 32)
-        if (bad == 0x7fffffff &&
-            lemire_rejects(at(c0 + d), sample_bound(n, k, d)))
-          bad = d;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-        bad = min(bad, __shfl_xor_sync(0xffffffffu, bad, o));
-      if (lane == 0 && bad != 0x7fffffff)
-        atomicMin(&s_bad, ((unsigned long long)(c0 + bad) << 16) | w);
-    }
-    __syncthreads();
-    // (3) commit every event before the first one with a redraw (all warps),
-    //     then thread 0 consumes that event exactly (redraws stay inside the
-    //     ring margin) and the chain resumes after it
-    const int upto = s_bad == ~0ull ? ne : (int)(s_bad & 0xFFFF);
-    for (int w = tid; w < upto; w += kWalk) {
-      const int k = s_ek[w];
-      v.ev_k[e0 + w] = k;
-      v.ev_cursor[e0 + w] = (uint64_t)s_ec[w];
-      v.ev_end[e0 + w] =
-          (uint64_t)(s_ec[w] + (k >= 1 ? sample_draws(n, k) : 0));
-    }
-    if (tid == 0) {
-      if (upto < ne) {
-        const int w = upto, k = s_ek[w];
-        int64_t q = s_ec[w];
-        const int D = sample_draws(n, k);
-        bool ok = true;
-        for (int d = 0; d < D && ok; ++d) {
-          const uint32_t rng = sample_bound(n, k, d);
-          if (rng == 0) continue;
-          for (;;) {
-            if (q - h - s_wbase >= kRing) {
-              ok = false;  // redraw run beyond the ring: exact re-walk
-              break;
-            }
-            if (!lemire_rejects(at(q), rng)) break;
-            ++q;
-          }
-          ++q;
-        }
-        if (ok) {
-          v.ev_k[e0 + w] = k;
-          v.ev_cursor[e0 + w] = (uint64_t)s_ec[w];
-          v.ev_end[e0 + w] = (uint64_t)q;
-          s_q = q;
-          s_e = e0 + w + 1;
-        } else {
-          v.ctl->mut_bad = e0 + w;  // k_mut_fix redoes events >= w exactly
-          s_e = E;
-        }
-      }
-    }
-    __syncthreads();
-    if (s_e >= E) break;
+    const int slot = (int)(s % kNSeg);
+    const int64_t first = s_first + ((slot - s_first) % kNSeg + kNSeg) % kNSeg;
+    mbar_wait(&bars[slot], (uint32_t)(((s - first) / kNSeg) & 1));
+    *out = ring[(size_t)slot * kSeg + (f % kSeg)];
+    return true;
+  };
+  int64_t q = q0;
+  for (int e = e0; e < e_end; ++e) {
+    uint32_t u;
+    do {
+      if (!get(q, &u)) return false;
+      ++q;
+    } while (lemire_rejects(u, rng_k));
+    const int kraw = (int)(((uint64_t)u * (rng_k + 1u)) >> 32) + 1;
+    const int k = min(kraw, n / 2);
+    v.ev_k[e] = k;
+    v.ev_cursor[e] = (uint64_t)q;
+    if (k >= 1) q += sample_draws(n, k);
+    v.ev_end[e] = (uint64_t)q;  // speculative: no redraw in the sample
   }
+  // drain outstanding copies before the CTA exits
+  for (int64_t s = next_issue - kNSeg; s < next_issue; ++s) {
+    if (s < s_first || s >= nseg_total) continue;
+    const int slot = (int)(s % kNSeg);
+    const int64_t first = s_first + ((slot - s_first) % kNSeg + kNSeg) % kNSeg;
+    mbar_wait(&bars[slot], (uint32_t)(((s - first) / kNSeg) & 1));
+  }
+  return true;
 }
 
-// Numpy's choice(n, 2k, replace=False) from stream position `cur`, one
-// thread: writes the 2k sampled positions to idx; returns the u32 consumed.
-__device__ int64_t sample_event_seq(const PcgState& start, uint64_t cur,
-                                    int n, int k, uint16_t* idx,
+__device__ __forceinline__ StreamView stream_view(const SwarmView& v) {
+  const PcgState& g = *v.mut_start;
+  return {v.mstream, (int64_t)g.has_uint32, v.mstream_cap,
+          (uint32_t)g.uinteger};
+}
+
+// round 0: all P potential events from the call start; round r > 0: from
+// the event after the one flagged by the previous sample round.
+__global__ void __launch_bounds__(32) k_mut_walk(SwarmView v, int round) {
+  if (!v.ctl->mutating || v.ctl->done) return;
+  if (threadIdx.x != 0) return;
+  extern __shared__ __align__(128) uint32_t ring[];
+  __shared__ __align__(8) uint64_t bars[kNSeg];
+  int e0 = 0, e_end = v.P;
+  int64_t q0 = 0;
+  if (round > 0) {
+    const int bad = v.ctl->mut_bad, E = v.ctl->n_events;
+    if (v.ctl->mut_round != round - 1 || bad >= E) return;
+    e0 = bad + 1;
+    q0 = (int64_t)v.ev_end[bad];  // exact: the sampler consumed it exactly
+    e_end = E;
+    v.ctl->mut_bad = 0x7fffffff;
+    v.ctl->mut_from = e0;
+  }
+  if (!chain_events(v, stream_view(v), e0, q0, e_end, ring, bars))
+    v.ctl->mut_overflow = 1;
+  v.ctl->mut_round = round;
+}
+
+// Numpy's choice(n, 2k, replace=False) read from a stream, one thread:
+// writes the 2k sampled positions to idx; returns the u32 consumed (or -1
+// if the buffer ran out).
+template <typename Src>
+__device__ int64_t sample_event_seq(Src& c, int n, int k, uint16_t* idx,
                                     uint32_t* bits, uint16_t* arr) {
-  struct Counting {
-    Pcg r;
-    int64_t q = 0;
-    __device__ uint32_t bounded(uint32_t rng) {
-      if (rng == 0) return 0;
-      const uint32_t rng_excl = rng + 1u;
-      ++q;
-      uint64_t m = (uint64_t)r.next32() * rng_excl;
-      uint32_t leftover = (uint32_t)m;
-      if (leftover < rng_excl) {
-        const uint32_t threshold = (0xFFFFFFFFu - rng) % rng_excl;
-        while (leftover < threshold) {
-          ++q;
-          m = (uint64_t)r.next32() * rng_excl;
-          leftover = (uint32_t)m;
-        }
-      }
-      return (uint32_t)(m >> 32);
-    }
-  } c;
-  c.r.seek_u32(start, cur);
   const int size = 2 * k;
   if (n > 10000 && size > n / 50) {
+    for (int i = 0; i < n; ++i) arr[i] = (uint16_t)i;
     const int first = max(n - size, 1);
     for (int i = n - 1; i >= first; --i) {
       uint32_t j = c.bounded((uint32_t)i);
@@ -483,6 +438,7 @@ __device__ int64_t sample_event_seq(const PcgState& start, uint64_t cur,
     }
     for (int t = 0; t < size; ++t) idx[t] = arr[n - size + t];
   } else {
+    for (int i = 0; i < (n + 31) / 32; ++i) bits[i] = 0;
     for (int t = 0; t < size; ++t) {
       const uint32_t j = (uint32_t)(n - size + t);
       uint32_t val = c.bounded(j);
@@ -500,16 +456,55 @@ __device__ int64_t sample_event_seq(const PcgState& start, uint64_t cur,
   return c.q;
 }
 
-// One warp per event.  Shared memory per warp: draw values (u32, D+1) and
-// the n-bit Floyd bitmap (or arange(n) for the tail shuffle).
+// Lemire bounded draws with a u32 counter over a source of u32.
+template <typename Next>
+struct CountingBounded {
+  Next next;
+  int64_t q = 0;
+  __device__ uint32_t bounded(uint32_t rng) {
+    if (rng == 0) return 0;
+    const uint32_t rng_excl = rng + 1u;
+    ++q;
+    uint64_t m = (uint64_t)next() * rng_excl;
+    uint32_t leftover = (uint32_t)m;
+    if (leftover < rng_excl) {
+      const uint32_t threshold = (0xFFFFFFFFu - rng) % rng_excl;
+      while (leftover < threshold) {
+        ++q;
+        m = (uint64_t)next() * rng_excl;
+        leftover = (uint32_t)m;
+      }
+    }
+    return (uint32_t)(m >> 32);
+  }
+};
+
+struct BufNext {  // next32() over the generated stream buffer
+  StreamView sv;
+  int64_t pos;
+  __device__ uint32_t operator()() {
+    const int64_t p = pos++;
+    return p - sv.h < sv.cap ? sv.at(p) : 0u;
+  }
+};
+
+struct PcgNext {  // next32() regenerated from the stream state
+  Pcg r;
+  __device__ uint32_t operator()() { return r.next32(); }
+};
+
+// One warp per event.  Shared memory per warp: draw values (u32, D) and the
+// n-bit Floyd bitmap (or arange(n) for the tail shuffle).
 constexpr int kSampleWarps = 4;
 
 __global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample(
-    SwarmView v, int vals_cap, int scratch_words) {
+    SwarmView v, int round, int vals_cap, int scratch_words) {
   if (!v.ctl->mutating || v.ctl->done) return;
+  if (round > 0 && v.ctl->mut_round != round) return;  // no re-walk ran
   extern __shared__ __align__(16) uint32_t sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int e = blockIdx.x * (blockDim.x >> 5) + warp;
+  const int e = (round > 0 ? v.ctl->mut_from : 0) +
+                blockIdx.x * (blockDim.x >> 5) + warp;
   if (e >= v.ctl->n_events) return;
   const int n = v.n, k = v.ev_k[e];
   if (k < 1) return;
@@ -519,91 +514,58 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample(
   uint16_t* idx = v.ev_idx + (size_t)e * v.np;
   const int size = 2 * k;
   const bool tail = (n > 10000) && size > n / 50;
-  const uint64_t cur = v.ev_cursor[e];
+  const StreamView sv = stream_view(v);
+  const int64_t cur = (int64_t)v.ev_cursor[e];
   const int D = sample_draws(n, k);
-  if (tail || vals_cap == 0) {
-    // sequential sampler (tail shuffle, or n too large for a draw buffer)
-    if (tail) {
-      for (int i = lane; i < n; i += 32) arr[i] = (uint16_t)i;
-    } else {
-      for (int i = lane; i < (n + 31) / 32; i += 32) bits[i] = 0;
-    }
-    __syncwarp();
-    if (lane == 0) sample_event_seq(*v.mut_start, cur, n, k, idx, bits, arr);
-    return;
-  }
-  for (int i = lane; i < (n + 31) / 32; i += 32) bits[i] = 0;
-  // --- generate the event's D draws in parallel
-  const PcgState& g = *v.mut_start;
-  const int64_t h = (int64_t)g.has_uint32;
-  const u128 inc = {g.inc_hi, g.inc_lo};
-  // fresh index of the first draw; outputs counted from 1
-  const int64_t f0 = (int64_t)cur - h;  // >= 0: the k draw precedes cur
-  const int64_t m0 = f0 / 2 + 1;
-  const int skip = (int)(f0 & 1);  // first draw is the high half of m0
-  const int nout = (skip + D + 1) / 2;
-  u128 Al, Cl, A32, C32;
-  pcg_jump_coeffs((uint64_t)lane, inc, &Al, &Cl);
-  pcg_jump_coeffs(32, inc, &A32, &C32);
-  u128 base = {0, 0};
-  if (lane == 0)
-    base = pcg_advance({g.state_hi, g.state_lo}, inc, (uint64_t)m0);
-  base.hi = __shfl_sync(0xffffffffu, base.hi, 0);
-  base.lo = __shfl_sync(0xffffffffu, base.lo, 0);
-  u128 st = add128(mul128(Al, base), Cl);
-  for (int o = lane; o < nout; o += 32) {
-    const uint64_t out = pcg_output(st);
-    const int d0 = 2 * o - skip;  // draw index of the low half
-    if (d0 >= 0 && d0 < D) vals[d0] = (uint32_t)out;
-    if (d0 + 1 >= 0 && d0 + 1 < D) vals[d0 + 1] = (uint32_t)(out >> 32);
-    st = add128(mul128(A32, st), C32);
-  }
-  __syncwarp();
-  // --- rejection check and bounded values, in parallel
-  const int jstart = max(n - size, 1);
-  const int F = n - jstart;
   int rej = 0;
-  for (int d = lane; d < D; d += 32) {
-    const uint32_t rng = d < F ? (uint32_t)(jstart + d)
-                               : (uint32_t)(size - 1 - (d - F));
-    const uint32_t u = vals[d];
-    rej |= lemire_rejects(u, rng);
-    vals[d] = (uint32_t)(((uint64_t)u * (rng + 1u)) >> 32);
-  }
-  if (__any_sync(0xffffffffu, rej)) {
-    // this event holds a Lemire redraw (the walk accounted for it): sample
-    // it exactly, sequentially
-    __syncwarp();
-    if (lane == 0) {
-      for (int i = 0; i < (n + 31) / 32; ++i) bits[i] = 0;
-      sample_event_seq(*v.mut_start, cur, n, k, idx, bits, arr);
+  if (!tail && vals_cap > 0 && cur - sv.h + D <= sv.cap) {
+    for (int d = lane; d < D; d += 32) {
+      const uint32_t rng = sample_bound(n, k, d);
+      const uint32_t u = sv.buf[cur - sv.h + d];
+      rej |= lemire_rejects(u, rng);
+      vals[d] = (uint32_t)(((uint64_t)u * (rng + 1u)) >> 32);
     }
-    return;
+    rej = __any_sync(0xffffffffu, rej);
+    if (!rej) {
+      __syncwarp();
+      for (int i = lane; i < (n + 31) / 32; i += 32) bits[i] = 0;
+      __syncwarp();
+      if (lane == 0) {
+        // Floyd: j = n - 2k .. n-1 (j == 0 takes no draw and yields 0)
+        int d = 0;
+        for (int t = 0; t < size; ++t) {
+          const uint32_t j = (uint32_t)(n - size + t);
+          uint32_t val = j == 0 ? 0u : vals[d++];
+          if (bits[val >> 5] & (1u << (val & 31))) val = j;
+          bits[val >> 5] |= 1u << (val & 31);
+          idx[t] = (uint16_t)val;
+        }
+        // shuffle (numpy _shuffle_int): i = size-1 .. 1
+        for (int i = size - 1; i >= 1; --i) {
+          const uint32_t j = vals[d++];
+          const uint16_t t = idx[i];
+          idx[i] = idx[j];
+          idx[j] = t;
+        }
+      }
+      return;
+    }
   }
-  __syncwarp();
+  // sequential exact sampler: the event holds a redraw, uses the tail
+  // shuffle, or is too large for the draw buffer
   if (lane == 0) {
-    // Floyd: j = n - 2k .. n-1 (j == 0 takes no draw and yields 0)
-    int d = 0;
-    for (int t = 0; t < size; ++t) {
-      const uint32_t j = (uint32_t)(n - size + t);
-      uint32_t val = j == 0 ? 0u : vals[d++];
-      if (bits[val >> 5] & (1u << (val & 31))) val = j;
-      bits[val >> 5] |= 1u << (val & 31);
-      idx[t] = (uint16_t)val;
-    }
-    // shuffle (numpy _shuffle_int): i = size-1 .. 1
-    for (int i = size - 1; i >= 1; --i) {
-      const uint32_t j = vals[d++];
-      const uint16_t t = idx[i];
-      idx[i] = idx[j];
-      idx[j] = t;
+    CountingBounded<BufNext> c{BufNext{sv, cur}};
+    const int64_t used = sample_event_seq(c, n, k, idx, bits, arr);
+    if (cur - sv.h + used > sv.cap) v.ctl->mut_overflow = 1;
+    if (used != D) {
+      v.ev_end[e] = (uint64_t)(cur + used);
+      atomicMin(&v.ctl->mut_bad, e);
     }
   }
 }
 
-// Rare path + stream bookkeeping: exact sequential re-walk from the first
-// event the walk could not resolve (a redraw run beyond the ring margin,
-// never seen), then advance the persistent stream past the last event used.
+// Exact sequential fallback (a third flagged round, or a buffer overflow -
+// never seen) and the persistent stream update.
 __global__ void __launch_bounds__(32) k_mut_fix(SwarmView v) {
   if (!v.ctl->mutating || v.ctl->done) return;
   if (threadIdx.x != 0) return;
@@ -612,18 +574,23 @@ __global__ void __launch_bounds__(32) k_mut_fix(SwarmView v) {
   uint16_t* arr = (uint16_t*)smem;
   const int n = v.n;
   const int E = v.ctl->n_events;
-  const int bad = v.ctl->mut_bad;
+  int bad = v.ctl->mut_bad;
+  if (v.ctl->mut_overflow) bad = 0;  // redo the whole call exactly
   uint64_t q = 0;
   if (bad < E) {
     const int k_hi = max(2, n / 4);
     const uint32_t rng_k = (uint32_t)(k_hi - 1);
-    if (bad > 0) q = v.ev_end[bad - 1];
-    for (int e = bad; e < E; ++e) {
-      Pcg r;
-      r.seek_u32(*v.mut_start, q);
+    int from = 0;
+    if (!v.ctl->mut_overflow) {
+      q = v.ev_end[bad];  // the flagged event itself was sampled exactly
+      from = bad + 1;
+    }
+    for (int e = from; e < E; ++e) {
+      PcgNext pn;
+      pn.r.seek_u32(*v.mut_start, q);
       uint32_t u;
       do {
-        u = r.next32();
+        u = pn.r.next32();
         ++q;
       } while (lemire_rejects(u, rng_k));
       const int kraw = (int)(((uint64_t)u * (rng_k + 1u)) >> 32) + 1;
@@ -631,14 +598,8 @@ __global__ void __launch_bounds__(32) k_mut_fix(SwarmView v) {
       v.ev_k[e] = k;
       v.ev_cursor[e] = q;
       if (k < 1) continue;
-      const bool tail = (n > 10000) && 2 * k > n / 50;
-      if (tail) {
-        for (int i = 0; i < n; ++i) arr[i] = (uint16_t)i;
-      } else {
-        for (int i = 0; i < (n + 31) / 32; ++i) bits[i] = 0;
-      }
-      q += sample_event_seq(*v.mut_start, q, n, k,
-                            v.ev_idx + (size_t)e * v.np, bits, arr);
+      CountingBounded<PcgNext> c{pn};
+      q += sample_event_seq(c, n, k, v.ev_idx + (size_t)e * v.np, bits, arr);
     }
   } else if (E > 0) {
     q = v.ev_end[E - 1];
@@ -647,6 +608,7 @@ __global__ void __launch_bounds__(32) k_mut_fix(SwarmView v) {
   r.seek_u32(*v.mut_start, q);
   r.store(v.streams[1]);
   v.ctl->mut_q = q;
+  v.ctl->mut_overflow = 0;
 }
 
 __global__ void __launch_bounds__(128) k_mut_swap(SwarmView v) {
@@ -693,15 +655,20 @@ __global__ void __launch_bounds__(128) k_mut_swap(SwarmView v) {
 
 }  // namespace
 
-int64_t walk_ring_bytes(int n) {
-  const int64_t r = walk_ring_size(n);
-  return r == kRingSmem ? 0 : 4 * r;  // global ring only when smem is short
+int64_t mstream_words(int n, int P) {
+  const int k_hi = std::max(2, n / 4);
+  const int kmax = std::min(k_hi, n / 2);
+  const int64_t need = (int64_t)P * (1 + sample_draws(n, kmax)) + 4096;
+  return round_up(need, kSeg) + kSeg;  // whole segments for the ring copies
 }
 
 cudaError_t launch_mutation_walk(const SwarmView& v, cudaStream_t s) {
-  const size_t ring = (size_t)kRingSmem * 4;
+  const int64_t outs = v.mstream_cap / 2;
+  const int64_t threads = (outs + kGenPer - 1) / kGenPer;
+  k_mut_gen<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(v);
+  const size_t ring = (size_t)kNSeg * kSeg * 4;
   set_dyn_smem((const void*)k_mut_walk, ring);
-  k_mut_walk<<<1, kWalk, ring, s>>>(v);
+  k_mut_walk<<<1, 32, ring, s>>>(v, 0);
   return cudaGetLastError();
 }
 
@@ -722,8 +689,8 @@ cudaError_t launch_mutation_pre(const SwarmView& v, cudaStream_t s) {
 cudaError_t launch_mutation_post(const SwarmView& v, cudaStream_t s) {
   const int P = v.P;
   const int n = v.n;
-  // per warp: draw values (<= 2n + 1 u32) + Floyd bitmap / tail arange;
-  // without room for the draw buffer the warp samples sequentially
+  // per warp: draw values (<= 2n u32) + Floyd bitmap / tail arange; without
+  // room for the draw buffer the warp samples sequentially
   const int scratch_words =
       (int)round_up(std::max<int64_t>((n + 31) / 32, (n + 1) / 2), 4);
   int vals_cap = (int)round_up(2 * (int64_t)n + 2, 4);
@@ -735,8 +702,16 @@ cudaError_t launch_mutation_post(const SwarmView& v, cudaStream_t s) {
                                                 kBudget / per_warp));
   const size_t smem = (size_t)warps * per_warp;
   set_dyn_smem((const void*)k_mut_sample, smem);
-  k_mut_sample<<<(P + warps - 1) / warps, warps * 32, smem, s>>>(
-      v, vals_cap, scratch_words);
+  const size_t ring = (size_t)kNSeg * kSeg * 4;
+  set_dyn_smem((const void*)k_mut_walk, ring);
+  const unsigned grid = (unsigned)((P + warps - 1) / warps);
+  // round 0, then up to two re-walk rounds after a Lemire redraw
+  k_mut_sample<<<grid, warps * 32, smem, s>>>(v, 0, vals_cap, scratch_words);
+  for (int round = 1; round <= 2; ++round) {
+    k_mut_walk<<<1, 32, ring, s>>>(v, round);
+    k_mut_sample<<<grid, warps * 32, smem, s>>>(v, round, vals_cap,
+                                                scratch_words);
+  }
   const size_t scratch =
       std::max<size_t>(round_up((n + 31) / 32 * 4, 16), 2 * (size_t)v.np);
   set_dyn_smem((const void*)k_mut_fix, scratch);
