@@ -349,23 +349,39 @@ __device__ bool chain_events(const SwarmView& v, StreamView sv, int e0,
     ++next_issue;
   };
   for (int b = 0; b < kNSeg; ++b) issue();
+  // current segment (waited on once) and its shared-memory base
+  int64_t cur_seg = -1;
+  const uint32_t* seg = nullptr;
   auto get = [&](int64_t q, uint32_t* out) -> bool {
     if (q < sv.h) {
       *out = sv.ub;
       return true;
     }
     const int64_t f = q - sv.h;
-    const int64_t s = f / kSeg;
-    if (s >= nseg_total) return false;
-    while (s >= next_issue) {  // slide: the chain never looks back
-      fence_proxy_async();
-      issue();
+    const int64_t s = f >> 12;  // kSeg = 4096
+    if (s != cur_seg) {
+      if (s >= nseg_total) return false;
+      while (s >= next_issue) {  // slide: the chain never looks back
+        fence_proxy_async();
+        issue();
+      }
+      const int slot = (int)(s & (kNSeg - 1));
+      const int64_t first =
+          s_first + ((slot - s_first) % kNSeg + kNSeg) % kNSeg;
+      mbar_wait(&bars[slot], (uint32_t)(((s - first) / kNSeg) & 1));
+      cur_seg = s;
+      seg = ring + (size_t)slot * kSeg;
     }
-    const int slot = (int)(s % kNSeg);
-    const int64_t first = s_first + ((slot - s_first) % kNSeg + kNSeg) % kNSeg;
-    mbar_wait(&bars[slot], (uint32_t)(((s - first) / kNSeg) & 1));
-    *out = ring[(size_t)slot * kSeg + (f % kSeg)];
+    *out = seg[f & (kSeg - 1)];
     return true;
+  };
+  // D(k) without divisions: non-tail events take F + 2k - 1 draws with
+  // F = 2k when n - 2k >= 1
+  const int n50 = n / 50;
+  auto draws = [&](int k) -> int {
+    const int size = 2 * k;
+    if (n > 10000 && size > n50) return size <= n - 1 ? size : n - 1;
+    return (size <= n - 1 ? size : n - 1) + size - 1;
   };
   int64_t q = q0;
   for (int e = e0; e < e_end; ++e) {
@@ -378,7 +394,7 @@ __device__ bool chain_events(const SwarmView& v, StreamView sv, int e0,
     const int k = min(kraw, n / 2);
     v.ev_k[e] = k;
     v.ev_cursor[e] = (uint64_t)q;
-    if (k >= 1) q += sample_draws(n, k);
+    if (k >= 1) q += draws(k);
     v.ev_end[e] = (uint64_t)q;  // speculative: no redraw in the sample
   }
   // drain outstanding copies before the CTA exits
@@ -508,7 +524,9 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample(
   if (e >= v.ctl->n_events) return;
   const int n = v.n, k = v.ev_k[e];
   if (k < 1) return;
-  uint32_t* vals = sm + (size_t)warp * (vals_cap + scratch_words);
+  // per warp: vals[vals_cap] | bits/arr[scratch_words] | sidx[idx_words]
+  const int idx_words = (n + 1) / 2;
+  uint32_t* vals = sm + (size_t)warp * (vals_cap + scratch_words + idx_words);
   uint32_t* bits = vals + vals_cap;
   uint16_t* arr = (uint16_t*)bits;
   uint16_t* idx = v.ev_idx + (size_t)e * v.np;
@@ -530,6 +548,9 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample(
       __syncwarp();
       for (int i = lane; i < (n + 31) / 32; i += 32) bits[i] = 0;
       __syncwarp();
+      // Floyd + shuffle on a shared-memory copy of idx (the serial steps are
+      // dependent loads; global memory would put an L2 round trip in each)
+      uint16_t* sidx = (uint16_t*)(bits + scratch_words);
       if (lane == 0) {
         // Floyd: j = n - 2k .. n-1 (j == 0 takes no draw and yields 0)
         int d = 0;
@@ -538,16 +559,18 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample(
           uint32_t val = j == 0 ? 0u : vals[d++];
           if (bits[val >> 5] & (1u << (val & 31))) val = j;
           bits[val >> 5] |= 1u << (val & 31);
-          idx[t] = (uint16_t)val;
+          sidx[t] = (uint16_t)val;
         }
         // shuffle (numpy _shuffle_int): i = size-1 .. 1
         for (int i = size - 1; i >= 1; --i) {
           const uint32_t j = vals[d++];
-          const uint16_t t = idx[i];
-          idx[i] = idx[j];
-          idx[j] = t;
+          const uint16_t t = sidx[i];
+          sidx[i] = sidx[j];
+          sidx[j] = t;
         }
       }
+      __syncwarp();
+      for (int t = lane; t < size; t += 32) idx[t] = sidx[t];
       return;
     }
   }
@@ -694,9 +717,11 @@ cudaError_t launch_mutation_post(const SwarmView& v, cudaStream_t s) {
   const int scratch_words =
       (int)round_up(std::max<int64_t>((n + 31) / 32, (n + 1) / 2), 4);
   int vals_cap = (int)round_up(2 * (int64_t)n + 2, 4);
+  const int idx_words = (n + 1) / 2;
   constexpr size_t kBudget = 200 * 1024;
-  if ((size_t)(vals_cap + scratch_words) * 4 > kBudget) vals_cap = 0;
-  const size_t per_warp = (size_t)(vals_cap + scratch_words) * 4;
+  if ((size_t)(vals_cap + scratch_words + idx_words) * 4 > kBudget)
+    vals_cap = 0;
+  const size_t per_warp = (size_t)(vals_cap + scratch_words + idx_words) * 4;
   const int warps =
       (int)std::max<size_t>(1, std::min<size_t>(kSampleWarps,
                                                 kBudget / per_warp));
