@@ -54,7 +54,7 @@ int cuda_fail(cudaError_t e, const char* where) {
   } while (0)
 
 struct Layout {
-  size_t off_ctl, off_streams, off_mut_start, off_x, off_pbest, off_vmap,
+  size_t off_ctl, off_streams, off_mut_start, off_init_start, off_x, off_pbest, off_vmap,
       off_vel, off_vel_len, off_fit, off_pfit, off_dcache, off_gbest,
       off_conv, off_tores, off_chunk_row, off_rank, off_hash, off_flag,
       off_sidx, off_order, off_surv, off_keep, off_ev_slot, off_ev_k,
@@ -85,7 +85,8 @@ Layout make_layout(const dpso_params* prm, int n) {
   L.vel_cap = vel_capacity(prm, n);
   L.off_ctl = take(sizeof(DevCtl));
   L.off_streams = take(sizeof(PcgState) * (P + 2));
-  L.off_mut_start = take(sizeof(PcgState));
+  L.off_mut_start = take(2 * sizeof(PcgState));
+  L.off_init_start = take(sizeof(PcgState));
   L.off_x = take(2 * P * np);
   L.off_pbest = take(2 * P * np);
   L.off_vmap = take(prm->inertia == 1.0 ? 2 * P * np : 0);
@@ -106,11 +107,11 @@ Layout make_layout(const dpso_params* prm, int n) {
   L.off_surv = take(4 * P);
   L.off_keep = take(4 * P);
   L.off_ev_slot = take(4 * P);
-  L.off_ev_k = take(4 * P);
-  L.off_ev_cursor = take(8 * P);
-  L.off_ev_end = take(8 * P);
+  L.off_ev_k = take(2 * 4 * P);
+  L.off_ev_cursor = take(2 * 8 * P);
+  L.off_ev_end = take(2 * 8 * P);
   L.off_ev_idx = take(2 * P * np);
-  L.off_mstream = take(prm->use_mutation ? 4 * mstream_words(n, P) : 0);
+  L.off_mstream = take(prm->use_mutation ? 2 * 4 * mstream_words(n, P) : 0);
   L.off_init_cursor = take(8 * P);
   L.off_seed = take(2 * np);
   L.off_cost32 = take(prm->use_edge_exchange ? 4 * (int64_t)n * np : 0);
@@ -189,17 +190,16 @@ static cudaError_t enqueue_generation(const SwarmView& v, cudaStream_t s,
     if ((e = (call))) return e; \
   } while (0)
   STAGE("gen_begin", launch_gen_begin(v, s));
+  STAGE("update", launch_update(v, s));
   if (v.use_mutation) {
+    STAGE("mutation_pre", launch_mutation_pre(v, s));
+    STAGE("mutation_post", launch_mutation_post(v, s));
+    // the next call's stream walk overlaps the rest of this generation
     STAGE("fork", cudaEventRecord(fork, s));
     STAGE("fork", cudaStreamWaitEvent(s2, fork, 0));
     STAGE("mutation_walk", launch_mutation_walk(v, s2));
     STAGE("join", cudaEventRecord(join, s2));
-  }
-  STAGE("update", launch_update(v, s));
-  if (v.use_mutation) {
-    STAGE("mutation_pre", launch_mutation_pre(v, s));
-    STAGE("join", cudaStreamWaitEvent(s, join, 0));
-    STAGE("mutation_post", launch_mutation_post(v, s));
+    STAGE("mutation_swap", launch_mutation_swap(v, s));
   }
   if (v.use_edge_exchange) {
     STAGE("select", launch_select(v, false, s));
@@ -208,6 +208,7 @@ static cudaError_t enqueue_generation(const SwarmView& v, cudaStream_t s,
   } else {
     STAGE("select+finalize", launch_select(v, true, s));
   }
+  if (v.use_mutation) STAGE("join", cudaStreamWaitEvent(s, join, 0));
 #undef STAGE
   g_stage = "";
   return cudaSuccess;
@@ -274,6 +275,7 @@ int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
   v.ctl = (DevCtl*)(w + L.off_ctl);
   v.streams = (PcgState*)(w + L.off_streams);
   v.mut_start = (PcgState*)(w + L.off_mut_start);
+  v.init_start = (PcgState*)(w + L.off_init_start);
   v.x = (uint16_t*)(w + L.off_x);
   v.pbest = (uint16_t*)(w + L.off_pbest);
   v.vmap = prm->inertia == 1.0 ? (uint16_t*)(w + L.off_vmap) : nullptr;
@@ -402,6 +404,8 @@ int dpso_init(dpso_ctx* c, const int32_t* seed_body, int32_t n_seed) {
   if (rc) return rc;
   CK(launch_init(c->v, dseed, n_seed, c->stream));
   CK(launch_init_best(c->v, c->stream));
+  // stream walk of the first mutation call
+  if (c->v.use_mutation) CK(launch_mutation_walk(c->v, c->stream));
   c->initialized = true;
   return sync_out(c);
 }
@@ -452,13 +456,13 @@ int dpso_step_timed(dpso_ctx* c, int32_t gens, double* phase_ms,
     CK(launch_update(v, s));
     CK(cudaEventRecord(ev[1], s));
     if (v.use_mutation) {
+      CK(launch_mutation_pre(v, s));
+      CK(launch_mutation_post(v, s));
       CK(cudaEventRecord(c->ev_fork, s));
       CK(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
       CK(launch_mutation_walk(v, c->stream2));
       CK(cudaEventRecord(c->ev_join, c->stream2));
-      CK(launch_mutation_pre(v, s));
-      CK(cudaStreamWaitEvent(s, c->ev_join, 0));
-      CK(launch_mutation_post(v, s));
+      CK(launch_mutation_swap(v, s));
     }
     CK(cudaEventRecord(ev[2], s));
     CK(launch_select(v, !v.use_edge_exchange, s));
@@ -468,6 +472,7 @@ int dpso_step_timed(dpso_ctx* c, int32_t gens, double* phase_ms,
     if (v.use_edge_exchange) CK(launch_two_opt(v, s, 2));
     CK(cudaEventRecord(ev[5], s));
     if (v.use_edge_exchange) CK(launch_finalize(v, s));
+    if (v.use_mutation) CK(cudaStreamWaitEvent(s, c->ev_join, 0));
     CK(cudaEventRecord(ev[6], s));
     CK(cudaEventSynchronize(ev[6]));
     for (int i = 0; i < 6; ++i) {

@@ -48,6 +48,8 @@ struct DevCtl {
   int32_t mut_round;      // last stream-walk round run this call
   int32_t mut_from;       // first event of that round
   int32_t mut_overflow;   // stream buffer too short (exact fallback)
+  int32_t mut_cur;        // parity of the event buffers of the current call
+  int32_t mut_pending;    // the next call's stream walk is still to run
   uint64_t mut_q;     // u32 draws consumed by the current mutation call
 };
 
@@ -88,7 +90,8 @@ struct SwarmView {
   int64_t ld;
   DevCtl* ctl;
   PcgState* streams;   // [0] init, [1] mutation, [2+p] particle p
-  PcgState* mut_start; // copy of the mutation stream at call start
+  PcgState* mut_start; // [2] mutation stream at call start, per parity
+  PcgState* init_start; // init stream at init start
   uint16_t* x;
   uint16_t* pbest;
   uint16_t* vmap;
@@ -113,12 +116,14 @@ struct SwarmView {
   int32_t* surv_list;
   int32_t* keep;
   int32_t* ev_slot;
+  // per mutation call, double-buffered by call parity ([2][P]): the walk
+  // for the next call runs while the current generation finishes
   int32_t* ev_k;
   uint64_t* ev_cursor;
   uint64_t* ev_end;     // stream position after each event's draws
   uint16_t* ev_idx;    // P x np sampled positions per mutation event
-  uint32_t* mstream;   // generated mutation-stream span (u32)
-  int64_t mstream_cap; // u32 capacity of mstream
+  uint32_t* mstream;   // [2] generated mutation-stream span (u32)
+  int64_t mstream_cap; // u32 capacity of one mstream buffer
   uint64_t* init_cursor;
 };
 
@@ -126,10 +131,13 @@ struct SwarmView {
 cudaError_t launch_gen_begin(const SwarmView& v, cudaStream_t s);
 cudaError_t launch_update(const SwarmView& v, cudaStream_t s);
 cudaError_t launch_mutation(const SwarmView& v, cudaStream_t s);
-// the three parts of launch_mutation: the stream walk depends only on the
-// mutation stream and may run on a forked stream concurrently with the
-// update and launch_mutation_pre; launch_mutation_post must follow both.
+// The parts of one mutation call: launch_mutation_pre (dedupe, lists) and
+// launch_mutation_post (event sampling, stream update) then
+// launch_mutation_swap.  launch_mutation_walk prepares the NEXT call (it
+// depends only on the mutation stream after launch_mutation_post, or after
+// init) and may run on a forked stream concurrently with everything else.
 cudaError_t launch_mutation_walk(const SwarmView& v, cudaStream_t s);
+cudaError_t launch_mutation_swap(const SwarmView& v, cudaStream_t s);
 int64_t mstream_words(int n, int P);
 cudaError_t launch_mutation_pre(const SwarmView& v, cudaStream_t s);
 cudaError_t launch_mutation_post(const SwarmView& v, cudaStream_t s);

@@ -80,6 +80,7 @@ __global__ void k_gen_begin(SwarmView v) {
   if (c->done) return;
   c->gen += 1;
   c->mutating = v.use_mutation && (c->gen % v.mutation_period == 0);
+  if (c->mutating) c->mut_cur ^= 1;  // use the buffers the walk prepared
   c->two_opt_ran = 0;
   c->improved = 0;
 }
@@ -211,7 +212,7 @@ struct CountingPcg {
 __global__ void k_init_walk(SwarmView v, int n_seed) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const int n = v.n;
-  *v.mut_start = v.streams[0];  // keep the start of the init stream
+  *v.init_start = v.streams[0];  // keep the start of the init stream
   CountingPcg cr;
   cr.r.load(v.streams[0]);
   cr.q = 0;
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(128) k_init_build(SwarmView v,
     __syncthreads();
     if (tid == 0) {
       Pcg r;
-      r.seek_u32(*v.mut_start, v.init_cursor[p]);
+      r.seek_u32(*v.init_start, v.init_cursor[p]);
       if (p < n_seed) {
         if (p > 0 && n > 1) {
           uint32_t v0 = r.bounded((uint32_t)(n - 2));
@@ -319,6 +320,9 @@ __global__ void __launch_bounds__(kRed) k_init_best(SwarmView v) {
     c->collision = 0;
     c->vel_overflow = 0;
     c->two_opt_count = 0;
+    c->mut_cur = 0;
+    c->mut_pending = v.use_mutation;  // first call's walk (parity 1)
+    c->mut_overflow = 0;
     v.conv[0] = bv;
   }
 }

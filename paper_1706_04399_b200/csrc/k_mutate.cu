@@ -266,6 +266,21 @@ __global__ void __launch_bounds__(128) k_mut_copy(SwarmView v) {
 //   k_mut_fix     exact sequential fallback after two flagged rounds (never
 //                 seen) and the persistent stream update.
 
+// Buffers of one mutation call (parity 0/1).
+struct MutBufs {
+  int32_t* ev_k;
+  uint64_t* ev_cursor;
+  uint64_t* ev_end;
+  uint32_t* mstream;
+  PcgState* start;
+};
+
+__device__ __forceinline__ MutBufs mut_bufs(const SwarmView& v, int par) {
+  return {v.ev_k + (size_t)par * v.P, v.ev_cursor + (size_t)par * v.P,
+          v.ev_end + (size_t)par * v.P,
+          v.mstream + (size_t)par * v.mstream_cap, v.mut_start + par};
+}
+
 constexpr int kSeg = 4096;   // u32 per ring segment (16 KiB)
 constexpr int kNSeg = 8;     // ring slots (128 KiB)
 
@@ -290,23 +305,21 @@ __device__ __forceinline__ uint32_t sample_bound(int n, int k, int d) {
 
 constexpr int kGenPer = 64;  // outputs per k_mut_gen thread
 
+// Prepares the NEXT mutation call: writes its stream span into the buffer
+// of parity mut_cur ^ 1.
 __global__ void __launch_bounds__(256) k_mut_gen(SwarmView v) {
-  if (!v.ctl->mutating || v.ctl->done) return;
+  if (!v.ctl->mut_pending || v.ctl->done) return;
+  const MutBufs b = mut_bufs(v, v.ctl->mut_cur ^ 1);
   const PcgState g = v.streams[1];
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c == 0) {
-    *v.mut_start = g;
-    v.ctl->mut_bad = 0x7fffffff;
-    v.ctl->mut_round = 0;
-    v.ctl->mut_from = 0;
-  }
+  if (c == 0) *b.start = g;
   const int64_t outs = v.mstream_cap / 2;
   const int64_t o0 = c * kGenPer;
   if (o0 >= outs) return;
   const u128 inc = {g.inc_hi, g.inc_lo};
   u128 st = pcg_advance({g.state_hi, g.state_lo}, inc, (uint64_t)o0 + 1);
   const u128 M = pcg_mult();
-  uint2* out = reinterpret_cast<uint2*>(v.mstream);
+  uint2* out = reinterpret_cast<uint2*>(b.mstream);
   for (int r = 0; r < kGenPer && o0 + r < outs; ++r) {
     const uint64_t o = pcg_output(st);
     out[o0 + r] = make_uint2((uint32_t)o, (uint32_t)(o >> 32));
@@ -327,9 +340,9 @@ struct StreamView {
 
 // Chain of k-draws from (e0, q0) for events e0..e_end-1, one thread, ring of
 // stream segments in shared memory.  Returns false on buffer overflow.
-__device__ bool chain_events(const SwarmView& v, StreamView sv, int e0,
-                             int64_t q0, int e_end, uint32_t* ring,
-                             uint64_t* bars) {
+__device__ bool chain_events(const SwarmView& v, const MutBufs& b,
+                             StreamView sv, int e0, int64_t q0, int e_end,
+                             uint32_t* ring, uint64_t* bars) {
   const int n = v.n;
   const int k_hi = max(2, n / 4);
   const uint32_t rng_k = (uint32_t)(k_hi - 1);
@@ -392,10 +405,10 @@ __device__ bool chain_events(const SwarmView& v, StreamView sv, int e0,
     } while (lemire_rejects(u, rng_k));
     const int kraw = (int)(((uint64_t)u * (rng_k + 1u)) >> 32) + 1;
     const int k = min(kraw, n / 2);
-    v.ev_k[e] = k;
-    v.ev_cursor[e] = (uint64_t)q;
+    b.ev_k[e] = k;
+    b.ev_cursor[e] = (uint64_t)q;
     if (k >= 1) q += draws(k);
-    v.ev_end[e] = (uint64_t)q;  // speculative: no redraw in the sample
+    b.ev_end[e] = (uint64_t)q;  // speculative: no redraw in the sample
   }
   // drain outstanding copies before the CTA exits
   for (int64_t s = next_issue - kNSeg; s < next_issue; ++s) {
@@ -407,33 +420,46 @@ __device__ bool chain_events(const SwarmView& v, StreamView sv, int e0,
   return true;
 }
 
-__device__ __forceinline__ StreamView stream_view(const SwarmView& v) {
-  const PcgState& g = *v.mut_start;
-  return {v.mstream, (int64_t)g.has_uint32, v.mstream_cap,
+__device__ __forceinline__ StreamView stream_view(const SwarmView& v,
+                                                  const MutBufs& b) {
+  const PcgState& g = *b.start;
+  return {b.mstream, (int64_t)g.has_uint32, v.mstream_cap,
           (uint32_t)g.uinteger};
 }
 
-// round 0: all P potential events from the call start; round r > 0: from
-// the event after the one flagged by the previous sample round.
+// round 0: all P potential events of the NEXT call from its start (parity
+// mut_cur ^ 1); round r > 0: the current call, from the event after the one
+// flagged by the previous sample round.
 __global__ void __launch_bounds__(32) k_mut_walk(SwarmView v, int round) {
-  if (!v.ctl->mutating || v.ctl->done) return;
+  if (v.ctl->done) return;
   if (threadIdx.x != 0) return;
   extern __shared__ __align__(128) uint32_t ring[];
   __shared__ __align__(8) uint64_t bars[kNSeg];
-  int e0 = 0, e_end = v.P;
+  int e0 = 0, e_end = v.P, par;
   int64_t q0 = 0;
-  if (round > 0) {
+  if (round == 0) {
+    if (!v.ctl->mut_pending) return;
+    par = v.ctl->mut_cur ^ 1;
+  } else {
+    if (!v.ctl->mutating) return;
+    par = v.ctl->mut_cur;
+    const MutBufs b = mut_bufs(v, par);
     const int bad = v.ctl->mut_bad, E = v.ctl->n_events;
     if (v.ctl->mut_round != round - 1 || bad >= E) return;
     e0 = bad + 1;
-    q0 = (int64_t)v.ev_end[bad];  // exact: the sampler consumed it exactly
+    q0 = (int64_t)b.ev_end[bad];  // exact: the sampler consumed it exactly
     e_end = E;
     v.ctl->mut_bad = 0x7fffffff;
     v.ctl->mut_from = e0;
   }
-  if (!chain_events(v, stream_view(v), e0, q0, e_end, ring, bars))
-    v.ctl->mut_overflow = 1;
-  v.ctl->mut_round = round;
+  const MutBufs b = mut_bufs(v, par);
+  if (!chain_events(v, b, stream_view(v, b), e0, q0, e_end, ring, bars))
+    v.ctl->mut_overflow |= 1 << par;
+  if (round == 0) {
+    v.ctl->mut_pending = 0;
+  } else {
+    v.ctl->mut_round = round;
+  }
 }
 
 // Numpy's choice(n, 2k, replace=False) read from a stream, one thread:
@@ -517,12 +543,13 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample(
     SwarmView v, int round, int vals_cap, int scratch_words) {
   if (!v.ctl->mutating || v.ctl->done) return;
   if (round > 0 && v.ctl->mut_round != round) return;  // no re-walk ran
+  const MutBufs b = mut_bufs(v, v.ctl->mut_cur);
   extern __shared__ __align__(16) uint32_t sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int e = (round > 0 ? v.ctl->mut_from : 0) +
                 blockIdx.x * (blockDim.x >> 5) + warp;
   if (e >= v.ctl->n_events) return;
-  const int n = v.n, k = v.ev_k[e];
+  const int n = v.n, k = b.ev_k[e];
   if (k < 1) return;
   // per warp: vals[vals_cap] | bits/arr[scratch_words] | sidx[idx_words]
   const int idx_words = (n + 1) / 2;
@@ -532,8 +559,8 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample(
   uint16_t* idx = v.ev_idx + (size_t)e * v.np;
   const int size = 2 * k;
   const bool tail = (n > 10000) && size > n / 50;
-  const StreamView sv = stream_view(v);
-  const int64_t cur = (int64_t)v.ev_cursor[e];
+  const StreamView sv = stream_view(v, b);
+  const int64_t cur = (int64_t)b.ev_cursor[e];
   const int D = sample_draws(n, k);
   int rej = 0;
   if (!tail && vals_cap > 0 && cur - sv.h + D <= sv.cap) {
@@ -581,7 +608,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample(
     const int64_t used = sample_event_seq(c, n, k, idx, bits, arr);
     if (cur - sv.h + used > sv.cap) v.ctl->mut_overflow = 1;
     if (used != D) {
-      v.ev_end[e] = (uint64_t)(cur + used);
+      b.ev_end[e] = (uint64_t)(cur + used);
       atomicMin(&v.ctl->mut_bad, e);
     }
   }
@@ -595,22 +622,25 @@ __global__ void __launch_bounds__(32) k_mut_fix(SwarmView v) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* bits = (uint32_t*)smem;
   uint16_t* arr = (uint16_t*)smem;
+  const int par = v.ctl->mut_cur;
+  const MutBufs b = mut_bufs(v, par);
   const int n = v.n;
   const int E = v.ctl->n_events;
   int bad = v.ctl->mut_bad;
-  if (v.ctl->mut_overflow) bad = 0;  // redo the whole call exactly
+  const bool overflow = (v.ctl->mut_overflow >> par) & 1;
+  if (overflow) bad = 0;  // redo the whole call exactly
   uint64_t q = 0;
   if (bad < E) {
     const int k_hi = max(2, n / 4);
     const uint32_t rng_k = (uint32_t)(k_hi - 1);
     int from = 0;
-    if (!v.ctl->mut_overflow) {
-      q = v.ev_end[bad];  // the flagged event itself was sampled exactly
+    if (!overflow) {
+      q = b.ev_end[bad];  // the flagged event itself was sampled exactly
       from = bad + 1;
     }
     for (int e = from; e < E; ++e) {
       PcgNext pn;
-      pn.r.seek_u32(*v.mut_start, q);
+      pn.r.seek_u32(*b.start, q);
       uint32_t u;
       do {
         u = pn.r.next32();
@@ -618,20 +648,21 @@ __global__ void __launch_bounds__(32) k_mut_fix(SwarmView v) {
       } while (lemire_rejects(u, rng_k));
       const int kraw = (int)(((uint64_t)u * (rng_k + 1u)) >> 32) + 1;
       const int k = min(kraw, n / 2);
-      v.ev_k[e] = k;
-      v.ev_cursor[e] = q;
+      b.ev_k[e] = k;
+      b.ev_cursor[e] = q;
       if (k < 1) continue;
       CountingBounded<PcgNext> c{pn};
       q += sample_event_seq(c, n, k, v.ev_idx + (size_t)e * v.np, bits, arr);
     }
   } else if (E > 0) {
-    q = v.ev_end[E - 1];
+    q = b.ev_end[E - 1];
   }
   Pcg r;
-  r.seek_u32(*v.mut_start, q);
+  r.seek_u32(*b.start, q);
   r.store(v.streams[1]);
   v.ctl->mut_q = q;
-  v.ctl->mut_overflow = 0;
+  v.ctl->mut_overflow &= ~(1 << par);
+  v.ctl->mut_pending = 1;  // the next call's walk may start
 }
 
 __global__ void __launch_bounds__(128) k_mut_swap(SwarmView v) {
@@ -642,7 +673,7 @@ __global__ void __launch_bounds__(128) k_mut_swap(SwarmView v) {
   double* sd = (double*)smem;
   const int n = v.n, np = v.np, tid = threadIdx.x;
   const int p = v.ev_slot[e];
-  const int k = v.ev_k[e];
+  const int k = v.ev_k[(size_t)v.ctl->mut_cur * v.P + e];
   if (k < 1) return;
   const uint16_t* idx = v.ev_idx + (size_t)e * np;
   uint16_t* body = v.x + (size_t)p * np;
@@ -741,16 +772,21 @@ cudaError_t launch_mutation_post(const SwarmView& v, cudaStream_t s) {
       std::max<size_t>(round_up((n + 31) / 32 * 4, 16), 2 * (size_t)v.np);
   set_dyn_smem((const void*)k_mut_fix, scratch);
   k_mut_fix<<<1, 32, scratch, s>>>(v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mutation_swap(const SwarmView& v, cudaStream_t s) {
   const size_t sd = (size_t)8 * v.np;
   set_dyn_smem((const void*)k_mut_swap, sd);
-  k_mut_swap<<<P, 128, sd, s>>>(v);
+  k_mut_swap<<<v.P, 128, sd, s>>>(v);
   return cudaGetLastError();
 }
 
 cudaError_t launch_mutation(const SwarmView& v, cudaStream_t s) {
-  cudaError_t e = launch_mutation_walk(v, s);
-  if (!e) e = launch_mutation_pre(v, s);
+  cudaError_t e = launch_mutation_pre(v, s);
   if (!e) e = launch_mutation_post(v, s);
+  if (!e) e = launch_mutation_walk(v, s);
+  if (!e) e = launch_mutation_swap(v, s);
   return e;
 }
 
