@@ -80,7 +80,12 @@ __global__ void k_gen_begin(SwarmView v) {
   if (c->done) return;
   c->gen += 1;
   c->mutating = v.use_mutation && (c->gen % v.mutation_period == 0);
-  if (c->mutating) c->mut_cur ^= 1;  // use the buffers the walk prepared
+  if (c->mutating) {
+    c->mut_cur ^= 1;  // use the buffers the walk prepared
+    c->mut_bad = 0x7fffffff;
+    c->mut_round = 0;
+    c->mut_from = 0;
+  }
   c->two_opt_ran = 0;
   c->improved = 0;
 }
