@@ -35,6 +35,7 @@
 // Each lane keeps its first strict minimum in (i, j) order; warp shuffles
 // reduce (delta, i, j); the apply kernel merges bands in row order.
 #include <float.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -65,8 +66,10 @@ struct ScanArgs {
   const DevCtl* ctl;       // nullable: skip when done or improved
   uint32_t row_bytes;      // bytes streamed per cost row (multiple of 16)
   uint32_t buf_stride;     // bytes between ring buffers
+  uint32_t buf_stride2;    // bytes of one warp's smem (ring + d_j)
   float thr;               // FILTER32: 2 * eps
   int only_flagged;        // FP64 fallback: only tasks tagged kOverflowTag
+  int stream_only;         // debug: stream the rows, skip the pair compute
 };
 
 __device__ __forceinline__ bool res_less(double d1, int i1, int j1, double d2,
@@ -288,36 +291,30 @@ __device__ __noinline__ float cand_group(float t0, float t1, float t2,
   return lim;
 }
 
-// One CTA (4 warps) per task.  Column block m (columns j = l + 32m) belongs
-// to warp m % 4, so a thread holds NB = ceil(blocks / 4) blocks of state
-// (small register footprint -> high occupancy) and the CTA shares one row
-// ring.  Shift-reuse: the A term of pair (i+1, j) is C[a_{i+1}][a_j], which
-// is the B term the owner of column j-1 gathered for pair (i, j-1): lane l
-// gets it from lane l-1 by one warp rotate, lane 0 from the previous block's
-// lane 31 through a row-parity-buffered shared array.  Each row therefore
-// costs ONE random shared-memory gather per pair; the first row of a task is
-// primed by a B-gather of row a_r0.  Rows a_r0..a_r1 stream through a
-// 3-slot ring, two rows ahead, with one CTA barrier per row.  In fp32 modes
-// the order of the three adds is free (EXACT32 sums are exact; FILTER32 is
-// bounded).
-constexpr int kCtaWarps = 4;
+// One warp per task; lane l owns the columns j = l + 32m (m < NPL).
+// Shift-reuse: the A term of pair (i+1, j) is C[a_{i+1}][a_j], which is the
+// B term lane l-1 gathered for pair (i, j-1) (lane 0: lane 31 of block m-1),
+// so it arrives by ONE warp rotate and each row costs ONE random
+// shared-memory gather per pair; the first row of a task is primed by a
+// B-gather of row a_r0.  Per lane in registers: the gathered B values and
+// the gather indices s_j (two u16 per register); d_j sits in shared memory
+// (lane-contiguous, conflict free).  Rows a_r0..a_r1 stream through a
+// per-warp 3-slot ring, two rows ahead.  In fp32 modes the order of the
+// three adds is free (EXACT32 sums are exact; FILTER32 is bounded).
+constexpr int kBufs32 = 2;  // fp32 per-warp ring depth (one row ahead)
+constexpr int kG32 = 8;     // column blocks per uniform group (fp32 scan)
 
-template <int NB, int MODE>
-__global__ void __launch_bounds__(kCtaWarps * 32)
+template <int NPL, int MODE>
+__global__ void __launch_bounds__(kMaxWarps * 32, 4)
     k_two_opt_scan32(ScanArgs a) {
   if (a.ctl && (a.ctl->done || a.ctl->improved)) return;
-  constexpr int NPL = NB * kCtaWarps;  // column blocks
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bars[kBufs];
-  __shared__ float s_x[2][NPL];  // lane-31 B values per block, per parity
-  __shared__ uint32_t s_cij[kCtaWarps][kCand][32];
-  __shared__ float s_cd[kCtaWarps][kCand][32];
-  __shared__ float s_st[kCtaWarps][3][32];
-  __shared__ double s_rd[kCtaWarps];
-  __shared__ int s_ri[kCtaWarps], s_rj[kCtaWarps];
-  __shared__ float s_m[kCtaWarps];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int task = blockIdx.x;
+  __shared__ __align__(8) uint64_t bars[kMaxWarps][kBufs32];
+  __shared__ uint32_t s_cij[kMaxWarps][kCand][32];
+  __shared__ float s_cd[kMaxWarps][kCand][32];
+  __shared__ float s_st[kMaxWarps][3][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int task = blockIdx.x * (blockDim.x >> 5) + warp;
   const int p = task / a.chunks, c = task % a.chunks;
   if (p >= a.count) return;
   const int n = a.n;
@@ -331,110 +328,125 @@ __global__ void __launch_bounds__(kCtaWarps * 32)
     s_st[warp][2][lane] = __int_as_float(0);
   }
   if (r0 >= r1) {
-    if (tid == 0) *out = {kInf, 0x7fffffff, 0x7fffffff};
+    if (lane == 0) *out = {kInf, 0x7fffffff, 0x7fffffff};
     return;
   }
   const uint16_t* tour = a.tours + (size_t)p * a.np;
   const double* dg = a.dcache + (size_t)p * a.np;
   // FILTER32 excludes the structural pairs (i, i+1) (and (0, n-1) below)
   constexpr int kGap = MODE == 2 ? 1 : 0;
-  const int jbase = lane + 32 * warp;  // column of block b: jbase + 128 b
+  unsigned char* wbase = smem + (size_t)warp * a.buf_stride2;
+  float* sdj = (float*)(wbase + kBufs32 * a.buf_stride);  // d_j, fp32
 
-  uint32_t sj[NB];  // s_j = a_{j+1} (gather index of the B term)
-  float dj[NB];
+  constexpr int NH = (NPL + 1) / 2;
+  uint32_t sjp[NH];  // s_j = a_{j+1} for blocks 2h (lo) and 2h+1 (hi)
 #pragma unroll
-  for (int b = 0; b < NB; ++b) {
-    const int j = jbase + 128 * b;
+  for (int h = 0; h < NH; ++h) sjp[h] = 0;
+#pragma unroll
+  for (int m = 0; m < NPL; ++m) {
+    const int j = lane + 32 * m;
     if (j < n) {
-      sj[b] = tour[j + 1 == n ? 0 : j + 1];
-      dj[b] = (float)dg[j];
-    } else {
-      sj[b] = 0;
-      dj[b] = 0.f;
+      const uint32_t s_ = tour[j + 1 == n ? 0 : j + 1];
+      sjp[m / 2] |= (m & 1) ? (s_ << 16) : s_;
     }
   }
-  const int nrows = r1 - r0 + 1;  // cost rows a_r0 .. a_r1
-  auto issue = [&](int q) {
-    const int s = q % kBufs;
-    mbar_expect_tx(&bars[s], a.row_bytes);
-    bulk_g2s(smem + (size_t)s * a.buf_stride,
-             a.cost32 + (size_t)tour[r0 + q] * a.ld32, a.row_bytes, &bars[s]);
+  for (int j = lane; j < 32 * NPL; j += 32)
+    sdj[j] = j < n ? (float)dg[j] : 0.f;
+  auto sj = [&](int m) -> uint32_t {
+    return (m & 1) ? (sjp[m / 2] >> 16) : (sjp[m / 2] & 0xFFFFu);
   };
-  if (tid == 0) {
-    for (int s = 0; s < kBufs; ++s) mbar_init(&bars[s], 1);
+  const int nrows = r1 - r0 + 1;  // cost rows a_r0 .. a_r1
+  uint64_t* wb = bars[warp];
+  auto issue = [&](int q) {
+    const int s_ = q % kBufs32;
+    mbar_expect_tx(&wb[s_], a.row_bytes);
+    bulk_g2s(wbase + (size_t)s_ * a.buf_stride,
+             a.cost32 + (size_t)tour[r0 + q] * a.ld32, a.row_bytes, &wb[s_]);
+  };
+  if (lane == 0) {
+    for (int s_ = 0; s_ < kBufs32; ++s_) mbar_init(&wb[s_], 1);
     fence_barrier_init();
-    for (int q = 0; q < kBufs && q < nrows; ++q) issue(q);
+    for (int q = 0; q < kBufs32 && q < nrows; ++q) issue(q);
   }
-  __syncthreads();
+  __syncwarp();
   auto row = [&](int q) -> const float* {
-    const int s = q % kBufs;
-    mbar_wait(&bars[s], (uint32_t)((q / kBufs) & 1));
-    return (const float*)(smem + (size_t)s * a.buf_stride);
+    const int s_ = q % kBufs32;
+    mbar_wait(&wb[s_], (uint32_t)((q / kBufs32) & 1));
+    return (const float*)(wbase + (size_t)s_ * a.buf_stride);
   };
   // prime: Bv = row a_r0 gathered at s_j (the "B term of row r0 - 1")
-  float Bv[NB];
+  float Bv[NPL];
   {
     const float* R = row(0);
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      Bv[b] = R[sj[b]];
-      if (lane == 31) s_x[0][warp + 4 * b] = Bv[b];
-    }
+    for (int m = 0; m < NPL; ++m) Bv[m] = R[sj(m)];
   }
-  __syncthreads();
 
   float best = kInfF;
   int bi = 0x7fffffff, bj = 0x7fffffff;
   float lim = FLT_MAX;  // FILTER32: best + thr (finite: masked +inf never enters)
   for (int i = r0; i < r1; ++i) {
     const int q = i - r0 + 1;  // ring index of the B row a_{i+1}
-    const int par = (i - r0) & 1;
-    if (tid == 0 && q + kBufs - 1 < nrows) {
+    __syncwarp();
+    if (lane == 0 && q + kBufs32 - 1 < nrows) {
       fence_proxy_async();
-      issue(q + kBufs - 1);  // the slot of row q-1, consumed last iteration
+      issue(q + kBufs32 - 1);  // the slot of row q-1, consumed last iteration
     }
     const float* B = row(q);
+    if (a.stream_only) {
+      if (lane == 0 && B[0] == -1.f) bi = i;  // keep the load
+      continue;
+    }
     const float di = (float)dg[i];
     const int jlim = (MODE == 2 && i == 0) ? n - 1 : n;
     float rbest = kInfF;
     int rj = 0x7fffffff;
+    float rprev = 0.f;  // rotate of the previous block (lane 0's A term)
 #pragma unroll
-    for (int b0 = 0; b0 < NB; b0 += kGroup) {
-      // warp-uniform: largest column of the group
-      if (jbase - lane + 31 + 128 * (b0 + kGroup - 1) > i + kGap) {
-        float tv[kGroup];
+    for (int m0 = 0; m0 < NPL; m0 += kG32) {
+      if (32 * (m0 + kG32) - 1 > i + kGap) {  // warp-uniform: group not dead
+        if (m0 > 0 && !(32 * m0 - 1 > i + kGap))  // previous group was dead
+          rprev = __shfl_sync(0xffffffffu, Bv[m0 - 1], (lane + 31) & 31);
+        // fully live group: every column j > i + gap and < jlim (only the
+        // last block can reach n; row 0 also excludes (0, n-1) in FILTER32)
+        const bool full = (32 * m0 > i + kGap) && (m0 + kG32 < NPL) &&
+                          !(MODE == 2 && i == 0);
+        float tv[kG32];
 #pragma unroll
-        for (int g = 0; g < kGroup; ++g) {
+        for (int g = 0; g < kG32; ++g) {
           tv[g] = kInfF;
-          if (b0 + g < NB) {
-            const int b = b0 + g;
-            const int m = warp + 4 * b;
-            const float r = __shfl_sync(0xffffffffu, Bv[b], (lane + 31) & 31);
-            const float av = lane == 0 ? (m > 0 ? s_x[par][m - 1] : 0.f) : r;
-            const float bv = B[sj[b]];
-            Bv[b] = bv;
-            if (lane == 31) s_x[par ^ 1][m] = bv;
-            const int j = jbase + 128 * b;
-            float t = __fadd_rn(__fsub_rn(av, di), __fsub_rn(bv, dj[b]));
-            t = (j > i + kGap && j < jlim) ? t : kInfF;
-            if (MODE == 1) {
-              const bool lt = t < rbest;
-              rbest = lt ? t : rbest;
-              rj = lt ? j : rj;
-            } else {
-              tv[g] = t;
-            }
+          if (m0 + g < NPL) {
+            const int m = m0 + g;
+            const float r = __shfl_sync(0xffffffffu, Bv[m], (lane + 31) & 31);
+            const float av = lane == 0 ? rprev : r;
+            rprev = r;
+            const float bv = B[sj(m)];
+            Bv[m] = bv;
+            const int j = lane + 32 * m;
+            float t = __fadd_rn(__fsub_rn(av, di), __fsub_rn(bv, sdj[j]));
+            if (!full) t = (j > i + kGap && j < jlim) ? t : kInfF;
+            tv[g] = t;
           }
         }
-        if (MODE == 2) {
-          bool hit = false;
+        if (MODE == 1) {
 #pragma unroll
-          for (int g = 0; g < kGroup; ++g) hit |= tv[g] <= lim;
-          if (hit)
-            lim = cand_group(tv[0], tv[1], tv[2], tv[3], i,
-                             jbase + 128 * b0, 128, lim, a.thr,
-                             &s_cd[warp][0][lane], &s_cij[warp][0][lane],
-                             &s_st[warp][0][lane]);
+          for (int g = 0; g < kG32; ++g) {
+            const bool lt = tv[g] < rbest;
+            rbest = lt ? tv[g] : rbest;
+            rj = lt ? lane + 32 * (m0 + g) : rj;
+          }
+        } else {
+#pragma unroll
+          for (int g4 = 0; g4 < kG32; g4 += 4) {
+            bool hit = false;
+#pragma unroll
+            for (int g = 0; g < 4; ++g) hit |= tv[g4 + g] <= lim;
+            if (hit)
+              lim = cand_group(tv[g4], tv[g4 + 1], tv[g4 + 2], tv[g4 + 3], i,
+                               lane + 32 * (m0 + g4), 32, lim, a.thr,
+                               &s_cd[warp][0][lane], &s_cij[warp][0][lane],
+                               &s_st[warp][0][lane]);
+          }
         }
       }
     }
@@ -443,91 +455,74 @@ __global__ void __launch_bounds__(kCtaWarps * 32)
       bi = i;
       bj = rj;
     }
-    __syncthreads();  // row q consumed by every warp; s_x[par ^ 1] complete
   }
+  __syncwarp();
+  if (MODE == 1) {
+    double bd = best == kInfF ? kInf : (double)best;
+    warp_argmin(bd, bi, bj);
+    if (lane == 0) *out = {bd, bi, bj};
+    return;
+  }
+  // FILTER32: warp minimum, candidate re-evaluation in fp64
+  best = s_st[warp][0][lane];
+  const int ncand = __float_as_int(s_st[warp][1][lane]);
+  if (__any_sync(0xffffffffu, __float_as_int(s_st[warp][2][lane]))) {
+    if (lane == 0) *out = {kInf, kOverflowTag, kOverflowTag};
+    return;
+  }
+  float m = best;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+    m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const float keep = __fadd_ru(m, a.thr);
   double bd = kInf;
   int ei = 0x7fffffff, ej = 0x7fffffff;
-  if (MODE == 1) {
-    bd = best == kInfF ? kInf : (double)best;
-    ei = bi;
-    ej = bj;
-  } else {
-    // FILTER32: CTA minimum, candidate re-evaluation in fp64
-    best = s_st[warp][0][lane];
-    const int ncand = __float_as_int(s_st[warp][1][lane]);
-    if (__syncthreads_or(__float_as_int(s_st[warp][2][lane]))) {
-      if (tid == 0) *out = {kInf, kOverflowTag, kOverflowTag};
-      return;
-    }
-    float m = best;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-      m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) s_m[warp] = m;
-    __syncthreads();
-    m = fminf(fminf(s_m[0], s_m[1]), fminf(s_m[2], s_m[3]));
-    const float keep = __fadd_ru(m, a.thr);
-    for (int k = 0; k < ncand; ++k) {
-      if (s_cd[warp][k][lane] <= keep) {
-        const uint32_t ij = s_cij[warp][k][lane];
-        const int i = (int)(ij >> 16), j = (int)(ij & 0xFFFFu);
-        const int ai = tour[i], aj = tour[j];
-        const int si = tour[i + 1], sjj = tour[j + 1 == n ? 0 : j + 1];
-        double t = __dadd_rn(a.cost[(size_t)ai * a.ld + aj],
-                             a.cost[(size_t)si * a.ld + sjj]);
-        t = __dsub_rn(t, dg[i]);
-        t = __dsub_rn(t, dg[j]);
-        if (res_less(t, i, j, bd, ei, ej)) {
-          bd = t;
-          ei = i;
-          ej = j;
-        }
-      }
-    }
-    // structural pairs, exact from d: (i, i+1) has A = d_i, B = d_{i+1}
-    for (int i = r0 + tid; i < r1; i += kCtaWarps * 32) {
-      if (i + 1 < n) {
-        const double d0 = dg[i], d1 = dg[i + 1];
-        double t = __dadd_rn(d0, d1);
-        t = __dsub_rn(t, d0);
-        t = __dsub_rn(t, d1);
-        if (res_less(t, i, i + 1, bd, ei, ej)) {
-          bd = t;
-          ei = i;
-          ej = i + 1;
-        }
-      }
-    }
-    if (r0 == 0 && tid == 0 && n - 1 > 1) {  // (0, n-1): s_{n-1} = a_0
-      const int j = n - 1;
-      const int a0 = tour[0], aj = tour[j], s0 = tour[1], sjj = tour[0];
-      double t = __dadd_rn(a.cost[(size_t)a0 * a.ld + aj],
-                           a.cost[(size_t)s0 * a.ld + sjj]);
-      t = __dsub_rn(t, dg[0]);
+  for (int k = 0; k < ncand; ++k) {
+    if (s_cd[warp][k][lane] <= keep) {
+      const uint32_t ij = s_cij[warp][k][lane];
+      const int i = (int)(ij >> 16), j = (int)(ij & 0xFFFFu);
+      const int ai = tour[i], aj = tour[j];
+      const int si = tour[i + 1], sjj = tour[j + 1 == n ? 0 : j + 1];
+      double t = __dadd_rn(a.cost[(size_t)ai * a.ld + aj],
+                           a.cost[(size_t)si * a.ld + sjj]);
+      t = __dsub_rn(t, dg[i]);
       t = __dsub_rn(t, dg[j]);
-      if (res_less(t, 0, j, bd, ei, ej)) {
+      if (res_less(t, i, j, bd, ei, ej)) {
         bd = t;
-        ei = 0;
+        ei = i;
         ej = j;
       }
     }
   }
-  warp_argmin(bd, ei, ej);
-  if (lane == 0) {
-    s_rd[warp] = bd;
-    s_ri[warp] = ei;
-    s_rj[warp] = ej;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    for (int w = 1; w < kCtaWarps; ++w)
-      if (res_less(s_rd[w], s_ri[w], s_rj[w], bd, ei, ej)) {
-        bd = s_rd[w];
-        ei = s_ri[w];
-        ej = s_rj[w];
+  // structural pairs, exact from d: (i, i+1) has A = d_i, B = d_{i+1}
+  for (int i = r0 + lane; i < r1; i += 32) {
+    if (i + 1 < n) {
+      const double d0 = dg[i], d1 = dg[i + 1];
+      double t = __dadd_rn(d0, d1);
+      t = __dsub_rn(t, d0);
+      t = __dsub_rn(t, d1);
+      if (res_less(t, i, i + 1, bd, ei, ej)) {
+        bd = t;
+        ei = i;
+        ej = i + 1;
       }
-    *out = {bd, ei, ej};
+    }
   }
+  if (r0 == 0 && lane == 0 && n - 1 > 1) {  // (0, n-1): s_{n-1} = a_0
+    const int j = n - 1;
+    const int a0 = tour[0], aj = tour[j], s0 = tour[1], sjj = tour[0];
+    double t = __dadd_rn(a.cost[(size_t)a0 * a.ld + aj],
+                         a.cost[(size_t)s0 * a.ld + sjj]);
+    t = __dsub_rn(t, dg[0]);
+    t = __dsub_rn(t, dg[j]);
+    if (res_less(t, 0, j, bd, ei, ej)) {
+      bd = t;
+      ei = 0;
+      ej = j;
+    }
+  }
+  warp_argmin(bd, ei, ej);
+  if (lane == 0) *out = {bd, ei, ej};
 }
 
 struct ApplyArgs {
@@ -701,12 +696,13 @@ int two_opt_pick_chunks(int32_t n, int32_t P) {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // fp32 scan: one 4-warp CTA per task, one row ring per CTA
-  size_t per_cta = ring_bytes(n, 4) + 8 * 1024;
-  int ctas_per_sm = (int)(kSmemBudget / per_cta);
-  if (ctas_per_sm < 1) ctas_per_sm = 1;
-  if (ctas_per_sm > 12) ctas_per_sm = 12;
-  int64_t slots = (int64_t)sms * ctas_per_sm;
+  // fp32 scan: one warp per task (row ring + d_j in shared memory)
+  size_t per_warp = (size_t)kBufs32 * round_up((int64_t)round_up(n, 4) * 4, 128) +
+                    4 * (size_t)round_up(n, 32);
+  int warps_per_sm = (int)(kSmemBudget / per_warp);
+  if (warps_per_sm < 1) warps_per_sm = 1;
+  if (warps_per_sm > 16) warps_per_sm = 16;
+  int64_t slots = (int64_t)sms * warps_per_sm;
   int chunks = (int)((4 * slots + P - 1) / P);
   if (chunks < 1) chunks = 1;
   if (chunks > 32) chunks = 32;
@@ -758,6 +754,7 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
   a.res = res;
   a.ctl = ctl;
   a.thr = pl.thr;
+  a.stream_only = getenv("DPSO_SCAN_STREAM_ONLY") ? 1 : 0;
   const int64_t tasks = (int64_t)count * chunks;
   cudaError_t e = cudaSuccess;
   const int npl = npl_for(n);
@@ -793,20 +790,25 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
     } else {
       a.row_bytes = (uint32_t)(round_up(n, 4) * 4);
       a.buf_stride = (uint32_t)round_up(a.row_bytes, 128);
-      const size_t smem = ring_bytes(n, 4);  // one ring per CTA (task)
-      const int blocks = (int)tasks;
-#define SCAN32(NB)                                                         \
+      // per warp: 2-slot row ring + d_j (fp32, 32 * NPL entries)
+      a.buf_stride2 = (uint32_t)(kBufs32 * a.buf_stride +
+                                 round_up((int64_t)32 * std::max(npl, 1) * 4,
+                                          128));
+      const int warps = kMaxWarps;
+      const size_t smem = (size_t)warps * a.buf_stride2;
+      const int blocks = (int)((tasks + warps - 1) / warps);
+#define SCAN32(NPL)                                                        \
   (pl.mode == kScanExact32                                                 \
-       ? launch_scan32_t<NB, 1>(a, kCtaWarps, blocks, smem, s)             \
-       : launch_scan32_t<NB, 2>(a, kCtaWarps, blocks, smem, s))
+       ? launch_scan32_t<NPL, 1>(a, warps, blocks, smem, s)                \
+       : launch_scan32_t<NPL, 2>(a, warps, blocks, smem, s))
       switch (npl) {
-        case 1:
-        case 2:
-        case 4: e = SCAN32(1); break;
-        case 8: e = SCAN32(2); break;
-        case 16: e = SCAN32(4); break;
-        case 32: e = SCAN32(8); break;
-        default: e = SCAN32(16); break;
+        case 1: e = SCAN32(1); break;
+        case 2: e = SCAN32(2); break;
+        case 4: e = SCAN32(4); break;
+        case 8: e = SCAN32(8); break;
+        case 16: e = SCAN32(16); break;
+        case 32: e = SCAN32(32); break;
+        default: e = SCAN32(64); break;
       }
 #undef SCAN32
       // FILTER32 candidate-list overflow: exact fp64 re-scan of those tasks
