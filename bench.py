@@ -84,9 +84,19 @@ def make_matrix(cfg):
     return c, None
 
 
+RNG = "numpy"
+
+
 def solver_params(cfg, P, G, seed):
-    return dict(n_particles=P, max_generations=G, stall_generations=G,
-                use_edge_exchange=cfg.get("ee", True), random_state=seed)
+    p = dict(n_particles=P, max_generations=G, stall_generations=G,
+             use_edge_exchange=cfg.get("ee", True), random_state=seed)
+    return p
+
+
+def gpu_params(cfg, P, G, seed):
+    p = solver_params(cfg, P, G, seed)
+    p["rng"] = RNG
+    return p
 
 
 # ---------------------------------------------------------------- clocks
@@ -240,7 +250,8 @@ def config_dict(cfg_name, cfg, args):
             "generation_schedule": cfg["G"],
             "parallelism": f"islands{args.gpus}" if args.gpus > 1 else "1gpu",
             "exchange_every": args.exchange_every if args.gpus > 1 else None,
-            "rng": "numpy-pcg64-exact",
+            "rng": {"numpy": "numpy-pcg64-exact",
+                    "philox": "philox4x32-10"}[RNG],
             "l2": "flushed between timed steps (256 MiB write)"}
 
 
@@ -276,13 +287,14 @@ def run_ours(args, cfg_name, cfg):
     n, P = cost.shape[0], cfg["P"]
     W, K = args.warmup, args.steps
     G = W + K + args.profile_gens + 1
-    params = solver_params(cfg, P, G, 1000 + rank)
+    params = gpu_params(cfg, P, G, 1000 + rank)
     if seed_tour is not None:
         params["seed_tour"] = seed_tour
     solver = DiscreteSwarmSolver(**params)
     seed_body, n_seed = solver._seed(n)
     ctx = solver._make_context(cost)
-    ctx.set_streams(numpy_stream_states(params["random_state"], P + 2))
+    if RNG == "numpy":
+        ctx.set_streams(numpy_stream_states(params["random_state"], P + 2))
     ctx.init(seed_body, n_seed)
     ex = IslandExchange(ctx, n) if world > 1 else None
 
@@ -382,7 +394,7 @@ def run_ours(args, cfg_name, cfg):
     # RNG states, D2H of tour + convergence inside the timed region)
     if not args.no_e2e:
         Ge = cfg["G"]
-        ep = solver_params(cfg, P, Ge, 7)
+        ep = gpu_params(cfg, P, Ge, 7)
         if seed_tour is not None:
             ep["seed_tour"] = seed_tour
         torch.cuda.synchronize()
@@ -423,6 +435,9 @@ def main():
     ap.add_argument("--profile-gens", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--rng", choices=["numpy", "philox"], default="numpy",
+                    help="numpy: the reference's PCG64 streams bit for bit; "
+                         "philox: counter-based production RNG")
     ap.add_argument("--scan-mode", choices=["auto", "fp64", "exact32",
                                             "filter32"], default="auto",
                     help="force the 2-opt scan mode (default: chosen from "
@@ -431,6 +446,8 @@ def main():
     if args.warmup < 3:
         args.warmup = 3
     cfg = CONFIGS[args.config]
+    global RNG
+    RNG = args.rng
     if args.scan_mode != "auto":
         os.environ["DPSO_SCAN_MODE"] = {"fp64": "0", "exact32": "1",
                                         "filter32": "2"}[args.scan_mode]

@@ -150,6 +150,10 @@ int dpso_nn_tour(const double* dev_cost, int64_t ld, int32_t n, int32_t start,
 int dpso_nn_two_opt(const double* dev_cost, int64_t ld, int32_t n,
                     int32_t* host_tour, double* host_cost, void* cuda_stream);
 
+/* Philox4x32-10 block (host evaluation of the device RNG's code path, for
+ * known-answer tests): out = philox(ctr[4], key = k0 | k1 << 32). */
+int dpso_philox4x32_10(const uint32_t* ctr, uint64_t key, uint32_t* out);
+
 /* Build/version string. */
 const char* dpso_version(void);
 

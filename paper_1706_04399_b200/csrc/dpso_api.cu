@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "dpso_internal.cuh"
+#include "philox.cuh"
 
 using namespace dpso;
 
@@ -111,7 +112,9 @@ Layout make_layout(const dpso_params* prm, int n) {
   L.off_ev_cursor = take(2 * 8 * P);
   L.off_ev_end = take(2 * 8 * P);
   L.off_ev_idx = take(2 * P * np);
-  L.off_mstream = take(prm->use_mutation ? 2 * 4 * mstream_words(n, P) : 0);
+  L.off_mstream = take(prm->use_mutation && prm->rng_mode == DPSO_RNG_NUMPY
+                           ? 2 * 4 * mstream_words(n, P)
+                           : 0);
   L.off_init_cursor = take(8 * P);
   L.off_seed = take(2 * np);
   L.off_cost32 = take(prm->use_edge_exchange ? 4 * (int64_t)n * np : 0);
@@ -218,6 +221,14 @@ extern "C" {
 
 const char* dpso_last_error(void) { return g_err.c_str(); }
 
+int dpso_philox4x32_10(const uint32_t* ctr, uint64_t key, uint32_t* out) {
+  if (!ctr || !out) return fail(DPSO_EINVAL, "null argument");
+  uint32_t c[4] = {ctr[0], ctr[1], ctr[2], ctr[3]};
+  philox4x32_10(c, key);
+  for (int i = 0; i < 4; ++i) out[i] = c[i];
+  return DPSO_OK;
+}
+
 const char* dpso_version(void) {
   return "paper_1706_04399_b200 dpso 0.1.0 (sm_100a)";
 }
@@ -233,8 +244,6 @@ int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
                 size_t workspace_bytes, void* cuda_stream, dpso_ctx** out) {
   int rc = check_params(prm, n);
   if (rc) return rc;
-  if (prm->rng_mode == DPSO_RNG_PHILOX)
-    return fail(DPSO_EINVAL, "rng_mode philox is not available in this build");
   Layout L = make_layout(prm, n);
   if (!dev_workspace || workspace_bytes < L.total)
     return fail(DPSO_EINVAL, "workspace too small");
@@ -303,7 +312,9 @@ int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
   v.ev_end = (uint64_t*)(w + L.off_ev_end);
   v.ev_idx = (uint16_t*)(w + L.off_ev_idx);
   v.mstream = (uint32_t*)(w + L.off_mstream);
-  v.mstream_cap = prm->use_mutation ? mstream_words(n, v.P) : 0;
+  v.mstream_cap = prm->use_mutation && prm->rng_mode == DPSO_RNG_NUMPY
+                      ? mstream_words(n, v.P)
+                      : 0;
   v.init_cursor = (uint64_t*)(w + L.off_init_cursor);
   std::vector<int32_t> rows(L.chunks + 1);
   two_opt_chunk_rows(n, L.chunks, rows.data());
@@ -377,7 +388,8 @@ int dpso_set_streams(dpso_ctx* c, const uint64_t* host_states) {
 int dpso_init(dpso_ctx* c, const int32_t* seed_body, int32_t n_seed) {
   if (!c) return fail(DPSO_EINVAL, "null context");
   if (!c->have_cost) return fail(DPSO_EINVAL, "cost matrix not set");
-  if (!c->have_streams) return fail(DPSO_EINVAL, "rng streams not set");
+  if (!c->have_streams && c->prm.rng_mode == DPSO_RNG_NUMPY)
+    return fail(DPSO_EINVAL, "rng streams not set");
   const int n = c->n;
   if (n_seed < 0 || n_seed > c->prm.n_particles)
     return fail(DPSO_EINVAL, "n_seed out of range");

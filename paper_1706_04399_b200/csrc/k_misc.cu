@@ -17,6 +17,7 @@
 #include <float.h>
 
 #include "dpso_internal.cuh"
+#include "philox.cuh"
 
 namespace dpso {
 
@@ -252,7 +253,29 @@ __global__ void __launch_bounds__(128) k_init_build(SwarmView v,
       for (int i = tid; i < n; i += blockDim.x) body[i] = (uint16_t)i;
     }
     __syncthreads();
-    if (tid == 0) {
+    if (tid == 0 && v.rng_mode == DPSO_RNG_PHILOX) {
+      // production mode: independent Philox draws per particle; one random
+      // swap of the seed (two distinct positions) or a Fisher-Yates shuffle
+      PhiloxStream r;
+      r.init(v.philox_seed, (uint32_t)p, 0u, kTagInit);
+      if (p < n_seed) {
+        if (p > 0 && n > 1) {
+          const uint32_t a = r.bounded((uint32_t)(n - 1));
+          uint32_t b = r.bounded((uint32_t)(n - 2));
+          if (b >= a) ++b;
+          const uint16_t x = body[a];
+          body[a] = body[b];
+          body[b] = x;
+        }
+      } else {
+        for (int j = n - 1; j >= 1; --j) {
+          const uint32_t jj = r.bounded((uint32_t)j);
+          const uint16_t x = body[j];
+          body[j] = body[jj];
+          body[jj] = x;
+        }
+      }
+    } else if (tid == 0) {
       Pcg r;
       r.seek_u32(*v.init_start, v.init_cursor[p]);
       if (p < n_seed) {
@@ -479,7 +502,7 @@ cudaError_t launch_finalize(const SwarmView& v, cudaStream_t s) {
 
 cudaError_t launch_init(const SwarmView& v, const uint16_t* dev_seed,
                         int32_t n_seed, cudaStream_t s) {
-  k_init_walk<<<1, 32, 0, s>>>(v, n_seed);
+  if (v.rng_mode == DPSO_RNG_NUMPY) k_init_walk<<<1, 32, 0, s>>>(v, n_seed);
   size_t smem = round_up((int64_t)2 * v.np, 16) + (size_t)8 * v.np;
   set_dyn_smem((const void*)k_init_build, smem);
   k_init_build<<<v.P, 128, smem, s>>>(v, dev_seed, n_seed);

@@ -19,6 +19,7 @@
 
 #include "dpso_internal.cuh"
 #include "tma.cuh"
+#include "philox.cuh"
 
 namespace dpso {
 
@@ -665,6 +666,51 @@ __global__ void __launch_bounds__(32) k_mut_fix(SwarmView v) {
   v.ctl->mut_pending = 1;  // the next call's walk may start
 }
 
+// Production RNG mode: every event's draws are Philox keyed by (slot,
+// generation), so events are sampled independently with no stream walk:
+// k = integers(1, k_hi + 1) semantics, then numpy's choice(n, 2k, False)
+// algorithm (Floyd + shuffle) on Philox draws.  One warp per event.
+__global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample_philox(
+    SwarmView v, int words_per_warp) {
+  if (!v.ctl->mutating || v.ctl->done) return;
+  extern __shared__ __align__(16) uint32_t sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int e = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (e >= v.ctl->n_events) return;
+  const int n = v.n, P = v.P;
+  uint32_t* bits = sm + (size_t)warp * words_per_warp;
+  uint16_t* sidx = (uint16_t*)(bits + (n + 31) / 32);
+  for (int i = lane; i < (n + 31) / 32; i += 32) bits[i] = 0;
+  __syncwarp();
+  const int slot = v.ev_slot[e];
+  int k = 0;
+  if (lane == 0) {
+    PhiloxStream r;
+    r.init(v.philox_seed, (uint32_t)slot, (uint32_t)v.ctl->gen, kTagMutate);
+    const int k_hi = max(2, n / 4);
+    k = min((int)r.bounded((uint32_t)(k_hi - 1)) + 1, n / 2);
+    v.ev_k[(size_t)v.ctl->mut_cur * P + e] = k;
+    const int size = 2 * k;
+    for (int t = 0; t < size; ++t) {  // Floyd
+      const uint32_t j = (uint32_t)(n - size + t);
+      uint32_t val = r.bounded(j);
+      if (bits[val >> 5] & (1u << (val & 31))) val = j;
+      bits[val >> 5] |= 1u << (val & 31);
+      sidx[t] = (uint16_t)val;
+    }
+    for (int i = size - 1; i >= 1; --i) {  // shuffle
+      const uint32_t j = r.bounded((uint32_t)i);
+      const uint16_t t = sidx[i];
+      sidx[i] = sidx[j];
+      sidx[j] = t;
+    }
+  }
+  k = __shfl_sync(0xffffffffu, k, 0);
+  __syncwarp();
+  uint16_t* idx = v.ev_idx + (size_t)e * v.np;
+  for (int t = lane; t < 2 * k; t += 32) idx[t] = sidx[t];
+}
+
 __global__ void __launch_bounds__(128) k_mut_swap(SwarmView v) {
   if (!v.ctl->mutating || v.ctl->done) return;
   const int e = blockIdx.x;
@@ -717,6 +763,7 @@ int64_t mstream_words(int n, int P) {
 }
 
 cudaError_t launch_mutation_walk(const SwarmView& v, cudaStream_t s) {
+  if (v.rng_mode == DPSO_RNG_PHILOX) return cudaSuccess;  // no stream walk
   const int64_t outs = v.mstream_cap / 2;
   const int64_t threads = (outs + kGenPer - 1) / kGenPer;
   k_mut_gen<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(v);
@@ -743,6 +790,14 @@ cudaError_t launch_mutation_pre(const SwarmView& v, cudaStream_t s) {
 cudaError_t launch_mutation_post(const SwarmView& v, cudaStream_t s) {
   const int P = v.P;
   const int n = v.n;
+  if (v.rng_mode == DPSO_RNG_PHILOX) {
+    const int words = (int)round_up((n + 31) / 32 + (n + 1) / 2, 4);
+    const size_t smem = (size_t)kSampleWarps * words * 4;
+    set_dyn_smem((const void*)k_mut_sample_philox, smem);
+    k_mut_sample_philox<<<(P + kSampleWarps - 1) / kSampleWarps,
+                          kSampleWarps * 32, smem, s>>>(v, words);
+    return cudaGetLastError();
+  }
   // per warp: draw values (<= 2n u32) + Floyd bitmap / tail arange; without
   // room for the draw buffer the warp samples sequentially
   const int scratch_words =

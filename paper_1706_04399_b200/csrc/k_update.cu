@@ -20,10 +20,29 @@
 // it (solver.py:213-216); that path runs the repair sequentially in one
 // thread per particle (k_update_seq) on a bounded per-particle ring.
 #include "dpso_internal.cuh"
+#include "philox.cuh"
 
 namespace dpso {
 
 namespace {
+
+// r1, r2 = p.rng.random(2) (solver.py:191): the particle's numpy stream, or
+// Philox keyed by (particle, generation) in the production mode
+__device__ __forceinline__ void draw_r1r2(const SwarmView& v, int p,
+                                          double* r1, double* r2) {
+  if (v.rng_mode == DPSO_RNG_PHILOX) {
+    PhiloxStream ps;
+    ps.init(v.philox_seed, (uint32_t)p, (uint32_t)v.ctl->gen, kTagUpdate);
+    *r1 = ps.next_double();
+    *r2 = ps.next_double();
+    return;
+  }
+  Pcg r;
+  r.load(v.streams[2 + p]);
+  *r1 = r.next_double();
+  *r2 = r.next_double();
+  r.store(v.streams[2 + p]);
+}
 
 template <int T>
 __device__ __forceinline__ int block_excl_scan(int val, int* s_warp,
@@ -188,11 +207,8 @@ __global__ void __launch_bounds__(T) k_update_w1(SwarmView v, int R) {
     __syncthreads();
     for (int i = tid; i < n; i += T) sposx[sx[i]] = (uint16_t)i;
     if (tid == 0) {
-      Pcg r;
-      r.load(v.streams[2 + p]);
-      double r1 = r.next_double();
-      double r2 = r.next_double();
-      r.store(v.streams[2 + p]);
+      double r1, r2;
+      draw_r1r2(v, p, &r1, &r2);
       s_c[0] = __dmul_rn(v.cognitive, r1);
       s_c[1] = __dmul_rn(v.social, r2);
     }
@@ -248,10 +264,8 @@ __global__ void __launch_bounds__(32) k_update_seq(SwarmView v) {
     for (int i = tid; i < n; i += 32) sx[i] = xg[i];
     __syncwarp();
     if (tid == 0) {
-      Pcg r;
-      r.load(v.streams[2 + p]);
-      double r1 = r.next_double(), r2 = r.next_double();
-      r.store(v.streams[2 + p]);
+      double r1, r2;
+      draw_r1r2(v, p, &r1, &r2);
       double c1 = __dmul_rn(v.cognitive, r1), c2 = __dmul_rn(v.social, r2);
       const int64_t stride = v.vel_cap + 2 * (int64_t)n;
       uint32_t* lst = v.vel + (size_t)p * stride;

@@ -244,6 +244,12 @@ class DiscreteSwarmSolver(BaseEstimator):
             raise ValueError("cost matrix must be finite")
         return X
 
+    def _philox_seed(self) -> int:
+        """64-bit Philox key from random_state (SeedSequence entropy)."""
+        w = np.random.SeedSequence(self.random_state).generate_state(
+            2, np.uint32)
+        return int(w[0]) | (int(w[1]) << 32)
+
     def _params(self) -> "_lib.DpsoParams":
         return _lib.DpsoParams(
             n_particles=int(self.n_particles), inertia=float(self.inertia),
@@ -256,7 +262,7 @@ class DiscreteSwarmSolver(BaseEstimator):
             use_edge_exchange=int(bool(self.use_edge_exchange)),
             parallel=int(bool(self.parallel)),
             rng_mode=_lib.RNG_MODES[self.rng],
-            philox_seed=0)
+            philox_seed=self._philox_seed() if self.rng == "philox" else 0)
 
     def _seed(self, n):
         """solver.py:167-174."""
@@ -287,8 +293,9 @@ class DiscreteSwarmSolver(BaseEstimator):
         seed_body, n_seed = self._seed(n)
         ctx = self._make_context(cost)
         try:
-            ctx.set_streams(numpy_stream_states(self.random_state,
-                                                self.n_particles + 2))
+            if self.rng == "numpy":
+                ctx.set_streams(numpy_stream_states(self.random_state,
+                                                    self.n_particles + 2))
             ctx.init(seed_body, n_seed)
             gens = ctx.run()
             tour, fit, conv = ctx.result()

@@ -76,3 +76,24 @@ def test_estimator_api_cpu():
         DiscreteSwarmSolver(mutation_period=0).fit(np.zeros((3, 3)))
     r = DiscreteSwarmSolver(random_state=0).fit(np.zeros((1, 1)))
     assert r.best_tour_ == (0, 0) and r.n_generations_ == 1
+
+
+def test_philox_known_answers(lib):
+    # Random123 kat_vectors for philox4x32_10
+    import numpy as np
+    kats = [
+        ((0, 0, 0, 0), (0, 0), (0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8)),
+        ((0xffffffff,) * 4, (0xffffffff, 0xffffffff),
+         (0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd)),
+        ((0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344),
+         (0xa4093822, 0x299f31d0),
+         (0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1)),
+    ]
+    for ctr, key, want in kats:
+        c = np.array(ctr, dtype=np.uint32)
+        out = np.zeros(4, dtype=np.uint32)
+        rc = lib.dpso_philox4x32_10(c.ctypes.data_as(ctypes.c_void_p),
+                                    key[0] | (key[1] << 32),
+                                    out.ctypes.data_as(ctypes.c_void_p))
+        assert rc == 0
+        assert tuple(int(v) for v in out) == want
