@@ -59,7 +59,8 @@ struct Layout {
       off_vel, off_vel_len, off_fit, off_pfit, off_dcache, off_gbest,
       off_conv, off_tores, off_chunk_row, off_rank, off_hash, off_flag,
       off_sidx, off_order, off_surv, off_keep, off_ev_slot, off_ev_k,
-      off_ev_cursor, off_ev_end, off_ev_idx, off_mstream, off_init_cursor, off_seed, off_cost32,
+      off_ev_cursor, off_ev_end, off_ev_idx, off_mstream, off_init_buf,
+      off_init_state, off_init_cursor, off_seed, off_cost32,
       off_stats, total;
   int64_t vel_cap;
   int chunks;
@@ -116,6 +117,8 @@ Layout make_layout(const dpso_params* prm, int n) {
                            ? 2 * 4 * mstream_words(n, P)
                            : 0);
   L.off_init_cursor = take(8 * P);
+  L.off_init_buf = take(prm->rng_mode == DPSO_RNG_NUMPY ? 4 * init_buf_words(n, P) : 0);
+  L.off_init_state = take(64);
   L.off_seed = take(2 * np);
   L.off_cost32 = take(prm->use_edge_exchange ? 4 * (int64_t)n * np : 0);
   L.off_stats = take(sizeof(CostStats));
@@ -316,6 +319,9 @@ int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
                       ? mstream_words(n, v.P)
                       : 0;
   v.init_cursor = (uint64_t*)(w + L.off_init_cursor);
+  v.init_buf = (uint32_t*)(w + L.off_init_buf);
+  v.init_buf_cap = prm->rng_mode == DPSO_RNG_NUMPY ? init_buf_words(n, v.P) : 0;
+  v.init_state = (void*)(w + L.off_init_state);
   std::vector<int32_t> rows(L.chunks + 1);
   two_opt_chunk_rows(n, L.chunks, rows.data());
   if ((rc = sync_in(c))) {

@@ -125,6 +125,9 @@ struct SwarmView {
   uint32_t* mstream;   // [2] generated mutation-stream span (u32)
   int64_t mstream_cap; // u32 capacity of one mstream buffer
   uint64_t* init_cursor;
+  uint32_t* init_buf;  // generated init-stream window (u32)
+  int64_t init_buf_cap;
+  void* init_state;    // InitScanState
 };
 
 // ---- kernel launchers (each .cu owns its kernels) -------------------------
@@ -139,6 +142,7 @@ cudaError_t launch_mutation(const SwarmView& v, cudaStream_t s);
 cudaError_t launch_mutation_walk(const SwarmView& v, cudaStream_t s);
 cudaError_t launch_mutation_swap(const SwarmView& v, cudaStream_t s);
 int64_t mstream_words(int n, int P);
+int64_t init_buf_words(int n, int P);
 cudaError_t launch_mutation_pre(const SwarmView& v, cudaStream_t s);
 cudaError_t launch_mutation_post(const SwarmView& v, cudaStream_t s);
 cudaError_t launch_select(const SwarmView& v, bool finalize, cudaStream_t s);

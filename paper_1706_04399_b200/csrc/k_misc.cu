@@ -7,8 +7,9 @@
 //   k_finalize      argmin again after 2-opt (solver.py:318-319), gbest copy
 //                   from the current position, stall, convergence, stall
 //                   break (solver.py:320-328)
-//   k_init_walk     one pass over the init stream recording where each
-//                   particle's draws start (solver.py:176-183)
+//   k_init_gen/scan generated init-stream windows + one-thread acceptance
+//                   scan recording where each particle's draws start
+//                   (solver.py:176-183)
 //   k_init_build    per particle: seed / one-swap seed / permutation(n),
 //                   fitness, pbest = self, vmap = identity (solver.py:37-45)
 //   k_init_best     initial gbest = first minimum (solver.py:284-287)
@@ -174,69 +175,128 @@ __global__ void __launch_bounds__(kRed) k_finalize(SwarmView v) {
 
 // ---- init (numpy streams) --------------------------------------------------
 
-// Counts next32() calls so each particle's first draw can be located.
-struct CountingPcg {
-  Pcg r;
-  uint64_t q;
-  __device__ uint32_t next32() {
-    ++q;
-    return r.next32();
-  }
-  __device__ uint32_t lemire32(uint32_t rng) {
-    const uint32_t rng_excl = rng + 1u;
-    uint64_t m = (uint64_t)next32() * rng_excl;
-    uint32_t leftover = (uint32_t)m;
-    if (leftover < rng_excl) {
-      const uint32_t threshold = (0xFFFFFFFFu - rng) % rng_excl;
-      while (leftover < threshold) {
-        m = (uint64_t)next32() * rng_excl;
-        leftover = (uint32_t)m;
-      }
-    }
-    return (uint32_t)(m >> 32);
-  }
-  __device__ uint32_t bounded(uint32_t rng) {
-    if (rng == 0) return 0;
-    if (rng == 0xFFFFFFFFu) return next32();
-    return lemire32(rng);
-  }
-  __device__ uint32_t interval(uint32_t mx) {
-    if (mx == 0) return 0;
-    uint32_t mask = mx;
-    mask |= mask >> 1;
-    mask |= mask >> 2;
-    mask |= mask >> 4;
-    mask |= mask >> 8;
-    mask |= mask >> 16;
-    uint32_t v;
-    while ((v = (next32() & mask)) > mx) {
-    }
-    return v;
-  }
+// ---- init stream walk over a generated window buffer -----------------------
+// The init stream (solver.py:176-183) is one numpy stream consumed by all
+// particles in order, so where particle p's draws start depends on every
+// earlier particle.  k_init_gen writes a window of the stream grid-wide;
+// k_init_scan (one thread) runs numpy's acceptance tests over it from
+// registers filled by 16-byte loads, records each particle's first draw and
+// keeps its state on the device so it resumes in the next window.  The
+// builder (k_init_build) then regenerates each particle's draws from its
+// cursor by jump-ahead, in parallel.
+struct InitScanState {
+  int64_t q;      // u32 draws consumed
+  int32_t p;      // particle in progress
+  int32_t step;   // permutation: current max index i; seed: draw t (0..2)
+  int32_t fresh;  // particle p not started yet
+  int32_t done;
 };
 
-__global__ void k_init_walk(SwarmView v, int n_seed) {
+constexpr int kInitGenPer = 64;
+
+__global__ void __launch_bounds__(256) k_init_gen(SwarmView v, int64_t win0) {
+  const PcgState g = *v.init_start;
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t outs = v.init_buf_cap / 2;
+  const int64_t o0 = c * kInitGenPer;
+  if (o0 >= outs) return;
+  const u128 inc = {g.inc_hi, g.inc_lo};
+  // window starts at fresh u32 index win0 (even): output win0/2 (0-based)
+  u128 st = pcg_advance({g.state_hi, g.state_lo}, inc,
+                        (uint64_t)(win0 / 2 + o0 + 1));
+  const u128 M = pcg_mult();
+  uint2* out = reinterpret_cast<uint2*>(v.init_buf);
+  for (int r = 0; r < kInitGenPer && o0 + r < outs; ++r) {
+    const uint64_t o = pcg_output(st);
+    out[o0 + r] = make_uint2((uint32_t)o, (uint32_t)(o >> 32));
+    st = add128(mul128(st, M), inc);
+  }
+}
+
+__global__ void k_init_scan(SwarmView v, int n_seed, int64_t win0,
+                            InitScanState* stp) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const int n = v.n;
-  *v.init_start = v.streams[0];  // keep the start of the init stream
-  CountingPcg cr;
-  cr.r.load(v.streams[0]);
-  cr.q = 0;
-  for (int i = 0; i < v.P; ++i) {
-    v.init_cursor[i] = cr.q;
-    if (i < n_seed) {
-      if (i > 0 && n > 1) {
-        // choice(n, 2, replace=False): Floyd (2 draws) + shuffle (1 draw)
-        cr.bounded((uint32_t)(n - 2));
-        cr.bounded((uint32_t)(n - 1));
-        cr.bounded(1u);
-      }
+  InitScanState st = *stp;
+  if (st.done) return;
+  const int n = v.n, P = v.P;
+  const PcgState& g = *v.init_start;
+  const int64_t h = (int64_t)g.has_uint32;
+  const uint32_t ub = (uint32_t)g.uinteger;
+  const int64_t wend = win0 + v.init_buf_cap;  // fresh index past the window
+  const uint4* buf4 = reinterpret_cast<const uint4*>(v.init_buf);
+  // particle setup: permutation step = n-1 (max index); seed step = 0
+  auto start = [&](int p) {
+    v.init_cursor[p] = (uint64_t)st.q;
+    st.fresh = 0;
+    if (p < n_seed) {
+      st.step = (p > 0 && n > 1) ? 0 : 3;  // 3 = no draws
     } else {
-      for (int j = n - 1; j >= 1; --j) cr.interval((uint32_t)j);
+      st.step = n - 1;
+    }
+  };
+  auto finished = [&](int p) -> bool {
+    return p < n_seed ? st.step >= 3 : st.step <= 0;
+  };
+  while (st.p < P) {
+    if (st.fresh) start(st.p);
+    if (finished(st.p)) {
+      ++st.p;
+      st.fresh = 1;
+      continue;
+    }
+    // seed choice(n, 2): bounds n-2 (no draw when 0), n-1, then 1
+    if (st.p < n_seed && st.step == 0 && n - 2 == 0) {
+      st.step = 1;
+      continue;
+    }
+    // next draw
+    uint32_t u;
+    if (st.q < h) {
+      u = ub;
+    } else {
+      const int64_t f = st.q - h;
+      if (f >= wend) break;  // window exhausted: resume after the next gen
+      const uint4 w = buf4[(f - win0) >> 2];
+      const int k = (int)((f - win0) & 3);
+      u = k == 0 ? w.x : k == 1 ? w.y : k == 2 ? w.z : w.w;
+    }
+    ++st.q;
+    if (st.p < n_seed) {
+      const uint32_t rng = st.step == 0 ? (uint32_t)(n - 2)
+                           : st.step == 1 ? (uint32_t)(n - 1)
+                                          : 1u;
+      if (!lemire_rejects(u, rng)) ++st.step;
+    } else {
+      uint32_t mask = (uint32_t)st.step;
+      mask |= mask >> 1;
+      mask |= mask >> 2;
+      mask |= mask >> 4;
+      mask |= mask >> 8;
+      mask |= mask >> 16;
+      if ((u & mask) <= (uint32_t)st.step) --st.step;
     }
   }
-  cr.r.store(v.streams[0]);
+  if (st.p >= P) {
+    st.done = 1;
+    Pcg r;
+    r.seek_u32(g, (uint64_t)st.q);
+    r.store(v.streams[0]);
+  }
+  *stp = st;
 }
+
+__global__ void k_init_scan_begin(SwarmView v, InitScanState* stp) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  *v.init_start = v.streams[0];  // keep the start of the init stream
+  InitScanState st;
+  st.q = 0;
+  st.p = 0;
+  st.step = 0;
+  st.fresh = 1;
+  st.done = 0;
+  *stp = st;
+}
+
 
 __global__ void __launch_bounds__(128) k_init_build(SwarmView v,
                                                     const uint16_t* seed,
@@ -245,7 +305,6 @@ __global__ void __launch_bounds__(128) k_init_build(SwarmView v,
   const int n = v.n, np = v.np, tid = threadIdx.x;
   uint16_t* body = (uint16_t*)smem;
   double* sd = (double*)(smem + round_up((int64_t)2 * np, 16));
-  __shared__ int s_flag;
   for (int p = blockIdx.x; p < v.P; p += gridDim.x) {
     if (p < n_seed) {
       for (int i = tid; i < n; i += blockDim.x) body[i] = seed[i];
@@ -323,7 +382,6 @@ __global__ void __launch_bounds__(128) k_init_build(SwarmView v,
     }
     __syncthreads();
   }
-  (void)s_flag;
 }
 
 __global__ void __launch_bounds__(kRed) k_init_best(SwarmView v) {
@@ -500,13 +558,37 @@ cudaError_t launch_finalize(const SwarmView& v, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// Host loop over init-stream windows (one sync per window; init runs once).
 cudaError_t launch_init(const SwarmView& v, const uint16_t* dev_seed,
                         int32_t n_seed, cudaStream_t s) {
-  if (v.rng_mode == DPSO_RNG_NUMPY) k_init_walk<<<1, 32, 0, s>>>(v, n_seed);
-  size_t smem = round_up((int64_t)2 * v.np, 16) + (size_t)8 * v.np;
+  if (v.rng_mode == DPSO_RNG_NUMPY) {
+    InitScanState* stp = reinterpret_cast<InitScanState*>(v.init_state);
+    k_init_scan_begin<<<1, 32, 0, s>>>(v, stp);
+    InitScanState h;
+    for (int64_t win0 = 0;; win0 += v.init_buf_cap) {
+      const int64_t outs = v.init_buf_cap / 2;
+      const int64_t thr = (outs + kInitGenPer - 1) / kInitGenPer;
+      k_init_gen<<<(unsigned)((thr + 255) / 256), 256, 0, s>>>(v, win0);
+      k_init_scan<<<1, 32, 0, s>>>(v, n_seed, win0, stp);
+      cudaError_t e = cudaMemcpyAsync(&h, stp, sizeof h,
+                                      cudaMemcpyDeviceToHost, s);
+      if (!e) e = cudaStreamSynchronize(s);
+      if (e) return e;
+      if (h.done) break;
+    }
+  }
+  const size_t smem = round_up((int64_t)2 * v.np, 16) + (size_t)8 * v.np;
   set_dyn_smem((const void*)k_init_build, smem);
   k_init_build<<<v.P, 128, smem, s>>>(v, dev_seed, n_seed);
   return cudaGetLastError();
+}
+
+int64_t init_buf_words(int n, int P) {
+  // expected need ~1.4 n per permutation; the scan resumes across windows
+  int64_t want = (int64_t)P * (2 * (int64_t)n + 64) + 4096;
+  const int64_t cap = 32ll << 20;  // 128 MiB window
+  want = want < cap ? want : cap;
+  return round_up(want, 8);
 }
 
 cudaError_t launch_init_best(const SwarmView& v, cudaStream_t s) {
