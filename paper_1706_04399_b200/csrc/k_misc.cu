@@ -213,9 +213,17 @@ __global__ void __launch_bounds__(256) k_init_gen(SwarmView v, int64_t win0) {
   }
 }
 
-__global__ void k_init_scan(SwarmView v, int n_seed, int64_t win0,
-                            InitScanState* stp) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// One warp.  Fast path (a permutation that still needs >= 32 accepts):
+// lane l takes draw l of a 32-draw chunk and assumes every earlier draw in
+// the chunk was accepted, which fixes its max index i_l = i - K - (l - s)
+// and mask; a ballot finds the first lane whose draw is genuinely rejected,
+// and the scan resumes after it.  (#rejections + 1) ballot rounds resolve a
+// chunk.  Seeded particles and permutation tails take the one-lane path.
+__global__ void __launch_bounds__(32) k_init_scan(SwarmView v, int n_seed,
+                                                  int64_t win0,
+                                                  InitScanState* stp) {
+  if (blockIdx.x != 0) return;
+  const int lane = threadIdx.x;
   InitScanState st = *stp;
   if (st.done) return;
   const int n = v.n, P = v.P;
@@ -223,42 +231,73 @@ __global__ void k_init_scan(SwarmView v, int n_seed, int64_t win0,
   const int64_t h = (int64_t)g.has_uint32;
   const uint32_t ub = (uint32_t)g.uinteger;
   const int64_t wend = win0 + v.init_buf_cap;  // fresh index past the window
-  const uint4* buf4 = reinterpret_cast<const uint4*>(v.init_buf);
-  // particle setup: permutation step = n-1 (max index); seed step = 0
-  auto start = [&](int p) {
-    v.init_cursor[p] = (uint64_t)st.q;
-    st.fresh = 0;
-    if (p < n_seed) {
-      st.step = (p > 0 && n > 1) ? 0 : 3;  // 3 = no draws
-    } else {
-      st.step = n - 1;
-    }
-  };
-  auto finished = [&](int p) -> bool {
-    return p < n_seed ? st.step >= 3 : st.step <= 0;
+  const uint32_t* buf = v.init_buf;
+  auto mask_of = [](uint32_t x) {
+    x |= x >> 1;
+    x |= x >> 2;
+    x |= x >> 4;
+    x |= x >> 8;
+    x |= x >> 16;
+    return x;
   };
   while (st.p < P) {
-    if (st.fresh) start(st.p);
-    if (finished(st.p)) {
+    if (st.fresh) {
+      if (lane == 0) v.init_cursor[st.p] = (uint64_t)st.q;
+      st.fresh = 0;
+      if (st.p < n_seed)
+        st.step = (st.p > 0 && n > 1) ? 0 : 3;  // 3 = no draws
+      else
+        st.step = n - 1;
+    }
+    if (st.p < n_seed ? st.step >= 3 : st.step <= 0) {
       ++st.p;
       st.fresh = 1;
       continue;
     }
-    // seed choice(n, 2): bounds n-2 (no draw when 0), n-1, then 1
-    if (st.p < n_seed && st.step == 0 && n - 2 == 0) {
-      st.step = 1;
+    const int64_t f = st.q - h;
+    if (st.p >= n_seed && st.step >= 32 && f >= 0 && f + 32 <= wend) {
+      // warp-speculative chunks of 32 draws while the permutation needs
+      // >= 32 more accepts; the next chunk is prefetched into a register
+      int i0 = st.step;
+      int64_t ff = f;
+      uint32_t u = buf[ff - win0 + lane];
+      while (i0 >= 32 && ff + 32 <= wend) {
+        const uint32_t un =
+            ff + 64 <= wend ? buf[ff + 32 - win0 + lane] : 0u;
+        int K = 0, s = 0;
+        for (;;) {
+          const int il = i0 - K - (lane - s);  // > 0: i0 >= 32
+          const uint32_t mask = 0xFFFFFFFFu >> __clz(il);
+          const bool rej = lane >= s && (u & mask) > (uint32_t)il;
+          const unsigned bal = __ballot_sync(0xffffffffu, rej);
+          if (bal == 0) {
+            K += 32 - s;
+            break;
+          }
+          const int fl = __ffs(bal) - 1;
+          K += fl - s;
+          s = fl + 1;
+          if (s == 32) break;
+        }
+        i0 -= K;
+        ff += 32;
+        u = un;
+      }
+      st.step = i0;
+      st.q = ff + h;
       continue;
     }
-    // next draw
+    // one-lane path: a single draw
+    if (st.p < n_seed && st.step == 0 && n - 2 == 0) {
+      st.step = 1;  // bounded(0) takes no draw
+      continue;
+    }
     uint32_t u;
     if (st.q < h) {
       u = ub;
     } else {
-      const int64_t f = st.q - h;
       if (f >= wend) break;  // window exhausted: resume after the next gen
-      const uint4 w = buf4[(f - win0) >> 2];
-      const int k = (int)((f - win0) & 3);
-      u = k == 0 ? w.x : k == 1 ? w.y : k == 2 ? w.z : w.w;
+      u = buf[f - win0];
     }
     ++st.q;
     if (st.p < n_seed) {
@@ -267,22 +306,18 @@ __global__ void k_init_scan(SwarmView v, int n_seed, int64_t win0,
                                           : 1u;
       if (!lemire_rejects(u, rng)) ++st.step;
     } else {
-      uint32_t mask = (uint32_t)st.step;
-      mask |= mask >> 1;
-      mask |= mask >> 2;
-      mask |= mask >> 4;
-      mask |= mask >> 8;
-      mask |= mask >> 16;
-      if ((u & mask) <= (uint32_t)st.step) --st.step;
+      if ((u & mask_of((uint32_t)st.step)) <= (uint32_t)st.step) --st.step;
     }
   }
-  if (st.p >= P) {
-    st.done = 1;
-    Pcg r;
-    r.seek_u32(g, (uint64_t)st.q);
-    r.store(v.streams[0]);
+  if (lane == 0) {
+    if (st.p >= P) {
+      st.done = 1;
+      Pcg r;
+      r.seek_u32(g, (uint64_t)st.q);
+      r.store(v.streams[0]);
+    }
+    *stp = st;
   }
-  *stp = st;
 }
 
 __global__ void k_init_scan_begin(SwarmView v, InitScanState* stp) {
