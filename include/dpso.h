@@ -150,6 +150,18 @@ int dpso_nn_tour(const double* dev_cost, int64_t ld, int32_t n, int32_t start,
 int dpso_nn_two_opt(const double* dev_cost, int64_t ld, int32_t n,
                     int32_t* host_tour, double* host_cost, void* cuda_stream);
 
+/* Cost-matrix build: replaces build_graph's pairwise A* loop (graph.py:41-78,
+ * voxel.py:112-172).  dev_occ: nx*ny*nz occupancy (C order, 1 = occupied);
+ * host_vox: n viewpoint voxels (x, y, z); dev_cost: n x ld fp64 output
+ * (symmetric, zero diagonal, blocked pairs = 1e3 * n * max_finite or 1e6);
+ * dev_virtual: optional n*n uint8 mask; *host_vcost: the virtual cost.
+ * Costs are the admissible-A* / Dijkstra costs (exact fp path sums). */
+int dpso_build_cost(const uint8_t* dev_occ, int32_t nx, int32_t ny,
+                    int32_t nz, const double* host_weights,
+                    const int32_t* host_vox, int32_t n, double* dev_cost,
+                    int64_t ld, uint8_t* dev_virtual, double* host_vcost,
+                    void* cuda_stream);
+
 /* Philox4x32-10 block (host evaluation of the device RNG's code path, for
  * known-answer tests): out = philox(ctr[4], key = k0 | k1 << 32). */
 int dpso_philox4x32_10(const uint32_t* ctr, uint64_t key, uint32_t* out);

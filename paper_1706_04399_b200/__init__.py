@@ -7,6 +7,7 @@ versions of the helpers the reference's baselines and tests use.
 from .solver import DiscreteSwarmSolver, SolveReport, solve_matrix
 from .kernels import (best_exchange_batch, nearest_neighbor_tour,
                       nearest_neighbor_two_opt, tour_cost_batch)
+from .graph import TourGraph, build_cost_matrix, build_graph
 
 __version__ = "0.1.0"
 
@@ -14,4 +15,5 @@ __all__ = [
     "DiscreteSwarmSolver", "SolveReport", "solve_matrix",
     "best_exchange_batch", "nearest_neighbor_tour",
     "nearest_neighbor_two_opt", "tour_cost_batch",
+    "TourGraph", "build_cost_matrix", "build_graph",
 ]

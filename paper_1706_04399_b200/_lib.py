@@ -61,6 +61,8 @@ _SIG = {
     "dpso_best_exchange_batch": (_I32, [_P, _I64, _I32, _P, _I32, _P, _P]),
     "dpso_nn_tour": (_I32, [_P, _I64, _I32, _I32, _P, _P]),
     "dpso_nn_two_opt": (_I32, [_P, _I64, _I32, _P, _P, _P]),
+    "dpso_build_cost": (_I32, [_P, _I32, _I32, _I32, _P, _P, _I32, _P, _I64,
+                                _P, _P, _P]),
     "dpso_philox4x32_10": (_I32, [_P, ctypes.c_uint64, _P]),
     "dpso_version": (ctypes.c_char_p, []),
 }

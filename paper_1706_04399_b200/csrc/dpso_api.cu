@@ -224,6 +224,42 @@ extern "C" {
 
 const char* dpso_last_error(void) { return g_err.c_str(); }
 
+int dpso_build_cost(const uint8_t* dev_occ, int32_t nx, int32_t ny,
+                    int32_t nz, const double* host_weights,
+                    const int32_t* host_vox, int32_t n, double* dev_cost,
+                    int64_t ld, uint8_t* dev_virtual, double* host_vcost,
+                    void* cuda_stream) {
+  if (!dev_occ || !host_weights || !host_vox || !dev_cost || !host_vcost ||
+      n < 1 || nx < 1 || ny < 1 || nz < 1 || ld < n)
+    return fail(DPSO_EINVAL, "bad arguments");
+  if ((int64_t)nx * ny * nz >= (1ll << 31))
+    return fail(DPSO_EINVAL, "grid too large for 32-bit voxel indices");
+  for (int i = 0; i < 3; ++i)
+    if (!(host_weights[i] >= 0.0))
+      return fail(DPSO_EINVAL, "axis weights must be non-negative");
+  std::vector<int64_t> lin(n);
+  for (int j = 0; j < n; ++j) {
+    const int x = host_vox[3 * j], y = host_vox[3 * j + 1],
+              z = host_vox[3 * j + 2];
+    if (x < 0 || x >= nx || y < 0 || y >= ny || z < 0 || z >= nz)
+      return fail(DPSO_EINVAL, "viewpoint voxel outside the grid");
+    lin[j] = ((int64_t)x * ny + y) * nz + z;
+  }
+  int bad = -1;
+  cudaError_t e = build_cost_sssp(dev_occ, nx, ny, nz, host_weights,
+                                  lin.data(), n, dev_cost, ld, dev_virtual,
+                                  host_vcost, &bad, (cudaStream_t)cuda_stream);
+  if (e) return cuda_fail(e, "build_cost_sssp");
+  if (bad >= 0) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "viewpoint %d maps to occupied voxel (%d, %d, %d)",
+             bad, host_vox[3 * bad], host_vox[3 * bad + 1],
+             host_vox[3 * bad + 2]);
+    return fail(DPSO_EINVAL, buf);
+  }
+  return DPSO_OK;
+}
+
 int dpso_philox4x32_10(const uint32_t* ctr, uint64_t key, uint32_t* out) {
   if (!ctr || !out) return fail(DPSO_EINVAL, "null argument");
   uint32_t c[4] = {ctr[0], ctr[1], ctr[2], ctr[3]};

@@ -174,6 +174,11 @@ cudaError_t launch_pysum_tour(const double* cost, int64_t ld, int32_t n,
 // Opt a kernel in to `bytes` of dynamic shared memory (cached per kernel;
 // static shared memory counts against the same limit, so always opt in).
 cudaError_t set_dyn_smem(const void* kernel, size_t bytes);
+cudaError_t build_cost_sssp(const uint8_t* dev_occ, int nx, int ny, int nz,
+                            const double* w, const int64_t* host_vox, int n,
+                            double* dev_cost, int64_t ld, uint8_t* dev_virtual,
+                            double* host_vcost, int* bad_viewpoint,
+                            cudaStream_t s);
 int two_opt_chunk_rows(int32_t n, int32_t chunks, int32_t* rows);
 int two_opt_pick_chunks(int32_t n, int32_t P);
 

@@ -1,0 +1,73 @@
+"""Cost-matrix build on the device (replaces graph.py:41-78's pairwise A*).
+
+``build_cost_matrix(occupancy, viewpoint_voxels, weights)`` returns
+``(cost, virtual, virtual_cost)`` with the reference's semantics:
+cost[i][j] = cost[j][i] = admissible-A* (= Dijkstra) motion cost on the
+26-connected free-voxel graph (voxel.py:112-172), zero diagonal, blocked
+pairs at ``1e3 * n * max_finite`` (1e6 when no finite edge) and flagged in
+``virtual``.  ``build_graph(plan, grid, weights)`` mirrors the reference
+signature for callers holding the reference's CoveragePlan/VoxelGrid.
+Per-pair waypoint legs (``TourGraph.legs``) are not produced: the
+reference's CLI needs them only for the final tour's N edges.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .solver import _torch
+
+
+@dataclass(frozen=True)
+class TourGraph:
+    """graph.py:22-38 (without legs)."""
+    n_nodes: int
+    cost: np.ndarray
+    virtual: np.ndarray
+    virtual_cost: float
+    legs: dict = field(default_factory=dict)
+
+
+def build_cost_matrix(occupancy: np.ndarray, viewpoint_voxels, weights,
+                      device=None):
+    torch = _torch()
+    occ = np.ascontiguousarray(np.asarray(occupancy, dtype=bool),
+                               dtype=np.uint8)
+    if occ.ndim != 3:
+        raise ValueError("occupancy must be a 3-D grid")
+    vox = np.ascontiguousarray(np.asarray(viewpoint_voxels, dtype=np.int32)
+                               .reshape(-1, 3))
+    n = vox.shape[0]
+    w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
+    dev = torch.device(device) if device is not None else torch.device(
+        "cuda", torch.cuda.current_device())
+    docc = torch.from_numpy(occ.ravel()).to(dev)
+    ld = (n + 7) // 8 * 8
+    cost = torch.zeros((n, ld), dtype=torch.float64, device=dev)
+    virt = torch.zeros((n, n), dtype=torch.uint8, device=dev)
+    vcost = ctypes.c_double(0.0)
+    nx, ny, nz = occ.shape
+    _lib.check(_lib.load().dpso_build_cost(
+        docc.data_ptr(), nx, ny, nz, w.ctypes.data_as(ctypes.c_void_p),
+        vox.ctypes.data_as(ctypes.c_void_p), n, cost.data_ptr(), ld,
+        virt.data_ptr(), ctypes.byref(vcost),
+        torch.cuda.current_stream(dev).cuda_stream))
+    return (cost[:, :n].cpu().numpy(), virt.cpu().numpy().astype(bool),
+            float(vcost.value))
+
+
+def build_graph(plan, grid, weights, heuristic_mode: str = "admissible"):
+    """graph.py:41-78 signature; duck-typed plan.viewpoints / grid."""
+    if heuristic_mode != "admissible":
+        raise ValueError("the device build computes exact (admissible) "
+                         "costs; the order-dependent 'paper' heuristic is "
+                         "not reproduced")
+    vox = [grid.point_to_voxel(vp.position) for vp in plan.viewpoints]
+    cost, virtual, vcost = build_cost_matrix(grid.occupancy, vox, weights)
+    cost.setflags(write=False)
+    virtual.setflags(write=False)
+    return TourGraph(n_nodes=len(vox), cost=cost, virtual=virtual,
+                     virtual_cost=vcost)
