@@ -339,58 +339,83 @@ struct StreamView {
   }
 };
 
-// Chain of k-draws from (e0, q0) for events e0..e_end-1, one thread, ring of
-// stream segments in shared memory.  Returns false on buffer overflow.
+// Exact chain of mutation events e0..e_end-1 from stream position q0, one
+// warp, with the stream segments in an 8-slot shared-memory ring fed by
+// cp.async.bulk.  Every lane runs the same control flow; lane 0 writes the
+// records.  Each event's k-draw is a Lemire draw with redraws; then the warp
+// checks the event's Floyd/shuffle draws for Lemire redraws in parallel, so
+// the event's exact end is known: D draws when nothing is redrawn (the common
+// case), otherwise the event is consumed sequentially.  Returns false on
+// buffer overflow (the exact sequential fallback then runs).
 __device__ bool chain_events(const SwarmView& v, const MutBufs& b,
                              StreamView sv, int e0, int64_t q0, int e_end,
                              uint32_t* ring, uint64_t* bars) {
+  const int lane = threadIdx.x & 31;
   const int n = v.n;
   const int k_hi = max(2, n / 4);
   const uint32_t rng_k = (uint32_t)(k_hi - 1);
   const int64_t nseg_total = (sv.cap + kSeg - 1) / kSeg;
   const int64_t f0 = q0 - sv.h < 0 ? 0 : q0 - sv.h;
   const int64_t s_first = f0 / kSeg;
-  int64_t next_issue = s_first;
-  for (int b = 0; b < kNSeg; ++b) mbar_init(&bars[b], 1);
-  fence_barrier_init();
+  int64_t next_issue = s_first;  // uniform across the warp
+  int64_t ready = s_first - 1;   // segments <= ready have been waited on
+  if (lane == 0) {
+    for (int i = 0; i < kNSeg; ++i) mbar_init(&bars[i], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  auto slot_parity = [&](int64_t sg, int* slot) -> uint32_t {
+    *slot = (int)(sg & (kNSeg - 1));
+    const int64_t first =
+        s_first + ((*slot - s_first) % kNSeg + kNSeg) % kNSeg;
+    return (uint32_t)(((sg - first) / kNSeg) & 1);
+  };
   auto issue = [&]() {
-    if (next_issue < nseg_total) {
-      const int slot = (int)(next_issue % kNSeg);
+    if (lane == 0 && next_issue < nseg_total) {
+      const int slot = (int)(next_issue & (kNSeg - 1));
+      fence_proxy_async();
       mbar_expect_tx(&bars[slot], kSeg * 4);
       bulk_g2s(ring + (size_t)slot * kSeg, sv.buf + next_issue * kSeg,
                kSeg * 4, &bars[slot]);
     }
     ++next_issue;
   };
-  for (int b = 0; b < kNSeg; ++b) issue();
-  // current segment (waited on once) and its shared-memory base
-  int64_t cur_seg = -1;
-  const uint32_t* seg = nullptr;
-  auto get = [&](int64_t q, uint32_t* out) -> bool {
-    if (q < sv.h) {
-      *out = sv.ub;
+  for (int i = 0; i < kNSeg; ++i) issue();
+  // make fresh positions [flo, fend) readable by every lane; the chain only
+  // moves forward, so slots below flo's segment are recycled
+  // segments are issued and waited on strictly in order; all segments
+  // <= ready are complete
+  auto wait_upto = [&](int64_t sg_hi) {
+    for (int64_t sg = ready + 1; sg <= sg_hi; ++sg) {
+      if (sg >= nseg_total) break;
+      int slot;
+      const uint32_t par = slot_parity(sg, &slot);
+      mbar_wait(&bars[slot], par);
+    }
+    if (sg_hi > ready) ready = sg_hi;
+  };
+  auto ensure = [&](int64_t flo, int64_t fend) -> bool {
+    const int64_t slo = flo < 0 ? 0 : flo / kSeg;
+    const int64_t shi = fend <= 0 ? 0 : (fend - 1) / kSeg;
+    if (shi >= nseg_total || shi - slo >= kNSeg) return false;
+    if (shi < next_issue) {
+      if (shi > ready) wait_upto(shi);
       return true;
     }
-    const int64_t f = q - sv.h;
-    const int64_t s = f >> 12;  // kSeg = 4096
-    if (s != cur_seg) {
-      if (s >= nseg_total) return false;
-      while (s >= next_issue) {  // slide: the chain never looks back
-        fence_proxy_async();
-        issue();
-      }
-      const int slot = (int)(s & (kNSeg - 1));
-      const int64_t first =
-          s_first + ((slot - s_first) % kNSeg + kNSeg) % kNSeg;
-      mbar_wait(&bars[slot], (uint32_t)(((s - first) / kNSeg) & 1));
-      cur_seg = s;
-      seg = ring + (size_t)slot * kSeg;
+    __syncwarp();  // every lane is done with the slots about to be reused
+    while (shi >= next_issue) {
+      // the slot's previous segment must be complete before it is reused
+      if (next_issue - kNSeg > ready) wait_upto(next_issue - kNSeg);
+      issue();
     }
-    *out = seg[f & (kSeg - 1)];
+    wait_upto(shi);
     return true;
   };
-  // D(k) without divisions: non-tail events take F + 2k - 1 draws with
-  // F = 2k when n - 2k >= 1
+  auto at = [&](int64_t q) -> uint32_t {
+    if (q < sv.h) return sv.ub;
+    const int64_t f = q - sv.h;
+    return ring[(size_t)((f / kSeg) & (kNSeg - 1)) * kSeg + (f % kSeg)];
+  };
   const int n50 = n / 50;
   auto draws = [&](int k) -> int {
     const int size = 2 * k;
@@ -399,24 +424,53 @@ __device__ bool chain_events(const SwarmView& v, const MutBufs& b,
   };
   int64_t q = q0;
   for (int e = e0; e < e_end; ++e) {
+    // k = integers(1, k_hi + 1): Lemire with redraws (warp-uniform loop)
     uint32_t u;
     do {
-      if (!get(q, &u)) return false;
+      if (!ensure(q - sv.h, q - sv.h + 1)) return false;
+      u = at(q);
       ++q;
     } while (lemire_rejects(u, rng_k));
     const int kraw = (int)(((uint64_t)u * (rng_k + 1u)) >> 32) + 1;
     const int k = min(kraw, n / 2);
-    b.ev_k[e] = k;
-    b.ev_cursor[e] = (uint64_t)q;
-    if (k >= 1) q += draws(k);
-    b.ev_end[e] = (uint64_t)q;  // speculative: no redraw in the sample
+    const int64_t cur = q;
+    int64_t end = q;
+    if (k >= 1) {
+      const int D = draws(k);
+      if (!ensure(cur - sv.h, cur - sv.h + D)) return false;
+      int bad = 0;
+      for (int d = lane; d < D && !bad; d += 32)
+        bad = lemire_rejects(at(cur + d), sample_bound(n, k, d));
+      if (__any_sync(0xffffffffu, bad)) {
+        // this event holds a redraw: consume it exactly (warp-uniform)
+        int64_t p = cur;
+        for (int d = 0; d < D; ++d) {
+          const uint32_t rng = sample_bound(n, k, d);
+          if (rng == 0) continue;
+          for (;;) {
+            if (!ensure(cur - sv.h, p - sv.h + 1)) return false;
+            if (!lemire_rejects(at(p), rng)) break;
+            ++p;
+          }
+          ++p;
+        }
+        end = p;
+      } else {
+        end = cur + D;
+      }
+    }
+    if (lane == 0) {
+      b.ev_k[e] = k;
+      b.ev_cursor[e] = (uint64_t)cur;
+      b.ev_end[e] = (uint64_t)end;
+    }
+    q = end;
   }
   // drain outstanding copies before the CTA exits
-  for (int64_t s = next_issue - kNSeg; s < next_issue; ++s) {
-    if (s < s_first || s >= nseg_total) continue;
-    const int slot = (int)(s % kNSeg);
-    const int64_t first = s_first + ((slot - s_first) % kNSeg + kNSeg) % kNSeg;
-    mbar_wait(&bars[slot], (uint32_t)(((s - first) / kNSeg) & 1));
+  for (int64_t sg = ready + 1; sg < next_issue && sg < nseg_total; ++sg) {
+    int slot;
+    const uint32_t par = slot_parity(sg, &slot);
+    mbar_wait(&bars[slot], par);
   }
   return true;
 }
@@ -428,38 +482,19 @@ __device__ __forceinline__ StreamView stream_view(const SwarmView& v,
           (uint32_t)g.uinteger};
 }
 
-// round 0: all P potential events of the NEXT call from its start (parity
-// mut_cur ^ 1); round r > 0: the current call, from the event after the one
-// flagged by the previous sample round.
-__global__ void __launch_bounds__(32) k_mut_walk(SwarmView v, int round) {
-  if (v.ctl->done) return;
-  if (threadIdx.x != 0) return;
+// All P potential events of the NEXT call from its start (parity
+// mut_cur ^ 1); one warp.
+__global__ void __launch_bounds__(32) k_mut_walk(SwarmView v) {
+  if (v.ctl->done || !v.ctl->mut_pending) return;
   extern __shared__ __align__(128) uint32_t ring[];
   __shared__ __align__(8) uint64_t bars[kNSeg];
-  int e0 = 0, e_end = v.P, par;
-  int64_t q0 = 0;
-  if (round == 0) {
-    if (!v.ctl->mut_pending) return;
-    par = v.ctl->mut_cur ^ 1;
-  } else {
-    if (!v.ctl->mutating) return;
-    par = v.ctl->mut_cur;
-    const MutBufs b = mut_bufs(v, par);
-    const int bad = v.ctl->mut_bad, E = v.ctl->n_events;
-    if (v.ctl->mut_round != round - 1 || bad >= E) return;
-    e0 = bad + 1;
-    q0 = (int64_t)b.ev_end[bad];  // exact: the sampler consumed it exactly
-    e_end = E;
-    v.ctl->mut_bad = 0x7fffffff;
-    v.ctl->mut_from = e0;
-  }
+  const int par = v.ctl->mut_cur ^ 1;
   const MutBufs b = mut_bufs(v, par);
-  if (!chain_events(v, b, stream_view(v, b), e0, q0, e_end, ring, bars))
-    v.ctl->mut_overflow |= 1 << par;
-  if (round == 0) {
+  const bool ok = chain_events(v, b, stream_view(v, b), 0, 0, v.P, ring, bars);
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    if (!ok) v.ctl->mut_overflow |= 1 << par;
     v.ctl->mut_pending = 0;
-  } else {
-    v.ctl->mut_round = round;
   }
 }
 
@@ -541,14 +576,12 @@ struct PcgNext {  // next32() regenerated from the stream state
 constexpr int kSampleWarps = 4;
 
 __global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample(
-    SwarmView v, int round, int vals_cap, int scratch_words) {
+    SwarmView v, int vals_cap, int scratch_words) {
   if (!v.ctl->mutating || v.ctl->done) return;
-  if (round > 0 && v.ctl->mut_round != round) return;  // no re-walk ran
   const MutBufs b = mut_bufs(v, v.ctl->mut_cur);
   extern __shared__ __align__(16) uint32_t sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int e = (round > 0 ? v.ctl->mut_from : 0) +
-                blockIdx.x * (blockDim.x >> 5) + warp;
+  const int e = blockIdx.x * (blockDim.x >> 5) + warp;
   if (e >= v.ctl->n_events) return;
   const int n = v.n, k = b.ev_k[e];
   if (k < 1) return;
@@ -608,10 +641,10 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample(
     CountingBounded<BufNext> c{BufNext{sv, cur}};
     const int64_t used = sample_event_seq(c, n, k, idx, bits, arr);
     if (cur - sv.h + used > sv.cap) v.ctl->mut_overflow = 1;
-    if (used != D) {
-      b.ev_end[e] = (uint64_t)(cur + used);
-      atomicMin(&v.ctl->mut_bad, e);
-    }
+    // the walk resolved redraws exactly; a mismatch would be a walk bug:
+    // fall back to the exact sequential path
+    if (cur + used != (int64_t)b.ev_end[e])
+      atomicOr(&v.ctl->mut_overflow, 1 << v.ctl->mut_cur);
   }
 }
 
@@ -627,9 +660,8 @@ __global__ void __launch_bounds__(32) k_mut_fix(SwarmView v) {
   const MutBufs b = mut_bufs(v, par);
   const int n = v.n;
   const int E = v.ctl->n_events;
-  int bad = v.ctl->mut_bad;
   const bool overflow = (v.ctl->mut_overflow >> par) & 1;
-  if (overflow) bad = 0;  // redo the whole call exactly
+  const int bad = overflow ? 0 : 0x7fffffff;  // redo the whole call exactly
   uint64_t q = 0;
   if (bad < E) {
     const int k_hi = max(2, n / 4);
@@ -769,7 +801,7 @@ cudaError_t launch_mutation_walk(const SwarmView& v, cudaStream_t s) {
   k_mut_gen<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(v);
   const size_t ring = (size_t)kNSeg * kSeg * 4;
   set_dyn_smem((const void*)k_mut_walk, ring);
-  k_mut_walk<<<1, 32, ring, s>>>(v, 0);
+  k_mut_walk<<<1, 32, ring, s>>>(v);
   return cudaGetLastError();
 }
 
@@ -813,16 +845,8 @@ cudaError_t launch_mutation_post(const SwarmView& v, cudaStream_t s) {
                                                 kBudget / per_warp));
   const size_t smem = (size_t)warps * per_warp;
   set_dyn_smem((const void*)k_mut_sample, smem);
-  const size_t ring = (size_t)kNSeg * kSeg * 4;
-  set_dyn_smem((const void*)k_mut_walk, ring);
   const unsigned grid = (unsigned)((P + warps - 1) / warps);
-  // round 0, then up to two re-walk rounds after a Lemire redraw
-  k_mut_sample<<<grid, warps * 32, smem, s>>>(v, 0, vals_cap, scratch_words);
-  for (int round = 1; round <= 2; ++round) {
-    k_mut_walk<<<1, 32, ring, s>>>(v, round);
-    k_mut_sample<<<grid, warps * 32, smem, s>>>(v, round, vals_cap,
-                                                scratch_words);
-  }
+  k_mut_sample<<<grid, warps * 32, smem, s>>>(v, vals_cap, scratch_words);
   const size_t scratch =
       std::max<size_t>(round_up((n + 31) / 32 * 4, 16), 2 * (size_t)v.np);
   set_dyn_smem((const void*)k_mut_fix, scratch);
