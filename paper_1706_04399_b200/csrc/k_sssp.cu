@@ -11,7 +11,8 @@
 // improved voxels to the next worklist (a flag array dedupes).  Rounds repeat
 // until every worklist is empty.  Because fl(d + w) is monotone in d, the
 // fixed point is the minimum over paths of the left-to-right fp path sums,
-// exactly what A*/Dijkstra return, for any weights.
+// which is what Dijkstra returns.  The reference's A* returns the same bits
+// for integer weights (all its scenes); otherwise it may be 1 ulp above.
 //
 // Then cost[i][j] = dist_min(i,j)(vox[max(i,j)]) (the reference computes
 // each pair from its lower index), blocked pairs get
