@@ -52,7 +52,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     procs = []
     for src in sources():
         obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
-        cmd = [nvcc(), *NVCC_FLAGS, "-c", src, "-o", obj]
+        # DPSO_EXTRA_NVCC_FLAGS: debug/profiling builds only (e.g.
+        # -DDPSO_WALK_PROF for the mutation walk's phase timers)
+        extra = os.environ.get("DPSO_EXTRA_NVCC_FLAGS", "").split()
+        cmd = [nvcc(), *NVCC_FLAGS, *extra, "-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE,

@@ -114,7 +114,7 @@ Layout make_layout(const dpso_params* prm, int n) {
   L.off_ev_end = take(2 * 8 * P);
   L.off_ev_idx = take(2 * P * np);
   L.off_mstream = take(prm->use_mutation && prm->rng_mode == DPSO_RNG_NUMPY
-                           ? 2 * 4 * mstream_words(n, P)
+                           ? 2 * 6 * mstream_words(n, P)  // u32 + u16 skip
                            : 0);
   L.off_init_cursor = take(8 * P);
   L.off_init_buf = take(prm->rng_mode == DPSO_RNG_NUMPY ? 4 * init_buf_words(n, P) : 0);

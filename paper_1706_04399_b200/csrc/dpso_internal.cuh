@@ -122,7 +122,8 @@ struct SwarmView {
   uint64_t* ev_cursor;
   uint64_t* ev_end;     // stream position after each event's draws
   uint16_t* ev_idx;    // P x np sampled positions per mutation event
-  uint32_t* mstream;   // [2] generated mutation-stream span (u32)
+  uint32_t* mstream;   // [2] generated mutation-stream span (u32), then
+                       // [2] per-word event skips (u16, k_mut_gen)
   int64_t mstream_cap; // u32 capacity of one mstream buffer
   uint64_t* init_cursor;
   uint32_t* init_buf;  // generated init-stream window (u32)

@@ -15,6 +15,7 @@
 //                 the section comment below)
 //   k_mut_swap    k disjoint swaps, fitness in reference order, pbest
 //                 (solver.py:241-258)
+#include <cstdio>
 #include <algorithm>
 
 #include "dpso_internal.cuh"
@@ -251,21 +252,20 @@ __global__ void __launch_bounds__(128) k_mut_copy(SwarmView v) {
 //   k_mut_gen     (grid-wide) writes the span of the stream this call can
 //                 use into an L2-resident buffer (fresh u32 index f ->
 //                 mstream[f]); every thread jumps to its own chunk.
-//   k_mut_walk    one thread chains the k-draws for all P potential events
-//                 through an 8-slot shared-memory ring of 16 KiB stream
-//                 segments fed by cp.async.bulk, assuming the events'
-//                 Floyd/shuffle draws need no Lemire redraw.  It only needs the
-//                 stream, so it runs on a forked stream concurrently with the
-//                 update and the dedupe pipeline.
-//   k_mut_sample  one warp per event reads its draws from the buffer, checks
-//                 them for redraws in parallel and runs numpy's Floyd sampler
-//                 + shuffle; an event that does contain a redraw is sampled
-//                 exactly (sequentially), its true end recorded, and the first
-//                 such event flagged.
-//   rounds 1, 2   k_mut_walk/k_mut_sample again from the event after the
-//                 flagged one (no-ops when nothing was flagged).
-//   k_mut_fix     exact sequential fallback after two flagged rounds (never
-//                 seen) and the persistent stream update.
+//   k_mut_walk    one CTA chains all P potential events exactly: warp 0
+//                 chains the k-draws of a block of events speculatively
+//                 through a shared-memory ring of stream segments fed by
+//                 cp.async.bulk, all warps then test the block's draws for
+//                 Lemire redraws, and only an event that holds one is
+//                 consumed draw by draw.  It only needs the stream, so the
+//                 walk for the NEXT call runs on a forked stream and
+//                 overlaps the following generations (double-buffered by
+//                 call parity).
+//   k_mut_sample  one warp per event reads its draws from the buffer and
+//                 runs numpy's Floyd sampler + shuffle; it re-checks its
+//                 consumption against the walk's record (safety net).
+//   k_mut_fix     the persistent stream update; the exact sequential
+//                 sampler for the whole call only if the walk overflowed.
 
 // Buffers of one mutation call (parity 0/1).
 struct MutBufs {
@@ -273,13 +273,16 @@ struct MutBufs {
   uint64_t* ev_cursor;
   uint64_t* ev_end;
   uint32_t* mstream;
+  uint16_t* skip;  // per stream word: the skip of an event whose k-draw it is
   PcgState* start;
 };
 
 __device__ __forceinline__ MutBufs mut_bufs(const SwarmView& v, int par) {
+  uint16_t* skips = reinterpret_cast<uint16_t*>(v.mstream + 2 * v.mstream_cap);
   return {v.ev_k + (size_t)par * v.P, v.ev_cursor + (size_t)par * v.P,
           v.ev_end + (size_t)par * v.P,
-          v.mstream + (size_t)par * v.mstream_cap, v.mut_start + par};
+          v.mstream + (size_t)par * v.mstream_cap,
+          skips + (size_t)par * v.mstream_cap, v.mut_start + par};
 }
 
 constexpr int kSeg = 4096;   // u32 per ring segment (16 KiB)
@@ -306,6 +309,36 @@ __device__ __forceinline__ uint32_t sample_bound(int n, int k, int d) {
 
 constexpr int kGenPer = 64;  // outputs per k_mut_gen thread
 
+// The event an accepted k-draw u opens: k = integers(1, k_hi + 1) clipped
+// to n // 2 (solver.py:232-236), then its D Floyd/shuffle draws when none is
+// redrawn.  skip = 1 + D, or 0 when the k-draw itself is rejected (Lemire).
+struct KDraw {
+  int n, n2;
+  uint32_t mk, thr;  // k_hi and Lemire's rejection threshold for it
+  __host__ __device__ static KDraw make(int n) {
+    KDraw r;
+    r.n = n;
+    r.n2 = n / 2;
+    r.mk = (uint32_t)(n / 4 > 2 ? n / 4 : 2);
+    r.thr = (0u - r.mk) % r.mk;
+    return r;
+  }
+  __device__ __forceinline__ int k(uint32_t u) const {
+    return min((int)__umulhi(u, mk) + 1, n2);
+  }
+  __device__ __forceinline__ uint32_t skip(uint32_t u) const {
+    if (u * mk < thr) return 0u;
+    const int kk = k(u);
+    return 1u + (uint32_t)(kk >= 1 ? sample_draws(n, kk) : 0);
+  }
+  // skips fit u16 (else the walker computes them itself)
+  __host__ __device__ static bool fits16(int n) {
+    const int kmax = (n / 4 > 2 ? n / 4 : 2) < n / 2 ? (n / 4 > 2 ? n / 4 : 2)
+                                                      : n / 2;
+    return 1 + sample_draws(n, kmax) <= 0xFFFF;
+  }
+};
+
 // Prepares the NEXT mutation call: writes its stream span into the buffer
 // of parity mut_cur ^ 1.
 __global__ void __launch_bounds__(256) k_mut_gen(SwarmView v) {
@@ -321,9 +354,15 @@ __global__ void __launch_bounds__(256) k_mut_gen(SwarmView v) {
   u128 st = pcg_advance({g.state_hi, g.state_lo}, inc, (uint64_t)o0 + 1);
   const u128 M = pcg_mult();
   uint2* out = reinterpret_cast<uint2*>(b.mstream);
+  ushort2* sk = reinterpret_cast<ushort2*>(b.skip);
+  const KDraw kd = KDraw::make(v.n);
+  const bool skips = KDraw::fits16(v.n);
   for (int r = 0; r < kGenPer && o0 + r < outs; ++r) {
     const uint64_t o = pcg_output(st);
-    out[o0 + r] = make_uint2((uint32_t)o, (uint32_t)(o >> 32));
+    const uint32_t lo = (uint32_t)o, hi = (uint32_t)(o >> 32);
+    out[o0 + r] = make_uint2(lo, hi);
+    if (skips)
+      sk[o0 + r] = make_ushort2((uint16_t)kd.skip(lo), (uint16_t)kd.skip(hi));
     st = add128(mul128(st, M), inc);
   }
 }
@@ -339,141 +378,38 @@ struct StreamView {
   }
 };
 
-// Exact chain of mutation events e0..e_end-1 from stream position q0, one
-// warp, with the stream segments in an 8-slot shared-memory ring fed by
-// cp.async.bulk.  Every lane runs the same control flow; lane 0 writes the
-// records.  Each event's k-draw is a Lemire draw with redraws; then the warp
-// checks the event's Floyd/shuffle draws for Lemire redraws in parallel, so
-// the event's exact end is known: D draws when nothing is redrawn (the common
-// case), otherwise the event is consumed sequentially.  Returns false on
-// buffer overflow (the exact sequential fallback then runs).
-__device__ bool chain_events(const SwarmView& v, const MutBufs& b,
-                             StreamView sv, int e0, int64_t q0, int e_end,
-                             uint32_t* ring, uint64_t* bars) {
-  const int lane = threadIdx.x & 31;
-  const int n = v.n;
-  const int k_hi = max(2, n / 4);
-  const uint32_t rng_k = (uint32_t)(k_hi - 1);
-  const int64_t nseg_total = (sv.cap + kSeg - 1) / kSeg;
-  const int64_t f0 = q0 - sv.h < 0 ? 0 : q0 - sv.h;
-  const int64_t s_first = f0 / kSeg;
-  int64_t next_issue = s_first;  // uniform across the warp
-  int64_t ready = s_first - 1;   // segments <= ready have been waited on
-  if (lane == 0) {
-    for (int i = 0; i < kNSeg; ++i) mbar_init(&bars[i], 1);
-    fence_barrier_init();
-  }
-  __syncwarp();
-  auto slot_parity = [&](int64_t sg, int* slot) -> uint32_t {
-    *slot = (int)(sg & (kNSeg - 1));
-    const int64_t first =
-        s_first + ((*slot - s_first) % kNSeg + kNSeg) % kNSeg;
-    return (uint32_t)(((sg - first) / kNSeg) & 1);
-  };
-  auto issue = [&]() {
-    if (lane == 0 && next_issue < nseg_total) {
-      const int slot = (int)(next_issue & (kNSeg - 1));
-      fence_proxy_async();
-      mbar_expect_tx(&bars[slot], kSeg * 4);
-      bulk_g2s(ring + (size_t)slot * kSeg, sv.buf + next_issue * kSeg,
-               kSeg * 4, &bars[slot]);
-    }
-    ++next_issue;
-  };
-  for (int i = 0; i < kNSeg; ++i) issue();
-  // make fresh positions [flo, fend) readable by every lane; the chain only
-  // moves forward, so slots below flo's segment are recycled
-  // segments are issued and waited on strictly in order; all segments
-  // <= ready are complete
-  auto wait_upto = [&](int64_t sg_hi) {
-    for (int64_t sg = ready + 1; sg <= sg_hi; ++sg) {
-      if (sg >= nseg_total) break;
-      int slot;
-      const uint32_t par = slot_parity(sg, &slot);
-      mbar_wait(&bars[slot], par);
-    }
-    if (sg_hi > ready) ready = sg_hi;
-  };
-  auto ensure = [&](int64_t flo, int64_t fend) -> bool {
-    const int64_t slo = flo < 0 ? 0 : flo / kSeg;
-    const int64_t shi = fend <= 0 ? 0 : (fend - 1) / kSeg;
-    if (shi >= nseg_total || shi - slo >= kNSeg) return false;
-    if (shi < next_issue) {
-      if (shi > ready) wait_upto(shi);
-      return true;
-    }
-    __syncwarp();  // every lane is done with the slots about to be reused
-    while (shi >= next_issue) {
-      // the slot's previous segment must be complete before it is reused
-      if (next_issue - kNSeg > ready) wait_upto(next_issue - kNSeg);
-      issue();
-    }
-    wait_upto(shi);
-    return true;
-  };
-  auto at = [&](int64_t q) -> uint32_t {
-    if (q < sv.h) return sv.ub;
-    const int64_t f = q - sv.h;
-    return ring[(size_t)((f / kSeg) & (kNSeg - 1)) * kSeg + (f % kSeg)];
-  };
-  const int n50 = n / 50;
-  auto draws = [&](int k) -> int {
-    const int size = 2 * k;
-    if (n > 10000 && size > n50) return size <= n - 1 ? size : n - 1;
-    return (size <= n - 1 ? size : n - 1) + size - 1;
-  };
-  int64_t q = q0;
-  for (int e = e0; e < e_end; ++e) {
-    // k = integers(1, k_hi + 1): Lemire with redraws (warp-uniform loop)
-    uint32_t u;
-    do {
-      if (!ensure(q - sv.h, q - sv.h + 1)) return false;
-      u = at(q);
-      ++q;
-    } while (lemire_rejects(u, rng_k));
-    const int kraw = (int)(((uint64_t)u * (rng_k + 1u)) >> 32) + 1;
-    const int k = min(kraw, n / 2);
-    const int64_t cur = q;
-    int64_t end = q;
-    if (k >= 1) {
-      const int D = draws(k);
-      if (!ensure(cur - sv.h, cur - sv.h + D)) return false;
-      int bad = 0;
-      for (int d = lane; d < D && !bad; d += 32)
-        bad = lemire_rejects(at(cur + d), sample_bound(n, k, d));
-      if (__any_sync(0xffffffffu, bad)) {
-        // this event holds a redraw: consume it exactly (warp-uniform)
-        int64_t p = cur;
-        for (int d = 0; d < D; ++d) {
-          const uint32_t rng = sample_bound(n, k, d);
-          if (rng == 0) continue;
-          for (;;) {
-            if (!ensure(cur - sv.h, p - sv.h + 1)) return false;
-            if (!lemire_rejects(at(p), rng)) break;
-            ++p;
-          }
-          ++p;
-        }
-        end = p;
-      } else {
-        end = cur + D;
-      }
-    }
-    if (lane == 0) {
-      b.ev_k[e] = k;
-      b.ev_cursor[e] = (uint64_t)cur;
-      b.ev_end[e] = (uint64_t)end;
-    }
-    q = end;
-  }
-  // drain outstanding copies before the CTA exits
-  for (int64_t sg = ready + 1; sg < next_issue && sg < nseg_total; ++sg) {
-    int slot;
-    const uint32_t par = slot_parity(sg, &slot);
-    mbar_wait(&bars[slot], par);
-  }
-  return true;
-}
+// Exact chain of all P potential events of the NEXT call (parity
+// mut_cur ^ 1) from its start; one CTA of kWalkWarps warps.
+//
+// The stream is staged in a kNSeg-slot shared-memory ring of kSeg-word
+// segments by cp.async.bulk (warp 0 issues, mbarrier completion, segments
+// issued and waited on strictly in order, free slots refilled ahead of the
+// walk).  The walk proceeds in speculative blocks over a window of W stream
+// positions starting at the block start qs:
+//   1. one thread chains the events starting in the window: a k-draw
+//      (Lemire; its redraws are exact since they are serial), then a skip
+//      of the D(k) Floyd/shuffle draws assuming none of them is redrawn;
+//   2. all warps test every Floyd/shuffle draw of the block against its
+//      Lemire bound (one warp per event);
+//   3. the events before the first one holding a redraw (about 1e-7 per
+//      draw at n = 1000) are committed; that event is consumed draw by draw
+//      by warp 0 and the next block starts after it.
+// So the recorded (k, cursor, end) of every event is exact; k_mut_sample
+// re-checks its event against the record as a safety net.
+constexpr int kWalkWarps = 16;
+constexpr int kWalkThreads = kWalkWarps * 32;
+constexpr int kBlockEv = 512;
+constexpr int kWalkWin = 4 * kSeg;  // window cap (stream positions)
+
+struct WalkSmem {
+  uint64_t bars[kNSeg];
+  int64_t cur[kBlockEv];      // first Floyd draw of event j (after its k)
+  int32_t k[kBlockEv];        // its k
+  int32_t off[kBlockEv + 1];  // prefix sums of the draw counts
+  int64_t q;                  // next block start
+  int32_t e;                  // next event
+  int32_t nb, first_bad, stop;
+};
 
 __device__ __forceinline__ StreamView stream_view(const SwarmView& v,
                                                   const MutBufs& b) {
@@ -482,19 +418,286 @@ __device__ __forceinline__ StreamView stream_view(const SwarmView& v,
           (uint32_t)g.uinteger};
 }
 
-// All P potential events of the NEXT call from its start (parity
-// mut_cur ^ 1); one warp.
-__global__ void __launch_bounds__(32) k_mut_walk(SwarmView v) {
+// walk window for n.  A block touches the window plus its longest event
+// (+1 segment when unaligned); when 2W + Dmax fits in kNSeg - 2 segments,
+// the next block's segments were already issued one block earlier, so the
+// copies overlap the walk.  0 = an event alone does not fit the ring.
+__host__ __device__ __forceinline__ int walk_window(int n) {
+  const int k_hi = n / 4 > 2 ? n / 4 : 2;
+  const int kmax = k_hi < n / 2 ? k_hi : n / 2;
+  const int room = (kNSeg - 2) * kSeg - (1 + sample_draws(n, kmax));
+  int w = room / 2 >= 1024 ? room / 2 : room;
+  w = w < kWalkWin ? w : kWalkWin;
+  return w >= 256 ? w : 0;
+}
+
+__global__ void __launch_bounds__(kWalkThreads) k_mut_walk(SwarmView v) {
   if (v.ctl->done || !v.ctl->mut_pending) return;
   extern __shared__ __align__(128) uint32_t ring[];
-  __shared__ __align__(8) uint64_t bars[kNSeg];
+  uint16_t* sring = reinterpret_cast<uint16_t*>(ring + kNSeg * kSeg);
+  __shared__ WalkSmem s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int par = v.ctl->mut_cur ^ 1;
   const MutBufs b = mut_bufs(v, par);
-  const bool ok = chain_events(v, b, stream_view(v, b), 0, 0, v.P, ring, bars);
-  __syncwarp();
-  if (threadIdx.x == 0) {
-    if (!ok) v.ctl->mut_overflow |= 1 << par;
-    v.ctl->mut_pending = 0;
+  const StreamView sv = stream_view(v, b);
+  const int n = v.n, P = v.P;
+  const int k_hi = max(2, n / 4);
+  const int64_t nseg_total = (sv.cap + kSeg - 1) / kSeg;
+  const int W = walk_window(n);
+  const KDraw kd = KDraw::make(n);
+  const bool skips = KDraw::fits16(n);
+  const int Dmax = sample_draws(n, min(k_hi, n / 2));
+  // segment sg sits in slot sg % kNSeg, so stream word f is ring[f & kMask]
+  constexpr uint32_t kMask = kNSeg * kSeg - 1;
+  static_assert((kNSeg & (kNSeg - 1)) == 0, "ring slots: a power of two");
+  auto at = [&](int64_t q) -> uint32_t {
+    return q < sv.h ? sv.ub : ring[(uint32_t)(q - sv.h) & kMask];
+  };
+  auto seg_of = [&](int64_t q) -> int64_t {
+    return q - sv.h < 0 ? 0 : (q - sv.h) / kSeg;
+  };
+  // ring state, meaningful in warp 0 only (warp-uniform there)
+  int64_t next_issue = 0, ready = -1;
+  auto wait_upto = [&](int64_t sg_hi) {
+    for (int64_t sg = ready + 1; sg <= sg_hi && sg < nseg_total; ++sg)
+      mbar_wait(&s.bars[sg % kNSeg], (uint32_t)((sg / kNSeg) & 1));
+    if (sg_hi > ready) ready = sg_hi;
+  };
+  // refill every slot below segment slo (no thread reads those any more)
+  auto prefetch = [&](int64_t slo) {
+    bool fenced = false;
+    while (next_issue < slo + kNSeg && next_issue < nseg_total) {
+      if (next_issue - kNSeg > ready) wait_upto(next_issue - kNSeg);
+      if (lane == 0) {
+        const int slot = (int)(next_issue % kNSeg);
+        if (!fenced) fence_proxy_async();  // generic reads before the refill
+        fenced = true;
+        mbar_expect_tx(&s.bars[slot], kSeg * (skips ? 6 : 4));
+        bulk_g2s(ring + (size_t)slot * kSeg, sv.buf + next_issue * kSeg,
+                 kSeg * 4, &s.bars[slot]);
+        if (skips)
+          bulk_g2s(sring + (size_t)slot * kSeg, b.skip + next_issue * kSeg,
+                   kSeg * 2, &s.bars[slot]);
+      }
+      ++next_issue;
+    }
+  };
+  // positions [qlo, qhi] resident (qlo = the oldest position still needed)
+  auto ensure = [&](int64_t qlo, int64_t qhi) -> bool {
+    const int64_t slo = seg_of(qlo), shi = seg_of(qhi);
+    if (shi >= nseg_total || shi - slo >= kNSeg) return false;
+    if (shi >= next_issue) prefetch(slo);
+    if (shi > ready) wait_upto(shi);
+    return true;
+  };
+
+#ifdef DPSO_WALK_PROF
+  long long t_ens = 0, t_chain = 0, t_check = 0, t_commit = 0, t0 = 0;
+  int nblocks = 0;
+#define WPROF(acc)                   \
+  if (tid == 0) {                    \
+    const long long t1 = clock64();  \
+    acc += t1 - t0;                  \
+    t0 = t1;                         \
+  }
+#else
+#define WPROF(acc)
+#endif
+  if (tid == 0) {
+    for (int i = 0; i < kNSeg; ++i) mbar_init(&s.bars[i], 1);
+    fence_barrier_init();
+    s.e = 0;
+    s.q = 0;
+    s.stop = W == 0;
+  }
+  __syncthreads();
+  if (warp == 0) prefetch(0);
+
+#ifdef DPSO_WALK_PROF
+  if (tid == 0) t0 = clock64();
+#endif
+  while (!s.stop) {
+#ifdef DPSO_WALK_PROF
+    if (tid == 0) ++nblocks;
+#endif
+    const int64_t qs = s.q;
+    const int e0 = s.e;
+    // window [qs, qs + wlen) and every draw of an event starting in it
+    const int64_t lim = sv.h + sv.cap;  // first position past the buffer
+    const int wlen = (int)(lim - qs < W ? lim - qs : W);
+    if (warp == 0) {
+      prefetch(seg_of(qs));  // every slot below the block refills ahead
+      if (!ensure(qs, qs + wlen + Dmax < lim ? qs + wlen + Dmax : lim - 1))
+        if (lane == 0) s.stop = 1;
+    }
+    __syncthreads();
+    WPROF(t_ens)
+    if (s.stop) break;
+    // ---- 1. the chain through the window (one thread) ----
+    // per event: one shared load of the precomputed skip and an add
+    if (tid == 0) {
+      int nb = 0, tot = 0;
+      const int nev = min(kBlockEv, P - e0);
+      int64_t p = qs;
+      const int64_t wend = qs + wlen;
+      if (p < sv.h && p < wend && nb < nev) {  // numpy's buffered half
+        const uint32_t sk = kd.skip(sv.ub);
+        if (sk != 0) {
+          s.cur[0] = p + 1;
+          s.off[0] = 0;
+          tot = (int)sk - 1;
+          nb = 1;
+        }
+        p += sk != 0 ? sk : 1;
+      }
+      if (p >= sv.h) {
+        // stream word index f = p - h (< cap < 2^31); branch-free body so
+        // the loop-carried path is load -> select -> add
+        uint32_t f = (uint32_t)(p - sv.h);
+        const uint32_t fend = (uint32_t)(wend - sv.h);
+        if (skips) {
+          while (f < fend && nb < nev) {
+            const uint32_t sk = sring[f & kMask];
+            if (sk != 0) {
+              s.cur[nb] = sv.h + f + 1;
+              s.off[nb] = tot;
+            }
+            tot += sk != 0 ? (int)sk - 1 : 0;
+            nb += sk != 0;
+            f += sk != 0 ? sk : 1u;
+          }
+        } else {
+          while (f < fend && nb < nev) {
+            const uint32_t sk = kd.skip(ring[f & kMask]);
+            if (sk != 0) {
+              s.cur[nb] = sv.h + f + 1;
+              s.off[nb] = tot;
+            }
+            tot += sk != 0 ? (int)sk - 1 : 0;
+            nb += sk != 0;
+            f += sk != 0 ? sk : 1u;
+          }
+        }
+        p = sv.h + f;
+      }
+      // only the last event can run past the buffer: drop it and stop
+      int stop = 0;
+      if (nb > 0 && p > lim) {
+        --nb;
+        tot = s.off[nb];
+        stop = 1;
+      }
+      s.off[nb] = tot;
+      s.nb = nb;
+      s.first_bad = 0x7fffffff;
+      s.q = p;  // provisional: the block end
+      s.stop = stop || (nb == 0 && p >= lim);
+    }
+    __syncthreads();
+    WPROF(t_chain)
+    const int nb = s.nb;
+    // ---- 2. every draw of the block against its Lemire bound ----
+    // one warp per event; the bounds are affine in the draw index
+    // (sample_bound): Floyd m = jstart + 1 + d, shuffle m = size - t,
+    // tail shuffle m = n - d.  The scan tests only Lemire's necessary
+    // condition leftover < m (two instructions per draw); an event where
+    // it fires (~m / 2^32 per draw) is re-tested exactly.
+    for (int j = warp; j < nb; j += kWalkWarps) {
+      const int64_t cur = s.cur[j];
+      const int k = kd.k(at(cur - 1));
+      if (lane == 0) s.k[j] = k;
+      if (k < 1) continue;
+      const uint32_t fc = (uint32_t)(cur - sv.h);
+      const int size = 2 * k;
+      const int jstart = max(n - size, 1);
+      const int F = n - jstart;
+      const bool tail = n > 10000 && size > n / 50;
+      uint32_t cand = 0;
+      if (tail) {
+        for (int t = lane; t < F; t += 32) {
+          const uint32_t m = (uint32_t)(n - t);
+          cand |= (ring[(fc + t) & kMask] * m) < m;
+        }
+      } else {
+#pragma unroll 4
+        for (int t = lane; t < F; t += 32) {
+          const uint32_t m = (uint32_t)(jstart + 1 + t);
+          cand |= (ring[(fc + t) & kMask] * m) < m;
+        }
+        const uint32_t fs = fc + (uint32_t)F;
+#pragma unroll 4
+        for (int t = lane; t < size - 1; t += 32) {
+          const uint32_t m = (uint32_t)(size - t);
+          cand |= (ring[(fs + t) & kMask] * m) < m;
+        }
+      }
+      if (__any_sync(0xffffffffu, cand)) {  // rare: the exact test
+        bool bad = false;
+        const int D = s.off[j + 1] - s.off[j];
+        for (int d = lane; d < D; d += 32)
+          bad |= lemire_rejects(ring[(fc + d) & kMask], sample_bound(n, k, d));
+        if (__any_sync(0xffffffffu, bad) && lane == 0)
+          atomicMin(&s.first_bad, j);
+      }
+    }
+    __syncthreads();
+    WPROF(t_check)
+    // ---- 3. commit; an event holding a redraw is consumed exactly ----
+    const int fb = s.first_bad;
+    const int ncommit = min(fb, nb);
+    for (int t = tid; t < ncommit; t += kWalkThreads) {
+      const int64_t cur = s.cur[t];
+      b.ev_k[e0 + t] = s.k[t];
+      b.ev_cursor[e0 + t] = (uint64_t)cur;
+      b.ev_end[e0 + t] = (uint64_t)(cur + (s.off[t + 1] - s.off[t]));
+    }
+    if (fb < nb && warp == 0) {
+      const int64_t cur = s.cur[fb];
+      const int k = s.k[fb];
+      const int D = s.off[fb + 1] - s.off[fb];
+      int64_t p = cur;
+      bool over = false;
+      for (int d = 0; d < D && !over; ++d) {
+        const uint32_t rng = sample_bound(n, k, d);
+        if (rng == 0) continue;
+        for (;;) {
+          if (!ensure(cur, p)) {
+            over = true;
+            break;
+          }
+          if (!lemire_rejects(at(p), rng)) break;
+          ++p;
+        }
+        ++p;
+      }
+      if (lane == 0) {
+        b.ev_k[e0 + fb] = k;
+        b.ev_cursor[e0 + fb] = (uint64_t)cur;
+        b.ev_end[e0 + fb] = (uint64_t)p;
+        s.q = p;
+        s.e = e0 + fb + 1;
+        s.stop = over;
+      }
+    } else if (fb >= nb && tid == 0) {
+      s.e = e0 + nb;
+    }
+    __syncthreads();
+    WPROF(t_commit)
+    if (s.e >= P) break;
+  }
+#ifdef DPSO_WALK_PROF
+  if (tid == 0)
+    printf("walk: blocks %d events %d ensure %lld chain %lld check %lld "
+           "commit %lld cycles\n", nblocks, s.e, t_ens, t_chain, t_check,
+           t_commit);
+#endif
+  if (warp == 0) {
+    // drain outstanding copies before the CTA exits
+    wait_upto(next_issue - 1);
+    if (lane == 0) {
+      if (s.stop) v.ctl->mut_overflow |= 1 << par;
+      v.ctl->mut_pending = 0;
+    }
   }
 }
 
@@ -562,7 +765,9 @@ struct BufNext {  // next32() over the generated stream buffer
   int64_t pos;
   __device__ uint32_t operator()() {
     const int64_t p = pos++;
-    return p - sv.h < sv.cap ? sv.at(p) : 0u;
+    // past the buffer: an always-accepted word, so the sampler terminates
+    // (the caller flags the overflow and the exact fallback redoes the call)
+    return p - sv.h < sv.cap ? sv.at(p) : 0xFFFFFFFFu;
   }
 };
 
@@ -640,7 +845,8 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample(
   if (lane == 0) {
     CountingBounded<BufNext> c{BufNext{sv, cur}};
     const int64_t used = sample_event_seq(c, n, k, idx, bits, arr);
-    if (cur - sv.h + used > sv.cap) v.ctl->mut_overflow = 1;
+    if (cur - sv.h + used > sv.cap)
+      atomicOr(&v.ctl->mut_overflow, 1 << v.ctl->mut_cur);
     // the walk resolved redraws exactly; a mismatch would be a walk bug:
     // fall back to the exact sequential path
     if (cur + used != (int64_t)b.ev_end[e])
@@ -799,9 +1005,9 @@ cudaError_t launch_mutation_walk(const SwarmView& v, cudaStream_t s) {
   const int64_t outs = v.mstream_cap / 2;
   const int64_t threads = (outs + kGenPer - 1) / kGenPer;
   k_mut_gen<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(v);
-  const size_t ring = (size_t)kNSeg * kSeg * 4;
-  set_dyn_smem((const void*)k_mut_walk, ring);
-  k_mut_walk<<<1, 32, ring, s>>>(v);
+  const size_t smem = (size_t)kNSeg * kSeg * 6;  // words + skips
+  set_dyn_smem((const void*)k_mut_walk, smem);
+  k_mut_walk<<<1, kWalkThreads, smem, s>>>(v);
   return cudaGetLastError();
 }
 
