@@ -57,7 +57,7 @@ int cuda_fail(cudaError_t e, const char* where) {
 struct Layout {
   size_t off_ctl, off_streams, off_mut_start, off_init_start, off_x, off_pbest, off_vmap,
       off_vel, off_vel_len, off_fit, off_pfit, off_dcache, off_gbest,
-      off_conv, off_tores, off_chunk_row, off_rank, off_hash, off_flag,
+      off_conv, off_tores, off_chunk_tab, off_rank, off_hash, off_flag,
       off_sidx, off_order, off_surv, off_keep, off_ev_slot, off_ev_k,
       off_ev_cursor, off_ev_end, off_ev_idx, off_mstream, off_init_buf,
       off_init_state, off_init_cursor, off_seed, off_cost32,
@@ -100,7 +100,7 @@ Layout make_layout(const dpso_params* prm, int n) {
   L.off_gbest = take(2 * np);
   L.off_conv = take(8 * ((int64_t)prm->max_generations + 1));
   L.off_tores = take(sizeof(TwoOptRes) * P * L.chunks);
-  L.off_chunk_row = take(4 * (L.chunks + 1));
+  L.off_chunk_tab = take(16 * L.chunks);
   L.off_rank = take(4 * P);
   L.off_hash = take(8 * P);
   L.off_flag = take(4 * P);
@@ -337,7 +337,7 @@ int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
   v.conv = (double*)(w + L.off_conv);
   v.tores = (TwoOptRes*)(w + L.off_tores);
   v.chunks = L.chunks;
-  v.chunk_row = (int32_t*)(w + L.off_chunk_row);
+  v.chunk_tab = (int32_t*)(w + L.off_chunk_tab);
   v.rank = (int32_t*)(w + L.off_rank);
   v.hash = (uint64_t*)(w + L.off_hash);
   v.flag = (int32_t*)(w + L.off_flag);
@@ -358,13 +358,13 @@ int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
   v.init_buf = (uint32_t*)(w + L.off_init_buf);
   v.init_buf_cap = prm->rng_mode == DPSO_RNG_NUMPY ? init_buf_words(n, v.P) : 0;
   v.init_state = (void*)(w + L.off_init_state);
-  std::vector<int32_t> rows(L.chunks + 1);
-  two_opt_chunk_rows(n, L.chunks, rows.data());
+  std::vector<int32_t> tab(4 * L.chunks);
+  two_opt_chunk_table(n, L.chunks, tab.data());
   if ((rc = sync_in(c))) {
     dpso_destroy(c);
     return rc;
   }
-  e = cudaMemcpyAsync(v.chunk_row, rows.data(), 4 * rows.size(),
+  e = cudaMemcpyAsync(v.chunk_tab, tab.data(), 4 * tab.size(),
                       cudaMemcpyHostToDevice, c->stream);
   if (!e) e = cudaMemsetAsync(v.ctl, 0, sizeof(DevCtl), c->stream);
   if (!e) e = cudaStreamSynchronize(c->stream);
@@ -785,12 +785,12 @@ int dpso_best_exchange_batch(const double* dev_cost, int64_t ld, int32_t n,
   cudaStream_t s = (cudaStream_t)cuda_stream;
   const int64_t np = round_up(n, 8);
   const int chunks = two_opt_pick_chunks(n, std::max(count, 1));
-  std::vector<int32_t> rows(chunks + 1);
-  two_opt_chunk_rows(n, chunks, rows.data());
+  std::vector<int32_t> tab(4 * chunks);
+  two_opt_chunk_table(n, chunks, tab.data());
   const int64_t cnt = std::max(count, 1);
   size_t bytes = round_up(2 * np * cnt, 256) + round_up(8 * np * cnt, 256) +
                  round_up(sizeof(TwoOptRes) * chunks * cnt, 256) +
-                 round_up(4 * (chunks + 1), 256) + round_up(8 * cnt, 256) +
+                 round_up(16 * chunks, 256) + round_up(8 * cnt, 256) +
                  round_up(4 * (int64_t)n * np, 256) + 256;
   unsigned char* tmp = nullptr;
   CK(cudaMallocAsync(&tmp, bytes, s));
@@ -803,11 +803,11 @@ int dpso_best_exchange_batch(const double* dev_cost, int64_t ld, int32_t n,
   uint16_t* t16 = (uint16_t*)take(2 * np * cnt);
   double* dc = (double*)take(8 * np * cnt);
   TwoOptRes* res = (TwoOptRes*)take(sizeof(TwoOptRes) * chunks * cnt);
-  int32_t* crow = (int32_t*)take(4 * (chunks + 1));
+  int32_t* ctab = (int32_t*)take(16 * chunks);
   double* fsum = (double*)take(8 * cnt);
   float* c32 = (float*)take(4 * (int64_t)n * np);
   CostStats* st = (CostStats*)take(sizeof(CostStats));
-  CK(cudaMemcpyAsync(crow, rows.data(), 4 * (chunks + 1),
+  CK(cudaMemcpyAsync(ctab, tab.data(), 16 * chunks,
                      cudaMemcpyHostToDevice, s));
   int rc = to_u16_tours(dev_tours, n, count, t16, np, s);
   if (rc) return rc;
@@ -825,7 +825,7 @@ int dpso_best_exchange_batch(const double* dev_cost, int64_t ld, int32_t n,
   if (getenv("DPSO_SCAN_MODE")) pl.mode = atoi(getenv("DPSO_SCAN_MODE"));
   if (pl.mode == kScanFilter32 && pl.thr == 0.f) pl.mode = kScanFP64;
   CK(launch_two_opt_batch(pl, n, (int32_t)np, t16, dc, count, res, chunks,
-                          crow, dev_delta, s));
+                          ctab, dev_delta, s));
   if (count > 0) k_u16_to_i32<<<count, 256, 0, s>>>(t16, n, count, dev_tours, np);
   CK(cudaGetLastError());
   CK(cudaFreeAsync(tmp, s));

@@ -105,8 +105,9 @@ struct SwarmView {
   double* conv;
   TwoOptPlan plan;     // cost matrix views + 2-opt scan mode
   TwoOptRes* tores;
-  int32_t chunks;      // 2-opt row chunks per particle
-  int32_t* chunk_row;  // chunks + 1 row boundaries
+  int32_t chunks;      // 2-opt tasks per particle
+  int32_t* chunk_tab;  // chunks x (r0, r1, jlo, jhi): pairs i < j with
+                       // r0 <= i < r1, jlo <= j < jhi
   // mutation scratch
   int32_t* rank;
   uint64_t* hash;
@@ -161,7 +162,7 @@ cudaError_t launch_tour_cost_rows(const double* cost, int64_t ld, int32_t n,
 cudaError_t launch_two_opt_batch(const TwoOptPlan& pl, int32_t n, int32_t np,
                                  uint16_t* tours, const double* dcache,
                                  int32_t count, TwoOptRes* res, int32_t chunks,
-                                 const int32_t* chunk_row, double* delta_out,
+                                 const int32_t* chunk_tab, double* delta_out,
                                  cudaStream_t s);
 cudaError_t launch_cost_prep(const double* cost, int64_t ld, int32_t n,
                              float* cost32, int64_t ld32, CostStats* st,
@@ -180,7 +181,7 @@ cudaError_t build_cost_sssp(const uint8_t* dev_occ, int nx, int ny, int nz,
                             double* dev_cost, int64_t ld, uint8_t* dev_virtual,
                             double* host_vcost, int* bad_viewpoint,
                             cudaStream_t s);
-int two_opt_chunk_rows(int32_t n, int32_t chunks, int32_t* rows);
+int two_opt_chunk_table(int32_t n, int32_t chunks, int32_t* tab);
 int two_opt_pick_chunks(int32_t n, int32_t P);
 
 // Fitness in the reference's order (solver.py:48-54):

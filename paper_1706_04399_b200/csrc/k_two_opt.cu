@@ -39,6 +39,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "dpso_internal.cuh"
 #include "tma.cuh"
@@ -61,7 +62,7 @@ struct ScanArgs {
   int32_t n, np, count, chunks;
   const uint16_t* tours;   // count x np
   const double* dcache;    // count x np
-  const int32_t* chunk_row;
+  const int32_t* chunk_tab;  // chunks x (r0, r1, jlo, jhi)
   TwoOptRes* res;          // count x chunks
   const DevCtl* ctl;       // nullable: skip when done or improved
   uint32_t row_bytes;      // bytes streamed per cost row (multiple of 16)
@@ -148,7 +149,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
   const int p = task / a.chunks, c = task % a.chunks;
   if (p >= a.count) return;
   const int n = a.n;
-  const int r0 = a.chunk_row[c], r1 = a.chunk_row[c + 1];
+  const int4 tb = reinterpret_cast<const int4*>(a.chunk_tab)[c];
+  const int r0 = tb.x, r1 = tb.y, jlo = tb.z, jhi = tb.w;
   TwoOptRes* out = a.res + (size_t)p * a.chunks + c;
   if (a.only_flagged && out->i != kOverflowTag) return;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
@@ -198,7 +200,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
     if (NPL > 0) {
 #pragma unroll
       for (int m0 = 0; m0 < NR; m0 += kGroup) {
-        if (32 * (m0 + kGroup) - 1 > i) {  // warp-uniform: group not dead
+        if (32 * (m0 + kGroup) - 1 > i && 32 * m0 < jhi &&
+            32 * (m0 + kGroup) > jlo) {  // warp-uniform: group not dead
           double av[kGroup], bv[kGroup];
 #pragma unroll
           for (int g = 0; g < kGroup; ++g) {
@@ -214,7 +217,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
               double t = __dadd_rn(av[g], bv[g]);
               t = __dsub_rn(t, di);
               t = __dsub_rn(t, dj[m0 + g]);
-              t = (j > i && j < n) ? t : kInf;
+              t = (j > i && j >= jlo && j < jhi) ? t : kInf;
               const bool lt = t < rbest;
               rbest = lt ? t : rbest;
               rj = lt ? j : rj;
@@ -223,7 +226,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
         }
       }
     } else {
-      for (int j = i + 1 + lane; j < n; j += 32) {
+      for (int j = max(i + 1, jlo) + lane; j < jhi; j += 32) {
         const int aj = tour[j], sj = tour[j + 1 == n ? 0 : j + 1];
         double t = __dadd_rn(A[aj], B[sj]);
         t = __dsub_rn(t, di);
@@ -245,65 +248,106 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
 }
 
 // ---- FP32 scan: EXACT32 (MODE 1) and FILTER32 (MODE 2) ---------------------
-// FILTER32 candidate bookkeeping, out of line (rarely taken; keeping it out
-// of the unrolled column loop keeps the kernel inside the instruction cache).
-// Per lane state lives in shared memory (stride 32 between words): st[0] =
-// running fp32 minimum, st[32] = candidate count, st[64] = overflow flag; cd/cij are this lane's
-// candidate slots (stride 32).  Returns the new window limit.
-__device__ __noinline__ float cand_group(float t0, float t1, float t2,
-                                         float t3, int i, int j0, int jstep,
-                                         float lim, float thr, float* cd,
-                                         uint32_t* cij, float* st) {
+// Shared by both modes: a lane computes u = A + (B - d_j) per pair (d_i is
+// folded into a per-row threshold Lrow) and tests min(u) of each group of
+// kG32 column blocks against Lrow.  A hit (rare once the running minimum has
+// settled) goes to the out-of-line handler below, which keeps the kernel
+// inside the instruction cache:
+//   EXACT32  Lrow = best + d_i (exact: |u|, |best + d_i| < 2^24) and the
+//            handler keeps the lane's first strict minimum t = u - d_i with
+//            its (i, j): the reference argmin, bit for bit.
+//   FILTER32 Lrow = fl_ru(best + thr + d_i) (+inf-free: capped at FLT_MAX);
+//            the handler records every pair with u <= Lrow as a candidate
+//            (t = u - d_i, its (i, j)) and tightens the window when t
+//            improves.  The window sits ~10x inside thr = 2 eps of the
+//            rounding bound, so the fp64 argmin and its ties are candidates.
+// Per-lane state in shared memory (stride 32 between words): st[0] = the
+// running minimum t; EXACT32: st[32], st[64] = its i, j; FILTER32: st[32] =
+// candidate count, st[64] = overflow flag, cd/cij = candidate slots.
+constexpr int kBufs32 = 2;     // fp32 per-warp ring depth (one row ahead)
+constexpr int kG32 = 4;        // column blocks per skip test and pre-test
+constexpr int kNplMax32 = 32;  // column blocks per fp32 task (1024 columns)
+
+template <int MODE>
+__device__ __noinline__ float scan_hit(float u0, float u1, float u2, float u3,
+                                       float di, float lrow, int i, int j0,
+                                       float thr, float* cd, uint32_t* cij,
+                                       float* st) {
+  // entered by the whole warp (the pre-test is warp-uniform); returns the
+  // warp-wide threshold base: EXACT32 the warp minimum, FILTER32 the warp
+  // minimum + thr
+  const float uv[4] = {u0, u1, u2, u3};
   float best = st[0];
-  int ncand = __float_as_int(st[32]);
-  int overflow = __float_as_int(st[64]);
-  const float tv[4] = {t0, t1, t2, t3};
+  if (MODE == 1) {
+    int bi = __float_as_int(st[32]), bj = __float_as_int(st[64]);
 #pragma unroll
-  for (int g = 0; g < 4; ++g) {
-    const float t = tv[g];
-    if (t <= lim) {
+    for (int g = 0; g < 4; ++g) {
+      const float t = __fsub_rn(uv[g], di);  // exact
       if (t < best) {
         best = t;
-        lim = __fadd_ru(t, thr);
-        int w = 0;
-        for (int k = 0; k < ncand; ++k) {
-          const float d = cd[32 * k];
-          if (d <= lim) {
-            cd[32 * w] = d;
-            cij[32 * w] = cij[32 * k];
-            ++w;
-          }
-        }
-        ncand = w;
+        bi = i;
+        bj = j0 + 32 * g;
       }
+    }
+    st[0] = best;
+    st[32] = __int_as_float(bi);
+    st[64] = __int_as_float(bj);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+      best = fminf(best, __shfl_xor_sync(0xffffffffu, best, o));
+    return best;
+  }
+  int ncand = __float_as_int(st[32]);
+  int overflow = __float_as_int(st[64]);
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const float u = uv[g];
+    if (u <= lrow) {
+      const float t = __fsub_rn(u, di);
+      best = fminf(best, t);
       if (ncand < kCand) {
         cd[32 * ncand] = t;
-        cij[32 * ncand] = ((uint32_t)i << 16) | (uint32_t)(j0 + jstep * g);
+        cij[32 * ncand] = ((uint32_t)i << 16) | (uint32_t)(j0 + 32 * g);
         ++ncand;
       } else {
         overflow = 1;
       }
     }
   }
+  float wbest = best;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+    wbest = fminf(wbest, __shfl_xor_sync(0xffffffffu, wbest, o));
+  const float lim = wbest < FLT_MAX ? __fadd_ru(wbest, thr) : FLT_MAX;
+  // drop the candidates the tighter window excludes
+  int w = 0;
+  for (int k = 0; k < ncand; ++k) {
+    const float dv = cd[32 * k];
+    if (dv <= lim) {
+      cd[32 * w] = dv;
+      cij[32 * w] = cij[32 * k];
+      ++w;
+    }
+  }
   st[0] = best;
-  st[32] = __int_as_float(ncand);
+  st[32] = __int_as_float(w);
   st[64] = __int_as_float(overflow);
   return lim;
 }
 
-// One warp per task; lane l owns the columns j = l + 32m (m < NPL).
+// One warp per task (particle, rows [r0, r1), columns [jlo, jhi)); lane l
+// owns the columns j = jlo + l + 32m (m < NPL).
 // Shift-reuse: the A term of pair (i+1, j) is C[a_{i+1}][a_j], which is the
-// B term lane l-1 gathered for pair (i, j-1) (lane 0: lane 31 of block m-1),
-// so it arrives by ONE warp rotate and each row costs ONE random
-// shared-memory gather per pair; the first row of a task is primed by a
-// B-gather of row a_r0.  Per lane in registers: the gathered B values and
-// the gather indices s_j (two u16 per register); d_j sits in shared memory
-// (lane-contiguous, conflict free).  Rows a_r0..a_r1 stream through a
-// per-warp 3-slot ring, two rows ahead.  In fp32 modes the order of the
-// three adds is free (EXACT32 sums are exact; FILTER32 is bounded).
-constexpr int kBufs32 = 2;  // fp32 per-warp ring depth (one row ahead)
-constexpr int kG32 = 8;     // column blocks per uniform group (fp32 scan)
-
+// B term lane l-1 gathered for pair (i, j-1) (lane 0: lane 31 of block m-1;
+// block 0 of a range with jlo > 0 gathers it once per row), so it arrives by
+// ONE warp rotate and each row costs ONE random shared-memory gather per
+// pair.  Per lane in registers: the gathered B values and the gather byte
+// offsets 4 s_j (two u16 per register).  d_j sits in shared memory
+// (lane-owned, conflict free) as fp32, and a column that is dead for the
+// rest of the task (j <= i + gap, or past the range) holds -inf there, so
+// its u is +inf with no per-pair mask: at row i the owning lane retires
+// column i + gap with one store.  Groups of kG32 blocks with no live column
+// are skipped (warp-uniform test).
 template <int NPL, int MODE>
 __global__ void __launch_bounds__(kMaxWarps * 32, 4)
     k_two_opt_scan32(ScanArgs a) {
@@ -318,15 +362,15 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 4)
   const int p = task / a.chunks, c = task % a.chunks;
   if (p >= a.count) return;
   const int n = a.n;
-  const int r0 = a.chunk_row[c], r1 = a.chunk_row[c + 1];
+  const int4 tb = reinterpret_cast<const int4*>(a.chunk_tab)[c];
+  const int r0 = tb.x, r1 = tb.y, jlo = tb.z, jhi = tb.w;
   TwoOptRes* out = a.res + (size_t)p * a.chunks + c;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
   const float kInfF = __int_as_float(0x7f800000);
-  if (MODE == 2) {
-    s_st[warp][0][lane] = kInfF;
-    s_st[warp][1][lane] = __int_as_float(0);
-    s_st[warp][2][lane] = __int_as_float(0);
-  }
+  float* st = &s_st[warp][0][lane];
+  st[0] = kInfF;
+  st[32] = __int_as_float(MODE == 1 ? 0x7fffffff : 0);
+  st[64] = __int_as_float(MODE == 1 ? 0x7fffffff : 0);
   if (r0 >= r1) {
     if (lane == 0) *out = {kInf, 0x7fffffff, 0x7fffffff};
     return;
@@ -336,137 +380,149 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 4)
   // FILTER32 excludes the structural pairs (i, i+1) (and (0, n-1) below)
   constexpr int kGap = MODE == 2 ? 1 : 0;
   unsigned char* wbase = smem + (size_t)warp * a.buf_stride2;
-  float* sdj = (float*)(wbase + kBufs32 * a.buf_stride);  // d_j, fp32
+  float* sdj = (float*)(wbase + kBufs32 * a.buf_stride);  // local column
+  const bool excl_last = MODE == 2 && r0 == 0 && n - 1 >= jlo && n - 1 < jhi;
 
   constexpr int NH = (NPL + 1) / 2;
-  uint32_t sjp[NH];  // s_j = a_{j+1} for blocks 2h (lo) and 2h+1 (hi)
+  uint32_t sjp[NH];  // 4 s_j for blocks 2h (lo) and 2h+1 (hi)
 #pragma unroll
   for (int h = 0; h < NH; ++h) sjp[h] = 0;
 #pragma unroll
   for (int m = 0; m < NPL; ++m) {
-    const int j = lane + 32 * m;
-    if (j < n) {
-      const uint32_t s_ = tour[j + 1 == n ? 0 : j + 1];
-      sjp[m / 2] |= (m & 1) ? (s_ << 16) : s_;
+    const int j = jlo + lane + 32 * m;
+    if (j < jhi) {
+      const uint32_t s4 = 4u * tour[j + 1 == n ? 0 : j + 1];
+      sjp[m / 2] |= (m & 1) ? (s4 << 16) : s4;
     }
   }
-  for (int j = lane; j < 32 * NPL; j += 32)
-    sdj[j] = j < n ? (float)dg[j] : 0.f;
+  for (int jl = lane; jl < 32 * NPL; jl += 32) {
+    const int j = jlo + jl;
+    sdj[jl] = (j > r0 + kGap && j < jhi && !(excl_last && j == n - 1))
+                  ? (float)dg[j]
+                  : -kInfF;
+  }
   auto sj = [&](int m) -> uint32_t {
     return (m & 1) ? (sjp[m / 2] >> 16) : (sjp[m / 2] & 0xFFFFu);
   };
   const int nrows = r1 - r0 + 1;  // cost rows a_r0 .. a_r1
   uint64_t* wb = bars[warp];
-  auto issue = [&](int q) {
+  auto issue = [&](int q, int city) {
     const int s_ = q % kBufs32;
     mbar_expect_tx(&wb[s_], a.row_bytes);
     bulk_g2s(wbase + (size_t)s_ * a.buf_stride,
-             a.cost32 + (size_t)tour[r0 + q] * a.ld32, a.row_bytes, &wb[s_]);
+             a.cost32 + (size_t)city * a.ld32, a.row_bytes, &wb[s_]);
   };
   if (lane == 0) {
     for (int s_ = 0; s_ < kBufs32; ++s_) mbar_init(&wb[s_], 1);
     fence_barrier_init();
-    for (int q = 0; q < kBufs32 && q < nrows; ++q) issue(q);
+    for (int q = 0; q < kBufs32 && q < nrows; ++q) issue(q, tour[r0 + q]);
   }
+  // Per-row scalars come from lane-parallel loads of 32 rows at a time,
+  // one block of rows ahead: cb = the cities of ring rows (copy issued for
+  // row index k + kBufs32 at row k), db = d_i as fp32.
+  auto city_at = [&](int k) -> int {  // ring row k = tour[r0 + k]
+    return k < nrows ? (int)tour[r0 + k] : 0;
+  };
+  auto d_at = [&](int k) -> float {  // d_{r0 + k}
+    return r0 + k < r1 ? (float)dg[r0 + k] : 0.f;
+  };
+  int cb = city_at(kBufs32 + lane), cb_next = city_at(kBufs32 + 32 + lane);
+  float db = d_at(lane), db_next = d_at(32 + lane);
   __syncwarp();
-  auto row = [&](int q) -> const float* {
+  auto row = [&](int q) -> const unsigned char* {
     const int s_ = q % kBufs32;
     mbar_wait(&wb[s_], (uint32_t)((q / kBufs32) & 1));
-    return (const float*)(wbase + (size_t)s_ * a.buf_stride);
+    return wbase + (size_t)s_ * a.buf_stride;
   };
-  // prime: Bv = row a_r0 gathered at s_j (the "B term of row r0 - 1")
+  auto at4 = [](const unsigned char* R, uint32_t off4) -> float {
+    return *reinterpret_cast<const float*>(R + off4);
+  };
+  // prime: Bv = row a_r0 gathered at s_j (the "B term of row r0 - 1"); for
+  // jlo > 0 lane 0's A term of block 0 is C[a_i][a_jlo], gathered per row
+  const uint32_t s4lo = jlo > 0 ? 4u * tour[jlo] : 0u;
   float Bv[NPL];
+  float a0;
   {
-    const float* R = row(0);
+    const unsigned char* R = row(0);
 #pragma unroll
-    for (int m = 0; m < NPL; ++m) Bv[m] = R[sj(m)];
+    for (int m = 0; m < NPL; ++m) Bv[m] = at4(R, sj(m));
+    a0 = at4(R, s4lo);
   }
-
-  float best = kInfF;
-  int bi = 0x7fffffff, bj = 0x7fffffff;
-  float lim = FLT_MAX;  // FILTER32: best + thr (finite: masked +inf never enters)
+  float lim = MODE == 1 ? kInfF : FLT_MAX;
   for (int i = r0; i < r1; ++i) {
-    const int q = i - r0 + 1;  // ring index of the B row a_{i+1}
-    __syncwarp();
-    if (lane == 0 && q + kBufs32 - 1 < nrows) {
-      fence_proxy_async();
-      issue(q + kBufs32 - 1);  // the slot of row q-1, consumed last iteration
+    const int k = i - r0;
+    const int q = k + 1;  // ring index of the B row a_{i+1}
+    if (k > 0 && (k & 31) == 0) {  // next block of per-row scalars
+      cb = cb_next;
+      db = db_next;
+      cb_next = city_at(kBufs32 + k + 32 + lane);
+      db_next = d_at(k + 32 + lane);
     }
-    const float* B = row(q);
+    const int city = __shfl_sync(0xffffffffu, cb, k & 31);
+    const float di = __shfl_sync(0xffffffffu, db, k & 31);
+    // the slot of row q - 1 (read last iteration; those shared loads have
+    // completed, their values consumed) takes row q + 1
+    if (lane == 0 && q + kBufs32 - 1 < nrows) issue(q + kBufs32 - 1, city);
+    {  // retire column i + gap (its owner lane); row 0's (0, n-1) is back
+      const int cl = i + kGap - jlo;
+      if (cl >= 0 && cl < 32 * NPL && lane == (cl & 31)) sdj[cl] = -kInfF;
+      if (excl_last && i == 1 && lane == ((n - 1 - jlo) & 31))
+        sdj[n - 1 - jlo] = (float)dg[n - 1];
+    }
+    const unsigned char* B = row(q);
     if (a.stream_only) {
-      if (lane == 0 && B[0] == -1.f) bi = i;  // keep the load
+      if (lane == 0 && at4(B, 0) == -1.f) lim = 0.f;  // keep the load
       continue;
     }
-    const float di = (float)dg[i];
-    const int jlim = (MODE == 2 && i == 0) ? n - 1 : n;
-    float rbest = kInfF;
-    int rj = 0x7fffffff;
-    float rprev = 0.f;  // rotate of the previous block (lane 0's A term)
+    float lrow = MODE == 1 ? __fadd_rn(lim, di)
+                           : fminf(__fadd_ru(lim, di), FLT_MAX);
+    float rprev = a0;  // lane 0's A term of the next block
+    a0 = at4(B, s4lo);  // for row i + 1
 #pragma unroll
     for (int m0 = 0; m0 < NPL; m0 += kG32) {
-      if (32 * (m0 + kG32) - 1 > i + kGap) {  // warp-uniform: group not dead
-        if (m0 > 0 && !(32 * m0 - 1 > i + kGap))  // previous group was dead
-          rprev = __shfl_sync(0xffffffffu, Bv[m0 - 1], (lane + 31) & 31);
-        // fully live group: every column j > i + gap and < jlim (only the
-        // last block can reach n; row 0 also excludes (0, n-1) in FILTER32)
-        const bool full = (32 * m0 > i + kGap) && (m0 + kG32 < NPL) &&
-                          !(MODE == 2 && i == 0);
-        float tv[kG32];
+      if (jlo + 32 * (m0 + kG32) - 1 > i + kGap) {  // warp-uniform: live
+        if (m0 > 0 && !(jlo + 32 * m0 - 1 > i + kGap))  // previous skipped
+          rprev = __shfl_sync(0xffffffffu, Bv[m0 - 1], 31);
+        float u[kG32];
 #pragma unroll
         for (int g = 0; g < kG32; ++g) {
-          tv[g] = kInfF;
-          if (m0 + g < NPL) {
-            const int m = m0 + g;
+          const int m = m0 + g;
+          if (m < NPL) {
             const float r = __shfl_sync(0xffffffffu, Bv[m], (lane + 31) & 31);
             const float av = lane == 0 ? rprev : r;
             rprev = r;
-            const float bv = B[sj(m)];
+            const float bv = at4(B, sj(m));
             Bv[m] = bv;
-            const int j = lane + 32 * m;
-            float t = __fadd_rn(__fsub_rn(av, di), __fsub_rn(bv, sdj[j]));
-            if (!full) t = (j > i + kGap && j < jlim) ? t : kInfF;
-            tv[g] = t;
+            u[g] = __fadd_rn(av, __fsub_rn(bv, sdj[lane + 32 * m]));
+          } else {
+            u[g] = kInfF;
           }
         }
-        if (MODE == 1) {
-#pragma unroll
-          for (int g = 0; g < kG32; ++g) {
-            const bool lt = tv[g] < rbest;
-            rbest = lt ? tv[g] : rbest;
-            rj = lt ? lane + 32 * (m0 + g) : rj;
-          }
-        } else {
-#pragma unroll
-          for (int g4 = 0; g4 < kG32; g4 += 4) {
-            bool hit = false;
-#pragma unroll
-            for (int g = 0; g < 4; ++g) hit |= tv[g4 + g] <= lim;
-            if (hit)
-              lim = cand_group(tv[g4], tv[g4 + 1], tv[g4 + 2], tv[g4 + 3], i,
-                               lane + 32 * (m0 + g4), 32, lim, a.thr,
+        const float mn = fminf(fminf(u[0], u[1]), fminf(u[2], u[3]));
+        if (__any_sync(0xffffffffu, MODE == 1 ? mn < lrow : mn <= lrow)) {
+          lim = scan_hit<MODE>(u[0], u[1], u[2], u[3], di, lrow, i,
+                               jlo + lane + 32 * m0, a.thr,
                                &s_cd[warp][0][lane], &s_cij[warp][0][lane],
-                               &s_st[warp][0][lane]);
-          }
+                               st);
+          lrow = MODE == 1 ? __fadd_rn(lim, di)
+                           : fminf(__fadd_ru(lim, di), FLT_MAX);
         }
       }
-    }
-    if (MODE == 1 && rbest < best) {
-      best = rbest;
-      bi = i;
-      bj = rj;
     }
   }
   __syncwarp();
   if (MODE == 1) {
+    const float best = st[0];
     double bd = best == kInfF ? kInf : (double)best;
+    int bi = __float_as_int(st[32]), bj = __float_as_int(st[64]);
     warp_argmin(bd, bi, bj);
     if (lane == 0) *out = {bd, bi, bj};
     return;
   }
   // FILTER32: warp minimum, candidate re-evaluation in fp64
-  best = s_st[warp][0][lane];
-  const int ncand = __float_as_int(s_st[warp][1][lane]);
-  if (__any_sync(0xffffffffu, __float_as_int(s_st[warp][2][lane]))) {
+  const float best = st[0];
+  const int ncand = __float_as_int(st[32]);
+  if (__any_sync(0xffffffffu, __float_as_int(st[64]))) {
     if (lane == 0) *out = {kInf, kOverflowTag, kOverflowTag};
     return;
   }
@@ -494,9 +550,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 4)
       }
     }
   }
-  // structural pairs, exact from d: (i, i+1) has A = d_i, B = d_{i+1}
+  // structural pairs of this task, exact from d: (i, i+1) has A = d_i,
+  // B = d_{i+1}
   for (int i = r0 + lane; i < r1; i += 32) {
-    if (i + 1 < n) {
+    if (i + 1 < n && i + 1 >= jlo && i + 1 < jhi) {
       const double d0 = dg[i], d1 = dg[i + 1];
       double t = __dadd_rn(d0, d1);
       t = __dsub_rn(t, d0);
@@ -508,10 +565,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 4)
       }
     }
   }
-  if (r0 == 0 && lane == 0 && n - 1 > 1) {  // (0, n-1): s_{n-1} = a_0
+  if (excl_last && lane == 0 && n - 1 > 1) {  // (0, n-1): s_{n-1} = a_0
     const int j = n - 1;
-    const int a0 = tour[0], aj = tour[j], s0 = tour[1], sjj = tour[0];
-    double t = __dadd_rn(a.cost[(size_t)a0 * a.ld + aj],
+    const int a0c = tour[0], aj = tour[j], s0 = tour[1], sjj = tour[0];
+    double t = __dadd_rn(a.cost[(size_t)a0c * a.ld + aj],
                          a.cost[(size_t)s0 * a.ld + sjj]);
     t = __dsub_rn(t, dg[0]);
     t = __dsub_rn(t, dg[j]);
@@ -692,49 +749,89 @@ cudaError_t launch_cost_prep(const double* cost, int64_t ld, int32_t n,
   return cudaGetLastError();
 }
 
+// Column ranges of the fp32 scan (kNplMax32 blocks of 32 columns each).
+static int column_ranges(int32_t n) {
+  const int w = 32 * kNplMax32;
+  return n <= w ? 1 : (n + w - 1) / w;
+}
+
 int two_opt_pick_chunks(int32_t n, int32_t P) {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // fp32 scan: one warp per task (row ring + d_j in shared memory)
-  size_t per_warp = (size_t)kBufs32 * round_up((int64_t)round_up(n, 4) * 4, 128) +
-                    4 * (size_t)round_up(n, 32);
+  const int npl = std::min(std::max(npl_for(n), 1), kNplMax32);
+  size_t per_warp =
+      (size_t)kBufs32 * round_up((int64_t)round_up(n, 4) * 4, 128) +
+      4 * (size_t)32 * npl;
   int warps_per_sm = (int)(kSmemBudget / per_warp);
   if (warps_per_sm < 1) warps_per_sm = 1;
   if (warps_per_sm > 16) warps_per_sm = 16;
-  int64_t slots = (int64_t)sms * warps_per_sm;
+  const int64_t slots = (int64_t)sms * warps_per_sm;
+  const int R = column_ranges(n);
   int chunks = (int)((4 * slots + P - 1) / P);
-  if (chunks < 1) chunks = 1;
-  if (chunks > 32) chunks = 32;
-  if (chunks > n / 8 + 1) chunks = n / 8 + 1;
+  chunks = std::max(chunks, R);
+  chunks = std::min(chunks, 32 * R);
+  chunks = std::min(chunks, std::max(R, n / 8 + 1));
   return chunks;
 }
 
-// Split pair rows 0..n-2 into `chunks` bands of roughly equal pair count.
-int two_opt_chunk_rows(int32_t n, int32_t chunks, int32_t* rows) {
-  const int last = n - 1;  // pair rows are 0 .. n-2
-  const double total = 0.5 * (double)(n - 1) * n;
-  rows[0] = 0;
-  int r = 0;
-  double acc = 0.0;
-  for (int c = 1; c < chunks; ++c) {
-    const double target = total * c / chunks;
-    while (r < last && acc + (n - 1 - r) <= target) {
-      acc += n - 1 - r;
-      ++r;
-    }
-    rows[c] = r;
+// Task table: chunks x (r0, r1, jlo, jhi).  Columns are split into ranges
+// of 32 * kNplMax32; each range's pairs (i < j, j in the range) are cut into
+// row bands of roughly equal pair count, with bands given to the ranges in
+// proportion to their pairs.  Every pair i < j is in exactly one task.
+int two_opt_chunk_table(int32_t n, int32_t chunks, int32_t* tab) {
+  const int R = column_ranges(n);
+  const int w = 32 * kNplMax32;
+  std::vector<double> pairs(R);
+  double total = 0.0;
+  for (int k = 0; k < R; ++k) {
+    const double lo = (double)k * w, hi = std::min<double>(n, (k + 1.0) * w);
+    pairs[k] = 0.5 * (lo + hi - 1.0) * (hi - lo);  // column c has c pairs
+    total += pairs[k];
   }
-  rows[chunks] = last > 0 ? last : 0;
-  for (int c = 1; c <= chunks; ++c)
-    if (rows[c] < rows[c - 1]) rows[c] = rows[c - 1];
+  std::vector<int> bands(R, 1);
+  int given = R;
+  for (int k = 0; k < R && total > 0; ++k) {
+    const int extra = (int)((chunks - R) * pairs[k] / total);
+    bands[k] += extra;
+    given += extra;
+  }
+  for (int k = R - 1; given < chunks; k = (k + R - 1) % R) {
+    ++bands[k];
+    ++given;
+  }
+  int c = 0;
+  for (int k = 0; k < R; ++k) {
+    const int jlo = k * w, jhi = std::min(n, (k + 1) * w);
+    const int last = std::max(jhi - 1, 0);  // rows 0 .. jhi - 2
+    auto cnt = [&](int i) { return (double)(jhi - std::max(jlo, i + 1)); };
+    double acc = 0.0;
+    int r = 0;
+    for (int b = 0; b < bands[k]; ++b, ++c) {
+      const int r0 = r;
+      const double target = pairs[k] * (b + 1) / bands[k];
+      if (b + 1 == bands[k]) {
+        r = last;
+      } else {
+        while (r < last && acc + cnt(r) <= target) {
+          acc += cnt(r);
+          ++r;
+        }
+      }
+      tab[4 * c + 0] = r0;
+      tab[4 * c + 1] = std::max(r, r0);
+      tab[4 * c + 2] = jlo;
+      tab[4 * c + 3] = jhi;
+    }
+  }
   return 0;
 }
 
 cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
                                 uint16_t* tours, const double* dcache,
                                 int32_t count, TwoOptRes* res, int32_t chunks,
-                                const int32_t* chunk_row, const DevCtl* ctl,
+                                const int32_t* chunk_tab, const DevCtl* ctl,
                                 double* fit, double* pfit, uint16_t* pbest,
                                 double* delta_out, double* dcache_rw,
                                 cudaStream_t s, int parts) {
@@ -750,7 +847,7 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
   a.chunks = chunks;
   a.tours = tours;
   a.dcache = dcache;
-  a.chunk_row = chunk_row;
+  a.chunk_tab = chunk_tab;
   a.res = res;
   a.ctl = ctl;
   a.thr = pl.thr;
@@ -791,9 +888,9 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
       a.row_bytes = (uint32_t)(round_up(n, 4) * 4);
       a.buf_stride = (uint32_t)round_up(a.row_bytes, 128);
       // per warp: 2-slot row ring + d_j (fp32, 32 * NPL entries)
+      const int npl32 = std::min(std::max(npl, 1), kNplMax32);
       a.buf_stride2 = (uint32_t)(kBufs32 * a.buf_stride +
-                                 round_up((int64_t)32 * std::max(npl, 1) * 4,
-                                          128));
+                                 round_up((int64_t)32 * npl32 * 4, 128));
       const int warps = kMaxWarps;
       const size_t smem = (size_t)warps * a.buf_stride2;
       const int blocks = (int)((tasks + warps - 1) / warps);
@@ -801,14 +898,13 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
   (pl.mode == kScanExact32                                                 \
        ? launch_scan32_t<NPL, 1>(a, warps, blocks, smem, s)                \
        : launch_scan32_t<NPL, 2>(a, warps, blocks, smem, s))
-      switch (npl) {
+      switch (npl32) {
         case 1: e = SCAN32(1); break;
         case 2: e = SCAN32(2); break;
         case 4: e = SCAN32(4); break;
         case 8: e = SCAN32(8); break;
         case 16: e = SCAN32(16); break;
-        case 32: e = SCAN32(32); break;
-        default: e = SCAN32(64); break;
+        default: e = SCAN32(32); break;
       }
 #undef SCAN32
       // FILTER32 candidate-list overflow: exact fp64 re-scan of those tasks
@@ -843,17 +939,17 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
 
 cudaError_t launch_two_opt(const SwarmView& v, cudaStream_t s, int parts) {
   return launch_two_opt_core(v.plan, v.n, v.np, v.x, v.dcache, v.P, v.tores,
-                             v.chunks, v.chunk_row, v.ctl, v.fit, v.pfit,
+                             v.chunks, v.chunk_tab, v.ctl, v.fit, v.pfit,
                              v.pbest, nullptr, nullptr, s, parts);
 }
 
 cudaError_t launch_two_opt_batch(const TwoOptPlan& pl, int32_t n, int32_t np,
                                  uint16_t* tours, const double* dcache,
                                  int32_t count, TwoOptRes* res, int32_t chunks,
-                                 const int32_t* chunk_row, double* delta_out,
+                                 const int32_t* chunk_tab, double* delta_out,
                                  cudaStream_t s) {
   return launch_two_opt_core(pl, n, np, tours, dcache, count, res, chunks,
-                             chunk_row, nullptr, nullptr, nullptr, nullptr,
+                             chunk_tab, nullptr, nullptr, nullptr, nullptr,
                              delta_out, const_cast<double*>(dcache), s, 3);
 }
 
