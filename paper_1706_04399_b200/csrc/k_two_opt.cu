@@ -69,7 +69,7 @@ struct ScanArgs {
   uint32_t buf_stride;     // bytes between ring buffers
   uint32_t buf_stride2;    // bytes of one warp's smem (ring + d_j)
   float thr;               // FILTER32: 2 * eps
-  int only_flagged;        // FP64 fallback: only tasks tagged kOverflowTag
+  int32_t* ovf;            // FILTER32 overflow list: [0] count, [1..] tasks
   int stream_only;         // debug: stream the rows, skip the pair compute
 };
 
@@ -152,7 +152,6 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
   const int4 tb = reinterpret_cast<const int4*>(a.chunk_tab)[c];
   const int r0 = tb.x, r1 = tb.y, jlo = tb.z, jhi = tb.w;
   TwoOptRes* out = a.res + (size_t)p * a.chunks + c;
-  if (a.only_flagged && out->i != kOverflowTag) return;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
   if (r0 >= r1) {
     if (lane == 0) *out = {kInf, 0x7fffffff, 0x7fffffff};
@@ -247,6 +246,47 @@ __global__ void __launch_bounds__(kMaxWarps * 32)
   if (lane == 0) *out = {best, bi, bj};
 }
 
+// FILTER32 candidate-list overflow: the listed tasks re-scanned exactly in
+// fp64 with the reference expression, rows straight from L2, one warp per
+// listed task (grid-stride; a no-op when the list is empty).
+__global__ void __launch_bounds__(128) k_two_opt_rescan64(ScanArgs a) {
+  if (a.ctl && (a.ctl->done || a.ctl->improved)) return;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int cnt = a.ovf[0];
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  const int n = a.n;
+  for (int t = gw; t < cnt; t += nw) {
+    const int task = a.ovf[1 + t];
+    const int p = task / a.chunks, c = task % a.chunks;
+    const int4 tb = reinterpret_cast<const int4*>(a.chunk_tab)[c];
+    const int r0 = tb.x, r1 = tb.y, jlo = tb.z, jhi = tb.w;
+    const uint16_t* tour = a.tours + (size_t)p * a.np;
+    const double* dg = a.dcache + (size_t)p * a.np;
+    double best = kInf;
+    int bi = 0x7fffffff, bj = 0x7fffffff;
+    for (int i = r0; i < r1; ++i) {
+      const double* A = a.cost + (size_t)tour[i] * a.ld;
+      const double* B = a.cost + (size_t)tour[i + 1] * a.ld;
+      const double di = dg[i];
+      for (int j = max(i + 1, jlo) + lane; j < jhi; j += 32) {
+        const int aj = tour[j], sj = tour[j + 1 == n ? 0 : j + 1];
+        double v = __dadd_rn(A[aj], B[sj]);
+        v = __dsub_rn(v, di);
+        v = __dsub_rn(v, dg[j]);
+        if (v < best) {  // lane order: (i, j) increasing, first strict min
+          best = v;
+          bi = i;
+          bj = j;
+        }
+      }
+    }
+    warp_argmin(best, bi, bj);
+    if (lane == 0) a.res[(size_t)p * a.chunks + c] = {best, bi, bj};
+  }
+}
+
 // ---- FP32 scan: EXACT32 (MODE 1) and FILTER32 (MODE 2) ---------------------
 // Shared by both modes: a lane computes u = A + (B - d_j) per pair (d_i is
 // folded into a per-row threshold Lrow) and tests min(u) of each group of
@@ -299,27 +339,19 @@ __device__ __noinline__ float scan_hit(float u0, float u1, float u2, float u3,
   }
   int ncand = __float_as_int(st[32]);
   int overflow = __float_as_int(st[64]);
+  // the new values in the window, then the new warp minimum, then the list
+  // against the tightened window (so transient entries never overflow it)
+  float tv[4];
 #pragma unroll
   for (int g = 0; g < 4; ++g) {
-    const float u = uv[g];
-    if (u <= lrow) {
-      const float t = __fsub_rn(u, di);
-      best = fminf(best, t);
-      if (ncand < kCand) {
-        cd[32 * ncand] = t;
-        cij[32 * ncand] = ((uint32_t)i << 16) | (uint32_t)(j0 + 32 * g);
-        ++ncand;
-      } else {
-        overflow = 1;
-      }
-    }
+    tv[g] = uv[g] <= lrow ? __fsub_rn(uv[g], di) : __int_as_float(0x7f800000);
+    best = fminf(best, tv[g]);
   }
   float wbest = best;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1)
     wbest = fminf(wbest, __shfl_xor_sync(0xffffffffu, wbest, o));
   const float lim = wbest < FLT_MAX ? __fadd_ru(wbest, thr) : FLT_MAX;
-  // drop the candidates the tighter window excludes
   int w = 0;
   for (int k = 0; k < ncand; ++k) {
     const float dv = cd[32 * k];
@@ -329,8 +361,21 @@ __device__ __noinline__ float scan_hit(float u0, float u1, float u2, float u3,
       ++w;
     }
   }
+  ncand = w;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    if (tv[g] <= lim) {
+      if (ncand < kCand) {
+        cd[32 * ncand] = tv[g];
+        cij[32 * ncand] = ((uint32_t)i << 16) | (uint32_t)(j0 + 32 * g);
+        ++ncand;
+      } else {
+        overflow = 1;
+      }
+    }
+  }
   st[0] = best;
-  st[32] = __int_as_float(w);
+  st[32] = __int_as_float(ncand);
   st[64] = __int_as_float(overflow);
   return lim;
 }
@@ -523,7 +568,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 4)
   const float best = st[0];
   const int ncand = __float_as_int(st[32]);
   if (__any_sync(0xffffffffu, __float_as_int(st[64]))) {
-    if (lane == 0) *out = {kInf, kOverflowTag, kOverflowTag};
+    if (lane == 0) {  // listed for the exact fp64 re-scan
+      *out = {kInf, kOverflowTag, kOverflowTag};
+      a.ovf[1 + atomicAdd(&a.ovf[0], 1)] = task;
+    }
     return;
   }
   float m = best;
@@ -855,8 +903,8 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
   const int64_t tasks = (int64_t)count * chunks;
   cudaError_t e = cudaSuccess;
   const int npl = npl_for(n);
-  auto fp64_scan = [&](int only_flagged) -> cudaError_t {
-    a.only_flagged = only_flagged;
+  a.ovf = reinterpret_cast<int32_t*>(res + (size_t)count * chunks);
+  auto fp64_scan = [&]() -> cudaError_t {
     a.row_bytes = (uint32_t)(round_up(n, 2) * 8);
     a.buf_stride = (uint32_t)round_up(a.row_bytes, 128);
     const size_t per_warp = ring_bytes(n, 8);
@@ -883,7 +931,7 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
   };
   if ((parts & 1) && n >= 4 && tasks > 0) {
     if (pl.mode == kScanFP64 || !pl.cost32) {
-      e = fp64_scan(0);
+      e = fp64_scan();
     } else {
       a.row_bytes = (uint32_t)(round_up(n, 4) * 4);
       a.buf_stride = (uint32_t)round_up(a.row_bytes, 128);
@@ -893,6 +941,8 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
                                  round_up((int64_t)32 * npl32 * 4, 128));
       const int warps = kMaxWarps;
       const size_t smem = (size_t)warps * a.buf_stride2;
+      if (pl.mode == kScanFilter32) e = cudaMemsetAsync(a.ovf, 0, 4, s);
+      if (e != cudaSuccess) return e;
       const int blocks = (int)((tasks + warps - 1) / warps);
 #define SCAN32(NPL)                                                        \
   (pl.mode == kScanExact32                                                 \
@@ -908,7 +958,10 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
       }
 #undef SCAN32
       // FILTER32 candidate-list overflow: exact fp64 re-scan of those tasks
-      if (!e && pl.mode == kScanFilter32) e = fp64_scan(1);
+      if (!e && pl.mode == kScanFilter32) {
+        k_two_opt_rescan64<<<2 * 148, 128, 0, s>>>(a);
+        e = cudaGetLastError();
+      }
     }
     if (e != cudaSuccess) return e;
   }
