@@ -19,6 +19,7 @@
 
 #include "dpso_internal.cuh"
 #include "philox.cuh"
+#include "tma.cuh"
 
 namespace dpso {
 
@@ -179,9 +180,9 @@ __global__ void __launch_bounds__(kRed) k_finalize(SwarmView v) {
 // The init stream (solver.py:176-183) is one numpy stream consumed by all
 // particles in order, so where particle p's draws start depends on every
 // earlier particle.  k_init_gen writes a window of the stream grid-wide;
-// k_init_scan (one thread) runs numpy's acceptance tests over it from
-// registers filled by 16-byte loads, records each particle's first draw and
-// keeps its state on the device so it resumes in the next window.  The
+// k_init_scan (one warp, speculative) runs numpy's acceptance tests over it
+// from a shared-memory ring, records each particle's first draw and keeps
+// its state on the device so it resumes in the next window.  The
 // builder (k_init_build) then regenerates each particle's draws from its
 // cursor by jump-ahead, in parallel.
 struct InitScanState {
@@ -213,25 +214,83 @@ __global__ void __launch_bounds__(256) k_init_gen(SwarmView v, int64_t win0) {
   }
 }
 
-// One warp.  Fast path (a permutation that still needs >= 32 accepts):
-// lane l takes draw l of a 32-draw chunk and assumes every earlier draw in
-// the chunk was accepted, which fixes its max index i_l = i - K - (l - s)
-// and mask; a ballot finds the first lane whose draw is genuinely rejected,
-// and the scan resumes after it.  (#rejections + 1) ballot rounds resolve a
-// chunk.  Seeded particles and permutation tails take the one-lane path.
+// One thread.  The window (fresh u32 indices [win0, win0 + cap)) streams
+// through a kINSeg-slot shared-memory ring of kISeg-word segments fed by
+// cp.async.bulk, prefetched ahead.  The acceptance chain of numpy's masked
+// rejection (random_interval) is inherently serial, but its loop-carried
+// part is tiny: within a mask band a draw is accepted iff (u & mask) <= i,
+// and i drops by the acceptance - a compare and a subtract per draw.  Groups
+// of 8 draws (two 16-byte shared loads) run that chain back to back while
+// the band cannot change inside the group; band changes, permutation ends,
+// segment edges, seeded particles (a 3-draw Lemire pattern) and numpy's
+// buffered half take the one-draw path.
+constexpr int kISeg = 4096;  // u32 per ring segment (16 KiB)
+constexpr int kINSeg = 8;    // ring slots (128 KiB), a power of two
+
 __global__ void __launch_bounds__(32) k_init_scan(SwarmView v, int n_seed,
                                                   int64_t win0,
                                                   InitScanState* stp) {
   if (blockIdx.x != 0) return;
+  extern __shared__ __align__(128) uint32_t ring[];
+  __shared__ __align__(8) uint64_t bars[kINSeg];
+  // All 32 lanes run the same scan (lane 0 issues copies and writes
+  // results).  The loop-carried state gets a lane-dependent zero read from
+  // shared memory, which keeps the chain on the vector datapath: with
+  // provably uniform values the compiler moves it to the uniform datapath,
+  // several times slower per dependent step.
   const int lane = threadIdx.x;
+  __shared__ int s_zero[32];
+  s_zero[lane] = 0;
   InitScanState st = *stp;
   if (st.done) return;
   const int n = v.n, P = v.P;
   const PcgState& g = *v.init_start;
   const int64_t h = (int64_t)g.has_uint32;
   const uint32_t ub = (uint32_t)g.uinteger;
-  const int64_t wend = win0 + v.init_buf_cap;  // fresh index past the window
+  const int64_t cap = v.init_buf_cap;
+  const int64_t wend = win0 + cap;  // fresh index past the window
   const uint32_t* buf = v.init_buf;
+  const int64_t nseg = (cap + kISeg - 1) / kISeg;
+  // ring: segment sg (of the window) in slot (sg - sg0) % kINSeg
+  const int64_t f_start = st.q - h > win0 ? st.q - h : win0;
+  const int64_t sg0 = (f_start - win0) / kISeg;
+  int64_t next_issue = sg0, ready = sg0 - 1;
+  if (lane == 0) {
+    for (int i = 0; i < kINSeg; ++i) mbar_init(&bars[i], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  auto wait_upto = [&](int64_t sg_hi) {
+    for (int64_t sg = ready + 1; sg <= sg_hi && sg < nseg; ++sg)
+      mbar_wait(&bars[(sg - sg0) % kINSeg],
+                (uint32_t)(((sg - sg0) / kINSeg) & 1));
+    if (sg_hi > ready) ready = sg_hi;
+  };
+  auto prefetch = [&](int64_t slo) {  // slots below segment slo are free
+    while (next_issue < slo + kINSeg && next_issue < nseg) {
+      if (next_issue - kINSeg > ready) wait_upto(next_issue - kINSeg);
+      if (lane == 0) {
+        const int slot = (int)((next_issue - sg0) % kINSeg);
+        mbar_expect_tx(&bars[slot], kISeg * 4);
+        bulk_g2s(ring + (size_t)slot * kISeg, buf + next_issue * kISeg,
+                 kISeg * 4, &bars[slot]);
+      }
+      ++next_issue;
+    }
+  };
+  constexpr uint32_t kMask = kINSeg * kISeg - 1;
+  const uint32_t fbase = (uint32_t)(sg0 * kISeg);  // window offset of slot 0
+  auto ridx = [&](int64_t f) -> uint32_t {  // ring index of fresh index f
+    return ((uint32_t)(f - win0) - fbase) & kMask;
+  };
+  // make f's segment resident; returns the fresh index past it
+  auto ensure_seg = [&](int64_t f) -> int64_t {
+    const int64_t sg = (f - win0) / kISeg;
+    prefetch(sg);
+    wait_upto(sg);
+    const int64_t e = win0 + (sg + 1) * kISeg;
+    return e < wend ? e : wend;
+  };
   auto mask_of = [](uint32_t x) {
     x |= x >> 1;
     x |= x >> 2;
@@ -240,7 +299,9 @@ __global__ void __launch_bounds__(32) k_init_scan(SwarmView v, int n_seed,
     x |= x >> 16;
     return x;
   };
-  while (st.p < P) {
+  int64_t resident_end = -1;  // fresh indices [.., resident_end) resident
+  bool exhausted = false;
+  while (st.p < P && !exhausted) {
     if (st.fresh) {
       if (lane == 0) v.init_cursor[st.p] = (uint64_t)st.q;
       st.fresh = 0;
@@ -254,40 +315,62 @@ __global__ void __launch_bounds__(32) k_init_scan(SwarmView v, int n_seed,
       st.fresh = 1;
       continue;
     }
-    const int64_t f = st.q - h;
-    if (st.p >= n_seed && st.step >= 32 && f >= 0 && f + 32 <= wend) {
-      // warp-speculative chunks of 32 draws while the permutation needs
-      // >= 32 more accepts; the next chunk is prefetched into a register
-      int i0 = st.step;
-      int64_t ff = f;
-      uint32_t u = buf[ff - win0 + lane];
-      while (i0 >= 32 && ff + 32 <= wend) {
-        const uint32_t un =
-            ff + 64 <= wend ? buf[ff + 32 - win0 + lane] : 0u;
-        int K = 0, s = 0;
-        for (;;) {
-          const int il = i0 - K - (lane - s);  // > 0: i0 >= 32
-          const uint32_t mask = 0xFFFFFFFFu >> __clz(il);
-          const bool rej = lane >= s && (u & mask) > (uint32_t)il;
-          const unsigned bal = __ballot_sync(0xffffffffu, rej);
-          if (bal == 0) {
-            K += 32 - s;
-            break;
-          }
-          const int fl = __ffs(bal) - 1;
-          K += fl - s;
-          s = fl + 1;
-          if (s == 32) break;
+    if (st.p >= n_seed && st.q >= h) {
+      // a permutation in progress: the serial chain
+      int64_t f = st.q - h;
+      int S = st.step + s_zero[lane ^ 1];
+      uint32_t mask = mask_of((uint32_t)S), half = mask >> 1;
+      bool done = false;
+      while (!done) {
+        if (f >= wend) {
+          exhausted = true;
+          break;
         }
-        i0 -= K;
-        ff += 32;
-        u = un;
+        if (f >= resident_end) resident_end = ensure_seg(f);
+        // accepted iff (u & mask) <= S; S -= accepted, branch-free:
+        // S += (int)((u & mask) - S - 1) >> 31.  Groups run while the band
+        // (mask) cannot change inside them: at most `room` accepts
+        // (room = S - half - 1 >= group size; no permutation end either).
+        while (S - (int)half - 1 >= 32 && f + 32 <= resident_end) {
+          uint32_t w[32];
+#pragma unroll
+          for (int k = 0; k < 32; ++k) w[k] = ring[ridx(f + k)] & mask;
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            S += (int)(w[k] - (uint32_t)S - 1u) >> 31;
+          f += 32;
+        }
+        if (S - (int)half - 1 >= 8 && f + 8 <= resident_end) {
+          uint32_t w[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) w[k] = ring[ridx(f + k)] & mask;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            S += (int)(w[k] - (uint32_t)S - 1u) >> 31;
+          f += 8;
+          continue;
+        }
+        const uint32_t u = ring[ridx(f)];
+        ++f;
+        if ((u & mask) <= (uint32_t)S) {
+          --S;
+          if (S == 0) {
+            done = true;
+          } else if (S <= (int)half) {
+            mask = half;
+            half >>= 1;
+          }
+        }
       }
-      st.step = i0;
-      st.q = ff + h;
+      st.q = f + h;
+      st.step = S;
+      if (done) {
+        ++st.p;
+        st.fresh = 1;
+      }
       continue;
     }
-    // one-lane path: a single draw
+    // one-draw path: seeded particles and numpy's buffered half
     if (st.p < n_seed && st.step == 0 && n - 2 == 0) {
       st.step = 1;  // bounded(0) takes no draw
       continue;
@@ -296,8 +379,10 @@ __global__ void __launch_bounds__(32) k_init_scan(SwarmView v, int n_seed,
     if (st.q < h) {
       u = ub;
     } else {
+      const int64_t f = st.q - h;
       if (f >= wend) break;  // window exhausted: resume after the next gen
-      u = buf[f - win0];
+      if (f >= resident_end) resident_end = ensure_seg(f);
+      u = ring[ridx(f)];
     }
     ++st.q;
     if (st.p < n_seed) {
@@ -309,6 +394,7 @@ __global__ void __launch_bounds__(32) k_init_scan(SwarmView v, int n_seed,
       if ((u & mask_of((uint32_t)st.step)) <= (uint32_t)st.step) --st.step;
     }
   }
+  wait_upto(next_issue - 1);  // drain outstanding copies
   if (lane == 0) {
     if (st.p >= P) {
       st.done = 1;
@@ -604,7 +690,9 @@ cudaError_t launch_init(const SwarmView& v, const uint16_t* dev_seed,
       const int64_t outs = v.init_buf_cap / 2;
       const int64_t thr = (outs + kInitGenPer - 1) / kInitGenPer;
       k_init_gen<<<(unsigned)((thr + 255) / 256), 256, 0, s>>>(v, win0);
-      k_init_scan<<<1, 32, 0, s>>>(v, n_seed, win0, stp);
+      const size_t ring = (size_t)kINSeg * kISeg * 4;
+      set_dyn_smem((const void*)k_init_scan, ring);
+      k_init_scan<<<1, 32, ring, s>>>(v, n_seed, win0, stp);
       cudaError_t e = cudaMemcpyAsync(&h, stp, sizeof h,
                                       cudaMemcpyDeviceToHost, s);
       if (!e) e = cudaStreamSynchronize(s);
@@ -623,7 +711,7 @@ int64_t init_buf_words(int n, int P) {
   int64_t want = (int64_t)P * (2 * (int64_t)n + 64) + 4096;
   const int64_t cap = 32ll << 20;  // 128 MiB window
   want = want < cap ? want : cap;
-  return round_up(want, 8);
+  return round_up(want, kISeg);  // whole ring segments
 }
 
 cudaError_t launch_init_best(const SwarmView& v, cudaStream_t s) {
