@@ -288,45 +288,60 @@ __global__ void __launch_bounds__(128) k_two_opt_rescan64(ScanArgs a) {
 }
 
 // ---- FP32 scan: EXACT32 (MODE 1) and FILTER32 (MODE 2) ---------------------
-// Shared by both modes: a lane computes u = A + (B - d_j) per pair (d_i is
-// folded into a per-row threshold Lrow) and tests min(u) of each group of
-// kG32 column blocks against Lrow.  A hit (rare once the running minimum has
-// settled) goes to the out-of-line handler below, which keeps the kernel
-// inside the instruction cache:
-//   EXACT32  Lrow = best + d_i (exact: |u|, |best + d_i| < 2^24) and the
-//            handler keeps the lane's first strict minimum t = u - d_i with
-//            its (i, j): the reference argmin, bit for bit.
-//   FILTER32 Lrow = fl_ru(best + thr + d_i) (+inf-free: capped at FLT_MAX);
-//            the handler records every pair with u <= Lrow as a candidate
-//            (t = u - d_i, its (i, j)) and tightens the window when t
-//            improves.  The window sits ~10x inside thr = 2 eps of the
+// Two pair rows (i, i+1) per pass.  Per pair a lane computes
+// u = A + (B - d_j); d_i is folded into a per-row threshold Lrow, and one
+// warp-uniform pre-test per group of kG32 column blocks (min of the group's
+// u per row against Lrow) is the only per-pair branch.  Hits (rare once the
+// running minimum has settled) go to an out-of-line handler, which keeps
+// the kernel inside the instruction cache and maintains a warp-wide
+// running minimum:
+//   EXACT32  Lrow = best + d_i (exact: |u|, |best + d_i| < 2^24).  The
+//            handler keeps the lane's first minimum in (t, i, j) order
+//            (lexicographic, since the pass interleaves the two rows); the
+//            pre-test is non-strict for row i and strict for row i+1.  The
+//            reference argmin, bit for bit.
+//   FILTER32 Lrow = fl_ru(best + thr + d_i) (capped at FLT_MAX).  The
+//            handler records every pair with u <= Lrow as a candidate and
+//            tightens the window to the warp minimum + thr, ~10x inside the
 //            rounding bound, so the fp64 argmin and its ties are candidates.
+// The structural pairs (i, i+1) and (0, n-1) are exact no-ops: 0 in
+// EXACT32 (they can only be the argmin when no move is applied), and
+// evaluated exactly in fp64 at the end in FILTER32 - so the fp32 pass may
+// skip or repeat them freely.
 // Per-lane state in shared memory (stride 32 between words): st[0] = the
 // running minimum t; EXACT32: st[32], st[64] = its i, j; FILTER32: st[32] =
 // candidate count, st[64] = overflow flag, cd/cij = candidate slots.
-constexpr int kBufs32 = 2;     // fp32 per-warp ring depth (one row ahead)
+constexpr int kBufs32 = 4;     // fp32 per-warp row ring (one pass ahead)
 constexpr int kG32 = 4;        // column blocks per skip test and pre-test
 constexpr int kNplMax32 = 32;  // column blocks per fp32 task (1024 columns)
+constexpr int kW32 = 2;        // warps (tasks) per CTA, fp32 scan
+
+__device__ __forceinline__ bool lex_less(float t, int i, int j, float bt,
+                                         int bi, int bj) {
+  return t < bt || (t == bt && (i < bi || (i == bi && j < bj)));
+}
 
 template <int MODE>
 __device__ __noinline__ float scan_hit(float u0, float u1, float u2, float u3,
-                                       float di, float lrow, int i, int j0,
-                                       float thr, float* cd, uint32_t* cij,
-                                       float* st) {
-  // entered by the whole warp (the pre-test is warp-uniform); returns the
-  // warp-wide threshold base: EXACT32 the warp minimum, FILTER32 the warp
-  // minimum + thr
-  const float uv[4] = {u0, u1, u2, u3};
+                                       float w0, float w1, float w2, float w3,
+                                       float da, float db, float la, float lb,
+                                       int i, int j0, float thr, float* cd,
+                                       uint32_t* cij, float* st) {
+  // entered by the whole warp (the pre-test is warp-uniform): u = row i,
+  // w = row i+1 of the same 4 column blocks; returns the warp-wide
+  // threshold base (EXACT32: warp minimum; FILTER32: warp minimum + thr)
+  const float uv[8] = {u0, u1, u2, u3, w0, w1, w2, w3};
   float best = st[0];
   if (MODE == 1) {
     int bi = __float_as_int(st[32]), bj = __float_as_int(st[64]);
 #pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      const float t = __fsub_rn(uv[g], di);  // exact
-      if (t < best) {
+    for (int g = 0; g < 8; ++g) {
+      const int ii = i + (g >> 2), jj = j0 + 32 * (g & 3);
+      const float t = __fsub_rn(uv[g], g < 4 ? da : db);  // exact
+      if (lex_less(t, ii, jj, best, bi, bj)) {
         best = t;
-        bi = i;
-        bj = j0 + 32 * g;
+        bi = ii;
+        bj = jj;
       }
     }
     st[0] = best;
@@ -341,10 +356,12 @@ __device__ __noinline__ float scan_hit(float u0, float u1, float u2, float u3,
   int overflow = __float_as_int(st[64]);
   // the new values in the window, then the new warp minimum, then the list
   // against the tightened window (so transient entries never overflow it)
-  float tv[4];
+  float tv[8];
 #pragma unroll
-  for (int g = 0; g < 4; ++g) {
-    tv[g] = uv[g] <= lrow ? __fsub_rn(uv[g], di) : __int_as_float(0x7f800000);
+  for (int g = 0; g < 8; ++g) {
+    const bool in = uv[g] <= (g < 4 ? la : lb);
+    tv[g] = in ? __fsub_rn(uv[g], g < 4 ? da : db)
+               : __int_as_float(0x7f800000);
     best = fminf(best, tv[g]);
   }
   float wbest = best;
@@ -363,11 +380,12 @@ __device__ __noinline__ float scan_hit(float u0, float u1, float u2, float u3,
   }
   ncand = w;
 #pragma unroll
-  for (int g = 0; g < 4; ++g) {
+  for (int g = 0; g < 8; ++g) {
     if (tv[g] <= lim) {
       if (ncand < kCand) {
         cd[32 * ncand] = tv[g];
-        cij[32 * ncand] = ((uint32_t)i << 16) | (uint32_t)(j0 + 32 * g);
+        cij[32 * ncand] = ((uint32_t)(i + (g >> 2)) << 16) |
+                          (uint32_t)(j0 + 32 * (g & 3));
         ++ncand;
       } else {
         overflow = 1;
@@ -385,23 +403,25 @@ __device__ __noinline__ float scan_hit(float u0, float u1, float u2, float u3,
 // Shift-reuse: the A term of pair (i+1, j) is C[a_{i+1}][a_j], which is the
 // B term lane l-1 gathered for pair (i, j-1) (lane 0: lane 31 of block m-1;
 // block 0 of a range with jlo > 0 gathers it once per row), so it arrives by
-// ONE warp rotate and each row costs ONE random shared-memory gather per
-// pair.  Per lane in registers: the gathered B values and the gather byte
-// offsets 4 s_j (two u16 per register).  d_j sits in shared memory
-// (lane-owned, conflict free) as fp32, and a column that is dead for the
-// rest of the task (j <= i + gap, or past the range) holds -inf there, so
-// its u is +inf with no per-pair mask: at row i the owning lane retires
-// column i + gap with one store.  Groups of kG32 blocks with no live column
-// are skipped (warp-uniform test).
+// ONE warp rotate.  A pass over rows (i, i+1) gathers both B rows at the
+// same offsets 4 s_j (unpacked once) and subtracts the same d_j (loaded
+// once): two gathers, two rotates, one d_j load per column block.  The
+// offsets stay in registers (two u16 per register).  d_j sits in shared
+// memory (lane-owned, conflict free) as fp32; a column that is dead for the
+// rest of the task (j <= i, or past the range) holds -inf there, so its u
+// is +inf with no per-pair mask: before the pass the owning lanes retire
+// columns i and i+1.  Groups of kG32 blocks with no live column are skipped
+// (warp-uniform test).  Rows a_r0..a_r1 stream through a 4-slot per-warp
+// ring, one pass (two rows) ahead.
 template <int NPL, int MODE>
-__global__ void __launch_bounds__(kMaxWarps * 32, 4)
+__global__ void __launch_bounds__(kW32 * 32, 5)
     k_two_opt_scan32(ScanArgs a) {
   if (a.ctl && (a.ctl->done || a.ctl->improved)) return;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bars[kMaxWarps][kBufs32];
-  __shared__ uint32_t s_cij[kMaxWarps][kCand][32];
-  __shared__ float s_cd[kMaxWarps][kCand][32];
-  __shared__ float s_st[kMaxWarps][3][32];
+  __shared__ __align__(8) uint64_t bars[kW32][kBufs32];
+  __shared__ uint32_t s_cij[kW32][kCand][32];
+  __shared__ float s_cd[kW32][kCand][32];
+  __shared__ float s_st[kW32][3][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int task = blockIdx.x * (blockDim.x >> 5) + warp;
   const int p = task / a.chunks, c = task % a.chunks;
@@ -422,11 +442,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 4)
   }
   const uint16_t* tour = a.tours + (size_t)p * a.np;
   const double* dg = a.dcache + (size_t)p * a.np;
-  // FILTER32 excludes the structural pairs (i, i+1) (and (0, n-1) below)
-  constexpr int kGap = MODE == 2 ? 1 : 0;
   unsigned char* wbase = smem + (size_t)warp * a.buf_stride2;
   float* sdj = (float*)(wbase + kBufs32 * a.buf_stride);  // local column
-  const bool excl_last = MODE == 2 && r0 == 0 && n - 1 >= jlo && n - 1 < jhi;
 
   constexpr int NH = (NPL + 1) / 2;
   uint32_t sjp[NH];  // 4 s_j for blocks 2h (lo) and 2h+1 (hi)
@@ -442,14 +459,12 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 4)
   }
   for (int jl = lane; jl < 32 * NPL; jl += 32) {
     const int j = jlo + jl;
-    sdj[jl] = (j > r0 + kGap && j < jhi && !(excl_last && j == n - 1))
-                  ? (float)dg[j]
-                  : -kInfF;
+    sdj[jl] = (j >= r0 && j < jhi) ? (float)dg[j] : -kInfF;
   }
   auto sj = [&](int m) -> uint32_t {
     return (m & 1) ? (sjp[m / 2] >> 16) : (sjp[m / 2] & 0xFFFFu);
   };
-  const int nrows = r1 - r0 + 1;  // cost rows a_r0 .. a_r1
+  const int nrows = r1 - r0 + 1;  // cost rows a_r0 .. a_r1 (ring index q)
   uint64_t* wb = bars[warp];
   auto issue = [&](int q, int city) {
     const int s_ = q % kBufs32;
@@ -460,18 +475,17 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 4)
   if (lane == 0) {
     for (int s_ = 0; s_ < kBufs32; ++s_) mbar_init(&wb[s_], 1);
     fence_barrier_init();
-    for (int q = 0; q < kBufs32 && q < nrows; ++q) issue(q, tour[r0 + q]);
+    for (int q = 0; q < 3 && q < nrows; ++q) issue(q, tour[r0 + q]);
   }
-  // Per-row scalars come from lane-parallel loads of 32 rows at a time,
-  // one block of rows ahead: cb = the cities of ring rows (copy issued for
-  // row index k + kBufs32 at row k), db = d_i as fp32.
-  auto city_at = [&](int k) -> int {  // ring row k = tour[r0 + k]
-    return k < nrows ? (int)tour[r0 + k] : 0;
+  // Per-pass scalars from lane-parallel loads of 32 rows at a time, one
+  // block ahead: cb = the cities of ring rows 3 + k (+1), db = d_{r0 + k}.
+  auto city_at = [&](int q) -> int {
+    return q < nrows ? (int)tour[r0 + q] : 0;
   };
-  auto d_at = [&](int k) -> float {  // d_{r0 + k}
+  auto d_at = [&](int k) -> float {
     return r0 + k < r1 ? (float)dg[r0 + k] : 0.f;
   };
-  int cb = city_at(kBufs32 + lane), cb_next = city_at(kBufs32 + 32 + lane);
+  int cb = city_at(3 + lane), cb_next = city_at(3 + 32 + lane);
   float db = d_at(lane), db_next = d_at(32 + lane);
   __syncwarp();
   auto row = [&](int q) -> const unsigned char* {
@@ -494,63 +508,89 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 4)
     a0 = at4(R, s4lo);
   }
   float lim = MODE == 1 ? kInfF : FLT_MAX;
-  for (int i = r0; i < r1; ++i) {
-    const int k = i - r0;
-    const int q = k + 1;  // ring index of the B row a_{i+1}
-    if (k > 0 && (k & 31) == 0) {  // next block of per-row scalars
+  for (int i = r0; i < r1; i += 2) {
+    const int k = i - r0;  // even
+    const bool two = i + 1 < r1;
+    if (k > 0 && (k & 31) == 0) {  // next block of per-pass scalars
       cb = cb_next;
       db = db_next;
-      cb_next = city_at(kBufs32 + k + 32 + lane);
+      cb_next = city_at(3 + k + 32 + lane);
       db_next = d_at(k + 32 + lane);
     }
-    const int city = __shfl_sync(0xffffffffu, cb, k & 31);
-    const float di = __shfl_sync(0xffffffffu, db, k & 31);
-    // the slot of row q - 1 (read last iteration; those shared loads have
-    // completed, their values consumed) takes row q + 1
-    if (lane == 0 && q + kBufs32 - 1 < nrows) issue(q + kBufs32 - 1, city);
-    {  // retire column i + gap (its owner lane); row 0's (0, n-1) is back
-      const int cl = i + kGap - jlo;
-      if (cl >= 0 && cl < 32 * NPL && lane == (cl & 31)) sdj[cl] = -kInfF;
-      if (excl_last && i == 1 && lane == ((n - 1 - jlo) & 31))
-        sdj[n - 1 - jlo] = (float)dg[n - 1];
+    {  // rows k + 3, k + 4 into the slots of rows k - 1, k (read last pass;
+       // those shared loads have completed, their values consumed)
+      const int c3 = __shfl_sync(0xffffffffu, cb, k & 31);
+      const int c4 = __shfl_sync(0xffffffffu, cb, (k + 1) & 31);
+      if (lane == 0) {
+        if (k + 3 < nrows) issue(k + 3, c3);
+        if (k + 4 < nrows) issue(k + 4, c4);
+      }
     }
-    const unsigned char* B = row(q);
+    const float di = __shfl_sync(0xffffffffu, db, k & 31);
+    const float di2 = __shfl_sync(0xffffffffu, db, (k + 1) & 31);
+    {  // retire columns i and i + 1 (their owner lanes)
+      const int c0 = i - jlo, c1 = i + 1 - jlo;
+      if (c0 >= 0 && c0 < 32 * NPL && lane == (c0 & 31)) sdj[c0] = -kInfF;
+      if (two && c1 >= 0 && c1 < 32 * NPL && lane == (c1 & 31))
+        sdj[c1] = -kInfF;
+    }
+    const unsigned char* B1 = row(k + 1);
+    const unsigned char* B2 = two ? row(k + 2) : B1;
     if (a.stream_only) {
-      if (lane == 0 && at4(B, 0) == -1.f) lim = 0.f;  // keep the load
+      if (lane == 0 && at4(B2, 0) == -1.f) lim = 0.f;  // keep the loads
       continue;
     }
-    float lrow = MODE == 1 ? __fadd_rn(lim, di)
-                           : fminf(__fadd_ru(lim, di), FLT_MAX);
-    float rprev = a0;  // lane 0's A term of the next block
-    a0 = at4(B, s4lo);  // for row i + 1
+    auto lrow_of = [&](float d) -> float {
+      return MODE == 1 ? __fadd_rn(lim, d) : fminf(__fadd_ru(lim, d), FLT_MAX);
+    };
+    float la = lrow_of(di);
+    float lb = two ? lrow_of(di2) : -kInfF;
+    float rp1 = a0;             // lane 0's A term of the next block, row i
+    float rp2 = at4(B1, s4lo);  // ... row i + 1
+    a0 = at4(B2, s4lo);         // row i + 2 (next pass)
 #pragma unroll
     for (int m0 = 0; m0 < NPL; m0 += kG32) {
-      if (jlo + 32 * (m0 + kG32) - 1 > i + kGap) {  // warp-uniform: live
-        if (m0 > 0 && !(jlo + 32 * m0 - 1 > i + kGap))  // previous skipped
-          rprev = __shfl_sync(0xffffffffu, Bv[m0 - 1], 31);
-        float u[kG32];
+      if (jlo + 32 * (m0 + kG32) - 1 > i + 1) {  // warp-uniform: live
+        if (m0 > 0 && !(jlo + 32 * m0 - 1 > i + 1)) {  // previous skipped
+          // lane 0's A terms: column c - 1 of the previous pass's B row
+          // (still in Bv) and of B1, c = the group's first column
+          rp1 = __shfl_sync(0xffffffffu, Bv[m0 - 1], 31);
+          rp2 = at4(B1, __shfl_sync(0xffffffffu, sj(m0 - 1), 31));
+        }
+        float u[kG32], w[kG32];
 #pragma unroll
         for (int g = 0; g < kG32; ++g) {
           const int m = m0 + g;
           if (m < NPL) {
-            const float r = __shfl_sync(0xffffffffu, Bv[m], (lane + 31) & 31);
-            const float av = lane == 0 ? rprev : r;
-            rprev = r;
-            const float bv = at4(B, sj(m));
-            Bv[m] = bv;
-            u[g] = __fadd_rn(av, __fsub_rn(bv, sdj[lane + 32 * m]));
+            const uint32_t o = sj(m);
+            const float b1 = at4(B1, o), b2 = at4(B2, o);
+            const float dj = sdj[lane + 32 * m];
+            const float r1v =
+                __shfl_sync(0xffffffffu, Bv[m], (lane + 31) & 31);
+            const float av1 = lane == 0 ? rp1 : r1v;
+            rp1 = r1v;
+            const float r2v = __shfl_sync(0xffffffffu, b1, (lane + 31) & 31);
+            const float av2 = lane == 0 ? rp2 : r2v;
+            rp2 = r2v;
+            Bv[m] = b2;
+            u[g] = __fadd_rn(av1, __fsub_rn(b1, dj));
+            w[g] = __fadd_rn(av2, __fsub_rn(b2, dj));
           } else {
             u[g] = kInfF;
+            w[g] = kInfF;
           }
         }
-        const float mn = fminf(fminf(u[0], u[1]), fminf(u[2], u[3]));
-        if (__any_sync(0xffffffffu, MODE == 1 ? mn < lrow : mn <= lrow)) {
-          lim = scan_hit<MODE>(u[0], u[1], u[2], u[3], di, lrow, i,
-                               jlo + lane + 32 * m0, a.thr,
-                               &s_cd[warp][0][lane], &s_cij[warp][0][lane],
-                               st);
-          lrow = MODE == 1 ? __fadd_rn(lim, di)
-                           : fminf(__fadd_ru(lim, di), FLT_MAX);
+        const float mu = fminf(fminf(u[0], u[1]), fminf(u[2], u[3]));
+        const float mw = fminf(fminf(w[0], w[1]), fminf(w[2], w[3]));
+        const bool hit = MODE == 1 ? (mu <= la || mw < lb)
+                                   : (mu <= la || mw <= lb);
+        if (__any_sync(0xffffffffu, hit)) {
+          lim = scan_hit<MODE>(u[0], u[1], u[2], u[3], w[0], w[1], w[2], w[3],
+                               di, di2, la, lb, i, jlo + lane + 32 * m0,
+                               a.thr, &s_cd[warp][0][lane],
+                               &s_cij[warp][0][lane], st);
+          la = lrow_of(di);
+          lb = two ? lrow_of(di2) : -kInfF;
         }
       }
     }
@@ -581,40 +621,40 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 4)
   const float keep = __fadd_ru(m, a.thr);
   double bd = kInf;
   int ei = 0x7fffffff, ej = 0x7fffffff;
-  for (int k = 0; k < ncand; ++k) {
-    if (s_cd[warp][k][lane] <= keep) {
-      const uint32_t ij = s_cij[warp][k][lane];
-      const int i = (int)(ij >> 16), j = (int)(ij & 0xFFFFu);
-      const int ai = tour[i], aj = tour[j];
-      const int si = tour[i + 1], sjj = tour[j + 1 == n ? 0 : j + 1];
+  for (int kc = 0; kc < ncand; ++kc) {
+    if (s_cd[warp][kc][lane] <= keep) {
+      const uint32_t ij = s_cij[warp][kc][lane];
+      const int ci = (int)(ij >> 16), cj = (int)(ij & 0xFFFFu);
+      const int ai = tour[ci], aj = tour[cj];
+      const int si = tour[ci + 1], sjj = tour[cj + 1 == n ? 0 : cj + 1];
       double t = __dadd_rn(a.cost[(size_t)ai * a.ld + aj],
                            a.cost[(size_t)si * a.ld + sjj]);
-      t = __dsub_rn(t, dg[i]);
-      t = __dsub_rn(t, dg[j]);
-      if (res_less(t, i, j, bd, ei, ej)) {
+      t = __dsub_rn(t, dg[ci]);
+      t = __dsub_rn(t, dg[cj]);
+      if (res_less(t, ci, cj, bd, ei, ej)) {
         bd = t;
-        ei = i;
-        ej = j;
+        ei = ci;
+        ej = cj;
       }
     }
   }
   // structural pairs of this task, exact from d: (i, i+1) has A = d_i,
-  // B = d_{i+1}
-  for (int i = r0 + lane; i < r1; i += 32) {
-    if (i + 1 < n && i + 1 >= jlo && i + 1 < jhi) {
-      const double d0 = dg[i], d1 = dg[i + 1];
+  // B = d_{i+1}; (0, n-1) from the matrix
+  for (int ii = r0 + lane; ii < r1; ii += 32) {
+    if (ii + 1 < n && ii + 1 >= jlo && ii + 1 < jhi) {
+      const double d0 = dg[ii], d1 = dg[ii + 1];
       double t = __dadd_rn(d0, d1);
       t = __dsub_rn(t, d0);
       t = __dsub_rn(t, d1);
-      if (res_less(t, i, i + 1, bd, ei, ej)) {
+      if (res_less(t, ii, ii + 1, bd, ei, ej)) {
         bd = t;
-        ei = i;
-        ej = i + 1;
+        ei = ii;
+        ej = ii + 1;
       }
     }
   }
-  if (excl_last && lane == 0 && n - 1 > 1) {  // (0, n-1): s_{n-1} = a_0
-    const int j = n - 1;
+  if (r0 == 0 && n - 1 >= jlo && n - 1 < jhi && lane == 0 && n - 1 > 1) {
+    const int j = n - 1;  // s_{n-1} = a_0
     const int a0c = tour[0], aj = tour[j], s0 = tour[1], sjj = tour[0];
     double t = __dadd_rn(a.cost[(size_t)a0c * a.ld + aj],
                          a.cost[(size_t)s0 * a.ld + sjj]);
@@ -939,7 +979,7 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
       const int npl32 = std::min(std::max(npl, 1), kNplMax32);
       a.buf_stride2 = (uint32_t)(kBufs32 * a.buf_stride +
                                  round_up((int64_t)32 * npl32 * 4, 128));
-      const int warps = kMaxWarps;
+      const int warps = kW32;
       const size_t smem = (size_t)warps * a.buf_stride2;
       if (pl.mode == kScanFilter32) e = cudaMemsetAsync(a.ovf, 0, 4, s);
       if (e != cudaSuccess) return e;

@@ -104,6 +104,13 @@ def test_best_exchange_near_ties_and_converged(pkg, scan_mode):
         tour, _ = O.nearest_neighbor_two_opt(cost)
         body = np.array([tour[:-1]], dtype=np.int32)
         check_batch(pkg, cost, body, ("converged", n, scan_mode))
+    # a 2-opt-optimal tour across the fp32 scan's column ranges (n > 1024:
+    # the structural pair (1023, 1024) sits on a range boundary), built by
+    # the device NN + 2-opt (bit-exact to the oracle, test_nn_two_opt_golden)
+    cost = random_euclidean_matrix(1100, rng)
+    tour, _ = pkg.nearest_neighbor_two_opt(cost)
+    body = np.array([list(tour)[:-1]], dtype=np.int32)
+    check_batch(pkg, cost, body, ("converged", 1100, scan_mode))
     # large values: fp64 residues of the no-op pairs exceed 1e-12
     cost = random_euclidean_matrix(60, rng) * 1e9
     tours = np.array([rng.permutation(60) for _ in range(4)], dtype=np.int32)
