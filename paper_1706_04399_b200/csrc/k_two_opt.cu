@@ -488,13 +488,17 @@ __global__ void __launch_bounds__(kW32 * 32, 5)
   int cb = city_at(3 + lane), cb_next = city_at(3 + 32 + lane);
   float db = d_at(lane), db_next = d_at(32 + lane);
   __syncwarp();
-  auto row = [&](int q) -> const unsigned char* {
+  // rows as 32-bit shared-window addresses: gathers are plain LDS [R]
+  const uint32_t wbase_s = smem_u32(wbase);
+  auto row = [&](int q) -> uint32_t {
     const int s_ = q % kBufs32;
     mbar_wait(&wb[s_], (uint32_t)((q / kBufs32) & 1));
-    return wbase + (size_t)s_ * a.buf_stride;
+    return wbase_s + (uint32_t)s_ * a.buf_stride;
   };
-  auto at4 = [](const unsigned char* R, uint32_t off4) -> float {
-    return *reinterpret_cast<const float*>(R + off4);
+  auto at4 = [](uint32_t R, uint32_t off4) -> float {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(R + off4));
+    return v;
   };
   // prime: Bv = row a_r0 gathered at s_j (the "B term of row r0 - 1"); for
   // jlo > 0 lane 0's A term of block 0 is C[a_i][a_jlo], gathered per row
@@ -502,7 +506,7 @@ __global__ void __launch_bounds__(kW32 * 32, 5)
   float Bv[NPL];
   float a0;
   {
-    const unsigned char* R = row(0);
+    const uint32_t R = row(0);
 #pragma unroll
     for (int m = 0; m < NPL; ++m) Bv[m] = at4(R, sj(m));
     a0 = at4(R, s4lo);
@@ -534,8 +538,8 @@ __global__ void __launch_bounds__(kW32 * 32, 5)
       if (two && c1 >= 0 && c1 < 32 * NPL && lane == (c1 & 31))
         sdj[c1] = -kInfF;
     }
-    const unsigned char* B1 = row(k + 1);
-    const unsigned char* B2 = two ? row(k + 2) : B1;
+    const uint32_t B1 = row(k + 1);
+    const uint32_t B2 = two ? row(k + 2) : B1;
     if (a.stream_only) {
       if (lane == 0 && at4(B2, 0) == -1.f) lim = 0.f;  // keep the loads
       continue;
