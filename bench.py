@@ -55,8 +55,9 @@ CONFIGS = {
     "c4": dict(n=2000, P=65536, G=50, matrix="euclid",
                workload="C4: synthetic N=2000 extended TSP, P=65536"),
     "c5": dict(n=10000, P=65536, G=20, matrix="euclid", ee=False,
+               rng="philox",
                workload="C5: synthetic N=10000, P=65536 per GPU, islands, "
-                        "use_edge_exchange=False"),
+                        "use_edge_exchange=False, Philox production RNG"),
 }
 
 
@@ -257,10 +258,20 @@ def config_dict(cfg_name, cfg, args):
 
 # --------------------------------------------------------------- our arm
 def kernels_per_generation(cfg):
-    k = 2 + 1  # begin, update, select
-    k += 7  # mutation pipeline (no-op kernels on non-mutating generations)
+    """Kernels one generation's CUDA graph launches (device flags make the
+    ones a generation does not need exit at entry; they still launch)."""
+    k = 1 + 1 + 2  # gen_begin, update, fitness + pbest copy
+    k += 6         # mutation: hash, rank, dedupe, verify, lists, copy
+    if RNG == "philox":
+        k += 1     # Philox sampler
+    else:
+        k += 2 + 2  # sampler + fix; stream gen + walk (forked stream)
+    k += 1 + 2     # swap, then fitness + pbest copy of the mutated
+    k += 1         # select
     if cfg.get("ee", True):
-        k += 3  # 2-opt scan, apply, finalize
+        # scan (FILTER32 adds the overflow re-scan), apply, finalize
+        k += (1 if cfg["matrix"] in ("grid", "euclid_int", "wall") else 2)
+        k += 2
     return k
 
 
@@ -435,9 +446,10 @@ def main():
     ap.add_argument("--profile-gens", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--rng", choices=["numpy", "philox"], default="numpy",
+    ap.add_argument("--rng", choices=["numpy", "philox"], default=None,
                     help="numpy: the reference's PCG64 streams bit for bit; "
-                         "philox: counter-based production RNG")
+                         "philox: counter-based production RNG (default: "
+                         "the config's; numpy except C5)")
     ap.add_argument("--scan-mode", choices=["auto", "fp64", "exact32",
                                             "filter32"], default="auto",
                     help="force the 2-opt scan mode (default: chosen from "
@@ -447,7 +459,7 @@ def main():
         args.warmup = 3
     cfg = CONFIGS[args.config]
     global RNG
-    RNG = args.rng
+    RNG = args.rng or cfg.get("rng", "numpy")
     if args.scan_mode != "auto":
         os.environ["DPSO_SCAN_MODE"] = {"fp64": "0", "exact32": "1",
                                         "filter32": "2"}[args.scan_mode]

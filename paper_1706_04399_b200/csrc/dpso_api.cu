@@ -57,7 +57,7 @@ int cuda_fail(cudaError_t e, const char* where) {
 struct Layout {
   size_t off_ctl, off_streams, off_mut_start, off_init_start, off_x, off_pbest, off_vmap,
       off_vel, off_vel_len, off_fit, off_pfit, off_dcache, off_gbest,
-      off_conv, off_tores, off_chunk_tab, off_rank, off_hash, off_flag,
+      off_conv, off_tores, off_chunk_tab, off_rank, off_hash, off_flag, off_pbflag,
       off_sidx, off_order, off_surv, off_keep, off_ev_slot, off_ev_k,
       off_ev_cursor, off_ev_end, off_ev_idx, off_mstream, off_init_buf,
       off_init_state, off_init_cursor, off_seed, off_cost32,
@@ -105,6 +105,7 @@ Layout make_layout(const dpso_params* prm, int n) {
   L.off_rank = take(4 * P);
   L.off_hash = take(8 * P);
   L.off_flag = take(4 * P);
+  L.off_pbflag = take(4 * P);
   L.off_sidx = take(4 * P);
   L.off_order = take(4 * P);
   L.off_surv = take(4 * P);
@@ -342,6 +343,7 @@ int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
   v.rank = (int32_t*)(w + L.off_rank);
   v.hash = (uint64_t*)(w + L.off_hash);
   v.flag = (int32_t*)(w + L.off_flag);
+  v.pbflag = (int32_t*)(w + L.off_pbflag);
   v.sidx = (int32_t*)(w + L.off_sidx);
   v.order = (int32_t*)(w + L.off_order);
   v.surv_list = (int32_t*)(w + L.off_surv);

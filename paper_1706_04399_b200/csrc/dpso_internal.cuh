@@ -112,6 +112,7 @@ struct SwarmView {
   int32_t* rank;
   uint64_t* hash;
   int32_t* flag;       // 1 = dropped duplicate
+  int32_t* pbflag;     // P: the last fitness pass improved pbest
   int32_t* sidx;       // survivor / dropped index in rank order
   int32_t* order;      // slot at each rank
   int32_t* surv_list;
@@ -142,6 +143,7 @@ cudaError_t launch_mutation(const SwarmView& v, cudaStream_t s);
 // depends only on the mutation stream after launch_mutation_post, or after
 // init) and may run on a forked stream concurrently with everything else.
 cudaError_t launch_mutation_walk(const SwarmView& v, cudaStream_t s);
+cudaError_t launch_fitness(const SwarmView& v, int use_list, cudaStream_t s);
 cudaError_t launch_mutation_swap(const SwarmView& v, cudaStream_t s);
 int64_t mstream_words(int n, int P);
 int64_t init_buf_words(int n, int P);

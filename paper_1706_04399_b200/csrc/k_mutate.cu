@@ -953,8 +953,6 @@ __global__ void __launch_bounds__(128) k_mut_swap(SwarmView v) {
   if (!v.ctl->mutating || v.ctl->done) return;
   const int e = blockIdx.x;
   if (e >= v.ctl->n_events) return;
-  extern __shared__ __align__(16) unsigned char smem[];
-  double* sd = (double*)smem;
   const int n = v.n, np = v.np, tid = threadIdx.x;
   const int p = v.ev_slot[e];
   const int k = v.ev_k[(size_t)v.ctl->mut_cur * v.P + e];
@@ -969,25 +967,11 @@ __global__ void __launch_bounds__(128) k_mut_swap(SwarmView v) {
     body[b] = x;
   }
   __syncthreads();
+  // edge costs; the fitness and pbest follow in k_fitness (event list)
   double* dg = v.dcache + (size_t)p * np;
   for (int i = tid; i < n; i += blockDim.x) {
     const int a = body[i], b = body[i + 1 == n ? 0 : i + 1];
-    const double d = v.cost[(size_t)a * v.ld + b];
-    sd[i] = d;
-    dg[i] = d;
-  }
-  __syncthreads();
-  __shared__ int s_better;
-  if (tid == 0) {
-    const double f = seq_tour_sum(sd, n);
-    v.fit[p] = f;
-    s_better = f < v.pfit[p];
-    if (s_better) v.pfit[p] = f;
-  }
-  __syncthreads();
-  if (s_better) {
-    uint16_t* pb = v.pbest + (size_t)p * np;
-    for (int i = tid; i < n; i += blockDim.x) pb[i] = body[i];
+    dg[i] = v.cost[(size_t)a * v.ld + b];
   }
 }
 
@@ -1061,10 +1045,9 @@ cudaError_t launch_mutation_post(const SwarmView& v, cudaStream_t s) {
 }
 
 cudaError_t launch_mutation_swap(const SwarmView& v, cudaStream_t s) {
-  const size_t sd = (size_t)8 * v.np;
-  set_dyn_smem((const void*)k_mut_swap, sd);
-  k_mut_swap<<<v.P, 128, sd, s>>>(v);
-  return cudaGetLastError();
+  k_mut_swap<<<v.P, 128, 0, s>>>(v);
+  cudaError_t e = cudaGetLastError();
+  return e ? e : launch_fitness(v, 1, s);
 }
 
 cudaError_t launch_mutation(const SwarmView& v, cudaStream_t s) {

@@ -861,7 +861,10 @@ int two_opt_pick_chunks(int32_t n, int32_t P) {
   if (warps_per_sm > 16) warps_per_sm = 16;
   const int64_t slots = (int64_t)sms * warps_per_sm;
   const int R = column_ranges(n);
-  int chunks = (int)((4 * slots + P - 1) / P);
+  // tasks per resident warp slot: balances the tail against per-task setup
+  int per_slot = 4;
+  if (const char* e = getenv("DPSO_TASKS_PER_SLOT")) per_slot = std::max(1, atoi(e));
+  int chunks = (int)((per_slot * slots + P - 1) / P);
   chunks = std::max(chunks, R);
   chunks = std::min(chunks, 32 * R);
   chunks = std::min(chunks, std::max(R, n / 8 + 1));

@@ -19,8 +19,11 @@
 // For w < 1 the reference keeps an explicit transposition list and replays
 // it (solver.py:213-216); that path runs the repair sequentially in one
 // thread per particle (k_update_seq) on a bounded per-particle ring.
+#include <algorithm>
+
 #include "dpso_internal.cuh"
 #include "philox.cuh"
+#include "tma.cuh"
 
 namespace dpso {
 
@@ -153,33 +156,19 @@ __device__ void sigma_pass(const uint16_t* __restrict__ tgt_g, double c,
   __syncthreads();
 }
 
-// x' is in sx; compute d_i, the sequential fitness, write x/dcache/fit and
-// update pbest (solver.py:217-220).  sd is an 8*np-byte scratch.
+// x' is in sx: write x and the edge costs d_i (dcache).  The fitness and
+// pbest (solver.py:217-220) follow in k_fitness / k_pbest_copy, one thread
+// per particle, so the sequential fp64 sums of all particles run
+// concurrently instead of on one thread of each CTA.
 template <int T>
-__device__ void finish_particle(const SwarmView& v, int p, const uint16_t* sx,
-                                double* sd, int* s_flag) {
+__device__ void finish_particle(const SwarmView& v, int p, const uint16_t* sx) {
   const int n = v.n, np = v.np, tid = threadIdx.x;
   uint16_t* xg = v.x + (size_t)p * np;
   double* dg = v.dcache + (size_t)p * np;
   for (int i = tid; i < n; i += T) {
     int a = sx[i], b = sx[i + 1 == n ? 0 : i + 1];
-    double d = __ldg(v.cost + (size_t)a * v.ld + b);
-    sd[i] = d;
-    dg[i] = d;
+    dg[i] = __ldg(v.cost + (size_t)a * v.ld + b);
     xg[i] = (uint16_t)a;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double f = seq_tour_sum(sd, n);
-    v.fit[p] = f;
-    int better = f < v.pfit[p];
-    if (better) v.pfit[p] = f;
-    s_flag[0] = better;
-  }
-  __syncthreads();
-  if (s_flag[0]) {
-    uint16_t* pb = v.pbest + (size_t)p * np;
-    for (int i = tid; i < n; i += T) pb[i] = sx[i];
   }
   __syncthreads();
 }
@@ -196,7 +185,6 @@ __global__ void __launch_bounds__(T) k_update_w1(SwarmView v, int R) {
   uint16_t* sT = ssig2 + np;
   uint16_t* sB = sT + np;
   uint32_t* sW = (uint32_t*)(sB + np);
-  double* sd = (double*)sT;  // aliases sT, sB, sW (8*np bytes)
   __shared__ int s_warp[32];
   __shared__ int s_misc[4];
   __shared__ double s_c[2];
@@ -224,7 +212,7 @@ __global__ void __launch_bounds__(T) k_update_w1(SwarmView v, int R) {
     for (int u = tid; u < n; u += T) vm[u] = sB[u];
     for (int i = tid; i < n; i += T) sx[i] = sB[sx[i]];
     __syncthreads();
-    finish_particle<T>(v, p, sx, sd, s_misc);
+    finish_particle<T>(v, p, sx);
   }
 }
 
@@ -257,8 +245,6 @@ __global__ void __launch_bounds__(32) k_update_seq(SwarmView v) {
   uint16_t* scur = sx + np;
   uint16_t* spos = scur + np;
   uint16_t* sgt = spos + np;
-  double* sd = (double*)(sgt + np);
-  __shared__ int s_flag[2];
   for (int p = blockIdx.x; p < v.P; p += gridDim.x) {
     const uint16_t* xg = v.x + (size_t)p * np;
     for (int i = tid; i < n; i += 32) sx[i] = xg[i];
@@ -305,7 +291,93 @@ __global__ void __launch_bounds__(32) k_update_seq(SwarmView v) {
       for (int i = 0; i < n; ++i) sx[i] = scur[i];
     }
     __syncwarp();
-    finish_particle<32>(v, p, sx, sd, s_flag);
+    finish_particle<32>(v, p, sx);
+  }
+}
+
+// Fitness of a particle from its dcache row in the reference's order
+// (_tour_cost, solver.py:48-54: the closing edge first, then left to
+// right), then pbest (solver.py:217-220).  One warp per particle (all
+// particles, or the mutated ones of this call: the mutation's event list,
+// events with k < 1 leave their particle untouched).  The sum is one
+// dependent fp64 chain; lane 0 feeds it from a 2-slot shared-memory ring of
+// kFitChunk-double chunks that cp.async.bulk copies one chunk ahead, so the
+// chain never waits on L2.
+constexpr int kFitChunk = 256;  // doubles per chunk (2 KiB)
+constexpr int kFitWarps = 4;    // particles per CTA
+
+__global__ void __launch_bounds__(kFitWarps * 32) k_fitness(SwarmView v,
+                                                            int use_list) {
+  if (v.ctl->done) return;
+  if (use_list && !v.ctl->mutating) return;
+  __shared__ __align__(16) double s_buf[kFitWarps][2][kFitChunk];
+  __shared__ __align__(8) uint64_t s_bar[kFitWarps][2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = blockIdx.x * kFitWarps + warp;
+  const int cnt = use_list ? v.ctl->n_events : v.P;
+  if (t >= cnt || lane != 0) return;
+  int p = t;
+  if (use_list) {
+    if (v.ev_k[(size_t)v.ctl->mut_cur * v.P + t] < 1) return;
+    p = v.ev_slot[t];
+  }
+  const int n = v.n;
+  const double* dg = v.dcache + (size_t)p * v.np;
+  uint64_t* bar = s_bar[warp];
+  mbar_init(&bar[0], 1);
+  mbar_init(&bar[1], 1);
+  fence_barrier_init();
+  const int nch = (n + kFitChunk - 1) / kFitChunk;  // chunks of d_0..d_{n-1}
+  auto issue = [&](int c) {
+    const int lo = c * kFitChunk;
+    const int len = min(kFitChunk, v.np - lo);  // np: whole 16-B units
+    mbar_expect_tx(&bar[c & 1], (uint32_t)len * 8u);
+    bulk_g2s(s_buf[warp][c & 1], dg + lo, (uint32_t)len * 8u, &bar[c & 1]);
+  };
+  issue(0);
+  if (nch > 1) issue(1);
+  double total = __dadd_rn(0.0, __ldg(dg + n - 1));
+  const int m = n - 1;  // d_0 .. d_{n-2}
+  for (int c = 0; c < nch; ++c) {
+    mbar_wait(&bar[c & 1], (uint32_t)((c >> 1) & 1));
+    const double* b = s_buf[warp][c & 1];
+    const int lo = c * kFitChunk;
+    const int hi = min(m, lo + kFitChunk);
+    int i = lo;
+    for (; i + 4 <= hi; i += 4) {
+      const double2 x0 = *reinterpret_cast<const double2*>(b + (i - lo));
+      const double2 x1 = *reinterpret_cast<const double2*>(b + (i - lo) + 2);
+      total = __dadd_rn(total, x0.x);
+      total = __dadd_rn(total, x0.y);
+      total = __dadd_rn(total, x1.x);
+      total = __dadd_rn(total, x1.y);
+    }
+    for (; i < hi; ++i) total = __dadd_rn(total, b[i - lo]);
+    if (c + 2 < nch) issue(c + 2);  // the slot just read (generic reads
+                                    // completed: their values are summed)
+  }
+  v.fit[p] = total;
+  const int better = total < v.pfit[p];
+  if (better) v.pfit[p] = total;
+  v.pbflag[p] = better;
+}
+
+// pbest <- x for the particles k_fitness flagged (16-byte copies).
+__global__ void __launch_bounds__(128) k_pbest_copy(SwarmView v,
+                                                    int use_list) {
+  if (v.ctl->done) return;
+  if (use_list && !v.ctl->mutating) return;
+  const int cnt = use_list ? v.ctl->n_events : v.P;
+  for (int t = blockIdx.x; t < cnt; t += gridDim.x) {
+    int p = t;
+    if (use_list) {
+      if (v.ev_k[(size_t)v.ctl->mut_cur * v.P + t] < 1) continue;
+      p = v.ev_slot[t];
+    }
+    if (!v.pbflag[p]) continue;
+    const uint4* src = reinterpret_cast<const uint4*>(v.x + (size_t)p * v.np);
+    uint4* dst = reinterpret_cast<uint4*>(v.pbest + (size_t)p * v.np);
+    for (int w = threadIdx.x; w < v.np / 8; w += blockDim.x) dst[w] = src[w];
   }
 }
 
@@ -336,6 +408,13 @@ cudaError_t launch_update(const SwarmView& v, cudaStream_t s) {
     set_dyn_smem((const void*)k_update_seq, smem);
     k_update_seq<<<grid, 32, smem, s>>>(v);
   }
+  return launch_fitness(v, 0, s);
+}
+
+cudaError_t launch_fitness(const SwarmView& v, int use_list, cudaStream_t s) {
+  k_fitness<<<(v.P + kFitWarps - 1) / kFitWarps, kFitWarps * 32, 0, s>>>(
+      v, use_list);
+  k_pbest_copy<<<std::min(v.P, 148 * 8), 128, 0, s>>>(v, use_list);
   return cudaGetLastError();
 }
 
