@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(128) k_two_opt_rescan64(ScanArgs a) {
 // ---- FP32 scan: EXACT32 (MODE 1) and FILTER32 (MODE 2) ---------------------
 // Two pair rows (i, i+1) per pass.  Per pair a lane computes
 // u = A + (B - d_j); d_i is folded into a per-row threshold Lrow, and one
-// warp-uniform pre-test per group of kG32 column blocks (min of the group's
+// warp-uniform pre-test per group of column blocks (min of the group's
 // u per row against Lrow) is the only per-pair branch.  Hits (rare once the
 // running minimum has settled) go to an out-of-line handler, which keeps
 // the kernel inside the instruction cache and maintains a warp-wide
@@ -312,7 +312,10 @@ __global__ void __launch_bounds__(128) k_two_opt_rescan64(ScanArgs a) {
 // running minimum t; EXACT32: st[32], st[64] = its i, j; FILTER32: st[32] =
 // candidate count, st[64] = overflow flag, cd/cij = candidate slots.
 constexpr int kBufs32 = 4;     // fp32 per-warp row ring (one pass ahead)
-constexpr int kG32 = 4;        // column blocks per skip test and pre-test
+// column blocks per skip test and pre-test: 8 for full-width tasks (more
+// independent work per pre-test), 4 for narrow ones (finer dead-group skip)
+template <int NPL>
+constexpr int group_blocks() { return NPL >= 32 ? 8 : 4; }
 constexpr int kNplMax32 = 32;  // column blocks per fp32 task (1024 columns)
 constexpr int kW32 = 2;        // warps (tasks) per CTA, fp32 scan
 
@@ -410,7 +413,7 @@ __device__ __noinline__ float scan_hit(float u0, float u1, float u2, float u3,
 // memory (lane-owned, conflict free) as fp32; a column that is dead for the
 // rest of the task (j <= i, or past the range) holds -inf there, so its u
 // is +inf with no per-pair mask: before the pass the owning lanes retire
-// columns i and i+1.  Groups of kG32 blocks with no live column are skipped
+// columns i and i+1.  Groups of 4-8 blocks with no live column are skipped
 // (warp-uniform test).  Rows a_r0..a_r1 stream through a 4-slot per-warp
 // ring, one pass (two rows) ahead.
 template <int NPL, int MODE>
@@ -552,6 +555,7 @@ __global__ void __launch_bounds__(kW32 * 32, 5)
     float rp1 = a0;             // lane 0's A term of the next block, row i
     float rp2 = at4(B1, s4lo);  // ... row i + 1
     a0 = at4(B2, s4lo);         // row i + 2 (next pass)
+    constexpr int kG32 = group_blocks<NPL>();
 #pragma unroll
     for (int m0 = 0; m0 < NPL; m0 += kG32) {
       if (jlo + 32 * (m0 + kG32) - 1 > i + 1) {  // warp-uniform: live
@@ -584,17 +588,25 @@ __global__ void __launch_bounds__(kW32 * 32, 5)
             w[g] = kInfF;
           }
         }
-        const float mu = fminf(fminf(u[0], u[1]), fminf(u[2], u[3]));
-        const float mw = fminf(fminf(w[0], w[1]), fminf(w[2], w[3]));
+        float mu = u[0], mw = w[0];
+#pragma unroll
+        for (int g = 1; g < kG32; ++g) {
+          mu = fminf(mu, u[g]);
+          mw = fminf(mw, w[g]);
+        }
         const bool hit = MODE == 1 ? (mu <= la || mw < lb)
                                    : (mu <= la || mw <= lb);
         if (__any_sync(0xffffffffu, hit)) {
-          lim = scan_hit<MODE>(u[0], u[1], u[2], u[3], w[0], w[1], w[2], w[3],
-                               di, di2, la, lb, i, jlo + lane + 32 * m0,
-                               a.thr, &s_cd[warp][0][lane],
-                               &s_cij[warp][0][lane], st);
-          la = lrow_of(di);
-          lb = two ? lrow_of(di2) : -kInfF;
+#pragma unroll
+          for (int h = 0; h < kG32; h += 4) {
+            lim = scan_hit<MODE>(u[h], u[h + 1], u[h + 2], u[h + 3], w[h],
+                                 w[h + 1], w[h + 2], w[h + 3], di, di2, la, lb,
+                                 i, jlo + lane + 32 * (m0 + h), a.thr,
+                                 &s_cd[warp][0][lane], &s_cij[warp][0][lane],
+                                 st);
+            la = lrow_of(di);
+            lb = two ? lrow_of(di2) : -kInfF;
+          }
         }
       }
     }
