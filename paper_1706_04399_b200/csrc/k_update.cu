@@ -131,26 +131,20 @@ __device__ void sigma_pass(const uint16_t* __restrict__ tgt_g, double c,
   }
   __syncthreads();
   const int t = s_misc[0];
-  // backward jumping to the first position > t: word = ptr | done << 16
+  // cur_t[q] = T[q] for q <= t; for q > t, T[r] with r the first position
+  // > t on q's backward orbit pi^-1(q), pi^-2(q), ... (q itself at the
+  // latest).  A direct walk: the positions <= t skipped on the way are each
+  // on exactly one walk, so the total work is O(n), and runs are short
+  // (the prefix fraction is c = phi * r < 1).
   for (int q = tid; q < n; q += T) {
-    uint32_t b = sB[q];
-    sW[q] = b | ((b > (uint32_t)t ? 1u : 0u) << 16);
-  }
-  __syncthreads();
-  for (int r = 0; r < 2 * R + 2; ++r) {
-    int pending = 0;
-    for (int q = tid; q < n; q += T) {
-      uint32_t w = sW[q];
-      if (!(w >> 16)) {
-        uint32_t w2 = sW[w & 0xFFFFu];
-        sW[q] = w2;
-        if (q > t && !(w2 >> 16)) pending = 1;
-      }
+    uint16_t cur;
+    if (q <= t) {
+      cur = sT[q];
+    } else {
+      int b = sB[q];
+      while (b <= t) b = sB[b];
+      cur = sT[b];
     }
-    if (!__syncthreads_or(pending)) break;
-  }
-  for (int q = tid; q < n; q += T) {
-    uint16_t cur = (q <= t) ? sT[q] : sT[sW[q] & 0xFFFFu];
     sout[sx[q]] = cur;
   }
   __syncthreads();
