@@ -281,6 +281,32 @@ int dpso_workspace_size(const dpso_params* prm, int32_t n, size_t* bytes) {
   return DPSO_OK;
 }
 
+// Pinned control blocks are recycled process-wide: cudaMallocHost /
+// cudaFreeHost pin and unpin pages and can take milliseconds each, which a
+// short fit() would pay on every call.
+static std::mutex g_pinned_mu;
+static std::vector<DevCtl*> g_pinned_free;
+
+static DevCtl* pinned_ctl_get() {
+  {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    if (!g_pinned_free.empty()) {
+      DevCtl* p = g_pinned_free.back();
+      g_pinned_free.pop_back();
+      return p;
+    }
+  }
+  DevCtl* p = nullptr;
+  if (cudaMallocHost(&p, sizeof(DevCtl)) != cudaSuccess) return nullptr;
+  return p;
+}
+
+static void pinned_ctl_put(DevCtl* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pinned_mu);
+  g_pinned_free.push_back(p);
+}
+
 int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
                 size_t workspace_bytes, void* cuda_stream, dpso_ctx** out) {
   int rc = check_params(prm, n);
@@ -305,7 +331,7 @@ int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
   cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking);
-  cudaMallocHost(&c->host_ctl, sizeof(DevCtl));
+  c->host_ctl = pinned_ctl_get();
   SwarmView& v = c->v;
   memset(&v, 0, sizeof v);
   v.n = n;
@@ -730,7 +756,7 @@ void dpso_destroy(dpso_ctx* c) {
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->stream2) cudaStreamDestroy(c->stream2);
   if (c->stream) cudaStreamDestroy(c->stream);
-  if (c->host_ctl) cudaFreeHost(c->host_ctl);
+  pinned_ctl_put(c->host_ctl);
   delete c;
 }
 

@@ -41,9 +41,90 @@ class SolveReport:
 _M64 = (1 << 64) - 1
 
 
+# numpy's SeedSequence constants (numpy/random/bit_generator.pyx)
+_INIT_A, _MULT_A = 0x43B0D7E5, 0x931E8875
+_INIT_B, _MULT_B = 0x8B51F9DD, 0x58F38DED
+_MIX_L, _MIX_R = 0xCA01F9DD, 0x4973F715
+_PCG_MULT = 0x2360ED051FC65DA44385DF649FCCF645
+_M32 = 0xFFFFFFFF
+_M128 = (1 << 128) - 1
+
+
+def _int_words(x: int) -> list:
+    """numpy's _int_to_uint32_array."""
+    if x == 0:
+        return [0]
+    out = []
+    while x > 0:
+        out.append(x & _M32)
+        x >>= 32
+    return out
+
+
+def _spawned_pcg64_states(entropy: int, count: int) -> np.ndarray:
+    """``SeedSequence(entropy).spawn(count)`` then ``PCG64(child).state``,
+    vectorised over the children: the hash constants of SeedSequence's
+    hashmix advance identically for every child, so the pool mixing and
+    generate_state run as uint32 array arithmetic."""
+    u32 = np.uint32
+    i = np.arange(count, dtype=np.uint64)
+    if count > 0 and int(i[-1]) > _M32:
+        raise ValueError("too many streams")
+    run = _int_words(entropy)
+    run += [0] * max(0, 4 - len(run))  # a spawn key pads run entropy to 4
+    ent = [np.full(count, w, dtype=u32) for w in run] + [i.astype(u32)]
+    hc = _INIT_A
+
+    def hashmix(v):
+        nonlocal hc
+        v = v ^ u32(hc)
+        hc = (hc * _MULT_A) & _M32
+        v = v * u32(hc)
+        return v ^ (v >> u32(16))
+
+    def mix(x, y):
+        r = u32(_MIX_L) * x - u32(_MIX_R) * y
+        return r ^ (r >> u32(16))
+
+    with np.errstate(over="ignore"):
+        pool = [hashmix(ent[k]) for k in range(4)]
+        for s in range(4):
+            for t in range(4):
+                if s != t:
+                    pool[t] = mix(pool[t], hashmix(pool[s]))
+        for s in range(4, len(ent)):
+            for t in range(4):
+                pool[t] = mix(pool[t], hashmix(ent[s]))
+        # generate_state(4, uint64): 8 uint32 words, little-endian pairs
+        hb = _INIT_B
+        w32 = []
+        for k in range(8):
+            v = pool[k % 4] ^ u32(hb)
+            hb = (hb * _MULT_B) & _M32
+            v = v * u32(hb)
+            w32.append(v ^ (v >> u32(16)))
+    w64 = [w32[2 * j].astype(np.uint64) | (w32[2 * j + 1].astype(np.uint64)
+                                           << np.uint64(32)) for j in range(4)]
+    s0, s1, i0, i1 = (w.tolist() for w in w64)
+    rows = []
+    for c in range(count):  # pcg64_set_seed -> pcg_setseq_128_srandom_r
+        seed = (s0[c] << 64) | s1[c]
+        inc = (((i0[c] << 64) | i1[c]) << 1 | 1) & _M128
+        st = (inc + seed) & _M128            # state 0, step, += seed ...
+        st = (st * _PCG_MULT + inc) & _M128  # ... step
+        rows.append((st >> 64, st & _M64, inc >> 64, inc & _M64, 0, 0))
+    return np.array(rows, dtype=np.uint64).reshape(count, 6)
+
+
 def numpy_stream_states(random_state, count: int) -> np.ndarray:
     """PCG64 states of ``SeedSequence(random_state).spawn(count)`` as the
-    (count, 6) uint64 records ``dpso_set_streams`` expects."""
+    (count, 6) uint64 records ``dpso_set_streams`` expects (solver.py:278-282:
+    the reference spawns its streams this way).  Integer seeds take the
+    vectorised restatement above (pinned against numpy by
+    tests/test_lib_abi.py); any other entropy goes through numpy itself."""
+    if isinstance(random_state, (int, np.integer)) and not isinstance(
+            random_state, bool) and int(random_state) >= 0:
+        return _spawned_pcg64_states(int(random_state), count)
     seqs = np.random.SeedSequence(random_state).spawn(count)
     out = np.empty((count, 6), dtype=np.uint64)
     for i, s in enumerate(seqs):

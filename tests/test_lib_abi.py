@@ -97,3 +97,21 @@ def test_philox_known_answers(lib):
                                     out.ctypes.data_as(ctypes.c_void_p))
         assert rc == 0
         assert tuple(int(v) for v in out) == want
+
+
+def test_stream_states_match_numpy_seedsequence():
+    """The vectorised SeedSequence.spawn -> PCG64 restatement used to seed
+    the device streams equals numpy's own, for one- and multi-word seeds."""
+    import numpy as np
+    from paper_1706_04399_b200.solver import _spawned_pcg64_states
+    m = (1 << 64) - 1
+    for seed in (0, 1, 7, 2923, 2**32 - 1, 2**32, 2**32 + 5, 2**70 + 3):
+        for count in (1, 5, 130):
+            want = np.empty((count, 6), dtype=np.uint64)
+            for i, s in enumerate(np.random.SeedSequence(seed).spawn(count)):
+                st = np.random.PCG64(s).state
+                a, b = st["state"]["state"], st["state"]["inc"]
+                want[i] = (a >> 64, a & m, b >> 64, b & m, st["has_uint32"],
+                           st["uinteger"])
+            got = _spawned_pcg64_states(seed, count)
+            assert np.array_equal(got, want), (seed, count)
