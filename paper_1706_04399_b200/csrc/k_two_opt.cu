@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kW32 * 32, 5)
     k_two_opt_scan32(ScanArgs a) {
   if (a.ctl && (a.ctl->done || a.ctl->improved)) return;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t bars[kW32][kBufs32];
+  __shared__ __align__(8) uint64_t bars[kW32][2];
   __shared__ uint32_t s_cij[kW32][kCand][32];
   __shared__ float s_cd[kW32][kCand][32];
   __shared__ float s_st[kW32][3][32];
@@ -468,18 +468,28 @@ __global__ void __launch_bounds__(kW32 * 32, 5)
     return (m & 1) ? (sjp[m / 2] >> 16) : (sjp[m / 2] & 0xFFFFu);
   };
   const int nrows = r1 - r0 + 1;  // cost rows a_r0 .. a_r1 (ring index q)
+  // The ring is two slot pairs with one mbarrier each: a pass's two B rows
+  // sit in one pair (B2 one slot after B1) and arrive on one barrier; the
+  // next pass's rows fill the other pair.  The prime row a_r0 uses pair 1
+  // before pass 1 refills it.
   uint64_t* wb = bars[warp];
-  auto issue = [&](int q, int city) {
-    const int s_ = q % kBufs32;
-    mbar_expect_tx(&wb[s_], a.row_bytes);
-    bulk_g2s(wbase + (size_t)s_ * a.buf_stride,
-             a.cost32 + (size_t)city * a.ld32, a.row_bytes, &wb[s_]);
+  auto issue2 = [&](int pair, int ca, int cb2, int nr) {  // nr rows: 1 or 2
+    mbar_expect_tx(&wb[pair], (uint32_t)nr * a.row_bytes);
+    unsigned char* dst = wbase + (size_t)(2 * pair) * a.buf_stride;
+    bulk_g2s(dst, a.cost32 + (size_t)ca * a.ld32, a.row_bytes, &wb[pair]);
+    if (nr > 1)
+      bulk_g2s(dst + a.buf_stride, a.cost32 + (size_t)cb2 * a.ld32,
+               a.row_bytes, &wb[pair]);
   };
   if (lane == 0) {
-    for (int s_ = 0; s_ < kBufs32; ++s_) mbar_init(&wb[s_], 1);
+    mbar_init(&wb[0], 1);
+    mbar_init(&wb[1], 1);
     fence_barrier_init();
-    for (int q = 0; q < 3 && q < nrows; ++q) issue(q, tour[r0 + q]);
+    issue2(1, tour[r0], 0, 1);                                 // prime row
+    issue2(0, tour[r0 + 1], nrows > 2 ? tour[r0 + 2] : 0,      // pass 0
+           nrows > 2 ? 2 : 1);
   }
+  uint32_t ph = 0;  // phase bit per pair (bit 0: pair 0, bit 1: pair 1)
   // Per-pass scalars from lane-parallel loads of 32 rows at a time, one
   // block ahead: cb = the cities of ring rows 3 + k (+1), db = d_{r0 + k}.
   auto city_at = [&](int q) -> int {
@@ -493,10 +503,10 @@ __global__ void __launch_bounds__(kW32 * 32, 5)
   __syncwarp();
   // rows as 32-bit shared-window addresses: gathers are plain LDS [R]
   const uint32_t wbase_s = smem_u32(wbase);
-  auto row = [&](int q) -> uint32_t {
-    const int s_ = q % kBufs32;
-    mbar_wait(&wb[s_], (uint32_t)((q / kBufs32) & 1));
-    return wbase_s + (uint32_t)s_ * a.buf_stride;
+  auto pair_rows = [&](int pair) -> uint32_t {  // waits; the pair's base
+    mbar_wait(&wb[pair], (ph >> pair) & 1u);
+    ph ^= 1u << pair;
+    return wbase_s + (uint32_t)(2 * pair) * a.buf_stride;
   };
   auto at4 = [](uint32_t R, uint32_t off4) -> float {
     float v;
@@ -509,7 +519,7 @@ __global__ void __launch_bounds__(kW32 * 32, 5)
   float Bv[NPL];
   float a0;
   {
-    const uint32_t R = row(0);
+    const uint32_t R = pair_rows(1);
 #pragma unroll
     for (int m = 0; m < NPL; ++m) Bv[m] = at4(R, sj(m));
     a0 = at4(R, s4lo);
@@ -524,14 +534,13 @@ __global__ void __launch_bounds__(kW32 * 32, 5)
       cb_next = city_at(3 + k + 32 + lane);
       db_next = d_at(k + 32 + lane);
     }
-    {  // rows k + 3, k + 4 into the slots of rows k - 1, k (read last pass;
-       // those shared loads have completed, their values consumed)
+    const int pass = k >> 1;
+    {  // rows k + 3, k + 4 into the other pair (read by the previous pass,
+       // or the prime row; those shared loads have completed)
       const int c3 = __shfl_sync(0xffffffffu, cb, k & 31);
       const int c4 = __shfl_sync(0xffffffffu, cb, (k + 1) & 31);
-      if (lane == 0) {
-        if (k + 3 < nrows) issue(k + 3, c3);
-        if (k + 4 < nrows) issue(k + 4, c4);
-      }
+      if (lane == 0 && k + 3 < nrows)
+        issue2((pass + 1) & 1, c3, c4, k + 4 < nrows ? 2 : 1);
     }
     const float di = __shfl_sync(0xffffffffu, db, k & 31);
     const float di2 = __shfl_sync(0xffffffffu, db, (k + 1) & 31);
@@ -541,8 +550,8 @@ __global__ void __launch_bounds__(kW32 * 32, 5)
       if (two && c1 >= 0 && c1 < 32 * NPL && lane == (c1 & 31))
         sdj[c1] = -kInfF;
     }
-    const uint32_t B1 = row(k + 1);
-    const uint32_t B2 = two ? row(k + 2) : B1;
+    const uint32_t B1 = pair_rows(pass & 1);
+    const uint32_t B2 = two ? B1 + a.buf_stride : B1;
     if (a.stream_only) {
       if (lane == 0 && at4(B2, 0) == -1.f) lim = 0.f;  // keep the loads
       continue;
