@@ -151,6 +151,22 @@ int check_params(const dpso_params* p, int n) {
     return fail(DPSO_EINVAL, "seed_fraction must be in [0, 1]");
   if (n < 2 || n > kMaxN)
     return fail(DPSO_EINVAL, "n must be in [2, 65535] for the device path");
+  {
+    // the update kernel keeps a particle's six u16 arrays and the repair's
+    // u32 words in shared memory: 16 bytes per node
+    int dev = 0, smax = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                               dev) == cudaSuccess &&
+        smax > 0 && (int64_t)16 * round_up(n, 8) > smax - 1024) {
+      char buf[160];
+      snprintf(buf, sizeof buf,
+               "n = %d exceeds the device update kernel's shared memory "
+               "(max n = %d on this device)",
+               n, (int)((smax - 1024) / 16 / 8 * 8));
+      return fail(DPSO_EINVAL, buf);
+    }
+  }
   if (p->rng_mode != DPSO_RNG_NUMPY && p->rng_mode != DPSO_RNG_PHILOX)
     return fail(DPSO_EINVAL, "unknown rng_mode");
   return DPSO_OK;

@@ -541,20 +541,31 @@ __global__ void __launch_bounds__(128) k_tour_cost(const double* cost,
                                                    int64_t stride, int count,
                                                    double* out,
                                                    double* dcache) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  // one warp per tour, no shared memory (any n): lanes gather 32 edge costs
+  // at a time, lane 0 sums them in the reference order (closing edge first,
+  // _tour_cost solver.py:48-54) from warp shuffles
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x * 4 + warp;
-  double* sd = (double*)smem + (size_t)warp * n;
   if (t >= count) return;
   const uint16_t* tour = tours + (size_t)t * stride;
-  for (int i = lane; i < n; i += 32) {
-    int a = tour[i], b = tour[i + 1 == n ? 0 : i + 1];
-    double d = cost[(size_t)a * ld + b];
-    sd[i] = d;
-    if (dcache) dcache[(size_t)t * stride + i] = d;
+  double total = 0.0;
+  if (lane == 0)
+    total = __dadd_rn(0.0, cost[(size_t)tour[n - 1] * ld + tour[0]]);
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int i = i0 + lane;
+    double dv = 0.0;
+    if (i < n) {
+      const int a = tour[i], b = tour[i + 1 == n ? 0 : i + 1];
+      dv = cost[(size_t)a * ld + b];
+      if (dcache) dcache[(size_t)t * stride + i] = dv;
+    }
+    const int m = min(32, n - 1 - i0);  // d_0 .. d_{n-2}
+    for (int j = 0; j < 32; ++j) {
+      const double x = __shfl_sync(0xffffffffu, dv, j);
+      if (lane == 0 && j < m) total = __dadd_rn(total, x);
+    }
   }
-  __syncwarp();
-  if (lane == 0) out[t] = seq_tour_sum(sd, n);
+  if (lane == 0) out[t] = total;
 }
 
 // Greedy nearest neighbour from `start` (baselines.py:110-116): n-1 steps,
@@ -723,10 +734,8 @@ cudaError_t launch_tour_cost_rows(const double* cost, int64_t ld, int32_t n,
                                   const uint16_t* tours, int64_t stride,
                                   int32_t count, double* out, double* dcache,
                                   cudaStream_t s) {
-  size_t smem = (size_t)4 * n * sizeof(double);
-  set_dyn_smem((const void*)k_tour_cost, smem);
-  k_tour_cost<<<(count + 3) / 4, 128, smem, s>>>(cost, ld, n, tours, stride,
-                                                 count, out, dcache);
+  k_tour_cost<<<(count + 3) / 4, 128, 0, s>>>(cost, ld, n, tours, stride,
+                                              count, out, dcache);
   return cudaGetLastError();
 }
 

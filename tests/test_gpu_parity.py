@@ -200,3 +200,29 @@ def test_full_size_properties(pkg):
         assert fit == conv[-1]
     finally:
         ctx.close()
+
+
+def test_tour_cost_batch_large_n(pkg):
+    # no shared-memory staging: any n (the earlier version staged 4 rows of
+    # 8n bytes per CTA and stopped near n = 7000)
+    rng = np.random.default_rng(21)
+    n = 9000
+    pts = rng.random((n, 2)) * 10.0
+    cost = np.abs(pts[:, None, 0] - pts[None, :, 0]) + np.abs(
+        pts[:, None, 1] - pts[None, :, 1])
+    tours = np.array([rng.permutation(n) for _ in range(3)], dtype=np.int32)
+    got = pkg.tour_cost_batch(cost, tours)
+    for t, g in zip(tours, got):
+        assert float(g) == O.tour_cost(list(t), cost)
+
+
+def test_n_beyond_update_kernel_shared_memory_is_rejected(pkg):
+    import ctypes
+    from paper_1706_04399_b200 import _lib
+    s = pkg.DiscreteSwarmSolver(n_particles=8)
+    nbytes = ctypes.c_size_t(0)
+    rc = _lib.load().dpso_workspace_size(ctypes.byref(s._params()), 20000,
+                                         ctypes.byref(nbytes))
+    assert rc != 0
+    msg = _lib.load().dpso_last_error().decode()
+    assert "shared memory" in msg and "max n" in msg
