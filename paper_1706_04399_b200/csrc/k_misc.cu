@@ -17,6 +17,8 @@
 //   k_nn            nearest-neighbour construction (baselines.py:110-116)
 #include <float.h>
 
+#include <type_traits>
+
 #include "dpso_internal.cuh"
 #include "philox.cuh"
 #include "tma.cuh"
@@ -340,14 +342,36 @@ __global__ void __launch_bounds__(32) k_init_scan(SwarmView v, int n_seed,
             S += (int)(w[k] - (uint32_t)S - 1u) >> 31;
           f += 32;
         }
-        if (S - (int)half - 1 >= 8 && f + 8 <= resident_end) {
-          uint32_t w[8];
+        // groups that may cross one band edge: each draw masked with this
+        // band's mask and the next band's (half); the chain selects by
+        // S > half.  With half >= G the group cannot cross a second edge
+        // (S stays > half - G >= half / 2) nor end the permutation.
+        auto group2 = [&](auto G) {
+          constexpr int kG = decltype(G)::value;
+          uint32_t v1[kG], v2[kG];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) w[k] = ring[ridx(f + k)] & mask;
+          for (int k = 0; k < kG; ++k) {
+            const uint32_t w = ring[ridx(f + k)];
+            v1[k] = w & mask;
+            v2[k] = w & half;
+          }
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
-            S += (int)(w[k] - (uint32_t)S - 1u) >> 31;
-          f += 8;
+          for (int k = 0; k < kG; ++k) {
+            const uint32_t vv = S > (int)half ? v1[k] : v2[k];
+            S += (int)(vv - (uint32_t)S - 1u) >> 31;
+          }
+          f += kG;
+          if (S <= (int)half) {
+            mask = half;
+            half >>= 1;
+          }
+        };
+        if (half >= 32 && f + 16 <= resident_end) {
+          group2(std::integral_constant<int, 16>());
+          continue;
+        }
+        if (half >= 16 && f + 8 <= resident_end) {
+          group2(std::integral_constant<int, 8>());
           continue;
         }
         const uint32_t u = ring[ridx(f)];
