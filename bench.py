@@ -422,6 +422,31 @@ def run_ours(args, cfg_name, cfg):
                        "generations": gens, "wall_s": dt,
                        "api": "DiscreteSwarmSolver.fit(host numpy matrix)"}
 
+        # time-to-reference-best tour length (BASELINE metric, second part):
+        # with numpy-exact streams this run IS the reference's run for this
+        # seed (bit for bit), so the reference's best over the schedule is
+        # conv[-1] and it is first reached at generation g*; a fit capped at
+        # g* generations times how long this path takes to reach it
+        if RNG == "numpy" and world == 1:
+            conv = list(s.convergence_)
+            g_star = next(i for i, c in enumerate(conv) if c == conv[-1])
+            g_run = max(1, g_star)
+            tp = dict(ep, max_generations=g_run, stall_generations=g_run)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            s2 = DiscreteSwarmSolver(**tp).fit(cost)
+            torch.cuda.synchronize()
+            t_best = time.perf_counter() - t1
+            assert s2.best_fitness_ == conv[-1]
+            line["time_to_reference_best"] = {
+                "value": t_best, "unit": "s", "higher_is_better": False,
+                "reference_best": conv[-1], "generation": g_star,
+                "schedule": gens,
+                "note": "fit() wall time (host matrix in, tour out) to the "
+                        "reference's best tour length over the schedule for "
+                        "this seed; numpy-exact streams make this the "
+                        "reference's own trajectory"}
+
     if not args.no_cpu_baseline and world == 1:
         rate, g, dt = cpu_sample(cost, cfg, seed_tour=seed_tour)
         line["cpu_baseline"] = {
@@ -429,6 +454,11 @@ def run_ours(args, cfg_name, cfg):
             "sample": (f"oracle port (oracle/dpso_oracle.py) of the reference"
                        f" solve, 32-particle swarm on the same matrix, 1 warm"
                        f"-up + {g} timed generations ({dt:.1f}s), 1 thread")}
+        if "time_to_reference_best" in line:
+            ttb = line["time_to_reference_best"]
+            # the reference (single-threaded, parallel=False) needs g*
+            # generations of P particles at the port's one-core rate
+            ttb["reference_cpu_estimate_s"] = ttb["generation"] * P / rate
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
