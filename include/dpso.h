@@ -85,6 +85,13 @@ int dpso_init(dpso_ctx* ctx, const int32_t* host_seed_body, int32_t n_seed);
  * DPSO_SCAN_MODE overrides it (testing). */
 int dpso_scan_mode(dpso_ctx* ctx);
 
+/* How the last dpso_init located each particle's draws in the shared numpy
+ * init stream: 1 = parallel walk (every start's walk length, then pointer
+ * doubling), 0 = serial scan (too large a span, a walk ran off the span, or
+ * DPSO_INIT_SERIAL set), -1 = no numpy-mode init yet.  Diagnostic only:
+ * both give the same cursors. */
+int dpso_init_path(dpso_ctx* ctx);
+
 /* Run generations until max_generations or the stall break.  Blocks the
  * calling thread; returns the number of generations run. */
 int dpso_run(dpso_ctx* ctx, int32_t* gens_run);

@@ -60,7 +60,7 @@ struct Layout {
       off_conv, off_tores, off_chunk_tab, off_rank, off_hash, off_flag, off_pbflag,
       off_sidx, off_order, off_surv, off_keep, off_ev_slot, off_ev_k,
       off_ev_cursor, off_ev_end, off_ev_idx, off_mstream, off_init_buf,
-      off_init_state, off_init_cursor, off_seed, off_cost32,
+      off_init_state, off_init_cursor, off_init_aux, off_init_anchor, off_seed, off_cost32,
       off_stats, total;
   int64_t vel_cap;
   int chunks;
@@ -121,6 +121,11 @@ Layout make_layout(const dpso_params* prm, int n) {
   L.off_init_cursor = take(8 * P);
   L.off_init_buf = take(prm->rng_mode == DPSO_RNG_NUMPY ? 4 * init_buf_words(n, P) : 0);
   L.off_init_state = take(64);
+  {
+    const bool par = prm->rng_mode == DPSO_RNG_NUMPY && init_parallel_ok(n, (int)P);
+    L.off_init_aux = take(par ? 3 * 4 * init_buf_words(n, P) : 0);
+    L.off_init_anchor = take(par ? 8 * (P + 2) : 0);
+  }
   L.off_seed = take(2 * np);
   L.off_cost32 = take(prm->use_edge_exchange ? 4 * (int64_t)n * np : 0);
   L.off_stats = take(sizeof(CostStats));
@@ -187,6 +192,7 @@ struct dpso_ctx {
   bool have_cost, have_streams, initialized;
   SwarmView v;
   DevCtl* host_ctl;  // pinned
+  int init_path = -1;
 };
 
 static int sync_in(dpso_ctx* c) {
@@ -403,6 +409,9 @@ int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
   v.init_buf = (uint32_t*)(w + L.off_init_buf);
   v.init_buf_cap = prm->rng_mode == DPSO_RNG_NUMPY ? init_buf_words(n, v.P) : 0;
   v.init_state = (void*)(w + L.off_init_state);
+  v.init_parallel = prm->rng_mode == DPSO_RNG_NUMPY && init_parallel_ok(n, v.P);
+  v.init_aux = (int32_t*)(w + L.off_init_aux);
+  v.init_anchor = (int64_t*)(w + L.off_init_anchor);
   std::vector<int32_t> tab(4 * L.chunks);
   two_opt_chunk_table(n, L.chunks, tab.data());
   if ((rc = sync_in(c))) {
@@ -460,6 +469,8 @@ int dpso_set_cost(dpso_ctx* c, const double* dev_cost, int64_t ld) {
 
 int dpso_scan_mode(dpso_ctx* c) { return c ? c->v.plan.mode : -1; }
 
+int dpso_init_path(dpso_ctx* c) { return c ? c->init_path : -1; }
+
 int dpso_set_streams(dpso_ctx* c, const uint64_t* host_states) {
   if (!c || !host_states) return fail(DPSO_EINVAL, "null argument");
   const int64_t P = c->prm.n_particles;
@@ -501,7 +512,7 @@ int dpso_init(dpso_ctx* c, const int32_t* seed_body, int32_t n_seed) {
   }
   int rc = sync_in(c);
   if (rc) return rc;
-  CK(launch_init(c->v, dseed, n_seed, c->stream));
+  CK(launch_init(c->v, dseed, n_seed, c->stream, &c->init_path));
   CK(launch_init_best(c->v, c->stream));
   // stream walk of the first mutation call
   if (c->v.use_mutation) CK(launch_mutation_walk(c->v, c->stream));

@@ -131,6 +131,12 @@ struct SwarmView {
   uint32_t* init_buf;  // generated init-stream window (u32)
   int64_t init_buf_cap;
   void* init_state;    // InitScanState
+  // parallel init walk (init_parallel): the buffer holds the whole expected
+  // span; init_aux = 3 x init_buf_cap i32 (walk lengths + two doubling
+  // levels), init_anchor = P + 2 i64
+  int32_t init_parallel;
+  int32_t* init_aux;
+  int64_t* init_anchor;
 };
 
 // ---- kernel launchers (each .cu owns its kernels) -------------------------
@@ -147,13 +153,14 @@ cudaError_t launch_fitness(const SwarmView& v, int use_list, cudaStream_t s);
 cudaError_t launch_mutation_swap(const SwarmView& v, cudaStream_t s);
 int64_t mstream_words(int n, int P);
 int64_t init_buf_words(int n, int P);
+bool init_parallel_ok(int n, int P);
 cudaError_t launch_mutation_pre(const SwarmView& v, cudaStream_t s);
 cudaError_t launch_mutation_post(const SwarmView& v, cudaStream_t s);
 cudaError_t launch_select(const SwarmView& v, bool finalize, cudaStream_t s);
 cudaError_t launch_two_opt(const SwarmView& v, cudaStream_t s, int parts = 3);
 cudaError_t launch_finalize(const SwarmView& v, cudaStream_t s);
 cudaError_t launch_init(const SwarmView& v, const uint16_t* dev_seed,
-                        int32_t n_seed, cudaStream_t s);
+                        int32_t n_seed, cudaStream_t s, int* path);
 cudaError_t launch_init_best(const SwarmView& v, cudaStream_t s);
 
 // generic batch kernels (kernel-level ABI and internal reuse)

@@ -16,6 +16,8 @@
 //   k_tour_cost     _tour_cost (solver.py:48-54) for a batch of tours
 //   k_nn            nearest-neighbour construction (baselines.py:110-116)
 #include <float.h>
+#include <math.h>
+#include <stdlib.h>
 
 #include <type_traits>
 
@@ -193,6 +195,7 @@ struct InitScanState {
   int32_t step;   // permutation: current max index i; seed: draw t (0..2)
   int32_t fresh;  // particle p not started yet
   int32_t done;
+  int32_t fail;   // parallel walk ran off its buffer: sequential fallback
 };
 
 constexpr int kInitGenPer = 64;
@@ -231,7 +234,8 @@ constexpr int kINSeg = 8;    // ring slots (128 KiB), a power of two
 
 __global__ void __launch_bounds__(32) k_init_scan(SwarmView v, int n_seed,
                                                   int64_t win0,
-                                                  InitScanState* stp) {
+                                                  InitScanState* stp,
+                                                  int stop_perm) {
   if (blockIdx.x != 0) return;
   extern __shared__ __align__(128) uint32_t ring[];
   __shared__ __align__(8) uint64_t bars[kINSeg];
@@ -305,6 +309,8 @@ __global__ void __launch_bounds__(32) k_init_scan(SwarmView v, int n_seed,
   bool exhausted = false;
   while (st.p < P && !exhausted) {
     if (st.fresh) {
+      // prefix mode: hand the permutation particles to the parallel walk
+      if (stop_perm && st.p >= n_seed && st.q >= h) break;
       if (lane == 0) v.init_cursor[st.p] = (uint64_t)st.q;
       st.fresh = 0;
       if (st.p < n_seed)
@@ -439,9 +445,235 @@ __global__ void k_init_scan_begin(SwarmView v, InitScanState* stp) {
   st.step = 0;
   st.fresh = 1;
   st.done = 0;
+  st.fail = 0;
   *stp = st;
 }
 
+// Sequential fallback after a failed parallel walk: restart the scan state
+// without re-reading streams[0] (the walk may already have advanced it).
+__global__ void k_init_scan_reset(SwarmView v, InitScanState* stp) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  InitScanState st;
+  st.q = 0;
+  st.p = 0;
+  st.step = 0;
+  st.fresh = 1;
+  st.done = 0;
+  st.fail = 0;
+  *stp = st;
+}
+
+
+// ---- parallel init walk ----------------------------------------------------
+// The permutation particles' draws are a chain: particle p+1 starts where
+// particle p's permutation(n) stopped consuming the stream.  Where a walk
+// stops depends only on where it starts, so k_init_ends computes, for EVERY
+// fresh index f of the generated span, the number of u32 words E[f] a
+// permutation started at f consumes (numpy's masked rejection,
+// random_interval: draw u accepted iff (u & mask(i)) <= i, i = n-1 .. 1).
+// That is O(span x 1.4n) independent work instead of an O(span) serial
+// chain.  The chain itself is then followed with pointer doubling:
+// E^K by log2(K) squarings, one thread hops the P/K anchors, and P/K threads
+// fill K particles each.  A walk that runs off the span marks -1 and the
+// host falls back to the serial scan (k_init_scan), which stays exact.
+constexpr int kEB = 256;   // starts per CTA (one per thread)
+constexpr int kECH = 512;  // steps per staged chunk
+constexpr int kEG = 8;     // draws per branch-free group
+
+__device__ __forceinline__ uint32_t mask_cover(uint32_t x) {
+  x |= x >> 1;
+  x |= x >> 2;
+  x |= x >> 4;
+  x |= x >> 8;
+  x |= x >> 16;
+  return x;
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kEB) k_init_ends(SwarmView v,
+                                                   const InitScanState* stp) {
+  __shared__ __align__(16) uint32_t sw[2][kEB + kECH];
+  const int64_t L = v.init_buf_cap;
+  const int64_t f0 = (int64_t)blockIdx.x * kEB;
+  const int l = threadIdx.x;
+  const int64_t f = f0 + l;
+  int32_t* E = v.init_aux;
+  if (stp->done) return;
+  const int64_t lo = stp->q - (int64_t)v.init_start->has_uint32;
+  if (f0 + kEB <= lo) {  // before the first permutation: never read
+    if (f < L) E[f] = -1;
+    return;
+  }
+  const uint32_t* buf = v.init_buf;
+  auto stage = [&](int c, int b) {
+    const int64_t w0 = f0 + (int64_t)c * kECH;
+    for (int u = l; u < (kEB + kECH) / 4; u += kEB) {
+      const int64_t w = w0 + 4 * u;
+      if (w + 4 <= L) cp_async16(&sw[b][4 * u], buf + w);
+    }
+    cp_async_commit();
+  };
+  int S = v.n - 1;
+  uint32_t mask = mask_cover((uint32_t)S), half = mask >> 1;
+  bool active = f >= lo && f < L && S > 0;
+  int32_t res = (S > 0) ? -1 : 0;
+  stage(0, 0);
+  for (int c = 0;; ++c) {
+    cp_async_wait_all();
+    if (!__syncthreads_or(active)) break;
+    stage(c + 1, (c + 1) & 1);
+    if (active) {
+      const int64_t t0 = (int64_t)c * kECH;
+      int lim = kECH;
+      if (f + t0 + lim > L) lim = (int)(L - f - t0);
+      const uint32_t* w = &sw[c & 1][l];
+      int t = 0;
+      while (t < lim) {
+        if (S - (int)half - 1 >= kEG && t + kEG <= lim) {
+          // no band edge and no end inside the group
+          uint32_t u[kEG];
+#pragma unroll
+          for (int k = 0; k < kEG; ++k) u[k] = w[t + k] & mask;
+#pragma unroll
+          for (int k = 0; k < kEG; ++k)
+            S += (int)(u[k] - (uint32_t)S - 1u) >> 31;
+          t += kEG;
+        } else if (half >= (uint32_t)kEG && t + kEG <= lim) {
+          // at most one band edge inside the group (half >= 2G - 1)
+          uint32_t v1[kEG], v2[kEG];
+#pragma unroll
+          for (int k = 0; k < kEG; ++k) {
+            const uint32_t x = w[t + k];
+            v1[k] = x & mask;
+            v2[k] = x & half;
+          }
+#pragma unroll
+          for (int k = 0; k < kEG; ++k) {
+            const uint32_t vv = S > (int)half ? v1[k] : v2[k];
+            S += (int)(vv - (uint32_t)S - 1u) >> 31;
+          }
+          t += kEG;
+          if (S <= (int)half) {
+            mask = half;
+            half >>= 1;
+          }
+        } else {
+          const uint32_t x = w[t];
+          ++t;
+          if ((x & mask) <= (uint32_t)S) {
+            --S;
+            if (S == 0) {
+              res = (int32_t)(t0 + t);
+              active = false;
+              break;
+            }
+            if (S <= (int)half) {
+              mask = half;
+              half >>= 1;
+            }
+          }
+        }
+      }
+      if (active && f + t0 + lim >= L) active = false;  // ran off: res = -1
+    }
+  }
+  if (f < L) E[f] = f >= lo ? res : -1;
+}
+
+// F2[f] = F[f] + F[f + F[f]]: K-step walk lengths from K/2-step ones
+__global__ void __launch_bounds__(256) k_init_square(const int32_t* F,
+                                                     int32_t* F2, int64_t L) {
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < L;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t a = F[f];
+    int32_t r = -1;
+    if (a >= 0 && f + a < L) {
+      const int32_t b = F[f + a];
+      if (b >= 0) r = a + b;
+    }
+    F2[f] = r;
+  }
+}
+
+// one thread: the start of every K-th permutation particle.
+// anchor[0] = first permutation particle, anchor[1] = anchors (or -1),
+// anchor[2 + j] = fresh index where particle anchor[0] + jK starts
+__global__ void k_init_chain(SwarmView v, const InitScanState* stp,
+                             const int32_t* FK, int K) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const InitScanState st = *stp;
+  int64_t* anc = v.init_anchor;
+  if (st.done) return;
+  const int64_t L = v.init_buf_cap;
+  int64_t f = st.q - (int64_t)v.init_start->has_uint32;
+  anc[0] = st.p;
+  int64_t j = 0;
+  for (int64_t p = st.p; p < v.P; p += K) {
+    anc[2 + j++] = f;
+    if (p + K >= v.P) break;
+    const int32_t a = (f >= 0 && f < L) ? FK[f] : -1;
+    if (a < 0) {
+      anc[1] = -1;
+      return;
+    }
+    f += a;
+  }
+  anc[1] = j;
+}
+
+// thread j: particles anchor[0] + jK .. + K-1 from anchor j; the thread
+// holding particle P-1 writes the final scan state and the stream position
+__global__ void __launch_bounds__(128) k_init_fill(SwarmView v,
+                                                   InitScanState* stp, int K) {
+  const int64_t* anc = v.init_anchor;
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (stp->done) return;
+  const int64_t na = anc[1];
+  if (na < 0) {
+    if (j == 0) stp->fail = 1;
+    return;
+  }
+  if (j >= na) return;
+  const int64_t L = v.init_buf_cap;
+  const int64_t h = (int64_t)v.init_start->has_uint32;
+  const int32_t* E = v.init_aux;
+  int64_t f = anc[2 + j];
+  const int64_t p0 = anc[0] + j * K;
+  for (int i = 0; i < K; ++i) {
+    const int64_t p = p0 + i;
+    if (p >= v.P) break;
+    v.init_cursor[p] = (uint64_t)(f + h);
+    const int32_t a = (f >= 0 && f < L) ? E[f] : -1;
+    if (a < 0) {
+      stp->fail = 1;
+      return;
+    }
+    f += a;
+    if (p == v.P - 1) {
+      const int64_t q = f + h;
+      stp->q = q;
+      stp->p = v.P;
+      stp->step = 0;
+      stp->fresh = 1;
+      stp->done = 1;
+      Pcg r;
+      r.seek_u32(*v.init_start, (uint64_t)q);
+      r.store(v.streams[0]);
+    }
+  }
+}
 
 __global__ void __launch_bounds__(128) k_init_build(SwarmView v,
                                                     const uint16_t* seed,
@@ -714,26 +946,78 @@ cudaError_t launch_finalize(const SwarmView& v, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// Host loop over init-stream windows (one sync per window; init runs once).
+// Init of the numpy streams: the parallel walk when the expected span fits
+// the buffer (init_parallel), else (or if a walk ran off the span) the
+// serial scan, window by window (one sync per window; init runs once).
+static cudaError_t init_serial(const SwarmView& v, int32_t n_seed,
+                               InitScanState* stp, cudaStream_t s) {
+  InitScanState h;
+  const size_t ring = (size_t)kINSeg * kISeg * 4;
+  cudaError_t e = set_dyn_smem((const void*)k_init_scan, ring);
+  if (e) return e;
+  for (int64_t win0 = 0;; win0 += v.init_buf_cap) {
+    const int64_t outs = v.init_buf_cap / 2;
+    const int64_t thr = (outs + kInitGenPer - 1) / kInitGenPer;
+    k_init_gen<<<(unsigned)((thr + 255) / 256), 256, 0, s>>>(v, win0);
+    k_init_scan<<<1, 32, ring, s>>>(v, n_seed, win0, stp, 0);
+    e = cudaMemcpyAsync(&h, stp, sizeof h, cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaStreamSynchronize(s);
+    if (e) return e;
+    if (h.done) return cudaSuccess;
+  }
+}
+
+static cudaError_t init_parallel(const SwarmView& v, int32_t n_seed,
+                                 InitScanState* stp, cudaStream_t s,
+                                 bool* ok) {
+  const int64_t L = v.init_buf_cap;
+  const int64_t outs = L / 2;
+  const int64_t thr = (outs + kInitGenPer - 1) / kInitGenPer;
+  k_init_gen<<<(unsigned)((thr + 255) / 256), 256, 0, s>>>(v, 0);
+  // seeded particles (and a permutation whose first draw is numpy's
+  // buffered half) stay on the serial scan: a few draws each
+  const size_t ring = (size_t)kINSeg * kISeg * 4;
+  cudaError_t e = set_dyn_smem((const void*)k_init_scan, ring);
+  if (e) return e;
+  k_init_scan<<<1, 32, ring, s>>>(v, n_seed, 0, stp, 1);
+  k_init_ends<<<(unsigned)((L + kEB - 1) / kEB), kEB, 0, s>>>(v, stp);
+  const int64_t perms = (int64_t)v.P - n_seed;
+  int K = 1;
+  while ((int64_t)K * K < perms) K <<= 1;
+  const int32_t* FK = v.init_aux;
+  int32_t* T[2] = {v.init_aux + L, v.init_aux + 2 * L};
+  int lev = 0;
+  for (int k = 1; k < K; k <<= 1, ++lev) {
+    k_init_square<<<148 * 8, 256, 0, s>>>(FK, T[lev & 1], L);
+    FK = T[lev & 1];
+  }
+  k_init_chain<<<1, 32, 0, s>>>(v, stp, FK, K);
+  const int64_t na = (perms + K - 1) / K + 2;
+  k_init_fill<<<(unsigned)((na + 127) / 128), 128, 0, s>>>(v, stp, K);
+  InitScanState h;
+  e = cudaMemcpyAsync(&h, stp, sizeof h, cudaMemcpyDeviceToHost, s);
+  if (!e) e = cudaStreamSynchronize(s);
+  if (e) return e;
+  *ok = h.done && !h.fail;
+  return cudaSuccess;
+}
+
 cudaError_t launch_init(const SwarmView& v, const uint16_t* dev_seed,
-                        int32_t n_seed, cudaStream_t s) {
+                        int32_t n_seed, cudaStream_t s, int* path) {
   if (v.rng_mode == DPSO_RNG_NUMPY) {
     InitScanState* stp = reinterpret_cast<InitScanState*>(v.init_state);
     k_init_scan_begin<<<1, 32, 0, s>>>(v, stp);
-    InitScanState h;
-    for (int64_t win0 = 0;; win0 += v.init_buf_cap) {
-      const int64_t outs = v.init_buf_cap / 2;
-      const int64_t thr = (outs + kInitGenPer - 1) / kInitGenPer;
-      k_init_gen<<<(unsigned)((thr + 255) / 256), 256, 0, s>>>(v, win0);
-      const size_t ring = (size_t)kINSeg * kISeg * 4;
-      set_dyn_smem((const void*)k_init_scan, ring);
-      k_init_scan<<<1, 32, ring, s>>>(v, n_seed, win0, stp);
-      cudaError_t e = cudaMemcpyAsync(&h, stp, sizeof h,
-                                      cudaMemcpyDeviceToHost, s);
-      if (!e) e = cudaStreamSynchronize(s);
+    bool ok = false;
+    cudaError_t e = cudaSuccess;
+    if (v.init_parallel && !getenv("DPSO_INIT_SERIAL"))
+      e = init_parallel(v, n_seed, stp, s, &ok);
+    if (e) return e;
+    if (!ok) {
+      k_init_scan_reset<<<1, 32, 0, s>>>(v, stp);
+      e = init_serial(v, n_seed, stp, s);
       if (e) return e;
-      if (h.done) break;
     }
+    if (path) *path = ok ? 1 : 0;
   }
   const size_t smem = round_up((int64_t)2 * v.np, 16) + (size_t)8 * v.np;
   set_dyn_smem((const void*)k_init_build, smem);
@@ -741,8 +1025,42 @@ cudaError_t launch_init(const SwarmView& v, const uint16_t* dev_seed,
   return cudaGetLastError();
 }
 
+// numpy's permutation(n): mean and variance of the u32 draws one
+// permutation consumes (masked rejection, accept probability (i+1)/(mask+1))
+static void perm_draw_moments(int n, double* mean, double* var) {
+  double m = 0.0, q = 0.0;
+  for (int i = 1; i < n; ++i) {
+    uint32_t mk = (uint32_t)i;
+    mk |= mk >> 1;
+    mk |= mk >> 2;
+    mk |= mk >> 4;
+    mk |= mk >> 8;
+    mk |= mk >> 16;
+    const double p = (i + 1.0) / ((double)mk + 1.0);
+    m += 1.0 / p;
+    q += (1.0 - p) / (p * p);
+  }
+  *mean = m;
+  *var = q;
+}
+
+static int64_t init_span_words(int n, int P) {
+  double mu, var;
+  perm_draw_moments(n, &mu, &var);
+  const double span = (double)P * (mu + 4.0) + 12.0 * sqrt((double)P * var) +
+                      4.0 * mu + 8192.0;
+  return round_up((int64_t)span, kISeg);
+}
+
+constexpr int64_t kInitParCap = 1ll << 28;  // u32 words (1 GiB + 3 GiB aux)
+
+bool init_parallel_ok(int n, int P) {
+  return init_span_words(n, P) <= kInitParCap;
+}
+
 int64_t init_buf_words(int n, int P) {
-  // expected need ~1.4 n per permutation; the scan resumes across windows
+  if (init_parallel_ok(n, P)) return init_span_words(n, P);
+  // serial scan: a window it resumes across
   int64_t want = (int64_t)P * (2 * (int64_t)n + 64) + 4096;
   const int64_t cap = 32ll << 20;  // 128 MiB window
   want = want < cap ? want : cap;

@@ -226,3 +226,48 @@ def test_n_beyond_update_kernel_shared_memory_is_rejected(pkg):
     assert rc != 0
     msg = _lib.load().dpso_last_error().decode()
     assert "shared memory" in msg and "max n" in msg
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,P,frac,rs", [
+    (2, 5, 0.0, 1), (3, 7, 0.5, 2), (15, 32, 0.1, 0), (64, 300, 0.0, 5),
+    (257, 129, 0.2, 9), (1000, 1024, 0.0, 0), (1500, 3000, 0.05, 11),
+    (2000, 96, 1.0, 4),
+])
+def test_parallel_init_walk_matches_serial(pkg, monkeypatch, n, P, frac, rs):
+    # The parallel init walk (every start's permutation length + pointer
+    # doubling) must find exactly the cursors of the serial scan, which the
+    # oracle pins (test_per_generation_state_matches_oracle, step 0).
+    from paper_1706_04399_b200.solver import numpy_stream_states
+    cost = random_euclidean_matrix(n, np.random.default_rng(n))
+    seed = list(range(n)) + [0]
+    states = {}
+    for path in ("parallel", "serial"):
+        if path == "serial":
+            monkeypatch.setenv("DPSO_INIT_SERIAL", "1")
+        s = pkg.DiscreteSwarmSolver(n_particles=P, max_generations=1,
+                                    random_state=rs, seed_tour=seed,
+                                    seed_fraction=frac)
+        seed_body, n_seed = s._seed(n)
+        ctx = s._make_context(cost)
+        try:
+            ctx.set_streams(numpy_stream_states(rs, P + 2))
+            ctx.init(seed_body, n_seed)
+            used = ctx.lib.dpso_init_path(ctx.h)
+            assert used == (1 if path == "parallel" else 0), (path, used)
+            states[path] = ctx.state()
+            ctx.step(1)  # one generation from each init
+            states[path + "1"] = ctx.state()
+        finally:
+            ctx.close()
+    for key in ("x", "fit", "pbest", "gbest"):
+        assert np.array_equal(states["parallel"][key], states["serial"][key])
+        assert np.array_equal(states["parallel1"][key],
+                              states["serial1"][key])
+    if P * n <= 300 * 64:
+        orc = O.OracleSolver(n_particles=P, max_generations=1,
+                             random_state=rs, seed_tour=seed,
+                             seed_fraction=frac)
+        trace = []
+        orc.fit(cost, trace=trace)
+        assert states["parallel"]["x"].tolist() == trace[0][1].x
