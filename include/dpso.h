@@ -85,6 +85,12 @@ int dpso_init(dpso_ctx* ctx, const int32_t* host_seed_body, int32_t n_seed);
  * DPSO_SCAN_MODE overrides it (testing). */
 int dpso_scan_mode(dpso_ctx* ctx);
 
+/* Bytes per matrix entry the fp32 scan streams: 2 = fp16 rows (EXACT32
+ * with integer |C| <= 2048; FILTER32 with the window widened to the fp16
+ * rounding bound), 4 = fp32 rows, 8 = fp64 (FP64 mode).  DPSO_SCAN16=0
+ * forces fp32 rows (testing). */
+int dpso_scan_rows_bytes(dpso_ctx* ctx);
+
 /* How the last dpso_init located each particle's draws in the shared numpy
  * init stream: 1 = parallel walk (every start's walk length, then pointer
  * doubling), 0 = serial scan (too large a span, a walk ran off the span, or

@@ -127,7 +127,7 @@ Layout make_layout(const dpso_params* prm, int n) {
     L.off_init_anchor = take(par ? 8 * (P + 2) : 0);
   }
   L.off_seed = take(2 * np);
-  L.off_cost32 = take(prm->use_edge_exchange ? 4 * (int64_t)n * np : 0);
+  L.off_cost32 = take(prm->use_edge_exchange ? 6 * (int64_t)n * np : 0);  // fp32 + fp16 rows
   L.off_stats = take(sizeof(CostStats));
   L.total = o;
   return L;
@@ -439,25 +439,21 @@ int dpso_set_cost(dpso_ctx* c, const double* dev_cost, int64_t ld) {
   c->v.cost = dev_cost;
   c->v.ld = ld;
   TwoOptPlan& pl = c->v.plan;
+  memset(&pl, 0, sizeof pl);
   pl.cost = dev_cost;
   pl.ld = ld;
-  pl.cost32 = nullptr;
   pl.ld32 = c->v.np;
   pl.mode = kScanFP64;
-  pl.thr = 0.f;
+  pl.es = 4;
+  pl.dscale = 1.f;
   if (c->prm.use_edge_exchange) {
     float* c32 = (float*)(c->ws + c->L.off_cost32);
+    uint16_t* c16 = (uint16_t*)(c32 + (size_t)c->n * c->v.np);
     CostStats* st = (CostStats*)(c->ws + c->L.off_stats);
     int rc = sync_in(c);
     if (rc) return rc;
-    CK(launch_cost_prep(dev_cost, ld, c->n, c32, c->v.np, st, c->stream));
-    CostStats h;
-    CK(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    pl.cost32 = c32;
-    pl.mode = two_opt_mode(h, c->n, &pl.thr);
-    if (getenv("DPSO_SCAN_MODE")) pl.mode = atoi(getenv("DPSO_SCAN_MODE"));
-    if (pl.mode == kScanFilter32 && pl.thr == 0.f) pl.mode = kScanFP64;
+    CK(two_opt_prepare(dev_cost, ld, c->n, c->v.np, c32, c16, st, c->stream,
+                       &pl));
   }
   c->have_cost = true;
   if (c->graph) {
@@ -470,6 +466,12 @@ int dpso_set_cost(dpso_ctx* c, const double* dev_cost, int64_t ld) {
 int dpso_scan_mode(dpso_ctx* c) { return c ? c->v.plan.mode : -1; }
 
 int dpso_init_path(dpso_ctx* c) { return c ? c->init_path : -1; }
+
+int dpso_scan_rows_bytes(dpso_ctx* c) {
+  if (!c) return -1;
+  if (c->v.plan.mode == kScanFP64) return 8;
+  return c->v.plan.es == 2 && c->v.plan.cost16 ? 2 : 4;
+}
 
 int dpso_set_streams(dpso_ctx* c, const uint64_t* host_states) {
   if (!c || !host_states) return fail(DPSO_EINVAL, "null argument");
@@ -847,7 +849,7 @@ int dpso_best_exchange_batch(const double* dev_cost, int64_t ld, int32_t n,
   size_t bytes = round_up(2 * np * cnt, 256) + round_up(8 * np * cnt, 256) +
                  round_up(sizeof(TwoOptRes) * chunks * cnt + 4 * (1 + chunks * cnt), 256) +
                  round_up(16 * chunks, 256) + round_up(8 * cnt, 256) +
-                 round_up(4 * (int64_t)n * np, 256) + 256;
+                 round_up(6 * (int64_t)n * np, 256) + 256;  // fp32 + fp16 rows
   unsigned char* tmp = nullptr;
   CK(cudaMallocAsync(&tmp, bytes, s));
   size_t o = 0;
@@ -862,7 +864,7 @@ int dpso_best_exchange_batch(const double* dev_cost, int64_t ld, int32_t n,
                                     4 * (1 + chunks * cnt));
   int32_t* ctab = (int32_t*)take(16 * chunks);
   double* fsum = (double*)take(8 * cnt);
-  float* c32 = (float*)take(4 * (int64_t)n * np);
+  float* c32 = (float*)take(6 * (int64_t)n * np);
   CostStats* st = (CostStats*)take(sizeof(CostStats));
   CK(cudaMemcpyAsync(ctab, tab.data(), 16 * chunks,
                      cudaMemcpyHostToDevice, s));
@@ -870,17 +872,8 @@ int dpso_best_exchange_batch(const double* dev_cost, int64_t ld, int32_t n,
   if (rc) return rc;
   CK(launch_tour_cost_rows(dev_cost, ld, n, t16, np, count, fsum, dc, s));
   TwoOptPlan pl;
-  pl.cost = dev_cost;
-  pl.ld = ld;
-  pl.cost32 = c32;
-  pl.ld32 = np;
-  CK(launch_cost_prep(dev_cost, ld, n, c32, np, st, s));
-  CostStats h;
-  CK(cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  pl.mode = two_opt_mode(h, n, &pl.thr);
-  if (getenv("DPSO_SCAN_MODE")) pl.mode = atoi(getenv("DPSO_SCAN_MODE"));
-  if (pl.mode == kScanFilter32 && pl.thr == 0.f) pl.mode = kScanFP64;
+  CK(two_opt_prepare(dev_cost, ld, n, np, c32,
+                     (uint16_t*)(c32 + (size_t)n * np), st, s, &pl));
   CK(launch_two_opt_batch(pl, n, (int32_t)np, t16, dc, count, res, chunks,
                           ctab, dev_delta, s));
   if (count > 0) k_u16_to_i32<<<count, 256, 0, s>>>(t16, n, count, dev_tours, np);

@@ -70,7 +70,14 @@ struct TwoOptPlan {
   const float* cost32;  // fp32 copy (EXACT32 / FILTER32), may be null
   int64_t ld32;
   int mode;
-  float thr;  // FILTER32 candidate window (2 eps)
+  float thr;  // FILTER32 candidate window (2 eps), in row units
+  // 16-bit rows (es == 2): fp16 copy of C * dscale streamed by the fp32 scan
+  // instead of cost32 (half the L2 -> shared-memory bytes).  EXACT32 with
+  // integer |C| <= 2048 (exact in fp16, dscale 1); FILTER32 with the window
+  // widened to the fp16 rounding bound (dscale = 2^k, max |C| dscale <= 2^15)
+  const uint16_t* cost16;
+  int es;        // 4 (cost32 rows) or 2 (cost16 rows)
+  float dscale;  // power of two applied to d values (rows are pre-scaled)
 };
 
 struct TwoOptRes {
@@ -177,6 +184,11 @@ cudaError_t launch_cost_prep(const double* cost, int64_t ld, int32_t n,
                              float* cost32, int64_t ld32, CostStats* st,
                              cudaStream_t s);
 int two_opt_mode(const CostStats& st, int n, float* thr);
+// cost_prep + mode choice + optional fp16 rows; c16 may be null (no 16-bit
+// rows).  Synchronizes the stream once (reads the matrix statistics).
+cudaError_t two_opt_prepare(const double* cost, int64_t ld, int32_t n,
+                            int64_t np, float* c32, uint16_t* c16,
+                            CostStats* st, cudaStream_t s, TwoOptPlan* pl);
 cudaError_t launch_nn(const double* cost, int64_t ld, int32_t n, int32_t start,
                       int32_t* out, cudaStream_t s);
 cudaError_t launch_pysum_tour(const double* cost, int64_t ld, int32_t n,

@@ -41,6 +41,9 @@
 #include <algorithm>
 #include <vector>
 
+#include <cuda_fp16.h>
+#include <math.h>
+
 #include "dpso_internal.cuh"
 #include "tma.cuh"
 
@@ -68,7 +71,10 @@ struct ScanArgs {
   uint32_t row_bytes;      // bytes streamed per cost row (multiple of 16)
   uint32_t buf_stride;     // bytes between ring buffers
   uint32_t buf_stride2;    // bytes of one warp's smem (ring + d_j)
-  float thr;               // FILTER32: 2 * eps
+  float thr;               // FILTER32: 2 * eps (row units)
+  const void* rows;        // staged rows of the fp32 scan: cost32 or cost16
+  int64_t row_pitch;       // bytes between staged rows
+  float dscale;            // d values -> row units (power of two)
   int32_t* ovf;            // FILTER32 overflow list: [0] count, [1..] tasks
   int stream_only;         // debug: stream the rows, skip the pair compute
 };
@@ -416,7 +422,7 @@ __device__ __noinline__ float scan_hit(float u0, float u1, float u2, float u3,
 // columns i and i+1.  Groups of 4-8 blocks with no live column are skipped
 // (warp-uniform test).  Rows a_r0..a_r1 stream through a 4-slot per-warp
 // ring, one pass (two rows) ahead.
-template <int NPL, int MODE>
+template <int NPL, int MODE, int ES>
 __global__ void __launch_bounds__(kW32 * 32, 5)
     k_two_opt_scan32(ScanArgs a) {
   if (a.ctl && (a.ctl->done || a.ctl->improved)) return;
@@ -456,13 +462,13 @@ __global__ void __launch_bounds__(kW32 * 32, 5)
   for (int m = 0; m < NPL; ++m) {
     const int j = jlo + lane + 32 * m;
     if (j < jhi) {
-      const uint32_t s4 = 4u * tour[j + 1 == n ? 0 : j + 1];
+      const uint32_t s4 = (uint32_t)ES * tour[j + 1 == n ? 0 : j + 1];
       sjp[m / 2] |= (m & 1) ? (s4 << 16) : s4;
     }
   }
   for (int jl = lane; jl < 32 * NPL; jl += 32) {
     const int j = jlo + jl;
-    sdj[jl] = (j >= r0 && j < jhi) ? (float)dg[j] : -kInfF;
+    sdj[jl] = (j >= r0 && j < jhi) ? (float)(dg[j] * a.dscale) : -kInfF;
   }
   auto sj = [&](int m) -> uint32_t {
     return (m & 1) ? (sjp[m / 2] >> 16) : (sjp[m / 2] & 0xFFFFu);
@@ -476,9 +482,10 @@ __global__ void __launch_bounds__(kW32 * 32, 5)
   auto issue2 = [&](int pair, int ca, int cb2, int nr) {  // nr rows: 1 or 2
     mbar_expect_tx(&wb[pair], (uint32_t)nr * a.row_bytes);
     unsigned char* dst = wbase + (size_t)(2 * pair) * a.buf_stride;
-    bulk_g2s(dst, a.cost32 + (size_t)ca * a.ld32, a.row_bytes, &wb[pair]);
+    const unsigned char* rows = (const unsigned char*)a.rows;
+    bulk_g2s(dst, rows + (size_t)ca * a.row_pitch, a.row_bytes, &wb[pair]);
     if (nr > 1)
-      bulk_g2s(dst + a.buf_stride, a.cost32 + (size_t)cb2 * a.ld32,
+      bulk_g2s(dst + a.buf_stride, rows + (size_t)cb2 * a.row_pitch,
                a.row_bytes, &wb[pair]);
   };
   if (lane == 0) {
@@ -496,7 +503,7 @@ __global__ void __launch_bounds__(kW32 * 32, 5)
     return q < nrows ? (int)tour[r0 + q] : 0;
   };
   auto d_at = [&](int k) -> float {
-    return r0 + k < r1 ? (float)dg[r0 + k] : 0.f;
+    return r0 + k < r1 ? (float)(dg[r0 + k] * a.dscale) : 0.f;
   };
   int cb = city_at(3 + lane), cb_next = city_at(3 + 32 + lane);
   float db = d_at(lane), db_next = d_at(32 + lane);
@@ -510,12 +517,20 @@ __global__ void __launch_bounds__(kW32 * 32, 5)
   };
   auto at4 = [](uint32_t R, uint32_t off4) -> float {
     float v;
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(R + off4));
+    if (ES == 4) {
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(R + off4));
+    } else {  // fp16 row entry, widened exactly
+      asm volatile(
+          "{\n\t.reg .b16 h;\n\tld.shared.b16 h, [%1];\n\t"
+          "cvt.f32.f16 %0, h;\n\t}"
+          : "=f"(v)
+          : "r"(R + off4));
+    }
     return v;
   };
   // prime: Bv = row a_r0 gathered at s_j (the "B term of row r0 - 1"); for
   // jlo > 0 lane 0's A term of block 0 is C[a_i][a_jlo], gathered per row
-  const uint32_t s4lo = jlo > 0 ? 4u * tour[jlo] : 0u;
+  const uint32_t s4lo = jlo > 0 ? (uint32_t)ES * tour[jlo] : 0u;
   float Bv[NPL];
   float a0;
   {
@@ -796,6 +811,19 @@ __global__ void k_cost_prep(const double* cost, int64_t ld, int n,
   }
 }
 
+// fp16 rows: round(C * scale) (scale a power of two, so only the final
+// rounding to fp16 is inexact; integers <= 2048 are exact)
+__global__ void k_cost_to16(const double* cost, int64_t ld, int n,
+                            uint16_t* c16, int64_t ld16, double scale) {
+  const int64_t total = (int64_t)n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / n, c = e % n;
+    const __half h = __double2half(cost[r * ld + c] * scale);
+    c16[r * ld16 + c] = __half_as_ushort(h);
+  }
+}
+
 template <int NPL, bool STAGE>
 cudaError_t launch_scan64_t(const ScanArgs& a, int warps, int blocks,
                             size_t smem, cudaStream_t s) {
@@ -806,10 +834,10 @@ cudaError_t launch_scan64_t(const ScanArgs& a, int warps, int blocks,
   return cudaGetLastError();
 }
 
-template <int NPL, int MODE>
+template <int NPL, int MODE, int ES>
 cudaError_t launch_scan32_t(const ScanArgs& a, int warps, int blocks,
                             size_t smem, cudaStream_t s) {
-  auto k = k_two_opt_scan32<NPL, MODE>;
+  auto k = k_two_opt_scan32<NPL, MODE, ES>;
   cudaError_t e = set_dyn_smem((const void*)k, smem);
   if (e != cudaSuccess) return e;
   k<<<blocks, warps * 32, smem, s>>>(a);
@@ -848,6 +876,57 @@ int two_opt_mode(const CostStats& st, int n, float* thr) {
   // candidates within 2 eps of the fp32 minimum are re-evaluated in fp64.
   *thr = (float)(mx * (2.0 / 262144.0));
   return kScanFilter32;
+}
+
+cudaError_t two_opt_prepare(const double* cost, int64_t ld, int32_t n,
+                            int64_t np, float* c32, uint16_t* c16,
+                            CostStats* st, cudaStream_t s, TwoOptPlan* pl) {
+  memset(pl, 0, sizeof *pl);
+  pl->cost = cost;
+  pl->ld = ld;
+  pl->cost32 = c32;
+  pl->ld32 = np;
+  pl->es = 4;
+  pl->dscale = 1.f;
+  cudaError_t e = launch_cost_prep(cost, ld, n, c32, np, st, s);
+  if (e) return e;
+  CostStats h;
+  e = cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, s);
+  if (!e) e = cudaStreamSynchronize(s);
+  if (e) return e;
+  pl->mode = two_opt_mode(h, n, &pl->thr);
+  if (getenv("DPSO_SCAN_MODE")) pl->mode = atoi(getenv("DPSO_SCAN_MODE"));
+  if (pl->mode == kScanFilter32 && pl->thr == 0.f) pl->mode = kScanFP64;
+  const char* e16 = getenv("DPSO_SCAN16");
+  if (!c16 || (e16 && atoi(e16) == 0) || pl->mode == kScanFP64) return e;
+  double mx;
+  memcpy(&mx, &h.maxabs_bits, sizeof mx);
+  double scale = 1.0;
+  if (pl->mode == kScanExact32) {
+    if (!(mx <= 2048.0)) return e;  // fp16 integers are exact up to 2^11
+  } else {
+    if (!(mx > 1e-30 && mx < 1e30)) return e;
+    // max |C| scale in (2^14, 2^15]: every scaled entry is an fp16 normal
+    // or a subnormal with absolute error <= 2^-25
+    scale = ldexp(1.0, 15 - ilogb(mx) - 1);
+    while (mx * scale > 32768.0) scale *= 0.5;
+    while (mx * scale * 2.0 <= 32768.0) scale *= 2.0;
+    // |t - delta| <= e_max = 2^-11 (|A| + |B|) + fp32 terms
+    //               <= 1.002 * 2^-10 max|C| (row units); window = 4 e_max
+    // (a true tie of the argmin is within 2 e_max of its computed value,
+    // which is within 2 e_max of the computed minimum), with margin
+    pl->thr = (float)(mx * scale * 0.00403);
+  }
+  pl->dscale = (float)scale;
+  const int64_t total = (int64_t)n * n;
+  int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  if (blocks < 1) blocks = 1;
+  k_cost_to16<<<blocks, 256, 0, s>>>(cost, ld, n, c16, np, scale);
+  e = cudaGetLastError();
+  if (e) return e;
+  pl->cost16 = c16;
+  pl->es = 2;
+  return cudaSuccess;
 }
 
 cudaError_t launch_cost_prep(const double* cost, int64_t ld, int32_t n,
@@ -1001,7 +1080,11 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
     if (pl.mode == kScanFP64 || !pl.cost32) {
       e = fp64_scan();
     } else {
-      a.row_bytes = (uint32_t)(round_up(n, 4) * 4);
+      const int es = (pl.es == 2 && pl.cost16) ? 2 : 4;
+      a.rows = es == 2 ? (const void*)pl.cost16 : (const void*)pl.cost32;
+      a.row_pitch = (int64_t)es * pl.ld32;
+      a.dscale = es == 2 ? pl.dscale : 1.f;
+      a.row_bytes = (uint32_t)(round_up(n, 16 / es) * es);
       a.buf_stride = (uint32_t)round_up(a.row_bytes, 128);
       // per warp: 2-slot row ring + d_j (fp32, 32 * NPL entries)
       const int npl32 = std::min(std::max(npl, 1), kNplMax32);
@@ -1012,10 +1095,13 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
       if (pl.mode == kScanFilter32) e = cudaMemsetAsync(a.ovf, 0, 4, s);
       if (e != cudaSuccess) return e;
       const int blocks = (int)((tasks + warps - 1) / warps);
-#define SCAN32(NPL)                                                        \
-  (pl.mode == kScanExact32                                                 \
-       ? launch_scan32_t<NPL, 1>(a, warps, blocks, smem, s)                \
-       : launch_scan32_t<NPL, 2>(a, warps, blocks, smem, s))
+#define SCAN32(NPL)                                                      \
+  (es == 2 ? (pl.mode == kScanExact32                                    \
+                  ? launch_scan32_t<NPL, 1, 2>(a, warps, blocks, smem, s) \
+                  : launch_scan32_t<NPL, 2, 2>(a, warps, blocks, smem, s)) \
+           : (pl.mode == kScanExact32                                    \
+                  ? launch_scan32_t<NPL, 1, 4>(a, warps, blocks, smem, s) \
+                  : launch_scan32_t<NPL, 2, 4>(a, warps, blocks, smem, s)))
       switch (npl32) {
         case 1: e = SCAN32(1); break;
         case 2: e = SCAN32(2); break;

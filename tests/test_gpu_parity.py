@@ -47,10 +47,22 @@ def test_best_exchange_golden(pkg, golden_kernels):
 SCAN_MODES = {"fp64": "0", "exact32": "1", "filter32": "2"}
 
 
-@pytest.fixture(params=[None, "fp64", "filter32"])
+def set_scan_mode(monkeypatch, mode):
+    # "<mode>" streams fp16 rows where the mode allows them (the default);
+    # "<mode>/rows32" forces the fp32 rows (DPSO_SCAN16=0)
+    if not mode:
+        return
+    base, _, rows = mode.partition("/")
+    if base:
+        monkeypatch.setenv("DPSO_SCAN_MODE", SCAN_MODES[base])
+    if rows == "rows32":
+        monkeypatch.setenv("DPSO_SCAN16", "0")
+
+
+@pytest.fixture(params=[None, "/rows32", "fp64", "filter32",
+                        "filter32/rows32"])
 def scan_mode(request, monkeypatch):
-    if request.param:
-        monkeypatch.setenv("DPSO_SCAN_MODE", SCAN_MODES[request.param])
+    set_scan_mode(monkeypatch, request.param)
     return request.param
 
 
@@ -71,14 +83,17 @@ def test_best_exchange_vs_oracle_sizes(pkg, scan_mode):
         check_batch(pkg, cost, tours, (n, scan_mode))
 
 
-@pytest.mark.parametrize("mode", [None, "fp64", "exact32", "filter32"])
-def test_best_exchange_integer_ties(pkg, mode, monkeypatch):
+@pytest.mark.parametrize("mode", [None, "/rows32", "fp64", "exact32",
+                                  "exact32/rows32", "filter32",
+                                  "filter32/rows32"])
+@pytest.mark.parametrize("scale", [1.0, 300.0])
+def test_best_exchange_integer_ties(pkg, mode, scale, monkeypatch):
     # integer costs: many exact ties -> row-major first-index tie break
-    if mode:
-        monkeypatch.setenv("DPSO_SCAN_MODE", SCAN_MODES[mode])
+    # (max |C| ~ 14 -> exact fp16 rows; ~ 4200 -> fp32 rows for EXACT32)
+    set_scan_mode(monkeypatch, mode)
     rng = np.random.default_rng(8)
     for n in (17, 65, 300, 513, 1100):
-        cost = np.floor(random_euclidean_matrix(n, rng))
+        cost = np.floor(random_euclidean_matrix(n, rng) * scale)
         tours = np.array([rng.permutation(n) for _ in range(5)],
                          dtype=np.int32)
         check_batch(pkg, cost, tours, (n, mode))
@@ -115,6 +130,43 @@ def test_best_exchange_near_ties_and_converged(pkg, scan_mode):
     cost = random_euclidean_matrix(60, rng) * 1e9
     tours = np.array([rng.permutation(60) for _ in range(4)], dtype=np.int32)
     check_batch(pkg, cost, tours, ("big", scan_mode))
+
+
+def test_best_exchange_fp16_rows_wide_range(pkg, scan_mode):
+    # the fp16 filter's window scales with max |C|: a matrix with a few
+    # huge entries (virtual edges, graph.py:63-78) and a tiny-valued one
+    rng = np.random.default_rng(21)
+    cost = random_euclidean_matrix(300, rng)
+    blocked = rng.random(cost.shape) < 0.01
+    blocked = blocked | blocked.T
+    np.fill_diagonal(blocked, False)
+    cost[blocked] = 1e3 * 300 * cost.max()
+    tours = np.array([rng.permutation(300) for _ in range(4)], dtype=np.int32)
+    check_batch(pkg, cost, tours, ("virtual", scan_mode))
+    cost = random_euclidean_matrix(200, rng) * 1e-12
+    tours = np.array([rng.permutation(200) for _ in range(4)], dtype=np.int32)
+    check_batch(pkg, cost, tours, ("tiny", scan_mode))
+    # asymmetric
+    cost = random_euclidean_matrix(257, rng) * (1 + rng.random((257, 257)))
+    np.fill_diagonal(cost, 0.0)
+    tours = np.array([rng.permutation(257) for _ in range(4)], dtype=np.int32)
+    check_batch(pkg, cost, tours, ("asym", scan_mode))
+
+
+def test_scan_rows16_selected(pkg, monkeypatch):
+    # the default plan streams fp16 rows for these matrices
+    import ctypes
+    from paper_1706_04399_b200.solver import device_cost
+    rng = np.random.default_rng(5)
+    for cost, want in ((random_euclidean_matrix(100, rng), 2),
+                       (np.floor(random_euclidean_matrix(100, rng)), 1)):
+        s = pkg.DiscreteSwarmSolver(n_particles=8)
+        ctx = s._make_context(cost)
+        try:
+            assert ctx.lib.dpso_scan_mode(ctx.h) == want
+            assert ctx.lib.dpso_scan_rows_bytes(ctx.h) == 2
+        finally:
+            ctx.close()
 
 
 def test_nn_two_opt_golden(pkg, golden_kernels):
