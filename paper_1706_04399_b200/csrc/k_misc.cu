@@ -681,7 +681,6 @@ __global__ void __launch_bounds__(128) k_init_build(SwarmView v,
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = v.n, np = v.np, tid = threadIdx.x;
   uint16_t* body = (uint16_t*)smem;
-  double* sd = (double*)(smem + round_up((int64_t)2 * np, 16));
   for (int p = blockIdx.x; p < v.P; p += gridDim.x) {
     if (p < n_seed) {
       for (int i = tid; i < n; i += blockDim.x) body[i] = seed[i];
@@ -689,13 +688,14 @@ __global__ void __launch_bounds__(128) k_init_build(SwarmView v,
       for (int i = tid; i < n; i += blockDim.x) body[i] = (uint16_t)i;
     }
     __syncthreads();
-    if (tid == 0 && v.rng_mode == DPSO_RNG_PHILOX) {
+    if (v.rng_mode == DPSO_RNG_PHILOX) {
       // production mode: independent Philox draws per particle; one random
-      // swap of the seed (two distinct positions) or a Fisher-Yates shuffle
+      // swap of the seed (two distinct positions), or a random permutation
+      // as a keyed Feistel bijection filled by the whole CTA
       PhiloxStream r;
       r.init(v.philox_seed, (uint32_t)p, 0u, kTagInit);
       if (p < n_seed) {
-        if (p > 0 && n > 1) {
+        if (tid == 0 && p > 0 && n > 1) {
           const uint32_t a = r.bounded((uint32_t)(n - 1));
           uint32_t b = r.bounded((uint32_t)(n - 2));
           if (b >= a) ++b;
@@ -704,12 +704,10 @@ __global__ void __launch_bounds__(128) k_init_build(SwarmView v,
           body[b] = x;
         }
       } else {
-        for (int j = n - 1; j >= 1; --j) {
-          const uint32_t jj = r.bounded((uint32_t)j);
-          const uint16_t x = body[j];
-          body[j] = body[jj];
-          body[jj] = x;
-        }
+        FeistelPerm perm;
+        perm.init(r, (uint32_t)n);
+        for (int i = tid; i < n; i += blockDim.x)
+          body[i] = (uint16_t)perm((uint32_t)i);
       }
     } else if (tid == 0) {
       Pcg r;
@@ -743,21 +741,13 @@ __global__ void __launch_bounds__(128) k_init_build(SwarmView v,
     double* dg = v.dcache + (size_t)p * np;
     for (int i = tid; i < n; i += blockDim.x) {
       int a = body[i], b = body[i + 1 == n ? 0 : i + 1];
-      double d = v.cost[(size_t)a * v.ld + b];
-      sd[i] = d;
-      dg[i] = d;
+      dg[i] = v.cost[(size_t)a * v.ld + b];
       xg[i] = (uint16_t)a;
       pb[i] = (uint16_t)a;
       if (v.vmap) v.vmap[(size_t)p * np + i] = (uint16_t)i;
     }
-    __syncthreads();
-    if (tid == 0) {
-      double f = seq_tour_sum(sd, n);
-      v.fit[p] = f;
-      v.pfit[p] = f;
-      if (v.vel_len) v.vel_len[p] = 0;
-    }
-    __syncthreads();
+    if (tid == 0 && v.vel_len) v.vel_len[p] = 0;
+    __syncthreads();  // the fitness (fit = pfit) follows in k_fitness
   }
 }
 
@@ -1019,10 +1009,11 @@ cudaError_t launch_init(const SwarmView& v, const uint16_t* dev_seed,
     }
     if (path) *path = ok ? 1 : 0;
   }
-  const size_t smem = round_up((int64_t)2 * v.np, 16) + (size_t)8 * v.np;
+  const size_t smem = round_up((int64_t)2 * v.np, 16);
   set_dyn_smem((const void*)k_init_build, smem);
   k_init_build<<<v.P, 128, smem, s>>>(v, dev_seed, n_seed);
-  return cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  return e ? e : launch_fitness(v, 2, s);
 }
 
 // numpy's permutation(n): mean and variance of the u32 draws one

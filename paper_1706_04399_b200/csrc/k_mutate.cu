@@ -906,47 +906,26 @@ __global__ void __launch_bounds__(32) k_mut_fix(SwarmView v) {
 
 // Production RNG mode: every event's draws are Philox keyed by (slot,
 // generation), so events are sampled independently with no stream walk:
-// k = integers(1, k_hi + 1) semantics, then numpy's choice(n, 2k, False)
-// algorithm (Floyd + shuffle) on Philox draws.  One warp per event.
+// k = integers(1, k_hi + 1) semantics, then 2k distinct positions in random
+// order (choice(n, 2k, replace=False)) as the first 2k images of a keyed
+// Feistel permutation of [0, n), all lanes in parallel.  One warp per event.
 __global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample_philox(
-    SwarmView v, int words_per_warp) {
+    SwarmView v) {
   if (!v.ctl->mutating || v.ctl->done) return;
-  extern __shared__ __align__(16) uint32_t sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int e = blockIdx.x * (blockDim.x >> 5) + warp;
   if (e >= v.ctl->n_events) return;
   const int n = v.n, P = v.P;
-  uint32_t* bits = sm + (size_t)warp * words_per_warp;
-  uint16_t* sidx = (uint16_t*)(bits + (n + 31) / 32);
-  for (int i = lane; i < (n + 31) / 32; i += 32) bits[i] = 0;
-  __syncwarp();
   const int slot = v.ev_slot[e];
-  int k = 0;
-  if (lane == 0) {
-    PhiloxStream r;
-    r.init(v.philox_seed, (uint32_t)slot, (uint32_t)v.ctl->gen, kTagMutate);
-    const int k_hi = max(2, n / 4);
-    k = min((int)r.bounded((uint32_t)(k_hi - 1)) + 1, n / 2);
-    v.ev_k[(size_t)v.ctl->mut_cur * P + e] = k;
-    const int size = 2 * k;
-    for (int t = 0; t < size; ++t) {  // Floyd
-      const uint32_t j = (uint32_t)(n - size + t);
-      uint32_t val = r.bounded(j);
-      if (bits[val >> 5] & (1u << (val & 31))) val = j;
-      bits[val >> 5] |= 1u << (val & 31);
-      sidx[t] = (uint16_t)val;
-    }
-    for (int i = size - 1; i >= 1; --i) {  // shuffle
-      const uint32_t j = r.bounded((uint32_t)i);
-      const uint16_t t = sidx[i];
-      sidx[i] = sidx[j];
-      sidx[j] = t;
-    }
-  }
-  k = __shfl_sync(0xffffffffu, k, 0);
-  __syncwarp();
+  PhiloxStream r;
+  r.init(v.philox_seed, (uint32_t)slot, (uint32_t)v.ctl->gen, kTagMutate);
+  const int k_hi = max(2, n / 4);
+  const int k = min((int)r.bounded((uint32_t)(k_hi - 1)) + 1, n / 2);
+  if (lane == 0) v.ev_k[(size_t)v.ctl->mut_cur * P + e] = k;
+  FeistelPerm perm;
+  perm.init(r, (uint32_t)n);
   uint16_t* idx = v.ev_idx + (size_t)e * v.np;
-  for (int t = lane; t < 2 * k; t += 32) idx[t] = sidx[t];
+  for (int t = lane; t < 2 * k; t += 32) idx[t] = (uint16_t)perm((uint32_t)t);
 }
 
 __global__ void __launch_bounds__(128) k_mut_swap(SwarmView v) {
@@ -1013,11 +992,8 @@ cudaError_t launch_mutation_post(const SwarmView& v, cudaStream_t s) {
   const int P = v.P;
   const int n = v.n;
   if (v.rng_mode == DPSO_RNG_PHILOX) {
-    const int words = (int)round_up((n + 31) / 32 + (n + 1) / 2, 4);
-    const size_t smem = (size_t)kSampleWarps * words * 4;
-    set_dyn_smem((const void*)k_mut_sample_philox, smem);
     k_mut_sample_philox<<<(P + kSampleWarps - 1) / kSampleWarps,
-                          kSampleWarps * 32, smem, s>>>(v, words);
+                          kSampleWarps * 32, 0, s>>>(v);
     return cudaGetLastError();
   }
   // per warp: draw values (<= 2n u32) + Floyd bitmap / tail arange; without

@@ -422,8 +422,11 @@ __device__ __noinline__ float scan_hit(float u0, float u1, float u2, float u3,
 // columns i and i+1.  Groups of 4-8 blocks with no live column are skipped
 // (warp-uniform test).  Rows a_r0..a_r1 stream through a 4-slot per-warp
 // ring, one pass (two rows) ahead.
+#ifndef DPSO_SCAN_MINB
+#define DPSO_SCAN_MINB 5
+#endif
 template <int NPL, int MODE, int ES>
-__global__ void __launch_bounds__(kW32 * 32, 5)
+__global__ void __launch_bounds__(kW32 * 32, DPSO_SCAN_MINB)
     k_two_opt_scan32(ScanArgs a) {
   if (a.ctl && (a.ctl->done || a.ctl->improved)) return;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -962,7 +965,7 @@ int two_opt_pick_chunks(int32_t n, int32_t P) {
   const int64_t slots = (int64_t)sms * warps_per_sm;
   const int R = column_ranges(n);
   // tasks per resident warp slot: balances the tail against per-task setup
-  int per_slot = 4;
+  int per_slot = 3;
   if (const char* e = getenv("DPSO_TASKS_PER_SLOT")) per_slot = std::max(1, atoi(e));
   int chunks = (int)((per_slot * slots + P - 1) / P);
   chunks = std::max(chunks, R);

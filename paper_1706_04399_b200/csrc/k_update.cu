@@ -19,6 +19,8 @@
 // For w < 1 the reference keeps an explicit transposition list and replays
 // it (solver.py:213-216); that path runs the repair sequentially in one
 // thread per particle (k_update_seq) on a bounded per-particle ring.
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "dpso_internal.cuh"
@@ -75,6 +77,18 @@ __device__ __forceinline__ int block_excl_scan(int val, int* s_warp,
   return base + x - val;
 }
 
+// n u16 (16-B aligned rows) in 16-byte pieces plus a scalar tail; the
+// padding past n is left alone
+template <int T>
+__device__ __forceinline__ void copy_row16(uint16_t* dst, const uint16_t* src,
+                                           int n) {
+  const int nv = n >> 3;
+  for (int k = threadIdx.x; k < nv; k += T)
+    reinterpret_cast<uint4*>(dst)[k] = reinterpret_cast<const uint4*>(src)[k];
+  const int i = 8 * nv + (int)threadIdx.x;
+  if (i < n) dst[i] = src[i];
+}
+
 // sigma (value permutation of the first prefix_len(c, L) repair
 // transpositions of x -> target) into sout[value].
 template <int T>
@@ -84,7 +98,7 @@ __device__ void sigma_pass(const uint16_t* __restrict__ tgt_g, double c,
                            uint32_t* sW, uint16_t* sout, int* s_warp,
                            int* s_misc) {
   const int tid = threadIdx.x;
-  for (int i = tid; i < n; i += T) sT[i] = tgt_g[i];
+  copy_row16<T>(sT, tgt_g, n);
   __syncthreads();
   // pi, its inverse (backward orbit), and (J, M) = (pi(p), p) for jumping
   for (int i = tid; i < n; i += T) {
@@ -95,12 +109,25 @@ __device__ void sigma_pass(const uint16_t* __restrict__ tgt_g, double c,
   __syncthreads();
   // cycle maxima: M(p) = max over 2^r orbit elements, J(p) = pi^(2^r)(p).
   // (J, M) is one 32-bit word, so in-place jumping reads consistent pairs.
+  // Four elements per step with their loads in flight together (in place:
+  // a word read after its owner's update has jumped further, which only
+  // speeds convergence - M stays the max of a contiguous orbit segment)
   for (int r = 0; r < R; ++r) {
-    for (int p = tid; p < n; p += T) {
-      uint32_t w = sW[p];
-      uint32_t w2 = sW[w & 0xFFFFu];
-      uint32_t m = max(w >> 16, w2 >> 16);
-      sW[p] = (w2 & 0xFFFFu) | (m << 16);
+    for (int p0 = tid; p0 < n; p0 += 4 * T) {
+      uint32_t w[4], w2[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int p = p0 + k * T;
+        w[k] = p < n ? sW[p] : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) w2[k] = sW[w[k] & 0xFFFFu];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int p = p0 + k * T;
+        if (p < n)
+          sW[p] = (w2[k] & 0xFFFFu) | (max(w[k] >> 16, w2[k] >> 16) << 16);
+      }
     }
     __syncthreads();
   }
@@ -159,11 +186,25 @@ __device__ void finish_particle(const SwarmView& v, int p, const uint16_t* sx) {
   const int n = v.n, np = v.np, tid = threadIdx.x;
   uint16_t* xg = v.x + (size_t)p * np;
   double* dg = v.dcache + (size_t)p * np;
-  for (int i = tid; i < n; i += T) {
-    int a = sx[i], b = sx[i + 1 == n ? 0 : i + 1];
-    dg[i] = __ldg(v.cost + (size_t)a * v.ld + b);
-    xg[i] = (uint16_t)a;
+  // edge-cost gathers four at a time (L2 or, for a matrix beyond L2, HBM
+  // latency: keep them in flight together)
+  for (int i0 = tid; i0 < n; i0 += 4 * T) {
+    double d[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = i0 + k * T;
+      if (i < n) {
+        const int a = sx[i], b = sx[i + 1 == n ? 0 : i + 1];
+        d[k] = __ldg(v.cost + (size_t)a * v.ld + b);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = i0 + k * T;
+      if (i < n) dg[i] = d[k];
+    }
   }
+  copy_row16<T>(xg, sx, n);
   __syncthreads();
 }
 
@@ -185,7 +226,7 @@ __global__ void __launch_bounds__(T) k_update_w1(SwarmView v, int R) {
 
   for (int p = blockIdx.x; p < v.P; p += gridDim.x) {
     const uint16_t* xg = v.x + (size_t)p * np;
-    for (int i = tid; i < n; i += T) sx[i] = xg[i];
+    copy_row16<T>(sx, xg, n);
     __syncthreads();
     for (int i = tid; i < n; i += T) sposx[sx[i]] = (uint16_t)i;
     if (tid == 0) {
@@ -201,9 +242,11 @@ __global__ void __launch_bounds__(T) k_update_w1(SwarmView v, int R) {
                   s_misc);
     // vmap' = sigma2 o sigma1 o vmap (solver.py:201-209), x' = vmap' o x
     uint16_t* vm = v.vmap + (size_t)p * np;
-    for (int u = tid; u < n; u += T) sB[u] = ssig2[ssig1[vm[u]]];
+    copy_row16<T>(sT, vm, n);
     __syncthreads();
-    for (int u = tid; u < n; u += T) vm[u] = sB[u];
+    for (int u = tid; u < n; u += T) sB[u] = ssig2[ssig1[sT[u]]];
+    __syncthreads();
+    copy_row16<T>(vm, sB, n);
     for (int i = tid; i < n; i += T) sx[i] = sB[sx[i]];
     __syncthreads();
     finish_particle<T>(v, p, sx);
@@ -300,9 +343,14 @@ __global__ void __launch_bounds__(32) k_update_seq(SwarmView v) {
 constexpr int kFitChunk = 256;  // doubles per chunk (2 KiB)
 constexpr int kFitWarps = 4;    // particles per CTA
 
+// use_list: 0 = every particle, 1 = the mutation's event list, 2 = init
+// (every particle, fit = pfit, no control-block checks: the block is only
+// written by k_init_best afterwards)
 __global__ void __launch_bounds__(kFitWarps * 32) k_fitness(SwarmView v,
                                                             int use_list) {
-  if (v.ctl->done) return;
+  const bool init = use_list == 2;
+  if (init) use_list = 0;
+  if (!init && v.ctl->done) return;
   if (use_list && !v.ctl->mutating) return;
   __shared__ __align__(16) double s_buf[kFitWarps][2][kFitChunk];
   __shared__ __align__(8) uint64_t s_bar[kFitWarps][2];
@@ -351,6 +399,10 @@ __global__ void __launch_bounds__(kFitWarps * 32) k_fitness(SwarmView v,
                                     // completed: their values are summed)
   }
   v.fit[p] = total;
+  if (init) {
+    v.pfit[p] = total;
+    return;
+  }
   const int better = total < v.pfit[p];
   if (better) v.pfit[p] = total;
   v.pbflag[p] = better;
@@ -388,14 +440,21 @@ cudaError_t launch_update(const SwarmView& v, cudaStream_t s) {
   if (v.inertia == 1.0) {
     size_t smem = (size_t)16 * v.np;
     const int R = ceil_log2(v.n);
-    if (v.n <= 2048) {
-      auto k = k_update_w1<256>;
+    // ~8 nodes per thread up to 512 threads: small CTAs keep many
+    // particles per SM in flight (the work is barrier- and latency-bound)
+    int T = 64;
+    while (T < 512 && T * 8 < v.n) T <<= 1;
+    if (const char* e = getenv("DPSO_UPD_T")) T = atoi(e);
+    auto go = [&](auto k, int t) {
       set_dyn_smem((const void*)k, smem);
-      k<<<grid, 256, smem, s>>>(v, R);
-    } else {
-      auto k = k_update_w1<512>;
-      set_dyn_smem((const void*)k, smem);
-      k<<<grid, 512, smem, s>>>(v, R);
+      k<<<grid, t, smem, s>>>(v, R);
+    };
+    switch (T) {
+      case 64: go(k_update_w1<64>, 64); break;
+      case 128: go(k_update_w1<128>, 128); break;
+      case 512: go(k_update_w1<512>, 512); break;
+      case 1024: go(k_update_w1<1024>, 1024); break;
+      default: go(k_update_w1<256>, 256); break;
     }
   } else {
     size_t smem = (size_t)8 * v.np + (size_t)8 * v.np;
@@ -408,6 +467,7 @@ cudaError_t launch_update(const SwarmView& v, cudaStream_t s) {
 cudaError_t launch_fitness(const SwarmView& v, int use_list, cudaStream_t s) {
   k_fitness<<<(v.P + kFitWarps - 1) / kFitWarps, kFitWarps * 32, 0, s>>>(
       v, use_list);
+  if (use_list == 2) return cudaGetLastError();  // init: pbest = x already
   k_pbest_copy<<<std::min(v.P, 148 * 8), 128, 0, s>>>(v, use_list);
   return cudaGetLastError();
 }

@@ -100,4 +100,51 @@ struct PhiloxStream {
   }
 };
 
+// A keyed pseudorandom permutation of [0, n): a balanced 6-round Feistel
+// network on 2h bits (2^(2h) >= n, so at most 4n) with cycle walking.  Round
+// keys come from a Philox stream; the round function is a 32-bit avalanche
+// mixer.  Every image is computed independently, so a CTA or warp fills a
+// random permutation (or the first m images: an ordered m-subset) in
+// parallel - the bijective-shuffle construction - where numpy's Fisher-Yates
+// and Floyd samplers are serial.  Production (Philox) mode only.
+struct FeistelPerm {
+  static constexpr int kRounds = 6;
+  uint32_t n, h, mask;
+  uint32_t key[kRounds];
+
+  __host__ __device__ void init(PhiloxStream& r, uint32_t n_) {
+    n = n_;
+    uint32_t bits = 1;
+    while ((1u << bits) < n) ++bits;
+    h = (bits + 1) / 2;
+    mask = (1u << h) - 1u;
+    for (int i = 0; i < kRounds; ++i) key[i] = r.next32();
+  }
+  __host__ __device__ static uint32_t mix(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    x ^= x >> 16;
+    return x;
+  }
+  __host__ __device__ uint32_t round_trip(uint32_t x) const {
+    uint32_t L = x >> h, R = x & mask;
+#pragma unroll
+    for (int i = 0; i < kRounds; ++i) {
+      const uint32_t t = L ^ (mix(R ^ key[i]) & mask);
+      L = R;
+      R = t;
+    }
+    return (L << h) | R;
+  }
+  // image of x in [0, n)
+  __host__ __device__ uint32_t operator()(uint32_t x) const {
+    do {
+      x = round_trip(x);
+    } while (x >= n);
+    return x;
+  }
+};
+
 }  // namespace dpso
