@@ -1147,10 +1147,13 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
   return cudaGetLastError();
 }
 
+// The swarm keeps dcache equal to the edge costs of x at all times (the
+// update re-gathers only the edges it moved), so the apply refreshes the
+// edges i..j of a move.
 cudaError_t launch_two_opt(const SwarmView& v, cudaStream_t s, int parts) {
   return launch_two_opt_core(v.plan, v.n, v.np, v.x, v.dcache, v.P, v.tores,
                              v.chunks, v.chunk_tab, v.ctl, v.fit, v.pfit,
-                             v.pbest, nullptr, nullptr, s, parts);
+                             v.pbest, nullptr, v.dcache, s, parts);
 }
 
 cudaError_t launch_two_opt_batch(const TwoOptPlan& pl, int32_t n, int32_t np,

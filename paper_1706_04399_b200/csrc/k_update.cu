@@ -101,10 +101,13 @@ __device__ void sigma_pass(const uint16_t* __restrict__ tgt_g, double c,
   copy_row16<T>(sT, tgt_g, n);
   __syncthreads();
   // pi, its inverse (backward orbit), and (J, M) = (pi(p), p) for jumping
+  // J is kept as a byte offset into sW when it fits 16 bits (n <= 16384):
+  // a jump step is then LDS, LDS [sW + J], one SIMD max and one byte permute
+  const bool jb = n <= 16384;
   for (int i = tid; i < n; i += T) {
     int pi = sposx[sT[i]];
     sB[pi] = (uint16_t)i;
-    sW[i] = (uint32_t)pi | ((uint32_t)i << 16);
+    sW[i] = (uint32_t)(jb ? 4 * pi : pi) | ((uint32_t)i << 16);
   }
   __syncthreads();
   // cycle maxima: M(p) = max over 2^r orbit elements, J(p) = pi^(2^r)(p).
@@ -112,6 +115,29 @@ __device__ void sigma_pass(const uint16_t* __restrict__ tgt_g, double c,
   // Four elements per step with their loads in flight together (in place:
   // a word read after its owner's update has jumped further, which only
   // speeds convergence - M stays the max of a contiguous orbit segment)
+  if (jb) {
+    const unsigned char* base = reinterpret_cast<const unsigned char*>(sW);
+    for (int r = 0; r < R; ++r) {
+      for (int p0 = tid; p0 < n; p0 += 4 * T) {
+        uint32_t w[4], w2[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int p = p0 + k * T;
+          w[k] = p < n ? sW[p] : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          w2[k] = *reinterpret_cast<const uint32_t*>(base + (w[k] & 0xFFFFu));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int p = p0 + k * T;
+          // low half: J of the target; high half: max of the two M
+          if (p < n) sW[p] = __byte_perm(w2[k], __vmaxu2(w[k], w2[k]), 0x7610);
+        }
+      }
+      __syncthreads();
+    }
+  } else
   for (int r = 0; r < R; ++r) {
     for (int p0 = tid; p0 < n; p0 += 4 * T) {
       uint32_t w[4], w2[4];
@@ -181,8 +207,11 @@ __device__ void sigma_pass(const uint16_t* __restrict__ tgt_g, double c,
 // pbest (solver.py:217-220) follow in k_fitness / k_pbest_copy, one thread
 // per particle, so the sequential fp64 sums of all particles run
 // concurrently instead of on one thread of each CTA.
+// sold (nullable): the tour before the move; an edge whose two endpoints
+// are unchanged keeps its cached cost (no gather, no store)
 template <int T>
-__device__ void finish_particle(const SwarmView& v, int p, const uint16_t* sx) {
+__device__ void finish_particle(const SwarmView& v, int p, const uint16_t* sx,
+                                const uint16_t* sold = nullptr) {
   const int n = v.n, np = v.np, tid = threadIdx.x;
   uint16_t* xg = v.x + (size_t)p * np;
   double* dg = v.dcache + (size_t)p * np;
@@ -190,18 +219,22 @@ __device__ void finish_particle(const SwarmView& v, int p, const uint16_t* sx) {
   // latency: keep them in flight together)
   for (int i0 = tid; i0 < n; i0 += 4 * T) {
     double d[4];
+    bool moved[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int i = i0 + k * T;
+      moved[k] = false;
       if (i < n) {
-        const int a = sx[i], b = sx[i + 1 == n ? 0 : i + 1];
-        d[k] = __ldg(v.cost + (size_t)a * v.ld + b);
+        const int i1 = i + 1 == n ? 0 : i + 1;
+        const int a = sx[i], b = sx[i1];
+        moved[k] = !sold || a != sold[i] || b != sold[i1];
+        if (moved[k]) d[k] = __ldg(v.cost + (size_t)a * v.ld + b);
       }
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int i = i0 + k * T;
-      if (i < n) dg[i] = d[k];
+      if (moved[k]) dg[i] = d[k];
     }
   }
   copy_row16<T>(xg, sx, n);
@@ -247,9 +280,10 @@ __global__ void __launch_bounds__(T) k_update_w1(SwarmView v, int R) {
     for (int u = tid; u < n; u += T) sB[u] = ssig2[ssig1[sT[u]]];
     __syncthreads();
     copy_row16<T>(vm, sB, n);
-    for (int i = tid; i < n; i += T) sx[i] = sB[sx[i]];
+    // x' = vmap' o x into sposx (free now); sx keeps x for the edge reuse
+    for (int i = tid; i < n; i += T) sposx[i] = sB[sx[i]];
     __syncthreads();
-    finish_particle<T>(v, p, sx);
+    finish_particle<T>(v, p, sposx, sx);
   }
 }
 
