@@ -334,8 +334,8 @@ template <int MODE>
 __device__ __noinline__ float scan_hit(float u0, float u1, float u2, float u3,
                                        float w0, float w1, float w2, float w3,
                                        float da, float db, float la, float lb,
-                                       int i, int j0, float thr, float* cd,
-                                       uint32_t* cij, float* st) {
+                                       int i, int j0, int jstep, float thr,
+                                       float* cd, uint32_t* cij, float* st) {
   // entered by the whole warp (the pre-test is warp-uniform): u = row i,
   // w = row i+1 of the same 4 column blocks; returns the warp-wide
   // threshold base (EXACT32: warp minimum; FILTER32: warp minimum + thr)
@@ -345,7 +345,7 @@ __device__ __noinline__ float scan_hit(float u0, float u1, float u2, float u3,
     int bi = __float_as_int(st[32]), bj = __float_as_int(st[64]);
 #pragma unroll
     for (int g = 0; g < 8; ++g) {
-      const int ii = i + (g >> 2), jj = j0 + 32 * (g & 3);
+      const int ii = i + (g >> 2), jj = j0 + jstep * (g & 3);
       const float t = __fsub_rn(uv[g], g < 4 ? da : db);  // exact
       if (lex_less(t, ii, jj, best, bi, bj)) {
         best = t;
@@ -394,7 +394,7 @@ __device__ __noinline__ float scan_hit(float u0, float u1, float u2, float u3,
       if (ncand < kCand) {
         cd[32 * ncand] = tv[g];
         cij[32 * ncand] = ((uint32_t)(i + (g >> 2)) << 16) |
-                          (uint32_t)(j0 + 32 * (g & 3));
+                          (uint32_t)(j0 + jstep * (g & 3));
         ++ncand;
       } else {
         overflow = 1;
@@ -457,22 +457,37 @@ __global__ void __launch_bounds__(kW32 * 32, DPSO_SCAN_MINB)
   unsigned char* wbase = smem + (size_t)warp * a.buf_stride2;
   float* sdj = (float*)(wbase + kBufs32 * a.buf_stride);  // local column
 
+  // Column layout: groups of GL blocks (32 GL columns); inside a group lane l
+  // owns the GL consecutive columns jlo + 32 GL g + GL l + (0 .. GL-1), so
+  // the shift-reuse neighbour j - 1 of a column is the same lane's previous
+  // block except at a group's first block (one rotate per group and row).
+  constexpr int GL = group_blocks<NPL>() < NPL ? group_blocks<NPL>() : NPL;
+  auto col_of = [&](int m) -> int {
+    return jlo + 32 * GL * (m / GL) + GL * lane + (m % GL);
+  };
   constexpr int NH = (NPL + 1) / 2;
   uint32_t sjp[NH];  // 4 s_j for blocks 2h (lo) and 2h+1 (hi)
 #pragma unroll
   for (int h = 0; h < NH; ++h) sjp[h] = 0;
 #pragma unroll
   for (int m = 0; m < NPL; ++m) {
-    const int j = jlo + lane + 32 * m;
+    const int j = col_of(m);
     if (j < jhi) {
       const uint32_t s4 = (uint32_t)ES * tour[j + 1 == n ? 0 : j + 1];
       sjp[m / 2] |= (m & 1) ? (s4 << 16) : s4;
     }
   }
-  for (int jl = lane; jl < 32 * NPL; jl += 32) {
-    const int j = jlo + jl;
-    sdj[jl] = (j >= r0 && j < jhi) ? (float)(dg[j] * a.dscale) : -kInfF;
+  // d_j of block m at sdj[lane + 32 m] (lane-interleaved: conflict free)
+#pragma unroll
+  for (int m = 0; m < NPL; ++m) {
+    const int j = col_of(m);
+    sdj[lane + 32 * m] =
+        (j >= r0 && j < jhi) ? (float)(dg[j] * a.dscale) : -kInfF;
   }
+  auto sdj_index = [&](int c) -> int {  // c = j - jlo
+    const int grp = c / (32 * GL), within = c % (32 * GL);
+    return (within / GL) + 32 * (GL * grp + within % GL);
+  };
   auto sj = [&](int m) -> uint32_t {
     return (m & 1) ? (sjp[m / 2] >> 16) : (sjp[m / 2] & 0xFFFFu);
   };
@@ -562,11 +577,13 @@ __global__ void __launch_bounds__(kW32 * 32, DPSO_SCAN_MINB)
     }
     const float di = __shfl_sync(0xffffffffu, db, k & 31);
     const float di2 = __shfl_sync(0xffffffffu, db, (k + 1) & 31);
-    {  // retire columns i and i + 1 (their owner lanes)
+    {  // retire columns i and i + 1 (lane 0 writes both slots)
       const int c0 = i - jlo, c1 = i + 1 - jlo;
-      if (c0 >= 0 && c0 < 32 * NPL && lane == (c0 & 31)) sdj[c0] = -kInfF;
-      if (two && c1 >= 0 && c1 < 32 * NPL && lane == (c1 & 31))
-        sdj[c1] = -kInfF;
+      if (lane == 0) {
+        if (c0 >= 0 && c0 < 32 * NPL) sdj[sdj_index(c0)] = -kInfF;
+        if (two && c1 >= 0 && c1 < 32 * NPL) sdj[sdj_index(c1)] = -kInfF;
+      }
+      __syncwarp();
     }
     const uint32_t B1 = pair_rows(pass & 1);
     const uint32_t B2 = two ? B1 + a.buf_stride : B1;
@@ -592,29 +609,51 @@ __global__ void __launch_bounds__(kW32 * 32, DPSO_SCAN_MINB)
           rp1 = __shfl_sync(0xffffffffu, Bv[m0 - 1], 31);
           rp2 = at4(B1, __shfl_sync(0xffffffffu, sj(m0 - 1), 31));
         }
-        float u[kG32], w[kG32];
+        float u[kG32], w[kG32], b1v[kG32], b2v[kG32];
 #pragma unroll
         for (int g = 0; g < kG32; ++g) {
           const int m = m0 + g;
           if (m < NPL) {
             const uint32_t o = sj(m);
-            const float b1 = at4(B1, o), b2 = at4(B2, o);
+            b1v[g] = at4(B1, o);
+            b2v[g] = at4(B2, o);
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < kG32; ++g) {
+          const int m = m0 + g;
+          if (m < NPL) {
             const float dj = sdj[lane + 32 * m];
-            const float r1v =
-                __shfl_sync(0xffffffffu, Bv[m], (lane + 31) & 31);
-            const float av1 = lane == 0 ? rp1 : r1v;
-            rp1 = r1v;
-            const float r2v = __shfl_sync(0xffffffffu, b1, (lane + 31) & 31);
-            const float av2 = lane == 0 ? rp2 : r2v;
-            rp2 = r2v;
-            Bv[m] = b2;
-            u[g] = __fadd_rn(av1, __fsub_rn(b1, dj));
-            w[g] = __fadd_rn(av2, __fsub_rn(b2, dj));
+            float av1, av2;
+            if (m % GL == 0) {
+              // first block of a layout group: column j - 1 is lane l-1's
+              // last block (lane 0: the previous group's lane 31, carried
+              // in rp by the same rotate)
+              const int last = m + GL - 1;
+              const float r1v =
+                  __shfl_sync(0xffffffffu, Bv[last], (lane + 31) & 31);
+              av1 = lane == 0 ? rp1 : r1v;
+              rp1 = r1v;
+              const float r2v = __shfl_sync(
+                  0xffffffffu, b1v[last - m0], (lane + 31) & 31);
+              av2 = lane == 0 ? rp2 : r2v;
+              rp2 = r2v;
+            } else {
+              av1 = Bv[m - 1];  // previous pass's B row, column j - 1
+              av2 = b1v[g - 1];
+            }
+            u[g] = __fadd_rn(av1, __fsub_rn(b1v[g], dj));
+            w[g] = __fadd_rn(av2, __fsub_rn(b2v[g], dj));
           } else {
             u[g] = kInfF;
             w[g] = kInfF;
           }
         }
+        // Bv of the group is rewritten only now: the shifts above read the
+        // previous pass's values
+#pragma unroll
+        for (int g = 0; g < kG32; ++g)
+          if (m0 + g < NPL) Bv[m0 + g] = b2v[g];
         float mu = u[0], mw = w[0];
 #pragma unroll
         for (int g = 1; g < kG32; ++g) {
@@ -626,9 +665,12 @@ __global__ void __launch_bounds__(kW32 * 32, DPSO_SCAN_MINB)
         if (__any_sync(0xffffffffu, hit)) {
 #pragma unroll
           for (int h = 0; h < kG32; h += 4) {
+            // columns of blocks m0 + h .. + 3: consecutive within a layout
+            // group (GL >= 2); GL == 1 is the interleaved layout (step 32);
+            // blocks past NPL hold +inf
             lim = scan_hit<MODE>(u[h], u[h + 1], u[h + 2], u[h + 3], w[h],
                                  w[h + 1], w[h + 2], w[h + 3], di, di2, la, lb,
-                                 i, jlo + lane + 32 * (m0 + h), a.thr,
+                                 i, col_of(m0 + h), GL == 1 ? 32 : 1, a.thr,
                                  &s_cd[warp][0][lane], &s_cij[warp][0][lane],
                                  st);
             la = lrow_of(di);
