@@ -587,8 +587,23 @@ __global__ void __launch_bounds__(kW32 * 32, DPSO_SCAN_MINB)
     }
     const uint32_t B1 = pair_rows(pass & 1);
     const uint32_t B2 = two ? B1 + a.buf_stride : B1;
-    if (a.stream_only) {
+    if (a.stream_only == 1) {  // probe: the row stream alone
       if (lane == 0 && at4(B2, 0) == -1.f) lim = 0.f;  // keep the loads
+      continue;
+    }
+    if (a.stream_only == 2) {  // probe: stream + the live groups' gathers
+      constexpr int kGp = group_blocks<NPL>();
+      float acc = kInfF;
+#pragma unroll
+      for (int m0 = 0; m0 < NPL; m0 += kGp) {
+        if (jlo + 32 * (m0 + kGp) - 1 > i + 1) {
+#pragma unroll
+          for (int g = 0; g < kGp; ++g)
+            if (m0 + g < NPL)
+              acc = fminf(acc, at4(B1, sj(m0 + g)) + at4(B2, sj(m0 + g)));
+        }
+      }
+      if (acc == -1.f) lim = 0.f;  // keep the loads
       continue;
     }
     auto lrow_of = [&](float d) -> float {
@@ -1091,7 +1106,9 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
   a.res = res;
   a.ctl = ctl;
   a.thr = pl.thr;
-  a.stream_only = getenv("DPSO_SCAN_STREAM_ONLY") ? 1 : 0;
+  a.stream_only = getenv("DPSO_SCAN_STREAM_ONLY")
+                      ? atoi(getenv("DPSO_SCAN_STREAM_ONLY"))
+                      : 0;  // probes: 1 = row stream, 2 = stream + gathers
   const int64_t tasks = (int64_t)count * chunks;
   cudaError_t e = cudaSuccess;
   const int npl = npl_for(n);
