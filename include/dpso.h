@@ -175,6 +175,25 @@ int dpso_build_cost(const uint8_t* dev_occ, int32_t nx, int32_t ny,
                     int64_t ld, uint8_t* dev_virtual, double* host_vcost,
                     void* cuda_stream);
 
+/* Plain-text cost-matrix files (replaces graph.py:123-130
+ * save_cost_matrix and graph.py:133-143 load_cost_matrix, host code).
+ * Write: a header line "n", then n lines of n entries, each Python's
+ * repr(float(x)), single-space separated: byte-identical to the reference.
+ * Read: tokens split on whitespace, parsed like Python int()/float();
+ * with host_out == NULL only the header is read (*n_out = n, to size the
+ * buffer), else all n*n entries go to host_out (row-major, leading
+ * dimension ld >= n, capacity cap_n rows).  Errors (DPSO_EINVAL) carry the
+ * reference's messages: "empty cost matrix file <path>", "cost matrix
+ * <path>: expected <n*n> entries, got <k>", Python's int()/float()
+ * conversion messages. */
+int dpso_write_matrix_text(const char* path, const double* host, int64_t ld,
+                           int32_t n);
+int dpso_read_matrix_text(const char* path, double* host_out, int64_t ld,
+                          int32_t cap_n, int32_t* n_out);
+/* repr(float(x)) of one value into out (cap bytes incl. the NUL): the
+ * writer's formatter, exposed for tests. */
+int dpso_py_repr(double x, char* out, int32_t cap);
+
 /* Philox4x32-10 block (host evaluation of the device RNG's code path, for
  * known-answer tests): out = philox(ctr[4], key = k0 | k1 << 32). */
 int dpso_philox4x32_10(const uint32_t* ctr, uint64_t key, uint32_t* out);

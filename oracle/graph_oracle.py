@@ -16,6 +16,9 @@ oracle/dpso_oracle.py for the rules).
                     symmetric fill, blocked pairs -> VIRTUAL_SCALE * n *
                     max_finite (1e6 when no finite edge)
 
+* ``save_cost_matrix`` / ``load_cost_matrix`` — graph.py:123-143, the
+                    plain-text matrix format (repr(float(x)) entries)
+
 Pinned against golden_graph.npz (tests/golden/make_golden_graph.py, run on
 the unmodified reference) by tests/test_oracle_graph.py.
 """
@@ -86,3 +89,27 @@ def build_cost(occ: np.ndarray, vox, weights):
         cost[i, j] = cost[j, i] = vcost
         virtual[i, j] = virtual[j, i] = True
     return cost, virtual, vcost
+
+
+def save_cost_matrix(path, cost) -> None:
+    """graph.py:123-130."""
+    n = cost.shape[0]
+    with open(path, "w") as fh:
+        fh.write(f"{n}\n")
+        for row in cost:
+            fh.write(" ".join(repr(float(x)) for x in row))
+            fh.write("\n")
+
+
+def load_cost_matrix(path) -> np.ndarray:
+    """graph.py:133-143."""
+    with open(path) as fh:
+        tokens = fh.read().split()
+    if not tokens:
+        raise ValueError(f"empty cost matrix file {path}")
+    n = int(tokens[0])
+    vals = [float(t) for t in tokens[1:]]
+    if len(vals) != n * n:
+        raise ValueError(
+            f"cost matrix {path}: expected {n * n} entries, got {len(vals)}")
+    return np.asarray(vals, dtype=float).reshape(n, n)

@@ -7,7 +7,9 @@ versions of the helpers the reference's baselines and tests use.
 from .solver import DiscreteSwarmSolver, SolveReport, solve_matrix
 from .kernels import (best_exchange_batch, nearest_neighbor_tour,
                       nearest_neighbor_two_opt, tour_cost_batch)
-from .graph import TourGraph, build_cost_matrix, build_graph
+from .graph import (TourGraph, build_cost_matrix, build_graph,
+                    load_cost_matrix, load_cost_matrix_device,
+                    save_cost_matrix)
 
 __version__ = "0.1.0"
 
@@ -16,4 +18,5 @@ __all__ = [
     "best_exchange_batch", "nearest_neighbor_tour",
     "nearest_neighbor_two_opt", "tour_cost_batch",
     "TourGraph", "build_cost_matrix", "build_graph",
+    "load_cost_matrix", "load_cost_matrix_device", "save_cost_matrix",
 ]

@@ -66,6 +66,10 @@ _SIG = {
     "dpso_build_cost": (_I32, [_P, _I32, _I32, _I32, _P, _P, _I32, _P, _I64,
                                 _P, _P, _P]),
     "dpso_philox4x32_10": (_I32, [_P, ctypes.c_uint64, _P]),
+    "dpso_write_matrix_text": (_I32, [ctypes.c_char_p, _P, _I64, _I32]),
+    "dpso_read_matrix_text": (_I32, [ctypes.c_char_p, _P, _I64, _I32,
+                                     ctypes.POINTER(_I32)]),
+    "dpso_py_repr": (_I32, [ctypes.c_double, ctypes.c_char_p, _I32]),
     "dpso_version": (ctypes.c_char_p, []),
 }
 EXPORTED = tuple(_SIG)

@@ -74,7 +74,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc compilation failed")
     tmp = LIB + ".tmp"
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
-           "-o", tmp, *objs, "-lcudart"]
+           "-o", tmp, *objs, "-lcudart", "-lpthread"]
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
     return LIB

@@ -47,6 +47,14 @@ int cuda_fail(cudaError_t e, const char* where) {
   std::string m = std::string(where) + ": " + cudaGetErrorString(e);
   return fail(DPSO_ECUDA, m);
 }
+}  // namespace
+
+namespace dpso {
+// the thread-local last error for the other translation units
+int api_fail(int code, const char* msg) { return fail(code, msg); }
+}  // namespace dpso
+
+namespace {
 
 #define CK(call)                                        \
   do {                                                  \

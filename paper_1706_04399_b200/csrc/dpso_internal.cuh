@@ -146,6 +146,9 @@ struct SwarmView {
   int64_t* init_anchor;
 };
 
+// sets dpso_last_error() (thread-local) and returns code
+int api_fail(int code, const char* msg);
+
 // ---- kernel launchers (each .cu owns its kernels) -------------------------
 cudaError_t launch_gen_begin(const SwarmView& v, cudaStream_t s);
 cudaError_t launch_update(const SwarmView& v, cudaStream_t s);

@@ -9,6 +9,11 @@ pairs at ``1e3 * n * max_finite`` (1e6 when no finite edge) and flagged in
 signature for callers holding the reference's CoveragePlan/VoxelGrid.
 Per-pair waypoint legs (``TourGraph.legs``) are not produced: the
 reference's CLI needs them only for the final tour's N edges.
+
+``save_cost_matrix`` / ``load_cost_matrix`` are graph.py:123-143 (the
+plain-text ``--matrix`` format) in native host code: the file bytes are the
+reference's, and the reader parses straight into a pinned buffer that
+``load_cost_matrix_device`` uploads without another copy.
 """
 from __future__ import annotations
 
@@ -71,3 +76,58 @@ def build_graph(plan, grid, weights, heuristic_mode: str = "admissible"):
     virtual.setflags(write=False)
     return TourGraph(n_nodes=len(vox), cost=cost, virtual=virtual,
                      virtual_cost=vcost)
+
+
+def _path_bytes(path) -> bytes:
+    import os
+    return os.fsencode(os.fspath(path))
+
+
+def save_cost_matrix(path, cost) -> None:
+    """graph.py:123-130: header line n, then n lines of repr(float(x))."""
+    c = np.ascontiguousarray(np.asarray(cost, dtype=np.float64))
+    if c.ndim != 2 or c.shape[0] != c.shape[1]:
+        raise ValueError("cost matrix must be square")
+    n = c.shape[0]
+    with open(path, "w"):  # the reference's open() errors and truncation
+        pass
+    _lib.check(_lib.load().dpso_write_matrix_text(
+        _path_bytes(path), c.ctypes.data_as(ctypes.c_void_p), n, n))
+
+
+def _read_matrix(path, alloc):
+    with open(path):  # the reference's open() errors (FileNotFoundError ...)
+        pass
+    lib = _lib.load()
+    n = ctypes.c_int32(0)
+    _lib.check(lib.dpso_read_matrix_text(_path_bytes(path), None, 0, 0,
+                                         ctypes.byref(n)))
+    buf, ptr, ld = alloc(int(n.value))
+    _lib.check(lib.dpso_read_matrix_text(_path_bytes(path), ptr, ld,
+                                         int(n.value), ctypes.byref(n)))
+    return buf, int(n.value), ld
+
+
+def load_cost_matrix(path) -> np.ndarray:
+    """graph.py:133-143 (same values, same ValueError messages)."""
+    def alloc(n):
+        a = np.empty((n, n), dtype=np.float64)
+        return a, a.ctypes.data_as(ctypes.c_void_p), n
+    a, _, _ = _read_matrix(path, alloc)
+    return a
+
+
+def load_cost_matrix_device(path, device=None):
+    """Parse into a pinned host buffer (rows padded to the device layout)
+    and upload it: returns (cost tensor (n, ld) on the device, ld)."""
+    torch = _torch()
+
+    def alloc(n):
+        ld = max(8, (n + 7) // 8 * 8)
+        t = torch.zeros((max(n, 1), ld), dtype=torch.float64,
+                        pin_memory=True)
+        return t, ctypes.c_void_p(t.data_ptr()), ld
+    host, n, ld = _read_matrix(path, alloc)
+    dev = torch.device(device) if device is not None else torch.device(
+        "cuda", torch.cuda.current_device())
+    return host[:n].to(dev, non_blocking=False), ld
