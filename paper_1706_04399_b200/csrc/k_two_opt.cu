@@ -322,7 +322,17 @@ constexpr int kBufs32 = 4;     // fp32 per-warp row ring (one pass ahead)
 // independent work per pre-test), 4 for narrow ones (finer dead-group skip)
 template <int NPL>
 constexpr int group_blocks() { return NPL >= 32 ? 8 : 4; }
-constexpr int kNplMax32 = 32;  // column blocks per fp32 task (1024 columns)
+// column blocks per fp32 task: 32 (1024 columns) or, by DPSO_SCAN_NPL, 16
+// or 8 (narrower tasks: fewer registers per thread, more warps per SM, each
+// row streamed once per column range)
+static int npl_max32() {
+  static const int v = [] {
+    const char* e = getenv("DPSO_SCAN_NPL");
+    const int x = e ? atoi(e) : 32;
+    return (x == 8 || x == 16) ? x : 32;
+  }();
+  return v;
+}
 constexpr int kW32 = 2;        // warps (tasks) per CTA, fp32 scan
 
 __device__ __forceinline__ bool lex_less(float t, int i, int j, float bt,
@@ -1001,9 +1011,9 @@ cudaError_t launch_cost_prep(const double* cost, int64_t ld, int32_t n,
   return cudaGetLastError();
 }
 
-// Column ranges of the fp32 scan (kNplMax32 blocks of 32 columns each).
+// Column ranges of the fp32 scan (npl_max32() blocks of 32 columns each).
 static int column_ranges(int32_t n) {
-  const int w = 32 * kNplMax32;
+  const int w = 32 * npl_max32();
   return n <= w ? 1 : (n + w - 1) / w;
 }
 
@@ -1012,7 +1022,7 @@ int two_opt_pick_chunks(int32_t n, int32_t P) {
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // fp32 scan: one warp per task (row ring + d_j in shared memory)
-  const int npl = std::min(std::max(npl_for(n), 1), kNplMax32);
+  const int npl = std::min(std::max(npl_for(n), 1), npl_max32());
   size_t per_warp =
       (size_t)kBufs32 * round_up((int64_t)round_up(n, 4) * 4, 128) +
       4 * (size_t)32 * npl;
@@ -1032,12 +1042,12 @@ int two_opt_pick_chunks(int32_t n, int32_t P) {
 }
 
 // Task table: chunks x (r0, r1, jlo, jhi).  Columns are split into ranges
-// of 32 * kNplMax32; each range's pairs (i < j, j in the range) are cut into
+// of 32 * npl_max32(); each range's pairs (i < j, j in the range) are cut into
 // row bands of roughly equal pair count, with bands given to the ranges in
 // proportion to their pairs.  Every pair i < j is in exactly one task.
 int two_opt_chunk_table(int32_t n, int32_t chunks, int32_t* tab) {
   const int R = column_ranges(n);
-  const int w = 32 * kNplMax32;
+  const int w = 32 * npl_max32();
   std::vector<double> pairs(R);
   double total = 0.0;
   for (int k = 0; k < R; ++k) {
@@ -1149,7 +1159,7 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
       a.row_bytes = (uint32_t)(round_up(n, 16 / es) * es);
       a.buf_stride = (uint32_t)round_up(a.row_bytes, 128);
       // per warp: 2-slot row ring + d_j (fp32, 32 * NPL entries)
-      const int npl32 = std::min(std::max(npl, 1), kNplMax32);
+      const int npl32 = std::min(std::max(npl, 1), npl_max32());
       a.buf_stride2 = (uint32_t)(kBufs32 * a.buf_stride +
                                  round_up((int64_t)32 * npl32 * 4, 128));
       const int warps = kW32;

@@ -115,9 +115,15 @@ __device__ void sigma_pass(const uint16_t* __restrict__ tgt_g, double c,
   // Four elements per step with their loads in flight together (in place:
   // a word read after its owner's update has jumped further, which only
   // speeds convergence - M stays the max of a contiguous orbit segment)
+  // A round in which no M changes ends the jumping: then every segment
+  // already covers its cycle's maximum (the non-covering element nearest
+  // the maximum would have picked it up from its jump target), so M is the
+  // cycle maximum everywhere.  Converged swarms (x near its target: short
+  // cycles) stop after a few rounds.
   if (jb) {
     const unsigned char* base = reinterpret_cast<const unsigned char*>(sW);
     for (int r = 0; r < R; ++r) {
+      int changed = 0;
       for (int p0 = tid; p0 < n; p0 += 4 * T) {
         uint32_t w[4], w2[4];
 #pragma unroll
@@ -132,10 +138,14 @@ __device__ void sigma_pass(const uint16_t* __restrict__ tgt_g, double c,
         for (int k = 0; k < 4; ++k) {
           const int p = p0 + k * T;
           // low half: J of the target; high half: max of the two M
-          if (p < n) sW[p] = __byte_perm(w2[k], __vmaxu2(w[k], w2[k]), 0x7610);
+          const uint32_t m2 = __vmaxu2(w[k], w2[k]);
+          if (p < n) {
+            changed |= (m2 ^ w[k]) >> 16;
+            sW[p] = __byte_perm(w2[k], m2, 0x7610);
+          }
         }
       }
-      __syncthreads();
+      if (!__syncthreads_or(changed)) break;
     }
   } else
   for (int r = 0; r < R; ++r) {
