@@ -165,18 +165,19 @@ int check_params(const dpso_params* p, int n) {
   if (n < 2 || n > kMaxN)
     return fail(DPSO_EINVAL, "n must be in [2, 65535] for the device path");
   {
-    // the update kernel keeps a particle's six u16 arrays and the repair's
-    // u32 words in shared memory: 16 bytes per node
+    // the update kernel keeps a particle's arrays in shared memory: 16
+    // bytes per node (w < 1, or n <= 14000), 10 beyond (k_update_w1_lowmem)
+    const int bpn = (p->inertia < 1.0 || n <= 14000) ? 16 : 10;
     int dev = 0, smax = 0;
     if (cudaGetDevice(&dev) == cudaSuccess &&
         cudaDeviceGetAttribute(&smax, cudaDevAttrMaxSharedMemoryPerBlockOptin,
                                dev) == cudaSuccess &&
-        smax > 0 && (int64_t)16 * round_up(n, 8) > smax - 1024) {
+        smax > 0 && (int64_t)bpn * round_up(n, 8) > smax - 1024) {
       char buf[160];
       snprintf(buf, sizeof buf,
                "n = %d exceeds the device update kernel's shared memory "
                "(max n = %d on this device)",
-               n, (int)((smax - 1024) / 16 / 8 * 8));
+               n, (int)((smax - 1024) / bpn / 8 * 8));
       return fail(DPSO_EINVAL, buf);
     }
   }

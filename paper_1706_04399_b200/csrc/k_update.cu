@@ -90,22 +90,29 @@ __device__ __forceinline__ void copy_row16(uint16_t* dst, const uint16_t* src,
 }
 
 // sigma (value permutation of the first prefix_len(c, L) repair
-// transpositions of x -> target) into sout[value].
-template <int T>
+// transpositions of x -> target) into sout[value].  GT: the target is read
+// from global memory (tgt_g) instead of a shared copy sT (large n: the
+// low-shared-memory update); sout may then alias sW (written only after the
+// last read of sW).
+template <int T, bool GT = false>
 __device__ void sigma_pass(const uint16_t* __restrict__ tgt_g, double c,
                            int n, int R, const uint16_t* sx,
                            const uint16_t* sposx, uint16_t* sT, uint16_t* sB,
                            uint32_t* sW, uint16_t* sout, int* s_warp,
                            int* s_misc) {
   const int tid = threadIdx.x;
-  copy_row16<T>(sT, tgt_g, n);
-  __syncthreads();
+  if (GT) {
+    sT = const_cast<uint16_t*>(tgt_g);  // reads only (via the cache)
+  } else {
+    copy_row16<T>(sT, tgt_g, n);
+    __syncthreads();
+  }
   // pi, its inverse (backward orbit), and (J, M) = (pi(p), p) for jumping
   // J is kept as a byte offset into sW when it fits 16 bits (n <= 16384):
   // a jump step is then LDS, LDS [sW + J], one SIMD max and one byte permute
   const bool jb = n <= 16384;
   for (int i = tid; i < n; i += T) {
-    int pi = sposx[sT[i]];
+    int pi = sposx[GT ? __ldg(tgt_g + i) : sT[i]];
     sB[pi] = (uint16_t)i;
     sW[i] = (uint32_t)(jb ? 4 * pi : pi) | ((uint32_t)i << 16);
   }
@@ -202,11 +209,11 @@ __device__ void sigma_pass(const uint16_t* __restrict__ tgt_g, double c,
   for (int q = tid; q < n; q += T) {
     uint16_t cur;
     if (q <= t) {
-      cur = sT[q];
+      cur = GT ? __ldg(tgt_g + q) : sT[q];
     } else {
       int b = sB[q];
       while (b <= t) b = sB[b];
-      cur = sT[b];
+      cur = GT ? __ldg(tgt_g + b) : sT[b];
     }
     sout[sx[q]] = cur;
   }
@@ -291,6 +298,55 @@ __global__ void __launch_bounds__(T) k_update_w1(SwarmView v, int R) {
     __syncthreads();
     copy_row16<T>(vm, sB, n);
     // x' = vmap' o x into sposx (free now); sx keeps x for the edge reuse
+    for (int i = tid; i < n; i += T) sposx[i] = sB[sx[i]];
+    __syncthreads();
+    finish_particle<T>(v, p, sposx, sx);
+  }
+}
+
+// Large n (beyond what 16 B/node of shared memory allows, n > 14000): 10
+// B/node - x, pos_x, the backward orbit and the jump words, which also hold
+// sigma once the jumping is done; the targets are read through the cache and
+// sigma1 is folded into vmap in global memory right away.
+template <int T>
+__global__ void __launch_bounds__(T) k_update_w1_lowmem(SwarmView v, int R) {
+  if (v.ctl->done) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = v.n, np = v.np, tid = threadIdx.x;
+  uint16_t* sx = (uint16_t*)smem;
+  uint16_t* sposx = sx + np;
+  uint16_t* sB = sposx + np;
+  uint32_t* sW = (uint32_t*)(sB + np);
+  uint16_t* ssig = (uint16_t*)sW;  // sigma after the jumping
+  __shared__ int s_warp[32];
+  __shared__ int s_misc[4];
+  __shared__ double s_c[2];
+  for (int p = blockIdx.x; p < v.P; p += gridDim.x) {
+    copy_row16<T>(sx, v.x + (size_t)p * np, n);
+    __syncthreads();
+    for (int i = tid; i < n; i += T) sposx[sx[i]] = (uint16_t)i;
+    if (tid == 0) {
+      double r1, r2;
+      draw_r1r2(v, p, &r1, &r2);
+      s_c[0] = __dmul_rn(v.cognitive, r1);
+      s_c[1] = __dmul_rn(v.social, r2);
+    }
+    __syncthreads();
+    uint16_t* vm = v.vmap + (size_t)p * np;
+    sigma_pass<T, true>(v.pbest + (size_t)p * np, s_c[0], n, R, sx, sposx,
+                        nullptr, sB, sW, ssig, s_warp, s_misc);
+    // vmap1 = sigma1 o vmap (solver.py:201-205), in place in global memory
+    for (int u = tid; u < n; u += T) vm[u] = ssig[vm[u]];
+    __syncthreads();
+    sigma_pass<T, true>(v.gbest, s_c[1], n, R, sx, sposx, nullptr, sB, sW,
+                        ssig, s_warp, s_misc);
+    // vmap' = sigma2 o vmap1 into sB (free now) and global; x' = vmap' o x
+    for (int u = tid; u < n; u += T) {
+      const uint16_t w = ssig[vm[u]];
+      sB[u] = w;
+      vm[u] = w;
+    }
+    __syncthreads();
     for (int i = tid; i < n; i += T) sposx[i] = sB[sx[i]];
     __syncthreads();
     finish_particle<T>(v, p, sposx, sx);
@@ -493,6 +549,24 @@ cudaError_t launch_update(const SwarmView& v, cudaStream_t s) {
       set_dyn_smem((const void*)k, smem);
       k<<<grid, t, smem, s>>>(v, R);
     };
+    // 10 B/node only where 16 no longer fits (n > 14000): at C5 (n =
+    // 10000) two 10 B/node CTAs per SM measured slower (35 vs 27 ms) than
+    // one 16 B/node CTA - the cached target reads and the global vmap fold
+    // cost more than the extra occupancy gains.  DPSO_UPD_LOWMEM=1 forces it.
+    const bool low = v.n > 14000 || getenv("DPSO_UPD_LOWMEM");
+    if (low) {
+      smem = (size_t)10 * v.np;
+      auto go2 = [&](auto k, int t) {
+        set_dyn_smem((const void*)k, smem);
+        k<<<grid, t, smem, s>>>(v, R);
+      };
+      switch (T) {
+        case 1024: go2(k_update_w1_lowmem<1024>, 1024); break;
+        case 256: go2(k_update_w1_lowmem<256>, 256); break;
+        default: go2(k_update_w1_lowmem<512>, 512); break;
+      }
+      return launch_fitness(v, 0, s);
+    }
     switch (T) {
       case 64: go(k_update_w1<64>, 64); break;
       case 128: go(k_update_w1<128>, 128); break;

@@ -273,7 +273,8 @@ def test_n_beyond_update_kernel_shared_memory_is_rejected(pkg):
     from paper_1706_04399_b200 import _lib
     s = pkg.DiscreteSwarmSolver(n_particles=8)
     nbytes = ctypes.c_size_t(0)
-    rc = _lib.load().dpso_workspace_size(ctypes.byref(s._params()), 20000,
+    # 10 bytes per node (n > 6000): 30000 nodes need 300 KB
+    rc = _lib.load().dpso_workspace_size(ctypes.byref(s._params()), 30000,
                                          ctypes.byref(nbytes))
     assert rc != 0
     msg = _lib.load().dpso_last_error().decode()
@@ -323,3 +324,46 @@ def test_parallel_init_walk_matches_serial(pkg, monkeypatch, n, P, frac, rs):
         trace = []
         orc.fit(cost, trace=trace)
         assert states["parallel"]["x"].tolist() == trace[0][1].x
+
+
+@pytest.mark.gpu
+def test_lowmem_update_large_n(pkg, monkeypatch):
+    # the 10-byte-per-node update (default for n > 14000; forced here by
+    # DPSO_UPD_LOWMEM at n = 6500: targets read through the cache, sigma
+    # folded into vmap in global memory): the same swarm state as the
+    # 16-byte kernel generation by generation, and the oracle's after one
+    # generation
+    from paper_1706_04399_b200.solver import numpy_stream_states
+    n, P, G = 6500, 12, 4
+    cost = random_euclidean_matrix(n, np.random.default_rng(65))
+    params = dict(n_particles=P, max_generations=G, stall_generations=G,
+                  random_state=3, mutation_period=2)
+    states = {}
+    for kind in ("low", "full"):
+        if kind == "low":
+            monkeypatch.setenv("DPSO_UPD_LOWMEM", "1")
+        else:
+            monkeypatch.delenv("DPSO_UPD_LOWMEM", raising=False)
+        s = pkg.DiscreteSwarmSolver(**params)
+        ctx = s._make_context(cost)
+        try:
+            ctx.set_streams(numpy_stream_states(3, P + 2))
+            ctx.init(None, 0)
+            seq = []
+            for _ in range(G):
+                ctx.step(1)
+                seq.append(ctx.state())
+            states[kind] = seq
+        finally:
+            ctx.close()
+    for a, b in zip(states["low"], states["full"]):
+        for key in ("x", "pbest", "fit", "pfit", "vmap", "gbest"):
+            assert np.array_equal(a[key], b[key]), key
+    orc = O.OracleSolver(**dict(params, max_generations=1,
+                                stall_generations=1))
+    trace = []
+    orc.fit(cost, trace=trace)
+    _, st, gbest, gfit = trace[1]
+    assert states["low"][0]["x"].tolist() == st.x
+    assert states["low"][0]["vmap"].tolist() == st.vmap
+    assert states["low"][0]["fit"].tolist() == st.fit
