@@ -353,8 +353,11 @@ __device__ __noinline__ float scan_hit(float u0, float u1, float u2, float u3,
   float best = st[0];
   if (MODE == 1) {
     int bi = __float_as_int(st[32]), bj = __float_as_int(st[64]);
+    // lb == -inf: the pass has no row i+1 (its values are not pairs)
+    const int gend = lb == -__int_as_float(0x7f800000) ? 4 : 8;
 #pragma unroll
     for (int g = 0; g < 8; ++g) {
+      if (g >= gend) break;
       const int ii = i + (g >> 2), jj = j0 + jstep * (g & 3);
       const float t = __fsub_rn(uv[g], g < 4 ? da : db);  // exact
       if (lex_less(t, ii, jj, best, bi, bj)) {

@@ -367,3 +367,19 @@ def test_lowmem_update_large_n(pkg, monkeypatch):
     assert states["low"][0]["x"].tolist() == st.x
     assert states["low"][0]["vmap"].tolist() == st.vmap
     assert states["low"][0]["fit"].tolist() == st.fit
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", [None, "/rows32", "exact32", "fp64"])
+def test_best_exchange_nonmetric_integer(pkg, mode, monkeypatch):
+    # integer, asymmetric, far from metric (EXACT32 scan): no structure for
+    # the scan to lean on; many tours so the row bands take every parity
+    set_scan_mode(monkeypatch, mode)
+    rng = np.random.default_rng(31)
+    for n in (37, 130, 301, 700):
+        cost = rng.integers(0, 1000, size=(n, n)).astype(float)
+        cost[rng.random((n, n)) < 0.3] = 0.0
+        np.fill_diagonal(cost, 0.0)
+        tours = np.array([rng.permutation(n) for _ in range(48)],
+                         dtype=np.int32)
+        check_batch(pkg, cost, tours, ("nonmetric", n, mode))
