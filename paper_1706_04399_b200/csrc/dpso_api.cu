@@ -107,8 +107,9 @@ Layout make_layout(const dpso_params* prm, int n) {
   L.off_dcache = take(8 * P * np);
   L.off_gbest = take(2 * np);
   L.off_conv = take(8 * ((int64_t)prm->max_generations + 1));
-  // partial argmins, then the FILTER32 overflow list (count + tasks)
-  L.off_tores = take(sizeof(TwoOptRes) * P * L.chunks + 4 * (1 + P * L.chunks));
+  // partial argmins, the FILTER32 overflow list (count + tasks), the scan's
+  // task counter
+  L.off_tores = take(sizeof(TwoOptRes) * P * L.chunks + 4 * (2 + P * L.chunks));
   L.off_chunk_tab = take(16 * L.chunks);
   L.off_rank = take(4 * P);
   L.off_hash = take(8 * P);
@@ -856,7 +857,7 @@ int dpso_best_exchange_batch(const double* dev_cost, int64_t ld, int32_t n,
   two_opt_chunk_table(n, chunks, tab.data());
   const int64_t cnt = std::max(count, 1);
   size_t bytes = round_up(2 * np * cnt, 256) + round_up(8 * np * cnt, 256) +
-                 round_up(sizeof(TwoOptRes) * chunks * cnt + 4 * (1 + chunks * cnt), 256) +
+                 round_up(sizeof(TwoOptRes) * chunks * cnt + 4 * (2 + chunks * cnt), 256) +
                  round_up(16 * chunks, 256) + round_up(8 * cnt, 256) +
                  round_up(6 * (int64_t)n * np, 256) + 256;  // fp32 + fp16 rows
   unsigned char* tmp = nullptr;
@@ -870,7 +871,7 @@ int dpso_best_exchange_batch(const double* dev_cost, int64_t ld, int32_t n,
   uint16_t* t16 = (uint16_t*)take(2 * np * cnt);
   double* dc = (double*)take(8 * np * cnt);
   TwoOptRes* res = (TwoOptRes*)take(sizeof(TwoOptRes) * chunks * cnt +
-                                    4 * (1 + chunks * cnt));
+                                    4 * (2 + chunks * cnt));
   int32_t* ctab = (int32_t*)take(16 * chunks);
   double* fsum = (double*)take(8 * cnt);
   float* c32 = (float*)take(6 * (int64_t)n * np);

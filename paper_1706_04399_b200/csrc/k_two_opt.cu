@@ -38,6 +38,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <stdio.h>
+
 #include <algorithm>
 #include <vector>
 
@@ -76,6 +78,7 @@ struct ScanArgs {
   int64_t row_pitch;       // bytes between staged rows
   float dscale;            // d values -> row units (power of two)
   int32_t* ovf;            // FILTER32 overflow list: [0] count, [1..] tasks
+  int32_t* task_ctr;       // fp32 scan: next task (persistent warps)
   int stream_only;         // debug: stream the rows, skip the pair compute
 };
 
@@ -438,7 +441,7 @@ __device__ __noinline__ float scan_hit(float u0, float u1, float u2, float u3,
 #ifndef DPSO_SCAN_MINB
 #define DPSO_SCAN_MINB 5
 #endif
-template <int NPL, int MODE, int ES>
+template <int NPL, int MODE, int ES, bool PERSIST>
 __global__ void __launch_bounds__(kW32 * 32, DPSO_SCAN_MINB)
     k_two_opt_scan32(ScanArgs a) {
   if (a.ctl && (a.ctl->done || a.ctl->improved)) return;
@@ -448,9 +451,34 @@ __global__ void __launch_bounds__(kW32 * 32, DPSO_SCAN_MINB)
   __shared__ float s_cd[kW32][kCand][32];
   __shared__ float s_st[kW32][3][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int task = blockIdx.x * (blockDim.x >> 5) + warp;
+  uint64_t* wb = bars[warp];
+  if (lane == 0) {
+    mbar_init(&wb[0], 1);
+    mbar_init(&wb[1], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  uint32_t ph = 0;  // phase bit per pair (bit 0: pair 0, bit 1: pair 1)
+  // Persistent warps: tasks are taken from a counter until none is left, so
+  // the grid is one resident wave and the tail is at most one task per warp.
+  // Every row a task issues is waited by the task itself, so the ring and
+  // the barrier phases carry over cleanly.
+  // (PERSIST false: one task per warp, task = global warp index - the
+  // launch has a warp for every task; measured faster when each particle is
+  // one task, C3)
+  const int ntasks = a.count * a.chunks;
+  for (int it = 0;; ++it) {
+  __syncwarp();
+  int task = 0;
+  if (PERSIST) {
+    if (lane == 0) task = atomicAdd(a.task_ctr, 1);
+    task = __shfl_sync(0xffffffffu, task, 0);
+  } else {
+    if (it > 0) break;
+    task = blockIdx.x * (blockDim.x >> 5) + warp;
+  }
+  if (task >= ntasks) break;
   const int p = task / a.chunks, c = task % a.chunks;
-  if (p >= a.count) return;
   const int n = a.n;
   const int4 tb = reinterpret_cast<const int4*>(a.chunk_tab)[c];
   const int r0 = tb.x, r1 = tb.y, jlo = tb.z, jhi = tb.w;
@@ -463,7 +491,7 @@ __global__ void __launch_bounds__(kW32 * 32, DPSO_SCAN_MINB)
   st[64] = __int_as_float(MODE == 1 ? 0x7fffffff : 0);
   if (r0 >= r1) {
     if (lane == 0) *out = {kInf, 0x7fffffff, 0x7fffffff};
-    return;
+    continue;
   }
   const uint16_t* tour = a.tours + (size_t)p * a.np;
   const double* dg = a.dcache + (size_t)p * a.np;
@@ -509,7 +537,6 @@ __global__ void __launch_bounds__(kW32 * 32, DPSO_SCAN_MINB)
   // sit in one pair (B2 one slot after B1) and arrive on one barrier; the
   // next pass's rows fill the other pair.  The prime row a_r0 uses pair 1
   // before pass 1 refills it.
-  uint64_t* wb = bars[warp];
   auto issue2 = [&](int pair, int ca, int cb2, int nr) {  // nr rows: 1 or 2
     mbar_expect_tx(&wb[pair], (uint32_t)nr * a.row_bytes);
     unsigned char* dst = wbase + (size_t)(2 * pair) * a.buf_stride;
@@ -520,14 +547,10 @@ __global__ void __launch_bounds__(kW32 * 32, DPSO_SCAN_MINB)
                a.row_bytes, &wb[pair]);
   };
   if (lane == 0) {
-    mbar_init(&wb[0], 1);
-    mbar_init(&wb[1], 1);
-    fence_barrier_init();
     issue2(1, tour[r0], 0, 1);                                 // prime row
     issue2(0, tour[r0 + 1], nrows > 2 ? tour[r0 + 2] : 0,      // pass 0
            nrows > 2 ? 2 : 1);
   }
-  uint32_t ph = 0;  // phase bit per pair (bit 0: pair 0, bit 1: pair 1)
   // Per-pass scalars from lane-parallel loads of 32 rows at a time, one
   // block ahead: cb = the cities of ring rows 3 + k (+1), db = d_{r0 + k}.
   auto city_at = [&](int q) -> int {
@@ -715,7 +738,7 @@ __global__ void __launch_bounds__(kW32 * 32, DPSO_SCAN_MINB)
     int bi = __float_as_int(st[32]), bj = __float_as_int(st[64]);
     warp_argmin(bd, bi, bj);
     if (lane == 0) *out = {bd, bi, bj};
-    return;
+    continue;
   }
   // FILTER32: warp minimum, candidate re-evaluation in fp64
   const float best = st[0];
@@ -725,7 +748,7 @@ __global__ void __launch_bounds__(kW32 * 32, DPSO_SCAN_MINB)
       *out = {kInf, kOverflowTag, kOverflowTag};
       a.ovf[1 + atomicAdd(&a.ovf[0], 1)] = task;
     }
-    return;
+    continue;
   }
   float m = best;
 #pragma unroll
@@ -781,6 +804,7 @@ __global__ void __launch_bounds__(kW32 * 32, DPSO_SCAN_MINB)
   }
   warp_argmin(bd, ei, ej);
   if (lane == 0) *out = {bd, ei, ej};
+  }  // task loop
 }
 
 struct ApplyArgs {
@@ -910,9 +934,28 @@ cudaError_t launch_scan64_t(const ScanArgs& a, int warps, int blocks,
 template <int NPL, int MODE, int ES>
 cudaError_t launch_scan32_t(const ScanArgs& a, int warps, int blocks,
                             size_t smem, cudaStream_t s) {
-  auto k = k_two_opt_scan32<NPL, MODE, ES>;
+  if (a.chunks == 1 || getenv("DPSO_SCAN_NOPERSIST")) {
+    auto k = k_two_opt_scan32<NPL, MODE, ES, false>;
+    cudaError_t e = set_dyn_smem((const void*)k, smem);
+    if (e != cudaSuccess) return e;
+    k<<<blocks, warps * 32, smem, s>>>(a);
+    return cudaGetLastError();
+  }
+  auto k = k_two_opt_scan32<NPL, MODE, ES, true>;
   cudaError_t e = set_dyn_smem((const void*)k, smem);
   if (e != cudaSuccess) return e;
+  // one resident wave of persistent warps
+  int per_sm = 0, dev = 0, sms = 148;
+  static const int mult = [] {  // resident waves launched (testing knob)
+    const char* e = getenv("DPSO_SCAN_WAVES");
+    return e ? std::max(1, atoi(e)) : 1;
+  }();
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, warps * 32,
+                                                    smem) == cudaSuccess &&
+      per_sm > 0 && cudaGetDevice(&dev) == cudaSuccess &&
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) ==
+          cudaSuccess)
+    blocks = std::min(blocks, per_sm * sms * mult);
   k<<<blocks, warps * 32, smem, s>>>(a);
   return cudaGetLastError();
 }
@@ -1035,7 +1078,7 @@ int two_opt_pick_chunks(int32_t n, int32_t P) {
   const int64_t slots = (int64_t)sms * warps_per_sm;
   const int R = column_ranges(n);
   // tasks per resident warp slot: balances the tail against per-task setup
-  int per_slot = 3;
+  int per_slot = 6;
   if (const char* e = getenv("DPSO_TASKS_PER_SLOT")) per_slot = std::max(1, atoi(e));
   int chunks = (int)((per_slot * slots + P - 1) / P);
   chunks = std::max(chunks, R);
@@ -1167,7 +1210,9 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
                                  round_up((int64_t)32 * npl32 * 4, 128));
       const int warps = kW32;
       const size_t smem = (size_t)warps * a.buf_stride2;
-      if (pl.mode == kScanFilter32) e = cudaMemsetAsync(a.ovf, 0, 4, s);
+      a.task_ctr = a.ovf + 1 + tasks;
+      e = cudaMemsetAsync(a.task_ctr, 0, 4, s);
+      if (!e && pl.mode == kScanFilter32) e = cudaMemsetAsync(a.ovf, 0, 4, s);
       if (e != cudaSuccess) return e;
       const int blocks = (int)((tasks + warps - 1) / warps);
 #define SCAN32(NPL)                                                      \
