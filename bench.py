@@ -323,10 +323,11 @@ def run_ours(args, cfg_name, cfg):
             flush.fill_(k & 0xFF)
             ev[k][0].record(stream)
             ctx.step(1)
-            ev[k][1].record(stream)
             if ex is not None and (k + 1) % args.exchange_every == 0:
-                torch.cuda.synchronize()
-                ex.exchange()
+                # island gbest exchange, inside the timed step; stream-
+                # ordered (pack, NCCL all_gather, adopt): no host sync
+                ex.exchange_device()
+            ev[k][1].record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

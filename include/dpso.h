@@ -135,6 +135,19 @@ int dpso_set_state(dpso_ctx* ctx, const int32_t* x, const int32_t* pbest,
  * better; the host layer moves the 16-byte records and tours with NCCL. */
 int dpso_offer_gbest(dpso_ctx* ctx, const int32_t* host_tour, double fitness);
 
+/* Island exchange on the device, stream-ordered, no host synchronisation
+ * (SURVEY §8(e)).  A record is (gbest fitness f64, rank i64, gbest tour
+ * u16[round_up(n, 8)]) = dpso_island_record_bytes(n) bytes.
+ * dpso_island_pack writes this island's record into dev_record;
+ * after an all_gather of the records of all `world` ranks (NCCL on the
+ * same stream), dpso_island_adopt picks the winner - smallest fitness,
+ * lowest rank on ties - and adopts its tour iff it is another rank's and
+ * strictly better than this island's gbest (as dpso_offer_gbest). */
+int64_t dpso_island_record_bytes(int32_t n);
+int dpso_island_pack(dpso_ctx* ctx, void* dev_record, int32_t rank);
+int dpso_island_adopt(dpso_ctx* ctx, const void* dev_records, int32_t world,
+                      int32_t rank);
+
 void dpso_destroy(dpso_ctx* ctx);
 const char* dpso_last_error(void);
 

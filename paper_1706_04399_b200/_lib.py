@@ -57,6 +57,9 @@ _SIG = {
     "dpso_get_state": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P]),
     "dpso_set_state": (_I32, [_P, _P, _P, _P, _P, _P, _P, ctypes.c_double]),
     "dpso_offer_gbest": (_I32, [_P, _P, ctypes.c_double]),
+    "dpso_island_record_bytes": (_I64, [_I32]),
+    "dpso_island_pack": (_I32, [_P, _P, _I32]),
+    "dpso_island_adopt": (_I32, [_P, _P, _I32, _I32]),
     "dpso_destroy": (None, [_P]),
     "dpso_last_error": (ctypes.c_char_p, []),
     "dpso_tour_cost_batch": (_I32, [_P, _I64, _I32, _P, _I32, _P, _P]),

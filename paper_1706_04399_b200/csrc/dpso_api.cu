@@ -786,6 +786,30 @@ int dpso_offer_gbest(dpso_ctx* c, const int32_t* tour, double fitness) {
   return DPSO_OK;
 }
 
+int64_t dpso_island_record_bytes(int32_t n) {
+  return island_rec_bytes((int)round_up(n, 8));
+}
+
+int dpso_island_pack(dpso_ctx* c, void* dev_record, int32_t rank) {
+  if (!c || !dev_record) return fail(DPSO_EINVAL, "null argument");
+  if (!c->initialized) return fail(DPSO_EINVAL, "context not initialized");
+  int rc = sync_in(c);
+  if (rc) return rc;
+  CK(launch_island_pack(c->v, dev_record, rank, c->stream));
+  return sync_out(c);
+}
+
+int dpso_island_adopt(dpso_ctx* c, const void* dev_records, int32_t world,
+                      int32_t rank) {
+  if (!c || !dev_records || world < 1 || rank < 0 || rank >= world)
+    return fail(DPSO_EINVAL, "bad arguments");
+  if (!c->initialized) return fail(DPSO_EINVAL, "context not initialized");
+  int rc = sync_in(c);
+  if (rc) return rc;
+  CK(launch_island_adopt(c->v, dev_records, world, rank, c->stream));
+  return sync_out(c);
+}
+
 void dpso_destroy(dpso_ctx* c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);

@@ -172,6 +172,11 @@ cudaError_t launch_finalize(const SwarmView& v, cudaStream_t s);
 cudaError_t launch_init(const SwarmView& v, const uint16_t* dev_seed,
                         int32_t n_seed, cudaStream_t s, int* path);
 cudaError_t launch_init_best(const SwarmView& v, cudaStream_t s);
+int64_t island_rec_bytes(int np);
+cudaError_t launch_island_pack(const SwarmView& v, void* rec, int rank,
+                               cudaStream_t s);
+cudaError_t launch_island_adopt(const SwarmView& v, const void* recs,
+                                int world, int rank, cudaStream_t s);
 
 // generic batch kernels (kernel-level ABI and internal reuse)
 cudaError_t launch_tour_cost_rows(const double* cost, int64_t ld, int32_t n,

@@ -178,6 +178,57 @@ __global__ void __launch_bounds__(kRed) k_finalize(SwarmView v) {
   }
 }
 
+// ---- island exchange on the device ---------------------------
+// Record of one island: gbest fitness (fp64), rank (i64), gbest tour (np
+// u16).  Every rank packs its record, an all_gather (NCCL, stream-ordered)
+// concatenates them, and k_island_adopt picks the winner - smallest
+// fitness, lowest rank on ties - and adopts its tour iff strictly better
+// than the island's own gbest.  No host synchronisation anywhere.
+struct IslandRec {
+  double fit;
+  int64_t rank;
+};
+
+__global__ void k_island_pack(SwarmView v, unsigned char* rec, int rank) {
+  IslandRec* h = reinterpret_cast<IslandRec*>(rec);
+  uint16_t* t = reinterpret_cast<uint16_t*>(rec + sizeof(IslandRec));
+  if (threadIdx.x == 0) {
+    h->fit = v.ctl->gbest_fit;
+    h->rank = rank;
+  }
+  for (int i = threadIdx.x; i < v.np; i += blockDim.x)
+    t[i] = i < v.n ? v.gbest[i] : (uint16_t)0;
+}
+
+__global__ void k_island_adopt(SwarmView v, const unsigned char* recs,
+                               int64_t rec_bytes, int world, int rank) {
+  __shared__ int s_win;
+  __shared__ double s_fit;
+  if (threadIdx.x == 0) {
+    int win = -1;
+    double wf = 0.0;
+    int64_t wr = 0;
+    for (int r = 0; r < world; ++r) {
+      const IslandRec* h =
+          reinterpret_cast<const IslandRec*>(recs + (size_t)r * rec_bytes);
+      if (win < 0 || h->fit < wf || (h->fit == wf && h->rank < wr)) {
+        win = r;
+        wf = h->fit;
+        wr = h->rank;
+      }
+    }
+    const bool adopt = wr != rank && wf < v.ctl->gbest_fit;
+    s_win = adopt ? win : -1;
+    s_fit = wf;
+  }
+  __syncthreads();
+  if (s_win < 0) return;
+  const uint16_t* t = reinterpret_cast<const uint16_t*>(
+      recs + (size_t)s_win * rec_bytes + sizeof(IslandRec));
+  for (int i = threadIdx.x; i < v.n; i += blockDim.x) v.gbest[i] = t[i];
+  if (threadIdx.x == 0) v.ctl->gbest_fit = s_fit;
+}
+
 // ---- init (numpy streams) --------------------------------------------------
 
 // ---- init stream walk over a generated window buffer -----------------------
@@ -918,6 +969,23 @@ cudaError_t launch_pysum_tour(const double* cost, int64_t ld, int32_t n,
                               const int32_t* body, double* out,
                               cudaStream_t s) {
   k_pysum_tour<<<1, 32, 0, s>>>(cost, ld, n, body, out);
+  return cudaGetLastError();
+}
+
+int64_t island_rec_bytes(int np) {
+  return (int64_t)sizeof(IslandRec) + round_up(2 * (int64_t)np, 16);
+}
+
+cudaError_t launch_island_pack(const SwarmView& v, void* rec, int rank,
+                               cudaStream_t s) {
+  k_island_pack<<<1, 256, 0, s>>>(v, (unsigned char*)rec, rank);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_island_adopt(const SwarmView& v, const void* recs,
+                                int world, int rank, cudaStream_t s) {
+  k_island_adopt<<<1, 256, 0, s>>>(v, (const unsigned char*)recs,
+                                   island_rec_bytes(v.np), world, rank);
   return cudaGetLastError();
 }
 

@@ -11,6 +11,13 @@ gbest migration:
 Latency-bound (tens of microseconds over NVLink); amortised over K
 generations.  Works with any torch.distributed backend (NCCL on the GPU box,
 gloo in the CPU tests).
+
+``exchange_device`` is the same exchange without a host round trip (NCCL):
+each island packs (gbest fitness, rank, gbest tour) into a device record
+(``dpso_island_pack``), one ``all_gather_into_tensor`` concatenates the
+records of all ranks on the stream, and ``dpso_island_adopt`` picks the
+winner and adopts it on the device - so generations keep streaming while
+the exchange runs.
 """
 from __future__ import annotations
 
@@ -64,3 +71,18 @@ class IslandExchange:
             self.ctx.offer_gbest(buf.cpu().numpy(), wfit)
             self.adopted += 1
         return winner, wfit
+
+    def exchange_device(self) -> None:
+        """Stream-ordered exchange (needs ``ctx.island_pack/adopt`` and a
+        backend whose tensors live on the GPU, i.e. NCCL)."""
+        torch, dist = self.torch, self.dist
+        if not hasattr(self, "_rec"):
+            nbytes = self.ctx.island_record_bytes()
+            self._rec = torch.empty(nbytes, dtype=torch.uint8,
+                                    device=self.device)
+            self._recs = torch.empty(nbytes * self.world, dtype=torch.uint8,
+                                     device=self.device)
+        self.ctx.island_pack(self._rec, self.rank)
+        dist.all_gather_into_tensor(self._recs, self._rec, group=self.group)
+        self.ctx.island_adopt(self._recs, self.world, self.rank)
+        self.exchanges += 1

@@ -255,6 +255,17 @@ class SwarmContext:
         _lib.check(self.lib.dpso_offer_gbest(
             self.h, arr.ctypes.data_as(ctypes.c_void_p), float(fitness)))
 
+    def island_record_bytes(self) -> int:
+        return int(self.lib.dpso_island_record_bytes(self.n))
+
+    def island_pack(self, dev_record, rank: int) -> None:
+        _lib.check(self.lib.dpso_island_pack(self.h, dev_record.data_ptr(),
+                                             int(rank)))
+
+    def island_adopt(self, dev_records, world: int, rank: int) -> None:
+        _lib.check(self.lib.dpso_island_adopt(
+            self.h, dev_records.data_ptr(), int(world), int(rank)))
+
     def close(self) -> None:
         if getattr(self, "h", None):
             self.lib.dpso_destroy(self.h)

@@ -383,3 +383,94 @@ def test_best_exchange_nonmetric_integer(pkg, mode, monkeypatch):
         tours = np.array([rng.permutation(n) for _ in range(48)],
                          dtype=np.int32)
         check_batch(pkg, cost, tours, ("nonmetric", n, mode))
+
+
+@pytest.mark.gpu
+def test_island_adopt_on_device(pkg):
+    # dpso_island_pack / dpso_island_adopt without NCCL: records of two
+    # "other ranks" written by hand; the winner (smallest fitness, lowest
+    # rank on ties) is adopted iff it is another rank's and strictly better
+    import torch
+    from paper_1706_04399_b200.solver import numpy_stream_states
+    n, P = 30, 16
+    cost = random_euclidean_matrix(n, np.random.default_rng(4))
+    s = pkg.DiscreteSwarmSolver(n_particles=P, max_generations=3,
+                                stall_generations=3, random_state=1)
+    ctx = s._make_context(cost)
+    try:
+        ctx.set_streams(numpy_stream_states(1, P + 2))
+        ctx.init(None, 0)
+        ctx.step(2)
+        nb = ctx.island_record_bytes()
+        assert nb == 16 + (2 * 32 + 15) // 16 * 16
+        recs = torch.zeros(3 * nb, dtype=torch.uint8, device="cuda")
+        ctx.island_pack(recs[nb:2 * nb], 1)  # this island is rank 1
+        own = ctx.state()
+        mine = recs[nb:2 * nb].cpu().numpy()
+        assert mine[:8].view(np.float64)[0] == own["gbest_fit"]
+        assert mine[8:16].view(np.int64)[0] == 1
+        assert mine[16:16 + 2 * n].view(np.uint16).tolist() == \
+            own["gbest"].tolist()
+        other = np.random.default_rng(9).permutation(n)
+
+        def put(r, fit, tour):
+            b = np.zeros(nb, np.uint8)
+            b[:8] = np.frombuffer(np.float64(fit).tobytes(), np.uint8)
+            b[8:16] = np.frombuffer(np.int64(r).tobytes(), np.uint8)
+            b[16:16 + 2 * n] = np.frombuffer(
+                tour.astype(np.uint16).tobytes(), np.uint8)
+            recs[r * nb:(r + 1) * nb] = torch.from_numpy(b).cuda()
+        # rank 2 ties rank 0 below ours: rank 0 wins the tie and is adopted
+        put(0, own["gbest_fit"] - 1.0, other)
+        put(2, own["gbest_fit"] - 1.0, other[::-1].copy())
+        ctx.island_adopt(recs, 3, 1)
+        got = ctx.state()
+        assert got["gbest_fit"] == own["gbest_fit"] - 1.0
+        assert got["gbest"].tolist() == other.tolist()
+        # nobody better now (our own record wins): nothing changes
+        ctx.island_pack(recs[nb:2 * nb], 1)
+        put(0, got["gbest_fit"] + 5.0, np.arange(n))
+        put(2, got["gbest_fit"], np.arange(n))
+        ctx.island_adopt(recs, 3, 1)
+        assert ctx.state()["gbest"].tolist() == other.tolist()
+        ctx.step(1)  # the swarm carries on from the adopted gbest
+    finally:
+        ctx.close()
+
+
+@pytest.mark.gpu
+def test_island_exchange_device_nccl_single_rank(pkg):
+    # the stream-ordered exchange through a real NCCL group (one rank: the
+    # box has one GPU); its own record wins, so nothing is adopted
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_1706_04399_b200.islands import IslandExchange
+    from paper_1706_04399_b200.solver import numpy_stream_states
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}",
+                            rank=0, world_size=1)
+    try:
+        n, P = 40, 16
+        cost = random_euclidean_matrix(n, np.random.default_rng(6))
+        s = pkg.DiscreteSwarmSolver(n_particles=P, max_generations=4,
+                                    stall_generations=4, random_state=2)
+        ctx = s._make_context(cost)
+        try:
+            ctx.set_streams(numpy_stream_states(2, P + 2))
+            ctx.init(None, 0)
+            ctx.step(2)
+            before = ctx.state()
+            ex = IslandExchange(ctx, n)
+            ex.exchange_device()
+            ctx.step(1)
+            torch.cuda.synchronize()
+            assert ex.exchanges == 1
+            assert ctx.state()["gbest_fit"] <= before["gbest_fit"]
+        finally:
+            ctx.close()
+    finally:
+        dist.destroy_process_group()
