@@ -474,3 +474,4 @@ def test_island_exchange_device_nccl_single_rank(pkg):
             ctx.close()
     finally:
         dist.destroy_process_group()
+
