@@ -198,7 +198,9 @@ struct dpso_ctx {
   cudaStream_t stream;
   cudaStream_t stream2;  // fork for the mutation-stream walk
   cudaEvent_t ev, ev_fork, ev_join;
-  cudaGraphExec_t graph;
+  cudaGraphExec_t graph;        // a generation with the mutation call
+  cudaGraphExec_t graph_plain;  // a generation without it (gen % period)
+  int64_t gen_next = 1;         // generation the next launch runs
   bool have_cost, have_streams, initialized;
   SwarmView v;
   DevCtl* host_ctl;  // pinned
@@ -222,7 +224,8 @@ static const char* g_stage = "";
 // forked stream (s2) concurrently with the update and the dedupe pipeline.
 static cudaError_t enqueue_generation(const SwarmView& v, cudaStream_t s,
                                       cudaStream_t s2, cudaEvent_t fork,
-                                      cudaEvent_t join) {
+                                      cudaEvent_t join,
+                                      bool with_mutation = true) {
   cudaError_t e;
 #define STAGE(name, call)      \
   do {                         \
@@ -231,7 +234,8 @@ static cudaError_t enqueue_generation(const SwarmView& v, cudaStream_t s,
   } while (0)
   STAGE("gen_begin", launch_gen_begin(v, s));
   STAGE("update", launch_update(v, s));
-  if (v.use_mutation) {
+  const bool mut = v.use_mutation && with_mutation;
+  if (mut) {
     STAGE("mutation_pre", launch_mutation_pre(v, s));
     STAGE("mutation_post", launch_mutation_post(v, s));
     // the next call's stream walk overlaps the rest of this generation
@@ -248,7 +252,7 @@ static cudaError_t enqueue_generation(const SwarmView& v, cudaStream_t s,
   } else {
     STAGE("select+finalize", launch_select(v, true, s));
   }
-  if (v.use_mutation) STAGE("join", cudaStreamWaitEvent(s, join, 0));
+  if (mut) STAGE("join", cudaStreamWaitEvent(s, join, 0));
 #undef STAGE
   g_stage = "";
   return cudaSuccess;
@@ -353,6 +357,7 @@ int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
   c->ws = (unsigned char*)dev_workspace;
   c->user = (cudaStream_t)cuda_stream;
   c->graph = nullptr;
+  c->graph_plain = nullptr;
   c->have_cost = c->have_streams = c->initialized = false;
   cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
   if (e) {
@@ -470,6 +475,10 @@ int dpso_set_cost(dpso_ctx* c, const double* dev_cost, int64_t ld) {
     cudaGraphExecDestroy(c->graph);
     c->graph = nullptr;
   }
+  if (c->graph_plain) {
+    cudaGraphExecDestroy(c->graph_plain);
+    c->graph_plain = nullptr;
+  }
   return DPSO_OK;
 }
 
@@ -528,26 +537,49 @@ int dpso_init(dpso_ctx* c, const int32_t* seed_body, int32_t n_seed) {
   CK(launch_init_best(c->v, c->stream));
   // stream walk of the first mutation call
   if (c->v.use_mutation) CK(launch_mutation_walk(c->v, c->stream));
+  c->gen_next = 1;  // init leaves the device at generation 0
   c->initialized = true;
   return sync_out(c);
 }
 
-static int ensure_graph(dpso_ctx* c) {
-  if (c->graph) return DPSO_OK;
+// Two graphs: a generation that runs the mutation call and one that does
+// not (gen % mutation_period != 0: the mutation kernels would only exit at
+// entry).  The host knows which generation each launch runs (gen_next; a
+// generation after the stall break is a no-op either way).
+static int capture_generation(dpso_ctx* c, bool with_mutation,
+                              cudaGraphExec_t* out) {
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   cudaError_t e = enqueue_generation(c->v, c->stream, c->stream2, c->ev_fork,
-                                     c->ev_join);
+                                     c->ev_join, with_mutation);
   cudaError_t e2 = cudaStreamEndCapture(c->stream, &g);
   if (e) {
     std::string where = std::string("capture generation (") + g_stage + ")";
     return cuda_fail(e, where.c_str());
   }
   if (e2) return cuda_fail(e2, "cudaStreamEndCapture");
-  e = cudaGraphInstantiate(&c->graph, g, 0);
+  e = cudaGraphInstantiate(out, g, 0);
   cudaGraphDestroy(g);
   if (e) return cuda_fail(e, "cudaGraphInstantiate");
   return DPSO_OK;
+}
+
+static int ensure_graph(dpso_ctx* c) {
+  if (c->graph) return DPSO_OK;
+  int rc = capture_generation(c, true, &c->graph);
+  if (rc) return rc;
+  if (c->v.use_mutation && c->v.mutation_period > 1 &&
+      !getenv("DPSO_ONE_GRAPH")) {
+    rc = capture_generation(c, false, &c->graph_plain);
+    if (rc) return rc;
+  }
+  return DPSO_OK;
+}
+
+static cudaError_t launch_generation(dpso_ctx* c) {
+  const int64_t g = c->gen_next++;
+  const bool mut = !c->graph_plain || (g % c->v.mutation_period == 0);
+  return cudaGraphLaunch(mut ? c->graph : c->graph_plain, c->stream);
 }
 
 int dpso_step(dpso_ctx* c, int32_t gens) {
@@ -555,7 +587,7 @@ int dpso_step(dpso_ctx* c, int32_t gens) {
   int rc = ensure_graph(c);
   if (rc) return rc;
   if ((rc = sync_in(c))) return rc;
-  for (int g = 0; g < gens; ++g) CK(cudaGraphLaunch(c->graph, c->stream));
+  for (int g = 0; g < gens; ++g) CK(launch_generation(c));
   return sync_out(c);
 }
 
@@ -604,6 +636,7 @@ int dpso_step_timed(dpso_ctx* c, int32_t gens, double* phase_ms,
     }
   }
   for (int i = 0; i < 7; ++i) cudaEventDestroy(ev[i]);
+  c->gen_next += gens;
   if (phase_ms)
     for (int i = 0; i < 6; ++i) phase_ms[i] = acc[i];
   if (two_opt_count) {
@@ -645,7 +678,7 @@ int dpso_run(dpso_ctx* c, int32_t* gens_run) {
   int batch = 4;
   while (launched < G) {
     const int b = std::min(batch, G - launched);
-    for (int g = 0; g < b; ++g) CK(cudaGraphLaunch(c->graph, c->stream));
+    for (int g = 0; g < b; ++g) CK(launch_generation(c));
     launched += b;
     CK(cudaMemcpyAsync(c->host_ctl, c->v.ctl, sizeof(DevCtl),
                        cudaMemcpyDeviceToHost, c->stream));
@@ -814,6 +847,7 @@ void dpso_destroy(dpso_ctx* c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->graph) cudaGraphExecDestroy(c->graph);
+  if (c->graph_plain) cudaGraphExecDestroy(c->graph_plain);
   if (c->ev) cudaEventDestroy(c->ev);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
