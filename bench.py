@@ -263,7 +263,7 @@ def kernels_per_generation(cfg):
     a graph without the mutation call; device flags make kernels a
     generation does not need (the 2-opt scan when gbest improved, ...) exit
     at entry, but they still launch."""
-    k = 1 + 1 + 2  # gen_begin, update, fitness + pbest copy
+    k = 1 + 1 + 1  # gen_begin, update, fitness (with the pbest copy)
     k += 1         # select
     if cfg.get("ee", True):
         # scan (FILTER32 adds the overflow re-scan), apply, finalize
@@ -274,7 +274,7 @@ def kernels_per_generation(cfg):
         m += 1     # Philox sampler
     else:
         m += 2 + 2  # sampler + fix; stream gen + walk (forked stream)
-    m += 1 + 2     # swap, then fitness + pbest copy of the mutated
+    m += 1 + 1     # swap, then fitness (+ pbest copy) of the mutated
     return k, m
 
 

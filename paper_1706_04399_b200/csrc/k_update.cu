@@ -221,9 +221,9 @@ __device__ void sigma_pass(const uint16_t* __restrict__ tgt_g, double c,
 }
 
 // x' is in sx: write x and the edge costs d_i (dcache).  The fitness and
-// pbest (solver.py:217-220) follow in k_fitness / k_pbest_copy, one thread
-// per particle, so the sequential fp64 sums of all particles run
-// concurrently instead of on one thread of each CTA.
+// pbest (solver.py:217-220) follow in k_fitness, one warp per particle, so
+// the sequential fp64 sums of all particles run concurrently instead of on
+// one thread of each CTA.
 // sold (nullable): the tour before the move; an edge whose two endpoints
 // are unchanged keeps its cached cost (no gather, no store)
 template <int T>
@@ -443,6 +443,11 @@ __global__ void __launch_bounds__(32) k_update_seq(SwarmView v) {
 constexpr int kFitChunk = 256;  // doubles per chunk (2 KiB)
 constexpr int kFitWarps = 4;    // particles per CTA
 
+__device__ __noinline__ int fitness_lane0(const SwarmView& v, int p, int warp,
+                                          bool init,
+                                          double (*s_buf)[2][kFitChunk],
+                                          uint64_t (*s_bar)[2]);
+
 // use_list: 0 = every particle, 1 = the mutation's event list, 2 = init
 // (every particle, fit = pfit, no control-block checks: the block is only
 // written by k_init_best afterwards)
@@ -457,12 +462,28 @@ __global__ void __launch_bounds__(kFitWarps * 32) k_fitness(SwarmView v,
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = blockIdx.x * kFitWarps + warp;
   const int cnt = use_list ? v.ctl->n_events : v.P;
-  if (t >= cnt || lane != 0) return;
+  if (t >= cnt) return;
   int p = t;
   if (use_list) {
     if (v.ev_k[(size_t)v.ctl->mut_cur * v.P + t] < 1) return;
     p = v.ev_slot[t];
   }
+  // lane 0 sums; the warp then copies the tour into pbest if it improved
+  // (solver.py:217-220), in 16-byte pieces
+  int better = 0;
+  if (lane == 0) better = fitness_lane0(v, p, warp, init, s_buf, s_bar);
+  better = __shfl_sync(0xffffffffu, better, 0);
+  if (better) {
+    const uint4* src = reinterpret_cast<const uint4*>(v.x + (size_t)p * v.np);
+    uint4* dst = reinterpret_cast<uint4*>(v.pbest + (size_t)p * v.np);
+    for (int w = lane; w < v.np / 8; w += 32) dst[w] = src[w];
+  }
+}
+
+__device__ __noinline__ int fitness_lane0(const SwarmView& v, int p, int warp,
+                                          bool init,
+                                          double (*s_buf)[2][kFitChunk],
+                                          uint64_t (*s_bar)[2]) {
   const int n = v.n;
   const double* dg = v.dcache + (size_t)p * v.np;
   uint64_t* bar = s_bar[warp];
@@ -501,30 +522,12 @@ __global__ void __launch_bounds__(kFitWarps * 32) k_fitness(SwarmView v,
   v.fit[p] = total;
   if (init) {
     v.pfit[p] = total;
-    return;
+    return 0;
   }
   const int better = total < v.pfit[p];
   if (better) v.pfit[p] = total;
   v.pbflag[p] = better;
-}
-
-// pbest <- x for the particles k_fitness flagged (16-byte copies).
-__global__ void __launch_bounds__(128) k_pbest_copy(SwarmView v,
-                                                    int use_list) {
-  if (v.ctl->done) return;
-  if (use_list && !v.ctl->mutating) return;
-  const int cnt = use_list ? v.ctl->n_events : v.P;
-  for (int t = blockIdx.x; t < cnt; t += gridDim.x) {
-    int p = t;
-    if (use_list) {
-      if (v.ev_k[(size_t)v.ctl->mut_cur * v.P + t] < 1) continue;
-      p = v.ev_slot[t];
-    }
-    if (!v.pbflag[p]) continue;
-    const uint4* src = reinterpret_cast<const uint4*>(v.x + (size_t)p * v.np);
-    uint4* dst = reinterpret_cast<uint4*>(v.pbest + (size_t)p * v.np);
-    for (int w = threadIdx.x; w < v.np / 8; w += blockDim.x) dst[w] = src[w];
-  }
+  return better;
 }
 
 }  // namespace
@@ -583,10 +586,9 @@ cudaError_t launch_update(const SwarmView& v, cudaStream_t s) {
 }
 
 cudaError_t launch_fitness(const SwarmView& v, int use_list, cudaStream_t s) {
+  // (the pbest copy of an improved particle is fused into k_fitness)
   k_fitness<<<(v.P + kFitWarps - 1) / kFitWarps, kFitWarps * 32, 0, s>>>(
       v, use_list);
-  if (use_list == 2) return cudaGetLastError();  // init: pbest = x already
-  k_pbest_copy<<<std::min(v.P, 148 * 8), 128, 0, s>>>(v, use_list);
   return cudaGetLastError();
 }
 
