@@ -207,6 +207,13 @@ int dpso_read_matrix_text(const char* path, double* host_out, int64_t ld,
  * writer's formatter, exposed for tests. */
 int dpso_py_repr(double x, char* out, int32_t cap);
 
+/* numpy's SeedSequence(entropy).spawn(count) + PCG64(child) (the reference's
+ * stream setup, solver.py:278-282), host code: entropy as little-endian
+ * uint32 words (numpy's _int_to_uint32_array), out = count x 6 uint64
+ * records in dpso_set_streams' layout. */
+int dpso_spawn_pcg64_states(const uint32_t* entropy_words, int32_t n_words,
+                            int64_t count, uint64_t* out);
+
 /* Philox4x32-10 block (host evaluation of the device RNG's code path, for
  * known-answer tests): out = philox(ctr[4], key = k0 | k1 << 32). */
 int dpso_philox4x32_10(const uint32_t* ctr, uint64_t key, uint32_t* out);

@@ -124,6 +124,15 @@ def numpy_stream_states(random_state, count: int) -> np.ndarray:
     tests/test_lib_abi.py); any other entropy goes through numpy itself."""
     if isinstance(random_state, (int, np.integer)) and not isinstance(
             random_state, bool) and int(random_state) >= 0:
+        if count <= 0xFFFFFFFF:
+            # native (libdpso host code, threaded); the restatement above is
+            # the same arithmetic in numpy
+            words = np.array(_int_words(int(random_state)), dtype=np.uint32)
+            out = np.empty((count, 6), dtype=np.uint64)
+            _lib.check(_lib.load().dpso_spawn_pcg64_states(
+                words.ctypes.data_as(ctypes.c_void_p), len(words), count,
+                out.ctypes.data_as(ctypes.c_void_p)))
+            return out
         return _spawned_pcg64_states(int(random_state), count)
     seqs = np.random.SeedSequence(random_state).spawn(count)
     out = np.empty((count, 6), dtype=np.uint64)

@@ -115,3 +115,24 @@ def test_stream_states_match_numpy_seedsequence():
                            st["uinteger"])
             got = _spawned_pcg64_states(seed, count)
             assert np.array_equal(got, want), (seed, count)
+
+
+def test_native_stream_states_match_numpy():
+    """dpso_spawn_pcg64_states (host code, threaded) equals numpy's
+    SeedSequence.spawn -> PCG64, including counts that cross its thread
+    chunks and multi-word seeds."""
+    import numpy as np
+    from paper_1706_04399_b200.solver import (_spawned_pcg64_states,
+                                              numpy_stream_states)
+    m = (1 << 64) - 1
+    for seed in (0, 7, 2923, 2**32 + 5, 2**70 + 3, 2**128 + 11):
+        for count in (1, 130):
+            want = np.empty((count, 6), dtype=np.uint64)
+            for i, s in enumerate(np.random.SeedSequence(seed).spawn(count)):
+                st = np.random.PCG64(s).state
+                a, b = st["state"]["state"], st["state"]["inc"]
+                want[i] = (a >> 64, a & m, b >> 64, b & m, st["has_uint32"],
+                           st["uinteger"])
+            assert np.array_equal(numpy_stream_states(seed, count), want)
+    big = numpy_stream_states(1000, 20000)  # several threads
+    assert np.array_equal(big, _spawned_pcg64_states(1000, 20000))
