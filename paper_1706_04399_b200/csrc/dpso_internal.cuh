@@ -61,7 +61,8 @@ constexpr int kScanFilter32 = 2;
 struct CostStats {
   unsigned long long maxabs_bits;  // bits of max |C| (non-negative double)
   int nonintegral;
-  int pad_;
+  int negmax;                      // some entry equals -max|C|
+  unsigned long long second_bits;  // bits of max |C| over |C| < max|C|
 };
 
 struct TwoOptPlan {
@@ -78,6 +79,13 @@ struct TwoOptPlan {
   const uint16_t* cost16;
   int es;        // 4 (cost32 rows) or 2 (cost16 rows)
   float dscale;  // power of two applied to d values (rows are pre-scaled)
+  // Capped virtual level: every entry equal to vfrom (max|C|, far above all
+  // other entries - the reference's blocked pairs, graph.py:63-78) reads as
+  // vto (5 x the next largest |C|) in the fp32/fp16 rows and d values.
+  // Deltas are F + g V with g = (#virtual added - #virtual removed) and
+  // |F| spread <= 4 max_finite, so both V and V' order the pairs alike;
+  // the apply re-evaluates the chosen pair in fp64.  vfrom == 0: none.
+  double vfrom, vto;
 };
 
 struct TwoOptRes {

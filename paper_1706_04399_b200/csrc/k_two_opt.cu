@@ -77,6 +77,7 @@ struct ScanArgs {
   const void* rows;        // staged rows of the fp32 scan: cost32 or cost16
   int64_t row_pitch;       // bytes between staged rows
   float dscale;            // d values -> row units (power of two)
+  double vfrom, vto;       // capped virtual level (TwoOptPlan), 0: none
   int32_t* ovf;            // FILTER32 overflow list: [0] count, [1..] tasks
   int32_t* task_ctr;       // fp32 scan: next task (persistent warps)
   int stream_only;         // debug: stream the rows, skip the pair compute
@@ -523,7 +524,9 @@ __global__ void __launch_bounds__(kW32 * 32, DPSO_SCAN_MINB)
   for (int m = 0; m < NPL; ++m) {
     const int j = col_of(m);
     sdj[lane + 32 * m] =
-        (j >= r0 && j < jhi) ? (float)(dg[j] * a.dscale) : -kInfF;
+        (j >= r0 && j < jhi)
+            ? (float)((dg[j] == a.vfrom ? a.vto : dg[j]) * a.dscale)
+            : -kInfF;
   }
   auto sdj_index = [&](int c) -> int {  // c = j - jlo
     const int grp = c / (32 * GL), within = c % (32 * GL);
@@ -557,7 +560,9 @@ __global__ void __launch_bounds__(kW32 * 32, DPSO_SCAN_MINB)
     return q < nrows ? (int)tour[r0 + q] : 0;
   };
   auto d_at = [&](int k) -> float {
-    return r0 + k < r1 ? (float)(dg[r0 + k] * a.dscale) : 0.f;
+    if (r0 + k >= r1) return 0.f;
+    const double d = dg[r0 + k];
+    return (float)((d == a.vfrom ? a.vto : d) * a.dscale);
   };
   int cb = city_at(3 + lane), cb_next = city_at(3 + 32 + lane);
   float db = d_at(lane), db_next = d_at(32 + lane);
@@ -819,6 +824,8 @@ struct ApplyArgs {
   const double* cost;  // non-null: refresh dcache after the move
   int64_t ld;
   double* dcache;
+  const double* cost64;  // capped plan: re-evaluate the chosen pair in fp64
+  const double* dcache_in;  // (with the tour's d values)
 };
 
 __global__ void __launch_bounds__(128) k_two_opt_apply(ApplyArgs a) {
@@ -839,6 +846,19 @@ __global__ void __launch_bounds__(128) k_two_opt_apply(ApplyArgs a) {
         bi = r[c].i;
         bj = r[c].j;
       }
+    if (a.cost64 && bi != 0x7fffffff && bj != 0x7fffffff &&
+        best != __longlong_as_double(0x7ff0000000000000ll)) {
+      // the scan compared capped values: the reference's fp64 delta of the
+      // chosen pair (solver.py:94-101)
+      const uint16_t* t = a.tours + (size_t)p * a.np;
+      const double* dg = a.dcache_in + (size_t)p * a.np;
+      const int ai = t[bi], aj = t[bj], si = t[bi + 1],
+                sj = t[bj + 1 == a.n ? 0 : bj + 1];
+      double v = __dadd_rn(a.cost64[(size_t)ai * a.ld + aj],
+                           a.cost64[(size_t)si * a.ld + sj]);
+      v = __dsub_rn(v, dg[bi]);
+      best = __dsub_rn(v, dg[bj]);
+    }
     int move = (a.n >= 4) && (best < -1e-12);
     s_move[0] = move;
     s_move[1] = bi;
@@ -909,15 +929,61 @@ __global__ void k_cost_prep(const double* cost, int64_t ld, int n,
 }
 
 // fp16 rows: round(C * scale) (scale a power of two, so only the final
-// rounding to fp16 is inexact; integers <= 2048 are exact)
+// rounding to fp16 is inexact; integers <= 2048 are exact); entries equal to
+// vfrom (vfrom > 0) read as vto
 __global__ void k_cost_to16(const double* cost, int64_t ld, int n,
-                            uint16_t* c16, int64_t ld16, double scale) {
+                            uint16_t* c16, int64_t ld16, double scale,
+                            double vfrom, double vto) {
   const int64_t total = (int64_t)n * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / n, c = e % n;
-    const __half h = __double2half(cost[r * ld + c] * scale);
+    double v = cost[r * ld + c];
+    if (vfrom > 0.0 && v == vfrom) v = vto;
+    const __half h = __double2half(v * scale);
     c16[r * ld16 + c] = __half_as_ushort(h);
+  }
+}
+
+// second statistics pass: max |C| over |C| < max (the finite level under a
+// virtual one) and whether -max occurs
+__global__ void k_cost_second(const double* cost, int64_t ld, int n,
+                              CostStats* st) {
+  const double mx = __longlong_as_double((long long)st->maxabs_bits);
+  unsigned long long m2 = 0;
+  int neg = 0;
+  const int64_t total = (int64_t)n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double v = cost[(e / n) * ld + e % n];
+    const double a = fabs(v);
+    if (a < mx) {
+      const unsigned long long b = (unsigned long long)__double_as_longlong(a);
+      m2 = b > m2 ? b : m2;
+    } else if (v < 0.0) {
+      neg = 1;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, m2, o);
+    m2 = x > m2 ? x : m2;
+    neg |= __shfl_xor_sync(0xffffffffu, neg, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&st->second_bits, m2);
+    if (neg) atomicOr(&st->negmax, 1);
+  }
+}
+
+// fp32 rows: entries equal to (float)vfrom read as vto
+__global__ void k_cost_cap32(float* c32, int64_t ld32, int n, float from,
+                             float to) {
+  const int64_t total = (int64_t)n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    float* q = c32 + (e / n) * ld32 + e % n;
+    if (*q == from) *q = to;
   }
 }
 
@@ -1006,13 +1072,38 @@ cudaError_t two_opt_prepare(const double* cost, int64_t ld, int32_t n,
   pl->dscale = 1.f;
   cudaError_t e = launch_cost_prep(cost, ld, n, c32, np, st, s);
   if (e) return e;
+  const int64_t total = (int64_t)n * n;
+  int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  if (blocks < 1) blocks = 1;
+  k_cost_second<<<blocks, 256, 0, s>>>(cost, ld, n, st);
   CostStats h;
-  e = cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, s);
+  e = cudaGetLastError();
+  if (!e) e = cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, s);
   if (!e) e = cudaStreamSynchronize(s);
   if (e) return e;
+  {
+    // a virtual level (entries equal to max|C|, > 64 x every other |C|):
+    // cap it at 5 x the finite maximum in the fp32/fp16 rows (> the spread
+    // 4 max_finite of the finite parts of two deltas)
+    double mx, m2;
+    memcpy(&mx, &h.maxabs_bits, sizeof mx);
+    memcpy(&m2, &h.second_bits, sizeof m2);
+    if (!h.negmax && m2 > 0.0 && mx > 64.0 * m2 && mx < 1e300 &&
+        !getenv("DPSO_NO_VCAP")) {
+      pl->vfrom = mx;
+      pl->vto = 5.0 * m2;
+      k_cost_cap32<<<blocks, 256, 0, s>>>(c32, np, n, (float)mx,
+                                           (float)pl->vto);
+      e = cudaGetLastError();
+      if (e) return e;
+      const double capped = pl->vto;
+      memcpy(&h.maxabs_bits, &capped, sizeof capped);
+    }
+  }
   pl->mode = two_opt_mode(h, n, &pl->thr);
   if (getenv("DPSO_SCAN_MODE")) pl->mode = atoi(getenv("DPSO_SCAN_MODE"));
   if (pl->mode == kScanFilter32 && pl->thr == 0.f) pl->mode = kScanFP64;
+  if (pl->mode == kScanFP64) pl->vfrom = pl->vto = 0.0;  // fp64 rows: exact
   const char* e16 = getenv("DPSO_SCAN16");
   if (!c16 || (e16 && atoi(e16) == 0) || pl->mode == kScanFP64) return e;
   double mx;
@@ -1034,10 +1125,8 @@ cudaError_t two_opt_prepare(const double* cost, int64_t ld, int32_t n,
     pl->thr = (float)(mx * scale * 0.00403);
   }
   pl->dscale = (float)scale;
-  const int64_t total = (int64_t)n * n;
-  int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-  if (blocks < 1) blocks = 1;
-  k_cost_to16<<<blocks, 256, 0, s>>>(cost, ld, n, c16, np, scale);
+  k_cost_to16<<<blocks, 256, 0, s>>>(cost, ld, n, c16, np, scale, pl->vfrom,
+                                     pl->vto);
   e = cudaGetLastError();
   if (e) return e;
   pl->cost16 = c16;
@@ -1202,6 +1291,8 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
       a.rows = es == 2 ? (const void*)pl.cost16 : (const void*)pl.cost32;
       a.row_pitch = (int64_t)es * pl.ld32;
       a.dscale = es == 2 ? pl.dscale : 1.f;
+      a.vfrom = pl.vfrom;
+      a.vto = pl.vto;
       a.row_bytes = (uint32_t)(round_up(n, 16 / es) * es);
       a.buf_stride = (uint32_t)round_up(a.row_bytes, 128);
       // per warp: 2-slot row ring + d_j (fp32, 32 * NPL entries)
@@ -1255,6 +1346,9 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
   b.cost = dcache_rw ? pl.cost : nullptr;
   b.ld = pl.ld;
   b.dcache = dcache_rw;
+  const bool capped = pl.vfrom > 0.0 && pl.mode != kScanFP64;
+  b.cost64 = capped ? pl.cost : nullptr;
+  b.dcache_in = dcache;
   if (n < 4) {
     // _best_exchange returns (body, 0.0) for n < 4 (solver.py:91-93)
     if (delta_out) cudaMemsetAsync(delta_out, 0, sizeof(double) * count, s);

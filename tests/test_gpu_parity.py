@@ -475,3 +475,50 @@ def test_island_exchange_device_nccl_single_rank(pkg):
     finally:
         dist.destroy_process_group()
 
+
+
+def _with_virtual(cost, rng, frac):
+    n = cost.shape[0]
+    blk = np.triu(rng.random((n, n)) < frac, 1)
+    blk = blk | blk.T
+    out = cost.copy()
+    out[blk] = 1e3 * n * cost.max()  # graph.py:63-78
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", [None, "/rows32", "exact32", "filter32"])
+def test_best_exchange_virtual_level_capped(pkg, mode, monkeypatch):
+    # blocked pairs at 1e3 * n * max_finite: the scan caps that level in its
+    # fp32/fp16 rows (orders pairs alike) and the apply re-evaluates the
+    # chosen pair in fp64 - bit-exact against the oracle, integer (EXACT32)
+    # and Euclidean (FILTER32), including tours that use virtual edges
+    set_scan_mode(monkeypatch, mode)
+    rng = np.random.default_rng(77)
+    for n, integer in ((60, True), (300, True), (300, False), (1100, False)):
+        base = random_euclidean_matrix(n, rng)
+        if integer:
+            base = np.floor(base * 20)
+        cost = _with_virtual(base, rng, 0.02)
+        tours = np.array([rng.permutation(n) for _ in range(16)],
+                         dtype=np.int32)
+        check_batch(pkg, cost, tours, ("virtual", n, integer, mode))
+
+
+@pytest.mark.gpu
+def test_swarm_with_virtual_edges_matches_oracle(pkg):
+    # whole solve on a matrix with blocked pairs: convergence and tour
+    # bit-identical to the oracle (the fitness += delta uses the fp64
+    # re-evaluated delta)
+    rng = np.random.default_rng(5)
+    for integer in (True, False):
+        base = random_euclidean_matrix(120, rng)
+        if integer:
+            base = np.floor(base * 20)
+        cost = _with_virtual(base, rng, 0.05)
+        params = dict(n_particles=24, max_generations=15,
+                      stall_generations=15, random_state=4)
+        ref = O.OracleSolver(**params).fit(cost)
+        got = pkg.DiscreteSwarmSolver(**params).fit(cost)
+        assert list(got.best_tour_) == list(ref.best_tour_)
+        assert got.convergence_ == ref.convergence_
