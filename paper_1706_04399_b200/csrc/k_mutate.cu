@@ -10,7 +10,8 @@
 //                 (a hash collision falls back to an exact search)
 //   k_mut_lists   survivors / dropped in rank order, keep = first ceil(S/3)
 //                 survivors, events = non-kept slots in slot order
-//   k_mut_copy    dropped #r copies body+fitness of survivors[r % S]
+//   k_mut_copy    dropped #r copies body+fitness (and edge costs) of
+//                 survivors[r % S]
 //   k_mut_gen/k_mut_walk/k_mut_sample/k_mut_fix: the mutation stream (see
 //                 the section comment below)
 //   k_mut_swap    k disjoint swaps, fitness in reference order, pbest
@@ -242,6 +243,10 @@ __global__ void __launch_bounds__(128) k_mut_copy(SwarmView v) {
   const uint16_t* a = v.x + (size_t)src * v.np;
   uint16_t* b = v.x + (size_t)p * v.np;
   for (int i = threadIdx.x; i < v.n; i += blockDim.x) b[i] = a[i];
+  // and its edge costs: k_mut_swap re-gathers only the edges it touches
+  const double* da = v.dcache + (size_t)src * v.np;
+  double* db = v.dcache + (size_t)p * v.np;
+  for (int i = threadIdx.x; i < v.n; i += blockDim.x) db[i] = da[i];
   if (threadIdx.x == 0) v.fit[p] = v.fit[src];
 }
 
@@ -946,11 +951,32 @@ __global__ void __launch_bounds__(128) k_mut_swap(SwarmView v) {
     body[b] = x;
   }
   __syncthreads();
-  // edge costs; the fitness and pbest follow in k_fitness (event list)
+  // edge costs of the edges the swaps touched (i-1 and i for each swapped
+  // position i; dcache holds the rest already - the copy from a survivor
+  // brings its edges along); the fitness and pbest follow in k_fitness
+  // (event list).  An edge two swaps share is written twice with the same
+  // value.  Four gathers in flight per thread.
   double* dg = v.dcache + (size_t)p * np;
-  for (int i = tid; i < n; i += blockDim.x) {
-    const int a = body[i], b = body[i + 1 == n ? 0 : i + 1];
-    dg[i] = v.cost[(size_t)a * v.ld + b];
+  const int ne = 4 * k;
+  for (int e0 = tid; e0 < ne; e0 += 4 * blockDim.x) {
+    double d[4];
+    int at[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * blockDim.x;
+      at[u] = -1;
+      if (e < ne) {
+        const int pos = idx[e >> 1];  // swapped position
+        int i = (e & 1) ? pos : pos - 1;  // edge (i, i+1)
+        if (i < 0) i += n;
+        const int a = body[i], b = body[i + 1 == n ? 0 : i + 1];
+        d[u] = v.cost[(size_t)a * v.ld + b];
+        at[u] = i;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (at[u] >= 0) dg[at[u]] = d[u];
   }
 }
 
