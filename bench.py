@@ -285,6 +285,39 @@ def gpu_launch_count(cfg, first_gen, gens, period=3):
     return base * gens + mut * n_mut
 
 
+def scan_floors(cost, params, seed_body, n_seed, P, gens=6):
+    import numpy as np
+    from paper_1706_04399_b200 import DiscreteSwarmSolver
+    from paper_1706_04399_b200.solver import numpy_stream_states
+    out = {}
+    for name, val in (("stream_only_ms", "1"), ("stream_gathers_ms", "2")):
+        os.environ["DPSO_SCAN_STREAM_ONLY"] = val
+        try:
+            p = dict(params, max_generations=gens + 4,
+                     stall_generations=gens + 4)
+            s = DiscreteSwarmSolver(**p)
+            ctx = s._make_context(cost)
+            try:
+                if RNG == "numpy":
+                    ctx.set_streams(numpy_stream_states(p["random_state"],
+                                                        P + 2))
+                ctx.init(seed_body, n_seed)
+                ctx.step_timed(2)
+                ms = []
+                for _ in range(gens):
+                    c0 = ctx.ctl()["two_opt_count"]
+                    ph, cnt = ctx.step_timed(1)
+                    if cnt > c0:
+                        ms.append(float(ph[3]))
+                if ms:
+                    out[name] = float(np.median(ms))
+            finally:
+                ctx.close()
+        finally:
+            os.environ.pop("DPSO_SCAN_STREAM_ONLY", None)
+    return out
+
+
 def run_ours(args, cfg_name, cfg):
     import numpy as np
     import torch
@@ -409,6 +442,19 @@ def run_ours(args, cfg_name, cfg):
         "phase_ms_per_gen": phases,
         "two_opt_fired": f"{fired}/{prof_gens}",
     }
+    # the scan's own floors, live: the same kernel reduced to its row stream
+    # and to the stream plus every pair's shared-memory gathers
+    # (DPSO_SCAN_STREAM_ONLY probes, tools/scan_floors.py)
+    if cfg.get("ee", True) and world == 1 and dom == "two_opt_scan":
+        try:
+            fl = scan_floors(cost, params, seed_body, n_seed, P)
+            if fl.get("stream_gathers_ms"):
+                # the fraction of the kernel's own gather floor it reaches
+                fl["frac_of_stream_gathers"] = fl["stream_gathers_ms"] / dur_ms
+            if fl:
+                line["roofline"]["floors"] = fl
+        except Exception as exc:  # a probe failing must not lose the line
+            line["roofline"]["floors"] = {"error": str(exc)[:200]}
     # clocks
     line["clocks"] = clk.summary()
 
