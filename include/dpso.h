@@ -207,6 +207,20 @@ int dpso_read_matrix_text(const char* path, double* host_out, int64_t ld,
  * writer's formatter, exposed for tests. */
 int dpso_py_repr(double x, char* out, int32_t cap);
 
+/* Voxel A* paths (replaces voxel.py:112-172 shortest_path for the legs
+ * graph.py:58-66 stores, host code, all cores): host_occ = nx*ny*nz uint8
+ * (C order, 1 = occupied), weights = axis weights (a1, a2, a3), mode 0 =
+ * admissible, 1 = paper heuristic; pairs = k x (start xyz, goal xyz).
+ * Path i goes to out_xyz + 3*cap_per*i as lens[i] (x, y, z) waypoints with
+ * motion cost costs[i]; a blocked pair gives lens[i] = 0, costs[i] = inf.
+ * The same path as the reference (heap order (f, g, voxel), neighbour
+ * order, fp64 step costs).  An occupied endpoint fails with the
+ * reference's message. */
+int dpso_voxel_paths(const uint8_t* host_occ, int32_t nx, int32_t ny,
+                     int32_t nz, const double* weights, int32_t mode,
+                     const int32_t* pairs, int32_t k, int32_t* out_xyz,
+                     int64_t cap_per, int64_t* lens, double* costs);
+
 /* numpy's SeedSequence(entropy).spawn(count) + PCG64(child) (the reference's
  * stream setup, solver.py:278-282), host code: entropy as little-endian
  * uint32 words (numpy's _int_to_uint32_array), out = count x 6 uint64

@@ -9,7 +9,7 @@ from .kernels import (best_exchange_batch, nearest_neighbor_tour,
                       nearest_neighbor_two_opt, tour_cost_batch)
 from .graph import (TourGraph, build_cost_matrix, build_graph,
                     load_cost_matrix, load_cost_matrix_device,
-                    save_cost_matrix)
+                    save_cost_matrix, shortest_path, tour_legs)
 
 __version__ = "0.1.0"
 
@@ -19,4 +19,5 @@ __all__ = [
     "nearest_neighbor_two_opt", "tour_cost_batch",
     "TourGraph", "build_cost_matrix", "build_graph",
     "load_cost_matrix", "load_cost_matrix_device", "save_cost_matrix",
+    "shortest_path", "tour_legs",
 ]

@@ -74,6 +74,8 @@ _SIG = {
                                      ctypes.POINTER(_I32)]),
     "dpso_py_repr": (_I32, [ctypes.c_double, ctypes.c_char_p, _I32]),
     "dpso_spawn_pcg64_states": (_I32, [_P, _I32, _I64, _P]),
+    "dpso_voxel_paths": (_I32, [_P, _I32, _I32, _I32, _P, _I32, _P, _I32,
+                                _P, _I64, _P, _P]),
     "dpso_version": (ctypes.c_char_p, []),
 }
 EXPORTED = tuple(_SIG)

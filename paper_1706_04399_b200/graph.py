@@ -7,8 +7,10 @@ cost[i][j] = cost[j][i] = admissible-A* (= Dijkstra) motion cost on the
 pairs at ``1e3 * n * max_finite`` (1e6 when no finite edge) and flagged in
 ``virtual``.  ``build_graph(plan, grid, weights)`` mirrors the reference
 signature for callers holding the reference's CoveragePlan/VoxelGrid.
-Per-pair waypoint legs (``TourGraph.legs``) are not produced: the
-reference's CLI needs them only for the final tour's N edges.
+Per-pair waypoint legs for all N(N-1)/2 pairs are not produced: the
+reference's CLI needs them only for the final tour's N edges, which
+``tour_legs`` computes with a native restatement of the reference's A*
+(same paths, byte for byte; ``shortest_path`` for single pairs).
 
 ``save_cost_matrix`` / ``load_cost_matrix`` are graph.py:123-143 (the
 plain-text ``--matrix`` format) in native host code: the file bytes are the
@@ -131,3 +133,72 @@ def load_cost_matrix_device(path, device=None):
     dev = torch.device(device) if device is not None else torch.device(
         "cuda", torch.cuda.current_device())
     return host[:n].to(dev, non_blocking=False), ld
+
+
+class OccupiedEndpointError(ValueError):
+    """voxel.py's error for an occupied start or goal voxel."""
+
+
+def _voxel_paths(occupancy, pairs, weights, heuristic_mode="admissible"):
+    occ = np.ascontiguousarray(np.asarray(occupancy, dtype=bool),
+                               dtype=np.uint8)
+    if occ.ndim != 3:
+        raise ValueError("occupancy must be a 3-D grid")
+    if heuristic_mode not in ("admissible", "paper"):
+        raise ValueError(f"unknown heuristic_mode {heuristic_mode!r}")
+    pr = np.ascontiguousarray(np.asarray(pairs, dtype=np.int32).reshape(-1, 6))
+    w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
+    k = pr.shape[0]
+    nx, ny, nz = occ.shape
+    cap = nx * ny * nz  # a path visits each voxel at most once
+    cap = min(cap, 1 << 16)
+    while True:
+        out = np.zeros((max(k, 1), cap, 3), dtype=np.int32)
+        lens = np.zeros(max(k, 1), dtype=np.int64)
+        costs = np.zeros(max(k, 1), dtype=np.float64)
+        lib = _lib.load()
+        rc = lib.dpso_voxel_paths(
+            occ.ctypes.data_as(ctypes.c_void_p), nx, ny, nz,
+            w.ctypes.data_as(ctypes.c_void_p),
+            0 if heuristic_mode == "admissible" else 1,
+            pr.ctypes.data_as(ctypes.c_void_p), k,
+            out.ctypes.data_as(ctypes.c_void_p), cap,
+            lens.ctypes.data_as(ctypes.c_void_p),
+            costs.ctypes.data_as(ctypes.c_void_p))
+        if rc != 0:
+            msg = lib.dpso_last_error().decode()
+            if "output capacity" in msg and cap < nx * ny * nz:
+                cap = nx * ny * nz
+                continue
+            if "is occupied" in msg:
+                raise OccupiedEndpointError(msg)
+            _lib.check(rc)
+        break
+    res = []
+    for i in range(k):
+        if lens[i] == 0:
+            res.append(None)
+        else:
+            res.append((tuple(tuple(int(v) for v in p)
+                              for p in out[i, :lens[i]]), float(costs[i])))
+    return res
+
+
+def shortest_path(occupancy, start, goal, weights,
+                  heuristic_mode="admissible"):
+    """voxel.py:112-172: (waypoints, motion_cost), or None when blocked."""
+    return _voxel_paths(occupancy, [list(start) + list(goal)], weights,
+                        heuristic_mode)[0]
+
+
+def tour_legs(occupancy, viewpoint_voxels, weights, tour,
+              heuristic_mode="admissible") -> dict:
+    """The legs of a closed tour as graph.py stores them: key (i, j) with
+    i < j -> (waypoints from viewpoint i to j, motion cost); None for a
+    blocked (virtual) edge.  TourGraph.leg(a, b) reverses for a > b."""
+    vox = np.asarray(viewpoint_voxels, dtype=np.int32).reshape(-1, 3)
+    keys = sorted({(min(a, b), max(a, b)) for a, b in zip(tour[:-1], tour[1:])
+                   if a != b})
+    pairs = [list(vox[i]) + list(vox[j]) for i, j in keys]
+    paths = _voxel_paths(occupancy, pairs, weights, heuristic_mode)
+    return dict(zip(keys, paths))
