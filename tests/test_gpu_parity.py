@@ -522,3 +522,21 @@ def test_swarm_with_virtual_edges_matches_oracle(pkg):
         got = pkg.DiscreteSwarmSolver(**params).fit(cost)
         assert list(got.best_tour_) == list(ref.best_tour_)
         assert got.convergence_ == ref.convergence_
+
+
+@pytest.mark.gpu
+def test_best_exchange_negative_and_mixed_costs(pkg, scan_mode):
+    # the reference does not forbid negative costs: mixed signs, integer and
+    # not, one large negative outlier (no capping then: -max|C| occurs)
+    rng = np.random.default_rng(99)
+    for n in (40, 333):
+        c = rng.normal(size=(n, n)) * 5
+        np.fill_diagonal(c, 0.0)
+        tours = np.array([rng.permutation(n) for _ in range(12)],
+                         dtype=np.int32)
+        check_batch(pkg, c, tours, ("normal", n, scan_mode))
+        ci = np.round(c)
+        check_batch(pkg, ci, tours, ("normal-int", n, scan_mode))
+        co = c.copy()
+        co[1, 2] = -1e6
+        check_batch(pkg, co, tours, ("outlier", n, scan_mode))
