@@ -131,6 +131,14 @@ int dpso_set_state(dpso_ctx* ctx, const int32_t* x, const int32_t* pbest,
                    const double* fit, const double* pfit, const int32_t* vmap,
                    const int32_t* gbest, double gbest_fit);
 
+/* Test hook: one mutation call (_mutate, solver.py:222-258) on the current
+ * state - dedupe by canonical form, reseed the dropped, mutate the non-kept
+ * in slot order from the mutation stream (stream 1 of dpso_set_streams),
+ * re-cost, pbest - without the velocity update.  Needs use_mutation and
+ * mutation_period == 1.  Pairs with dpso_set_state to replay the
+ * reference's golden _mutate swarms on the device. */
+int dpso_mutate_step(dpso_ctx* ctx);
+
 /* Island exchange (multi-GPU): overwrite gbest when `fitness` is strictly
  * better; the host layer moves the 16-byte records and tours with NCCL. */
 int dpso_offer_gbest(dpso_ctx* ctx, const int32_t* host_tour, double fitness);
@@ -158,6 +166,12 @@ const char* dpso_last_error(void);
 int dpso_tour_cost_batch(const double* dev_cost, int64_t ld, int32_t n,
                          const int32_t* dev_tours, int32_t count,
                          double* dev_out, void* cuda_stream);
+
+/* Tasks per particle the 2-opt scan cuts a batch of `count` tours of n
+ * nodes into (row bands x column ranges).  1 selects the one-warp-per-task
+ * launch, more than 1 the persistent-warp launch (k_two_opt.cu); -1 on bad
+ * arguments. */
+int dpso_scan_chunks(int32_t n, int32_t count);
 
 /* _best_exchange (solver.py:88-106) for `count` tours: best 2-opt move with
  * first-index tie break; tours are rewritten in place when the move is

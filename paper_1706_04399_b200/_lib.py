@@ -57,6 +57,8 @@ _SIG = {
     "dpso_get_state": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P]),
     "dpso_set_state": (_I32, [_P, _P, _P, _P, _P, _P, _P, ctypes.c_double]),
     "dpso_offer_gbest": (_I32, [_P, _P, ctypes.c_double]),
+    "dpso_mutate_step": (_I32, [_P]),
+    "dpso_scan_chunks": (_I32, [_I32, _I32]),
     "dpso_island_record_bytes": (_I64, [_I32]),
     "dpso_island_pack": (_I32, [_P, _P, _I32]),
     "dpso_island_adopt": (_I32, [_P, _P, _I32, _I32]),

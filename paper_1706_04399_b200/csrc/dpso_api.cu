@@ -767,38 +767,66 @@ int dpso_set_state(dpso_ctx* c, const int32_t* x, const int32_t* pbest,
   const int64_t P = c->prm.n_particles, n = c->n, np = c->v.np;
   int rc = sync_in(c);
   if (rc) return rc;
-  CK(cudaStreamSynchronize(c->stream));
-  std::vector<uint16_t> buf(P * np, 0);
-  auto put = [&](uint16_t* dst, const int32_t* src) -> int {
+  // every copy is stream-ordered on c->stream (pageable host sources are
+  // staged by the driver; the stream sync below keeps them alive)
+  std::vector<uint16_t> bx, bp, bv;
+  auto put = [&](uint16_t* dst, const int32_t* src,
+                 std::vector<uint16_t>& buf) -> int {
     if (!dst || !src) return DPSO_OK;
+    buf.assign(P * np, 0);
     for (int64_t p = 0; p < P; ++p)
       for (int64_t i = 0; i < n; ++i) buf[p * np + i] = (uint16_t)src[p * n + i];
-    CK(cudaMemcpy(dst, buf.data(), 2 * P * np, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(dst, buf.data(), 2 * P * np, cudaMemcpyHostToDevice,
+                       c->stream));
     return DPSO_OK;
   };
-  if ((rc = put(c->v.x, x))) return rc;
-  if ((rc = put(c->v.pbest, pbest))) return rc;
-  if ((rc = put(c->v.vmap, vmap))) return rc;
-  if (fit) CK(cudaMemcpy(c->v.fit, fit, 8 * P, cudaMemcpyHostToDevice));
-  if (pfit) CK(cudaMemcpy(c->v.pfit, pfit, 8 * P, cudaMemcpyHostToDevice));
+  if ((rc = put(c->v.x, x, bx))) return rc;
+  if ((rc = put(c->v.pbest, pbest, bp))) return rc;
+  if ((rc = put(c->v.vmap, vmap, bv))) return rc;
+  if (pfit)
+    CK(cudaMemcpyAsync(c->v.pfit, pfit, 8 * P, cudaMemcpyHostToDevice,
+                       c->stream));
+  std::vector<uint16_t> g;
   if (gbest) {
-    std::vector<uint16_t> g(n);
+    g.resize(n);
     for (int i = 0; i < n; ++i) g[i] = (uint16_t)gbest[i];
-    CK(cudaMemcpy(c->v.gbest, g.data(), 2 * n, cudaMemcpyHostToDevice));
-    DevCtl h;
-    CK(cudaMemcpy(&h, c->v.ctl, sizeof h, cudaMemcpyDeviceToHost));
-    h.gbest_fit = gbest_fit;
-    CK(cudaMemcpy(c->v.ctl, &h, sizeof h, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(c->v.gbest, g.data(), 2 * n, cudaMemcpyHostToDevice,
+                       c->stream));
+    c->host_ctl->gbest_fit = gbest_fit;
+    CK(cudaMemcpyAsync(&c->v.ctl->gbest_fit, &c->host_ctl->gbest_fit,
+                       sizeof(double), cudaMemcpyHostToDevice, c->stream));
   }
-  // refresh the edge-cost cache for the new positions
+  // refresh the edge-cost cache (and fitness) for the new positions, then
+  // let explicit fitness values override the recomputed ones
   CK(launch_tour_cost_rows(c->v.cost, c->v.ld, c->n, c->v.x, np,
                            c->prm.n_particles, c->v.fit, c->v.dcache,
                            c->stream));
-  if (fit) CK(cudaMemcpyAsync(c->v.fit, fit, 8 * P, cudaMemcpyHostToDevice,
-                              c->stream));
+  if (fit)
+    CK(cudaMemcpyAsync(c->v.fit, fit, 8 * P, cudaMemcpyHostToDevice,
+                       c->stream));
   CK(cudaStreamSynchronize(c->stream));
   c->initialized = true;
-  return DPSO_OK;
+  return sync_out(c);
+}
+
+int dpso_mutate_step(dpso_ctx* c) {
+  if (!c || !c->initialized) return fail(DPSO_EINVAL, "context not initialized");
+  if (!c->prm.use_mutation || c->prm.mutation_period != 1)
+    return fail(DPSO_EINVAL,
+                "dpso_mutate_step needs use_mutation and mutation_period == 1");
+  int rc = sync_in(c);
+  if (rc) return rc;
+  const SwarmView& v = c->v;
+  // one generation reduced to its mutation call: gen_begin (marks it
+  // mutating, selects the buffers the last walk prepared), the dedupe /
+  // sampling pipeline, the next call's stream walk, swap + fitness + pbest
+  CK(launch_gen_begin(v, c->stream));
+  CK(launch_mutation_pre(v, c->stream));
+  CK(launch_mutation_post(v, c->stream));
+  CK(launch_mutation_walk(v, c->stream));
+  CK(launch_mutation_swap(v, c->stream));
+  c->gen_next += 1;
+  return sync_out(c);
 }
 
 int dpso_offer_gbest(dpso_ctx* c, const int32_t* tour, double fitness) {
@@ -812,11 +840,14 @@ int dpso_offer_gbest(dpso_ctx* c, const int32_t* tour, double fitness) {
   if (!(fitness < c->host_ctl->gbest_fit)) return DPSO_OK;
   std::vector<uint16_t> g(n);
   for (int i = 0; i < n; ++i) g[i] = (uint16_t)tour[i];
-  CK(cudaMemcpy(c->v.gbest, g.data(), 2 * n, cudaMemcpyHostToDevice));
+  // tour and fitness in the same stream, ordered before the next generation
   c->host_ctl->gbest_fit = fitness;
-  CK(cudaMemcpy(&c->v.ctl->gbest_fit, &fitness, sizeof(double),
-                cudaMemcpyHostToDevice));
-  return DPSO_OK;
+  CK(cudaMemcpyAsync(c->v.gbest, g.data(), 2 * n, cudaMemcpyHostToDevice,
+                     c->stream));
+  CK(cudaMemcpyAsync(&c->v.ctl->gbest_fit, &c->host_ctl->gbest_fit,
+                     sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return sync_out(c);
 }
 
 int64_t dpso_island_record_bytes(int32_t n) {
@@ -897,6 +928,14 @@ static int to_u16_tours(const int32_t* dev_tours, int32_t n, int32_t count,
   if (count > 0) k_i32_to_u16<<<count, 256, 0, s>>>(dev_tours, n, count, dst, np);
   CK(cudaGetLastError());
   return DPSO_OK;
+}
+
+int dpso_scan_chunks(int32_t n, int32_t count) {
+  if (n < 1 || count < 0) {
+    fail(DPSO_EINVAL, "bad arguments");
+    return -1;
+  }
+  return two_opt_pick_chunks(n, std::max(count, 1));
 }
 
 int dpso_best_exchange_batch(const double* dev_cost, int64_t ld, int32_t n,

@@ -259,6 +259,27 @@ class SwarmContext:
         return {"x": x, "pbest": pb, "fit": fit, "pfit": pfit, "vmap": vm,
                 "gbest": gb, "gbest_fit": float(gf.value)}
 
+    def set_state(self, x=None, pbest=None, fit=None, pfit=None, vmap=None,
+                  gbest=None, gbest_fit: float = 0.0) -> None:
+        """Overwrite swarm state (P x n int32 tours, P fp64 values); None
+        leaves a buffer as it is (dpso_set_state)."""
+        keep = []
+
+        def ptr(a, dt):
+            if a is None:
+                return None
+            a = np.ascontiguousarray(a, dtype=dt)
+            keep.append(a)
+            return a.ctypes.data_as(ctypes.c_void_p)
+        _lib.check(self.lib.dpso_set_state(
+            self.h, ptr(x, np.int32), ptr(pbest, np.int32),
+            ptr(fit, np.float64), ptr(pfit, np.float64), ptr(vmap, np.int32),
+            ptr(gbest, np.int32), float(gbest_fit)))
+
+    def mutate_step(self) -> None:
+        """One mutation call without the update (dpso_mutate_step)."""
+        _lib.check(self.lib.dpso_mutate_step(self.h))
+
     def offer_gbest(self, tour, fitness: float) -> None:
         arr = np.ascontiguousarray(tour, dtype=np.int32)
         _lib.check(self.lib.dpso_offer_gbest(
