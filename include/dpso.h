@@ -91,6 +91,13 @@ int dpso_scan_mode(dpso_ctx* ctx);
  * forces fp32 rows (testing). */
 int dpso_scan_rows_bytes(dpso_ctx* ctx);
 
+/* Which 2-opt scan runs: 0 = the column-per-lane scan of dpso_scan_mode,
+ * 1 = the row-per-lane band scan, exact (integer |C| <= 32767), 2 = the
+ * band scan with int16 fixed-point rows and exact fp64 re-evaluation of
+ * the candidates (k_two_opt_band.cu).  DPSO_SCAN_BAND=0, or any of the
+ * column scan's knobs, selects 0 (testing). */
+int dpso_scan_band(dpso_ctx* ctx);
+
 /* How the last dpso_init located each particle's draws in the shared numpy
  * init stream: 1 = parallel walk (every start's walk length, then pointer
  * doubling), 0 = serial scan (too large a span, a walk ran off the span, or

@@ -69,7 +69,7 @@ struct Layout {
       off_sidx, off_order, off_surv, off_keep, off_ev_slot, off_ev_k,
       off_ev_cursor, off_ev_end, off_ev_idx, off_mstream, off_init_buf,
       off_init_state, off_init_cursor, off_init_aux, off_init_anchor, off_seed, off_cost32,
-      off_stats, total;
+      off_stats, off_band_cols, total;
   int64_t vel_cap;
   int chunks;
 };
@@ -136,8 +136,14 @@ Layout make_layout(const dpso_params* prm, int n) {
     L.off_init_anchor = take(par ? 8 * (P + 2) : 0);
   }
   L.off_seed = take(2 * np);
-  L.off_cost32 = take(prm->use_edge_exchange ? 6 * (int64_t)n * np : 0);  // fp32 + fp16 rows
+  // fp32 + fp16 rows, then the band scan's int16 row versions
+  L.off_cost32 = take(prm->use_edge_exchange
+                          ? round_up(6 * (int64_t)n * np, 256) +
+                                band_rows_bytes(n)
+                          : 0);
   L.off_stats = take(sizeof(CostStats));
+  L.off_band_cols =
+      take(prm->use_edge_exchange ? band_cols_bytes(n, P) : 0);
   L.total = o;
   return L;
 }
@@ -467,8 +473,14 @@ int dpso_set_cost(dpso_ctx* c, const double* dev_cost, int64_t ld) {
     CostStats* st = (CostStats*)(c->ws + c->L.off_stats);
     int rc = sync_in(c);
     if (rc) return rc;
-    CK(two_opt_prepare(dev_cost, ld, c->n, c->v.np, c32, c16, st, c->stream,
-                       &pl));
+    unsigned char* band = band_rows_bytes(c->n)
+                              ? (unsigned char*)c32 +
+                                    round_up(6 * (int64_t)c->n * c->v.np, 256)
+                              : nullptr;
+    CK(two_opt_prepare(dev_cost, ld, c->n, c->v.np, c32, c16, band, st,
+                       c->stream, &pl));
+    pl.band_cols = (int32_t*)(c->ws + c->L.off_band_cols);
+    pl.band_cols_cap = c->prm.n_particles;
   }
   c->have_cost = true;
   if (c->graph) {
@@ -483,6 +495,8 @@ int dpso_set_cost(dpso_ctx* c, const double* dev_cost, int64_t ld) {
 }
 
 int dpso_scan_mode(dpso_ctx* c) { return c ? c->v.plan.mode : -1; }
+
+int dpso_scan_band(dpso_ctx* c) { return c ? c->v.plan.band_mode : -1; }
 
 int dpso_init_path(dpso_ctx* c) { return c ? c->init_path : -1; }
 
@@ -956,7 +970,10 @@ int dpso_best_exchange_batch(const double* dev_cost, int64_t ld, int32_t n,
   size_t bytes = round_up(2 * np * cnt, 256) + round_up(8 * np * cnt, 256) +
                  round_up(sizeof(TwoOptRes) * chunks * cnt + 4 * (2 + chunks * cnt), 256) +
                  round_up(16 * chunks, 256) + round_up(8 * cnt, 256) +
-                 round_up(6 * (int64_t)n * np, 256) + 256;  // fp32 + fp16 rows
+                 // fp32 + fp16 rows, band rows, stats, band column arrays
+                 round_up(round_up(6 * (int64_t)n * np, 256) +
+                              band_rows_bytes(n), 256) +
+                 256 + round_up(band_cols_bytes(n, cnt), 256);
   unsigned char* tmp = nullptr;
   CK(cudaMallocAsync(&tmp, bytes, s));
   size_t o = 0;
@@ -971,16 +988,24 @@ int dpso_best_exchange_batch(const double* dev_cost, int64_t ld, int32_t n,
                                     4 * (2 + chunks * cnt));
   int32_t* ctab = (int32_t*)take(16 * chunks);
   double* fsum = (double*)take(8 * cnt);
-  float* c32 = (float*)take(6 * (int64_t)n * np);
+  float* c32 = (float*)take(round_up(6 * (int64_t)n * np, 256) +
+                            band_rows_bytes(n));
   CostStats* st = (CostStats*)take(sizeof(CostStats));
+  int32_t* bcols = (int32_t*)take(band_cols_bytes(n, cnt));
   CK(cudaMemcpyAsync(ctab, tab.data(), 16 * chunks,
                      cudaMemcpyHostToDevice, s));
   int rc = to_u16_tours(dev_tours, n, count, t16, np, s);
   if (rc) return rc;
   CK(launch_tour_cost_rows(dev_cost, ld, n, t16, np, count, fsum, dc, s));
   TwoOptPlan pl;
+  unsigned char* band =
+      band_rows_bytes(n)
+          ? (unsigned char*)c32 + round_up(6 * (int64_t)n * np, 256)
+          : nullptr;
   CK(two_opt_prepare(dev_cost, ld, n, np, c32,
-                     (uint16_t*)(c32 + (size_t)n * np), st, s, &pl));
+                     (uint16_t*)(c32 + (size_t)n * np), band, st, s, &pl));
+  pl.band_cols = bcols;
+  pl.band_cols_cap = cnt;
   CK(launch_two_opt_batch(pl, n, (int32_t)np, t16, dc, count, res, chunks,
                           ctab, dev_delta, s));
   if (count > 0) k_u16_to_i32<<<count, 256, 0, s>>>(t16, n, count, dev_tours, np);

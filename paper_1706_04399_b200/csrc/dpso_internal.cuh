@@ -86,6 +86,17 @@ struct TwoOptPlan {
   // |F| spread <= 4 max_finite, so both V and V' order the pairs alike;
   // the apply re-evaluates the chosen pair in fp64.  vfrom == 0: none.
   double vfrom, vto;
+  // Row-per-lane band scan (k_two_opt_band.cu): 4 rotated int16 versions
+  // of round(C * band_scale); band_mode 1 EXACT, 2 FILTER (window
+  // band_win), 0 not used.  band_vfrom/vto: the virtual cap of those rows.
+  const unsigned char* band;
+  int band_line;
+  int band_mode;
+  double band_scale;
+  int band_win;
+  double band_vfrom, band_vto;
+  int32_t* band_cols;      // scratch: band_cols_cap x 2 x band_cw(n) ints
+  int64_t band_cols_cap;
 };
 
 struct TwoOptRes {
@@ -202,9 +213,11 @@ cudaError_t launch_cost_prep(const double* cost, int64_t ld, int32_t n,
 int two_opt_mode(const CostStats& st, int n, float* thr);
 // cost_prep + mode choice + optional fp16 rows; c16 may be null (no 16-bit
 // rows).  Synchronizes the stream once (reads the matrix statistics).
+// band: the band scan's row versions (band_rows_bytes(n)), may be null.
 cudaError_t two_opt_prepare(const double* cost, int64_t ld, int32_t n,
                             int64_t np, float* c32, uint16_t* c16,
-                            CostStats* st, cudaStream_t s, TwoOptPlan* pl);
+                            unsigned char* band, CostStats* st,
+                            cudaStream_t s, TwoOptPlan* pl);
 cudaError_t launch_nn(const double* cost, int64_t ld, int32_t n, int32_t start,
                       int32_t* out, cudaStream_t s);
 cudaError_t launch_pysum_tour(const double* cost, int64_t ld, int32_t n,
@@ -219,6 +232,22 @@ cudaError_t build_cost_sssp(const uint8_t* dev_occ, int nx, int ny, int nz,
                             double* host_vcost, int* bad_viewpoint,
                             cudaStream_t s);
 int two_opt_chunk_table(int32_t n, int32_t chunks, int32_t* tab);
+// band scan (k_two_opt_band.cu): two stages of 32 rows must fit shared
+// memory (n <= ~1330)
+constexpr int kBandMaxN = 2900;
+int band_line(int n);
+int band_cw(int n);
+int64_t band_rows_bytes(int n);  // 0 when the band scan cannot run
+int64_t band_cols_bytes(int n, int64_t count);
+cudaError_t band_prepare(const double* cost, int64_t ld, int32_t n,
+                         unsigned char* buf, double mx, bool integral,
+                         double vfrom, double vto, cudaStream_t s,
+                         TwoOptPlan* pl);
+cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
+                                const uint16_t* tours, const double* dcache,
+                                int32_t count, TwoOptRes* res, int32_t chunks,
+                                int32_t* ovf, const DevCtl* ctl,
+                                cudaStream_t s);
 int two_opt_pick_chunks(int32_t n, int32_t P);
 
 // Fitness in the reference's order (solver.py:48-54):

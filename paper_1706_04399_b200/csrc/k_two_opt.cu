@@ -1062,7 +1062,8 @@ int two_opt_mode(const CostStats& st, int n, float* thr) {
 
 cudaError_t two_opt_prepare(const double* cost, int64_t ld, int32_t n,
                             int64_t np, float* c32, uint16_t* c16,
-                            CostStats* st, cudaStream_t s, TwoOptPlan* pl) {
+                            unsigned char* band, CostStats* st,
+                            cudaStream_t s, TwoOptPlan* pl) {
   memset(pl, 0, sizeof *pl);
   pl->cost = cost;
   pl->ld = ld;
@@ -1099,6 +1100,13 @@ cudaError_t two_opt_prepare(const double* cost, int64_t ld, int32_t n,
       const double capped = pl->vto;
       memcpy(&h.maxabs_bits, &capped, sizeof capped);
     }
+  }
+  {
+    double mxc;
+    memcpy(&mxc, &h.maxabs_bits, sizeof mxc);
+    e = band_prepare(cost, ld, n, band, mxc, !h.nonintegral, pl->vfrom,
+                     pl->vto, s, pl);
+    if (e) return e;
   }
   pl->mode = two_opt_mode(h, n, &pl->thr);
   if (getenv("DPSO_SCAN_MODE")) pl->mode = atoi(getenv("DPSO_SCAN_MODE"));
@@ -1284,7 +1292,18 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
 #undef SCAN64
   };
   if ((parts & 1) && n >= 4 && tasks > 0) {
-    if (pl.mode == kScanFP64 || !pl.cost32) {
+    if (pl.band_mode) {
+      // row-per-lane band scan (k_two_opt_band.cu), then the FILTER
+      // overflow re-scan over the listed chunk tasks
+      if (pl.band_mode == 2) e = cudaMemsetAsync(a.ovf, 0, 4, s);
+      if (!e)
+        e = launch_two_opt_band(pl, n, np, tours, dcache, count, res, chunks,
+                                a.ovf, ctl, s);
+      if (!e && pl.band_mode == 2) {
+        k_two_opt_rescan64<<<2 * 148, 128, 0, s>>>(a);
+        e = cudaGetLastError();
+      }
+    } else if (pl.mode == kScanFP64 || !pl.cost32) {
       e = fp64_scan();
     } else {
       const int es = (pl.es == 2 && pl.cost16) ? 2 : 4;
@@ -1346,7 +1365,8 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
   b.cost = dcache_rw ? pl.cost : nullptr;
   b.ld = pl.ld;
   b.dcache = dcache_rw;
-  const bool capped = pl.vfrom > 0.0 && pl.mode != kScanFP64;
+  const bool capped = pl.band_mode ? pl.band_vfrom > 0.0
+                                   : pl.vfrom > 0.0 && pl.mode != kScanFP64;
   b.cost64 = capped ? pl.cost : nullptr;
   b.dcache_in = dcache;
   if (n < 4) {

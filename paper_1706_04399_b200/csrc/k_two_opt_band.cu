@@ -1,0 +1,686 @@
+// Best-improvement 2-opt scan, row-per-lane band formulation
+// (solver.py:88-106: delta(i,j) = ((C[a_i,a_j] + C[s_i,s_j]) - d_i) - d_j
+// over i < j, first row-major argmin, applied when < -1e-12).
+//
+// Write M[x][y] = C[a_x][a_y] (the tour-permuted matrix).  Then
+// delta(i, j) = M[i][j] + M[i+1][j+1] - d_i - d_j: a pair needs two entries
+// on one diagonal of M.
+//
+// One CTA owns a particle at a time and walks its pair rows in bands of 31.
+// The 32 cost rows a_i0 .. a_i0+31 of a band are staged in shared memory
+// (slot l = row a_{i0+l}) by 32 bulk copies.  Lane l of every warp owns pair
+// row i = i0 + l.  The warps of the CTA split the band's columns; a warp
+// sweeps its columns c in order, and at step c every lane gathers from its
+// own slot at the SAME offset a_c:
+//     G_l(c) = M[i0+l][c]        (one LDS per lane per step)
+// The pair (i0+l, c-1) is G_l(c-1) + G_{l+1}(c) - d_i - d_{c-1}: its first
+// term is the lane's previous gather, its second arrives from lane l+1 by
+// one shuffle.  So each pair costs one shared-memory gather, one shuffle and
+// one IADD3.
+//
+// Bank-conflict freedom: slot l's element a sits at byte l*(S+4) + 2a of the
+// stage (S a multiple of 128), i.e. in bank (l + a/2) mod 32 - a different
+// bank for every lane, whatever a is.  Bulk copies need 16-byte aligned
+// destinations, so the 4-byte rotation comes from the source: the int16 row
+// copy is kept in four versions in HBM/L2, version q shifted by 4q bytes,
+// and slot l copies version l mod 4 to l*S + 16*(l div 4).
+//
+// Arithmetic is integer: rows are int16 round(C * s) (s a power of two),
+// d values round(d * s).
+//   EXACT   integer matrix, max|C| <= 32767, s = 1: every delta is exact;
+//           each lane keeps its first minimum in (t, i, j) order, the
+//           warp-wide threshold is lexicographic, so the result is the
+//           reference's argmin bit for bit.
+//   FILTER  otherwise: |t - delta*s| <= 2 (four roundings of <= 1/2), so the
+//           reference's fp64 argmin and all its fp64 ties lie within 4 of
+//           the integer minimum (the fp64 rounding of delta is < 2^-30 in
+//           these units).  Each lane keeps the pairs within t_min + 4 as
+//           candidates (<= 4 per lane); at the end of a particle the
+//           candidates are re-evaluated with the reference expression in
+//           fp64, the structural pairs (i, i+1) exactly from d.  A lane whose
+//           list overflows sends the particle to the fp64 re-scan.
+// The structural pairs (i, i+1) are arithmetic no-ops (exactly 0 in EXACT)
+// and are not scanned; (0, n-1) is scanned (it is not a no-op for
+// asymmetric matrices).
+//
+// Pipeline: persistent CTAs (one per SM), particles blockIdx.x + k*grid;
+// two band stages (the next band's 32 rows stream in while this one is
+// scanned), refilled by the last warp done with a stage, so warps only
+// wait on the rows, not on each other; the particle's column arrays
+// (offsets 2*a_c and d values, k_band_cols) ride along with its band 0.
+#include <float.h>
+#include <limits.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "dpso_internal.cuh"
+#include "tma.cuh"
+
+namespace dpso {
+
+namespace {
+
+constexpr int kBandRows = 31;      // pair rows per band (lanes 0..30)
+constexpr int kBandCand = 4;       // FILTER candidates per lane
+constexpr int kBig = 0x40000000;   // dead column (D) / no candidate
+constexpr int kNone = 0x20000000;  // no pair seen yet
+constexpr int kBandWarps = 16;   // consumer warps
+constexpr int kMaxStages = 4;
+constexpr int kOvfTag = -2;        // as k_two_opt.cu's kOverflowTag
+constexpr int kLaneState = 3 + 2 * kBandCand;  // ints per lane
+
+struct BandArgs {
+  const double* cost;   // fp64 matrix (FILTER re-evaluation)
+  int64_t ld;
+  const unsigned char* rows;  // 4 rotated int16 versions (band_rows_bytes)
+  int line;             // bytes per row line
+  uint32_t slot;        // S: bytes between slots of a stage
+  int n, np, count, chunks;
+  const uint16_t* tours;
+  const double* dcache;
+  TwoOptRes* res;
+  const DevCtl* ctl;
+  int32_t* ovf;         // [0] count, [1..] tasks for the fp64 re-scan
+  double scale, vfrom, vto;
+  int win;              // FILTER window (integer units)
+  int cw;               // ints per column array
+  const int32_t* cols;  // count x [O | D] (k_band_cols)
+  int nst;              // stages in the row ring
+  int ncb;              // column buffers / result slots (particles)
+};
+
+__device__ __forceinline__ int lds_s16(uint32_t addr) {
+  int v;
+  asm volatile("ld.shared.s16 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ bool lex_lt(double d1, int i1, int j1, double d2,
+                                       int i2, int j2) {
+  if (d1 < d2) return true;
+  if (d2 < d1) return false;
+  return (i1 < i2) || (i1 == i2 && j1 < j2);
+}
+
+__device__ __forceinline__ void warp_lexmin(double& d, int& i, int& j) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double d2 = __shfl_xor_sync(0xffffffffu, d, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, i, o);
+    const int j2 = __shfl_xor_sync(0xffffffffu, j, o);
+    if (lex_lt(d2, i2, j2, d, i, j)) {
+      d = d2;
+      i = i2;
+      j = j2;
+    }
+  }
+}
+
+// Threshold of a lane for its row i: a later pair (t, i, j) hits when
+// t - D_i <= L - D_i.
+//   EXACT: beats the warp best (wb, wi) lexicographically: t < wb, or
+//          t == wb for a row above the best's (i < wi).
+//   FILTER: within the window lim = t_min + win.
+template <int MODE>
+__device__ __forceinline__ int lane_limit(bool live, int Di, int i, int w0,
+                                          int w1) {
+  if (!live) return INT_MIN;
+  if (MODE == 1) return w0 + Di - (i >= w1 ? 1 : 0);
+  return w0 + Di;
+}
+
+// Entered by the whole warp (the pre-test is warp-uniform); updates the
+// lane state (st: stride 32) and the warp state ws[0..1], returns the lane's
+// new limit.
+template <int MODE>
+__device__ __noinline__ int band_hit(int u0, int u1, int u2, int u3, int u4,
+                                     int u5, int u6, int u7, int c0, int i,
+                                     int Di, int L, int live, int win,
+                                     int* st, int* ws) {
+  const int uv[8] = {u0, u1, u2, u3, u4, u5, u6, u7};
+  const int lane = threadIdx.x & 31;
+  if (MODE == 1) {
+    int bt = st[0], bi = st[32], bj = st[64];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      // the lane's own pairs arrive in (i, j) order: its first minimum
+      const int t = uv[g] - Di;
+      if (live && t < bt) {
+        bt = t;
+        bi = i;
+        bj = c0 + g;
+      }
+    }
+    st[0] = bt;
+    st[32] = bi;
+    st[64] = bj;
+    int wt = bt, wi = bi;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int t2 = __shfl_xor_sync(0xffffffffu, wt, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, wi, o);
+      if (t2 < wt || (t2 == wt && i2 < wi)) {
+        wt = t2;
+        wi = i2;
+      }
+    }
+    if (lane == 0) {
+      ws[0] = wt;
+      ws[1] = wi;
+    }
+    return lane_limit<1>(live, Di, i, wt, wi);
+  }
+  int lb = st[0], nc = st[32], of = st[64];
+  int* cd = st + 96;
+  int* cij = cd + 32 * kBandCand;
+  int tv[8];
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    tv[g] = (live && uv[g] <= L) ? uv[g] - Di : kBig;
+    lb = min(lb, tv[g]);
+  }
+  int wm = lb;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+    wm = min(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+  const int lim = wm + win;
+  int w = 0;
+  for (int k = 0; k < nc; ++k) {
+    const int dv = cd[32 * k];
+    if (dv <= lim) {
+      cd[32 * w] = dv;
+      cij[32 * w] = cij[32 * k];
+      ++w;
+    }
+  }
+  nc = w;
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    if (tv[g] <= lim) {
+      if (nc < kBandCand) {
+        cd[32 * nc] = tv[g];
+        cij[32 * nc] = (i << 16) | (c0 + g);
+        ++nc;
+      } else {
+        of = 1;
+      }
+    }
+  }
+  st[0] = lb;
+  st[32] = nc;
+  st[64] = of;
+  if (lane == 0) ws[0] = lim;
+  return lane_limit<2>(live, Di, i, lim, 0);
+}
+
+// Column arrays of every particle, precomputed for the scan (one CTA per
+// particle): O[3 + k] = 2 a_k for k in [0, n] (a_n = a_0, byte offsets of
+// the gathers), zero elsewhere; D[c] = round(d_c s) for c < n, -kBig past
+// the end (dead columns).  The scan moves them to shared memory with one
+// bulk copy per particle.
+__global__ void k_band_cols(const uint16_t* tours, int np,
+                            const double* dcache, int n, int cw, int count,
+                            double scale, double vfrom, double vto,
+                            int32_t* out) {
+  const int p = blockIdx.x;
+  if (p >= count) return;
+  const uint16_t* t = tours + (size_t)p * np;
+  const double* dg = dcache + (size_t)p * np;
+  int32_t* O = out + (size_t)p * 2 * cw;
+  int32_t* D = O + cw;
+  for (int k = threadIdx.x; k < cw; k += blockDim.x) {
+    const int kk = k - 3;
+    O[k] = (kk >= 0 && kk <= n) ? 2 * (int)t[kk == n ? 0 : kk] : 0;
+    if (k < n) {
+      double d = dg[k];
+      if (vfrom > 0.0 && d == vfrom) d = vto;
+      D[k] = __double2int_rn(d * scale);
+    } else {
+      D[k] = -kBig;
+    }
+  }
+}
+
+// Scan of one 8-column group [c0, c0 + 8) of a band by one warp: the lane's
+// gathers G(c0 + 1 .. c0 + 8) at the group's offsets, the pairs (i, c0 + k)
+// = G_l(c0 + k) + G_{l+1}(c0 + k + 1) - D[c0 + k], the warp-uniform
+// pre-test against the lane limits.  MASK: columns c < i + 2 are dead
+// (the band's triangle).
+template <int MODE, bool MASK>
+__device__ __forceinline__ void band_group(const int* O, const int* D,
+                                           int c0, uint32_t R, int& prev,
+                                           int& L, int i, int Di, bool live,
+                                           int win, int* st, int* ws) {
+  const int4 oa = *reinterpret_cast<const int4*>(O + 4 + c0);
+  const int4 ob = *reinterpret_cast<const int4*>(O + 8 + c0);
+  const int4 da = *reinterpret_cast<const int4*>(D + c0);
+  const int4 db = *reinterpret_cast<const int4*>(D + c0 + 4);
+  const int off[8] = {oa.x, oa.y, oa.z, oa.w, ob.x, ob.y, ob.z, ob.w};
+  const int dv[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
+  int g[8], u[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) g[k] = lds_s16(R + (uint32_t)off[k]);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int nb = __shfl_down_sync(0xffffffffu, g[k], 1);
+    u[k] = (k ? g[k - 1] : prev) + nb - dv[k];
+  }
+  prev = g[7];
+  if (MASK) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (c0 + k < i + 2) u[k] = kBig;
+  }
+  const int mn = min(min(min(u[0], u[1]), min(u[2], u[3])),
+                     min(min(u[4], u[5]), min(u[6], u[7])));
+  if (__any_sync(0xffffffffu, mn <= L))
+    L = band_hit<MODE>(u[0], u[1], u[2], u[3], u[4], u[5], u[6], u[7], c0, i,
+                       Di, L, live, win, st, ws);
+}
+
+// Persistent CTAs: kBandWarps consumer warps + kProdWarps producer warps.
+// CTA b scans particles b, b + grid, ...; a particle's bands run in order
+// and band t sits in stage t % nst of a ring.  Producer warp w issues rows
+// 8w .. 8w+7 of every band (bulk copies; a warp's copies serialize on the
+// issue path, so four producers quarter the issue time of a band) once the
+// consumers have released the stage (empty barrier, one arrival per
+// consumer warp), and producer 0 adds the particle's column arrays to its
+// band 0 (full barrier: one expect-tx arrival per producer).  Consumer
+// warps walk the bands at their own pace; a particle's result is reduced by
+// the last consumer to finish it.  Column buffers and per-particle result
+// slots rotate over ncb >= 2 particles, enough that the producers' lead of
+// nst bands never reaches a buffer still in use.
+constexpr int kProdWarps = 4;
+constexpr int kMaxNcb = 8;
+
+template <int MODE>
+__global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
+    k_two_opt_band(BandArgs a) {
+  if (a.ctl && (a.ctl->done || a.ctl->improved)) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
+  __shared__ int s_fin[kMaxNcb], s_of[kMaxNcb];
+  __shared__ double s_rd[kMaxNcb][kBandWarps];
+  __shared__ int s_ri[kMaxNcb][kBandWarps], s_rj[kMaxNcb][kBandWarps];
+  __shared__ int s_ws[kBandWarps][2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = kBandWarps;
+  const int n = a.n, nst = a.nst, ncb = a.ncb;
+  const int nb = (n + kBandRows - 2) / kBandRows;  // bands: rows 0 .. n-2
+  const int nmine =
+      (int)blockIdx.x < a.count ? (a.count - 1 - (int)blockIdx.x) / gridDim.x + 1
+                                : 0;
+  if (nmine == 0) return;
+  const int total = nmine * nb;
+  const uint32_t S = a.slot;
+  unsigned char* rowbuf = smem;
+  int* cols = (int*)(smem + (size_t)nst * 32 * S);  // [ncb][O | D]
+  int* lstate = cols + ncb * 2 * a.cw;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  const uint32_t colbytes = (uint32_t)(2 * a.cw * 4);
+
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < nst; ++k) {
+      mbar_init(&full[k], kProdWarps);
+      mbar_init(&empty[k], NW);
+    }
+    fence_barrier_init();
+    for (int k = 0; k < kMaxNcb; ++k) s_fin[k] = s_of[k] = 0;
+  }
+  __syncthreads();
+
+  if (warp >= NW) {
+    // ---- producer warp pw: rows 8 pw .. 8 pw + 7 of every band
+    const int pw = warp - NW;
+    int band = 0, pl = 0;
+    for (int t = 0; t < total; ++t) {
+      const int s = t % nst, use = t / nst;
+      if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
+      const int pp = (int)blockIdx.x + pl * (int)gridDim.x;
+      const int i0 = band * kBandRows;
+      const int r0 = 8 * pw;
+      const int nr = max(0, min(8, n - i0 - r0));
+      const bool withcols = band == 0 && pw == 0;
+      if (lane == 0)
+        mbar_expect_tx(&full[s], (uint32_t)nr * (uint32_t)a.line +
+                                     (withcols ? colbytes : 0u));
+      __syncwarp();
+      if (lane < nr) {
+        fence_proxy_async();  // the consumers' reads of the stage first
+        const int l = r0 + lane;
+        const int city = a.tours[(size_t)pp * a.np + i0 + l];
+        const unsigned char* src =
+            a.rows + ((size_t)(l & 3) * n + city) * (size_t)a.line;
+        bulk_g2s(rowbuf + (size_t)s * 32 * S + (size_t)l * S + 16 * (l >> 2),
+                 src, (uint32_t)a.line, &full[s]);
+      }
+      if (withcols && lane == 0)
+        bulk_g2s(cols + (pl % ncb) * 2 * a.cw,
+                 a.cols + (size_t)pp * 2 * a.cw, colbytes, &full[s]);
+      if (++band == nb) {
+        band = 0;
+        ++pl;
+      }
+    }
+    return;
+  }
+
+  // ---- consumer warp
+  int* st = lstate + warp * kLaneState * 32 + lane;
+  int* ws = s_ws[warp];
+  auto reset_state = [&]() {
+    st[0] = MODE == 1 ? kNone : kBig;
+    st[32] = MODE == 1 ? INT_MAX : 0;
+    st[64] = MODE == 1 ? INT_MAX : 0;
+    if (lane == 0) {
+      ws[0] = kNone;
+      ws[1] = INT_MAX;
+    }
+    __syncwarp();
+  };
+  reset_state();
+  int band = 0, pl = 0;
+  for (int t = 0; t < total; ++t) {
+    const int s = t % nst;
+    const int pp = (int)blockIdx.x + pl * (int)gridDim.x;
+    const int i0 = band * kBandRows;
+    const int cb = pl % ncb;
+    mbar_wait(&full[s], (uint32_t)((t / nst) & 1));
+    const int* O = cols + cb * 2 * a.cw;
+    const int* D = O + a.cw;
+    const int i = i0 + lane;
+    const bool live = lane < kBandRows && i <= n - 2;
+    const int Di = live ? D[i] : 0;
+    const uint32_t R =
+        smem_u32(rowbuf + (size_t)s * 32 * S) + (uint32_t)lane * (S + 4u);
+    int L = lane_limit<MODE>(live, Di, i, ws[0], ws[1]);
+    const int cs = (i0 + 2) & ~7;
+    const int per = (((n - cs + NW - 1) / NW) + 7) & ~7;
+    const int cA = cs + warp * per, cB = min(n, cA + per);
+    if (cA < cB) {
+      int prev = lds_s16(R + (uint32_t)O[3 + cA]);
+      int c0 = cA;
+      for (; c0 < cB && c0 < i0 + 32; c0 += 8)
+        band_group<MODE, true>(O, D, c0, R, prev, L, i, Di, live, a.win, st,
+                               ws);
+      for (; c0 < cB; c0 += 8)
+        band_group<MODE, false>(O, D, c0, R, prev, L, i, Di, live, a.win, st,
+                                ws);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // the stage's reads are done
+    if (band == nb - 1) {
+      // ---- particle done: this warp's result, then the CTA's (last warp)
+      double bd = kInf;
+      int bi = INT_MAX, bj = INT_MAX;
+      const uint16_t* tour = a.tours + (size_t)pp * a.np;
+      const double* dg = a.dcache + (size_t)pp * a.np;
+      if (MODE == 1) {
+        if (st[0] < kNone) {
+          bd = (double)st[0];
+          bi = st[32];
+          bj = st[64];
+        }
+      } else if (__any_sync(0xffffffffu, st[64])) {
+        if (lane == 0) atomicOr(&s_of[cb], 1);
+      } else {
+        const int nc = st[32];
+        int wm = st[0];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+          wm = min(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+        const int keep = wm + a.win;
+        const int* cd = st + 96;
+        const int* cij = cd + 32 * kBandCand;
+        for (int k = 0; k < nc; ++k) {
+          if (cd[32 * k] <= keep) {
+            const int ci = cij[32 * k] >> 16, cj = cij[32 * k] & 0xFFFF;
+            const int ai = tour[ci], aj = tour[cj];
+            const int si = tour[ci + 1], sj = tour[cj + 1 == n ? 0 : cj + 1];
+            double v = __dadd_rn(a.cost[(size_t)ai * a.ld + aj],
+                                 a.cost[(size_t)si * a.ld + sj]);
+            v = __dsub_rn(v, dg[ci]);
+            v = __dsub_rn(v, dg[cj]);
+            if (lex_lt(v, ci, cj, bd, bi, bj)) {
+              bd = v;
+              bi = ci;
+              bj = cj;
+            }
+          }
+        }
+        // structural pairs, exactly from d (this warp's share of rows)
+        for (int ii = warp * 32 + lane; ii < n - 1; ii += NW * 32) {
+          const double d0 = dg[ii], d1 = dg[ii + 1];
+          double v = __dadd_rn(d0, d1);
+          v = __dsub_rn(v, d0);
+          v = __dsub_rn(v, d1);
+          if (lex_lt(v, ii, ii + 1, bd, bi, bj)) {
+            bd = v;
+            bi = ii;
+            bj = ii + 1;
+          }
+        }
+        if (warp == 0 && lane == 0 && n - 1 > 1) {  // (0, n-1): s = a_0
+          const int j = n - 1;
+          double v = __dadd_rn(a.cost[(size_t)tour[0] * a.ld + tour[j]],
+                               a.cost[(size_t)tour[1] * a.ld + tour[0]]);
+          v = __dsub_rn(v, dg[0]);
+          v = __dsub_rn(v, dg[j]);
+          if (lex_lt(v, 0, j, bd, bi, bj)) {
+            bd = v;
+            bi = 0;
+            bj = j;
+          }
+        }
+      }
+      warp_lexmin(bd, bi, bj);
+      int last = 0;
+      if (lane == 0) {
+        s_rd[cb][warp] = bd;
+        s_ri[cb][warp] = bi;
+        s_rj[cb][warp] = bj;
+        __threadfence_block();
+        last = atomicAdd(&s_fin[cb], 1) == NW - 1;
+        __threadfence_block();
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        double d = lane < NW ? s_rd[cb][lane] : kInf;
+        int ri = lane < NW ? s_ri[cb][lane] : INT_MAX;
+        int rj = lane < NW ? s_rj[cb][lane] : INT_MAX;
+        warp_lexmin(d, ri, rj);
+        TwoOptRes* out = a.res + (size_t)pp * a.chunks;
+        const int of = MODE == 2 ? s_of[cb] : 0;
+        int base = 0;
+        if (of && lane == 0) base = atomicAdd(&a.ovf[0], a.chunks);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        for (int c = lane; c < a.chunks; c += 32) {
+          if (of) {
+            out[c] = {kInf, kOvfTag, kOvfTag};
+            a.ovf[1 + base + c] = pp * a.chunks + c;
+          } else {
+            out[c] = c == 0 ? TwoOptRes{d, ri, rj}
+                            : TwoOptRes{kInf, INT_MAX, INT_MAX};
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          s_fin[cb] = 0;
+          s_of[cb] = 0;
+        }
+      }
+      reset_state();
+    }
+    if (++band == nb) {
+      band = 0;
+      ++pl;
+    }
+  }
+}
+
+// 4 rotated int16 versions of round(C * scale): version q, row r is the
+// line at byte (q n + r) line; element c at byte 4q + 2c of it.
+__global__ void k_cost_band16(const double* cost, int64_t ld, int n,
+                              int16_t* out, int line, double scale,
+                              double vfrom, double vto) {
+  const int per = line / 2;
+  const int64_t total = 4 * (int64_t)n * per;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / per;
+    const int c = (int)(e % per);
+    const int qv = (int)(row / n), r = (int)(row % n);
+    const int cc = c - 2 * qv;
+    int16_t v = 0;
+    if (cc >= 0 && cc < n) {
+      double x = cost[(int64_t)r * ld + cc];
+      if (vfrom > 0.0 && x == vfrom) x = vto;
+      v = (int16_t)__double2int_rn(x * scale);
+    }
+    out[e] = v;
+  }
+}
+
+uint32_t band_slot(int line) { return (uint32_t)round_up(line + 112, 128); }
+
+int band_nb(int n) { return (n + kBandRows - 2) / kBandRows; }
+
+// column buffers for nst stages: the producers run up to nst bands ahead
+int band_ncb(int n, int nst) {
+  const int nb = band_nb(n);
+  return std::min(kMaxNcb, std::max(2, (nst - 1 + nb - 1) / nb + 1));
+}
+
+size_t band_smem(int n, int nst) {
+  const int line = band_line(n);
+  return (size_t)nst * 32 * band_slot(line) +
+         (size_t)band_ncb(n, nst) * 2 * band_cw(n) * 4 +
+         (size_t)kBandWarps * kLaneState * 32 * 4;
+}
+
+constexpr size_t kBandSmemMax = 225 * 1024;
+
+// stages: as many as fit, up to kMaxStages
+int band_stages(int n) {
+  int nst = kMaxStages;
+  while (nst > 2 && band_smem(n, nst) > kBandSmemMax) --nst;
+  if (const char* e = getenv("DPSO_BAND_STAGES")) {
+    const int x = atoi(e);
+    if (x >= 2 && x <= kMaxStages && band_smem(n, x) <= kBandSmemMax) nst = x;
+  }
+  return nst;
+}
+
+}  // namespace
+
+int band_line(int n) { return (int)round_up(2 * (int64_t)n + 12, 16); }
+
+int band_cw(int n) { return (int)round_up(n + 16, 8); }
+
+int64_t band_rows_bytes(int n) {
+  if (n < 4 || n > kBandMaxN || band_smem(n, 2) > kBandSmemMax) return 0;
+  return 4 * (int64_t)n * band_line(n);
+}
+
+int64_t band_cols_bytes(int n, int64_t count) {
+  return band_rows_bytes(n) ? 8 * (int64_t)band_cw(n) * count : 0;
+}
+
+cudaError_t band_prepare(const double* cost, int64_t ld, int32_t n,
+                         unsigned char* buf, double mx, bool integral,
+                         double vfrom, double vto, cudaStream_t s,
+                         TwoOptPlan* pl) {
+  pl->band = nullptr;
+  pl->band_mode = 0;
+  if (!buf || band_rows_bytes(n) == 0) return cudaSuccess;
+  if (const char* e = getenv("DPSO_SCAN_BAND"))
+    if (atoi(e) == 0) return cudaSuccess;
+  // the knobs that select variants of the column-per-lane scan
+  // (k_two_opt.cu) select that scan
+  if (getenv("DPSO_SCAN_MODE") || getenv("DPSO_SCAN16") ||
+      getenv("DPSO_SCAN_NOPERSIST") || getenv("DPSO_SCAN_STREAM_ONLY") ||
+      getenv("DPSO_SCAN_NPL"))
+    return cudaSuccess;
+  if (!(mx > 1e-30 && mx < 1e30)) return cudaSuccess;
+  int mode;
+  double scale = 1.0;
+  if (integral && mx <= 32767.0) {
+    mode = 1;
+  } else {
+    mode = 2;
+    scale = ldexp(1.0, 14 - ilogb(mx));
+    while (mx * scale > 32767.0) scale *= 0.5;
+  }
+  // testing: FILTER on an EXACT-eligible matrix (same rows, scale 1)
+  if (const char* e = getenv("DPSO_BAND_MODE")) mode = atoi(e) == 2 ? 2 : mode;
+  const int line = band_line(n);
+  const int64_t total = 4 * (int64_t)n * (line / 2);
+  int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  k_cost_band16<<<std::max(blocks, 1), 256, 0, s>>>(
+      cost, ld, n, (int16_t*)buf, line, scale, vfrom, vto);
+  cudaError_t e = cudaGetLastError();
+  if (e) return e;
+  pl->band = buf;
+  pl->band_line = line;
+  pl->band_mode = mode;
+  pl->band_scale = scale;
+  pl->band_win = mode == 2 ? 4 : 0;
+  pl->band_vfrom = vfrom;
+  pl->band_vto = vto;
+  return cudaSuccess;
+}
+
+cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
+                                const uint16_t* tours, const double* dcache,
+                                int32_t count, TwoOptRes* res, int32_t chunks,
+                                int32_t* ovf, const DevCtl* ctl,
+                                cudaStream_t s) {
+  if (!pl.band_cols || count > pl.band_cols_cap) return cudaErrorInvalidValue;
+  BandArgs a;
+  memset(&a, 0, sizeof a);
+  a.cost = pl.cost;
+  a.ld = pl.ld;
+  a.rows = pl.band;
+  a.line = pl.band_line;
+  a.slot = band_slot(pl.band_line);
+  a.n = n;
+  a.np = np;
+  a.count = count;
+  a.chunks = chunks;
+  a.tours = tours;
+  a.dcache = dcache;
+  a.res = res;
+  a.ctl = ctl;
+  a.ovf = ovf;
+  a.scale = pl.band_scale;
+  a.vfrom = pl.band_vfrom;
+  a.vto = pl.band_vto;
+  a.win = pl.band_win;
+  a.cw = band_cw(n);
+  a.cols = pl.band_cols;
+  k_band_cols<<<count, 256, 0, s>>>(tours, np, dcache, n, a.cw, count,
+                                     a.scale, a.vfrom, a.vto, pl.band_cols);
+  cudaError_t e = cudaGetLastError();
+  if (e) return e;
+  a.nst = band_stages(n);
+  a.ncb = band_ncb(n, a.nst);
+  const size_t smem = band_smem(n, a.nst);
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int blocks = std::max(1, std::min(count, sms));
+  if (pl.band_mode == 1) {
+    e = set_dyn_smem((const void*)k_two_opt_band<1>, smem);
+    if (e) return e;
+    k_two_opt_band<1><<<blocks, (kBandWarps + kProdWarps) * 32, smem, s>>>(a);
+  } else {
+    e = set_dyn_smem((const void*)k_two_opt_band<2>, smem);
+    if (e) return e;
+    k_two_opt_band<2><<<blocks, (kBandWarps + kProdWarps) * 32, smem, s>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace dpso

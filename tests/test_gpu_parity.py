@@ -48,9 +48,18 @@ SCAN_MODES = {"fp64": "0", "exact32": "1", "filter32": "2"}
 
 
 def set_scan_mode(monkeypatch, mode):
-    # "<mode>" streams fp16 rows where the mode allows them (the default);
-    # "<mode>/rows32" forces the fp32 rows (DPSO_SCAN16=0)
+    # None: the default plan (the row-per-lane band scan where it applies);
+    # "band/filter": the band scan forced to FILTER on integer matrices;
+    # "column": the column-per-lane scan's default plan (DPSO_SCAN_BAND=0);
+    # "<mode>" the column scan in that mode, fp16 rows where the mode allows
+    # them; "<mode>/rows32" forces its fp32 rows (DPSO_SCAN16=0)
     if not mode:
+        return
+    if mode == "band/filter":
+        monkeypatch.setenv("DPSO_BAND_MODE", "2")
+        return
+    if mode == "column":
+        monkeypatch.setenv("DPSO_SCAN_BAND", "0")
         return
     base, _, rows = mode.partition("/")
     if base:
@@ -59,8 +68,8 @@ def set_scan_mode(monkeypatch, mode):
         monkeypatch.setenv("DPSO_SCAN16", "0")
 
 
-@pytest.fixture(params=[None, "/rows32", "fp64", "filter32",
-                        "filter32/rows32"])
+@pytest.fixture(params=[None, "band/filter", "column", "/rows32", "fp64",
+                        "filter32", "filter32/rows32"])
 def scan_mode(request, monkeypatch):
     set_scan_mode(monkeypatch, request.param)
     return request.param
