@@ -1296,6 +1296,8 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
       // row-per-lane band scan (k_two_opt_band.cu), then the FILTER
       // overflow re-scan over the listed chunk tasks
       if (pl.band_mode == 2) e = cudaMemsetAsync(a.ovf, 0, 4, s);
+      if (!e && getenv("DPSO_BAND_DEBUG"))  // unwritten results read as NaN
+        e = cudaMemsetAsync(res, 0xFF, sizeof(TwoOptRes) * count * chunks, s);
       if (!e)
         e = launch_two_opt_band(pl, n, np, tours, dcache, count, res, chunks,
                                 a.ovf, ctl, s);

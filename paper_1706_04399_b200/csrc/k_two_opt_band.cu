@@ -89,6 +89,7 @@ struct BandArgs {
   const int32_t* cols;  // count x [O | D] (k_band_cols)
   int nst;              // stages in the row ring
   int ncb;              // column buffers / result slots (particles)
+  int groups;           // warp groups scanning alternate bands (1 or 2)
 };
 
 __device__ __forceinline__ int lds_s16(uint32_t addr) {
@@ -282,9 +283,12 @@ __device__ __forceinline__ void band_group(const int* O, const int* D,
 
 // Persistent CTAs: kBandWarps consumer warps + kProdWarps producer warps.
 // CTA b scans particles b, b + grid, ...; a particle's bands run in order
-// and band t sits in stage t % nst of a ring.  Producer warp w issues rows
-// 8w .. 8w+7 of every band (bulk copies; a warp's copies serialize on the
-// issue path, so four producers quarter the issue time of a band) once the
+// and band t sits in stage t % nst of a ring; a particle's column arrays
+// have their own barrier (every warp group waits for them at its first band
+// of the particle).  Producer warp w issues its
+// 32 / kProdWarps rows of every band (bulk copies; a warp's copies
+// serialize on the issue path, so several producers divide the issue time
+// of a band) once the
 // consumers have released the stage (empty barrier, one arrival per
 // consumer warp), and producer 0 adds the particle's column arrays to its
 // band 0 (full barrier: one expect-tx arrival per producer).  Consumer
@@ -301,6 +305,7 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
   if (a.ctl && (a.ctl->done || a.ctl->improved)) return;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
+  __shared__ __align__(8) uint64_t colfull[kMaxNcb];
   __shared__ int s_fin[kMaxNcb], s_of[kMaxNcb];
   __shared__ double s_rd[kMaxNcb][kBandWarps];
   __shared__ int s_ri[kMaxNcb][kBandWarps], s_rj[kMaxNcb][kBandWarps];
@@ -324,28 +329,30 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
   if (threadIdx.x == 0) {
     for (int k = 0; k < nst; ++k) {
       mbar_init(&full[k], kProdWarps);
-      mbar_init(&empty[k], NW);
+      mbar_init(&empty[k], NW / a.groups);
     }
     fence_barrier_init();
+    for (int k = 0; k < ncb; ++k) mbar_init(&colfull[k], 1);
     for (int k = 0; k < kMaxNcb; ++k) s_fin[k] = s_of[k] = 0;
   }
   __syncthreads();
 
   if (warp >= NW) {
-    // ---- producer warp pw: rows 8 pw .. 8 pw + 7 of every band
+    // ---- producer warp pw: rows rpp pw .. rpp pw + rpp - 1 of every band
     const int pw = warp - NW;
-    int band = 0, pl = 0;
+    constexpr int rpp = 32 / kProdWarps;  // rows per producer warp
+    int band = 0, pl = 0, cb = 0, s = 0, use = 0;
     for (int t = 0; t < total; ++t) {
-      const int s = t % nst, use = t / nst;
-      if (use > 0) mbar_wait(&empty[s], (uint32_t)((use - 1) & 1));
+      if (use > 0) mbar_wait_sleep(&empty[s], (uint32_t)((use - 1) & 1));
       const int pp = (int)blockIdx.x + pl * (int)gridDim.x;
       const int i0 = band * kBandRows;
-      const int r0 = 8 * pw;
-      const int nr = max(0, min(8, n - i0 - r0));
+      const int r0 = rpp * pw;
+      const int nr = max(0, min(rpp, n - i0 - r0));
       const bool withcols = band == 0 && pw == 0;
-      if (lane == 0)
-        mbar_expect_tx(&full[s], (uint32_t)nr * (uint32_t)a.line +
-                                     (withcols ? colbytes : 0u));
+      if (lane == 0) {
+        mbar_expect_tx(&full[s], (uint32_t)nr * (uint32_t)a.line);
+        if (withcols) mbar_expect_tx(&colfull[cb], colbytes);
+      }
       __syncwarp();
       if (lane < nr) {
         fence_proxy_async();  // the consumers' reads of the stage first
@@ -357,11 +364,16 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
                  src, (uint32_t)a.line, &full[s]);
       }
       if (withcols && lane == 0)
-        bulk_g2s(cols + (pl % ncb) * 2 * a.cw,
-                 a.cols + (size_t)pp * 2 * a.cw, colbytes, &full[s]);
+        bulk_g2s(cols + cb * 2 * a.cw, a.cols + (size_t)pp * 2 * a.cw,
+                 colbytes, &colfull[cb]);
+      if (++s == nst) {
+        s = 0;
+        ++use;
+      }
       if (++band == nb) {
         band = 0;
         ++pl;
+        if (++cb == ncb) cb = 0;
       }
     }
     return;
@@ -381,13 +393,32 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
     __syncwarp();
   };
   reset_state();
-  int band = 0, pl = 0;
-  for (int t = 0; t < total; ++t) {
-    const int s = t % nst;
+  // warp groups: group g scans bands g, g + G, ... (G = a.groups), its
+  // NWg warps splitting each band's columns
+  const int G = a.groups, NWg = NW / G;
+  const int grp = warp / NWg, wl = warp - grp * NWg;
+  int band = 0, pl = 0, cb = 0, s = 0, use = 0, cuse = 0;
+  auto step = [&]() {  // to the next band of the sequence
+    if (++s == nst) {
+      s = 0;
+      ++use;
+    }
+    if (++band == nb) {
+      band = 0;
+      ++pl;
+      if (++cb == ncb) {
+        cb = 0;
+        ++cuse;
+      }
+    }
+  };
+  for (int k = 0; k < grp; ++k) step();
+  for (int t = grp; t < total; t += G) {
     const int pp = (int)blockIdx.x + pl * (int)gridDim.x;
     const int i0 = band * kBandRows;
-    const int cb = pl % ncb;
-    mbar_wait(&full[s], (uint32_t)((t / nst) & 1));
+    // the particle's column arrays (its first band for this warp), rows
+    if (band < G) mbar_wait_sleep(&colfull[cb], (uint32_t)(cuse & 1));
+    mbar_wait_sleep(&full[s], (uint32_t)(use & 1));
     const int* O = cols + cb * 2 * a.cw;
     const int* D = O + a.cw;
     const int i = i0 + lane;
@@ -397,8 +428,8 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
         smem_u32(rowbuf + (size_t)s * 32 * S) + (uint32_t)lane * (S + 4u);
     int L = lane_limit<MODE>(live, Di, i, ws[0], ws[1]);
     const int cs = (i0 + 2) & ~7;
-    const int per = (((n - cs + NW - 1) / NW) + 7) & ~7;
-    const int cA = cs + warp * per, cB = min(n, cA + per);
+    const int per = ((((n - cs) + NWg - 1) / NWg) + 7) & ~7;
+    const int cA = cs + wl * per, cB = min(n, cA + per);
     if (cA < cB) {
       int prev = lds_s16(R + (uint32_t)O[3 + cA]);
       int c0 = cA;
@@ -411,7 +442,9 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);  // the stage's reads are done
-    if (band == nb - 1) {
+    // this warp's last band of the particle: the next band of its group is
+    // in a later particle (nb >= G, so every group has a band in each)
+    if (band + G >= nb || t + G >= total) {
       // ---- particle done: this warp's result, then the CTA's (last warp)
       double bd = kInf;
       int bi = INT_MAX, bj = INT_MAX;
@@ -513,10 +546,7 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
       }
       reset_state();
     }
-    if (++band == nb) {
-      band = 0;
-      ++pl;
-    }
+    for (int k = 0; k < G; ++k) step();
   }
 }
 
@@ -547,10 +577,23 @@ uint32_t band_slot(int line) { return (uint32_t)round_up(line + 112, 128); }
 
 int band_nb(int n) { return (n + kBandRows - 2) / kBandRows; }
 
-// column buffers for nst stages: the producers run up to nst bands ahead
+// column buffers / result slots for nst stages: no warp runs more than nst
+// bands ahead of another, so (ncb - 1) nb >= nst keeps a particle's buffers
+// until every warp is past it
 int band_ncb(int n, int nst) {
   const int nb = band_nb(n);
-  return std::min(kMaxNcb, std::max(2, (nst - 1 + nb - 1) / nb + 1));
+  return std::min(kMaxNcb, std::max(2, (nst + nb - 1) / nb + 1));
+}
+
+// warp groups: two groups scan alternate bands when two stages can be
+// scanned while the others load (nst == 4) and every group has a band in
+// every particle
+int band_groups(int n, int nst) {
+  if (const char* e = getenv("DPSO_BAND_GROUPS")) {
+    const int g = atoi(e);
+    if (g == 1 || (g == 2 && nst % 2 == 0 && band_nb(n) >= 2)) return g;
+  }
+  return nst == 4 && band_nb(n) >= 2 ? 2 : 1;
 }
 
 size_t band_smem(int n, int nst) {
@@ -666,6 +709,7 @@ cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
   if (e) return e;
   a.nst = band_stages(n);
   a.ncb = band_ncb(n, a.nst);
+  a.groups = band_groups(n, a.nst);
   const size_t smem = band_smem(n, a.nst);
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess)

@@ -57,4 +57,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// try_wait with a suspend-time hint: a waiting warp sleeps instead of
+// spinning on issue slots the working warps of its SM need
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar,
+                                                uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+
 }  // namespace dpso

@@ -149,6 +149,18 @@ def test_band_more_particles_than_ctas(pkg):
         check(pkg, cost / 7.0, perms(rng, P, n), ("multi-f", n, P), 64, rng)
 
 
+def test_band_many_particles_per_cta(pkg):
+    # ~100 particles per CTA, two warp groups on alternate bands (n = 300,
+    # 500: four stages), the column arrays of a particle arriving on their
+    # own barrier
+    rng = np.random.default_rng(43)
+    for n, P in ((300, 12000), (500, 16384)):
+        side = int(math.ceil(math.sqrt(n)))
+        cost = grid(n) if n == 500 else np.floor(
+            random_euclidean_matrix(n, rng) * 100.0)
+        check(pkg, cost, perms(rng, P, n), ("many", n, P), 48, rng)
+
+
 def test_band_whole_solves_match_oracle(pkg):
     rng = np.random.default_rng(41)
     for n, P, kind in ((60, 20, "int"), (90, 16, "euclid")):
