@@ -90,6 +90,7 @@ struct BandArgs {
   int nst;              // stages in the row ring
   int ncb;              // column buffers / result slots (particles)
   int groups;           // warp groups scanning alternate bands (1 or 2)
+  int probe;            // debug: 1 = stream the bands, skip the pairs
 };
 
 __device__ __forceinline__ int lds_s16(uint32_t addr) {
@@ -321,7 +322,8 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
   const int total = nmine * nb;
   const uint32_t S = a.slot;
   unsigned char* rowbuf = smem;
-  int* cols = (int*)(smem + (size_t)nst * 32 * S);  // [ncb][O | D]
+  const uint32_t stage_bytes = 32 * S + 128;
+  int* cols = (int*)(smem + (size_t)nst * stage_bytes);  // [ncb][O | D]
   int* lstate = cols + ncb * 2 * a.cw;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
   const uint32_t colbytes = (uint32_t)(2 * a.cw * 4);
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
     constexpr int rpp = 32 / kProdWarps;  // rows per producer warp
     int band = 0, pl = 0, cb = 0, s = 0, use = 0;
     for (int t = 0; t < total; ++t) {
-      if (use > 0) mbar_wait_sleep(&empty[s], (uint32_t)((use - 1) & 1));
+      if (use > 0) mbar_wait_backoff(&empty[s], (uint32_t)((use - 1) & 1));
       const int pp = (int)blockIdx.x + pl * (int)gridDim.x;
       const int i0 = band * kBandRows;
       const int r0 = rpp * pw;
@@ -360,7 +362,7 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
         const int city = a.tours[(size_t)pp * a.np + i0 + l];
         const unsigned char* src =
             a.rows + ((size_t)(l & 3) * n + city) * (size_t)a.line;
-        bulk_g2s(rowbuf + (size_t)s * 32 * S + (size_t)l * S + 16 * (l >> 2),
+        bulk_g2s(rowbuf + (size_t)s * stage_bytes + (size_t)l * S + 16 * (l >> 2),
                  src, (uint32_t)a.line, &full[s]);
       }
       if (withcols && lane == 0)
@@ -396,7 +398,8 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
   // warp groups: group g scans bands g, g + G, ... (G = a.groups), its
   // NWg warps splitting each band's columns
   const int G = a.groups, NWg = NW / G;
-  const int grp = warp / NWg, wl = warp - grp * NWg;
+  const int lgw = G == 2 ? 3 : 4;  // log2 NWg
+  const int grp = warp >> lgw, wl = warp - (grp << lgw);
   int band = 0, pl = 0, cb = 0, s = 0, use = 0, cuse = 0;
   auto step = [&]() {  // to the next band of the sequence
     if (++s == nst) {
@@ -425,12 +428,12 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
     const bool live = lane < kBandRows && i <= n - 2;
     const int Di = live ? D[i] : 0;
     const uint32_t R =
-        smem_u32(rowbuf + (size_t)s * 32 * S) + (uint32_t)lane * (S + 4u);
+        smem_u32(rowbuf + (size_t)s * stage_bytes) + (uint32_t)lane * (S + 4u);
     int L = lane_limit<MODE>(live, Di, i, ws[0], ws[1]);
     const int cs = (i0 + 2) & ~7;
-    const int per = ((((n - cs) + NWg - 1) / NWg) + 7) & ~7;
+    const int per = ((((n - cs) + NWg - 1) >> lgw) + 7) & ~7;
     const int cA = cs + wl * per, cB = min(n, cA + per);
-    if (cA < cB) {
+    if (cA < cB && !a.probe) {
       int prev = lds_s16(R + (uint32_t)O[3 + cA]);
       int c0 = cA;
       for (; c0 < cB && c0 < i0 + 32; c0 += 8)
@@ -573,7 +576,9 @@ __global__ void k_cost_band16(const double* cost, int64_t ld, int n,
   }
 }
 
-uint32_t band_slot(int line) { return (uint32_t)round_up(line + 112, 128); }
+// slot l of a stage starts at l S + 16 (l div 4): S >= line keeps slots
+// apart (the stagger never decreases); a stage spans 32 S + 128 bytes
+uint32_t band_slot(int line) { return (uint32_t)round_up(line, 128); }
 
 int band_nb(int n) { return (n + kBandRows - 2) / kBandRows; }
 
@@ -598,7 +603,7 @@ int band_groups(int n, int nst) {
 
 size_t band_smem(int n, int nst) {
   const int line = band_line(n);
-  return (size_t)nst * 32 * band_slot(line) +
+  return (size_t)nst * (32 * band_slot(line) + 128) +
          (size_t)band_ncb(n, nst) * 2 * band_cw(n) * 4 +
          (size_t)kBandWarps * kLaneState * 32 * 4;
 }
@@ -710,6 +715,7 @@ cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
   a.nst = band_stages(n);
   a.ncb = band_ncb(n, a.nst);
   a.groups = band_groups(n, a.nst);
+  if (const char* e = getenv("DPSO_BAND_PROBE")) a.probe = atoi(e);
   const size_t smem = band_smem(n, a.nst);
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess)

@@ -73,4 +73,23 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar,
       : "memory");
 }
 
+// producer-side wait: poll with a short sleep between tries (a producer is
+// usually far ahead of its consumers; its polls would take their slots)
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar,
+                                                  uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  for (;;) {
+    asm volatile(
+        "{\n.reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(256);
+  }
+}
+
 }  // namespace dpso

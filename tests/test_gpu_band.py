@@ -130,13 +130,13 @@ def test_band_largest_n(pkg):
     # the largest n whose two stages fit shared memory, and the first n
     # past it (column scan)
     rng = np.random.default_rng(29)
-    for n, kind in ((1000, 2), (1300, 2), (1400, 0)):
+    for n, kind in ((1000, 2), (1400, 2), (2000, 0)):
         cost = random_euclidean_matrix(n, rng)
         assert band_kind(pkg, cost) == kind, n
         check(pkg, cost, perms(rng, 300, n), ("large", n), 6, rng)
-    cost = np.floor(random_euclidean_matrix(1300, rng) * 1000.0)
+    cost = np.floor(random_euclidean_matrix(1400, rng) * 1000.0)
     assert band_kind(pkg, cost) == 1
-    check(pkg, cost, perms(rng, 300, 1300), ("large-int", 1300), 6, rng)
+    check(pkg, cost, perms(rng, 300, 1400), ("large-int", 1400), 6, rng)
 
 
 def test_band_more_particles_than_ctas(pkg):

@@ -78,11 +78,14 @@ def main():
         cost = matrix(n, kind)
         gens = int(os.environ.get("AB_GENS", "8"))
         rec = {"n": n, "P": P, "matrix": kind}
-        for tag, env in (("band", {}), ("column", {"DPSO_SCAN_BAND": "0"})):
+        variants = [("band", {}), ("column", {"DPSO_SCAN_BAND": "0"})]
+        if os.environ.get("AB_PROBE"):
+            variants.append(("band_stream_only", {"DPSO_BAND_PROBE": "1"}))
+        for tag, env in variants:
             band, ms = time_scan(n, P, cost, gens, env)
             rec[tag] = {"scan_kind": band, "scan_apply_ms": ms}
         pairs = P * n * (n - 1) / 2
-        for tag in ("band", "column"):
+        for tag in [v[0] for v in variants]:
             ms = rec[tag]["scan_apply_ms"]
             if ms:
                 rec[tag]["gpairs_per_s"] = pairs / ms / 1e6
