@@ -229,7 +229,8 @@ def run_reference(args, cfg_name, cfg):
         "ms_per_step": 1e3 * tmax / steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": config_dict(cfg_name, cfg, args),
+        "config": config_dict(cfg_name, cfg, args,
+                              int(os.environ.get("WORLD_SIZE", args.gpus))),
         "cpu_baseline": {
             "value": value, "unit": UNIT, "cores": cores, "kind": "port",
             "sample": (f"{cores} concurrent processes of the oracle port "
@@ -244,30 +245,34 @@ def run_reference(args, cfg_name, cfg):
     print(json.dumps(line), flush=True)
 
 
-def config_dict(cfg_name, cfg, args):
+def config_dict(cfg_name, cfg, args, world=1):
     return {"workload": cfg["workload"], "config": cfg_name, "n": cfg["n"],
             "particles_per_gpu": cfg["P"], "global_particles":
-                cfg["P"] * args.gpus,
+                cfg["P"] * world,
             "generation_schedule": cfg["G"],
-            "parallelism": f"islands{args.gpus}" if args.gpus > 1 else "1gpu",
-            "exchange_every": args.exchange_every if args.gpus > 1 else None,
+            "parallelism": f"islands{world}" if world > 1 else "1gpu",
+            "exchange_every": args.exchange_every if world > 1 else None,
             "rng": {"numpy": "numpy-pcg64-exact",
                     "philox": "philox4x32-10"}[RNG],
             "l2": "flushed between timed steps (256 MiB write)"}
 
 
 # --------------------------------------------------------------- our arm
-def kernels_per_generation(cfg):
+def kernels_per_generation(cfg, band=0):
     """(kernels every generation's CUDA graph launches, extra kernels of a
     mutating generation).  Generations with gen % mutation_period != 0 run
     a graph without the mutation call; device flags make kernels a
     generation does not need (the 2-opt scan when gbest improved, ...) exit
-    at entry, but they still launch."""
+    at entry, but they still launch.  band: dpso_scan_band (1/2: the band
+    scan and its column-record kernel)."""
     k = 1 + 1 + 1  # gen_begin, update, fitness (with the pbest copy)
     k += 1         # select
     if cfg.get("ee", True):
-        # scan (FILTER32 adds the overflow re-scan), apply, finalize
-        k += (1 if cfg["matrix"] in ("grid", "euclid_int", "wall") else 2)
+        exact = (band == 1 if band else
+                 cfg["matrix"] in ("grid", "euclid_int", "wall"))
+        # [column records +] scan (FILTER adds the overflow re-scan), apply,
+        # finalize
+        k += (2 if band else 1) + (0 if exact else 1)
         k += 2
     m = 6          # mutation: hash, rank, dedupe, verify, lists, copy
     if RNG == "philox":
@@ -278,20 +283,26 @@ def kernels_per_generation(cfg):
     return k, m
 
 
-def gpu_launch_count(cfg, first_gen, gens, period=3):
-    base, mut = kernels_per_generation(cfg)
+def gpu_launch_count(cfg, first_gen, gens, period=3, band=0):
+    base, mut = kernels_per_generation(cfg, band)
     n_mut = sum(1 for g in range(first_gen, first_gen + gens)
                 if g % period == 0)
     return base * gens + mut * n_mut
 
 
-def scan_floors(cost, params, seed_body, n_seed, P, gens=6):
+def scan_floors(cost, params, seed_body, n_seed, P, gens=6, band=0):
+    """The scan's own floor, live: the same launch reduced to its row stream
+    (band scan: DPSO_BAND_PROBE=1; column scan: DPSO_SCAN_STREAM_ONLY=1,
+    and =2 for the stream plus every pair's gathers)."""
     import numpy as np
     from paper_1706_04399_b200 import DiscreteSwarmSolver
     from paper_1706_04399_b200.solver import numpy_stream_states
     out = {}
-    for name, val in (("stream_only_ms", "1"), ("stream_gathers_ms", "2")):
-        os.environ["DPSO_SCAN_STREAM_ONLY"] = val
+    probes = ((("stream_only_ms", "DPSO_BAND_PROBE", "1"),) if band else
+              (("stream_only_ms", "DPSO_SCAN_STREAM_ONLY", "1"),
+               ("stream_gathers_ms", "DPSO_SCAN_STREAM_ONLY", "2")))
+    for name, var, val in probes:
+        os.environ[var] = val
         try:
             p = dict(params, max_generations=gens + 4,
                      stall_generations=gens + 4)
@@ -314,8 +325,35 @@ def scan_floors(cost, params, seed_body, n_seed, P, gens=6):
             finally:
                 ctx.close()
         finally:
-            os.environ.pop("DPSO_SCAN_STREAM_ONLY", None)
+            os.environ.pop(var, None)
     return out
+
+
+def load_gather_peaks():
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02",
+                               "gather_peaks.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+def row_stream_peak(peaks, line):
+    """Measured L2 -> shared-memory bulk-copy bandwidth (GB/s) for rows of
+    `line` bytes, 32 rows per stage, 4 issuing warps (tools/gather_peaks.cu,
+    profiles/r02/gather_peaks.json).  The rate is per copy at these sizes,
+    so other row sizes scale from the nearest measured one, capped at the
+    largest measured bandwidth."""
+    meas = {}
+    for k, v in peaks.items():
+        if k.startswith("bulk_rows") and "_warps4_" in k:
+            size = int(k[len("bulk_rows"):].split("_")[0])
+            meas[size] = max(meas.get(size, 0.0), float(v["gbs"]))
+    if not meas:
+        return None, None
+    near = min(meas, key=lambda z: abs(math.log(z / line)))
+    cap = max(meas.values())
+    return min(cap, meas[near] * line / near), near
 
 
 def run_ours(args, cfg_name, cfg):
@@ -347,6 +385,7 @@ def run_ours(args, cfg_name, cfg):
     solver = DiscreteSwarmSolver(**params)
     seed_body, n_seed = solver._seed(n)
     ctx = solver._make_context(cost)
+    band = int(ctx.lib.dpso_scan_band(ctx.h))
     if RNG == "numpy":
         ctx.set_streams(numpy_stream_states(params["random_state"], P + 2))
     ctx.init(seed_body, n_seed)
@@ -393,6 +432,47 @@ def run_ours(args, cfg_name, cfg):
     phases = {k: v / prof_gens for k, v in zip(names, phase_ms)}
     ctx.close()
 
+    # e2e through the public API with host buffers (H2D of the matrix and
+    # RNG states, D2H of tour + convergence inside the timed region); with
+    # N ranks: the island model's public API (IslandSolver, one island per
+    # rank, gbest exchange every --exchange-every generations), timed
+    # between barriers, max over ranks
+    e2e, e2e_solver, e2e_params = None, None, None
+    if not args.no_e2e:
+        Ge = cfg["G"]
+        ep = gpu_params(cfg, P, Ge, 7)
+        if seed_tour is not None:
+            ep["seed_tour"] = seed_tour
+        if world > 1:
+            from paper_1706_04399_b200 import IslandSolver
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            s = IslandSolver(exchange_every=args.exchange_every,
+                             **ep).fit(cost)
+            torch.cuda.synchronize()
+            dt_t = torch.tensor([time.perf_counter() - t0],
+                                dtype=torch.float64, device=dev)
+            dist.all_reduce(dt_t, op=dist.ReduceOp.MAX)
+            dt = float(dt_t.item())
+            api = (f"IslandSolver(exchange_every={args.exchange_every})"
+                   f".fit(host numpy matrix), {world} ranks")
+        else:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            s = DiscreteSwarmSolver(**ep).fit(cost)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            api = "DiscreteSwarmSolver.fit(host numpy matrix)"
+        gens = s.n_generations_
+        h2d = cost.nbytes + (P + 2) * 48 + (2 * n if seed_tour else 0)
+        d2h = 4 * (n + 1) + 8 * (gens + 1)
+        e2e = {"value": P * world * gens / dt, "unit": UNIT,
+                       "h2d_bytes_per_step": h2d * world / gens,
+                       "d2h_bytes_per_step": d2h * world / gens,
+                       "generations": gens, "wall_s": dt, "api": api}
+        e2e_solver, e2e_params = s, ep
+
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -407,78 +487,91 @@ def run_ours(args, cfg_name, cfg):
         pass
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    scan_bytes = P * 4.0 * n * (n - 1)  # 8 B x n(n-1)/2 unique pair entries
+    gpk = load_gather_peaks()
+    scan_alg = P * 4.0 * n * (n - 1)  # 8 B x n(n-1)/2 pairs
     upd_bytes = P * 26.0 * n           # update 16n + fitness 10n
-    if cfg.get("ee", True) and fired > 0:
-        dom, dur_ms, alg = "two_opt_scan", phase_ms[3] / fired, scan_bytes
-    else:
-        dom, dur_ms, alg = "update", phase_ms[0] / prof_gens, upd_bytes
-    achieved = alg / (dur_ms / 1e3) / 1e9
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             tr = json.load(fh)
-        key = f"{cfg_name}:{dom}"
-        if key in tr:
-            traffic = tr[key]
     except Exception:
-        pass
+        tr = {}
+    if cfg.get("ee", True) and fired > 0:
+        dom, dur_ms = "two_opt_scan", phase_ms[3] / fired
+        traffic = tr.get(f"{cfg_name}:{dom}")
+        # the binding resource of the scan: the cost rows it stages from L2
+        # into shared memory.  Band scan: every row of the particle's tour
+        # once, as int16 lines of round_up(2n + 12, 16) B (33 bands of 32
+        # rows at n = 1000: the 31-row bands overlap by one row).  Column
+        # scan: fp16/fp32 rows once per task.
+        if band:
+            line_b = int(math.ceil((2 * n + 12) / 16.0) * 16)
+            nbands = (n + 29) // 31
+            staged = float(P) * nbands * min(32, n) * line_b
+        else:
+            line_b = int(math.ceil(2 * n / 16.0) * 16)
+            staged = float(P) * (n + 1) * line_b * max(1, -(-n // 1024))
+        achieved = staged / (dur_ms / 1e3) / 1e9
+        peak, near = row_stream_peak(gpk, line_b)
+        roof = {"bound": "l2", "kernel": dom,
+                "scan": ("band-exact", "band-filter")[band - 1]
+                if band else "column",
+                "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if peak else None,
+                "traffic": traffic,
+                "staged_bytes_per_launch": staged,
+                "algorithmic_fp64_bytes_per_launch": scan_alg,
+                "algorithmic_fp64_gbs": scan_alg / (dur_ms / 1e3) / 1e9,
+                "avg_launch_ms": dur_ms,
+                "peak_source": (f"measured: L2->shared bulk-copy row stream, "
+                                f"{near}-B rows, 32 per stage, 4 issuing "
+                                f"warps (profiles/r02/gather_peaks.json, "
+                                f"tools/gather_peaks.cu), scaled to "
+                                f"{line_b}-B rows"),
+                "l2_random_gather_f64_gbs":
+                    gpk.get("gather_f64_8MB", {}).get("useful_gbs"),
+                "note": "the matrix is L2-resident and each staged row "
+                        "serves a whole band of pairs, so the kernel is "
+                        "bound by the L2->SMEM row stream and SM issue, "
+                        "not by HBM"}
+    else:
+        dom, dur_ms, alg = "update", phase_ms[0] / prof_gens, upd_bytes
+        traffic = tr.get(f"{cfg_name}:{dom}")
+        achieved = alg / (dur_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved,
+                "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": traffic, "algorithmic_bytes_per_launch": alg,
+                "avg_launch_ms": dur_ms,
+                "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": K, "warmup": W, "ms_per_step": total_ms / K,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": config_dict(cfg_name, cfg, args),
-        "gpu_launches": gpu_launch_count(cfg, W + 1, K),
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved,
-                     "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": traffic,
-                     "algorithmic_bytes_per_launch": alg,
-                     "avg_launch_ms": dur_ms,
-                     "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json"
-                                    "); the cost matrix is L2-resident, so "
-                                    "this kernel is L2-gather bound"},
+        "config": config_dict(cfg_name, cfg, args, world),
+        "gpu_launches": gpu_launch_count(cfg, W + 1, K, band=band),
+        "roofline": roof,
         "phase_ms_per_gen": phases,
         "two_opt_fired": f"{fired}/{prof_gens}",
     }
-    # the scan's own floors, live: the same kernel reduced to its row stream
-    # and to the stream plus every pair's shared-memory gathers
-    # (DPSO_SCAN_STREAM_ONLY probes, tools/scan_floors.py)
+    # the scan's own floor, live (the same launch reduced to its row stream)
     if cfg.get("ee", True) and world == 1 and dom == "two_opt_scan":
         try:
-            fl = scan_floors(cost, params, seed_body, n_seed, P)
-            if fl.get("stream_gathers_ms"):
-                # the fraction of the kernel's own gather floor it reaches
-                fl["frac_of_stream_gathers"] = fl["stream_gathers_ms"] / dur_ms
+            fl = scan_floors(cost, params, seed_body, n_seed, P, band=band)
+            if fl.get("stream_only_ms"):
+                fl["frac_of_stream_only"] = fl["stream_only_ms"] / dur_ms
             if fl:
                 line["roofline"]["floors"] = fl
         except Exception as exc:  # a probe failing must not lose the line
             line["roofline"]["floors"] = {"error": str(exc)[:200]}
     # clocks
     line["clocks"] = clk.summary()
+    if e2e is not None:
+        line["e2e"] = e2e
 
-    # e2e through the public API with host buffers (H2D of the matrix and
-    # RNG states, D2H of tour + convergence inside the timed region)
     if not args.no_e2e:
-        Ge = cfg["G"]
-        ep = gpu_params(cfg, P, Ge, 7)
-        if seed_tour is not None:
-            ep["seed_tour"] = seed_tour
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        s = DiscreteSwarmSolver(**ep).fit(cost)
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        gens = s.n_generations_
-        h2d = cost.nbytes + (P + 2) * 48 + (2 * n if seed_tour else 0)
-        d2h = 4 * (n + 1) + 8 * (gens + 1)
-        line["e2e"] = {"value": P * gens / dt, "unit": UNIT,
-                       "h2d_bytes_per_step": h2d / gens,
-                       "d2h_bytes_per_step": d2h / gens,
-                       "generations": gens, "wall_s": dt,
-                       "api": "DiscreteSwarmSolver.fit(host numpy matrix)"}
-
+        s, ep = e2e_solver, e2e_params
         # time-to-reference-best tour length (BASELINE metric, second part):
         # with numpy-exact streams this run IS the reference's run for this
         # seed (bit for bit), so the reference's best over the schedule is
@@ -503,6 +596,25 @@ def run_ours(args, cfg_name, cfg):
                         "reference's best tour length over the schedule for "
                         "this seed; numpy-exact streams make this the "
                         "reference's own trajectory"}
+            # the unmodified reference's own run of this instance and seed
+            # (tests/golden/make_golden_c2.py, one core of the build host)
+            gp = os.path.join(ROOT, "tests", "golden", "golden_c2_full.json")
+            if cfg_name == "c2" and os.path.exists(gp):
+                with open(gp) as fh:
+                    g = json.load(fh)
+                pr = g["params"]
+                if (pr["random_state"] == ep["random_state"]
+                        and pr["n_particles"] == P
+                        and pr["max_generations"] == Ge):
+                    line["time_to_reference_best"]["reference_run"] = {
+                        "reference_best": g["best_fitness"],
+                        "trajectory_identical": conv == g["convergence"],
+                        "reference_time_to_best_s":
+                            g["reference_time_to_best_s"],
+                        "reference_generation": g["best_generation"],
+                        "reference_wall_s": g["reference_wall_s"],
+                        "host": g["host"],
+                        "fixture": "tests/golden/golden_c2_full.json"}
 
     if not args.no_cpu_baseline and world == 1:
         rate, g, dt = cpu_sample(cost, cfg, seed_tour=seed_tour)
@@ -552,8 +664,36 @@ def main():
                                         "filter32": "2"}[args.scan_mode]
     if args.impl == "reference":
         run_reference(args, args.config, cfg)
-    else:
-        run_ours(args, args.config, cfg)
+        return
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if args.gpus > 1 and world == 0:
+        sys.exit(launch_ranks(args))
+    if world and world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: "
+                 f"one rank per GPU is required")
+    run_ours(args, args.config, cfg)
+
+
+def launch_ranks(args) -> int:
+    """`--gpus N` without a torchrun environment: start N ranks (one per
+    GPU) with torch.distributed.run on this node and wait for them; fail
+    loudly when the node has fewer than N GPUs."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} "
+                         f"GPUs, this node has {have}\n")
+        return 2
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

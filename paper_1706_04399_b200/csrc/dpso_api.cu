@@ -198,6 +198,7 @@ int check_params(const dpso_params* p, int n) {
 struct dpso_ctx {
   dpso_params prm;
   int n;
+  int dev = -1;  // the device of the workspace (every entry runs on it)
   Layout L;
   unsigned char* ws;
   cudaStream_t user;
@@ -211,6 +212,22 @@ struct dpso_ctx {
   SwarmView v;
   DevCtl* host_ctl;  // pinned
   int init_path = -1;
+};
+
+// Every entry that takes a context runs on the context's device (the device
+// of its workspace) whatever device is current in the calling thread, and
+// gives the caller its current device back on return.
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int dev) {
+    if (dev >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != dev)
+      cudaSetDevice(dev);
+    else
+      prev = -1;
+  }
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
 };
 
 static int sync_in(dpso_ctx* c) {
@@ -351,6 +368,15 @@ static void pinned_ctl_put(DevCtl* p) {
 
 int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
                 size_t workspace_bytes, void* cuda_stream, dpso_ctx** out) {
+  int wdev = -1;
+  if (dev_workspace) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, dev_workspace) == cudaSuccess &&
+        at.type == cudaMemoryTypeDevice)
+      wdev = at.device;
+    cudaGetLastError();
+  }
+  DevGuard g_(wdev);
   int rc = check_params(prm, n);
   if (rc) return rc;
   Layout L = make_layout(prm, n);
@@ -359,6 +385,7 @@ int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
   dpso_ctx* c = new dpso_ctx();
   c->prm = *prm;
   c->n = n;
+  c->dev = wdev;
   c->L = L;
   c->ws = (unsigned char*)dev_workspace;
   c->user = (cudaStream_t)cuda_stream;
@@ -452,6 +479,7 @@ int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
 }
 
 int dpso_set_cost(dpso_ctx* c, const double* dev_cost, int64_t ld) {
+  DevGuard g_(c ? c->dev : -1);
   if (!c || !dev_cost) return fail(DPSO_EINVAL, "null argument");
   if (ld < round_up(c->n, 2) || (ld & 1) || ((uintptr_t)dev_cost & 15))
     return fail(DPSO_EINVAL,
@@ -507,6 +535,7 @@ int dpso_scan_rows_bytes(dpso_ctx* c) {
 }
 
 int dpso_set_streams(dpso_ctx* c, const uint64_t* host_states) {
+  DevGuard g_(c ? c->dev : -1);
   if (!c || !host_states) return fail(DPSO_EINVAL, "null argument");
   const int64_t P = c->prm.n_particles;
   int rc = sync_in(c);
@@ -519,6 +548,7 @@ int dpso_set_streams(dpso_ctx* c, const uint64_t* host_states) {
 }
 
 int dpso_init(dpso_ctx* c, const int32_t* seed_body, int32_t n_seed) {
+  DevGuard g_(c ? c->dev : -1);
   if (!c) return fail(DPSO_EINVAL, "null context");
   if (!c->have_cost) return fail(DPSO_EINVAL, "cost matrix not set");
   if (!c->have_streams && c->prm.rng_mode == DPSO_RNG_NUMPY)
@@ -597,6 +627,7 @@ static cudaError_t launch_generation(dpso_ctx* c) {
 }
 
 int dpso_step(dpso_ctx* c, int32_t gens) {
+  DevGuard g_(c ? c->dev : -1);
   if (!c || !c->initialized) return fail(DPSO_EINVAL, "context not initialized");
   int rc = ensure_graph(c);
   if (rc) return rc;
@@ -607,6 +638,7 @@ int dpso_step(dpso_ctx* c, int32_t gens) {
 
 int dpso_step_timed(dpso_ctx* c, int32_t gens, double* phase_ms,
                     int32_t* two_opt_count) {
+  DevGuard g_(c ? c->dev : -1);
   // Same launches as one graph replay, issued directly with CUDA events
   // between phases: [0] begin+update [1] mutation [2] select
   // [3] 2-opt scan [4] 2-opt apply [5] finalize.
@@ -664,6 +696,7 @@ int dpso_step_timed(dpso_ctx* c, int32_t gens, double* phase_ms,
 int dpso_ctl(dpso_ctx* c, int32_t* out /* gen, stall, done, gens_run,
                                            two_opt_count, n_events */,
              double* gbest_fit) {
+  DevGuard g_(c ? c->dev : -1);
   if (!c) return fail(DPSO_EINVAL, "null context");
   int rc = sync_in(c);
   if (rc) return rc;
@@ -683,6 +716,7 @@ int dpso_ctl(dpso_ctx* c, int32_t* out /* gen, stall, done, gens_run,
 }
 
 int dpso_run(dpso_ctx* c, int32_t* gens_run) {
+  DevGuard g_(c ? c->dev : -1);
   if (!c || !c->initialized) return fail(DPSO_EINVAL, "context not initialized");
   int rc = ensure_graph(c);
   if (rc) return rc;
@@ -712,6 +746,7 @@ int dpso_run(dpso_ctx* c, int32_t* gens_run) {
 
 int dpso_result(dpso_ctx* c, int32_t* tour, double* fitness, double* conv,
                 int32_t* n_conv) {
+  DevGuard g_(c ? c->dev : -1);
   if (!c || !c->initialized) return fail(DPSO_EINVAL, "context not initialized");
   const int n = c->n;
   int rc = sync_in(c);
@@ -738,6 +773,7 @@ int dpso_result(dpso_ctx* c, int32_t* tour, double* fitness, double* conv,
 int dpso_get_state(dpso_ctx* c, int32_t* x, int32_t* pbest, double* fit,
                    double* pfit, int32_t* vmap, int32_t* gbest,
                    double* gbest_fit) {
+  DevGuard g_(c ? c->dev : -1);
   if (!c) return fail(DPSO_EINVAL, "null context");
   const int64_t P = c->prm.n_particles, n = c->n, np = c->v.np;
   int rc = sync_in(c);
@@ -777,6 +813,7 @@ int dpso_get_state(dpso_ctx* c, int32_t* x, int32_t* pbest, double* fit,
 int dpso_set_state(dpso_ctx* c, const int32_t* x, const int32_t* pbest,
                    const double* fit, const double* pfit, const int32_t* vmap,
                    const int32_t* gbest, double gbest_fit) {
+  DevGuard g_(c ? c->dev : -1);
   if (!c) return fail(DPSO_EINVAL, "null context");
   const int64_t P = c->prm.n_particles, n = c->n, np = c->v.np;
   int rc = sync_in(c);
@@ -824,6 +861,7 @@ int dpso_set_state(dpso_ctx* c, const int32_t* x, const int32_t* pbest,
 }
 
 int dpso_mutate_step(dpso_ctx* c) {
+  DevGuard g_(c ? c->dev : -1);
   if (!c || !c->initialized) return fail(DPSO_EINVAL, "context not initialized");
   if (!c->prm.use_mutation || c->prm.mutation_period != 1)
     return fail(DPSO_EINVAL,
@@ -844,6 +882,7 @@ int dpso_mutate_step(dpso_ctx* c) {
 }
 
 int dpso_offer_gbest(dpso_ctx* c, const int32_t* tour, double fitness) {
+  DevGuard g_(c ? c->dev : -1);
   if (!c || !tour) return fail(DPSO_EINVAL, "null argument");
   const int n = c->n;
   int rc = sync_in(c);
@@ -869,6 +908,7 @@ int64_t dpso_island_record_bytes(int32_t n) {
 }
 
 int dpso_island_pack(dpso_ctx* c, void* dev_record, int32_t rank) {
+  DevGuard g_(c ? c->dev : -1);
   if (!c || !dev_record) return fail(DPSO_EINVAL, "null argument");
   if (!c->initialized) return fail(DPSO_EINVAL, "context not initialized");
   int rc = sync_in(c);
@@ -879,6 +919,7 @@ int dpso_island_pack(dpso_ctx* c, void* dev_record, int32_t rank) {
 
 int dpso_island_adopt(dpso_ctx* c, const void* dev_records, int32_t world,
                       int32_t rank) {
+  DevGuard g_(c ? c->dev : -1);
   if (!c || !dev_records || world < 1 || rank < 0 || rank >= world)
     return fail(DPSO_EINVAL, "bad arguments");
   if (!c->initialized) return fail(DPSO_EINVAL, "context not initialized");
@@ -890,6 +931,7 @@ int dpso_island_adopt(dpso_ctx* c, const void* dev_records, int32_t world,
 
 void dpso_destroy(dpso_ctx* c) {
   if (!c) return;
+  DevGuard g_(c->dev);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->graph) cudaGraphExecDestroy(c->graph);
   if (c->graph_plain) cudaGraphExecDestroy(c->graph_plain);

@@ -111,43 +111,48 @@ __global__ void __launch_bounds__(256) k_smem_gather(int iters, float* sink) {
 __device__ __forceinline__ uint32_t s32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
-__global__ void __launch_bounds__(64) k_bulk_rows(const unsigned char* mat,
-                                                  int nrows, int row_bytes,
-                                                  int rps, int nst,
-                                                  int stages, float* sink) {
-  // ring of nst stages of rps rows; nst - 1 stages in flight while one is
-  // consumed (the band scan's pattern with nst = 2)
+__global__ void __launch_bounds__(256) k_bulk_rows(const unsigned char* mat,
+                                                   int nrows, int row_bytes,
+                                                   int rps, int nst,
+                                                   int stages, float* sink) {
+  // ring of nst stages of rps rows, issued by every warp of the CTA (warp w
+  // copies rows w, w + nwarps, ...; one expect-tx arrival per warp), the
+  // stage consumed at once: the band scan's producer pattern
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t bar[8];
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
   const uint32_t stride = (uint32_t)((row_bytes + 127) / 128 * 128);
   if (threadIdx.x == 0) {
     for (int b = 0; b < nst; ++b)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(&bar[b])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                       s32(&bar[b])),
+                   "r"(nw));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   auto issue = [&](int st) {
     const int b = st % nst;
-    if (threadIdx.x < 32) {
-      if (lane == 0)
-        asm volatile(
-            "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                s32(&bar[b])),
-            "r"((uint32_t)(rps * row_bytes))
-            : "memory");
-      __syncwarp();
-      if (lane < rps) {
-        const uint32_t r =
-            hash32(blockIdx.x * 100003u + st * 32 + lane) % nrows;
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
-            "[%0], [%1], %2, [%3];" ::"r"(s32(sm + (size_t)b * rps * stride +
-                                             (size_t)lane * stride)),
-            "l"(mat + (size_t)r * row_bytes), "r"((uint32_t)row_bytes),
-            "r"(s32(&bar[b]))
-            : "memory");
-      }
+    int mine = 0;
+    for (int r = warp; r < rps; r += nw) ++mine;
+    if (lane == 0)
+      asm volatile(
+          "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+              s32(&bar[b])),
+          "r"((uint32_t)(mine * row_bytes))
+          : "memory");
+    __syncwarp();
+    const int r = warp + nw * lane;
+    if (lane < mine) {
+      const uint32_t row =
+          hash32(blockIdx.x * 100003u + st * 32 + r) % nrows;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+          "[%0], [%1], %2, [%3];" ::"r"(s32(sm + (size_t)b * rps * stride +
+                                           (size_t)r * stride)),
+          "l"(mat + (size_t)row * row_bytes), "r"((uint32_t)row_bytes),
+          "r"(s32(&bar[b]))
+          : "memory");
     }
   };
   float acc = 0.f;
@@ -268,7 +273,7 @@ int main() {
     int4* buf;
     CK(cudaMalloc(&buf, bytes));
     CK(cudaMemset(buf, 0, bytes));
-    const int blocks = sms * 8, reps = 16;
+    const int blocks = sms * 8, reps = 64;
     const float ms = time_ms(
         [&] { k_l2_seq<<<blocks, 256>>>(buf, bytes / 16, reps, (int*)sink); },
         10);
@@ -278,16 +283,18 @@ int main() {
   }
 
   // bulk row stream L2 -> shared memory: 2 KB rows (n = 1000 int16), 1 KB
-  // (n = 500); stage of 32 rows; ring of nst stages (nst - 1 in flight)
-  for (int row_bytes : {2016, 1008, 4032}) {
+  // (n = 500); stages of 32 rows; ring of nst stages (nst - 1 in flight);
+  // 1 or 4 issuing warps
+  for (int row_bytes : {2016, 1008}) {
     const int nrows = (int)((8u << 20) / row_bytes);  // 8 MB of rows
     unsigned char* mat;
     CK(cudaMalloc(&mat, (size_t)nrows * row_bytes));
     CK(cudaMemset(mat, 0, (size_t)nrows * row_bytes));
     auto k = k_bulk_rows;
     const int stride = (row_bytes + 127) / 128 * 128;
-    for (int rps : {32, 16}) {
-      for (int nst = 2; nst <= 8; ++nst) {
+    for (int nw : {1, 4, 8}) {
+      for (int nst = 2; nst <= 4; ++nst) {
+        const int rps = 32;
         const int smem = nst * rps * stride;
         if (smem > 200 * 1024) break;
         CK(cudaFuncSetAttribute(
@@ -295,14 +302,14 @@ int main() {
         const int blocks = sms, stages = 512;
         const float ms = time_ms(
             [&] {
-              k<<<blocks, 64, smem>>>(mat, nrows, row_bytes, rps, nst, stages,
-                                      sink);
+              k<<<blocks, 32 * nw, smem>>>(mat, nrows, row_bytes, rps, nst,
+                                           stages, sink);
             },
             5);
         const double bytes = (double)blocks * stages * rps * row_bytes;
-        printf(", \"bulk_rows%d_x%d_stages%d\": {\"inflight_kb\": %.0f, "
-               "\"ms\": %.4f, \"gbs\": %.1f}",
-               row_bytes, rps, nst, (nst - 1) * rps * row_bytes / 1024.0, ms,
+        printf(", \"bulk_rows%d_x32_warps%d_stages%d\": {\"inflight_kb\": "
+               "%.0f, \"ms\": %.4f, \"gbs\": %.1f}",
+               row_bytes, nw, nst, (nst - 1) * rps * row_bytes / 1024.0, ms,
                bytes / ms / 1e6);
       }
     }

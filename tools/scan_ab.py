@@ -46,13 +46,17 @@ def time_scan(n, P, cost, gens, env):
     old = {k: os.environ.get(k) for k in env}
     os.environ.update({k: v for k, v in env.items() if v is not None})
     try:
-        s = DiscreteSwarmSolver(n_particles=P, max_generations=gens + 8,
-                                stall_generations=gens + 8, random_state=7,
+        G = gens + 8 + int(os.environ.get("AB_WARM", "0"))
+        s = DiscreteSwarmSolver(n_particles=P, max_generations=G,
+                                stall_generations=G, random_state=7,
                                 rng="philox" if n * P > 50_000_000 else "numpy")
         ctx = s._make_context(cost)
         band = int(ctx.lib.dpso_scan_band(ctx.h))
         ctx.set_streams(numpy_stream_states(7, P + 2))
         ctx.init(None, 0)
+        # AB_WARM: generations run first (a converged swarm has many more
+        # near-tied deltas than random tours)
+        ctx.step(int(os.environ.get("AB_WARM", "0")))
         ctx.step_timed(2)
         ms = []
         for _ in range(gens):
