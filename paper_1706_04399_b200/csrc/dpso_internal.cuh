@@ -247,7 +247,7 @@ cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
                                 const uint16_t* tours, const double* dcache,
                                 int32_t count, TwoOptRes* res, int32_t chunks,
                                 int32_t* ovf, const DevCtl* ctl,
-                                cudaStream_t s);
+                                cudaStream_t s, int reserve_sms = 0);
 int two_opt_pick_chunks(int32_t n, int32_t P);
 
 // Fitness in the reference's order (solver.py:48-54):

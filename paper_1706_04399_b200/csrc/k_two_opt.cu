@@ -1242,7 +1242,7 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
                                 const int32_t* chunk_tab, const DevCtl* ctl,
                                 double* fit, double* pfit, uint16_t* pbest,
                                 double* delta_out, double* dcache_rw,
-                                cudaStream_t s, int parts) {
+                                cudaStream_t s, int parts, int reserve_sms) {
   ScanArgs a;
   memset(&a, 0, sizeof a);
   a.cost = pl.cost;
@@ -1300,7 +1300,7 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
         e = cudaMemsetAsync(res, 0xFF, sizeof(TwoOptRes) * count * chunks, s);
       if (!e)
         e = launch_two_opt_band(pl, n, np, tours, dcache, count, res, chunks,
-                                a.ovf, ctl, s);
+                                a.ovf, ctl, s, reserve_sms);
       if (!e && pl.band_mode == 2) {
         k_two_opt_rescan64<<<2 * 148, 128, 0, s>>>(a);
         e = cudaGetLastError();
@@ -1384,9 +1384,14 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
 // update re-gathers only the edges it moved), so the apply refreshes the
 // edges i..j of a move.
 cudaError_t launch_two_opt(const SwarmView& v, cudaStream_t s, int parts) {
+  // the numpy mutation-stream walk (one CTA, launch_mutation_walk) runs on
+  // a forked stream concurrently with the scan: the band scan, one CTA per
+  // SM, leaves it an SM
+  const int reserve =
+      v.use_mutation && v.rng_mode == DPSO_RNG_NUMPY ? 1 : 0;
   return launch_two_opt_core(v.plan, v.n, v.np, v.x, v.dcache, v.P, v.tores,
                              v.chunks, v.chunk_tab, v.ctl, v.fit, v.pfit,
-                             v.pbest, nullptr, v.dcache, s, parts);
+                             v.pbest, nullptr, v.dcache, s, parts, reserve);
 }
 
 cudaError_t launch_two_opt_batch(const TwoOptPlan& pl, int32_t n, int32_t np,
@@ -1396,7 +1401,7 @@ cudaError_t launch_two_opt_batch(const TwoOptPlan& pl, int32_t n, int32_t np,
                                  cudaStream_t s) {
   return launch_two_opt_core(pl, n, np, tours, dcache, count, res, chunks,
                              chunk_tab, nullptr, nullptr, nullptr, nullptr,
-                             delta_out, const_cast<double*>(dcache), s, 3);
+                             delta_out, const_cast<double*>(dcache), s, 3, 0);
 }
 
 }  // namespace dpso

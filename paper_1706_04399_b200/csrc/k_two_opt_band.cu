@@ -684,7 +684,7 @@ cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
                                 const uint16_t* tours, const double* dcache,
                                 int32_t count, TwoOptRes* res, int32_t chunks,
                                 int32_t* ovf, const DevCtl* ctl,
-                                cudaStream_t s) {
+                                cudaStream_t s, int reserve_sms) {
   if (!pl.band_cols || count > pl.band_cols_cap) return cudaErrorInvalidValue;
   BandArgs a;
   memset(&a, 0, sizeof a);
@@ -720,7 +720,7 @@ cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int blocks = std::max(1, std::min(count, sms));
+  const int blocks = std::max(1, std::min(count, sms - reserve_sms));
   if (pl.band_mode == 1) {
     e = set_dyn_smem((const void*)k_two_opt_band<1>, smem);
     if (e) return e;
