@@ -23,6 +23,7 @@ SHAPES = {
     "c3": (500, 16384, "grid"),
     "c4": (2000, 65536, "euclid"),
     "c4s": (2000, 4096, "euclid"),
+    "n900": (900, 1024, "euclid"),
 }
 
 
@@ -85,6 +86,10 @@ def main():
         gens = int(os.environ.get("AB_GENS", "8"))
         rec = {"n": n, "P": P, "matrix": kind}
         variants = [("band", {}), ("column", {"DPSO_SCAN_BAND": "0"})]
+        for st in os.environ.get("AB_STAGES", "").split(","):
+            if st:
+                variants.append(("band_stages" + st,
+                                 {"DPSO_BAND_STAGES": st}))
         if os.environ.get("AB_PROBE"):
             variants.append(("band_stream_only", {"DPSO_BAND_PROBE": "1"}))
         for tag, env in variants:
