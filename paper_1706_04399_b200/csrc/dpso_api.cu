@@ -74,10 +74,16 @@ struct Layout {
   int chunks;
 };
 
+// Initial velocity-list capacity for w < 1 (entries per particle).  A list
+// grows by at most 2(n - 1) per generation (k1, k2 <= n - 1) and shrinks to
+// round(w len) first, so it stays below ~(2n)/(1 - w); the workspace holds
+// up to 64n + 64 and ensure_velocity() moves the lists to a larger owned
+// buffer before any batch of generations could outgrow it (solver.py:
+// 213-216 has no bound).
 int64_t vel_capacity(const dpso_params* p, int n) {
   if (p->inertia >= 1.0) return 0;
   double cap = (2.0 * n + 1.0) / (1.0 - p->inertia) + 8.0;
-  if (cap > 64.0 * n + 64) cap = 64.0 * n + 64;  // bound memory; overflow flagged
+  if (cap > 64.0 * n + 64) cap = 64.0 * n + 64;
   return (int64_t)cap;
 }
 
@@ -212,6 +218,7 @@ struct dpso_ctx {
   SwarmView v;
   DevCtl* host_ctl;  // pinned
   int init_path = -1;
+  uint32_t* vel_owned = nullptr;  // grown velocity lists (w < 1)
 };
 
 // Every entry that takes a context runs on the context's device (the device
@@ -620,6 +627,48 @@ static int ensure_graph(dpso_ctx* c) {
   return DPSO_OK;
 }
 
+// w < 1: make room for `gens` more generations of velocity growth (each
+// adds at most 2n - 2 entries to a list) before launching them: read the
+// longest list, and if it could outgrow the capacity, move every list to a
+// larger owned buffer (rows keep their entries; the graphs, which hold the
+// old pointer, are re-captured).
+static int ensure_velocity(dpso_ctx* c, int gens) {
+  if (!c->v.vel) return DPSO_OK;
+  CK(cudaMemcpyAsync(c->host_ctl, c->v.ctl, sizeof(DevCtl),
+                     cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->host_ctl->vel_overflow)
+    return fail(DPSO_ECUDA, "velocity list capacity exceeded");
+  const int64_t n = c->n, P = c->prm.n_particles;
+  // len' = round(w len) + k1 + k2 <= max(len, L*), L* = (2n - 1.5)/(1 - w):
+  // a capacity of max(len, L*) is never outgrown
+  const double lstar = (2.0 * n + 1.0) / (1.0 - c->prm.inertia) + 8.0;
+  const int64_t need = std::min<int64_t>(
+      (int64_t)c->host_ctl->vel_max + 2 * n * (int64_t)gens,
+      std::max<int64_t>(c->host_ctl->vel_max, (int64_t)lstar));
+  if (need <= c->v.vel_cap) return DPSO_OK;
+  const int64_t cap = std::max<int64_t>(2 * c->v.vel_cap, need);
+  const int64_t old_stride = c->v.vel_cap + 2 * n, stride = cap + 2 * n;
+  uint32_t* nb = nullptr;
+  CK(cudaMallocAsync(&nb, 4 * (size_t)P * stride, c->stream));
+  CK(cudaMemcpy2DAsync(nb, 4 * stride, c->v.vel, 4 * old_stride,
+                       4 * c->v.vel_cap, P, cudaMemcpyDeviceToDevice,
+                       c->stream));
+  if (c->vel_owned) CK(cudaFreeAsync(c->vel_owned, c->stream));
+  c->vel_owned = nb;
+  c->v.vel = nb;
+  c->v.vel_cap = cap;
+  if (c->graph) {
+    cudaGraphExecDestroy(c->graph);
+    c->graph = nullptr;
+  }
+  if (c->graph_plain) {
+    cudaGraphExecDestroy(c->graph_plain);
+    c->graph_plain = nullptr;
+  }
+  return DPSO_OK;
+}
+
 static cudaError_t launch_generation(dpso_ctx* c) {
   const int64_t g = c->gen_next++;
   const bool mut = !c->graph_plain || (g % c->v.mutation_period == 0);
@@ -629,10 +678,24 @@ static cudaError_t launch_generation(dpso_ctx* c) {
 int dpso_step(dpso_ctx* c, int32_t gens) {
   DevGuard g_(c ? c->dev : -1);
   if (!c || !c->initialized) return fail(DPSO_EINVAL, "context not initialized");
-  int rc = ensure_graph(c);
+  int rc = sync_in(c);
   if (rc) return rc;
-  if ((rc = sync_in(c))) return rc;
-  for (int g = 0; g < gens; ++g) CK(launch_generation(c));
+  for (int done = 0; done < gens;) {
+    // w < 1: batches of at most 64 generations, each with room for its
+    // velocity growth
+    const int b = c->v.vel ? std::min(64, gens - done) : gens - done;
+    if ((rc = ensure_velocity(c, b))) return rc;
+    if ((rc = ensure_graph(c))) return rc;
+    for (int g = 0; g < b; ++g) CK(launch_generation(c));
+    done += b;
+  }
+  if (c->v.vel) {
+    CK(cudaMemcpyAsync(c->host_ctl, c->v.ctl, sizeof(DevCtl),
+                       cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->host_ctl->vel_overflow)
+      return fail(DPSO_ECUDA, "velocity list capacity exceeded");
+  }
   return sync_out(c);
 }
 
@@ -645,6 +708,7 @@ int dpso_step_timed(dpso_ctx* c, int32_t gens, double* phase_ms,
   if (!c || !c->initialized) return fail(DPSO_EINVAL, "context not initialized");
   int rc = sync_in(c);
   if (rc) return rc;
+  if ((rc = ensure_velocity(c, gens))) return rc;
   const SwarmView& v = c->v;
   cudaEvent_t ev[7];
   for (int i = 0; i < 7; ++i) CK(cudaEventCreate(&ev[i]));
@@ -718,14 +782,15 @@ int dpso_ctl(dpso_ctx* c, int32_t* out /* gen, stall, done, gens_run,
 int dpso_run(dpso_ctx* c, int32_t* gens_run) {
   DevGuard g_(c ? c->dev : -1);
   if (!c || !c->initialized) return fail(DPSO_EINVAL, "context not initialized");
-  int rc = ensure_graph(c);
+  int rc = sync_in(c);
   if (rc) return rc;
-  if ((rc = sync_in(c))) return rc;
   int launched = 0;
   const int G = c->prm.max_generations;
   int batch = 4;
   while (launched < G) {
     const int b = std::min(batch, G - launched);
+    if ((rc = ensure_velocity(c, b))) return rc;
+    if ((rc = ensure_graph(c))) return rc;
     for (int g = 0; g < b; ++g) CK(launch_generation(c));
     launched += b;
     CK(cudaMemcpyAsync(c->host_ctl, c->v.ctl, sizeof(DevCtl),
@@ -940,6 +1005,7 @@ void dpso_destroy(dpso_ctx* c) {
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->stream2) cudaStreamDestroy(c->stream2);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->vel_owned) cudaFree(c->vel_owned);
   pinned_ctl_put(c->host_ctl);
   delete c;
 }

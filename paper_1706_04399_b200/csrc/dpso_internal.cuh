@@ -43,6 +43,7 @@ struct DevCtl {
   int32_t n_events;
   int32_t collision;  // canonical-hash collision seen (diagnostic)
   int32_t vel_overflow;
+  int32_t vel_max;        // longest velocity list after the last update
   int32_t two_opt_count;  // generations in which the 2-opt pass ran
   int32_t mut_bad;        // first event whose sample needed a redraw
   int32_t mut_round;      // last stream-walk round run this call

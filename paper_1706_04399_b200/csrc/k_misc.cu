@@ -95,6 +95,7 @@ __global__ void k_gen_begin(SwarmView v) {
   }
   c->two_opt_ran = 0;
   c->improved = 0;
+  c->vel_max = 0;
 }
 
 __global__ void __launch_bounds__(kRed) k_select(SwarmView v, int finalize) {

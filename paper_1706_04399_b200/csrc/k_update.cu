@@ -403,14 +403,18 @@ __global__ void __launch_bounds__(32) k_update_seq(SwarmView v) {
       int k2 = prefix_len(c2, L2);
       int len = v.vel_len[p];
       int k0 = prefix_len(v.inertia, len);
+      // the host grows the lists before every batch of generations
+      // (dpso_api.cu ensure_velocity) so this cannot trigger; if it ever
+      // does, the run fails loudly instead of diverging from the reference
       if ((int64_t)k0 + k1 + k2 > v.vel_cap) {
         v.ctl->vel_overflow = 1;
-        k0 = 0;
+        k0 = k1 = k2 = 0;
       }
       for (int e = 0; e < k1; ++e) lst[k0 + e] = t1[e];
       for (int e = 0; e < k2; ++e) lst[k0 + k1 + e] = t2[e];
       len = k0 + k1 + k2;
       v.vel_len[p] = len;
+      atomicMax(&v.ctl->vel_max, len);
       // _apply_open (solver.py:72-79) on the whole new velocity
       for (int i = 0; i < n; ++i) {
         scur[i] = sx[i];

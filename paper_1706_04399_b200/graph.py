@@ -5,12 +5,17 @@
 cost[i][j] = cost[j][i] = admissible-A* (= Dijkstra) motion cost on the
 26-connected free-voxel graph (voxel.py:112-172), zero diagonal, blocked
 pairs at ``1e3 * n * max_finite`` (1e6 when no finite edge) and flagged in
-``virtual``.  ``build_graph(plan, grid, weights)`` mirrors the reference
-signature for callers holding the reference's CoveragePlan/VoxelGrid.
-Per-pair waypoint legs for all N(N-1)/2 pairs are not produced: the
-reference's CLI needs them only for the final tour's N edges, which
-``tour_legs`` computes with a native restatement of the reference's A*
-(same paths, byte for byte; ``shortest_path`` for single pairs).
+``virtual``.  ``build_graph(plan, grid, weights, heuristic_mode)`` is graph.py:41-78 for
+callers holding the reference's CoveragePlan/VoxelGrid: the same
+``TourGraph`` fields and ``leg(i, j)``, the same error for a viewpoint in
+occupied space.  The waypoint legs are produced lazily: the reference's CLI
+reads only the final tour's N legs (cli.py:122-133), so ``TourGraph.legs``
+computes a pair's path on first access with a native restatement of the
+reference's A* (same paths, byte for byte; ``tour_legs`` batches a tour's
+legs over all host cores).  ``heuristic_mode="paper"`` (voxel.py:107-109:
+the squared-distance priority, possibly suboptimal paths) takes every
+pair's cost from that A* as the reference does; "admissible" costs come
+from the device SSSP (equal to A*'s for a consistent heuristic).
 
 ``save_cost_matrix`` / ``load_cost_matrix`` are graph.py:123-143 (the
 plain-text ``--matrix`` format) in native host code: the file bytes are the
@@ -20,22 +25,94 @@ reference's, and the reader parses straight into a pinned buffer that
 from __future__ import annotations
 
 import ctypes
+from collections.abc import Mapping
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _lib
+from .errors import InfeasibleViewpointError, OccupiedEndpointError
 from .solver import _torch
+
+VIRTUAL_SCALE = 1e3        # graph.py:17
+_FALLBACK_VIRTUAL = 1e6    # graph.py:18
+
+
+@dataclass(frozen=True)
+class VoxelPath:
+    """voxel.py:101-104."""
+    waypoints: tuple
+    motion_cost: float
+
+
+class LazyLegs(Mapping):
+    """graph.py's ``legs`` dict ((i, j), i < j -> VoxelPath; virtual pairs
+    absent), with each path computed by the native A* on first access."""
+
+    def __init__(self, occupancy, voxels, weights, mode, virtual):
+        self._occ = occupancy
+        self._vox = [tuple(int(c) for c in v) for v in voxels]
+        self._w = tuple(float(x) for x in weights)
+        self._mode = mode
+        self._virtual = np.asarray(virtual, dtype=bool)
+        self._cache = {}
+
+    def _valid(self, key):
+        i, j = key
+        n = len(self._vox)
+        return 0 <= i < j < n and not self._virtual[i, j]
+
+    def prefetch(self, keys) -> None:
+        """Compute the listed pairs in one native batch (all host cores)."""
+        todo = [k for k in keys if self._valid(k) and k not in self._cache]
+        if not todo:
+            return
+        pairs = [list(self._vox[i]) + list(self._vox[j]) for i, j in todo]
+        for k, p in zip(todo, _voxel_paths(self._occ, pairs, self._w,
+                                           self._mode)):
+            self._cache[k] = None if p is None else VoxelPath(p[0], p[1])
+
+    def __getitem__(self, key):
+        key = (int(key[0]), int(key[1]))
+        if not self._valid(key):
+            raise KeyError(key)
+        if key not in self._cache:
+            self.prefetch([key])
+        path = self._cache[key]
+        if path is None:
+            raise KeyError(key)
+        return path
+
+    def __iter__(self):
+        n = len(self._vox)
+        return ((i, j) for i in range(n) for j in range(i + 1, n)
+                if not self._virtual[i, j])
+
+    def __len__(self):
+        n = len(self._vox)
+        return int(np.triu(~self._virtual, 1).sum()) if n > 1 else 0
 
 
 @dataclass(frozen=True)
 class TourGraph:
-    """graph.py:22-38 (without legs)."""
+    """graph.py:22-38."""
     n_nodes: int
     cost: np.ndarray
     virtual: np.ndarray
     virtual_cost: float
-    legs: dict = field(default_factory=dict)
+    legs: Mapping = field(default_factory=dict)
+
+    def leg(self, i: int, j: int):
+        """graph.py:30-38: the path from viewpoint i to j (reversed waypoints
+        for i > j), None for i == j or a virtual edge."""
+        if i == j:
+            return None
+        key = (i, j) if i < j else (j, i)
+        path = self.legs.get(key)
+        if path is not None and i > j:
+            return VoxelPath(waypoints=tuple(reversed(path.waypoints)),
+                             motion_cost=path.motion_cost)
+        return path
 
 
 def build_cost_matrix(occupancy: np.ndarray, viewpoint_voxels, weights,
@@ -66,18 +143,56 @@ def build_cost_matrix(occupancy: np.ndarray, viewpoint_voxels, weights,
             float(vcost.value))
 
 
+def _paper_costs(occupancy, vox, weights):
+    """Every pair's cost from the reference's A* with the paper heuristic
+    (graph.py:58-66 with heuristic_mode="paper"), native, all host cores;
+    blocked pairs virtual (graph.py:68-74).  Returns the paths too."""
+    n = len(vox)
+    keys = [(i, j) for i in range(n) for j in range(i + 1, n)]
+    pairs = [list(vox[i]) + list(vox[j]) for i, j in keys]
+    paths = _voxel_paths(occupancy, pairs, weights, "paper") if keys else []
+    cost = np.zeros((n, n), dtype=float)
+    virtual = np.zeros((n, n), dtype=bool)
+    blocked = []
+    for (i, j), p in zip(keys, paths):
+        if p is None:
+            blocked.append((i, j))
+        else:
+            cost[i, j] = cost[j, i] = p[1]
+    max_finite = float(cost.max()) if n > 1 else 0.0
+    vcost = (VIRTUAL_SCALE * n * max_finite if max_finite > 0
+             else _FALLBACK_VIRTUAL)
+    for i, j in blocked:
+        cost[i, j] = cost[j, i] = vcost
+        virtual[i, j] = virtual[j, i] = True
+    return cost, virtual, vcost, dict(zip(keys, paths))
+
+
 def build_graph(plan, grid, weights, heuristic_mode: str = "admissible"):
-    """graph.py:41-78 signature; duck-typed plan.viewpoints / grid."""
-    if heuristic_mode != "admissible":
-        raise ValueError("the device build computes exact (admissible) "
-                         "costs; the order-dependent 'paper' heuristic is "
-                         "not reproduced")
-    vox = [grid.point_to_voxel(vp.position) for vp in plan.viewpoints]
-    cost, virtual, vcost = build_cost_matrix(grid.occupancy, vox, weights)
+    """graph.py:41-78 (duck-typed plan.viewpoints / grid): the all-pairs
+    obstacle-aware cost graph over the plan's viewpoints."""
+    if heuristic_mode not in ("admissible", "paper"):
+        raise ValueError(f"unknown heuristic_mode {heuristic_mode!r}")
+    vox = []
+    for vp in plan.viewpoints:
+        idx = grid.point_to_voxel(vp.position)
+        if not grid.is_free(idx):
+            raise InfeasibleViewpointError(
+                f"viewpoint {vp.id} maps to occupied voxel {idx}")
+        vox.append(idx)
+    occ = grid.occupancy
+    if heuristic_mode == "paper":
+        cost, virtual, vcost, paths = _paper_costs(occ, vox, weights)
+    else:
+        cost, virtual, vcost = build_cost_matrix(occ, vox, weights)
+        paths = {}
+    legs = LazyLegs(occ, vox, weights, heuristic_mode, virtual)
+    for k, p in paths.items():
+        legs._cache[k] = None if p is None else VoxelPath(p[0], p[1])
     cost.setflags(write=False)
     virtual.setflags(write=False)
     return TourGraph(n_nodes=len(vox), cost=cost, virtual=virtual,
-                     virtual_cost=vcost)
+                     virtual_cost=vcost, legs=legs)
 
 
 def _path_bytes(path) -> bytes:
@@ -133,10 +248,6 @@ def load_cost_matrix_device(path, device=None):
     dev = torch.device(device) if device is not None else torch.device(
         "cuda", torch.cuda.current_device())
     return host[:n].to(dev, non_blocking=False), ld
-
-
-class OccupiedEndpointError(ValueError):
-    """voxel.py's error for an occupied start or goal voxel."""
 
 
 def _voxel_paths(occupancy, pairs, weights, heuristic_mode="admissible"):

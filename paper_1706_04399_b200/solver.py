@@ -399,9 +399,14 @@ class DiscreteSwarmSolver(BaseEstimator):
 
     # -- main entry (solver.py:262-335) -------------------------------------
     def fit(self, X, y=None):
+        """X: a square host cost matrix (the reference's input), or a CUDA
+        tensor holding one - (n, n), or (n, ld) rows padded to ld >= n as
+        ``load_cost_matrix_device`` returns them - which is used in place
+        (no host round trip)."""
         self._check_params()
-        cost = self._check_cost(X)
-        n = cost.shape[0]
+        dev_cost = self._device_cost(X)
+        cost = None if dev_cost is not None else self._check_cost(X)
+        n = dev_cost[0].shape[0] if dev_cost is not None else cost.shape[0]
         t0 = time.perf_counter()
         flags = {
             "init": self.seed_tour is not None and self.seed_fraction > 0,
@@ -413,7 +418,8 @@ class DiscreteSwarmSolver(BaseEstimator):
             self._finish((0, 0), 0.0, [0.0], 1, t0, flags)
             return self
         seed_body, n_seed = self._seed(n)
-        ctx = self._make_context(cost)
+        ctx = (SwarmContext(self._params(), n, *dev_cost)
+               if dev_cost is not None else self._make_context(cost))
         try:
             if self.rng == "numpy":
                 ctx.set_streams(numpy_stream_states(self.random_state,
@@ -427,9 +433,26 @@ class DiscreteSwarmSolver(BaseEstimator):
                      [float(c) for c in conv], gens, t0, flags)
         return self
 
-    def _make_context(self, cost: np.ndarray) -> SwarmContext:
-        cost_t, ld = device_cost(cost, self.device)
-        return SwarmContext(self._params(), cost.shape[0], cost_t, ld)
+    @staticmethod
+    def _device_cost(X):
+        """(tensor (n, ld) float64 contiguous on a CUDA device, ld) for a
+        device matrix, None for anything else."""
+        torch = _torch()
+        if not (isinstance(X, torch.Tensor) and X.is_cuda):
+            return None
+        if X.ndim != 2 or X.shape[0] > X.shape[1]:
+            raise ValueError(f"cost matrix must be square, got "
+                             f"{tuple(X.shape)}")
+        n, ld = X.shape
+        if X.dtype != torch.float64 or not X.is_contiguous() or \
+                (ld & 1) or X.data_ptr() % 16:
+            ld = (n + 7) // 8 * 8
+            buf = torch.zeros((n, ld), dtype=torch.float64, device=X.device)
+            buf[:, :n].copy_(X[:, :n])
+            X = buf
+        if not bool(torch.isfinite(X[:, :n]).all()):
+            raise ValueError("cost matrix must be finite")
+        return X, ld
 
     def _finish(self, tour, fitness, convergence, generations, t0, flags):
         self.best_tour_ = tuple(int(x) for x in tour)

@@ -77,3 +77,50 @@ def test_occupied_viewpoint_rejected(pkg):
     occ[2, 2, 2] = True
     with pytest.raises(ValueError, match="occupied"):
         pkg.build_cost_matrix(occ, [[0, 0, 0], [2, 2, 2]], (1, 1, 1))
+
+
+def test_load_cost_matrix_device_and_fit(pkg, tmp_path):
+    # graph.py:123-143 text format -> pinned host buffer -> device tensor
+    # (the --matrix path, cli.py:219-220) -> fit on the device matrix
+    from conftest import random_euclidean_matrix
+    import torch
+    rng = np.random.default_rng(9)
+    for n in (1, 7, 60):
+        c = random_euclidean_matrix(n, rng)
+        path = tmp_path / f"m{n}.txt"
+        pkg.save_cost_matrix(path, c)
+        host = pkg.load_cost_matrix(path)
+        dev, ld = pkg.load_cost_matrix_device(path)
+        assert dev.is_cuda and ld >= n and ld % 8 == 0
+        assert dev.shape == (n, ld)
+        got = dev.cpu().numpy()
+        assert np.array_equal(got[:, :n], host)
+        assert not got[:, n:].any()
+        if n > 3:
+            params = dict(n_particles=16, max_generations=30,
+                          stall_generations=30, random_state=4)
+            a = pkg.DiscreteSwarmSolver(**params).fit(host)
+            b = pkg.DiscreteSwarmSolver(**params).fit(dev)
+            assert a.best_tour_ == b.best_tour_
+            assert a.convergence_ == b.convergence_
+            # an unpadded (n, n) device tensor is padded on the way in
+            e = pkg.DiscreteSwarmSolver(**params).fit(
+                torch.as_tensor(host, device="cuda"))
+            assert e.best_tour_ == a.best_tour_
+    with pytest.raises(ValueError, match="finite"):
+        bad = torch.full((5, 8), float("inf"), dtype=torch.float64,
+                         device="cuda")
+        pkg.DiscreteSwarmSolver(n_particles=4).fit(bad)
+
+
+def test_fit_on_explicit_device_keeps_current_device(pkg):
+    # ADVICE: contexts run on their workspace's device; the caller's
+    # current device is handed back (one-GPU box: cuda:0 both ways)
+    import torch
+    from conftest import random_euclidean_matrix
+    c = random_euclidean_matrix(40, np.random.default_rng(3))
+    before = torch.cuda.current_device()
+    s = pkg.DiscreteSwarmSolver(n_particles=12, max_generations=10,
+                                device="cuda:0", random_state=1).fit(c)
+    assert torch.cuda.current_device() == before
+    assert sorted(s.best_tour_[:-1]) == list(range(40))
