@@ -437,6 +437,8 @@ class DiscreteSwarmSolver(BaseEstimator):
     def _device_cost(X):
         """(tensor (n, ld) float64 contiguous on a CUDA device, ld) for a
         device matrix, None for anything else."""
+        if type(X).__module__.split(".")[0] != "torch":
+            return None
         torch = _torch()
         if not (isinstance(X, torch.Tensor) and X.is_cuda):
             return None
@@ -453,6 +455,10 @@ class DiscreteSwarmSolver(BaseEstimator):
         if not bool(torch.isfinite(X[:, :n]).all()):
             raise ValueError("cost matrix must be finite")
         return X, ld
+
+    def _make_context(self, cost: np.ndarray) -> SwarmContext:
+        cost_t, ld = device_cost(cost, self.device)
+        return SwarmContext(self._params(), cost.shape[0], cost_t, ld)
 
     def _finish(self, tour, fitness, convergence, generations, t0, flags):
         self.best_tour_ = tuple(int(x) for x in tour)
