@@ -52,6 +52,18 @@ CONFIGS = {
     "c3": dict(n=500, P=16384, G=100, matrix="grid",
                workload="C3: bridge-sized synthetic instance N=500 (integer "
                         "grid costs, many ties), swarm P=16384"),
+    "c2s": dict(n=816, P=1024, G=500, matrix="scene:office",
+                workload="C2 scene-shaped: synthetic office floor (100x48x32"
+                         " voxels, walls, pillars, partition, desks), 816 "
+                         "viewpoints, obstacle-aware costs from the device "
+                         "cost build (graph.py:41-78 semantics), swarm "
+                         "P=1024"),
+    "c3s": dict(n=500, P=16384, G=100, matrix="scene:bridge",
+                workload="C3 scene-shaped: synthetic girder bridge with "
+                         "dense clutter (120x40x30 voxels), 500 viewpoints "
+                         "at 1-3 voxels standoff, axis weights (1,1,2), "
+                         "device cost build, swarm P=16384, 2-opt every "
+                         "stalled generation"),
     "c4": dict(n=2000, P=65536, G=50, matrix="euclid",
                workload="C4: synthetic N=2000 extended TSP, P=65536"),
     "c5": dict(n=10000, P=65536, G=20, matrix="euclid", ee=False,
@@ -61,9 +73,21 @@ CONFIGS = {
 }
 
 
+SCENE_META = {}
+
+
 def make_matrix(cfg):
     import numpy as np
     n = cfg["n"]
+    if cfg["matrix"].startswith("scene:"):
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import scenes
+        t0 = time.perf_counter()
+        cost, virt, vcost, meta = scenes.scene_matrix(cfg["matrix"][6:])
+        meta["cost_build_wall_s"] = time.perf_counter() - t0
+        meta["virtual_pairs"] = int(virt.sum() // 2)
+        SCENE_META.update(meta)
+        return cost, None
     if cfg["matrix"] == "wall":
         with open(os.path.join(ROOT, "tests", "golden",
                                "golden_e2e.json")) as fh:
@@ -254,7 +278,8 @@ def config_dict(cfg_name, cfg, args, world=1):
             "exchange_every": args.exchange_every if world > 1 else None,
             "rng": {"numpy": "numpy-pcg64-exact",
                     "philox": "philox4x32-10"}[RNG],
-            "l2": "flushed between timed steps (256 MiB write)"}
+            "l2": "flushed between timed steps (256 MiB write)",
+            **({"scene": dict(SCENE_META)} if SCENE_META else {})}
 
 
 # --------------------------------------------------------------- our arm
