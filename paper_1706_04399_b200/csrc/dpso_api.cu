@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "dpso_internal.cuh"
+#include <nvtx3/nvToolsExt.h>
 #include "philox.cuh"
 
 using namespace dpso;
@@ -219,6 +220,13 @@ struct dpso_ctx {
   DevCtl* host_ctl;  // pinned
   int init_path = -1;
   uint32_t* vel_owned = nullptr;  // grown velocity lists (w < 1)
+};
+
+// NVTX ranges around the host entry points (nsys / ncu --nvtx show the
+// solve's phases: cost preparation, init, generation batches, exchanges)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
 };
 
 // Every entry that takes a context runs on the context's device (the device
@@ -487,6 +495,7 @@ int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
 
 int dpso_set_cost(dpso_ctx* c, const double* dev_cost, int64_t ld) {
   DevGuard g_(c ? c->dev : -1);
+  NvtxRange nv_("dpso_set_cost (2-opt plan: cost prep, row versions)");
   if (!c || !dev_cost) return fail(DPSO_EINVAL, "null argument");
   if (ld < round_up(c->n, 2) || (ld & 1) || ((uintptr_t)dev_cost & 15))
     return fail(DPSO_EINVAL,
@@ -556,6 +565,7 @@ int dpso_set_streams(dpso_ctx* c, const uint64_t* host_states) {
 
 int dpso_init(dpso_ctx* c, const int32_t* seed_body, int32_t n_seed) {
   DevGuard g_(c ? c->dev : -1);
+  NvtxRange nv_("dpso_init (swarm init)");
   if (!c) return fail(DPSO_EINVAL, "null context");
   if (!c->have_cost) return fail(DPSO_EINVAL, "cost matrix not set");
   if (!c->have_streams && c->prm.rng_mode == DPSO_RNG_NUMPY)
@@ -677,6 +687,7 @@ static cudaError_t launch_generation(dpso_ctx* c) {
 
 int dpso_step(dpso_ctx* c, int32_t gens) {
   DevGuard g_(c ? c->dev : -1);
+  NvtxRange nv_("dpso_step");
   if (!c || !c->initialized) return fail(DPSO_EINVAL, "context not initialized");
   int rc = sync_in(c);
   if (rc) return rc;
@@ -702,6 +713,7 @@ int dpso_step(dpso_ctx* c, int32_t gens) {
 int dpso_step_timed(dpso_ctx* c, int32_t gens, double* phase_ms,
                     int32_t* two_opt_count) {
   DevGuard g_(c ? c->dev : -1);
+  NvtxRange nv_("dpso_step_timed");
   // Same launches as one graph replay, issued directly with CUDA events
   // between phases: [0] begin+update [1] mutation [2] select
   // [3] 2-opt scan [4] 2-opt apply [5] finalize.
@@ -781,6 +793,7 @@ int dpso_ctl(dpso_ctx* c, int32_t* out /* gen, stall, done, gens_run,
 
 int dpso_run(dpso_ctx* c, int32_t* gens_run) {
   DevGuard g_(c ? c->dev : -1);
+  NvtxRange nv_("dpso_run");
   if (!c || !c->initialized) return fail(DPSO_EINVAL, "context not initialized");
   int rc = sync_in(c);
   if (rc) return rc;
@@ -791,7 +804,10 @@ int dpso_run(dpso_ctx* c, int32_t* gens_run) {
     const int b = std::min(batch, G - launched);
     if ((rc = ensure_velocity(c, b))) return rc;
     if ((rc = ensure_graph(c))) return rc;
-    for (int g = 0; g < b; ++g) CK(launch_generation(c));
+    {
+      NvtxRange nv_b("generation batch");
+      for (int g = 0; g < b; ++g) CK(launch_generation(c));
+    }
     launched += b;
     CK(cudaMemcpyAsync(c->host_ctl, c->v.ctl, sizeof(DevCtl),
                        cudaMemcpyDeviceToHost, c->stream));
@@ -948,6 +964,7 @@ int dpso_mutate_step(dpso_ctx* c) {
 
 int dpso_offer_gbest(dpso_ctx* c, const int32_t* tour, double fitness) {
   DevGuard g_(c ? c->dev : -1);
+  NvtxRange nv_("dpso_offer_gbest");
   if (!c || !tour) return fail(DPSO_EINVAL, "null argument");
   const int n = c->n;
   int rc = sync_in(c);
@@ -974,6 +991,7 @@ int64_t dpso_island_record_bytes(int32_t n) {
 
 int dpso_island_pack(dpso_ctx* c, void* dev_record, int32_t rank) {
   DevGuard g_(c ? c->dev : -1);
+  NvtxRange nv_("dpso_island_pack");
   if (!c || !dev_record) return fail(DPSO_EINVAL, "null argument");
   if (!c->initialized) return fail(DPSO_EINVAL, "context not initialized");
   int rc = sync_in(c);
@@ -985,6 +1003,7 @@ int dpso_island_pack(dpso_ctx* c, void* dev_record, int32_t rank) {
 int dpso_island_adopt(dpso_ctx* c, const void* dev_records, int32_t world,
                       int32_t rank) {
   DevGuard g_(c ? c->dev : -1);
+  NvtxRange nv_("dpso_island_adopt");
   if (!c || !dev_records || world < 1 || rank < 0 || rank >= world)
     return fail(DPSO_EINVAL, "bad arguments");
   if (!c->initialized) return fail(DPSO_EINVAL, "context not initialized");
