@@ -250,6 +250,12 @@ static int sync_in(dpso_ctx* c) {
   CK(cudaStreamWaitEvent(c->stream, c->ev, 0));
   return DPSO_OK;
 }
+// entries that rewrite what the mutation-stream walk reads (the streams,
+// the swarm state) first wait for a walk still running on stream2
+static int join_walk(dpso_ctx* c) {
+  CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  return DPSO_OK;
+}
 static int sync_out(dpso_ctx* c) {
   CK(cudaEventRecord(c->ev, c->stream));
   CK(cudaStreamWaitEvent(c->user, c->ev, 0));
@@ -260,27 +266,39 @@ static const char* g_stage = "";
 
 // One generation.  With mutation on, the mutation-stream walk runs on a
 // forked stream (s2) concurrently with the update and the dedupe pipeline.
+// walk: whether the graph runs the next mutation call's stream walk
+// (launch_mutation_walk) on the forked stream s2 after this generation's
+// mutation call, overlapping its swap, select and 2-opt (mutation every
+// generation, or one graph for all generations: kWalkAfterMutation), or
+// leaves it to launch_generation (kWalkNone)
+enum { kWalkAfterMutation, kWalkNone };
+
 static cudaError_t enqueue_generation(const SwarmView& v, cudaStream_t s,
                                       cudaStream_t s2, cudaEvent_t fork,
                                       cudaEvent_t join,
-                                      bool with_mutation = true) {
+                                      bool with_mutation = true,
+                                      int walk = kWalkAfterMutation) {
   cudaError_t e;
 #define STAGE(name, call)      \
   do {                         \
     g_stage = name;            \
     if ((e = (call))) return e; \
   } while (0)
+  const bool mut = v.use_mutation && with_mutation;
+  bool forked = false;
   STAGE("gen_begin", launch_gen_begin(v, s));
   STAGE("update", launch_update(v, s));
-  const bool mut = v.use_mutation && with_mutation;
   if (mut) {
     STAGE("mutation_pre", launch_mutation_pre(v, s));
     STAGE("mutation_post", launch_mutation_post(v, s));
-    // the next call's stream walk overlaps the rest of this generation
-    STAGE("fork", cudaEventRecord(fork, s));
-    STAGE("fork", cudaStreamWaitEvent(s2, fork, 0));
-    STAGE("mutation_walk", launch_mutation_walk(v, s2));
-    STAGE("join", cudaEventRecord(join, s2));
+    if (walk == kWalkAfterMutation) {
+      // the next call's stream walk overlaps the rest of this generation
+      STAGE("fork", cudaEventRecord(fork, s));
+      STAGE("fork", cudaStreamWaitEvent(s2, fork, 0));
+      STAGE("mutation_walk", launch_mutation_walk(v, s2));
+      STAGE("join", cudaEventRecord(join, s2));
+      forked = true;
+    }
     STAGE("mutation_swap", launch_mutation_swap(v, s));
   }
   if (v.use_edge_exchange) {
@@ -290,7 +308,7 @@ static cudaError_t enqueue_generation(const SwarmView& v, cudaStream_t s,
   } else {
     STAGE("select+finalize", launch_select(v, true, s));
   }
-  if (mut) STAGE("join", cudaStreamWaitEvent(s, join, 0));
+  if (forked) STAGE("join", cudaStreamWaitEvent(s, join, 0));
 #undef STAGE
   g_stage = "";
   return cudaSuccess;
@@ -556,6 +574,7 @@ int dpso_set_streams(dpso_ctx* c, const uint64_t* host_states) {
   const int64_t P = c->prm.n_particles;
   int rc = sync_in(c);
   if (rc) return rc;
+  if ((rc = join_walk(c))) return rc;
   CK(cudaMemcpyAsync(c->v.streams, host_states, sizeof(PcgState) * (P + 2),
                      cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -594,6 +613,7 @@ int dpso_init(dpso_ctx* c, const int32_t* seed_body, int32_t n_seed) {
   }
   int rc = sync_in(c);
   if (rc) return rc;
+  if ((rc = join_walk(c))) return rc;
   CK(launch_init(c->v, dseed, n_seed, c->stream, &c->init_path));
   CK(launch_init_best(c->v, c->stream));
   // stream walk of the first mutation call
@@ -607,12 +627,12 @@ int dpso_init(dpso_ctx* c, const int32_t* seed_body, int32_t n_seed) {
 // not (gen % mutation_period != 0: the mutation kernels would only exit at
 // entry).  The host knows which generation each launch runs (gen_next; a
 // generation after the stall break is a no-op either way).
-static int capture_generation(dpso_ctx* c, bool with_mutation,
+static int capture_generation(dpso_ctx* c, bool with_mutation, int walk,
                               cudaGraphExec_t* out) {
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   cudaError_t e = enqueue_generation(c->v, c->stream, c->stream2, c->ev_fork,
-                                     c->ev_join, with_mutation);
+                                     c->ev_join, with_mutation, walk);
   cudaError_t e2 = cudaStreamEndCapture(c->stream, &g);
   if (e) {
     std::string where = std::string("capture generation (") + g_stage + ")";
@@ -625,13 +645,25 @@ static int capture_generation(dpso_ctx* c, bool with_mutation,
   return DPSO_OK;
 }
 
+static bool walk_eager(const dpso_ctx* c) {
+  return c->v.use_mutation && c->v.rng_mode == DPSO_RNG_NUMPY &&
+         c->v.mutation_period > 1 && !getenv("DPSO_ONE_GRAPH") &&
+         !getenv("DPSO_WALK_AFTER_MUTATION");
+}
+
 static int ensure_graph(dpso_ctx* c) {
   if (c->graph) return DPSO_OK;
-  int rc = capture_generation(c, true, &c->graph);
+  // mutation_period > 1: the walk is launched outside the graphs, right
+  // after each mutating generation, on the forked stream, and the next
+  // mutating generation waits for it (launch_generation): it hides behind
+  // every generation in between
+  int rc = capture_generation(c, true,
+                              walk_eager(c) ? kWalkNone : kWalkAfterMutation,
+                              &c->graph);
   if (rc) return rc;
   if (c->v.use_mutation && c->v.mutation_period > 1 &&
       !getenv("DPSO_ONE_GRAPH")) {
-    rc = capture_generation(c, false, &c->graph_plain);
+    rc = capture_generation(c, false, kWalkNone, &c->graph_plain);
     if (rc) return rc;
   }
   return DPSO_OK;
@@ -682,7 +714,18 @@ static int ensure_velocity(dpso_ctx* c, int gens) {
 static cudaError_t launch_generation(dpso_ctx* c) {
   const int64_t g = c->gen_next++;
   const bool mut = !c->graph_plain || (g % c->v.mutation_period == 0);
-  return cudaGraphLaunch(mut ? c->graph : c->graph_plain, c->stream);
+  const bool eager = mut && walk_eager(c);
+  cudaError_t e;
+  // this call's walk (launched after the previous mutating generation)
+  if (eager && (e = cudaStreamWaitEvent(c->stream, c->ev_join, 0))) return e;
+  if ((e = cudaGraphLaunch(mut ? c->graph : c->graph_plain, c->stream)))
+    return e;
+  if (!eager) return cudaSuccess;
+  // the next call's walk, concurrent with the generations until then
+  if ((e = cudaEventRecord(c->ev_fork, c->stream))) return e;
+  if ((e = cudaStreamWaitEvent(c->stream2, c->ev_fork, 0))) return e;
+  if ((e = launch_mutation_walk(c->v, c->stream2))) return e;
+  return cudaEventRecord(c->ev_join, c->stream2);
 }
 
 int dpso_step(dpso_ctx* c, int32_t gens) {
@@ -725,8 +768,13 @@ int dpso_step_timed(dpso_ctx* c, int32_t gens, double* phase_ms,
   cudaEvent_t ev[7];
   for (int i = 0; i < 7; ++i) CK(cudaEventCreate(&ev[i]));
   double acc[6] = {0, 0, 0, 0, 0, 0};
+  // the walk's place as in dpso_step (launch_generation)
+  const bool late = walk_eager(c);
   for (int g = 0; g < gens; ++g) {
     cudaStream_t s = c->stream;
+    const bool mut_gen =
+        v.use_mutation && (c->gen_next + g) % v.mutation_period == 0;
+    if (late && mut_gen) CK(cudaStreamWaitEvent(s, c->ev_join, 0));
     CK(cudaEventRecord(ev[0], s));
     CK(launch_gen_begin(v, s));
     CK(launch_update(v, s));
@@ -734,10 +782,12 @@ int dpso_step_timed(dpso_ctx* c, int32_t gens, double* phase_ms,
     if (v.use_mutation) {
       CK(launch_mutation_pre(v, s));
       CK(launch_mutation_post(v, s));
-      CK(cudaEventRecord(c->ev_fork, s));
-      CK(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
-      CK(launch_mutation_walk(v, c->stream2));
-      CK(cudaEventRecord(c->ev_join, c->stream2));
+      if (!late) {
+        CK(cudaEventRecord(c->ev_fork, s));
+        CK(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
+        CK(launch_mutation_walk(v, c->stream2));
+        CK(cudaEventRecord(c->ev_join, c->stream2));
+      }
       CK(launch_mutation_swap(v, s));
     }
     CK(cudaEventRecord(ev[2], s));
@@ -748,8 +798,14 @@ int dpso_step_timed(dpso_ctx* c, int32_t gens, double* phase_ms,
     if (v.use_edge_exchange) CK(launch_two_opt(v, s, 2));
     CK(cudaEventRecord(ev[5], s));
     if (v.use_edge_exchange) CK(launch_finalize(v, s));
-    if (v.use_mutation) CK(cudaStreamWaitEvent(s, c->ev_join, 0));
+    if (v.use_mutation && !late) CK(cudaStreamWaitEvent(s, c->ev_join, 0));
     CK(cudaEventRecord(ev[6], s));
+    if (late && mut_gen) {
+      CK(cudaEventRecord(c->ev_fork, s));
+      CK(cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
+      CK(launch_mutation_walk(v, c->stream2));
+      CK(cudaEventRecord(c->ev_join, c->stream2));
+    }
     CK(cudaEventSynchronize(ev[6]));
     for (int i = 0; i < 6; ++i) {
       float ms = 0.f;
@@ -899,6 +955,7 @@ int dpso_set_state(dpso_ctx* c, const int32_t* x, const int32_t* pbest,
   const int64_t P = c->prm.n_particles, n = c->n, np = c->v.np;
   int rc = sync_in(c);
   if (rc) return rc;
+  if ((rc = join_walk(c))) return rc;
   // every copy is stream-ordered on c->stream (pageable host sources are
   // staged by the driver; the stream sync below keeps them alive)
   std::vector<uint16_t> bx, bp, bv;
@@ -949,6 +1006,7 @@ int dpso_mutate_step(dpso_ctx* c) {
                 "dpso_mutate_step needs use_mutation and mutation_period == 1");
   int rc = sync_in(c);
   if (rc) return rc;
+  if ((rc = join_walk(c))) return rc;
   const SwarmView& v = c->v;
   // one generation reduced to its mutation call: gen_begin (marks it
   // mutating, selects the buffers the last walk prepared), the dedupe /
@@ -1016,6 +1074,7 @@ int dpso_island_adopt(dpso_ctx* c, const void* dev_records, int32_t world,
 void dpso_destroy(dpso_ctx* c) {
   if (!c) return;
   DevGuard g_(c->dev);
+  if (c->stream2) cudaStreamSynchronize(c->stream2);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->graph) cudaGraphExecDestroy(c->graph);
   if (c->graph_plain) cudaGraphExecDestroy(c->graph_plain);
