@@ -140,7 +140,7 @@ template <int MODE>
 __device__ __noinline__ int band_hit(int u0, int u1, int u2, int u3, int u4,
                                      int u5, int u6, int u7, int c0, int i,
                                      int Di, int L, int live, int win,
-                                     int* st, int* ws) {
+                                     int* st, int* ws, int* cmin) {
   const int uv[8] = {u0, u1, u2, u3, u4, u5, u6, u7};
   const int lane = threadIdx.x & 31;
   if (MODE == 1) {
@@ -168,11 +168,18 @@ __device__ __noinline__ int band_hit(int u0, int u1, int u2, int u3, int u4,
         wi = i2;
       }
     }
+    // the CTA-wide minimum t over all warps of this particle: a pair above
+    // it cannot be the argmin, so it caps every lane's limit (ties at it
+    // still hit; the final reduction breaks them)
+    int ct = wt;
     if (lane == 0) {
       ws[0] = wt;
       ws[1] = wi;
+      ct = min(atomicMin(cmin, wt), wt);
     }
-    return lane_limit<1>(live, Di, i, wt, wi);
+    ct = __shfl_sync(0xffffffffu, ct, 0);
+    return min(lane_limit<1>(live, Di, i, wt, wi),
+               live ? ct + Di : INT_MIN);
   }
   int lb = st[0], nc = st[32], of = st[64];
   int* cd = st + 96;
@@ -187,7 +194,11 @@ __device__ __noinline__ int band_hit(int u0, int u1, int u2, int u3, int u4,
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1)
     wm = min(wm, __shfl_xor_sync(0xffffffffu, wm, o));
-  const int lim = wm + win;
+  // the window around the CTA-wide minimum over all warps of the particle
+  int cm = wm;
+  if (lane == 0) cm = min(atomicMin(cmin, wm), wm);
+  cm = __shfl_sync(0xffffffffu, cm, 0);
+  const int lim = cm + win;
   int w = 0;
   for (int k = 0; k < nc; ++k) {
     const int dv = cd[32 * k];
@@ -254,7 +265,8 @@ template <int MODE, bool MASK>
 __device__ __forceinline__ void band_group(const int* O, const int* D,
                                            int c0, uint32_t R, int& prev,
                                            int& L, int i, int Di, bool live,
-                                           int win, int* st, int* ws) {
+                                           int win, int* st, int* ws,
+                                           int* cmin) {
   const int4 oa = *reinterpret_cast<const int4*>(O + 4 + c0);
   const int4 ob = *reinterpret_cast<const int4*>(O + 8 + c0);
   const int4 da = *reinterpret_cast<const int4*>(D + c0);
@@ -279,7 +291,7 @@ __device__ __forceinline__ void band_group(const int* O, const int* D,
                      min(min(u[4], u[5]), min(u[6], u[7])));
   if (__any_sync(0xffffffffu, mn <= L))
     L = band_hit<MODE>(u[0], u[1], u[2], u[3], u[4], u[5], u[6], u[7], c0, i,
-                       Di, L, live, win, st, ws);
+                       Di, L, live, win, st, ws, cmin);
 }
 
 // Persistent CTAs: kBandWarps consumer warps + kProdWarps producer warps.
@@ -308,6 +320,7 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ __align__(8) uint64_t colfull[kMaxNcb];
   __shared__ int s_fin[kMaxNcb], s_of[kMaxNcb];
+  __shared__ int s_cmin[kMaxNcb];  // CTA-wide running minimum t, per slot
   __shared__ double s_rd[kMaxNcb][kBandWarps];
   __shared__ int s_ri[kMaxNcb][kBandWarps], s_rj[kMaxNcb][kBandWarps];
   __shared__ int s_ws[kBandWarps][2];
@@ -335,7 +348,10 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
     }
     fence_barrier_init();
     for (int k = 0; k < ncb; ++k) mbar_init(&colfull[k], 1);
-    for (int k = 0; k < kMaxNcb; ++k) s_fin[k] = s_of[k] = 0;
+    for (int k = 0; k < kMaxNcb; ++k) {
+      s_fin[k] = s_of[k] = 0;
+      s_cmin[k] = kNone;
+    }
   }
   __syncthreads();
 
@@ -430,6 +446,10 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
     const uint32_t R =
         smem_u32(rowbuf + (size_t)s * stage_bytes) + (uint32_t)lane * (S + 4u);
     int L = lane_limit<MODE>(live, Di, i, ws[0], ws[1]);
+    {  // capped by the CTA-wide minimum (other warps' finds)
+      const int cm = *(volatile int*)&s_cmin[cb];
+      if (live) L = min(L, cm + (MODE == 2 ? a.win : 0) + Di);
+    }
     const int cs = (i0 + 2) & ~7;
     const int per = ((((n - cs) + NWg - 1) >> lgw) + 7) & ~7;
     const int cA = cs + wl * per, cB = min(n, cA + per);
@@ -438,10 +458,10 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
       int c0 = cA;
       for (; c0 < cB && c0 < i0 + 32; c0 += 8)
         band_group<MODE, true>(O, D, c0, R, prev, L, i, Di, live, a.win, st,
-                               ws);
+                               ws, &s_cmin[cb]);
       for (; c0 < cB; c0 += 8)
         band_group<MODE, false>(O, D, c0, R, prev, L, i, Di, live, a.win, st,
-                                ws);
+                                ws, &s_cmin[cb]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);  // the stage's reads are done
@@ -544,6 +564,7 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
         __syncwarp();
         if (lane == 0) {
           s_fin[cb] = 0;
+          s_cmin[cb] = kNone;
           s_of[cb] = 0;
         }
       }
