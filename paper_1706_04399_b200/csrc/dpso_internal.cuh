@@ -251,6 +251,19 @@ cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
                                 cudaStream_t s, int reserve_sms = 0);
 int two_opt_pick_chunks(int32_t n, int32_t P);
 
+// A random fp64 gather from the cost matrix (edge costs C[a][b]).  sm_100
+// fills 4 sectors (128 B) of L2 per random 8-B load by default; the
+// L2::64B prefetch-size hint halves that (measured: 117 -> 61 DRAM bytes
+// per load over a 1 GB table, tools/data/gran_probe), which matters when
+// the matrix is far beyond L2 (N = 10000: 800 MB).
+__device__ __forceinline__ double ld_cost(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::64B.f64 %0, [%1];"
+               : "=d"(v)
+               : "l"(p));
+  return v;
+}
+
 // Fitness in the reference's order (solver.py:48-54):
 // total = 0; total += d[n-1]; total += d[0]; ... total += d[n-2].
 __device__ __forceinline__ double seq_tour_sum(const double* d, int n) {

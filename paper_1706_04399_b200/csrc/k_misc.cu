@@ -793,7 +793,7 @@ __global__ void __launch_bounds__(128) k_init_build(SwarmView v,
     double* dg = v.dcache + (size_t)p * np;
     for (int i = tid; i < n; i += blockDim.x) {
       int a = body[i], b = body[i + 1 == n ? 0 : i + 1];
-      dg[i] = v.cost[(size_t)a * v.ld + b];
+      dg[i] = ld_cost(v.cost + (size_t)a * v.ld + b);
       xg[i] = (uint16_t)a;
       pb[i] = (uint16_t)a;
       if (v.vmap) v.vmap[(size_t)p * np + i] = (uint16_t)i;

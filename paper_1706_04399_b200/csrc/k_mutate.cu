@@ -970,7 +970,7 @@ __global__ void __launch_bounds__(128) k_mut_swap(SwarmView v) {
         int i = (e & 1) ? pos : pos - 1;  // edge (i, i+1)
         if (i < 0) i += n;
         const int a = body[i], b = body[i + 1 == n ? 0 : i + 1];
-        d[u] = v.cost[(size_t)a * v.ld + b];
+        d[u] = ld_cost(v.cost + (size_t)a * v.ld + b);
         at[u] = i;
       }
     }

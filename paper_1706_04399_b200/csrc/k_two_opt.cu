@@ -880,7 +880,7 @@ __global__ void __launch_bounds__(128) k_two_opt_apply(ApplyArgs a) {
   if (a.cost) {
     for (int k = i + tid; k <= j && k < a.n; k += blockDim.x) {
       int u = t[k], w = t[k + 1 == a.n ? 0 : k + 1];
-      a.dcache[(size_t)p * a.np + k] = a.cost[(size_t)u * a.ld + w];
+      a.dcache[(size_t)p * a.np + k] = ld_cost(a.cost + (size_t)u * a.ld + w);
     }
   }
   if (a.fit) {

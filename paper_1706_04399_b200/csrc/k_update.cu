@@ -245,7 +245,7 @@ __device__ void finish_particle(const SwarmView& v, int p, const uint16_t* sx,
         const int i1 = i + 1 == n ? 0 : i + 1;
         const int a = sx[i], b = sx[i1];
         moved[k] = !sold || a != sold[i] || b != sold[i1];
-        if (moved[k]) d[k] = __ldg(v.cost + (size_t)a * v.ld + b);
+        if (moved[k]) d[k] = ld_cost(v.cost + (size_t)a * v.ld + b);
       }
     }
 #pragma unroll
