@@ -62,13 +62,18 @@ def _lib():
     return L.load()
 
 
-@pytest.mark.parametrize("mode", [None, "filter32", "exact32/rows32"])
+@pytest.mark.parametrize("mode", [None, "column", "filter32",
+                                  "exact32/rows32"])
 def test_scan_one_task_per_particle_c3_shape(pkg, mode, monkeypatch):
-    # C3: N=500 integer grid, P=16384 -> chunks == 1 -> the non-persistent
-    # k_two_opt_scan32<16, EXACT32, fp16 rows> instantiation (the default)
+    # C3: N=500 integer grid, P=16384.  Default: the band scan (EXACT, two
+    # warp groups, ~110 particles per CTA); "column" and the modes: the
+    # column scan, chunks == 1 -> the non-persistent
+    # k_two_opt_scan32<16, EXACT32, fp16 rows> instantiation
     n, P = 500, 16384
     assert _lib().dpso_scan_chunks(n, P) == 1
-    if mode:
+    if mode == "column":
+        monkeypatch.setenv("DPSO_SCAN_BAND", "0")
+    elif mode:
         base, _, rows = mode.partition("/")
         monkeypatch.setenv("DPSO_SCAN_MODE", {"exact32": "1",
                                               "filter32": "2"}[base])
@@ -104,9 +109,13 @@ def test_scan_nopersist_c3_integer_euclid(pkg, mode, monkeypatch):
         check_subset(pkg, cost, tours, rng, 64, ("nopersist", n, mode))
 
 
-def test_scan_c2_shape_persistent(pkg):
-    # C2: N=1000 Euclidean (FILTER32, fp16 rows), P=1024 -> several tasks
-    # per particle -> the persistent-warp launch
+@pytest.mark.parametrize("scan", ["band", "column"])
+def test_scan_c2_shape_persistent(pkg, scan, monkeypatch):
+    # C2: N=1000 Euclidean, P=1024: the band scan (FILTER, two stages) by
+    # default; the column scan (FILTER32, fp16 rows) has several tasks per
+    # particle -> the persistent-warp launch
+    if scan == "column":
+        monkeypatch.setenv("DPSO_SCAN_BAND", "0")
     n, P = 1000, 1024
     assert _lib().dpso_scan_chunks(n, P) > 1
     rng = np.random.default_rng(1000)
