@@ -3,7 +3,8 @@
 // Pipeline (all kernels no-op unless ctl->mutating):
 //   k_mut_hash    per particle: canonical rotation/direction (graph.py:106-115)
 //                 and a 64-bit order-dependent hash of the canonical sequence
-//   k_mut_rank    rank in (fitness, slot) order by counting (solver.py:223-224)
+//   k_mut_rank    rank in (fitness, slot) order by counting over a 2-D grid
+//                 (solver.py:223-224)
 //   k_mut_dedupe  earliest-ranked particle with the same hash (candidate
 //                 duplicate source)
 //   k_mut_verify  one warp per candidate: exact canonical-form comparison
@@ -64,65 +65,69 @@ __global__ void __launch_bounds__(128) k_mut_hash(SwarmView v,
   if (tid == 0) {
     v.hash[p] = s_h;
     canon[p] = k | (rev << 31);
+    v.rank[p] = 0;             // k_mut_rank accumulates per column chunk
+    v.flag[p] = 0x7fffffff;    // k_mut_dedupe: lowest candidate rank
   }
 }
 
-constexpr int kTile = 2048;
+constexpr int kChunk = 1024;  // j values per CTA of the O(P^2) passes
 
+// fitness as an order-preserving u64 (fp64 bits, sign folded; -0.0 reads as
+// +0.0, since sorted() compares them equal): (key, slot) order is the
+// reference's (fitness, slot) order (solver.py:223-224)
+__device__ __forceinline__ uint64_t fit_key(double f) {
+  if (f == 0.0) f = 0.0;
+  const uint64_t b = (uint64_t)__double_as_longlong(f);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// rank in (fitness, slot) order by counting, P x P comparisons spread over
+// a 2-D grid (x: 256 particles i per CTA, y: a chunk of kChunk particles j);
+// each CTA adds its chunk's count (rank was zeroed by k_mut_hash)
 __global__ void __launch_bounds__(256) k_mut_rank(SwarmView v) {
   if (!v.ctl->mutating || v.ctl->done) return;
-  __shared__ double s_f[kTile];
+  __shared__ uint64_t s_k[kChunk];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const double fi = i < v.P ? v.fit[i] : 0.0;
+  const int base = blockIdx.y * kChunk;
+  const int m = min(kChunk, v.P - base);
+  for (int u = threadIdx.x; u < m; u += blockDim.x)
+    s_k[u] = fit_key(v.fit[base + u]);
+  __syncthreads();
+  if (i >= v.P) return;
+  const uint64_t ki = fit_key(v.fit[i]);
   int cnt = 0;
-  for (int base = 0; base < v.P; base += kTile) {
-    const int m = min(kTile, v.P - base);
-    __syncthreads();
-    for (int u = threadIdx.x; u < m; u += blockDim.x) s_f[u] = v.fit[base + u];
-    __syncthreads();
-    if (i < v.P) {
-      for (int u = 0; u < m; ++u) {
-        const double f = s_f[u];
-        const int j = base + u;
-        cnt += (f < fi) || (f == fi && j < i);
-      }
-    }
+  for (int u = 0; u < m; ++u) {
+    const uint64_t kj = s_k[u];
+    cnt += (kj < ki) || (kj == ki && base + u < i);
   }
-  if (i < v.P) {
-    v.rank[i] = cnt;
-    v.order[cnt] = i;
-  }
+  if (cnt) atomicAdd(&v.rank[i], cnt);
 }
 
-// Earliest-ranked particle with the same canonical hash and a lower rank
-// (-1: none) -> flag[i] holds that candidate + 1 until k_mut_verify.
+// The lowest rank among earlier-ranked particles with the same canonical
+// hash, over a 2-D grid as k_mut_rank (atomicMin into flag, which
+// k_mut_hash set to "none"); the first chunk also records order[rank].
 __global__ void __launch_bounds__(256) k_mut_dedupe(SwarmView v) {
   if (!v.ctl->mutating || v.ctl->done) return;
-  __shared__ unsigned long long s_h[kTile];
-  __shared__ int s_r[kTile];
+  __shared__ unsigned long long s_h[kChunk];
+  __shared__ int s_r[kChunk];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t hi = i < v.P ? v.hash[i] : 0;
-  const int ri = i < v.P ? v.rank[i] : 0;
-  int cand = -1, crank = 0x7fffffff;
-  for (int base = 0; base < v.P; base += kTile) {
-    const int m = min(kTile, v.P - base);
-    __syncthreads();
-    for (int u = threadIdx.x; u < m; u += blockDim.x) {
-      s_h[u] = v.hash[base + u];
-      s_r[u] = v.rank[base + u];
-    }
-    __syncthreads();
-    if (i < v.P) {
-      for (int u = 0; u < m; ++u) {
-        const int r = s_r[u];
-        if (s_h[u] == hi && r < ri && r < crank) {
-          crank = r;
-          cand = base + u;
-        }
-      }
-    }
+  const int base = blockIdx.y * kChunk;
+  const int m = min(kChunk, v.P - base);
+  for (int u = threadIdx.x; u < m; u += blockDim.x) {
+    s_h[u] = v.hash[base + u];
+    s_r[u] = v.rank[base + u];
   }
-  if (i < v.P) v.flag[i] = cand + 1;
+  __syncthreads();
+  if (i >= v.P) return;
+  const uint64_t hi = v.hash[i];
+  const int ri = v.rank[i];
+  if (blockIdx.y == 0) v.order[ri] = i;
+  int crank = 0x7fffffff;
+  for (int u = 0; u < m; ++u) {
+    const int r = s_r[u];
+    if (s_h[u] == hi && r < ri && r < crank) crank = r;
+  }
+  if (crank != 0x7fffffff) atomicMin(&v.flag[i], crank);
 }
 
 __device__ bool warp_canon_equal(const SwarmView& v, const int32_t* canon,
@@ -146,8 +151,12 @@ __global__ void __launch_bounds__(128) k_mut_verify(SwarmView v,
   if (!v.ctl->mutating || v.ctl->done) return;
   const int i = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (i >= v.P) return;
-  const int cand = v.flag[i] - 1;
-  if (cand < 0) return;  // flag already 0
+  const int crank = v.flag[i];
+  if (crank == 0x7fffffff) {  // no earlier particle with the same hash
+    if ((threadIdx.x & 31) == 0) v.flag[i] = 0;
+    return;
+  }
+  const int cand = v.order[crank];
   int dropped = warp_canon_equal(v, canon, i, cand);
   if (!dropped) {
     // 64-bit hash collision with a different tour: exact search over every
@@ -1006,8 +1015,9 @@ cudaError_t launch_mutation_pre(const SwarmView& v, cudaStream_t s) {
   // k_mut_lists rewrites it
   int32_t* canon = v.keep;
   k_mut_hash<<<P, 128, 0, s>>>(v, canon);
-  k_mut_rank<<<(P + 255) / 256, 256, 0, s>>>(v);
-  k_mut_dedupe<<<(P + 255) / 256, 256, 0, s>>>(v);
+  const dim3 g2((P + 255) / 256, (P + kChunk - 1) / kChunk);
+  k_mut_rank<<<g2, 256, 0, s>>>(v);
+  k_mut_dedupe<<<g2, 256, 0, s>>>(v);
   k_mut_verify<<<(P + 3) / 4, 128, 0, s>>>(v, canon);
   k_mut_lists<<<1, 1024, 0, s>>>(v);
   k_mut_copy<<<P, 128, 0, s>>>(v);
