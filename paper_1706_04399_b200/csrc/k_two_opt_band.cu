@@ -58,6 +58,10 @@
 #include "dpso_internal.cuh"
 #include "tma.cuh"
 
+#ifndef DPSO_BAND_NBLDS
+#define DPSO_BAND_NBLDS 1
+#endif
+
 namespace dpso {
 
 namespace {
@@ -266,7 +270,7 @@ __device__ __forceinline__ void band_group(const int* O, const int* D,
                                            int c0, uint32_t R, int& prev,
                                            int& L, int i, int Di, bool live,
                                            int win, int* st, int* ws,
-                                           int* cmin) {
+                                           int* cmin, uint32_t slot_next) {
   const int4 oa = *reinterpret_cast<const int4*>(O + 4 + c0);
   const int4 ob = *reinterpret_cast<const int4*>(O + 8 + c0);
   const int4 da = *reinterpret_cast<const int4*>(D + c0);
@@ -274,6 +278,19 @@ __device__ __forceinline__ void band_group(const int* O, const int* D,
   const int off[8] = {oa.x, oa.y, oa.z, oa.w, ob.x, ob.y, ob.z, ob.w};
   const int dv[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
   int g[8], u[8];
+#if DPSO_BAND_NBLDS
+  // the B term straight from slot l+1 (the next lane's row, S + 4 bytes
+  // on): a second LDS with an immediate offset instead of a shuffle
+  int nb[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t ad = R + (uint32_t)off[k];
+    g[k] = lds_s16(ad);
+    nb[k] = lds_s16(ad + slot_next);
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) u[k] = (k ? g[k - 1] : prev) + nb[k] - dv[k];
+#else
 #pragma unroll
   for (int k = 0; k < 8; ++k) g[k] = lds_s16(R + (uint32_t)off[k]);
 #pragma unroll
@@ -281,6 +298,7 @@ __device__ __forceinline__ void band_group(const int* O, const int* D,
     const int nb = __shfl_down_sync(0xffffffffu, g[k], 1);
     u[k] = (k ? g[k - 1] : prev) + nb - dv[k];
   }
+#endif
   prev = g[7];
   if (MASK) {
 #pragma unroll
@@ -458,10 +476,10 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
       int c0 = cA;
       for (; c0 < cB && c0 < i0 + 32; c0 += 8)
         band_group<MODE, true>(O, D, c0, R, prev, L, i, Di, live, a.win, st,
-                               ws, &s_cmin[cb]);
+                               ws, &s_cmin[cb], S + 4u);
       for (; c0 < cB; c0 += 8)
         band_group<MODE, false>(O, D, c0, R, prev, L, i, Di, live, a.win, st,
-                                ws, &s_cmin[cb]);
+                                ws, &s_cmin[cb], S + 4u);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);  // the stage's reads are done
