@@ -64,7 +64,7 @@ namespace {
   } while (0)
 
 struct Layout {
-  size_t off_ctl, off_streams, off_mut_start, off_init_start, off_x, off_pbest, off_vmap,
+  size_t off_ctl, off_streams, off_mut_start, off_init_start, off_x, off_pbest, off_vmap, off_vinv,
       off_vel, off_vel_len, off_fit, off_pfit, off_dcache, off_gbest,
       off_conv, off_tores, off_chunk_tab, off_rank, off_hash, off_flag, off_pbflag,
       off_sidx, off_order, off_surv, off_keep, off_ev_slot, off_ev_k,
@@ -106,7 +106,10 @@ Layout make_layout(const dpso_params* prm, int n) {
   L.off_init_start = take(sizeof(PcgState));
   L.off_x = take(2 * P * np);
   L.off_pbest = take(2 * P * np);
-  L.off_vmap = take(prm->inertia == 1.0 ? 2 * P * np : 0);
+  // vmap: w == 1 the composed velocity (solver.py:197-209); w < 1 the value
+  // map of the whole transposition list, with its inverse (k_update_wl)
+  L.off_vmap = take(2 * P * np);
+  L.off_vinv = take(prm->inertia < 1.0 ? 2 * P * np : 0);
   L.off_vel = take(L.vel_cap ? 4 * P * (L.vel_cap + 2 * (int64_t)n) : 0);
   L.off_vel_len = take(4 * P);
   L.off_fit = take(8 * P);
@@ -457,7 +460,8 @@ int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
   v.init_start = (PcgState*)(w + L.off_init_start);
   v.x = (uint16_t*)(w + L.off_x);
   v.pbest = (uint16_t*)(w + L.off_pbest);
-  v.vmap = prm->inertia == 1.0 ? (uint16_t*)(w + L.off_vmap) : nullptr;
+  v.vmap = (uint16_t*)(w + L.off_vmap);
+  v.vinv = prm->inertia < 1.0 ? (uint16_t*)(w + L.off_vinv) : nullptr;
   v.vel = L.vel_cap ? (uint32_t*)(w + L.off_vel) : nullptr;
   v.vel_len = (int32_t*)(w + L.off_vel_len);
   v.vel_cap = L.vel_cap;

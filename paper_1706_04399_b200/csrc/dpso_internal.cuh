@@ -122,6 +122,7 @@ struct SwarmView {
   uint16_t* x;
   uint16_t* pbest;
   uint16_t* vmap;
+  uint16_t* vinv;      // w < 1: inverse of vmap (the list's value map)
   uint32_t* vel;
   int32_t* vel_len;
   int64_t vel_cap;     // entries per particle list (excl. 2n scratch)

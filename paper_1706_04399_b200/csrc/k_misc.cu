@@ -797,6 +797,7 @@ __global__ void __launch_bounds__(128) k_init_build(SwarmView v,
       xg[i] = (uint16_t)a;
       pb[i] = (uint16_t)a;
       if (v.vmap) v.vmap[(size_t)p * np + i] = (uint16_t)i;
+      if (v.vinv) v.vinv[(size_t)p * np + i] = (uint16_t)i;
     }
     if (tid == 0 && v.vel_len) v.vel_len[p] = 0;
     __syncthreads();  // the fitness (fit = pfit) follows in k_fitness

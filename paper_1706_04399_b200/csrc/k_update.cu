@@ -94,12 +94,17 @@ __device__ __forceinline__ void copy_row16(uint16_t* dst, const uint16_t* src,
 // from global memory (tgt_g) instead of a shared copy sT (large n: the
 // low-shared-memory update); sout may then alias sW (written only after the
 // last read of sW).
+// emit (w < 1): also write the first k repair transpositions, in the
+// reference's order, to emit[0 .. k) as (have | want << 16) and return k
+// (the e-th emitting position p_e: want = T[p_e]; have = the value at p_e
+// after the positions < p_e are repaired = T[r], r the first position >= p_e
+// on p_e's backward pi-orbit - the sum of these walks is O(n log n))
 template <int T, bool GT = false>
-__device__ void sigma_pass(const uint16_t* __restrict__ tgt_g, double c,
-                           int n, int R, const uint16_t* sx,
-                           const uint16_t* sposx, uint16_t* sT, uint16_t* sB,
-                           uint32_t* sW, uint16_t* sout, int* s_warp,
-                           int* s_misc) {
+__device__ int sigma_pass(const uint16_t* __restrict__ tgt_g, double c,
+                          int n, int R, const uint16_t* sx,
+                          const uint16_t* sposx, uint16_t* sT, uint16_t* sB,
+                          uint32_t* sW, uint16_t* sout, int* s_warp,
+                          int* s_misc, uint32_t* emit = nullptr) {
   const int tid = threadIdx.x;
   if (GT) {
     sT = const_cast<uint16_t*>(tgt_g);  // reads only (via the cache)
@@ -185,7 +190,19 @@ __device__ void sigma_pass(const uint16_t* __restrict__ tgt_g, double c,
   if (k == 0) {
     for (int v = tid; v < n; v += T) sout[v] = (uint16_t)v;
     __syncthreads();
-    return;
+    return 0;
+  }
+  if (emit && excl < k) {
+    int e = excl;
+    for (int p = c0; p < c1 && e < k; ++p) {
+      if ((int)(sW[p] >> 16) != p) {
+        int b = sB[p];
+        while (b < p) b = sB[b];
+        const uint32_t want = GT ? __ldg(tgt_g + p) : sT[p];
+        const uint32_t have = GT ? __ldg(tgt_g + b) : sT[b];
+        emit[e++] = have | (want << 16);
+      }
+    }
   }
   if (excl <= k - 1 && k - 1 < excl + cnt) {
     int need = k - 1 - excl;
@@ -218,6 +235,7 @@ __device__ void sigma_pass(const uint16_t* __restrict__ tgt_g, double c,
     sout[sx[q]] = cur;
   }
   __syncthreads();
+  return k;
 }
 
 // x' is in sx: write x and the edge costs d_i (dcache).  The fitness and
@@ -372,6 +390,99 @@ __device__ int repair_seq(const uint16_t* sx, const uint16_t* tgt, int n,
     }
   }
   return cnt;
+}
+
+// w < 1, CTA-parallel (solver.py:213-216): the velocity list v is kept,
+// and with it V = the value map of the whole list (apply_open(body, v) ==
+// V o body) and V^-1, so a generation never replays the list:
+//   1. truncation to the kept prefix v[0:k0], k0 = _prefix_len(w, len):
+//      V <- tau_{k0+1} o ... o tau_len o V (the dropped suffix undone, last
+//      first, by left multiplication on V / V^-1: O(len - k0), one thread);
+//   2. t1, t2 = the first k1 / k2 repair transpositions x -> pbest /
+//      x -> gbest, data-parallel (sigma_pass, which also emits them in the
+//      reference's order straight into v[k0 ..]);
+//   3. V <- sigma2 o sigma1 o V, x' = V o x (as for w == 1).
+// The lists grow on the host (ensure_velocity); overflow fails loudly.
+template <int T>
+__global__ void __launch_bounds__(T) k_update_wl(SwarmView v, int R) {
+  if (v.ctl->done) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = v.n, np = v.np, tid = threadIdx.x;
+  uint16_t* sx = (uint16_t*)smem;
+  uint16_t* sposx = sx + np;
+  uint16_t* ssig1 = sposx + np;
+  uint16_t* ssig2 = ssig1 + np;
+  uint16_t* sT = ssig2 + np;
+  uint16_t* sB = sT + np;
+  uint32_t* sW = (uint32_t*)(sB + np);
+  uint16_t* sV = (uint16_t*)(sW + np);
+  uint16_t* sVi = sV + np;
+  __shared__ int s_warp[32];
+  __shared__ int s_misc[4];
+  __shared__ int s_k[4];
+  __shared__ double s_c[2];
+  const int64_t stride = v.vel_cap + 2 * (int64_t)n;
+  for (int p = blockIdx.x; p < v.P; p += gridDim.x) {
+    const uint16_t* xg = v.x + (size_t)p * np;
+    uint16_t* vg = v.vmap + (size_t)p * np;
+    uint16_t* vig = v.vinv + (size_t)p * np;
+    uint32_t* lst = v.vel + (size_t)p * stride;
+    copy_row16<T>(sx, xg, n);
+    copy_row16<T>(sV, vg, n);
+    copy_row16<T>(sVi, vig, n);
+    __syncthreads();
+    for (int i = tid; i < n; i += T) sposx[sx[i]] = (uint16_t)i;
+    if (tid == 0) {
+      double r1, r2;
+      draw_r1r2(v, p, &r1, &r2);
+      s_c[0] = __dmul_rn(v.cognitive, r1);
+      s_c[1] = __dmul_rn(v.social, r2);
+      const int len = v.vel_len[p];
+      const int k0 = prefix_len(v.inertia, len);
+      // undo the dropped suffix v[k0:len], last first
+      for (int e = len - 1; e >= k0; --e) {
+        const uint32_t ab = lst[e];
+        const uint16_t a = ab & 0xFFFFu, b = ab >> 16;
+        const uint16_t ia = sVi[a], ib = sVi[b];
+        sV[ia] = b;
+        sV[ib] = a;
+        sVi[a] = ib;
+        sVi[b] = ia;
+      }
+      s_k[0] = k0;
+    }
+    __syncthreads();
+    const int k0 = s_k[0];
+    // the lists have room for both prefixes (the host grows them); the
+    // emission writes the entries it keeps only
+    int k1 = sigma_pass<T>(v.pbest + (size_t)p * np, s_c[0], n, R, sx, sposx,
+                           sT, sB, sW, ssig1, s_warp, s_misc, lst + k0);
+    if (tid == 0) s_k[1] = k1;
+    __syncthreads();
+    k1 = s_k[1];
+    int k2 = sigma_pass<T>(v.gbest, s_c[1], n, R, sx, sposx, sT, sB, sW,
+                           ssig2, s_warp, s_misc, lst + k0 + k1);
+    if (tid == 0) s_k[2] = k2;
+    __syncthreads();
+    k2 = s_k[2];
+    if (tid == 0) {
+      if ((int64_t)k0 + k1 + k2 > v.vel_cap) v.ctl->vel_overflow = 1;
+      v.vel_len[p] = k0 + k1 + k2;
+      atomicMax(&v.ctl->vel_max, k0 + k1 + k2);
+    }
+    // V' = sigma2 o sigma1 o V, V'^-1, x' = V' o x
+    for (int u = tid; u < n; u += T) {
+      const uint16_t w = ssig2[ssig1[sV[u]]];
+      sT[u] = w;
+      sB[w] = (uint16_t)u;
+    }
+    __syncthreads();
+    copy_row16<T>(vg, sT, n);
+    copy_row16<T>(vig, sB, n);
+    for (int i = tid; i < n; i += T) sposx[i] = sT[sx[i]];
+    __syncthreads();
+    finish_particle<T>(v, p, sposx, sx);
+  }
 }
 
 __global__ void __launch_bounds__(32) k_update_seq(SwarmView v) {
@@ -581,7 +692,24 @@ cudaError_t launch_update(const SwarmView& v, cudaStream_t s) {
       case 1024: go(k_update_w1<1024>, 1024); break;
       default: go(k_update_w1<256>, 256); break;
     }
+  } else if (v.vinv && 20 * (size_t)v.np <= 200 * 1024 &&
+             !getenv("DPSO_UPD_SEQ")) {
+    const size_t smem = (size_t)20 * v.np;
+    const int R = ceil_log2(v.n);
+    int T = 64;
+    while (T < 512 && T * 8 < v.n) T <<= 1;
+    auto go = [&](auto k, int t) {
+      set_dyn_smem((const void*)k, smem);
+      k<<<grid, t, smem, s>>>(v, R);
+    };
+    switch (T) {
+      case 64: go(k_update_wl<64>, 64); break;
+      case 128: go(k_update_wl<128>, 128); break;
+      case 512: go(k_update_wl<512>, 512); break;
+      default: go(k_update_wl<256>, 256); break;
+    }
   } else {
+    // the sequential replay (n > ~5000 with w < 1, or DPSO_UPD_SEQ=1)
     size_t smem = (size_t)8 * v.np + (size_t)8 * v.np;
     set_dyn_smem((const void*)k_update_seq, smem);
     k_update_seq<<<grid, 32, smem, s>>>(v);
