@@ -14,9 +14,11 @@
 // own slot at the SAME offset a_c:
 //     G_l(c) = M[i0+l][c]        (one LDS per lane per step)
 // The pair (i0+l, c-1) is G_l(c-1) + G_{l+1}(c) - d_i - d_{c-1}: its first
-// term is the lane's previous gather, its second arrives from lane l+1 by
-// one shuffle.  So each pair costs one shared-memory gather, one shuffle and
-// one IADD3.
+// term is the lane's previous gather, its second the same gather from slot
+// l+1 - a second LDS at the lane's address plus the slot stride, which
+// ptxas folds into [R + UR] addressing.  So each pair costs two
+// conflict-free shared-memory loads, one IADD for the address, one IADD3
+// and one min (DPSO_BAND_NBLDS=0: a shuffle from lane l+1 instead).
 //
 // Bank-conflict freedom: slot l's element a sits at byte l*(S+4) + 2a of the
 // stage (S a multiple of 128), i.e. in bank (l + a/2) mod 32 - a different
@@ -44,10 +46,12 @@
 // asymmetric matrices).
 //
 // Pipeline: persistent CTAs (one per SM), particles blockIdx.x + k*grid;
-// two band stages (the next band's 32 rows stream in while this one is
-// scanned), refilled by the last warp done with a stage, so warps only
-// wait on the rows, not on each other; the particle's column arrays
-// (offsets 2*a_c and d values, k_band_cols) ride along with its band 0.
+// a ring of 2-4 band stages filled by producer warps (bulk copies, full /
+// empty mbarriers), consumed by consumer warps at their own pace (no CTA
+// barrier per band; with 4 stages two warp groups take alternate bands); a
+// CTA-wide running minimum caps every warp's hit threshold; the particle's
+// column records (offsets 2*a_c and d values, k_band_cols) arrive on their
+// own barrier; the last warp done with a particle reduces its result.
 #include <float.h>
 #include <limits.h>
 #include <stdlib.h>
