@@ -244,7 +244,8 @@ __device__ __noinline__ int band_hit(int u0, int u1, int u2, int u3, int u4,
 __global__ void k_band_cols(const uint16_t* tours, int np,
                             const double* dcache, int n, int cw, int count,
                             double scale, double vfrom, double vto,
-                            int32_t* out) {
+                            int32_t* out, const DevCtl* ctl) {
+  if (ctl && (ctl->done || ctl->improved)) return;  // no scan this time
   const int p = blockIdx.x;
   if (p >= count) return;
   const uint16_t* t = tours + (size_t)p * np;
@@ -752,7 +753,8 @@ cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
   a.cw = band_cw(n);
   a.cols = pl.band_cols;
   k_band_cols<<<count, 256, 0, s>>>(tours, np, dcache, n, a.cw, count,
-                                     a.scale, a.vfrom, a.vto, pl.band_cols);
+                                     a.scale, a.vfrom, a.vto, pl.band_cols,
+                                     ctl);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
   a.nst = band_stages(n);
