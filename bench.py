@@ -266,6 +266,17 @@ def run_reference(args, cfg_name, cfg):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    # the port against the unmodified reference solver, measured in the
+    # build container (tools/port_vs_reference.py): same results, same speed
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02",
+                               "port_vs_reference.json")) as fh:
+            pv = json.load(fh)
+        line["cpu_baseline"]["port_vs_reference"] = {
+            k: pv[k] for k in ("n", "P", "generations", "identical",
+                               "reference_rate", "port_rate", "unit")}
+    except Exception:
+        pass
     print(json.dumps(line), flush=True)
 
 
