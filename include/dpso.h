@@ -209,6 +209,25 @@ int dpso_build_cost(const uint8_t* dev_occ, int32_t nx, int32_t ny,
                     int64_t ld, uint8_t* dev_virtual, double* host_vcost,
                     void* cuda_stream);
 
+/* The same build in two steps, for a build sharded over GPUs (SURVEY
+ * §8(e): shard the SSSP sources, all-gather the row blocks).
+ * dpso_build_cost_rows: rows [src_begin, src_end) of the n x n distance
+ * table, dev_rows[(i - src_begin) * n + j] = cost of the i -> j motion
+ * (+inf when blocked), i.e. graph.py:58-66's pair loop for those sources.
+ * Every viewpoint is checked (occupied -> DPSO_EINVAL on every rank).
+ * dpso_build_cost_assemble: graph.py:63-78 over the complete table (its
+ * upper triangle): symmetric cost, virtual mask and virtual cost exactly as
+ * dpso_build_cost writes them. */
+int dpso_build_cost_rows(const uint8_t* dev_occ, int32_t nx, int32_t ny,
+                         int32_t nz, const double* host_weights,
+                         const int32_t* host_vox, int32_t n,
+                         int32_t src_begin, int32_t src_end, double* dev_rows,
+                         void* cuda_stream);
+int dpso_build_cost_assemble(const double* dev_rows, int32_t n,
+                             double* dev_cost, int64_t ld,
+                             uint8_t* dev_virtual, double* host_vcost,
+                             void* cuda_stream);
+
 /* Plain-text cost-matrix files (replaces graph.py:123-130
  * save_cost_matrix and graph.py:133-143 load_cost_matrix, host code).
  * Write: a header line "n", then n lines of n entries, each Python's

@@ -15,6 +15,9 @@ oracle/dpso_oracle.py for the rules).
 * ``build_cost``   — graph.py:41-78: pairwise costs for i < j from source i,
                     symmetric fill, blocked pairs -> VIRTUAL_SCALE * n *
                     max_finite (1e6 when no finite edge)
+* ``distance_rows`` / ``assemble`` — the same build split at the sharded
+                    build's exchange step: one rank's source rows, then
+                    graph.py:63-78 over the gathered table
 
 * ``save_cost_matrix`` / ``load_cost_matrix`` — graph.py:123-143, the
                     plain-text matrix format (repr(float(x)) entries)
@@ -88,6 +91,37 @@ def build_cost(occ: np.ndarray, vox, weights):
     for i, j in blocked:
         cost[i, j] = cost[j, i] = vcost
         virtual[i, j] = virtual[j, i] = True
+    return cost, virtual, vcost
+
+
+def distance_rows(occ: np.ndarray, vox, weights, lo: int, hi: int):
+    """Rows lo..hi-1 of the pairwise distance table (inf when blocked): the
+    sources a rank of the sharded build owns (graph.py:58-66's loop body)."""
+    n = len(vox)
+    vox = [tuple(int(c) for c in v) for v in vox]
+    rows = np.full((hi - lo, n), math.inf)
+    for i in range(lo, hi):
+        d = dijkstra_all(occ, weights, vox[i])
+        for j in range(n):
+            c = d.get(vox[j])
+            if c is not None:
+                rows[i - lo, j] = c
+    return rows
+
+
+def assemble(rows: np.ndarray):
+    """graph.py:63-78 over a complete distance table (upper triangle)."""
+    n = rows.shape[0]
+    up = np.triu(np.ones((n, n), dtype=bool), 1)
+    blocked = up & ~np.isfinite(rows)
+    fin = up & np.isfinite(rows)
+    max_finite = float(rows[fin].max()) if fin.any() else 0.0
+    vcost = (VIRTUAL_SCALE * n * max_finite if max_finite > 0
+             else FALLBACK_VIRTUAL)
+    cost = np.where(fin, rows, 0.0)
+    cost[blocked] = vcost
+    cost = cost + cost.T
+    virtual = blocked | blocked.T
     return cost, virtual, vcost
 
 

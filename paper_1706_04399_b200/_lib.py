@@ -71,6 +71,9 @@ _SIG = {
     "dpso_nn_two_opt": (_I32, [_P, _I64, _I32, _P, _P, _P]),
     "dpso_build_cost": (_I32, [_P, _I32, _I32, _I32, _P, _P, _I32, _P, _I64,
                                 _P, _P, _P]),
+    "dpso_build_cost_rows": (_I32, [_P, _I32, _I32, _I32, _P, _P, _I32, _I32,
+                                     _I32, _P, _P]),
+    "dpso_build_cost_assemble": (_I32, [_P, _I32, _P, _I64, _P, _P, _P]),
     "dpso_philox4x32_10": (_I32, [_P, ctypes.c_uint64, _P]),
     "dpso_write_matrix_text": (_I32, [ctypes.c_char_p, _P, _I64, _I32]),
     "dpso_read_matrix_text": (_I32, [ctypes.c_char_p, _P, _I64, _I32,

@@ -248,6 +248,17 @@ struct DevGuard {
   }
 };
 
+// the device a device pointer lives on, -1 if it is not a device pointer
+static int ptr_device(const void* p) {
+  cudaPointerAttributes at;
+  int d = -1;
+  if (p && cudaPointerGetAttributes(&at, p) == cudaSuccess &&
+      at.type == cudaMemoryTypeDevice)
+    d = at.device;
+  cudaGetLastError();
+  return d;
+}
+
 static int sync_in(dpso_ctx* c) {
   CK(cudaEventRecord(c->ev, c->user));
   CK(cudaStreamWaitEvent(c->stream, c->ev, 0));
@@ -321,20 +332,21 @@ extern "C" {
 
 const char* dpso_last_error(void) { return g_err.c_str(); }
 
-int dpso_build_cost(const uint8_t* dev_occ, int32_t nx, int32_t ny,
-                    int32_t nz, const double* host_weights,
-                    const int32_t* host_vox, int32_t n, double* dev_cost,
-                    int64_t ld, uint8_t* dev_virtual, double* host_vcost,
-                    void* cuda_stream) {
-  if (!dev_occ || !host_weights || !host_vox || !dev_cost || !host_vcost ||
-      n < 1 || nx < 1 || ny < 1 || nz < 1 || ld < n)
+namespace {
+// shared argument checks of the cost-build entry points; fills lin
+int check_build_args(const uint8_t* dev_occ, int32_t nx, int32_t ny,
+                     int32_t nz, const double* host_weights,
+                     const int32_t* host_vox, int32_t n,
+                     std::vector<int64_t>& lin) {
+  if (!dev_occ || !host_weights || !host_vox || n < 1 || nx < 1 || ny < 1 ||
+      nz < 1)
     return fail(DPSO_EINVAL, "bad arguments");
   if ((int64_t)nx * ny * nz >= (1ll << 31))
     return fail(DPSO_EINVAL, "grid too large for 32-bit voxel indices");
   for (int i = 0; i < 3; ++i)
     if (!(host_weights[i] >= 0.0))
       return fail(DPSO_EINVAL, "axis weights must be non-negative");
-  std::vector<int64_t> lin(n);
+  lin.resize(n);
   for (int j = 0; j < n; ++j) {
     const int x = host_vox[3 * j], y = host_vox[3 * j + 1],
               z = host_vox[3 * j + 2];
@@ -342,18 +354,74 @@ int dpso_build_cost(const uint8_t* dev_occ, int32_t nx, int32_t ny,
       return fail(DPSO_EINVAL, "viewpoint voxel outside the grid");
     lin[j] = ((int64_t)x * ny + y) * nz + z;
   }
+  return DPSO_OK;
+}
+
+int occupied_fail(const int32_t* host_vox, int bad) {
+  char buf[160];
+  snprintf(buf, sizeof buf, "viewpoint %d maps to occupied voxel (%d, %d, %d)",
+           bad, host_vox[3 * bad], host_vox[3 * bad + 1],
+           host_vox[3 * bad + 2]);
+  return fail(DPSO_EINVAL, buf);
+}
+}  // namespace
+
+int dpso_build_cost(const uint8_t* dev_occ, int32_t nx, int32_t ny,
+                    int32_t nz, const double* host_weights,
+                    const int32_t* host_vox, int32_t n, double* dev_cost,
+                    int64_t ld, uint8_t* dev_virtual, double* host_vcost,
+                    void* cuda_stream) {
+  std::vector<int64_t> lin;
+  if (int r = check_build_args(dev_occ, nx, ny, nz, host_weights, host_vox, n,
+                               lin))
+    return r;
+  if (!dev_cost || !host_vcost || ld < n)
+    return fail(DPSO_EINVAL, "bad arguments");
+  DevGuard g(ptr_device(dev_occ));
+  NvtxRange nv("dpso_build_cost");
   int bad = -1;
   cudaError_t e = build_cost_sssp(dev_occ, nx, ny, nz, host_weights,
                                   lin.data(), n, dev_cost, ld, dev_virtual,
                                   host_vcost, &bad, (cudaStream_t)cuda_stream);
   if (e) return cuda_fail(e, "build_cost_sssp");
-  if (bad >= 0) {
-    char buf[160];
-    snprintf(buf, sizeof buf, "viewpoint %d maps to occupied voxel (%d, %d, %d)",
-             bad, host_vox[3 * bad], host_vox[3 * bad + 1],
-             host_vox[3 * bad + 2]);
-    return fail(DPSO_EINVAL, buf);
-  }
+  if (bad >= 0) return occupied_fail(host_vox, bad);
+  return DPSO_OK;
+}
+
+int dpso_build_cost_rows(const uint8_t* dev_occ, int32_t nx, int32_t ny,
+                         int32_t nz, const double* host_weights,
+                         const int32_t* host_vox, int32_t n,
+                         int32_t src_begin, int32_t src_end, double* dev_rows,
+                         void* cuda_stream) {
+  std::vector<int64_t> lin;
+  if (int r = check_build_args(dev_occ, nx, ny, nz, host_weights, host_vox, n,
+                               lin))
+    return r;
+  if (src_begin < 0 || src_end < src_begin || src_end > n ||
+      (src_end > src_begin && !dev_rows))
+    return fail(DPSO_EINVAL, "bad source range");
+  DevGuard g(ptr_device(dev_occ));
+  NvtxRange nv("dpso_build_cost_rows");
+  int bad = -1;
+  cudaError_t e = sssp_rows(dev_occ, nx, ny, nz, host_weights, lin.data(), n,
+                            src_begin, src_end, dev_rows, &bad,
+                            (cudaStream_t)cuda_stream);
+  if (e) return cuda_fail(e, "sssp_rows");
+  if (bad >= 0) return occupied_fail(host_vox, bad);
+  return DPSO_OK;
+}
+
+int dpso_build_cost_assemble(const double* dev_rows, int32_t n,
+                             double* dev_cost, int64_t ld,
+                             uint8_t* dev_virtual, double* host_vcost,
+                             void* cuda_stream) {
+  if (!dev_rows || !dev_cost || !host_vcost || n < 1 || ld < n)
+    return fail(DPSO_EINVAL, "bad arguments");
+  DevGuard g(ptr_device(dev_rows));
+  NvtxRange nv("dpso_build_cost_assemble");
+  cudaError_t e = cost_assemble(dev_rows, n, dev_cost, ld, dev_virtual,
+                                host_vcost, (cudaStream_t)cuda_stream);
+  if (e) return cuda_fail(e, "cost_assemble");
   return DPSO_OK;
 }
 

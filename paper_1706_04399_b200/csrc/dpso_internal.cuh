@@ -233,6 +233,13 @@ cudaError_t build_cost_sssp(const uint8_t* dev_occ, int nx, int ny, int nz,
                             double* dev_cost, int64_t ld, uint8_t* dev_virtual,
                             double* host_vcost, int* bad_viewpoint,
                             cudaStream_t s);
+cudaError_t sssp_rows(const uint8_t* dev_occ, int nx, int ny, int nz,
+                      const double* w, const int64_t* host_vox, int n,
+                      int src_begin, int src_end, double* rows,
+                      int* bad_viewpoint, cudaStream_t s);
+cudaError_t cost_assemble(const double* rows, int n, double* dev_cost,
+                          int64_t ld, uint8_t* dev_virtual,
+                          double* host_vcost, cudaStream_t s);
 int two_opt_chunk_table(int32_t n, int32_t chunks, int32_t* tab);
 // band scan (k_two_opt_band.cu): two stages of 32 rows must fit shared
 // memory (n <= ~1330)

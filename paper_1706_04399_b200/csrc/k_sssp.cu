@@ -17,6 +17,7 @@
 // Then cost[i][j] = dist_min(i,j)(vox[max(i,j)]) (the reference computes
 // each pair from its lower index), blocked pairs get
 // VIRTUAL_SCALE * n * max_finite (1e6 when no finite edge).
+#include <cstdlib>
 #include <math.h>
 
 #include <algorithm>
@@ -183,25 +184,55 @@ __global__ void k_check_free(const uint8_t* occ, const int64_t* vox, int n,
   if (j < n && occ[vox[j]]) atomicMin(bad, j);
 }
 
+// The build's workspace comes from the device's default stream-ordered
+// pool; by default the pool returns freed memory to the driver at every
+// synchronisation, so each build (and each batch's host poll) re-maps
+// hundreds of MB.  Keep up to 1 GB cached (process-wide, once per device).
+void keep_pool_memory() {
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 ||
+      done[dev])
+    return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = 1ull << 30;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
+  done[dev] = true;
+}
+
 }  // namespace
 
-cudaError_t build_cost_sssp(const uint8_t* dev_occ, int nx, int ny, int nz,
-                            const double* w, const int64_t* host_vox, int n,
-                            double* dev_cost, int64_t ld, uint8_t* dev_virtual,
-                            double* host_vcost, int* bad_viewpoint,
-                            cudaStream_t s) {
+// Rows [src_begin, src_end) of the pairwise distance table:
+// rows[(i - src_begin) * n + j] = dist_i(vox[j]) (+inf when unreachable).
+// Every viewpoint is checked for occupancy first (all ranks of a sharded
+// build fail the same way).
+cudaError_t sssp_rows(const uint8_t* dev_occ, int nx, int ny, int nz,
+                      const double* w, const int64_t* host_vox, int n,
+                      int src_begin, int src_end, double* rows,
+                      int* bad_viewpoint, cudaStream_t s) {
   *bad_viewpoint = -1;
   const int64_t V = (int64_t)nx * ny * nz;
-  // memory budget for the concurrent sources: dist 8 + 2 worklists 8 + flag 4
+  const int ns = src_end - src_begin;
+  // concurrent sources: their distance arrays (8 B/voxel) capped at
+  // ~256 MB (about twice the L2: a batch's hot frontier stays L2-resident)
+  // (tools/sssp_batch_probe.py, profiles/r02/sssp_batch_probe.jsonl: ~220
+  // sources build the office scene in 38 ms, all 816 at once in 58 ms),
+  // under a 4 GB cap on dist + worklists + flags
   const int64_t per_src = 20 * V;
   const int64_t budget = 4ll << 30;
-  int B = (int)std::max<int64_t>(1, std::min<int64_t>(n, budget / per_src));
+  int B = (int)std::max<int64_t>(
+      1, std::min<int64_t>({(int64_t)std::max(ns, 1), budget / per_src,
+                            (256ll << 20) / (8 * V)}));
   B = std::min(B, 1024);
+  if (const char* ev = getenv("DPSO_SSSP_BATCH")) B = std::max(1, atoi(ev));
+  keep_pool_memory();
   unsigned char* buf = nullptr;
   auto rnd = [](int64_t b) { return round_up(b, 256); };
   const size_t bytes = rnd(8 * B * V) + 2 * rnd(4 * B * V) + rnd(4 * B * V) +
-                       2 * rnd(4 * B) + rnd(8 * (int64_t)n) +
-                       rnd(8 * (int64_t)n * n) + rnd(64);
+                       2 * rnd(4 * B) + rnd(8 * (int64_t)n) + rnd(64);
   cudaError_t e = cudaMallocAsync(&buf, bytes, s);
   if (e) return e;
   size_t o = 0;
@@ -233,10 +264,8 @@ cudaError_t build_cost_sssp(const uint8_t* dev_occ, int nx, int ny, int nz,
   a.qlen[0] = (int32_t*)take(4 * B);
   a.qlen[1] = (int32_t*)take(4 * B);
   int64_t* dvox = (int64_t*)take(8 * (int64_t)n);
-  double* rowd = (double*)take(8 * (int64_t)n * n);
   unsigned char* misc = take(64);
   int* next_total = (int*)misc;
-  unsigned long long* mx = (unsigned long long*)(misc + 8);
   int* dbad = (int*)(misc + 16);
   a.next_total = next_total;
   if (!e) e = cudaMemcpyAsync(dvox, host_vox, 8 * (int64_t)n,
@@ -253,8 +282,8 @@ cudaError_t build_cost_sssp(const uint8_t* dev_occ, int nx, int ny, int nz,
   }
   const int blocks_per_src =
       (int)std::max<int64_t>(1, std::min<int64_t>(64, (V + 255) / 256));
-  for (int first = 0; first < n && !e; first += B) {
-    const int bs = std::min(B, n - first);
+  for (int first = src_begin; first < src_end && !e; first += B) {
+    const int bs = std::min(B, src_end - first);
     a.batch = bs;
     a.src = dvox + first;
     const int64_t tot = (int64_t)bs * V;
@@ -276,22 +305,53 @@ cudaError_t build_cost_sssp(const uint8_t* dev_occ, int nx, int ny, int nz,
       }
     }
     if (!e)
-      k_sssp_gather<<<dim3((n + 255) / 256, bs), 256, 0, s>>>(a, first, n,
-                                                              dvox, rowd);
-  }
-  if (!e) e = cudaMemsetAsync(mx, 0, 8, s);
-  if (!e) {
-    const int blocks = (int)std::min<int64_t>(((int64_t)n * n + 255) / 256,
-                                              4096);
-    k_cost_maxfinite<<<std::max(blocks, 1), 256, 0, s>>>(rowd, n, mx);
-    double* dvc = (double*)(misc + 24);
-    k_cost_fill<<<std::max(blocks, 1), 256, 0, s>>>(rowd, n, mx, dev_cost, ld,
-                                                    dev_virtual, dvc);
-    e = cudaMemcpyAsync(host_vcost, dvc, 8, cudaMemcpyDeviceToHost, s);
+      k_sssp_gather<<<dim3((n + 255) / 256, bs), 256, 0, s>>>(
+          a, first - src_begin, n, dvox, rows);
   }
   if (!e) e = cudaStreamSynchronize(s);
   cudaFreeAsync(buf, s);
   if (!e) e = cudaGetLastError();
+  return e;
+}
+
+// graph.py:63-78 over a complete n x n distance table (upper triangle used)
+cudaError_t cost_assemble(const double* rows, int n, double* dev_cost,
+                          int64_t ld, uint8_t* dev_virtual,
+                          double* host_vcost, cudaStream_t s) {
+  unsigned char* misc = nullptr;
+  cudaError_t e = cudaMallocAsync(&misc, 64, s);
+  if (e) return e;
+  unsigned long long* mx = (unsigned long long*)misc;
+  double* dvc = (double*)(misc + 8);
+  e = cudaMemsetAsync(mx, 0, 8, s);
+  if (!e) {
+    const int blocks = (int)std::min<int64_t>(((int64_t)n * n + 255) / 256,
+                                              4096);
+    k_cost_maxfinite<<<std::max(blocks, 1), 256, 0, s>>>(rows, n, mx);
+    k_cost_fill<<<std::max(blocks, 1), 256, 0, s>>>(rows, n, mx, dev_cost, ld,
+                                                    dev_virtual, dvc);
+    e = cudaMemcpyAsync(host_vcost, dvc, 8, cudaMemcpyDeviceToHost, s);
+  }
+  if (!e) e = cudaStreamSynchronize(s);
+  cudaFreeAsync(misc, s);
+  if (!e) e = cudaGetLastError();
+  return e;
+}
+
+cudaError_t build_cost_sssp(const uint8_t* dev_occ, int nx, int ny, int nz,
+                            const double* w, const int64_t* host_vox, int n,
+                            double* dev_cost, int64_t ld, uint8_t* dev_virtual,
+                            double* host_vcost, int* bad_viewpoint,
+                            cudaStream_t s) {
+  double* rows = nullptr;
+  cudaError_t e = cudaMallocAsync(&rows, 8 * (size_t)n * n, s);
+  if (e) return e;
+  e = sssp_rows(dev_occ, nx, ny, nz, w, host_vox, n, 0, n, rows,
+                bad_viewpoint, s);
+  if (!e && *bad_viewpoint < 0)
+    e = cost_assemble(rows, n, dev_cost, ld, dev_virtual, host_vcost, s);
+  cudaFreeAsync(rows, s);
+  if (!e) e = cudaStreamSynchronize(s);
   return e;
 }
 

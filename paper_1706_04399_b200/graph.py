@@ -115,30 +115,84 @@ class TourGraph:
         return path
 
 
-def build_cost_matrix(occupancy: np.ndarray, viewpoint_voxels, weights,
-                      device=None):
-    torch = _torch()
+def source_blocks(n: int, world: int):
+    """The sharded build's source partition: rank r runs the
+    SSSPs of sources [r*B, min(n, (r+1)*B)), B = ceil(n / world).  Every
+    source costs one full-grid SSSP, so equal counts balance the ranks."""
+    if n < 1 or world < 1:
+        raise ValueError("n and world must be positive")
+    B = -(-n // world)
+    return B, [(min(n, r * B), min(n, (r + 1) * B)) for r in range(world)]
+
+
+def gather_rows(block, n: int, group=None):
+    """All-gather the ranks' (B, n) row blocks into the (n, n) table (one
+    exchange step: NCCL over NVLink for device tensors, gloo on the host)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    full = torch.empty((world * block.shape[0], block.shape[1]),
+                       dtype=block.dtype, device=block.device)
+    dist.all_gather_into_tensor(full, block.contiguous(), group=group)
+    return full[:n]
+
+
+def _grid_args(occupancy, viewpoint_voxels, weights):
     occ = np.ascontiguousarray(np.asarray(occupancy, dtype=bool),
                                dtype=np.uint8)
     if occ.ndim != 3:
         raise ValueError("occupancy must be a 3-D grid")
     vox = np.ascontiguousarray(np.asarray(viewpoint_voxels, dtype=np.int32)
                                .reshape(-1, 3))
-    n = vox.shape[0]
     w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
+    return occ, vox, w
+
+
+def build_cost_matrix(occupancy: np.ndarray, viewpoint_voxels, weights,
+                      device=None, group=None, return_device=False):
+    """graph.py:41-78's matrix from the device SSSP.  ``group``: a
+    torch.distributed process group (one rank per GPU) to shard the sources
+    over (``source_blocks``) and all-gather the row blocks; every rank gets
+    the whole matrix, bit-identical to the single-GPU build.
+    ``return_device``: (cost (n, ld) fp64, virtual (n, n) uint8) stay on
+    the device, with the virtual cost."""
+    torch = _torch()
+    occ, vox, w = _grid_args(occupancy, viewpoint_voxels, weights)
+    n = vox.shape[0]
     dev = torch.device(device) if device is not None else torch.device(
         "cuda", torch.cuda.current_device())
+    lib = _lib.load()
     docc = torch.from_numpy(occ.ravel()).to(dev)
     ld = (n + 7) // 8 * 8
     cost = torch.zeros((n, ld), dtype=torch.float64, device=dev)
     virt = torch.zeros((n, n), dtype=torch.uint8, device=dev)
     vcost = ctypes.c_double(0.0)
     nx, ny, nz = occ.shape
-    _lib.check(_lib.load().dpso_build_cost(
-        docc.data_ptr(), nx, ny, nz, w.ctypes.data_as(ctypes.c_void_p),
-        vox.ctypes.data_as(ctypes.c_void_p), n, cost.data_ptr(), ld,
-        virt.data_ptr(), ctypes.byref(vcost),
-        torch.cuda.current_stream(dev).cuda_stream))
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    grid_args = (docc.data_ptr(), nx, ny, nz,
+                 w.ctypes.data_as(ctypes.c_void_p),
+                 vox.ctypes.data_as(ctypes.c_void_p), n)
+    world = 1
+    if group is not None:
+        import torch.distributed as dist
+        world = dist.get_world_size(group)
+    if world == 1:
+        _lib.check(lib.dpso_build_cost(*grid_args, cost.data_ptr(), ld,
+                                       virt.data_ptr(), ctypes.byref(vcost),
+                                       stream))
+    else:
+        import torch.distributed as dist
+        B, blocks = source_blocks(n, world)
+        lo, hi = blocks[dist.get_rank(group)]
+        block = torch.zeros((B, n), dtype=torch.float64, device=dev)
+        _lib.check(lib.dpso_build_cost_rows(*grid_args, lo, hi,
+                                            block.data_ptr(), stream))
+        rows = gather_rows(block, n, group)
+        _lib.check(lib.dpso_build_cost_assemble(
+            rows.data_ptr(), n, cost.data_ptr(), ld, virt.data_ptr(),
+            ctypes.byref(vcost), stream))
+    if return_device:
+        return cost, virt, float(vcost.value)
     return (cost[:, :n].cpu().numpy(), virt.cpu().numpy().astype(bool),
             float(vcost.value))
 

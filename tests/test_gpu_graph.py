@@ -124,3 +124,106 @@ def test_fit_on_explicit_device_keeps_current_device(pkg):
                                 device="cuda:0", random_state=1).fit(c)
     assert torch.cuda.current_device() == before
     assert sorted(s.best_tour_[:-1]) == list(range(40))
+
+
+def _sharded_build(pkg, occ, vox, w, world):
+    """The sharded build's device steps on one GPU: every rank's
+    dpso_build_cost_rows block, concatenated (what gather_rows returns),
+    then dpso_build_cost_assemble."""
+    import ctypes
+
+    import torch
+    from paper_1706_04399_b200 import _lib
+    from paper_1706_04399_b200.graph import _grid_args, source_blocks
+    o, v, wt = _grid_args(occ, vox, w)
+    n = len(v)
+    lib = _lib.load()
+    docc = torch.from_numpy(o.ravel()).cuda()
+    stream = torch.cuda.current_stream().cuda_stream
+    B, blocks = source_blocks(n, world)
+    parts = []
+    for lo, hi in blocks:
+        blk = torch.full((B, n), -1.0, dtype=torch.float64, device="cuda")
+        _lib.check(lib.dpso_build_cost_rows(
+            docc.data_ptr(), *o.shape, wt.ctypes.data_as(ctypes.c_void_p),
+            v.ctypes.data_as(ctypes.c_void_p), n, lo, hi, blk.data_ptr(),
+            stream))
+        parts.append(blk)
+    rows = torch.cat(parts)[:n].contiguous()
+    ld = (n + 7) // 8 * 8
+    cost = torch.zeros((n, ld), dtype=torch.float64, device="cuda")
+    virt = torch.zeros((n, n), dtype=torch.uint8, device="cuda")
+    vc = ctypes.c_double()
+    _lib.check(lib.dpso_build_cost_assemble(
+        rows.data_ptr(), n, cost.data_ptr(), ld, virt.data_ptr(),
+        ctypes.byref(vc), stream))
+    return (cost[:, :n].cpu().numpy(), virt.cpu().numpy().astype(bool),
+            vc.value, rows.cpu().numpy())
+
+
+@pytest.mark.parametrize("name", ["wall", "ablation", "sealed"])
+def test_sharded_build_bit_exact(pkg, gg, name):
+    # SURVEY §8(e): sources sharded, row blocks gathered, then assembled:
+    # the reference's matrix for every shard count
+    occ, vox, w = unpack(gg, name), gg[f"{name}__vox"], gg[f"{name}__weights"]
+    for world in (2, 3, 8):
+        cost, virt, vcost, rows = _sharded_build(pkg, occ, vox, w, world)
+        assert np.array_equal(cost, gg[f"{name}__cost"]), world
+        assert np.array_equal(virt, gg[f"{name}__virtual"]), world
+        assert vcost == gg[f"{name}__vcost"][0]
+        want = G.distance_rows(occ, vox, tuple(w), 0, len(vox))
+        assert np.array_equal(rows, want)
+
+
+def test_sharded_build_scene_scale(pkg):
+    # the office scene (816 viewpoints): 8 shards == the one-call build
+    import sys
+    from conftest import ROOT
+    sys.path.insert(0, f"{ROOT}/tools")
+    import scenes
+    occ, vox, w = scenes.scene("office")
+    one = pkg.build_cost_matrix(occ, vox, w)
+    cost, virt, vcost, _ = _sharded_build(pkg, occ, vox, w, 8)
+    assert np.array_equal(cost, one[0])
+    assert np.array_equal(virt, one[1])
+    assert vcost == one[2]
+
+
+def test_build_rows_errors(pkg, gg):
+    import ctypes
+
+    import torch
+    from paper_1706_04399_b200 import _lib
+    from paper_1706_04399_b200.graph import _grid_args
+    occ, vox, w = _grid_args(unpack(gg, "wall"), gg["wall__vox"],
+                             gg["wall__weights"])
+    n = len(vox)
+    lib = _lib.load()
+    docc = torch.from_numpy(occ.ravel()).cuda()
+    blk = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+    args = (docc.data_ptr(), *occ.shape, w.ctypes.data_as(ctypes.c_void_p),
+            vox.ctypes.data_as(ctypes.c_void_p), n)
+    for lo, hi in ((-1, 2), (3, 2), (0, n + 1)):
+        with pytest.raises(ValueError, match="source range"):
+            _lib.check(lib.dpso_build_cost_rows(*args, lo, hi,
+                                                blk.data_ptr(), None))
+    # an occupied viewpoint fails on every shard, even one not owning it
+    bad = vox.copy()
+    bad[-1] = np.argwhere(occ)[0]
+    with pytest.raises(ValueError, match="occupied"):
+        _lib.check(lib.dpso_build_cost_rows(
+            *args[:5], bad.ctypes.data_as(ctypes.c_void_p), n, 0, 1,
+            blk.data_ptr(), None))
+
+
+def test_build_cost_matrix_return_device(pkg, gg):
+    occ, vox, w = unpack(gg, "wall"), gg["wall__vox"], gg["wall__weights"]
+    cost, virt, vcost = pkg.build_cost_matrix(occ, vox, w,
+                                              return_device=True)
+    n = len(vox)
+    assert cost.is_cuda and virt.is_cuda
+    assert np.array_equal(cost[:, :n].cpu().numpy(), gg["wall__cost"])
+    # the device matrix feeds fit() without a host round trip
+    res = pkg.DiscreteSwarmSolver(n_particles=8, max_generations=5,
+                                  random_state=1).fit(cost)
+    assert sorted(res.best_tour_[:-1]) == list(range(n))
