@@ -98,6 +98,10 @@ int dpso_scan_rows_bytes(dpso_ctx* ctx);
  * column scan's knobs, selects 0 (testing). */
 int dpso_scan_band(dpso_ctx* ctx);
 
+/* How the band scan stages its rows: 2 = TMA gather4 (four rows per copy,
+ * n <= ~960), 1 = one bulk copy per row, 0 = no band scan.  Diagnostic. */
+int dpso_band_staging(dpso_ctx* ctx);
+
 /* How the last dpso_init located each particle's draws in the shared numpy
  * init stream: 1 = parallel walk (every start's walk length, then pointer
  * doubling), 0 = serial scan (too large a span, a walk ran off the span, or

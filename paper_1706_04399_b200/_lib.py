@@ -52,6 +52,7 @@ _SIG = {
     "dpso_init_path": (_I32, [_P]),
     "dpso_scan_rows_bytes": (_I32, [_P]),
     "dpso_scan_band": (_I32, [_P]),
+    "dpso_band_staging": (_I32, [_P]),
     "dpso_step_timed": (_I32, [_P, _I32, _P, _P]),
     "dpso_ctl": (_I32, [_P, _P, _P]),
     "dpso_result": (_I32, [_P, _P, _P, _P, ctypes.POINTER(_I32)]),

@@ -632,6 +632,12 @@ int dpso_scan_mode(dpso_ctx* c) { return c ? c->v.plan.mode : -1; }
 
 int dpso_scan_band(dpso_ctx* c) { return c ? c->v.plan.band_mode : -1; }
 
+int dpso_band_staging(dpso_ctx* c) {
+  if (!c) return -1;
+  if (!c->v.plan.band_mode) return 0;
+  return c->v.plan.band_g4 ? 2 : 1;
+}
+
 int dpso_init_path(dpso_ctx* c) { return c ? c->init_path : -1; }
 
 int dpso_scan_rows_bytes(dpso_ctx* c) {

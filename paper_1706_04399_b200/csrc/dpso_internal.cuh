@@ -98,6 +98,10 @@ struct TwoOptPlan {
   double band_vfrom, band_vto;
   int32_t* band_cols;      // scratch: band_cols_cap x 2 x band_cw(n) ints
   int64_t band_cols_cap;
+  // TMA gather4 row staging (n <= ~960): the CUtensorMap of the row
+  // versions (a 2-D tensor of 4n lines), 0 = one bulk copy per row
+  int band_g4;
+  unsigned char band_tm[128];
 };
 
 struct TwoOptRes {

@@ -57,6 +57,9 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 
 #include "dpso_internal.cuh"
@@ -99,6 +102,7 @@ struct BandArgs {
   int ncb;              // column buffers / result slots (particles)
   int groups;           // warp groups scanning alternate bands (1 or 2)
   int probe;            // debug: 1 = stream the bands, skip the pairs
+  int g4;               // rows staged by TMA gather4 (4 rows per copy)
 };
 
 __device__ __forceinline__ int lds_s16(uint32_t addr) {
@@ -337,7 +341,7 @@ constexpr int kMaxNcb = 8;
 
 template <int MODE>
 __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
-    k_two_opt_band(BandArgs a) {
+    k_two_opt_band(BandArgs a, const __grid_constant__ CUtensorMap tm) {
   if (a.ctl && (a.ctl->done || a.ctl->improved)) return;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
@@ -390,19 +394,48 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
       const int r0 = rpp * pw;
       const int nr = max(0, min(rpp, n - i0 - r0));
       const bool withcols = band == 0 && pw == 0;
-      if (lane == 0) {
-        mbar_expect_tx(&full[s], (uint32_t)nr * (uint32_t)a.line);
-        if (withcols) mbar_expect_tx(&colfull[cb], colbytes);
-      }
-      __syncwarp();
-      if (lane < nr) {
-        fence_proxy_async();  // the consumers' reads of the stage first
-        const int l = r0 + lane;
-        const int city = a.tours[(size_t)pp * a.np + i0 + l];
-        const unsigned char* src =
-            a.rows + ((size_t)(l & 3) * n + city) * (size_t)a.line;
-        bulk_g2s(rowbuf + (size_t)s * stage_bytes + (size_t)l * S + 16 * (l >> 2),
-                 src, (uint32_t)a.line, &full[s]);
+      unsigned char* stg = rowbuf + (size_t)s * stage_bytes;
+      if (a.g4) {
+        // groups of 4 slots: group g = pw + kProdWarps k (k < 8 / kProdWarps)
+        // to stg + 4 g S (128-byte aligned), slot 4g + q from version q with
+        // the box starting 16 g bytes before the line: slot l's element c
+        // lands at l (S + 4) + 2c, the bulk-copy layout
+        constexpr int gpp = 8 / kProdWarps;
+        const int rows_left = n - i0;
+        int mine = 0;
+#pragma unroll
+        for (int k = 0; k < gpp; ++k) mine += 4 * (pw + kProdWarps * k) < rows_left;
+        if (lane == 0) {
+          mbar_expect_tx(&full[s], (uint32_t)mine * 4u * S);
+          if (withcols) mbar_expect_tx(&colfull[cb], colbytes);
+        }
+        __syncwarp();
+        const int g = pw + kProdWarps * lane;
+        if (lane < gpp && 4 * g < rows_left) {
+          fence_proxy_async();  // the consumers' reads of the stage first
+          const uint16_t* tr = a.tours + (size_t)pp * a.np + i0 + 4 * g;
+          int rw[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            rw[q] = q * n + (4 * g + q < rows_left ? (int)tr[q] : 0);
+          tma_gather4(stg + (size_t)4 * g * S, &tm, -2 * g, rw[0], rw[1],
+                      rw[2], rw[3], &full[s]);
+        }
+      } else {
+        if (lane == 0) {
+          mbar_expect_tx(&full[s], (uint32_t)nr * (uint32_t)a.line);
+          if (withcols) mbar_expect_tx(&colfull[cb], colbytes);
+        }
+        __syncwarp();
+        if (lane < nr) {
+          fence_proxy_async();  // the consumers' reads of the stage first
+          const int l = r0 + lane;
+          const int city = a.tours[(size_t)pp * a.np + i0 + l];
+          const unsigned char* src =
+              a.rows + ((size_t)(l & 3) * n + city) * (size_t)a.line;
+          bulk_g2s(stg + (size_t)l * S + 16 * (l >> 2), src,
+                   (uint32_t)a.line, &full[s]);
+        }
       }
       if (withcols && lane == 0)
         bulk_g2s(cols + cb * 2 * a.cw, a.cols + (size_t)pp * 2 * a.cw,
@@ -621,8 +654,18 @@ __global__ void k_cost_band16(const double* cost, int64_t ld, int n,
 }
 
 // slot l of a stage starts at l S + 16 (l div 4): S >= line keeps slots
-// apart (the stagger never decreases); a stage spans 32 S + 128 bytes
-uint32_t band_slot(int line) { return (uint32_t)round_up(line, 128); }
+// apart (the stagger never decreases); a stage spans 32 S + 128 bytes.
+// gather4 staging: a slot is one box of S bytes, the line shifted by up to
+// 112 bytes (16 g for group g), S a multiple of 32 (4 S: group starts
+// 128-byte aligned), at most 256 8-byte columns per box.
+uint32_t band_slot(int line, bool g4) {
+  return g4 ? (uint32_t)round_up(line + 112, 32) : (uint32_t)round_up(line, 128);
+}
+constexpr int kG4MaxBox = 2048;
+bool band_g4_fits(int n) {
+  return (int)band_slot((int)round_up(2 * (int64_t)n + 12, 16), true) <=
+         kG4MaxBox;
+}
 
 int band_nb(int n) { return (n + kBandRows - 2) / kBandRows; }
 
@@ -645,9 +688,9 @@ int band_groups(int n, int nst) {
   return nst == 4 && band_nb(n) >= 2 ? 2 : 1;
 }
 
-size_t band_smem(int n, int nst) {
+size_t band_smem(int n, int nst, bool g4) {
   const int line = band_line(n);
-  return (size_t)nst * (32 * band_slot(line) + 128) +
+  return (size_t)nst * (32 * band_slot(line, g4) + 128) +
          (size_t)band_ncb(n, nst) * 2 * band_cw(n) * 4 +
          (size_t)kBandWarps * kLaneState * 32 * 4;
 }
@@ -655,14 +698,48 @@ size_t band_smem(int n, int nst) {
 constexpr size_t kBandSmemMax = 225 * 1024;
 
 // stages: as many as fit, up to kMaxStages
-int band_stages(int n) {
+int band_stages(int n, bool g4) {
   int nst = kMaxStages;
-  while (nst > 2 && band_smem(n, nst) > kBandSmemMax) --nst;
+  while (nst > 2 && band_smem(n, nst, g4) > kBandSmemMax) --nst;
   if (const char* e = getenv("DPSO_BAND_STAGES")) {
     const int x = atoi(e);
-    if (x >= 2 && x <= kMaxStages && band_smem(n, x) <= kBandSmemMax) nst = x;
+    if (x >= 2 && x <= kMaxStages && band_smem(n, x, g4) <= kBandSmemMax)
+      nst = x;
   }
   return nst;
+}
+
+// The tensor map of the row versions for gather4: a 2-D tensor of 4n lines
+// (line bytes each) of 8-byte columns, one box = S / 8 columns x 1 line.
+// False when the driver entry point is missing or the encode fails (the
+// bulk-copy staging is used then).
+bool band_encode_g4(const unsigned char* rows, int n, int line,
+                    unsigned char* out) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  static bool looked = false;
+  if (!looked) {
+    looked = true;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode,
+                                cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      encode = nullptr;
+    cudaGetLastError();
+  }
+  if (!encode) return false;
+  alignas(64) CUtensorMap tm;
+  cuuint64_t gdim[2] = {(cuuint64_t)(line / 8), (cuuint64_t)(4 * (int64_t)n)};
+  cuuint64_t gstride[1] = {(cuuint64_t)line};
+  cuuint32_t box[2] = {band_slot(line, true) / 8, 1};
+  cuuint32_t estr[2] = {1, 1};
+  if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_INT64, 2, (void*)rows, gdim,
+             gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
+  memcpy(out, &tm, sizeof tm);
+  return true;
 }
 
 }  // namespace
@@ -672,7 +749,8 @@ int band_line(int n) { return (int)round_up(2 * (int64_t)n + 12, 16); }
 int band_cw(int n) { return (int)round_up(n + 16, 8); }
 
 int64_t band_rows_bytes(int n) {
-  if (n < 4 || n > kBandMaxN || band_smem(n, 2) > kBandSmemMax) return 0;
+  if (n < 4 || n > kBandMaxN || band_smem(n, 2, false) > kBandSmemMax)
+    return 0;
   return 4 * (int64_t)n * band_line(n);
 }
 
@@ -686,6 +764,7 @@ cudaError_t band_prepare(const double* cost, int64_t ld, int32_t n,
                          TwoOptPlan* pl) {
   pl->band = nullptr;
   pl->band_mode = 0;
+  pl->band_g4 = 0;
   if (!buf || band_rows_bytes(n) == 0) return cudaSuccess;
   if (const char* e = getenv("DPSO_SCAN_BAND"))
     if (atoi(e) == 0) return cudaSuccess;
@@ -721,6 +800,9 @@ cudaError_t band_prepare(const double* cost, int64_t ld, int32_t n,
   pl->band_win = mode == 2 ? 4 : 0;
   pl->band_vfrom = vfrom;
   pl->band_vto = vto;
+  bool g4 = band_g4_fits(n);
+  if (const char* e = getenv("DPSO_BAND_G4")) g4 = g4 && atoi(e) != 0;
+  pl->band_g4 = g4 && band_encode_g4(buf, n, line, pl->band_tm) ? 1 : 0;
   return cudaSuccess;
 }
 
@@ -736,7 +818,8 @@ cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
   a.ld = pl.ld;
   a.rows = pl.band;
   a.line = pl.band_line;
-  a.slot = band_slot(pl.band_line);
+  a.g4 = pl.band_g4;
+  a.slot = band_slot(pl.band_line, a.g4 != 0);
   a.n = n;
   a.np = np;
   a.count = count;
@@ -757,11 +840,13 @@ cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
                                      ctl);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
-  a.nst = band_stages(n);
+  a.nst = band_stages(n, a.g4 != 0);
   a.ncb = band_ncb(n, a.nst);
   a.groups = band_groups(n, a.nst);
   if (const char* e = getenv("DPSO_BAND_PROBE")) a.probe = atoi(e);
-  const size_t smem = band_smem(n, a.nst);
+  const size_t smem = band_smem(n, a.nst, a.g4 != 0);
+  alignas(64) CUtensorMap tm;
+  memcpy(&tm, pl.band_tm, sizeof tm);  // unused (zero) without gather4
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -769,11 +854,13 @@ cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
   if (pl.band_mode == 1) {
     e = set_dyn_smem((const void*)k_two_opt_band<1>, smem);
     if (e) return e;
-    k_two_opt_band<1><<<blocks, (kBandWarps + kProdWarps) * 32, smem, s>>>(a);
+    k_two_opt_band<1>
+        <<<blocks, (kBandWarps + kProdWarps) * 32, smem, s>>>(a, tm);
   } else {
     e = set_dyn_smem((const void*)k_two_opt_band<2>, smem);
     if (e) return e;
-    k_two_opt_band<2><<<blocks, (kBandWarps + kProdWarps) * 32, smem, s>>>(a);
+    k_two_opt_band<2>
+        <<<blocks, (kBandWarps + kProdWarps) * 32, smem, s>>>(a, tm);
   }
   return cudaGetLastError();
 }

@@ -39,6 +39,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src,
       : "memory");
 }
 
+// TMA gather4 (sm_100): four rows (r0..r3) of a 2-D tensor, columns
+// [x, x + box) each (out-of-bounds columns read as zero), to dst, dst + box
+// bytes, ... (dst 128-byte aligned)
+__device__ __forceinline__ void tma_gather4(void* dst, const void* tmap, int x,
+                                            int r0, int r1, int r2, int r3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4."
+      "mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::
+          "r"(smem_u32(dst)),
+      "l"(tmap), "r"(x), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
                : "memory");

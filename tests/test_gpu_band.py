@@ -21,10 +21,12 @@ def pkg():
     return pkg
 
 
-def band_kind(pkg, cost):
+def band_kind(pkg, cost, staging=False):
     s = pkg.DiscreteSwarmSolver(n_particles=4)
     ctx = s._make_context(cost)
     try:
+        if staging:
+            return int(ctx.lib.dpso_band_staging(ctx.h))
         return int(ctx.lib.dpso_scan_band(ctx.h))
     finally:
         ctx.close()
@@ -63,11 +65,17 @@ def test_band_selected(pkg, monkeypatch):
     assert band_kind(pkg, grid(100)) == 0
 
 
+@pytest.mark.parametrize("staging", ["gather4", "bulk"])
 @pytest.mark.parametrize("mode", ["exact", "filter"])
-def test_band_boundaries(pkg, mode, monkeypatch):
-    # band edges (31 pair rows), 8-column groups, warp column splits
+def test_band_boundaries(pkg, mode, staging, monkeypatch):
+    # band edges (31 pair rows), 8-column groups, warp column splits; rows
+    # staged by TMA gather4 (n <= ~960, the default) or one bulk copy each
     if mode == "filter":
         monkeypatch.setenv("DPSO_BAND_MODE", "2")
+    if staging == "bulk":
+        monkeypatch.setenv("DPSO_BAND_G4", "0")
+    assert band_kind(pkg, grid(100), staging=True) == (
+        2 if staging == "gather4" else 1)
     rng = np.random.default_rng(31)
     for n in list(range(4, 70)) + [93, 94, 95, 124, 125, 155, 156, 257, 511]:
         cost = np.floor(random_euclidean_matrix(n, rng) * 100.0)
@@ -147,6 +155,17 @@ def test_band_more_particles_than_ctas(pkg):
         cost = np.floor(random_euclidean_matrix(n, rng) * 100.0)
         check(pkg, cost, perms(rng, P, n), ("multi", n, P), 64, rng)
         check(pkg, cost / 7.0, perms(rng, P, n), ("multi-f", n, P), 64, rng)
+
+
+def test_band_gather4_limit(pkg):
+    # the largest n whose shifted lines fit one gather4 box (2048 bytes:
+    # 2n + 124 <= 2048) and the first n past it (bulk copies); partial last
+    # groups of 4 rows
+    rng = np.random.default_rng(47)
+    for n in (957, 958, 962, 963, 964, 965):
+        cost = np.floor(random_euclidean_matrix(n, rng) * 100.0)
+        assert band_kind(pkg, cost, staging=True) == (2 if n <= 962 else 1)
+        check(pkg, cost, perms(rng, 40, n), ("g4-limit", n), 8, rng)
 
 
 def test_band_many_particles_per_cta(pkg):

@@ -24,6 +24,7 @@ SHAPES = {
     "c4": (2000, 65536, "euclid"),
     "c4s": (2000, 4096, "euclid"),
     "n900": (900, 1024, "euclid"),
+    "n800": (816, 1024, "euclid_int"),
 }
 
 
@@ -90,6 +91,11 @@ def main():
             if st:
                 variants.append(("band_stages" + st,
                                  {"DPSO_BAND_STAGES": st}))
+        # AB_VARIANTS="tag:K=V,K=V;tag2:K=V": extra environment variants
+        for spec in filter(None, os.environ.get("AB_VARIANTS", "").split(";")):
+            tag, _, kvs = spec.partition(":")
+            variants.append((tag, dict(kv.split("=", 1)
+                                       for kv in kvs.split(",") if kv)))
         if os.environ.get("AB_PROBE"):
             variants.append(("band_stream_only", {"DPSO_BAND_PROBE": "1"}))
         for tag, env in variants:
