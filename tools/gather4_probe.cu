@@ -4,7 +4,9 @@
 //   gather4  one cp.async.bulk.tensor.2d.tile::gather4 per 4 rows (sm_100:
 //            a 2-D tensor map, one column start and four row indices)
 // at 1-KB and 2-KB rows, 1/2/4/8 issuing warps.  The question is whether a
-// gather4 costs the TMA unit one row's issue time or four.
+// gather4 costs the TMA unit one row's issue time or four (answer,
+// profiles/r02/gather4_probe.json: about 2.5 rows' time: 1-KB rows 7.8 TB/s
+// bulk vs 12.3 TB/s gather4, 2-KB rows 14.4 vs 20.2 TB/s).
 //
 // Output: one JSON object on stdout (tools/gather4_probe.py builds + runs).
 #include <cuda.h>
@@ -238,8 +240,10 @@ int main() {
     CK(cudaFuncSetAttribute(k_check,
                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                             check_smem));
-    for (int dst_off : {0, 16, 48, 112}) {
-      // 16-byte-aligned destinations: the band scan's slot rotation
+    // destinations must be 128-byte aligned: a 16-byte-aligned one faults
+    // with "misaligned address" (measured; the fault is sticky, so only
+    // aligned offsets are checked here)
+    for (int dst_off : {0, 128}) {
       CK(cudaMemset(bad, 0, 4));
       k_check<<<1, 128, check_smem>>>(tm, mat,
                                       row_bytes < pitch ? row_bytes : pitch,
