@@ -101,7 +101,9 @@ struct BandArgs {
   int nst;              // stages in the row ring
   int ncb;              // column buffers / result slots (particles)
   int groups;           // warp groups scanning alternate bands (1 or 2)
-  int probe;            // debug: 1 = stream the bands, skip the pairs
+  int probe;            // debug: 1 = stream the bands, skip the pairs;
+                        // 2 = scan, but copy rows only into the first nst
+                        // bands (later bands reuse them: consumer floor)
   int g4;               // rows staged by TMA gather4 (4 rows per copy)
 };
 
@@ -394,6 +396,26 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
       const int r0 = rpp * pw;
       const int nr = max(0, min(rpp, n - i0 - r0));
       const bool withcols = band == 0 && pw == 0;
+      if (a.probe == 2 && t >= nst) {  // consumer floor: no row copies
+        if (lane == 0) {
+          mbar_expect_tx(&full[s], 0);
+          if (withcols) mbar_expect_tx(&colfull[cb], colbytes);
+        }
+        __syncwarp();
+        if (withcols && lane == 0)
+          bulk_g2s(cols + cb * 2 * a.cw, a.cols + (size_t)pp * 2 * a.cw,
+                   colbytes, &colfull[cb]);
+        if (++s == nst) {
+          s = 0;
+          ++use;
+        }
+        if (++band == nb) {
+          band = 0;
+          ++pl;
+          if (++cb == ncb) cb = 0;
+        }
+        continue;
+      }
       unsigned char* stg = rowbuf + (size_t)s * stage_bytes;
       if (a.g4) {
         // groups of 4 slots: group g = pw + kProdWarps k (k < 8 / kProdWarps)
@@ -488,19 +510,22 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
     }
   };
   for (int k = 0; k < grp; ++k) step();
+  // shared-memory addresses computed once (not per band)
+  const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty);
+  const uint32_t colfull_a = smem_u32(colfull);
+  const uint32_t R0 = smem_u32(rowbuf) + (uint32_t)lane * (S + 4u);
   for (int t = grp; t < total; t += G) {
     const int pp = (int)blockIdx.x + pl * (int)gridDim.x;
     const int i0 = band * kBandRows;
     // the particle's column arrays (its first band for this warp), rows
-    if (band < G) mbar_wait_sleep(&colfull[cb], (uint32_t)(cuse & 1));
-    mbar_wait_sleep(&full[s], (uint32_t)(use & 1));
+    if (band < G) mbar_wait_sleep_u32(colfull_a + 8u * cb, (uint32_t)(cuse & 1));
+    mbar_wait_sleep_u32(full_a + 8u * s, (uint32_t)(use & 1));
     const int* O = cols + cb * 2 * a.cw;
     const int* D = O + a.cw;
     const int i = i0 + lane;
     const bool live = lane < kBandRows && i <= n - 2;
     const int Di = live ? D[i] : 0;
-    const uint32_t R =
-        smem_u32(rowbuf + (size_t)s * stage_bytes) + (uint32_t)lane * (S + 4u);
+    const uint32_t R = R0 + (uint32_t)s * stage_bytes;
     int L = lane_limit<MODE>(live, Di, i, ws[0], ws[1]);
     {  // capped by the CTA-wide minimum (other warps' finds)
       const int cm = *(volatile int*)&s_cmin[cb];
@@ -509,7 +534,7 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
     const int cs = (i0 + 2) & ~7;
     const int per = ((((n - cs) + NWg - 1) >> lgw) + 7) & ~7;
     const int cA = cs + wl * per, cB = min(n, cA + per);
-    if (cA < cB && !a.probe) {
+    if (cA < cB && a.probe != 1) {
       int prev = lds_s16(R + (uint32_t)O[3 + cA]);
       int c0 = cA;
       for (; c0 < cB && c0 < i0 + 32; c0 += 8)
@@ -520,7 +545,7 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
                                 ws, &s_cmin[cb], S + 4u);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);  // the stage's reads are done
+    if (lane == 0) mbar_arrive_u32(empty_a + 8u * s);  // stage reads done
     // this warp's last band of the particle: the next band of its group is
     // in a later particle (nb >= G, so every group has a band in each)
     if (band + G >= nb || t + G >= total) {

@@ -88,6 +88,26 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar,
       : "memory");
 }
 
+// the same on a precomputed shared-memory address (hot loops: the
+// generic -> shared conversion is not redone per wait)
+__device__ __forceinline__ void mbar_wait_sleep_u32(uint32_t addr,
+                                                    uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t addr) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr)
+               : "memory");
+}
+
 // producer-side wait: poll with a short sleep between tries (a producer is
 // usually far ahead of its consumers; its polls would take their slots)
 __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar,

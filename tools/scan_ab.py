@@ -98,6 +98,7 @@ def main():
                                        for kv in kvs.split(",") if kv)))
         if os.environ.get("AB_PROBE"):
             variants.append(("band_stream_only", {"DPSO_BAND_PROBE": "1"}))
+            variants.append(("band_consume_only", {"DPSO_BAND_PROBE": "2"}))
         for tag, env in variants:
             band, ms = time_scan(n, P, cost, gens, env)
             rec[tag] = {"scan_kind": band, "scan_apply_ms": ms}
