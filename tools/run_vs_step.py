@@ -32,16 +32,32 @@ def make(seed, G):
 def main():
     G = 500
     for seed in (7, 1000):
-        for mode in ("run", "step500", "step1"):
+        for mode in ("run", "step500", "step1", "bench_loop"):
             ctx = make(seed, G)
             t0 = time.perf_counter()
             if mode == "run":
                 ctx.run()
             elif mode == "step500":
                 ctx.step(G)
-            else:
+            elif mode == "step1":
                 for _ in range(G):
                     ctx.step(1)
+            else:
+                # bench.py's timed loop: an L2 flush (untimed) between
+                # CUDA-event-timed single steps
+                flush = torch.empty(256 << 20, dtype=torch.uint8,
+                                    device="cuda")
+                ev = [(torch.cuda.Event(enable_timing=True),
+                       torch.cuda.Event(enable_timing=True))
+                      for _ in range(G)]
+                for k in range(G):
+                    flush.fill_(k & 0xFF)
+                    ev[k][0].record()
+                    ctx.step(1)
+                    ev[k][1].record()
+                torch.cuda.synchronize()
+                tot = sum(a.elapsed_time(b) for a, b in ev)
+                print(seed, "bench_loop events", f"{tot / G:.4f} ms/gen")
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
             c = ctx.ctl()
