@@ -374,6 +374,31 @@ def load_gather_peaks():
         return {}
 
 
+def load_gather4_peaks():
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02",
+                               "gather4_probe.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+def gather4_stream_peak(peaks, line):
+    """Measured L2 -> shared-memory row stream with TMA gather4 (four rows
+    per copy), 32 rows per stage, 4 issuing warps (tools/gather4_probe.cu,
+    profiles/r02/gather4_probe.json), scaled like row_stream_peak."""
+    meas = {}
+    for k, v in peaks.items():
+        if k.startswith("gather4_") and k.endswith("B_w4"):
+            size = int(k[len("gather4_"):].split("B")[0])
+            meas[size] = float(v["tbs"]) * 1e3
+    if not meas:
+        return None, None
+    near = min(meas, key=lambda z: abs(math.log(z / line)))
+    cap = max(meas.values())
+    return min(cap, meas[near] * line / near), near
+
+
 def row_stream_peak(peaks, line):
     """Measured L2 -> shared-memory bulk-copy bandwidth (GB/s) for rows of
     `line` bytes, 32 rows per stage, 4 issuing warps (tools/gather_peaks.cu,
@@ -425,6 +450,7 @@ def run_ours(args, cfg_name, cfg):
     seed_body, n_seed = solver._seed(n)
     ctx = solver._make_context(cost)
     band = int(ctx.lib.dpso_scan_band(ctx.h))
+    staging = int(ctx.lib.dpso_band_staging(ctx.h))
     if RNG == "numpy":
         ctx.set_streams(numpy_stream_states(params["random_state"], P + 2))
     ctx.init(seed_body, n_seed)
@@ -553,7 +579,20 @@ def run_ours(args, cfg_name, cfg):
             line_b = int(math.ceil(2 * n / 16.0) * 16)
             staged = float(P) * (n + 1) * line_b * max(1, -(-n // 1024))
         achieved = staged / (dur_ms / 1e3) / 1e9
-        peak, near = row_stream_peak(gpk, line_b)
+        if staging == 2:
+            peak, near = gather4_stream_peak(load_gather4_peaks(), line_b)
+            peak_desc = (f"measured: L2->shared TMA gather4 row stream, "
+                         f"{near}-B rows, 32 per stage, 4 issuing warps "
+                         f"(profiles/r02/gather4_probe.json, "
+                         f"tools/gather4_probe.cu), scaled to {line_b}-B "
+                         f"rows")
+        else:
+            peak, near = row_stream_peak(gpk, line_b)
+            peak_desc = (f"measured: L2->shared bulk-copy row stream, "
+                         f"{near}-B rows, 32 per stage, 4 issuing "
+                         f"warps (profiles/r02/gather_peaks.json, "
+                         f"tools/gather_peaks.cu), scaled to "
+                         f"{line_b}-B rows")
         roof = {"bound": "l2", "kernel": dom,
                 "scan": ("band-exact", "band-filter")[band - 1]
                 if band else "column",
@@ -564,11 +603,9 @@ def run_ours(args, cfg_name, cfg):
                 "algorithmic_fp64_bytes_per_launch": scan_alg,
                 "algorithmic_fp64_gbs": scan_alg / (dur_ms / 1e3) / 1e9,
                 "avg_launch_ms": dur_ms,
-                "peak_source": (f"measured: L2->shared bulk-copy row stream, "
-                                f"{near}-B rows, 32 per stage, 4 issuing "
-                                f"warps (profiles/r02/gather_peaks.json, "
-                                f"tools/gather_peaks.cu), scaled to "
-                                f"{line_b}-B rows"),
+                "staging": {0: "column scan", 1: "bulk copies",
+                            2: "TMA gather4"}.get(staging),
+                "peak_source": peak_desc,
                 "l2_random_gather_f64_gbs":
                     gpk.get("gather_f64_8MB", {}).get("useful_gbs"),
                 "note": "the matrix is L2-resident and each staged row "
