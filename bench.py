@@ -195,7 +195,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ cpu baseline
-def cpu_sample(cost, cfg, P_cpu=32, budget_s=12.0, max_gens=12, warm=1,
+def cpu_sample(cost, cfg, P_cpu=32, budget_s=10.0, max_gens=400, warm=1,
                seed=0, seed_tour=None):
     """Oracle port of the reference (single thread) on a bounded sample:
     P_cpu particles of the same matrix; returns (rate, gens, seconds)."""
