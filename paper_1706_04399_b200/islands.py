@@ -141,10 +141,20 @@ class IslandSolver:
         return DiscreteSwarmSolver(**p)
 
     @staticmethod
-    def _start(solver, cost):
-        from .solver import numpy_stream_states
-        seed_body, n_seed = solver._seed(cost.shape[0])
-        ctx = solver._make_context(cost)
+    def _start(solver, cost, dev_cost=None, device=None):
+        from .solver import SwarmContext, numpy_stream_states
+        if dev_cost is not None:
+            # a device matrix: used in place on its own GPU, copied once to
+            # an island on another one
+            t, ld = dev_cost
+            if t.device != device:
+                t = t.to(device)
+            n = t.shape[0]
+            seed_body, n_seed = solver._seed(n)
+            ctx = SwarmContext(solver._params(), n, t, ld)
+        else:
+            seed_body, n_seed = solver._seed(cost.shape[0])
+            ctx = solver._make_context(cost)
         if solver.rng == "numpy":
             ctx.set_streams(numpy_stream_states(solver.random_state,
                                                 solver.n_particles + 2))
@@ -158,8 +168,11 @@ class IslandSolver:
         from .solver import DiscreteSwarmSolver, SolveReport
         probe = DiscreteSwarmSolver(**self.params)
         probe._check_params()
-        cost = probe._check_cost(X)
-        n = cost.shape[0]
+        # a CUDA tensor (e.g. build_cost_matrix(..., return_device=True))
+        # stays on the device, as DiscreteSwarmSolver.fit takes it
+        dev_cost = probe._device_cost(X)
+        cost = None if dev_cost is not None else probe._check_cost(X)
+        n = dev_cost[0].shape[0] if dev_cost is not None else cost.shape[0]
         t0 = time.perf_counter()
         G = int(probe.max_generations)
         distributed = self.devices is None and dist.is_available() and \
@@ -186,14 +199,15 @@ class IslandSolver:
                 base = int(np.random.SeedSequence().entropy % (1 << 62))
             islands = [(k, torch.device(d)) for k, d in enumerate(devs)]
         if n == 1:
-            probe.fit(cost)
+            probe.fit(X if cost is None else cost)
             self._copy(probe, world, 0)
             return self
         ctxs = []
         try:
             for k, dev in islands:
                 with torch.cuda.device(dev):
-                    ctxs.append(self._start(self._solver(k, dev, base), cost))
+                    ctxs.append(self._start(self._solver(k, dev, base), cost,
+                                            dev_cost, dev))
             ex = None
             if distributed:
                 ex = IslandExchange(ctxs[0], n, group=self.group)

@@ -84,3 +84,20 @@ def test_island_solver_single_island_is_a_swarm():
     assert s.best_tour_ == ref.best_tour_
     assert s.best_fitness_ == ref.best_fitness_
     assert s.convergence_ == ref.convergence_
+
+
+def test_island_solver_device_matrix():
+    # a CUDA-tensor matrix (build_cost_matrix(..., return_device=True) or
+    # load_cost_matrix_device) is used in place: same run as the host one
+    import torch
+    from paper_1706_04399_b200 import IslandSolver
+    cost = _cost()
+    host = IslandSolver(exchange_every=5, devices=["cuda:0", "cuda:0"],
+                        **PARAMS).fit(cost)
+    dev = torch.from_numpy(cost).cuda()
+    s = IslandSolver(exchange_every=5, devices=["cuda:0", "cuda:0"],
+                     **PARAMS).fit(dev)
+    assert s.best_tour_ == host.best_tour_
+    assert s.best_fitness_ == host.best_fitness_
+    assert s.convergence_ == host.convergence_
+    assert s.island_fitness_ == host.island_fitness_
