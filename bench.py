@@ -510,6 +510,10 @@ def run_ours(args, cfg_name, cfg):
         ep = gpu_params(cfg, P, Ge, 7)
         if seed_tour is not None:
             ep["seed_tour"] = seed_tour
+        # one short untimed fit first (module and pool warm-up, as the
+        # timed steps have theirs)
+        DiscreteSwarmSolver(**dict(ep, max_generations=max(1, W),
+                                   stall_generations=max(1, W))).fit(cost)
         if world > 1:
             from paper_1706_04399_b200 import IslandSolver
             dist.barrier()
