@@ -706,10 +706,11 @@ def run_ours(args, cfg_name, cfg):
             "sample": (f"oracle port (oracle/dpso_oracle.py) of the reference"
                        f" solve, 32-particle swarm on the same matrix, 1 warm"
                        f"-up + {g} timed generations ({dt:.1f}s), 1 thread")}
-        if "time_to_reference_best" in line:
-            ttb = line["time_to_reference_best"]
-            # the reference (single-threaded, parallel=False) needs g*
-            # generations of P particles at the port's one-core rate
+        ttb = line.get("time_to_reference_best")
+        if ttb is not None and "reference_run" not in ttb:
+            # no measured reference run for this config: the reference
+            # (single-threaded, parallel=False) needs g* generations of P
+            # particles at the port's one-core rate
             ttb["reference_cpu_estimate_s"] = ttb["generation"] * P / rate
     print(json.dumps(line), flush=True)
     if world > 1:
