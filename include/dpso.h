@@ -243,6 +243,17 @@ int dpso_build_cost_assemble(const double* dev_rows, int32_t n,
  * reference's messages: "empty cost matrix file <path>", "cost matrix
  * <path>: expected <n*n> entries, got <k>", Python's int()/float()
  * conversion messages. */
+/* Host -> device upload of a row-major fp64 matrix (rows x cols, host
+ * leading dimension host_ld, device leading dimension dev_ld >= cols; the
+ * device padding columns are not written).  Replaces the reference's
+ * in-memory hand-off of the matrix to the solver (solver.py:155-162 takes a
+ * host array): large matrices go through a ring of two pinned chunks
+ * filled by several host threads while the other chunk's DMA runs on
+ * cuda_stream; returns after the copy completed. */
+int dpso_upload_matrix(const double* host, int64_t host_ld, int32_t rows,
+                       int32_t cols, double* dev, int64_t dev_ld,
+                       void* cuda_stream);
+
 int dpso_write_matrix_text(const char* path, const double* host, int64_t ld,
                            int32_t n);
 int dpso_read_matrix_text(const char* path, double* host_out, int64_t ld,

@@ -76,6 +76,7 @@ _SIG = {
                                      _I32, _P, _P]),
     "dpso_build_cost_assemble": (_I32, [_P, _I32, _P, _I64, _P, _P, _P]),
     "dpso_philox4x32_10": (_I32, [_P, ctypes.c_uint64, _P]),
+    "dpso_upload_matrix": (_I32, [_P, _I64, _I32, _I32, _P, _I64, _P]),
     "dpso_write_matrix_text": (_I32, [ctypes.c_char_p, _P, _I64, _I32]),
     "dpso_read_matrix_text": (_I32, [ctypes.c_char_p, _P, _I64, _I32,
                                      ctypes.POINTER(_I32)]),

@@ -171,8 +171,10 @@ class IslandSolver:
         # a CUDA tensor (e.g. build_cost_matrix(..., return_device=True))
         # stays on the device, as DiscreteSwarmSolver.fit takes it
         dev_cost = probe._device_cost(X)
-        cost = None if dev_cost is not None else probe._check_cost(X)
-        n = dev_cost[0].shape[0] if dev_cost is not None else cost.shape[0]
+        if dev_cost is None:  # uploaded once, checked on the device
+            dev_cost = probe._upload_cost(X)
+        cost = None
+        n = dev_cost[0].shape[0]
         t0 = time.perf_counter()
         G = int(probe.max_generations)
         distributed = self.devices is None and dist.is_available() and \
@@ -199,7 +201,7 @@ class IslandSolver:
                 base = int(np.random.SeedSequence().entropy % (1 << 62))
             islands = [(k, torch.device(d)) for k, d in enumerate(devs)]
         if n == 1:
-            probe.fit(X if cost is None else cost)
+            probe.fit(X)
             self._copy(probe, world, 0)
             return self
         ctxs = []

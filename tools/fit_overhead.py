@@ -20,10 +20,11 @@ import bench  # noqa: E402
 def main():
     import torch
     from paper_1706_04399_b200 import DiscreteSwarmSolver
-    from paper_1706_04399_b200.solver import (SwarmContext, device_cost,
+    from paper_1706_04399_b200.solver import (SwarmContext,
                                               numpy_stream_states)
     name = sys.argv[1] if len(sys.argv) > 1 else "c2"
     cfg = bench.CONFIGS[name]
+    bench.RNG = cfg.get("rng", "numpy")  # as bench.py's main sets it
     cost, seed_tour = bench.make_matrix(cfg)
     P, G = cfg["P"], cfg["G"]
     params = bench.gpu_params(cfg, P, G, 7)
@@ -46,17 +47,19 @@ def main():
         t = time.perf_counter()
         s = DiscreteSwarmSolver(**params)
         s._check_params()
-        c = s._check_cost(cost)
-        t = mark("checks_ms", t)
-        cost_t, ld = device_cost(c, s.device)
-        t = mark("matrix_h2d_ms", t)
-        ctx = SwarmContext(s._params(), c.shape[0], cost_t, ld)
+        # fit()'s path: shape check on the host, upload, finiteness on the
+        # device
+        cost_t, ld = s._upload_cost(cost)
+        t = mark("checks_and_h2d_ms", t)
+        n = cost_t.shape[0]
+        ctx = SwarmContext(s._params(), n, cost_t, ld)
         t = mark("context_ms", t)
-        seed_body, n_seed = s._seed(c.shape[0])
-        st = numpy_stream_states(s.random_state, P + 2)
-        t = mark("stream_states_ms", t)
-        ctx.set_streams(st)
-        t = mark("set_streams_ms", t)
+        seed_body, n_seed = s._seed(n)
+        if s.rng == "numpy":
+            st = numpy_stream_states(s.random_state, P + 2)
+            t = mark("stream_states_ms", t)
+            ctx.set_streams(st)
+            t = mark("set_streams_ms", t)
         ctx.init(seed_body, n_seed)
         t = mark("init_ms", t)
         gens = ctx.run()

@@ -21,6 +21,7 @@ def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "c2"
     seg = int(sys.argv[2]) if len(sys.argv) > 2 else 50
     cfg = bench.CONFIGS[name]
+    bench.RNG = cfg.get("rng", "numpy")  # as bench.py's main sets it
     cost, seed_tour = bench.make_matrix(cfg)
     P, G = cfg["P"], cfg["G"]
     params = bench.gpu_params(cfg, P, G, 7)
