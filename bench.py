@@ -625,6 +625,23 @@ def run_ours(args, cfg_name, cfg):
                 "traffic": traffic, "algorithmic_bytes_per_launch": alg,
                 "avg_launch_ms": dur_ms,
                 "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)"}
+        wf = tr.get(f"{cfg_name}:{dom}:smem_wavefronts")
+        if wf:
+            # the resource that binds the update: the shared-memory pipe
+            # (pointer jumping, random gathers), one wavefront per clock per
+            # SM; wavefronts per launch from ncu, over the live launch time
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            clk_ghz = 1.965
+            pk = sms * clk_ghz * 1e9
+            roof["binding"] = {
+                "resource": "shared-memory pipe (wavefronts)",
+                "wavefronts_per_launch": wf,
+                "achieved_per_s": wf / (dur_ms / 1e3), "peak_per_s": pk,
+                "frac": wf / (dur_ms / 1e3) / pk,
+                "source": "ncu l1tex__data_pipe_lsu_wavefronts_mem_shared."
+                          "sum per launch (profiles/ncu_traffic.json); peak "
+                          f"= {sms} SMs x 1 wavefront/clock x "
+                          f"{clk_ghz} GHz"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
