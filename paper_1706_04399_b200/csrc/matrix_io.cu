@@ -376,11 +376,11 @@ int dpso_py_repr(double x, char* out, int32_t cap) {
 // of two pinned chunks, each filled by several host threads (memcpy of row
 // slices) while the other chunk's DMA runs on the caller's stream.
 namespace {
+// (the pinned chunks are kept for the process: page-locking 64 MB costs
+// more than an upload of it)
 struct PinnedRing {
   std::mutex mu;
   unsigned char* buf[2] = {nullptr, nullptr};
-  cudaEvent_t ev[2] = {nullptr, nullptr};
-  size_t bytes = 0;
 };
 PinnedRing& pinned_ring() {
   static PinnedRing r;
@@ -411,12 +411,22 @@ extern "C" int dpso_upload_matrix(const double* host, int64_t host_ld,
   std::lock_guard<std::mutex> lock(R.mu);
   if (!R.buf[0]) {
     for (int b = 0; b < 2; ++b) {
-      e = cudaHostAlloc((void**)&R.buf[b], kUploadChunk, cudaHostAllocDefault);
-      if (!e) e = cudaEventCreateWithFlags(&R.ev[b], cudaEventDisableTiming);
+      e = cudaHostAlloc((void**)&R.buf[b], kUploadChunk,
+                        cudaHostAllocPortable);
       if (e) return fail(DPSO_ECUDA, cudaGetErrorString(e));
     }
-    R.bytes = kUploadChunk;
   }
+  // events of the stream's device (the caller may upload to several GPUs)
+  struct Events {
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    ~Events() {
+      for (auto x : ev)
+        if (x) cudaEventDestroy(x);
+    }
+  } E;
+  for (int b = 0; b < 2; ++b)
+    if ((e = cudaEventCreateWithFlags(&E.ev[b], cudaEventDisableTiming)))
+      return fail(DPSO_ECUDA, cudaGetErrorString(e));
   const int per_chunk = (int)(kUploadChunk / row_b);
   const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
   const int nthr = (int)std::min<unsigned>(8, hw);
@@ -426,8 +436,13 @@ extern "C" int dpso_upload_matrix(const double* host, int64_t host_ld,
     const int nr = std::min(per_chunk, rows - r0);
     const int b = chunk & 1;
     // the DMA that last read this chunk is done
-    if (used[b] && (e = cudaEventSynchronize(R.ev[b])))
-      return fail(DPSO_ECUDA, cudaGetErrorString(e));
+    // (on an error, drain the stream: no DMA may still read a chunk the
+    // next call refills)
+    auto bail = [&](cudaError_t err) {
+      cudaStreamSynchronize(s);
+      return fail(DPSO_ECUDA, cudaGetErrorString(err));
+    };
+    if (used[b] && (e = cudaEventSynchronize(E.ev[b]))) return bail(e);
     unsigned char* dst = R.buf[b];
     auto fill = [&](int t) {
       const int a = r0 + (int)((int64_t)nr * t / nthr);
@@ -447,8 +462,8 @@ extern "C" int dpso_upload_matrix(const double* host, int64_t host_ld,
     for (auto& x : th) x.join();
     e = cudaMemcpy2DAsync(dev + (size_t)r0 * dev_ld, (size_t)dev_ld * 8, dst,
                           row_b, row_b, nr, cudaMemcpyHostToDevice, s);
-    if (!e) e = cudaEventRecord(R.ev[b], s);
-    if (e) return fail(DPSO_ECUDA, cudaGetErrorString(e));
+    if (!e) e = cudaEventRecord(E.ev[b], s);
+    if (e) return bail(e);
     used[b] = true;
   }
   e = cudaStreamSynchronize(s);

@@ -46,3 +46,19 @@ def test_upload_rejects_bad_arguments(lib):
     with pytest.raises(ValueError):
         lib.check(lib.load().dpso_upload_matrix(
             h.ctypes.data, 4, 4, 4, dev.data_ptr(), 2, None))
+
+
+def test_upload_to_a_second_device(lib):
+    # the chunk events belong to the target stream's device
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("one GPU")
+    host = np.random.default_rng(5).standard_normal((3000, 3000))
+    for d in range(2):
+        with torch.cuda.device(d):
+            dev = torch.zeros((3000, 3000), dtype=torch.float64,
+                              device=f"cuda:{d}")
+            lib.check(lib.load().dpso_upload_matrix(
+                host.ctypes.data, 3000, 3000, 3000, dev.data_ptr(), 3000,
+                torch.cuda.current_stream().cuda_stream))
+            assert np.array_equal(dev.cpu().numpy(), host)
