@@ -388,9 +388,14 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
     // ---- producer warp pw: rows rpp pw .. rpp pw + rpp - 1 of every band
     const int pw = warp - NW;
     constexpr int rpp = 32 / kProdWarps;  // rows per producer warp
-    int band = 0, pl = 0, cb = 0, s = 0, use = 0;
+    int band = 0, pl = 0, cb = 0, s = 0, use = 0, cuse = 0;
     for (int t = 0; t < total; ++t) {
       if (use > 0) mbar_wait_backoff(&empty[s], (uint32_t)((use - 1) & 1));
+      // from the particle's second band on, its cities come from the column
+      // records in shared memory (O[3 + k] = 2 a_k) instead of a dependent
+      // global load ahead of every copy
+      if (band == 1) mbar_wait_backoff(&colfull[cb], (uint32_t)(cuse & 1));
+      const int* Oc = cols + cb * 2 * a.cw + 3;
       const int pp = (int)blockIdx.x + pl * (int)gridDim.x;
       const int i0 = band * kBandRows;
       const int r0 = rpp * pw;
@@ -412,7 +417,10 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
         if (++band == nb) {
           band = 0;
           ++pl;
-          if (++cb == ncb) cb = 0;
+          if (++cb == ncb) {
+            cb = 0;
+            ++cuse;
+          }
         }
         continue;
       }
@@ -439,7 +447,10 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
           int rw[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            rw[q] = q * n + (4 * g + q < rows_left ? (int)tr[q] : 0);
+            rw[q] = q * n + (4 * g + q < rows_left
+                                 ? (band ? Oc[i0 + 4 * g + q] >> 1
+                                         : (int)tr[q])
+                                 : 0);
           tma_gather4(stg + (size_t)4 * g * S, &tm, -2 * g, rw[0], rw[1],
                       rw[2], rw[3], &full[s]);
         }
@@ -452,7 +463,8 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
         if (lane < nr) {
           fence_proxy_async();  // the consumers' reads of the stage first
           const int l = r0 + lane;
-          const int city = a.tours[(size_t)pp * a.np + i0 + l];
+          const int city = band ? Oc[i0 + l] >> 1
+                                : (int)a.tours[(size_t)pp * a.np + i0 + l];
           const unsigned char* src =
               a.rows + ((size_t)(l & 3) * n + city) * (size_t)a.line;
           bulk_g2s(stg + (size_t)l * S + 16 * (l >> 2), src,
@@ -469,7 +481,10 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
       if (++band == nb) {
         band = 0;
         ++pl;
-        if (++cb == ncb) cb = 0;
+        if (++cb == ncb) {
+            cb = 0;
+            ++cuse;
+          }
       }
     }
     return;
