@@ -45,6 +45,12 @@
 // and are not scanned; (0, n-1) is scanned (it is not a no-op for
 // asymmetric matrices).
 //
+// Two rows per lane (RPL = 2, wherever two 64-slot stages fit: n up to
+// ~600): 64-slot bands of 63 pair rows, lane l owning rows i0 + l and
+// i0 + 32 + l; one address and one set of column records per column serve
+// both rows (the second row's loads at uniform offsets 32 (S + 4) and
+// 33 (S + 4)), each row set with its own lane state.
+//
 // Pipeline: persistent CTAs (one per SM), particles blockIdx.x + k*grid;
 // a ring of 2-4 band stages filled by producer warps (bulk copies, full /
 // empty mbarriers), consumed by consumer warps at their own pace (no CTA
@@ -181,6 +187,14 @@ __device__ __noinline__ int band_hit(int u0, int u1, int u2, int u3, int u4,
         wt = t2;
         wi = i2;
       }
+    }
+    {  // with the warp's best so far (two rows per lane: the other set's)
+      const int ow = ws[0], oi = ws[1];
+      if (ow < wt || (ow == wt && oi < wi)) {
+        wt = ow;
+        wi = oi;
+      }
+      __syncwarp();
     }
     // the CTA-wide minimum t over all warps of this particle: a pair above
     // it cannot be the argmin, so it caps every lane's limit (ties at it
@@ -323,6 +337,64 @@ __device__ __forceinline__ void band_group(const int* O, const int* D,
                        Di, L, live, win, st, ws, cmin);
 }
 
+// Two rows per lane (64-slot bands): lane l owns pair rows i0 + l (slots l,
+// l + 1) and i0 + 32 + l (slots 32 + l, 33 + l).  One set of column records
+// and one address per column serve both rows; the second row's loads sit
+// at uniform offsets 32 (S + 4) and 33 (S + 4) from the first's.
+// M1 / M2: the columns c < i + 2 of row set 1 / 2 are dead (the triangle).
+template <int MODE, bool M1, bool M2>
+__device__ __forceinline__ void band_group2(
+    const int* O, const int* D, int c0, uint32_t R, int& prev, int& prev2,
+    int& L, int& L2, int i, int i2, int Di, int Di2, bool live, bool live2,
+    int win, int* st, int* st2, int* ws, int* cmin, uint32_t sn,
+    uint32_t s32, uint32_t s33) {
+  const int4 oa = *reinterpret_cast<const int4*>(O + 4 + c0);
+  const int4 ob = *reinterpret_cast<const int4*>(O + 8 + c0);
+  const int4 da = *reinterpret_cast<const int4*>(D + c0);
+  const int4 db = *reinterpret_cast<const int4*>(D + c0 + 4);
+  const int off[8] = {oa.x, oa.y, oa.z, oa.w, ob.x, ob.y, ob.z, ob.w};
+  const int dv[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
+  int g[8], nb[8], g2[8], nb2[8], u[8], u2[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t ad = R + (uint32_t)off[k];
+    g[k] = lds_s16(ad);
+    nb[k] = lds_s16(ad + sn);
+    g2[k] = lds_s16(ad + s32);
+    nb2[k] = lds_s16(ad + s33);
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    u[k] = (k ? g[k - 1] : prev) + nb[k] - dv[k];
+    u2[k] = (k ? g2[k - 1] : prev2) + nb2[k] - dv[k];
+  }
+  prev = g[7];
+  prev2 = g2[7];
+  if (M1) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (c0 + k < i + 2) u[k] = kBig;
+  }
+  if (M2) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (c0 + k < i2 + 2) u2[k] = kBig;
+  }
+  const int mn = min(min(min(u[0], u[1]), min(u[2], u[3])),
+                     min(min(u[4], u[5]), min(u[6], u[7])));
+  const int mn2 = min(min(min(u2[0], u2[1]), min(u2[2], u2[3])),
+                      min(min(u2[4], u2[5]), min(u2[6], u2[7])));
+  const bool h1 = mn <= L, h2 = mn2 <= L2;
+  if (__any_sync(0xffffffffu, h1 || h2)) {
+    if (__any_sync(0xffffffffu, h1))
+      L = band_hit<MODE>(u[0], u[1], u[2], u[3], u[4], u[5], u[6], u[7], c0,
+                         i, Di, L, live, win, st, ws, cmin);
+    if (__any_sync(0xffffffffu, h2))
+      L2 = band_hit<MODE>(u2[0], u2[1], u2[2], u2[3], u2[4], u2[5], u2[6],
+                          u2[7], c0, i2, Di2, L2, live2, win, st2, ws, cmin);
+  }
+}
+
 // Persistent CTAs: kBandWarps consumer warps + kProdWarps producer warps.
 // CTA b scans particles b, b + grid, ...; a particle's bands run in order
 // and band t sits in stage t % nst of a ring; a particle's column arrays
@@ -341,9 +413,11 @@ __device__ __forceinline__ void band_group(const int* O, const int* D,
 constexpr int kProdWarps = 4;
 constexpr int kMaxNcb = 8;
 
-template <int MODE>
+template <int MODE, int RPL>
 __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
     k_two_opt_band(BandArgs a, const __grid_constant__ CUtensorMap tm) {
+  // RPL rows per lane: 32 RPL slots and 32 RPL - 1 pair rows per band
+  constexpr int kSlots = 32 * RPL, kRows = kSlots - 1;
   if (a.ctl && (a.ctl->done || a.ctl->improved)) return;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
@@ -356,7 +430,7 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int NW = kBandWarps;
   const int n = a.n, nst = a.nst, ncb = a.ncb;
-  const int nb = (n + kBandRows - 2) / kBandRows;  // bands: rows 0 .. n-2
+  const int nb = (n + kRows - 2) / kRows;  // bands: rows 0 .. n-2
   const int nmine =
       (int)blockIdx.x < a.count ? (a.count - 1 - (int)blockIdx.x) / gridDim.x + 1
                                 : 0;
@@ -364,7 +438,7 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
   const int total = nmine * nb;
   const uint32_t S = a.slot;
   unsigned char* rowbuf = smem;
-  const uint32_t stage_bytes = 32 * S + 128;
+  const uint32_t stage_bytes = kSlots * S + 128 * RPL;
   int* cols = (int*)(smem + (size_t)nst * stage_bytes);  // [ncb][O | D]
   int* lstate = cols + ncb * 2 * a.cw;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
@@ -387,7 +461,7 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
   if (warp >= NW) {
     // ---- producer warp pw: rows rpp pw .. rpp pw + rpp - 1 of every band
     const int pw = warp - NW;
-    constexpr int rpp = 32 / kProdWarps;  // rows per producer warp
+    constexpr int rpp = kSlots / kProdWarps;  // rows per producer warp
     int band = 0, pl = 0, cb = 0, s = 0, use = 0, cuse = 0;
     for (int t = 0; t < total; ++t) {
       if (use > 0) mbar_wait_backoff(&empty[s], (uint32_t)((use - 1) & 1));
@@ -397,7 +471,7 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
       if (band == 1) mbar_wait_backoff(&colfull[cb], (uint32_t)(cuse & 1));
       const int* Oc = cols + cb * 2 * a.cw + 3;
       const int pp = (int)blockIdx.x + pl * (int)gridDim.x;
-      const int i0 = band * kBandRows;
+      const int i0 = band * kRows;  // kRows pair rows per band
       const int r0 = rpp * pw;
       const int nr = max(0, min(rpp, n - i0 - r0));
       const bool withcols = band == 0 && pw == 0;
@@ -430,7 +504,7 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
         // to stg + 4 g S (128-byte aligned), slot 4g + q from version q with
         // the box starting 16 g bytes before the line: slot l's element c
         // lands at l (S + 4) + 2c, the bulk-copy layout
-        constexpr int gpp = 8 / kProdWarps;
+        constexpr int gpp = kSlots / 4 / kProdWarps;
         const int rows_left = n - i0;
         int mine = 0;
 #pragma unroll
@@ -451,8 +525,10 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
                                  ? (band ? Oc[i0 + 4 * g + q] >> 1
                                          : (int)tr[q])
                                  : 0);
-          tma_gather4(stg + (size_t)4 * g * S, &tm, -2 * g, rw[0], rw[1],
-                      rw[2], rw[3], &full[s]);
+          // groups past the eighth: whole 128-byte steps of the shift go to
+          // the destination (it must stay 128-byte aligned)
+          tma_gather4(stg + (size_t)4 * g * S + 128 * (g >> 3), &tm,
+                      -2 * (g & 7), rw[0], rw[1], rw[2], rw[3], &full[s]);
         }
       } else {
         if (lane == 0) {
@@ -491,12 +567,18 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
   }
 
   // ---- consumer warp
-  int* st = lstate + warp * kLaneState * 32 + lane;
+  int* st = lstate + warp * kLaneState * 32 * RPL + lane;
+  int* st2 = st + kLaneState * 32;  // RPL == 2: the lane's second row
   int* ws = s_ws[warp];
   auto reset_state = [&]() {
     st[0] = MODE == 1 ? kNone : kBig;
     st[32] = MODE == 1 ? INT_MAX : 0;
     st[64] = MODE == 1 ? INT_MAX : 0;
+    if (RPL == 2) {
+      st2[0] = MODE == 1 ? kNone : kBig;
+      st2[32] = MODE == 1 ? INT_MAX : 0;
+      st2[64] = MODE == 1 ? INT_MAX : 0;
+    }
     if (lane == 0) {
       ws[0] = kNone;
       ws[1] = INT_MAX;
@@ -531,20 +613,26 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
   const uint32_t R0 = smem_u32(rowbuf) + (uint32_t)lane * (S + 4u);
   for (int t = grp; t < total; t += G) {
     const int pp = (int)blockIdx.x + pl * (int)gridDim.x;
-    const int i0 = band * kBandRows;
+    const int i0 = band * kRows;
     // the particle's column arrays (its first band for this warp), rows
     if (band < G) mbar_wait_sleep_u32(colfull_a + 8u * cb, (uint32_t)(cuse & 1));
     mbar_wait_sleep_u32(full_a + 8u * s, (uint32_t)(use & 1));
     const int* O = cols + cb * 2 * a.cw;
     const int* D = O + a.cw;
     const int i = i0 + lane;
-    const bool live = lane < kBandRows && i <= n - 2;
+    const bool live = (RPL == 2 || lane < kBandRows) && i <= n - 2;
     const int Di = live ? D[i] : 0;
     const uint32_t R = R0 + (uint32_t)s * stage_bytes;
     int L = lane_limit<MODE>(live, Di, i, ws[0], ws[1]);
+    const int i2 = i0 + 32 + lane;
+    const bool live2 = RPL == 2 && lane < 31 && i2 <= n - 2;
+    const int Di2 = live2 ? D[i2] : 0;
+    int L2 = RPL == 2 ? lane_limit<MODE>(live2, Di2, i2, ws[0], ws[1])
+                      : INT_MIN;
     {  // capped by the CTA-wide minimum (other warps' finds)
       const int cm = *(volatile int*)&s_cmin[cb];
       if (live) L = min(L, cm + (MODE == 2 ? a.win : 0) + Di);
+      if (live2) L2 = min(L2, cm + (MODE == 2 ? a.win : 0) + Di2);
     }
     const int cs = (i0 + 2) & ~7;
     const int per = ((((n - cs) + NWg - 1) >> lgw) + 7) & ~7;
@@ -552,12 +640,32 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
     if (cA < cB && a.probe != 1) {
       int prev = lds_s16(R + (uint32_t)O[3 + cA]);
       int c0 = cA;
-      for (; c0 < cB && c0 < i0 + 32; c0 += 8)
-        band_group<MODE, true>(O, D, c0, R, prev, L, i, Di, live, a.win, st,
-                               ws, &s_cmin[cb], S + 4u);
-      for (; c0 < cB; c0 += 8)
-        band_group<MODE, false>(O, D, c0, R, prev, L, i, Di, live, a.win, st,
-                                ws, &s_cmin[cb], S + 4u);
+      if (RPL == 1) {
+        for (; c0 < cB && c0 < i0 + 32; c0 += 8)
+          band_group<MODE, true>(O, D, c0, R, prev, L, i, Di, live, a.win,
+                                 st, ws, &s_cmin[cb], S + 4u);
+        for (; c0 < cB; c0 += 8)
+          band_group<MODE, false>(O, D, c0, R, prev, L, i, Di, live, a.win,
+                                  st, ws, &s_cmin[cb], S + 4u);
+      } else {
+        const uint32_t s32 = 32u * (S + 4u), s33 = s32 + S + 4u;
+        int prev2 = lds_s16(R + s32 + (uint32_t)O[3 + cA]);
+        for (; c0 < cB && c0 < i0 + 32; c0 += 8)
+          band_group2<MODE, true, true>(O, D, c0, R, prev, prev2, L, L2, i,
+                                        i2, Di, Di2, live, live2, a.win, st,
+                                        st2, ws, &s_cmin[cb], S + 4u, s32,
+                                        s33);
+        for (; c0 < cB && c0 < i0 + 64; c0 += 8)
+          band_group2<MODE, false, true>(O, D, c0, R, prev, prev2, L, L2, i,
+                                         i2, Di, Di2, live, live2, a.win, st,
+                                         st2, ws, &s_cmin[cb], S + 4u, s32,
+                                         s33);
+        for (; c0 < cB; c0 += 8)
+          band_group2<MODE, false, false>(O, D, c0, R, prev, prev2, L, L2, i,
+                                          i2, Di, Di2, live, live2, a.win,
+                                          st, st2, ws, &s_cmin[cb], S + 4u,
+                                          s32, s33);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive_u32(empty_a + 8u * s);  // stage reads done
@@ -575,30 +683,41 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
           bi = st[32];
           bj = st[64];
         }
-      } else if (__any_sync(0xffffffffu, st[64])) {
+        if (RPL == 2 && st2[0] < kNone &&
+            lex_lt((double)st2[0], st2[32], st2[64], bd, bi, bj)) {
+          bd = (double)st2[0];
+          bi = st2[32];
+          bj = st2[64];
+        }
+      } else if (__any_sync(0xffffffffu,
+                            st[64] || (RPL == 2 && st2[64]))) {
         if (lane == 0) atomicOr(&s_of[cb], 1);
       } else {
-        const int nc = st[32];
-        int wm = st[0];
+        int wm = RPL == 2 ? min(st[0], st2[0]) : st[0];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1)
           wm = min(wm, __shfl_xor_sync(0xffffffffu, wm, o));
         const int keep = wm + a.win;
-        const int* cd = st + 96;
-        const int* cij = cd + 32 * kBandCand;
-        for (int k = 0; k < nc; ++k) {
-          if (cd[32 * k] <= keep) {
-            const int ci = cij[32 * k] >> 16, cj = cij[32 * k] & 0xFFFF;
-            const int ai = tour[ci], aj = tour[cj];
-            const int si = tour[ci + 1], sj = tour[cj + 1 == n ? 0 : cj + 1];
-            double v = __dadd_rn(a.cost[(size_t)ai * a.ld + aj],
-                                 a.cost[(size_t)si * a.ld + sj]);
-            v = __dsub_rn(v, dg[ci]);
-            v = __dsub_rn(v, dg[cj]);
-            if (lex_lt(v, ci, cj, bd, bi, bj)) {
-              bd = v;
-              bi = ci;
-              bj = cj;
+        for (int set = 0; set < RPL; ++set) {
+          const int* sts = set ? st2 : st;
+          const int nc = sts[32];
+          const int* cd = sts + 96;
+          const int* cij = cd + 32 * kBandCand;
+          for (int k = 0; k < nc; ++k) {
+            if (cd[32 * k] <= keep) {
+              const int ci = cij[32 * k] >> 16, cj = cij[32 * k] & 0xFFFF;
+              const int ai = tour[ci], aj = tour[cj];
+              const int si = tour[ci + 1],
+                        sj = tour[cj + 1 == n ? 0 : cj + 1];
+              double v = __dadd_rn(a.cost[(size_t)ai * a.ld + aj],
+                                   a.cost[(size_t)si * a.ld + sj]);
+              v = __dsub_rn(v, dg[ci]);
+              v = __dsub_rn(v, dg[cj]);
+              if (lex_lt(v, ci, cj, bd, bi, bj)) {
+                bd = v;
+                bi = ci;
+                bj = cj;
+              }
             }
           }
         }
@@ -707,46 +826,60 @@ bool band_g4_fits(int n) {
          kG4MaxBox;
 }
 
-int band_nb(int n) { return (n + kBandRows - 2) / kBandRows; }
+// bands of 32 rpl - 1 pair rows (rpl rows per lane)
+int band_nb(int n, int rpl) {
+  const int rows = 32 * rpl - 1;
+  return (n + rows - 2) / rows;
+}
 
 // column buffers / result slots for nst stages: no warp runs more than nst
 // bands ahead of another, so (ncb - 1) nb >= nst keeps a particle's buffers
 // until every warp is past it
-int band_ncb(int n, int nst) {
-  const int nb = band_nb(n);
+int band_ncb(int n, int nst, int rpl) {
+  const int nb = band_nb(n, rpl);
   return std::min(kMaxNcb, std::max(2, (nst + nb - 1) / nb + 1));
 }
 
 // warp groups: two groups scan alternate bands when two stages can be
 // scanned while the others load (nst == 4) and every group has a band in
-// every particle
-int band_groups(int n, int nst) {
+// every particle (one row per lane only)
+int band_groups(int n, int nst, int rpl) {
+  if (rpl == 2) return 1;
   if (const char* e = getenv("DPSO_BAND_GROUPS")) {
     const int g = atoi(e);
-    if (g == 1 || (g == 2 && nst % 2 == 0 && band_nb(n) >= 2)) return g;
+    if (g == 1 || (g == 2 && nst % 2 == 0 && band_nb(n, 1) >= 2)) return g;
   }
-  return nst == 4 && band_nb(n) >= 2 ? 2 : 1;
+  return nst == 4 && band_nb(n, 1) >= 2 ? 2 : 1;
 }
 
-size_t band_smem(int n, int nst, bool g4) {
+size_t band_smem(int n, int nst, bool g4, int rpl) {
   const int line = band_line(n);
-  return (size_t)nst * (32 * band_slot(line, g4) + 128) +
-         (size_t)band_ncb(n, nst) * 2 * band_cw(n) * 4 +
-         (size_t)kBandWarps * kLaneState * 32 * 4;
+  return (size_t)nst * (32 * rpl * band_slot(line, g4) + 128 * rpl) +
+         (size_t)band_ncb(n, nst, rpl) * 2 * band_cw(n) * 4 +
+         (size_t)kBandWarps * kLaneState * 32 * 4 * rpl;
 }
 
 constexpr size_t kBandSmemMax = 225 * 1024;
 
 // stages: as many as fit, up to kMaxStages
-int band_stages(int n, bool g4) {
+int band_stages(int n, bool g4, int rpl) {
   int nst = kMaxStages;
-  while (nst > 2 && band_smem(n, nst, g4) > kBandSmemMax) --nst;
+  while (nst > 2 && band_smem(n, nst, g4, rpl) > kBandSmemMax) --nst;
   if (const char* e = getenv("DPSO_BAND_STAGES")) {
     const int x = atoi(e);
-    if (x >= 2 && x <= kMaxStages && band_smem(n, x, g4) <= kBandSmemMax)
+    if (x >= 2 && x <= kMaxStages &&
+        band_smem(n, x, g4, rpl) <= kBandSmemMax)
       nst = x;
   }
   return nst;
+}
+
+// two rows per lane (64-slot bands) wherever two such stages fit;
+// DPSO_BAND_RPL=1 keeps one
+int band_rpl(int n, bool g4) {
+  if (const char* e = getenv("DPSO_BAND_RPL"))
+    if (atoi(e) == 1) return 1;
+  return n >= 64 && band_smem(n, 2, g4, 2) <= kBandSmemMax ? 2 : 1;
 }
 
 // The tensor map of the row versions for gather4: a 2-D tensor of 4n lines
@@ -789,7 +922,7 @@ int band_line(int n) { return (int)round_up(2 * (int64_t)n + 12, 16); }
 int band_cw(int n) { return (int)round_up(n + 16, 8); }
 
 int64_t band_rows_bytes(int n) {
-  if (n < 4 || n > kBandMaxN || band_smem(n, 2, false) > kBandSmemMax)
+  if (n < 4 || n > kBandMaxN || band_smem(n, 2, false, 1) > kBandSmemMax)
     return 0;
   return 4 * (int64_t)n * band_line(n);
 }
@@ -880,29 +1013,27 @@ cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
                                      ctl);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
-  a.nst = band_stages(n, a.g4 != 0);
-  a.ncb = band_ncb(n, a.nst);
-  a.groups = band_groups(n, a.nst);
+  const int rpl = band_rpl(n, a.g4 != 0);
+  a.nst = band_stages(n, a.g4 != 0, rpl);
+  a.ncb = band_ncb(n, a.nst, rpl);
+  a.groups = band_groups(n, a.nst, rpl);
   if (const char* e = getenv("DPSO_BAND_PROBE")) a.probe = atoi(e);
-  const size_t smem = band_smem(n, a.nst, a.g4 != 0);
+  const size_t smem = band_smem(n, a.nst, a.g4 != 0, rpl);
   alignas(64) CUtensorMap tm;
   memcpy(&tm, pl.band_tm, sizeof tm);  // unused (zero) without gather4
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int blocks = std::max(1, std::min(count, sms - reserve_sms));
-  if (pl.band_mode == 1) {
-    e = set_dyn_smem((const void*)k_two_opt_band<1>, smem);
-    if (e) return e;
-    k_two_opt_band<1>
-        <<<blocks, (kBandWarps + kProdWarps) * 32, smem, s>>>(a, tm);
-  } else {
-    e = set_dyn_smem((const void*)k_two_opt_band<2>, smem);
-    if (e) return e;
-    k_two_opt_band<2>
-        <<<blocks, (kBandWarps + kProdWarps) * 32, smem, s>>>(a, tm);
-  }
-  return cudaGetLastError();
+  auto go = [&](auto kern) {
+    cudaError_t err = set_dyn_smem((const void*)kern, smem);
+    if (err) return err;
+    kern<<<blocks, (kBandWarps + kProdWarps) * 32, smem, s>>>(a, tm);
+    return cudaGetLastError();
+  };
+  if (pl.band_mode == 1)
+    return rpl == 2 ? go(k_two_opt_band<1, 2>) : go(k_two_opt_band<1, 1>);
+  return rpl == 2 ? go(k_two_opt_band<2, 2>) : go(k_two_opt_band<2, 1>);
 }
 
 }  // namespace dpso

@@ -157,6 +157,24 @@ def test_band_more_particles_than_ctas(pkg):
         check(pkg, cost / 7.0, perms(rng, P, n), ("multi-f", n, P), 64, rng)
 
 
+@pytest.mark.parametrize("rpl", ["2", "1"])
+@pytest.mark.parametrize("mode", ["exact", "filter"])
+def test_band_two_rows_per_lane(pkg, mode, rpl, monkeypatch):
+    # 64-slot bands (lane l: pair rows i0 + l and i0 + 32 + l), the default
+    # for 64 <= n <= ~600: 63-row band edges, the second set's triangle,
+    # partial last bands; DPSO_BAND_RPL=1 the 32-slot bands at the same n
+    if mode == "filter":
+        monkeypatch.setenv("DPSO_BAND_MODE", "2")
+    monkeypatch.setenv("DPSO_BAND_RPL", rpl)
+    rng = np.random.default_rng(53)
+    for n in (64, 65, 66, 95, 96, 97, 126, 127, 128, 129, 189, 190, 191,
+              252, 253, 300, 441, 500, 580, 600):
+        cost = np.floor(random_euclidean_matrix(n, rng) * 100.0)
+        check(pkg, cost, perms(rng, 5, n), (mode, rpl, n))
+    cost = grid(500)
+    check(pkg, cost, perms(rng, 300, 500), (mode, rpl, "grid"), 24, rng)
+
+
 def test_band_gather4_limit(pkg):
     # the largest n whose shifted lines fit one gather4 box (2048 bytes:
     # 2n + 124 <= 2048) and the first n past it (bulk copies); partial last
