@@ -451,6 +451,8 @@ def run_ours(args, cfg_name, cfg):
     ctx = solver._make_context(cost)
     band = int(ctx.lib.dpso_scan_band(ctx.h))
     staging = int(ctx.lib.dpso_band_staging(ctx.h))
+    band_line = int(ctx.lib.dpso_band_line(ctx.h))
+    band_rows = int(ctx.lib.dpso_band_rows(ctx.h))
     if RNG == "numpy":
         ctx.set_streams(numpy_stream_states(params["random_state"], P + 2))
     ctx.init(seed_body, n_seed)
@@ -576,9 +578,12 @@ def run_ours(args, cfg_name, cfg):
         # rows at n = 1000: the 31-row bands overlap by one row).  Column
         # scan: fp16/fp32 rows once per task.
         if band:
-            line_b = int(math.ceil((2 * n + 12) / 16.0) * 16)
-            nbands = (n + 29) // 31
-            staged = float(P) * nbands * min(32, n) * line_b
+            # int16 rows (int8 past n ~ 1400), 32-slot bands of 31 pair
+            # rows or 64-slot bands of 63 (two rows per lane): either way
+            # every row of the tour is staged once per band it falls in
+            line_b = band_line
+            nbands = (n + band_rows - 2) // band_rows
+            staged = float(P) * nbands * min(band_rows + 1, n) * line_b
         else:
             line_b = int(math.ceil(2 * n / 16.0) * 16)
             staged = float(P) * (n + 1) * line_b * max(1, -(-n // 1024))
@@ -609,6 +614,8 @@ def run_ours(args, cfg_name, cfg):
                 "avg_launch_ms": dur_ms,
                 "staging": {0: "column scan", 1: "bulk copies",
                             2: "TMA gather4"}.get(staging),
+                "row_line_bytes": line_b,
+                "pair_rows_per_band": band_rows if band else None,
                 "peak_source": peak_desc,
                 "l2_random_gather_f64_gbs":
                     gpk.get("gather_f64_8MB", {}).get("useful_gbs"),

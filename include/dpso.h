@@ -102,6 +102,15 @@ int dpso_scan_band(dpso_ctx* ctx);
  * n <= ~960), 1 = one bulk copy per row, 0 = no band scan.  Diagnostic. */
 int dpso_band_staging(dpso_ctx* ctx);
 
+/* Bytes per staged row line of the band scan (int16 rows: round_up(2n + 12,
+ * 16); int8 rows for n > ~1400: round_up(n + 12, 16)), 0 = no band scan.
+ * Diagnostic (the bench's staged-byte count). */
+int dpso_band_line(dpso_ctx* ctx);
+
+/* Pair rows per band of the band scan: 31 (one row per lane) or 63 (two
+ * rows per lane, n <= ~600), 0 = no band scan.  Diagnostic. */
+int dpso_band_rows(dpso_ctx* ctx);
+
 /* How the last dpso_init located each particle's draws in the shared numpy
  * init stream: 1 = parallel walk (every start's walk length, then pointer
  * doubling), 0 = serial scan (too large a span, a walk ran off the span, or

@@ -632,6 +632,16 @@ int dpso_scan_mode(dpso_ctx* c) { return c ? c->v.plan.mode : -1; }
 
 int dpso_scan_band(dpso_ctx* c) { return c ? c->v.plan.band_mode : -1; }
 
+int dpso_band_line(dpso_ctx* c) {
+  if (!c) return -1;
+  return c->v.plan.band_mode ? c->v.plan.band_line : 0;
+}
+
+int dpso_band_rows(dpso_ctx* c) {
+  if (!c) return -1;
+  return c->v.plan.band_mode ? 32 * c->v.plan.band_rpl - 1 : 0;
+}
+
 int dpso_band_staging(dpso_ctx* c) {
   if (!c) return -1;
   if (!c->v.plan.band_mode) return 0;

@@ -92,6 +92,8 @@ struct TwoOptPlan {
   // band_win), 0 not used.  band_vfrom/vto: the virtual cap of those rows.
   const unsigned char* band;
   int band_line;
+  int band_es;             // row element bytes: 2 (int16) or 1 (int8)
+  int band_rpl;            // pair rows per lane: 1 (32-slot) or 2 (64)
   int band_mode;
   double band_scale;
   int band_win;

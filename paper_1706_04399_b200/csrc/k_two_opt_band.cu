@@ -119,6 +119,15 @@ __device__ __forceinline__ int lds_s16(uint32_t addr) {
   return v;
 }
 
+// a row element: int16 (ES = 2) or int8 (ES = 1, the rows of n > ~1400)
+template <int ES>
+__device__ __forceinline__ int lds_el(uint32_t addr) {
+  if (ES == 2) return lds_s16(addr);
+  int v;
+  asm volatile("ld.shared.s8 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
 __device__ __forceinline__ bool lex_lt(double d1, int i1, int j1, double d2,
                                        int i2, int j2) {
   if (d1 < d2) return true;
@@ -264,7 +273,7 @@ __device__ __noinline__ int band_hit(int u0, int u1, int u2, int u3, int u4,
 __global__ void k_band_cols(const uint16_t* tours, int np,
                             const double* dcache, int n, int cw, int count,
                             double scale, double vfrom, double vto,
-                            int32_t* out, const DevCtl* ctl) {
+                            int32_t* out, const DevCtl* ctl, int es) {
   if (ctl && (ctl->done || ctl->improved)) return;  // no scan this time
   const int p = blockIdx.x;
   if (p >= count) return;
@@ -274,7 +283,7 @@ __global__ void k_band_cols(const uint16_t* tours, int np,
   int32_t* D = O + cw;
   for (int k = threadIdx.x; k < cw; k += blockDim.x) {
     const int kk = k - 3;
-    O[k] = (kk >= 0 && kk <= n) ? 2 * (int)t[kk == n ? 0 : kk] : 0;
+    O[k] = (kk >= 0 && kk <= n) ? es * (int)t[kk == n ? 0 : kk] : 0;
     if (k < n) {
       double d = dg[k];
       if (vfrom > 0.0 && d == vfrom) d = vto;
@@ -290,7 +299,7 @@ __global__ void k_band_cols(const uint16_t* tours, int np,
 // = G_l(c0 + k) + G_{l+1}(c0 + k + 1) - D[c0 + k], the warp-uniform
 // pre-test against the lane limits.  MASK: columns c < i + 2 are dead
 // (the band's triangle).
-template <int MODE, bool MASK>
+template <int MODE, bool MASK, int ES>
 __device__ __forceinline__ void band_group(const int* O, const int* D,
                                            int c0, uint32_t R, int& prev,
                                            int& L, int i, int Di, bool live,
@@ -310,14 +319,14 @@ __device__ __forceinline__ void band_group(const int* O, const int* D,
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const uint32_t ad = R + (uint32_t)off[k];
-    g[k] = lds_s16(ad);
-    nb[k] = lds_s16(ad + slot_next);
+    g[k] = lds_el<ES>(ad);
+    nb[k] = lds_el<ES>(ad + slot_next);
   }
 #pragma unroll
   for (int k = 0; k < 8; ++k) u[k] = (k ? g[k - 1] : prev) + nb[k] - dv[k];
 #else
 #pragma unroll
-  for (int k = 0; k < 8; ++k) g[k] = lds_s16(R + (uint32_t)off[k]);
+  for (int k = 0; k < 8; ++k) g[k] = lds_el<ES>(R + (uint32_t)off[k]);
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int nb = __shfl_down_sync(0xffffffffu, g[k], 1);
@@ -413,7 +422,7 @@ __device__ __forceinline__ void band_group2(
 constexpr int kProdWarps = 4;
 constexpr int kMaxNcb = 8;
 
-template <int MODE, int RPL>
+template <int MODE, int RPL, int ES>
 __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
     k_two_opt_band(BandArgs a, const __grid_constant__ CUtensorMap tm) {
   // RPL rows per lane: 32 RPL slots and 32 RPL - 1 pair rows per band
@@ -522,7 +531,7 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             rw[q] = q * n + (4 * g + q < rows_left
-                                 ? (band ? Oc[i0 + 4 * g + q] >> 1
+                                 ? (band ? Oc[i0 + 4 * g + q] >> (ES - 1)
                                          : (int)tr[q])
                                  : 0);
           // groups past the eighth: whole 128-byte steps of the shift go to
@@ -539,7 +548,7 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
         if (lane < nr) {
           fence_proxy_async();  // the consumers' reads of the stage first
           const int l = r0 + lane;
-          const int city = band ? Oc[i0 + l] >> 1
+          const int city = band ? Oc[i0 + l] >> (ES - 1)
                                 : (int)a.tours[(size_t)pp * a.np + i0 + l];
           const unsigned char* src =
               a.rows + ((size_t)(l & 3) * n + city) * (size_t)a.line;
@@ -638,15 +647,15 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
     const int per = ((((n - cs) + NWg - 1) >> lgw) + 7) & ~7;
     const int cA = cs + wl * per, cB = min(n, cA + per);
     if (cA < cB && a.probe != 1) {
-      int prev = lds_s16(R + (uint32_t)O[3 + cA]);
+      int prev = lds_el<ES>(R + (uint32_t)O[3 + cA]);
       int c0 = cA;
       if (RPL == 1) {
         for (; c0 < cB && c0 < i0 + 32; c0 += 8)
-          band_group<MODE, true>(O, D, c0, R, prev, L, i, Di, live, a.win,
-                                 st, ws, &s_cmin[cb], S + 4u);
+          band_group<MODE, true, ES>(O, D, c0, R, prev, L, i, Di, live,
+                                     a.win, st, ws, &s_cmin[cb], S + 4u);
         for (; c0 < cB; c0 += 8)
-          band_group<MODE, false>(O, D, c0, R, prev, L, i, Di, live, a.win,
-                                  st, ws, &s_cmin[cb], S + 4u);
+          band_group<MODE, false, ES>(O, D, c0, R, prev, L, i, Di, live,
+                                      a.win, st, ws, &s_cmin[cb], S + 4u);
       } else {
         const uint32_t s32 = 32u * (S + 4u), s33 = s32 + S + 4u;
         int prev2 = lds_s16(R + s32 + (uint32_t)O[3 + cA]);
@@ -789,24 +798,26 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
   }
 }
 
-// 4 rotated int16 versions of round(C * scale): version q, row r is the
-// line at byte (q n + r) line; element c at byte 4q + 2c of it.
-__global__ void k_cost_band16(const double* cost, int64_t ld, int n,
-                              int16_t* out, int line, double scale,
-                              double vfrom, double vto) {
-  const int per = line / 2;
+// 4 rotated int16 (or int8) versions of round(C * scale): version q, row r
+// is the line at byte (q n + r) line; element c at byte 4q + es c of it.
+template <typename T>
+__global__ void k_cost_band(const double* cost, int64_t ld, int n, T* out,
+                            int line, double scale, double vfrom,
+                            double vto) {
+  constexpr int es = (int)sizeof(T);
+  const int per = line / es;
   const int64_t total = 4 * (int64_t)n * per;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = e / per;
     const int c = (int)(e % per);
     const int qv = (int)(row / n), r = (int)(row % n);
-    const int cc = c - 2 * qv;
-    int16_t v = 0;
+    const int cc = c - 4 / es * qv;
+    T v = 0;
     if (cc >= 0 && cc < n) {
       double x = cost[(int64_t)r * ld + cc];
       if (vfrom > 0.0 && x == vfrom) x = vto;
-      v = (int16_t)__double2int_rn(x * scale);
+      v = (T)__double2int_rn(x * scale);
     }
     out[e] = v;
   }
@@ -821,10 +832,6 @@ uint32_t band_slot(int line, bool g4) {
   return g4 ? (uint32_t)round_up(line + 112, 32) : (uint32_t)round_up(line, 128);
 }
 constexpr int kG4MaxBox = 2048;
-bool band_g4_fits(int n) {
-  return (int)band_slot((int)round_up(2 * (int64_t)n + 12, 16), true) <=
-         kG4MaxBox;
-}
 
 // bands of 32 rpl - 1 pair rows (rpl rows per lane)
 int band_nb(int n, int rpl) {
@@ -852,14 +859,41 @@ int band_groups(int n, int nst, int rpl) {
   return nst == 4 && band_nb(n, 1) >= 2 ? 2 : 1;
 }
 
-size_t band_smem(int n, int nst, bool g4, int rpl) {
-  const int line = band_line(n);
+int band_line_es(int n, int es) {
+  return (int)round_up((int64_t)es * n + 12, 16);
+}
+
+size_t band_smem_l(int line, int n, int nst, bool g4, int rpl) {
   return (size_t)nst * (32 * rpl * band_slot(line, g4) + 128 * rpl) +
          (size_t)band_ncb(n, nst, rpl) * 2 * band_cw(n) * 4 +
          (size_t)kBandWarps * kLaneState * 32 * 4 * rpl;
 }
 
 constexpr size_t kBandSmemMax = 225 * 1024;
+
+// row element size: int16 wherever two 32-slot stages of int16 rows fit
+// (n <= ~1400), else int8 (n <= ~2500); 0: no band scan.  DPSO_BAND_ES=1
+// forces int8 rows (testing at small n).
+int band_es(int n) {
+  if (n < 4 || n > kBandMaxN) return 0;
+  const bool fit2 =
+      band_smem_l(band_line_es(n, 2), n, 2, false, 1) <= kBandSmemMax;
+  const bool fit1 =
+      band_smem_l(band_line_es(n, 1), n, 2, false, 1) <= kBandSmemMax;
+  if (const char* e = getenv("DPSO_BAND_ES"))
+    if (atoi(e) == 1 && fit1) return 1;
+  return fit2 ? 2 : fit1 ? 1 : 0;
+}
+
+size_t band_smem(int n, int nst, bool g4, int rpl) {
+  return band_smem_l(band_line_es(n, std::max(1, band_es(n))), n, nst, g4,
+                     rpl);
+}
+
+bool band_g4_fits(int n) {
+  return (int)band_slot(band_line_es(n, std::max(1, band_es(n))), true) <=
+         kG4MaxBox;
+}
 
 // stages: as many as fit, up to kMaxStages
 int band_stages(int n, bool g4, int rpl) {
@@ -879,7 +913,9 @@ int band_stages(int n, bool g4, int rpl) {
 int band_rpl(int n, bool g4) {
   if (const char* e = getenv("DPSO_BAND_RPL"))
     if (atoi(e) == 1) return 1;
-  return n >= 64 && band_smem(n, 2, g4, 2) <= kBandSmemMax ? 2 : 1;
+  return n >= 64 && band_es(n) == 2 && band_smem(n, 2, g4, 2) <= kBandSmemMax
+             ? 2
+             : 1;
 }
 
 // The tensor map of the row versions for gather4: a 2-D tensor of 4n lines
@@ -917,13 +953,12 @@ bool band_encode_g4(const unsigned char* rows, int n, int line,
 
 }  // namespace
 
-int band_line(int n) { return (int)round_up(2 * (int64_t)n + 12, 16); }
+int band_line(int n) { return band_line_es(n, std::max(1, band_es(n))); }
 
 int band_cw(int n) { return (int)round_up(n + 16, 8); }
 
 int64_t band_rows_bytes(int n) {
-  if (n < 4 || n > kBandMaxN || band_smem(n, 2, false, 1) > kBandSmemMax)
-    return 0;
+  if (band_es(n) == 0) return 0;
   return 4 * (int64_t)n * band_line(n);
 }
 
@@ -948,26 +983,33 @@ cudaError_t band_prepare(const double* cost, int64_t ld, int32_t n,
       getenv("DPSO_SCAN_NPL"))
     return cudaSuccess;
   if (!(mx > 1e-30 && mx < 1e30)) return cudaSuccess;
+  const int es = band_es(n);
+  const double emax = es == 2 ? 32767.0 : 127.0;
   int mode;
   double scale = 1.0;
-  if (integral && mx <= 32767.0) {
+  if (integral && mx <= emax) {
     mode = 1;
   } else {
     mode = 2;
-    scale = ldexp(1.0, 14 - ilogb(mx));
-    while (mx * scale > 32767.0) scale *= 0.5;
+    scale = ldexp(1.0, (es == 2 ? 14 : 6) - ilogb(mx));
+    while (mx * scale > emax) scale *= 0.5;
   }
   // testing: FILTER on an EXACT-eligible matrix (same rows, scale 1)
   if (const char* e = getenv("DPSO_BAND_MODE")) mode = atoi(e) == 2 ? 2 : mode;
   const int line = band_line(n);
-  const int64_t total = 4 * (int64_t)n * (line / 2);
+  const int64_t total = 4 * (int64_t)n * (line / es);
   int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-  k_cost_band16<<<std::max(blocks, 1), 256, 0, s>>>(
-      cost, ld, n, (int16_t*)buf, line, scale, vfrom, vto);
+  if (es == 2)
+    k_cost_band<int16_t><<<std::max(blocks, 1), 256, 0, s>>>(
+        cost, ld, n, (int16_t*)buf, line, scale, vfrom, vto);
+  else
+    k_cost_band<int8_t><<<std::max(blocks, 1), 256, 0, s>>>(
+        cost, ld, n, (int8_t*)buf, line, scale, vfrom, vto);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
   pl->band = buf;
   pl->band_line = line;
+  pl->band_es = es;
   pl->band_mode = mode;
   pl->band_scale = scale;
   pl->band_win = mode == 2 ? 4 : 0;
@@ -976,6 +1018,7 @@ cudaError_t band_prepare(const double* cost, int64_t ld, int32_t n,
   bool g4 = band_g4_fits(n);
   if (const char* e = getenv("DPSO_BAND_G4")) g4 = g4 && atoi(e) != 0;
   pl->band_g4 = g4 && band_encode_g4(buf, n, line, pl->band_tm) ? 1 : 0;
+  pl->band_rpl = band_rpl(n, pl->band_g4 != 0);
   return cudaSuccess;
 }
 
@@ -1010,10 +1053,10 @@ cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
   a.cols = pl.band_cols;
   k_band_cols<<<count, 256, 0, s>>>(tours, np, dcache, n, a.cw, count,
                                      a.scale, a.vfrom, a.vto, pl.band_cols,
-                                     ctl);
+                                     ctl, pl.band_es);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
-  const int rpl = band_rpl(n, a.g4 != 0);
+  const int rpl = pl.band_rpl;
   a.nst = band_stages(n, a.g4 != 0, rpl);
   a.ncb = band_ncb(n, a.nst, rpl);
   a.groups = band_groups(n, a.nst, rpl);
@@ -1031,9 +1074,13 @@ cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
     kern<<<blocks, (kBandWarps + kProdWarps) * 32, smem, s>>>(a, tm);
     return cudaGetLastError();
   };
+  if (pl.band_es == 1)
+    return pl.band_mode == 1 ? go(k_two_opt_band<1, 1, 1>)
+                             : go(k_two_opt_band<2, 1, 1>);
   if (pl.band_mode == 1)
-    return rpl == 2 ? go(k_two_opt_band<1, 2>) : go(k_two_opt_band<1, 1>);
-  return rpl == 2 ? go(k_two_opt_band<2, 2>) : go(k_two_opt_band<2, 1>);
+    return rpl == 2 ? go(k_two_opt_band<1, 2, 2>)
+                    : go(k_two_opt_band<1, 1, 2>);
+  return rpl == 2 ? go(k_two_opt_band<2, 2, 2>) : go(k_two_opt_band<2, 1, 2>);
 }
 
 }  // namespace dpso

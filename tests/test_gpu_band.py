@@ -135,13 +135,14 @@ def test_band_asymmetric_negative_virtual(pkg):
 
 
 def test_band_largest_n(pkg):
-    # the largest n whose two stages fit shared memory, and the first n
-    # past it (column scan)
+    # the largest n whose two int16 stages fit shared memory, int8 rows past
+    # it (n <= 2548), the column scan past that
     rng = np.random.default_rng(29)
-    for n, kind in ((1000, 2), (1400, 2), (2000, 0)):
+    for n, kind in ((1000, 2), (1402, 2), (1403, 2), (2000, 2), (2548, 2),
+                    (2549, 0)):
         cost = random_euclidean_matrix(n, rng)
         assert band_kind(pkg, cost) == kind, n
-        check(pkg, cost, perms(rng, 300, n), ("large", n), 6, rng)
+        check(pkg, cost, perms(rng, 300, n), ("large", n), 4, rng)
     cost = np.floor(random_euclidean_matrix(1400, rng) * 1000.0)
     assert band_kind(pkg, cost) == 1
     check(pkg, cost, perms(rng, 300, 1400), ("large-int", 1400), 6, rng)
@@ -155,6 +156,37 @@ def test_band_more_particles_than_ctas(pkg):
         cost = np.floor(random_euclidean_matrix(n, rng) * 100.0)
         check(pkg, cost, perms(rng, P, n), ("multi", n, P), 64, rng)
         check(pkg, cost / 7.0, perms(rng, P, n), ("multi-f", n, P), 64, rng)
+
+
+@pytest.mark.parametrize("mode", ["exact", "filter"])
+def test_band_int8_rows(pkg, mode, monkeypatch):
+    # int8 rows (the default for 1402 < n <= 2548), forced at small n:
+    # EXACT for integer matrices with |C| <= 127, FILTER at scale 2^k <=
+    # 127 / max|C| otherwise; band edges, the overflow re-scan
+    monkeypatch.setenv("DPSO_BAND_ES", "1")
+    if mode == "filter":
+        monkeypatch.setenv("DPSO_BAND_MODE", "2")
+    rng = np.random.default_rng(59)
+    for n in (4, 5, 31, 32, 33, 62, 63, 64, 65, 100, 155, 257, 300):
+        cost = np.floor(random_euclidean_matrix(n, rng) * 80.0)  # <= 113
+        check(pkg, cost, perms(rng, 6, n), ("int8", mode, n))
+    for n, mul in ((200, 1.0), (200, 1e-6), (200, 1e9), (300, 3.7)):
+        cost = random_euclidean_matrix(n, rng) * mul
+        check(pkg, cost, perms(rng, 12, n), ("int8-scale", mode, n, mul))
+    check(pkg, grid(144) / 3.0, perms(rng, 12, 144), ("int8-lattice", mode))
+    v = np.floor(random_euclidean_matrix(257, rng) * 100.0)
+    mask = np.triu(rng.random((257, 257)) < 0.02, 1)
+    mask = mask | mask.T
+    v[mask] = 1e3 * 257 * v[~mask].max()
+    check(pkg, v, perms(rng, 8, 257), ("int8-virtual", mode))
+
+
+def test_band_int8_large_integer(pkg):
+    # n = 2000 integer costs above the int8 range: FILTER int8 rows
+    rng = np.random.default_rng(61)
+    cost = np.floor(random_euclidean_matrix(2000, rng) * 1000.0)
+    assert band_kind(pkg, cost) == 2
+    check(pkg, cost, perms(rng, 200, 2000), "int8-large-int", 4, rng)
 
 
 @pytest.mark.parametrize("rpl", ["2", "1"])
