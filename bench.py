@@ -24,6 +24,7 @@ reference CPU algorithm (oracle/dpso_oracle.py) on the host cores.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import math
 import os
@@ -294,21 +295,29 @@ def config_dict(cfg_name, cfg, args, world=1):
 
 
 # --------------------------------------------------------------- our arm
-def kernels_per_generation(cfg, band=0):
+def band_kernels(cfg, band):
+    """Kernels of one band-scan launch: column records + scan (+ the FILTER
+    overflow re-scan)."""
+    exact = (band == 1 if band else
+             cfg["matrix"] in ("grid", "euclid_int", "wall"))
+    return (2 if band else 1) + (0 if exact else 1)
+
+
+def kernels_per_generation(cfg, band=0, bound=0):
     """(kernels every generation's CUDA graph launches, extra kernels of a
     mutating generation).  Generations with gen % mutation_period != 0 run
     a graph without the mutation call; device flags make kernels a
     generation does not need (the 2-opt scan when gbest improved, ...) exit
     at entry, but they still launch.  band: dpso_scan_band (1/2: the band
-    scan and its column-record kernel)."""
+    scan and its column-record kernel).  bound: the bounded scan runs
+    first; the band scan launches after it every pass (it exits at once
+    when the bounded scan hands it no particle)."""
     k = 1 + 1 + 1  # gen_begin, update, fitness (with the pbest copy)
     k += 1         # select
     if cfg.get("ee", True):
-        exact = (band == 1 if band else
-                 cfg["matrix"] in ("grid", "euclid_int", "wall"))
-        # [column records +] scan (FILTER adds the overflow re-scan), apply,
+        # scan kernels (bounded scan, or the band / column scan), apply,
         # finalize
-        k += (2 if band else 1) + (0 if exact else 1)
+        k += (1 if bound else 0) + band_kernels(cfg, band)
         k += 2
     m = 6          # mutation: hash, rank, dedupe, verify, lists, copy
     if RNG == "philox":
@@ -319,8 +328,8 @@ def kernels_per_generation(cfg, band=0):
     return k, m
 
 
-def gpu_launch_count(cfg, first_gen, gens, period=3, band=0):
-    base, mut = kernels_per_generation(cfg, band)
+def gpu_launch_count(cfg, first_gen, gens, period=3, band=0, bound=0):
+    base, mut = kernels_per_generation(cfg, band, bound)
     n_mut = sum(1 for g in range(first_gen, first_gen + gens)
                 if g % period == 0)
     return base * gens + mut * n_mut
@@ -453,6 +462,12 @@ def run_ours(args, cfg_name, cfg):
     staging = int(ctx.lib.dpso_band_staging(ctx.h))
     band_line = int(ctx.lib.dpso_band_line(ctx.h))
     band_rows = int(ctx.lib.dpso_band_rows(ctx.h))
+    bound = max(0, int(ctx.lib.dpso_scan_bound(ctx.h)))
+
+    def bound_counters():
+        pr = ctypes.c_ulonglong(0)
+        ctx.lib.dpso_bound_pairs(ctx.h, ctypes.byref(pr))
+        return int(ctx.lib.dpso_band_runs(ctx.h)), int(pr.value)
     if RNG == "numpy":
         ctx.set_streams(numpy_stream_states(params["random_state"], P + 2))
     ctx.init(seed_body, n_seed)
@@ -461,6 +476,7 @@ def run_ours(args, cfg_name, cfg):
     ctx.step(W)
     torch.cuda.synchronize()
     scans0 = ctx.ctl()["two_opt_count"]
+    runs0, _ = bound_counters()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
     ev = [(torch.cuda.Event(enable_timing=True),
@@ -482,6 +498,7 @@ def run_ours(args, cfg_name, cfg):
     if world > 1:
         dist.barrier()
     scans_timed = ctx.ctl()["two_opt_count"] - scans0
+    runs_timed = bound_counters()[0] - runs0  # passes with band-scan work
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = sum(step_ms)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -493,9 +510,11 @@ def run_ours(args, cfg_name, cfg):
     # live per-phase kernel timing for the roofline (CUDA events on the
     # launching stream, same generations continued)
     c0 = ctx.ctl()
+    runs_p0, pairs_p0 = bound_counters()
     prof_gens = args.profile_gens
     phase_ms, cnt = ctx.step_timed(prof_gens)
     fired = cnt - c0["two_opt_count"]
+    runs_p1, pairs_p1 = bound_counters()
     names = ["update", "mutation", "select", "two_opt_scan", "two_opt_apply",
              "finalize"]
     phases = {k: v / prof_gens for k, v in zip(names, phase_ms)}
@@ -569,7 +588,43 @@ def run_ours(args, cfg_name, cfg):
             tr = json.load(fh)
     except Exception:
         tr = {}
-    if cfg.get("ee", True) and fired > 0:
+    if cfg.get("ee", True) and fired > 0 and bound:
+        # the bounded scan (k_two_opt_bound.cu): per particle it reads the
+        # tour (2 B/row), d (8 B/row) and the two end points' row/column
+        # minima (2 x 16 B/row, an L1-resident table), then gathers two fp64
+        # entries per evaluated pair from the L2-resident matrix; random
+        # 8-B gathers from L2 are its binding resource
+        dom, dur_ms = "two_opt_scan", phase_ms[3] / fired
+        traffic = tr.get(f"{cfg_name}:two_opt_bound")
+        pairs = (pairs_p1 - pairs_p0) / fired
+        rows_b = float(P) * n * (2 + 8 + 32)
+        alg = rows_b + 16.0 * pairs
+        peak = gpk.get("gather_f64_8MB", {}).get("useful_gbs")
+        achieved = alg / (dur_ms / 1e3) / 1e9
+        roof = {"bound": "l2", "kernel": "two_opt_scan (bounded)",
+                "scan": "bounded (exact pair bound) + band fallback",
+                "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if peak else None,
+                "traffic": traffic,
+                "algorithmic_bytes_per_launch": alg,
+                "pairs_evaluated_per_launch": pairs,
+                "pairs_total_per_launch": P * n * (n - 1) / 2.0,
+                "pair_fraction": pairs / (P * n * (n - 1) / 2.0),
+                "band_fallback_passes": f"{runs_p1 - runs_p0}/{fired}",
+                "band_fallback_passes_timed": f"{runs_timed}/{scans_timed}",
+                "full_scan_equivalent_fp64_gbs":
+                    scan_alg / (dur_ms / 1e3) / 1e9,
+                "avg_launch_ms": dur_ms,
+                "peak_source": "measured: random fp64 gathers from an "
+                               "8-32 MB L2-resident table (profiles/r02/"
+                               "gather_peaks.json, tools/gather_peaks.cu)",
+                "note": "exact pruning: delta(i,j) >= -(h_i + h_j) skips "
+                        "every pair that cannot reach the best delta found "
+                        "so far; the rest are evaluated in fp64 (the "
+                        "reference's argmin bit for bit).  The scan phase "
+                        "includes the band scan launch for the particles it "
+                        "hands over (empty in most passes)"}
+    elif cfg.get("ee", True) and fired > 0:
         dom, dur_ms = "two_opt_scan", phase_ms[3] / fired
         traffic = tr.get(f"{cfg_name}:{dom}")
         # the binding resource of the scan: the cost rows it stages from L2
@@ -656,14 +711,16 @@ def run_ours(args, cfg_name, cfg):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": config_dict(cfg_name, cfg, args, world),
-        "gpu_launches": gpu_launch_count(cfg, W + 1, K, band=band),
+        "gpu_launches": gpu_launch_count(cfg, W + 1, K, band=band,
+                                         bound=bound),
         "roofline": roof,
         "phase_ms_per_gen": phases,
         "two_opt_fired": f"{fired}/{prof_gens}",
         "two_opt_scans_timed": f"{scans_timed}/{K}",
     }
     # the scan's own floor, live (the same launch reduced to its row stream)
-    if cfg.get("ee", True) and world == 1 and dom == "two_opt_scan":
+    if cfg.get("ee", True) and world == 1 and dom == "two_opt_scan" \
+            and not bound:
         try:
             fl = scan_floors(cost, params, seed_body, n_seed, P, band=band)
             if fl.get("stream_only_ms"):

@@ -98,6 +98,26 @@ int dpso_scan_rows_bytes(dpso_ctx* ctx);
  * column scan's knobs, selects 0 (testing). */
 int dpso_scan_band(dpso_ctx* ctx);
 
+/* 1 when the bounded 2-opt scan runs first (a finite matrix with the band
+ * scan available): every particle's pairs are pruned by an exact lower
+ * bound, the band scan takes only the particles whose bound is weak.
+ * Diagnostic; DPSO_BOUND=0 turns it off. */
+int dpso_scan_bound(dpso_ctx* ctx);
+
+/* Particles the bounded scan handed to the band scan in the last 2-opt
+ * pass (-1: no bounded scan).  Synchronizes the context's stream. */
+int dpso_bound_fallbacks(dpso_ctx* ctx);
+
+/* 2-opt passes in which the bounded scan handed the band scan at least one
+ * particle, since the context was created.  Synchronizes the context's
+ * stream.  Diagnostic. */
+int dpso_band_runs(dpso_ctx* ctx);
+
+/* Pairs the bounded scan evaluated in fp64 since the context was created
+ * (0 without a bounded scan).  Synchronizes the context's stream.
+ * Diagnostic (the bench's gathered-byte count). */
+int dpso_bound_pairs(dpso_ctx* ctx, unsigned long long* out);
+
 /* How the band scan stages its rows: 2 = TMA gather4 (four rows per copy,
  * n <= ~960), 1 = one bulk copy per row, 0 = no band scan.  Diagnostic. */
 int dpso_band_staging(dpso_ctx* ctx);

@@ -53,6 +53,10 @@ _SIG = {
     "dpso_scan_rows_bytes": (_I32, [_P]),
     "dpso_scan_band": (_I32, [_P]),
     "dpso_band_staging": (_I32, [_P]),
+    "dpso_scan_bound": (_I32, [_P]),
+    "dpso_bound_fallbacks": (_I32, [_P]),
+    "dpso_band_runs": (_I32, [_P]),
+    "dpso_bound_pairs": (_I32, [_P, _P]),
     "dpso_band_line": (_I32, [_P]),
     "dpso_band_rows": (_I32, [_P]),
     "dpso_step_timed": (_I32, [_P, _I32, _P, _P]),

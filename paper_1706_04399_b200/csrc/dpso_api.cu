@@ -70,7 +70,7 @@ struct Layout {
       off_sidx, off_order, off_surv, off_keep, off_ev_slot, off_ev_k,
       off_ev_cursor, off_ev_end, off_ev_idx, off_mstream, off_init_buf,
       off_init_state, off_init_cursor, off_init_aux, off_init_anchor, off_seed, off_cost32,
-      off_stats, off_band_cols, total;
+      off_stats, off_band_cols, off_bound, total;
   int64_t vel_cap;
   int chunks;
 };
@@ -154,6 +154,7 @@ Layout make_layout(const dpso_params* prm, int n) {
   L.off_stats = take(sizeof(CostStats));
   L.off_band_cols =
       take(prm->use_edge_exchange ? band_cols_bytes(n, P) : 0);
+  L.off_bound = take(prm->use_edge_exchange ? bound_bytes(n, P) : 0);
   L.total = o;
   return L;
 }
@@ -611,8 +612,11 @@ int dpso_set_cost(dpso_ctx* c, const double* dev_cost, int64_t ld) {
                               ? (unsigned char*)c32 +
                                     round_up(6 * (int64_t)c->n * c->v.np, 256)
                               : nullptr;
+    void* bbuf = bound_bytes(c->n, c->prm.n_particles)
+                     ? (void*)(c->ws + c->L.off_bound)
+                     : nullptr;
     CK(two_opt_prepare(dev_cost, ld, c->n, c->v.np, c32, c16, band, st,
-                       c->stream, &pl));
+                       c->stream, &pl, bbuf));
     pl.band_cols = (int32_t*)(c->ws + c->L.off_band_cols);
     pl.band_cols_cap = c->prm.n_particles;
   }
@@ -631,6 +635,40 @@ int dpso_set_cost(dpso_ctx* c, const double* dev_cost, int64_t ld) {
 int dpso_scan_mode(dpso_ctx* c) { return c ? c->v.plan.mode : -1; }
 
 int dpso_scan_band(dpso_ctx* c) { return c ? c->v.plan.band_mode : -1; }
+
+int dpso_scan_bound(dpso_ctx* c) { return c ? c->v.plan.bound : -1; }
+
+int dpso_band_runs(dpso_ctx* c) {
+  if (!c) return -1;
+  DevGuard g_(c->dev);
+  if (cudaMemcpyAsync(c->host_ctl, c->v.ctl, sizeof(DevCtl),
+                      cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess)
+    return -1;
+  return c->host_ctl->band_runs;
+}
+
+int dpso_bound_pairs(dpso_ctx* c, unsigned long long* out) {
+  if (!c || !out) return fail(DPSO_EINVAL, "bad arguments");
+  *out = 0;
+  if (!c->v.plan.bound) return DPSO_OK;
+  DevGuard g_(c->dev);
+  CK(cudaMemcpyAsync(out, c->v.plan.bound_pairs, 8, cudaMemcpyDeviceToHost,
+                     c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return DPSO_OK;
+}
+
+int dpso_bound_fallbacks(dpso_ctx* c) {
+  if (!c || !c->v.plan.bound) return -1;
+  DevGuard g_(c->dev);
+  int32_t v = 0;
+  if (cudaMemcpyAsync(&v, c->v.plan.bound_fb, 4, cudaMemcpyDeviceToHost,
+                      c->stream) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess)
+    return -1;
+  return v;
+}
 
 int dpso_band_line(dpso_ctx* c) {
   if (!c) return -1;
@@ -1247,7 +1285,8 @@ int dpso_best_exchange_batch(const double* dev_cost, int64_t ld, int32_t n,
                  // fp32 + fp16 rows, band rows, stats, band column arrays
                  round_up(round_up(6 * (int64_t)n * np, 256) +
                               band_rows_bytes(n), 256) +
-                 256 + round_up(band_cols_bytes(n, cnt), 256);
+                 256 + round_up(band_cols_bytes(n, cnt), 256) +
+                 round_up(bound_bytes(n, cnt), 256);
   unsigned char* tmp = nullptr;
   CK(cudaMallocAsync(&tmp, bytes, s));
   size_t o = 0;
@@ -1266,6 +1305,7 @@ int dpso_best_exchange_batch(const double* dev_cost, int64_t ld, int32_t n,
                             band_rows_bytes(n));
   CostStats* st = (CostStats*)take(sizeof(CostStats));
   int32_t* bcols = (int32_t*)take(band_cols_bytes(n, cnt));
+  void* bbuf = bound_bytes(n, cnt) ? take(bound_bytes(n, cnt)) : nullptr;
   CK(cudaMemcpyAsync(ctab, tab.data(), 16 * chunks,
                      cudaMemcpyHostToDevice, s));
   int rc = to_u16_tours(dev_tours, n, count, t16, np, s);
@@ -1277,7 +1317,8 @@ int dpso_best_exchange_batch(const double* dev_cost, int64_t ld, int32_t n,
           ? (unsigned char*)c32 + round_up(6 * (int64_t)n * np, 256)
           : nullptr;
   CK(two_opt_prepare(dev_cost, ld, n, np, c32,
-                     (uint16_t*)(c32 + (size_t)n * np), band, st, s, &pl));
+                     (uint16_t*)(c32 + (size_t)n * np), band, st, s, &pl,
+                     bbuf));
   pl.band_cols = bcols;
   pl.band_cols_cap = cnt;
   CK(launch_two_opt_batch(pl, n, (int32_t)np, t16, dc, count, res, chunks,

@@ -51,6 +51,7 @@ struct DevCtl {
   int32_t mut_overflow;   // stream buffer too short (exact fallback)
   int32_t mut_cur;        // parity of the event buffers of the current call
   int32_t mut_pending;    // the next call's stream walk is still to run
+  int32_t band_runs;      // 2-opt passes that handed the band scan work
   uint64_t mut_q;     // u32 draws consumed by the current mutation call
 };
 
@@ -104,6 +105,14 @@ struct TwoOptPlan {
   // versions (a 2-D tensor of 4n lines), 0 = one bulk copy per row
   int band_g4;
   unsigned char band_tm[128];
+  // Bounded scan (k_two_opt_bound.cu): per-city off-diagonal row / column
+  // minima, the fallback particle list ([0] count, [1..] particles) and the
+  // rounding slack of the pair bound.  bound == 0: not used.
+  int bound;
+  const double2* bound_cmn;
+  int32_t* bound_fb;
+  unsigned long long* bound_pairs;  // pairs evaluated (cumulative)
+  double bound_slack;
 };
 
 struct TwoOptRes {
@@ -225,7 +234,8 @@ int two_opt_mode(const CostStats& st, int n, float* thr);
 cudaError_t two_opt_prepare(const double* cost, int64_t ld, int32_t n,
                             int64_t np, float* c32, uint16_t* c16,
                             unsigned char* band, CostStats* st,
-                            cudaStream_t s, TwoOptPlan* pl);
+                            cudaStream_t s, TwoOptPlan* pl,
+                            void* bound_buf = nullptr);
 cudaError_t launch_nn(const double* cost, int64_t ld, int32_t n, int32_t start,
                       int32_t* out, cudaStream_t s);
 cudaError_t launch_pysum_tour(const double* cost, int64_t ld, int32_t n,
@@ -262,7 +272,21 @@ cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
                                 const uint16_t* tours, const double* dcache,
                                 int32_t count, TwoOptRes* res, int32_t chunks,
                                 int32_t* ovf, const DevCtl* ctl,
-                                cudaStream_t s, int reserve_sms = 0);
+                                cudaStream_t s, int reserve_sms = 0,
+                                const int32_t* plist = nullptr,
+                                const int32_t* pcnt = nullptr,
+                                int32_t* runs = nullptr);
+// bounded scan (k_two_opt_bound.cu): workspace bytes for count particles
+// (0: not available at this n), preparation (needs the band plan), launch
+constexpr int kBoundMaxN = kBandMaxN;
+int64_t bound_bytes(int n, int64_t count);
+cudaError_t bound_prepare(const double* cost, int64_t ld, int32_t n,
+                          void* buf, double maxabs, cudaStream_t s,
+                          TwoOptPlan* pl);
+cudaError_t launch_two_opt_bound(const TwoOptPlan& pl, int32_t n, int32_t np,
+                                 const uint16_t* tours, const double* dcache,
+                                 int32_t count, TwoOptRes* res, int32_t chunks,
+                                 const DevCtl* ctl, cudaStream_t s);
 int two_opt_pick_chunks(int32_t n, int32_t P);
 
 // A random fp64 gather from the cost matrix (edge costs C[a][b]).  sm_100

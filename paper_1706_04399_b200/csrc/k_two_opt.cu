@@ -1063,7 +1063,7 @@ int two_opt_mode(const CostStats& st, int n, float* thr) {
 cudaError_t two_opt_prepare(const double* cost, int64_t ld, int32_t n,
                             int64_t np, float* c32, uint16_t* c16,
                             unsigned char* band, CostStats* st,
-                            cudaStream_t s, TwoOptPlan* pl) {
+                            cudaStream_t s, TwoOptPlan* pl, void* bound_buf) {
   memset(pl, 0, sizeof *pl);
   pl->cost = cost;
   pl->ld = ld;
@@ -1082,6 +1082,8 @@ cudaError_t two_opt_prepare(const double* cost, int64_t ld, int32_t n,
   if (!e) e = cudaMemcpyAsync(&h, st, sizeof h, cudaMemcpyDeviceToHost, s);
   if (!e) e = cudaStreamSynchronize(s);
   if (e) return e;
+  double maxabs_raw;
+  memcpy(&maxabs_raw, &h.maxabs_bits, sizeof maxabs_raw);
   {
     // a virtual level (entries equal to max|C|, > 64 x every other |C|):
     // cap it at 5 x the finite maximum in the fp32/fp16 rows (> the spread
@@ -1106,6 +1108,8 @@ cudaError_t two_opt_prepare(const double* cost, int64_t ld, int32_t n,
     memcpy(&mxc, &h.maxabs_bits, sizeof mxc);
     e = band_prepare(cost, ld, n, band, mxc, !h.nonintegral, pl->vfrom,
                      pl->vto, s, pl);
+    if (e) return e;
+    e = bound_prepare(cost, ld, n, bound_buf, maxabs_raw, s, pl);
     if (e) return e;
   }
   pl->mode = two_opt_mode(h, n, &pl->thr);
@@ -1295,12 +1299,23 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
     if (pl.band_mode) {
       // row-per-lane band scan (k_two_opt_band.cu), then the FILTER
       // overflow re-scan over the listed chunk tasks
-      if (pl.band_mode == 2) e = cudaMemsetAsync(a.ovf, 0, 4, s);
-      if (!e && getenv("DPSO_BAND_DEBUG"))  // unwritten results read as NaN
+      if (getenv("DPSO_BAND_DEBUG"))  // unwritten results read as NaN
         e = cudaMemsetAsync(res, 0xFF, sizeof(TwoOptRes) * count * chunks, s);
+      // bounded scan first; the band scan takes the particles it lists (a
+      // launch that exits at once when the list is empty: measured as fast
+      // as a conditional graph node around it, which ncu cannot profile)
+      const bool bound = pl.bound != 0;
+      if (!e && bound)
+        e = launch_two_opt_bound(pl, n, np, tours, dcache, count, res, chunks,
+                                 ctl, s);
+      int32_t* runs =
+          ctl ? &const_cast<DevCtl*>(ctl)->band_runs : nullptr;
+      if (!e && pl.band_mode == 2) e = cudaMemsetAsync(a.ovf, 0, 4, s);
       if (!e)
         e = launch_two_opt_band(pl, n, np, tours, dcache, count, res, chunks,
-                                a.ovf, ctl, s, reserve_sms);
+                                a.ovf, ctl, s, reserve_sms,
+                                bound ? pl.bound_fb + 1 : nullptr,
+                                bound ? pl.bound_fb : nullptr, runs);
       if (!e && pl.band_mode == 2) {
         k_two_opt_rescan64<<<2 * 148, 128, 0, s>>>(a);
         e = cudaGetLastError();

@@ -111,6 +111,10 @@ struct BandArgs {
                         // 2 = scan, but copy rows only into the first nst
                         // bands (later bands reuse them: consumer floor)
   int g4;               // rows staged by TMA gather4 (4 rows per copy)
+  // particle list (the bounded scan's fallbacks): particles plist[0 ..
+  // *pcnt - 1] instead of 0 .. count - 1; null = all
+  const int32_t* plist;
+  const int32_t* pcnt;
 };
 
 __device__ __forceinline__ int lds_s16(uint32_t addr) {
@@ -273,10 +277,15 @@ __device__ __noinline__ int band_hit(int u0, int u1, int u2, int u3, int u4,
 __global__ void k_band_cols(const uint16_t* tours, int np,
                             const double* dcache, int n, int cw, int count,
                             double scale, double vfrom, double vto,
-                            int32_t* out, const DevCtl* ctl, int es) {
+                            int32_t* out, const DevCtl* ctl, int es,
+                            const int32_t* plist, const int32_t* pcnt,
+                            int32_t* runs) {
   if (ctl && (ctl->done || ctl->improved)) return;  // no scan this time
-  const int p = blockIdx.x;
-  if (p >= count) return;
+  const int q = blockIdx.x;
+  const int cnt = pcnt ? *pcnt : count;
+  if (runs && q == 0 && threadIdx.x == 0 && cnt > 0) atomicAdd(runs, 1);
+  if (q >= cnt) return;
+  const int p = plist ? plist[q] : q;
   const uint16_t* t = tours + (size_t)p * np;
   const double* dg = dcache + (size_t)p * np;
   int32_t* O = out + (size_t)p * 2 * cw;
@@ -440,9 +449,10 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
   constexpr int NW = kBandWarps;
   const int n = a.n, nst = a.nst, ncb = a.ncb;
   const int nb = (n + kRows - 2) / kRows;  // bands: rows 0 .. n-2
+  const int count = a.pcnt ? *a.pcnt : a.count;
   const int nmine =
-      (int)blockIdx.x < a.count ? (a.count - 1 - (int)blockIdx.x) / gridDim.x + 1
-                                : 0;
+      (int)blockIdx.x < count ? (count - 1 - (int)blockIdx.x) / gridDim.x + 1
+                              : 0;
   if (nmine == 0) return;
   const int total = nmine * nb;
   const uint32_t S = a.slot;
@@ -479,7 +489,8 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
       // global load ahead of every copy
       if (band == 1) mbar_wait_backoff(&colfull[cb], (uint32_t)(cuse & 1));
       const int* Oc = cols + cb * 2 * a.cw + 3;
-      const int pp = (int)blockIdx.x + pl * (int)gridDim.x;
+      const int pq = (int)blockIdx.x + pl * (int)gridDim.x;
+      const int pp = a.plist ? a.plist[pq] : pq;
       const int i0 = band * kRows;  // kRows pair rows per band
       const int r0 = rpp * pw;
       const int nr = max(0, min(rpp, n - i0 - r0));
@@ -621,7 +632,8 @@ __global__ void __launch_bounds__((kBandWarps + kProdWarps) * 32, 1)
   const uint32_t colfull_a = smem_u32(colfull);
   const uint32_t R0 = smem_u32(rowbuf) + (uint32_t)lane * (S + 4u);
   for (int t = grp; t < total; t += G) {
-    const int pp = (int)blockIdx.x + pl * (int)gridDim.x;
+    const int pq = (int)blockIdx.x + pl * (int)gridDim.x;
+    const int pp = a.plist ? a.plist[pq] : pq;
     const int i0 = band * kRows;
     // the particle's column arrays (its first band for this warp), rows
     if (band < G) mbar_wait_sleep_u32(colfull_a + 8u * cb, (uint32_t)(cuse & 1));
@@ -1026,7 +1038,9 @@ cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
                                 const uint16_t* tours, const double* dcache,
                                 int32_t count, TwoOptRes* res, int32_t chunks,
                                 int32_t* ovf, const DevCtl* ctl,
-                                cudaStream_t s, int reserve_sms) {
+                                cudaStream_t s, int reserve_sms,
+                                const int32_t* plist, const int32_t* pcnt,
+                                int32_t* runs) {
   if (!pl.band_cols || count > pl.band_cols_cap) return cudaErrorInvalidValue;
   BandArgs a;
   memset(&a, 0, sizeof a);
@@ -1051,9 +1065,11 @@ cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
   a.win = pl.band_win;
   a.cw = band_cw(n);
   a.cols = pl.band_cols;
+  a.plist = plist;
+  a.pcnt = pcnt;
   k_band_cols<<<count, 256, 0, s>>>(tours, np, dcache, n, a.cw, count,
                                      a.scale, a.vfrom, a.vto, pl.band_cols,
-                                     ctl, pl.band_es);
+                                     ctl, pl.band_es, plist, pcnt, runs);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
   const int rpl = pl.band_rpl;

@@ -1,0 +1,564 @@
+// Bounded best-improvement 2-opt scan: the reference's argmin
+// (solver.py:88-106) without visiting every pair.
+//
+// delta(i, j) = ((C[a_i,a_j] + C[s_i,s_j]) - d_i) - d_j over i < j, first
+// row-major argmin, applied when < -1e-12.
+//
+// Bound.  With r(c) = min_{b != c} C[c][b] and q(c) = min_{b != c} C[b][c]
+// (off-diagonal row / column minima, once per matrix), every pair has
+//     C[a_i,a_j] + C[s_i,s_j] >= (r(a_i) + q(a_j) + r(s_i) + q(s_j)) / 2
+//                              >= m_i + m_j,
+//     m_k = min((r(a_k) + r(s_k)) / 2, (q(a_k) + q(s_k)) / 2),
+// so delta(i, j) >= -(h_i + h_j) with h_k = d_k - m_k (the excess of edge k
+// over its end points' cheapest edges).  A pair with h_i + h_j < -T can
+// only have delta > T.
+//
+// Exactness.  Let T be the computed delta of some pair and Tq = min(T,
+// -1e-12).  If the reference's minimum m is < -1e-12 then m <= Tq, so every
+// pair achieving m has h_i + h_j >= -Tq and is evaluated here with the
+// reference expression in fp64: the lexicographic (delta, i, j) minimum
+// over the evaluated pairs is the reference's argmin, bit for bit.  If
+// m >= -1e-12 the reference makes no move, and neither does the apply (the
+// evaluated minimum is >= m).  The h values are rounded up to fp32 and the
+// threshold -Tq - slack down (slack = 2^-40 max|C|, far above the fp64
+// rounding of h and delta), so every skip is conservative.
+//
+// Per particle (one CTA of 256 threads): the tour and d (dcache) in shared
+// memory, h over the tour, the row of largest h of each 8 threads (32 seed
+// rows among the longest edges) and their 496 pairs give T; then R = {i : h_i + max h >= -Tq} (every surviving pair has both rows in
+// R) and its pairs with h_i + h_j >= -Tq.  The tours the swarm scans are
+// far from 2-opt optimal: at C2 |R| is ~50 of 1000 rows and ~200 of the
+// 499,500 pairs survive.  A particle with |R| above the list capacity (a
+// near-2-opt-optimal tour: the bound is weak) goes to the row-per-lane
+// band scan (k_two_opt_band.cu) through a particle list.
+#include <float.h>
+#include <limits.h>
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "dpso_internal.cuh"
+
+namespace dpso {
+
+namespace {
+
+constexpr int kBoundThreads = 256;  // one CTA per particle
+constexpr int kSeedRows = 32;       // seed rows (one per 8 threads)
+constexpr int kPairCap = 256;       // pair-list entries per warp
+constexpr int kMaxPeel = 64;        // rows peeled before the band fallback
+constexpr size_t kBoundSmem = 200 * 1024;
+
+struct BoundArgs {
+  const double* cost;
+  int64_t ld;
+  const double2* cmn;  // per city {r(c), q(c)}
+  int n, np, count, chunks;
+  const uint16_t* tours;
+  const double* dcache;
+  TwoOptRes* res;
+  const DevCtl* ctl;
+  int32_t* fb;  // [0] count, [1..] particles for the band scan
+  unsigned long long* pairs;  // pairs evaluated (cumulative, diagnostic)
+  double slack;
+  int rmax;     // row-list capacity
+  int maxpeel;  // rows peeled before the band fallback
+  uint32_t off_d, off_h, off_pos, off_lh, off_pairs;  // shared memory
+};
+
+__device__ __forceinline__ bool lex_less(double d1, int i1, int j1, double d2,
+                                         int i2, int j2) {
+  if (d1 < d2) return true;
+  if (d2 < d1) return false;
+  return (i1 < i2) || (i1 == i2 && j1 < j2);
+}
+
+__device__ __forceinline__ void warp_lexmin(double& d, int& i, int& j) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double d2 = __shfl_xor_sync(0xffffffffu, d, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, i, o);
+    const int j2 = __shfl_xor_sync(0xffffffffu, j, o);
+    if (lex_less(d2, i2, j2, d, i, j)) {
+      d = d2;
+      i = i2;
+      j = j2;
+    }
+  }
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Evaluate a warp's pair list: tour-position pairs x | y << 16, with the
+// reference expression in fp64, folded into the lane's (delta, i, j)
+// minimum; U pairs per lane in flight (2 U independent gathers).
+template <int U>
+__device__ __forceinline__ void eval_list(const BoundArgs& a, int np,
+                                          const uint32_t* pr,
+                                          const uint16_t* tr,
+                                          const double* dd, int lane,
+                                          double& bd, int& bi, int& bj,
+                                          int& evals) {
+  evals += np;  // warp-uniform: counted once per warp (lane 0)
+  for (int q0 = 0; q0 < np; q0 += 32 * U) {
+    double A[U], B[U], di[U], dj[U];
+    int I[U], J[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int q = q0 + 32 * k + lane;
+      I[k] = -1;
+      if (q < np) {
+        const uint32_t uv = pr[q];
+        const int pu = (int)(uv & 0xffffu), pv = (int)(uv >> 16);
+        const int i = min(pu, pv), j = max(pu, pv);
+        I[k] = i;
+        J[k] = j;
+        di[k] = dd[i];
+        dj[k] = dd[j];
+        A[k] = ld_cost(a.cost + (size_t)tr[i] * a.ld + tr[j]);
+        B[k] = ld_cost(a.cost + (size_t)tr[i + 1] * a.ld + tr[j + 1]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      if (I[k] < 0) continue;
+      double t = __dadd_rn(A[k], B[k]);
+      t = __dsub_rn(t, di[k]);
+      t = __dsub_rn(t, dj[k]);
+      if (lex_less(t, I[k], J[k], bd, bi, bj)) {
+        bd = t;
+        bi = I[k];
+        bj = J[k];
+      }
+    }
+  }
+}
+
+// CTA-wide lexicographic minimum (every thread gets it).
+__device__ __forceinline__ void cta_lexmin(double& d, int& i, int& j,
+                                           double* rd, int* ri, int* rj,
+                                           int lane, int warp, int nw) {
+  warp_lexmin(d, i, j);
+  if (lane == 0) {
+    rd[warp] = d;
+    ri[warp] = i;
+    rj[warp] = j;
+  }
+  __syncthreads();
+  for (int w = 0; w < nw; ++w)
+    if (lex_less(rd[w], ri[w], rj[w], d, i, j)) {
+      d = rd[w];
+      i = ri[w];
+      j = rj[w];
+    }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kBoundThreads)
+    k_two_opt_bound(BoundArgs a) {
+  if (a.ctl && (a.ctl->done || a.ctl->improved)) return;  // no scan
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double s_rd[kBoundThreads / 32];
+  __shared__ int s_ri[kBoundThreads / 32], s_rj[kBoundThreads / 32];
+  __shared__ float s_hmax[kBoundThreads / 32];
+  __shared__ int s_cnt;
+  constexpr int NW = kBoundThreads / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int p = blockIdx.x;
+  if (p >= a.count) return;
+  const int n = a.n;
+  const unsigned below = lanemask_lt();
+  uint16_t* tr = reinterpret_cast<uint16_t*>(smem);  // tour, tr[n] = tr[0]
+  double* dd = reinterpret_cast<double*>(smem + a.off_d);
+  float* hv = reinterpret_cast<float*>(smem + a.off_h);
+  int* lpos = reinterpret_cast<int*>(smem + a.off_pos);
+  float* lh = reinterpret_cast<float*>(smem + a.off_lh);
+  uint32_t* pr = reinterpret_cast<uint32_t*>(smem + a.off_pairs) +
+                 warp * kPairCap;
+  const uint16_t* tour = a.tours + (size_t)p * a.np;
+  const double* dg = a.dcache + (size_t)p * a.np;
+
+  // ---- the tour and its edge costs in shared memory
+  for (int i0 = 0; i0 < n; i0 += 4 * kBoundThreads) {
+    uint16_t t[4];
+    double d[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = i0 + k * kBoundThreads + tid;
+      if (i < n) {
+        t[k] = tour[i];
+        d[k] = dg[i];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = i0 + k * kBoundThreads + tid;
+      if (i < n) {
+        tr[i] = t[k];
+        dd[i] = d[k];
+      }
+    }
+  }
+  if (tid == 0) {
+    tr[n] = tour[0];
+    s_cnt = 0;
+  }
+  __syncthreads();
+
+  // ---- h_i (rounded up to fp32); the thread's largest
+  float lmax = -FLT_MAX;
+  int larg = -1;
+  for (int i0 = 0; i0 < n; i0 += 4 * kBoundThreads) {
+    double2 ra[4], rb[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = i0 + k * kBoundThreads + tid;
+      if (i < n) {
+        ra[k] = a.cmn[tr[i]];
+        rb[k] = a.cmn[tr[i + 1]];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = i0 + k * kBoundThreads + tid;
+      if (i < n) {
+        const double f = 0.5 * (ra[k].x + rb[k].x);
+        const double g = 0.5 * (ra[k].y + rb[k].y);
+        const float h = __double2float_ru(dd[i] - fmin(f, g));
+        hv[i] = h;
+        if (larg < 0 || h > lmax) {
+          lmax = h;
+          larg = i;
+        }
+      }
+    }
+  }
+  // seed rows: the largest h of each group of 8 threads (32 seeds among
+  // the longest edges; any rows give a valid threshold, long edges a tight
+  // one), and the maximum over the tour
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, lmax, o);
+    const int a2 = __shfl_xor_sync(0xffffffffu, larg, o);
+    if (a2 >= 0 && (larg < 0 || m2 > lmax)) {
+      lmax = m2;
+      larg = a2;
+    }
+  }
+  if ((lane & 7) == 0) lpos[warp * 4 + (lane >> 3)] = larg;
+  float hm = lmax;
+#pragma unroll
+  for (int o = 8; o < 32; o <<= 1)
+    hm = fmaxf(hm, __shfl_xor_sync(0xffffffffu, hm, o));
+  if (lane == 0) s_hmax[warp] = hm;
+  __syncthreads();
+  float hmax = s_hmax[0];
+  for (int w = 1; w < NW; ++w) hmax = fmaxf(hmax, s_hmax[w]);
+
+  // ---- the seed rows' pairs (496 for 32 seeds)
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  double bd = kInf;
+  int bi = INT_MAX, bj = INT_MAX;
+  int sv = 0;  // seed pairs this thread evaluated
+  {
+    constexpr int S = 4 * NW;
+    constexpr int NP = S * (S - 1) / 2;
+    double A[2], B[2], di[2], dj[2];
+    int I[2], J[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int q = tid + k * kBoundThreads;
+      I[k] = -1;
+      if (q < NP) {
+        // q -> (u, v), u < v: v (v - 1) / 2 <= q < v (v + 1) / 2
+        int v = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)q)) * 0.5f);
+        while (v * (v - 1) / 2 > q) --v;
+        while ((v + 1) * v / 2 <= q) ++v;
+        const int u = q - v * (v - 1) / 2;
+        const int pu = lpos[u], pv = lpos[v];
+        if (pu >= 0 && pv >= 0) {
+          const int i = min(pu, pv), j = max(pu, pv);
+          I[k] = i;
+          J[k] = j;
+          di[k] = dd[i];
+          dj[k] = dd[j];
+          A[k] = ld_cost(a.cost + (size_t)tr[i] * a.ld + tr[j]);
+          B[k] = ld_cost(a.cost + (size_t)tr[i + 1] * a.ld + tr[j + 1]);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (I[k] < 0) continue;
+      ++sv;
+      double t = __dadd_rn(A[k], B[k]);
+      t = __dsub_rn(t, di[k]);
+      t = __dsub_rn(t, dj[k]);
+      if (lex_less(t, I[k], J[k], bd, bi, bj)) {
+        bd = t;
+        bi = I[k];
+        bj = J[k];
+      }
+    }
+  }
+  double t0 = bd;
+  int ti = bi, tj = bj;
+  cta_lexmin(t0, ti, tj, s_rd, s_ri, s_rj, lane, warp, NW);
+  const double tq = fmin(t0, -1e-12);
+  // skip a pair iff h_i + h_j (rounded up) < thr <= -tq - slack
+  const float thr = __double2float_rd(__dsub_rd(-tq, a.slack));
+
+  int np = 0, evals = (int)__reduce_add_sync(0xffffffffu, (unsigned)sv);
+  // append position pairs to the warp's list (flushed when full)
+  auto push = [&](bool take, int x, int y) {
+    const unsigned bt = __ballot_sync(0xffffffffu, take);
+    if (np + __popc(bt) > kPairCap) {
+      __syncwarp();
+      eval_list<4>(a, np, pr, tr, dd, lane, bd, bi, bj, evals);
+      __syncwarp();
+      np = 0;
+    }
+    if (take) pr[np + __popc(bt & below)] = (uint32_t)x | ((uint32_t)y << 16);
+    np += __popc(bt);
+  };
+  // ---- peeling.  With hc the largest h left, every surviving pair has both
+  // rows in R = {i : h_i + hc >= thr}.  While R is too large for the list,
+  // the row of largest h is paired with every row it can reach and taken
+  // out (h = -inf): hc drops and R shrinks.
+  float hc = hmax;
+  int cnt = 0;
+  for (int peel = 0;; ++peel) {
+    int c = 0, am = INT_MAX;
+    float mv = -FLT_MAX;
+    for (int i = tid; i < n; i += kBoundThreads) {
+      const float h = hv[i];
+      c += __fadd_ru(h, hc) >= thr;
+      if (h > mv) {  // ascending i per thread: the first of equal maxima
+        mv = h;
+        am = i;
+      }
+    }
+    c = (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, mv, o);
+      const int a2 = __shfl_xor_sync(0xffffffffu, am, o);
+      if (m2 > mv || (m2 == mv && a2 < am)) {
+        mv = m2;
+        am = a2;
+      }
+    }
+    if (lane == 0) {
+      s_ri[warp] = c;
+      s_rj[warp] = am;
+      s_hmax[warp] = mv;
+    }
+    __syncthreads();
+    cnt = 0;
+    int m = INT_MAX;
+    float hm = -FLT_MAX;
+    for (int w = 0; w < NW; ++w) {
+      cnt += s_ri[w];
+      if (s_hmax[w] > hm || (s_hmax[w] == hm && s_rj[w] < m)) {
+        hm = s_hmax[w];
+        m = s_rj[w];
+      }
+    }
+    __syncthreads();
+    if (cnt <= a.rmax) break;
+    if (peel >= a.maxpeel || m == INT_MAX || !(hm > -FLT_MAX)) {
+      // weak bound everywhere (a nearly 2-opt-optimal tour): the band
+      // scan takes the particle
+      if (tid == 0) a.fb[1 + atomicAdd(&a.fb[0], 1)] = p;
+      return;
+    }
+    // row m (h = hm = hc) against every row it reaches
+    for (int i0 = 0; i0 < n; i0 += kBoundThreads) {
+      const int i = i0 + tid;
+      const bool take = i < n && i != m && __fadd_ru(hm, hv[i]) >= thr;
+      push(take, m, i);
+    }
+    __syncthreads();
+    if (tid == 0) hv[m] = -FLT_MAX;
+    __syncthreads();
+    // the next largest h (the first max of the remaining rows)
+    hc = -FLT_MAX;
+    for (int i = tid; i < n; i += kBoundThreads) hc = fmaxf(hc, hv[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+      hc = fmaxf(hc, __shfl_xor_sync(0xffffffffu, hc, o));
+    if (lane == 0) s_hmax[warp] = hc;
+    __syncthreads();
+    for (int w = 0; w < NW; ++w) hc = fmaxf(hc, s_hmax[w]);
+    __syncthreads();
+  }
+  // ---- R = {i : h_i + hc >= thr}: both rows of every remaining pair
+  if (tid == 0) s_cnt = 0;
+  __syncthreads();
+  for (int i0 = 0; i0 < n; i0 += kBoundThreads) {
+    const int i = i0 + tid;
+    const bool take = i < n && __fadd_ru(hv[i], hc) >= thr;
+    const unsigned bt = __ballot_sync(0xffffffffu, take);
+    if (bt) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&s_cnt, __popc(bt));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      const int slot = base + __popc(bt & below);
+      if (take && slot < a.rmax) {
+        lpos[slot] = i;
+        lh[slot] = hv[i];
+      }
+    }
+  }
+  __syncthreads();
+  cnt = min(s_cnt, a.rmax);
+  // ---- R's pairs with h_u + h_v >= thr: warp-compacted, evaluated
+  for (int u = warp; u + 1 < cnt; u += NW) {
+    const float hu = lh[u];
+    const int pu = lpos[u];
+    for (int v0 = u + 1; v0 < cnt; v0 += 32) {
+      const int v = v0 + lane;
+      const bool take = v < cnt && __fadd_ru(hu, lh[v]) >= thr;
+      push(take, pu, take ? lpos[v] : 0);
+    }
+  }
+  __syncwarp();
+  eval_list<4>(a, np, pr, tr, dd, lane, bd, bi, bj, evals);
+  if (lane == 0 && evals) atomicAdd(a.pairs, (unsigned long long)evals);
+  cta_lexmin(bd, bi, bj, s_rd, s_ri, s_rj, lane, warp, NW);
+  TwoOptRes* out = a.res + (size_t)p * a.chunks;
+  for (int c = tid; c < a.chunks; c += kBoundThreads)
+    out[c] = c == 0 ? TwoOptRes{bd, bi, bj} : TwoOptRes{kInf, INT_MAX, INT_MAX};
+}
+
+// Off-diagonal row and column minima {r(c), q(c)} (one warp per city).
+__global__ void k_bound_minima(const double* cost, int64_t ld, int n,
+                               double2* out) {
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= n) return;
+  double r = __longlong_as_double(0x7ff0000000000000ll), q = r;
+  for (int b = lane; b < n; b += 32) {
+    if (b == c) continue;
+    r = fmin(r, cost[(size_t)c * ld + b]);
+    q = fmin(q, cost[(size_t)b * ld + c]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    r = fmin(r, __shfl_xor_sync(0xffffffffu, r, o));
+    q = fmin(q, __shfl_xor_sync(0xffffffffu, q, o));
+  }
+  if (lane == 0) out[c] = make_double2(r, q);
+}
+
+struct BoundLayout {
+  uint32_t off_d, off_h, off_pos, off_lh, off_pairs, bytes;
+};
+
+// dynamic shared memory of one CTA: tour (u16, n + 1), d (f64, n), h (f32,
+// n), the row list (positions, h; rmax each), the warps' pair lists
+BoundLayout bound_layout(int n, int rmax) {
+  BoundLayout L;
+  int64_t o = round_up(2 * (int64_t)(n + 1), 16);
+  L.off_d = (uint32_t)o;
+  o += 8 * (int64_t)n;
+  L.off_h = (uint32_t)o;
+  o = round_up(o + 4 * (int64_t)n, 16);
+  L.off_pos = (uint32_t)o;
+  o = round_up(o + 4 * (int64_t)std::max(rmax, kSeedRows), 16);
+  L.off_lh = (uint32_t)o;
+  o = round_up(o + 4 * (int64_t)rmax, 16);
+  L.off_pairs = (uint32_t)o;
+  o += 4 * (int64_t)kPairCap * (kBoundThreads / 32);
+  L.bytes = (uint32_t)round_up(o, 128);
+  return L;
+}
+
+int bound_rmax() {
+  if (const char* e = getenv("DPSO_BOUND_RMAX")) {
+    const int v = atoi(e);
+    return v < kSeedRows ? kSeedRows : v;
+  }
+  return 256;
+}
+
+}  // namespace
+
+int64_t bound_bytes(int n, int64_t count) {
+  if (n < 4 || n > kBoundMaxN) return 0;
+  return round_up(16 * (int64_t)n, 256) + 16 + 4 * (count + 2);
+}
+
+cudaError_t bound_prepare(const double* cost, int64_t ld, int32_t n,
+                          void* buf, double maxabs, cudaStream_t s,
+                          TwoOptPlan* pl) {
+  pl->bound = 0;
+  if (!buf || n < 4 || n > kBoundMaxN || !pl->band_mode) return cudaSuccess;
+  if (const char* e = getenv("DPSO_BOUND"))
+    if (atoi(e) == 0) return cudaSuccess;
+  // finite matrices of moderate magnitude only (h and the threshold stay
+  // finite); others keep the full scan
+  if (!(maxabs < 1e300)) return cudaSuccess;
+  const BoundLayout L = bound_layout(n, bound_rmax());
+  if (L.bytes > kBoundSmem) return cudaSuccess;
+  double2* cmn = reinterpret_cast<double2*>(buf);
+  k_bound_minima<<<(n + 7) / 8, 256, 0, s>>>(cost, ld, n, cmn);
+  cudaError_t e = cudaGetLastError();
+  if (e) return e;
+  pl->bound = 1;
+  pl->bound_cmn = cmn;
+  unsigned char* st =
+      reinterpret_cast<unsigned char*>(buf) + round_up(16 * (int64_t)n, 256);
+  pl->bound_pairs = reinterpret_cast<unsigned long long*>(st);
+  pl->bound_fb = reinterpret_cast<int32_t*>(st + 16);
+  e = cudaMemsetAsync(st, 0, 16, s);
+  if (e) return e;
+  pl->bound_slack = ldexp(maxabs, -40);
+  return cudaSuccess;
+}
+
+cudaError_t launch_two_opt_bound(const TwoOptPlan& pl, int32_t n, int32_t np,
+                                 const uint16_t* tours, const double* dcache,
+                                 int32_t count, TwoOptRes* res, int32_t chunks,
+                                 const DevCtl* ctl, cudaStream_t s) {
+  BoundArgs a;
+  memset(&a, 0, sizeof a);
+  a.cost = pl.cost;
+  a.ld = pl.ld;
+  a.cmn = pl.bound_cmn;
+  a.n = n;
+  a.np = np;
+  a.count = count;
+  a.chunks = chunks;
+  a.tours = tours;
+  a.dcache = dcache;
+  a.res = res;
+  a.ctl = ctl;
+  a.fb = pl.bound_fb;
+  a.pairs = pl.bound_pairs;
+  a.slack = pl.bound_slack;
+  a.rmax = bound_rmax();
+  a.maxpeel = kMaxPeel;
+  if (const char* e = getenv("DPSO_BOUND_PEEL")) a.maxpeel = atoi(e);
+  const BoundLayout L = bound_layout(n, a.rmax);
+  a.off_d = L.off_d;
+  a.off_h = L.off_h;
+  a.off_pos = L.off_pos;
+  a.off_lh = L.off_lh;
+  a.off_pairs = L.off_pairs;
+  const size_t smem = L.bytes;
+  cudaError_t e = cudaMemsetAsync(a.fb, 0, 4, s);
+  if (e) return e;
+  e = set_dyn_smem((const void*)k_two_opt_bound, smem);
+  if (e) return e;
+  if (count > 0) k_two_opt_bound<<<count, kBoundThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace dpso

@@ -13,6 +13,13 @@ from oracle import dpso_oracle as O
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _full_band_scan(monkeypatch):
+    # the bounded scan (k_two_opt_bound.cu, tests/test_gpu_bound.py) would
+    # take almost every random tour before the band scan sees it
+    monkeypatch.setenv("DPSO_BOUND", "0")
+
+
 @pytest.fixture(scope="module")
 def pkg():
     from paper_1706_04399_b200.build import build
