@@ -109,7 +109,7 @@ struct TwoOptPlan {
   // minima, the fallback particle list ([0] count, [1..] particles) and the
   // rounding slack of the pair bound.  bound == 0: not used.
   int bound;
-  const double2* bound_cmn;
+  const float2* bound_cmn;
   int32_t* bound_fb;
   unsigned long long* bound_pairs;  // pairs evaluated (cumulative)
   double bound_slack;

@@ -23,10 +23,12 @@
 // threshold -Tq - slack down (slack = 2^-40 max|C|, far above the fp64
 // rounding of h and delta), so every skip is conservative.
 //
-// Per particle (one CTA of 256 threads): the tour and d (dcache) in shared
-// memory, h over the tour, the row of largest h of each 8 threads (32 seed
-// rows among the longest edges) and their 496 pairs give T; then R = {i : h_i + max h >= -Tq} (every surviving pair has both rows in
-// R) and its pairs with h_i + h_j >= -Tq.  The tours the swarm scans are
+// Per particle (one CTA of 256 threads, 128 for large swarms): the tour, d
+// (dcache) and the cities' minima in shared memory, h over the tour, the
+// row of largest h of each 8 threads (32 or 16 seed rows among the longest
+// edges) and their pairs give T; then R = {i : h_i + max h >= -Tq} (every
+// surviving pair has both rows in R) and its pairs with h_i + h_j >= -Tq
+// (none between two rows below -Tq / 2).  The tours the swarm scans are
 // far from 2-opt optimal: at C2 |R| is ~50 of 1000 rows and ~200 of the
 // 499,500 pairs survive.  A particle with |R| above the list capacity (a
 // near-2-opt-optimal tour: the bound is weak) goes to the row-per-lane
@@ -45,8 +47,8 @@ namespace dpso {
 
 namespace {
 
-constexpr int kBoundThreads = 256;  // one CTA per particle
-constexpr int kSeedRows = 32;       // seed rows (one per 8 threads)
+constexpr int kBoundThreads = 256;  // one CTA per particle (at most)
+constexpr int kSeedRows = 32;       // seed rows (one per 8 threads, at most)
 constexpr int kPairCap = 256;       // pair-list entries per warp
 constexpr int kMaxPeel = 64;        // rows peeled before the band fallback
 constexpr size_t kBoundSmem = 200 * 1024;
@@ -54,7 +56,7 @@ constexpr size_t kBoundSmem = 200 * 1024;
 struct BoundArgs {
   const double* cost;
   int64_t ld;
-  const double2* cmn;  // per city {r(c), q(c)}
+  const float2* cmn;  // per city {r(c), q(c)}, rounded down
   int n, np, count, chunks;
   const uint16_t* tours;
   const double* dcache;
@@ -65,7 +67,7 @@ struct BoundArgs {
   double slack;
   int rmax;     // row-list capacity
   int maxpeel;  // rows peeled before the band fallback
-  uint32_t off_d, off_h, off_pos, off_lh, off_pairs;  // shared memory
+  uint32_t off_d, off_h, off_c, off_pos, off_lh, off_pairs;  // shared
 };
 
 __device__ __forceinline__ bool lex_less(double d1, int i1, int j1, double d2,
@@ -160,15 +162,15 @@ __device__ __forceinline__ void cta_lexmin(double& d, int& i, int& j,
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kBoundThreads)
-    k_two_opt_bound(BoundArgs a) {
+template <int NT>
+__global__ void __launch_bounds__(NT) k_two_opt_bound(BoundArgs a) {
   if (a.ctl && (a.ctl->done || a.ctl->improved)) return;  // no scan
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ double s_rd[kBoundThreads / 32];
-  __shared__ int s_ri[kBoundThreads / 32], s_rj[kBoundThreads / 32];
-  __shared__ float s_hmax[kBoundThreads / 32];
-  __shared__ int s_cnt;
-  constexpr int NW = kBoundThreads / 32;
+  __shared__ double s_rd[NT / 32];
+  __shared__ int s_ri[NT / 32], s_rj[NT / 32];
+  __shared__ float s_hmax[NT / 32];
+  __shared__ int s_cnt[2];
+  constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int p = blockIdx.x;
   if (p >= a.count) return;
@@ -177,6 +179,7 @@ __global__ void __launch_bounds__(kBoundThreads)
   uint16_t* tr = reinterpret_cast<uint16_t*>(smem);  // tour, tr[n] = tr[0]
   double* dd = reinterpret_cast<double*>(smem + a.off_d);
   float* hv = reinterpret_cast<float*>(smem + a.off_h);
+  float2* cm = reinterpret_cast<float2*>(smem + a.off_c);  // minima of a_i
   int* lpos = reinterpret_cast<int*>(smem + a.off_pos);
   float* lh = reinterpret_cast<float*>(smem + a.off_lh);
   uint32_t* pr = reinterpret_cast<uint32_t*>(smem + a.off_pairs) +
@@ -184,62 +187,56 @@ __global__ void __launch_bounds__(kBoundThreads)
   const uint16_t* tour = a.tours + (size_t)p * a.np;
   const double* dg = a.dcache + (size_t)p * a.np;
 
-  // ---- the tour and its edge costs in shared memory
-  for (int i0 = 0; i0 < n; i0 += 4 * kBoundThreads) {
-    uint16_t t[4];
+  // ---- the tour, its edge costs and its cities' minima in shared memory
+  for (int i0 = 0; i0 < n; i0 += 4 * NT) {
+    int t[4];
     double d[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const int i = i0 + k * kBoundThreads + tid;
+      const int i = i0 + k * NT + tid;
       if (i < n) {
         t[k] = tour[i];
         d[k] = dg[i];
       }
     }
+    float2 c[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (i0 + k * NT + tid < n) c[k] = a.cmn[t[k]];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const int i = i0 + k * kBoundThreads + tid;
+      const int i = i0 + k * NT + tid;
       if (i < n) {
-        tr[i] = t[k];
+        tr[i] = (uint16_t)t[k];
         dd[i] = d[k];
+        cm[i] = c[k];
       }
     }
   }
   if (tid == 0) {
-    tr[n] = tour[0];
-    s_cnt = 0;
+    tr[n] = tr[0] = tour[0];
+    s_cnt[0] = s_cnt[1] = 0;
   }
   __syncthreads();
+  if (tid == 0) cm[n] = cm[0];
+  __syncthreads();
 
-  // ---- h_i (rounded up to fp32); the thread's largest
+  // ---- h_i >= d_i - m_i, in fp32 with every rounding upward (the minima
+  // are rounded down); the thread's largest
   float lmax = -FLT_MAX;
   int larg = -1;
-  for (int i0 = 0; i0 < n; i0 += 4 * kBoundThreads) {
-    double2 ra[4], rb[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int i = i0 + k * kBoundThreads + tid;
-      if (i < n) {
-        ra[k] = a.cmn[tr[i]];
-        rb[k] = a.cmn[tr[i + 1]];
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int i = i0 + k * kBoundThreads + tid;
-      if (i < n) {
-        const double f = 0.5 * (ra[k].x + rb[k].x);
-        const double g = 0.5 * (ra[k].y + rb[k].y);
-        const float h = __double2float_ru(dd[i] - fmin(f, g));
-        hv[i] = h;
-        if (larg < 0 || h > lmax) {
-          lmax = h;
-          larg = i;
-        }
-      }
+  for (int i = tid; i < n; i += NT) {
+    const float2 ca = cm[i], cs = cm[i + 1];
+    const float f = __fmul_rd(0.5f, __fadd_rd(ca.x, cs.x));
+    const float g = __fmul_rd(0.5f, __fadd_rd(ca.y, cs.y));
+    const float h = __fsub_ru(__double2float_ru(dd[i]), fminf(f, g));
+    hv[i] = h;
+    if (larg < 0 || h > lmax) {
+      lmax = h;
+      larg = i;
     }
   }
-  // seed rows: the largest h of each group of 8 threads (32 seeds among
+  // seed rows: the largest h of each group of 8 threads (NT / 8 seeds among
   // the longest edges; any rows give a valid threshold, long edges a tight
   // one), and the maximum over the tour
 #pragma unroll
@@ -269,11 +266,12 @@ __global__ void __launch_bounds__(kBoundThreads)
   {
     constexpr int S = 4 * NW;
     constexpr int NP = S * (S - 1) / 2;
-    double A[2], B[2], di[2], dj[2];
-    int I[2], J[2];
+    constexpr int KQ = (NP + NT - 1) / NT;
+    double A[KQ], B[KQ], di[KQ], dj[KQ];
+    int I[KQ], J[KQ];
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int q = tid + k * kBoundThreads;
+    for (int k = 0; k < KQ; ++k) {
+      const int q = tid + k * NT;
       I[k] = -1;
       if (q < NP) {
         // q -> (u, v), u < v: v (v - 1) / 2 <= q < v (v + 1) / 2
@@ -294,7 +292,7 @@ __global__ void __launch_bounds__(kBoundThreads)
       }
     }
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < KQ; ++k) {
       if (I[k] < 0) continue;
       ++sv;
       double t = __dadd_rn(A[k], B[k]);
@@ -311,8 +309,11 @@ __global__ void __launch_bounds__(kBoundThreads)
   int ti = bi, tj = bj;
   cta_lexmin(t0, ti, tj, s_rd, s_ri, s_rj, lane, warp, NW);
   const double tq = fmin(t0, -1e-12);
-  // skip a pair iff h_i + h_j (rounded up) < thr <= -tq - slack
+  // skip a pair iff h_i + h_j < thr <= -tq - slack (exactly: the fp32
+  // tests round up)
   const float thr = __double2float_rd(__dsub_rd(-tq, a.slack));
+  // two rows below half the threshold cannot make a pair
+  const float half = __fmul_rd(0.5f, thr);
 
   int np = 0, evals = (int)__reduce_add_sync(0xffffffffu, (unsigned)sv);
   // append position pairs to the warp's list (flushed when full)
@@ -327,24 +328,58 @@ __global__ void __launch_bounds__(kBoundThreads)
     if (take) pr[np + __popc(bt & below)] = (uint32_t)x | ((uint32_t)y << 16);
     np += __popc(bt);
   };
-  // ---- peeling.  With hc the largest h left, every surviving pair has both
-  // rows in R = {i : h_i + hc >= thr}.  While R is too large for the list,
-  // the row of largest h is paired with every row it can reach and taken
-  // out (h = -inf): hc drops and R shrinks.
+  // R(hc) = {i : h_i + hc >= thr}, hc the largest h left: both rows of
+  // every remaining surviving pair.  Compacted as H (h >= half, from the
+  // front of the list) and L (h < half, from the back); returns |R|.
+  auto compact = [&](float hc) -> int {
+    for (int i0 = 0; i0 < n; i0 += NT) {
+      const int i = i0 + tid;
+      const float h = i < n ? hv[i] : -FLT_MAX;
+      const bool take = i < n && __fadd_ru(h, hc) >= thr;
+      const bool hi = take && h >= half;
+      const unsigned bh = __ballot_sync(0xffffffffu, hi);
+      const unsigned bl = __ballot_sync(0xffffffffu, take && !hi);
+      int baseh = 0, basel = 0;
+      if (lane == 0) {
+        if (bh) baseh = atomicAdd(&s_cnt[0], __popc(bh));
+        if (bl) basel = atomicAdd(&s_cnt[1], __popc(bl));
+      }
+      baseh = __shfl_sync(0xffffffffu, baseh, 0);
+      basel = __shfl_sync(0xffffffffu, basel, 0);
+      if (hi) {
+        const int slot = baseh + __popc(bh & below);
+        if (slot < a.rmax) {
+          lpos[slot] = i;
+          lh[slot] = h;
+        }
+      } else if (take) {
+        const int slot = a.rmax - 1 - (basel + __popc(bl & below));
+        if (slot >= 0) {
+          lpos[slot] = i;
+          lh[slot] = h;
+        }
+      }
+    }
+    __syncthreads();
+    const int r = s_cnt[0] + s_cnt[1];
+    return r;
+  };
   float hc = hmax;
-  int cnt = 0;
-  for (int peel = 0;; ++peel) {
-    int c = 0, am = INT_MAX;
+  int cnt = compact(hc);
+  // ---- peeling: while R is too large for the list, the row of largest h
+  // is paired with every row it reaches and taken out (h = -FLT_MAX): hc
+  // drops and R shrinks
+  for (int peel = 0; cnt > a.rmax; ++peel) {
+    // the first row of largest h
+    int am = INT_MAX;
     float mv = -FLT_MAX;
-    for (int i = tid; i < n; i += kBoundThreads) {
+    for (int i = tid; i < n; i += NT) {
       const float h = hv[i];
-      c += __fadd_ru(h, hc) >= thr;
       if (h > mv) {  // ascending i per thread: the first of equal maxima
         mv = h;
         am = i;
       }
     }
-    c = (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const float m2 = __shfl_xor_sync(0xffffffffu, mv, o);
@@ -355,76 +390,62 @@ __global__ void __launch_bounds__(kBoundThreads)
       }
     }
     if (lane == 0) {
-      s_ri[warp] = c;
       s_rj[warp] = am;
       s_hmax[warp] = mv;
     }
     __syncthreads();
-    cnt = 0;
     int m = INT_MAX;
-    float hm = -FLT_MAX;
-    for (int w = 0; w < NW; ++w) {
-      cnt += s_ri[w];
-      if (s_hmax[w] > hm || (s_hmax[w] == hm && s_rj[w] < m)) {
-        hm = s_hmax[w];
+    float hmv = -FLT_MAX;
+    for (int w = 0; w < NW; ++w)
+      if (s_hmax[w] > hmv || (s_hmax[w] == hmv && s_rj[w] < m)) {
+        hmv = s_hmax[w];
         m = s_rj[w];
       }
-    }
     __syncthreads();
-    if (cnt <= a.rmax) break;
-    if (peel >= a.maxpeel || m == INT_MAX || !(hm > -FLT_MAX)) {
+    if (peel >= a.maxpeel || m == INT_MAX || !(hmv > -FLT_MAX)) {
       // weak bound everywhere (a nearly 2-opt-optimal tour): the band
       // scan takes the particle
       if (tid == 0) a.fb[1 + atomicAdd(&a.fb[0], 1)] = p;
       return;
     }
-    // row m (h = hm = hc) against every row it reaches
-    for (int i0 = 0; i0 < n; i0 += kBoundThreads) {
+    // row m against every row it reaches
+    for (int i0 = 0; i0 < n; i0 += NT) {
       const int i = i0 + tid;
-      const bool take = i < n && i != m && __fadd_ru(hm, hv[i]) >= thr;
+      const bool take = i < n && i != m && __fadd_ru(hmv, hv[i]) >= thr;
       push(take, m, i);
     }
     __syncthreads();
-    if (tid == 0) hv[m] = -FLT_MAX;
+    if (tid == 0) {
+      hv[m] = -FLT_MAX;
+      s_cnt[0] = s_cnt[1] = 0;
+    }
     __syncthreads();
-    // the next largest h (the first max of the remaining rows)
+    // the largest h left
     hc = -FLT_MAX;
-    for (int i = tid; i < n; i += kBoundThreads) hc = fmaxf(hc, hv[i]);
+    for (int i = tid; i < n; i += NT) hc = fmaxf(hc, hv[i]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
       hc = fmaxf(hc, __shfl_xor_sync(0xffffffffu, hc, o));
     if (lane == 0) s_hmax[warp] = hc;
     __syncthreads();
     for (int w = 0; w < NW; ++w) hc = fmaxf(hc, s_hmax[w]);
-    __syncthreads();
+    cnt = compact(hc);
   }
-  // ---- R = {i : h_i + hc >= thr}: both rows of every remaining pair
-  if (tid == 0) s_cnt = 0;
-  __syncthreads();
-  for (int i0 = 0; i0 < n; i0 += kBoundThreads) {
-    const int i = i0 + tid;
-    const bool take = i < n && __fadd_ru(hv[i], hc) >= thr;
-    const unsigned bt = __ballot_sync(0xffffffffu, take);
-    if (bt) {
-      int base = 0;
-      if (lane == 0) base = atomicAdd(&s_cnt, __popc(bt));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      const int slot = base + __popc(bt & below);
-      if (take && slot < a.rmax) {
-        lpos[slot] = i;
-        lh[slot] = hv[i];
-      }
-    }
-  }
-  __syncthreads();
-  cnt = min(s_cnt, a.rmax);
-  // ---- R's pairs with h_u + h_v >= thr: warp-compacted, evaluated
-  for (int u = warp; u + 1 < cnt; u += NW) {
+  // ---- R's pairs: H x H and H x L with h_u + h_v >= thr (two rows of L
+  // sum below thr), warp-compacted, evaluated
+  const int nh = s_cnt[0], nl = s_cnt[1];
+  const int l0 = a.rmax - nl;  // L occupies [l0, rmax)
+  for (int u = warp; u < nh; u += NW) {
     const float hu = lh[u];
     const int pu = lpos[u];
-    for (int v0 = u + 1; v0 < cnt; v0 += 32) {
+    for (int v0 = u + 1; v0 < nh; v0 += 32) {
       const int v = v0 + lane;
-      const bool take = v < cnt && __fadd_ru(hu, lh[v]) >= thr;
+      const bool take = v < nh && __fadd_ru(hu, lh[v]) >= thr;
+      push(take, pu, take ? lpos[v] : 0);
+    }
+    for (int v0 = l0; v0 < a.rmax; v0 += 32) {
+      const int v = v0 + lane;
+      const bool take = v < a.rmax && __fadd_ru(hu, lh[v]) >= thr;
       push(take, pu, take ? lpos[v] : 0);
     }
   }
@@ -433,13 +454,14 @@ __global__ void __launch_bounds__(kBoundThreads)
   if (lane == 0 && evals) atomicAdd(a.pairs, (unsigned long long)evals);
   cta_lexmin(bd, bi, bj, s_rd, s_ri, s_rj, lane, warp, NW);
   TwoOptRes* out = a.res + (size_t)p * a.chunks;
-  for (int c = tid; c < a.chunks; c += kBoundThreads)
+  for (int c = tid; c < a.chunks; c += NT)
     out[c] = c == 0 ? TwoOptRes{bd, bi, bj} : TwoOptRes{kInf, INT_MAX, INT_MAX};
 }
 
-// Off-diagonal row and column minima {r(c), q(c)} (one warp per city).
+// Off-diagonal row and column minima {r(c), q(c)}, rounded down to fp32
+// (lower bounds stay lower bounds), one warp per city.
 __global__ void k_bound_minima(const double* cost, int64_t ld, int n,
-                               double2* out) {
+                               float2* out) {
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (c >= n) return;
@@ -454,15 +476,17 @@ __global__ void k_bound_minima(const double* cost, int64_t ld, int n,
     r = fmin(r, __shfl_xor_sync(0xffffffffu, r, o));
     q = fmin(q, __shfl_xor_sync(0xffffffffu, q, o));
   }
-  if (lane == 0) out[c] = make_double2(r, q);
+  if (lane == 0)
+    out[c] = make_float2(__double2float_rd(r), __double2float_rd(q));
 }
 
 struct BoundLayout {
-  uint32_t off_d, off_h, off_pos, off_lh, off_pairs, bytes;
+  uint32_t off_d, off_h, off_c, off_pos, off_lh, off_pairs, bytes;
 };
 
 // dynamic shared memory of one CTA: tour (u16, n + 1), d (f64, n), h (f32,
-// n), the row list (positions, h; rmax each), the warps' pair lists
+// n), the cities' minima (f32 x 2, n + 1), the row list (positions, h;
+// rmax each), the warps' pair lists
 BoundLayout bound_layout(int n, int rmax) {
   BoundLayout L;
   int64_t o = round_up(2 * (int64_t)(n + 1), 16);
@@ -470,6 +494,8 @@ BoundLayout bound_layout(int n, int rmax) {
   o += 8 * (int64_t)n;
   L.off_h = (uint32_t)o;
   o = round_up(o + 4 * (int64_t)n, 16);
+  L.off_c = (uint32_t)o;
+  o += 8 * (int64_t)(n + 1);
   L.off_pos = (uint32_t)o;
   o = round_up(o + 4 * (int64_t)std::max(rmax, kSeedRows), 16);
   L.off_lh = (uint32_t)o;
@@ -507,7 +533,7 @@ cudaError_t bound_prepare(const double* cost, int64_t ld, int32_t n,
   if (!(maxabs < 1e300)) return cudaSuccess;
   const BoundLayout L = bound_layout(n, bound_rmax());
   if (L.bytes > kBoundSmem) return cudaSuccess;
-  double2* cmn = reinterpret_cast<double2*>(buf);
+  float2* cmn = reinterpret_cast<float2*>(buf);
   k_bound_minima<<<(n + 7) / 8, 256, 0, s>>>(cost, ld, n, cmn);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
@@ -549,15 +575,27 @@ cudaError_t launch_two_opt_bound(const TwoOptPlan& pl, int32_t n, int32_t np,
   const BoundLayout L = bound_layout(n, a.rmax);
   a.off_d = L.off_d;
   a.off_h = L.off_h;
+  a.off_c = L.off_c;
   a.off_pos = L.off_pos;
   a.off_lh = L.off_lh;
   a.off_pairs = L.off_pairs;
   const size_t smem = L.bytes;
   cudaError_t e = cudaMemsetAsync(a.fb, 0, 4, s);
   if (e) return e;
-  e = set_dyn_smem((const void*)k_two_opt_bound, smem);
+  // small swarms: 256 threads per particle (shorter per-particle latency
+  // chains); large swarms: 128 (more particles per SM, fewer seed pairs)
+  bool wide = count < 148 * 16;
+  if (const char* e = getenv("DPSO_BOUND_NT")) wide = atoi(e) == 256;
+  const void* kern = wide ? (const void*)k_two_opt_bound<256>
+                          : (const void*)k_two_opt_bound<128>;
+  e = set_dyn_smem(kern, smem);
   if (e) return e;
-  if (count > 0) k_two_opt_bound<<<count, kBoundThreads, smem, s>>>(a);
+  if (count > 0) {
+    if (wide)
+      k_two_opt_bound<256><<<count, 256, smem, s>>>(a);
+    else
+      k_two_opt_bound<128><<<count, 128, smem, s>>>(a);
+  }
   return cudaGetLastError();
 }
 

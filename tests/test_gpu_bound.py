@@ -82,8 +82,16 @@ def test_bound_selected(pkg, monkeypatch):
     assert ctx_query(pkg, grid(100), "dpso_scan_bound") == 0
 
 
+@pytest.fixture(params=["256", "128"])
+def threads(request, monkeypatch):
+    # CTA width: 256 threads (32 seed rows) for small swarms, 128 (16) for
+    # large ones; both forced here
+    monkeypatch.setenv("DPSO_BOUND_NT", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("kind", ["euclid", "grid", "int"])
-def test_bound_random_tours(pkg, kind):
+def test_bound_random_tours(pkg, kind, threads):
     rng = np.random.default_rng(3)
     for n in list(range(4, 40)) + [63, 64, 65, 100, 257, 511, 1000]:
         if kind == "grid":
@@ -102,7 +110,7 @@ def test_bound_large_n(pkg):
         check(pkg, cost, perms(rng, 8, n), ("large", n), 4, rng)
 
 
-def test_bound_ties_and_optimal_tours(pkg):
+def test_bound_ties_and_optimal_tours(pkg, threads):
     rng = np.random.default_rng(7)
     for n in (16, 49, 100, 300):
         cost = grid(n)
@@ -113,7 +121,7 @@ def test_bound_ties_and_optimal_tours(pkg):
               ("near", n))
 
 
-def test_bound_near_optimal_euclid(pkg):
+def test_bound_near_optimal_euclid(pkg, threads):
     rng = np.random.default_rng(9)
     for n in (50, 200, 600):
         cost = random_euclidean_matrix(n, rng)
@@ -133,7 +141,7 @@ def test_bound_scales(pkg):
     check(pkg, grid(144) / 3.0, perms(rng, 12, 144), "lattice")
 
 
-def test_bound_asymmetric_negative_virtual(pkg):
+def test_bound_asymmetric_negative_virtual(pkg, threads):
     rng = np.random.default_rng(17)
     n = 257
     c = random_euclidean_matrix(n, rng) * (1 + rng.random((n, n)))
@@ -160,7 +168,7 @@ def test_bound_asymmetric_negative_virtual(pkg):
 
 @pytest.mark.parametrize("peel", ["0", "3", "64"])
 @pytest.mark.parametrize("rmax", ["32", "40", "100"])
-def test_bound_small_row_list(pkg, rmax, peel, monkeypatch):
+def test_bound_small_row_list(pkg, rmax, peel, threads, monkeypatch):
     # a small row-list capacity makes the kernel peel rows of largest h
     # (paired with every row they reach) and, past the peel limit, send
     # the particle to the band scan: the two kernels' results interleave

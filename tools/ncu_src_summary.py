@@ -18,7 +18,7 @@ def sections(rows):
 
 
 def main():
-    rows = list(csv.reader(open(sys.argv[1])))
+    rows = list(csv.reader(open(sys.argv[1], errors="replace")))
     thr = float(sys.argv[2]) if len(sys.argv) > 2 else 0.002
     best = None
     for sec in sections(rows):
