@@ -163,7 +163,7 @@ __device__ __forceinline__ void cta_lexmin(double& d, int& i, int& j,
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT) k_two_opt_bound(BoundArgs a) {
+__global__ void __launch_bounds__(NT, 1024 / NT) k_two_opt_bound(BoundArgs a) {
   if (a.ctl && (a.ctl->done || a.ctl->improved)) return;  // no scan
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double s_rd[NT / 32];
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(NT) k_two_opt_bound(BoundArgs a) {
     const unsigned bt = __ballot_sync(0xffffffffu, take);
     if (np + __popc(bt) > kPairCap) {
       __syncwarp();
-      eval_list<4>(a, np, pr, tr, dd, lane, bd, bi, bj, evals);
+      eval_list<2>(a, np, pr, tr, dd, lane, bd, bi, bj, evals);
       __syncwarp();
       np = 0;
     }
@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(NT) k_two_opt_bound(BoundArgs a) {
     }
   }
   __syncwarp();
-  eval_list<4>(a, np, pr, tr, dd, lane, bd, bi, bj, evals);
+  eval_list<2>(a, np, pr, tr, dd, lane, bd, bi, bj, evals);
   if (lane == 0 && evals) atomicAdd(a.pairs, (unsigned long long)evals);
   cta_lexmin(bd, bi, bj, s_rd, s_ri, s_rj, lane, warp, NW);
   TwoOptRes* out = a.res + (size_t)p * a.chunks;
