@@ -162,7 +162,7 @@ __device__ __forceinline__ void cta_lexmin(double& d, int& i, int& j,
   __syncthreads();
 }
 
-template <int NT>
+template <int NT, int SPW>
 __global__ void __launch_bounds__(NT, 1024 / NT) k_two_opt_bound(BoundArgs a) {
   if (a.ctl && (a.ctl->done || a.ctl->improved)) return;  // no scan
   extern __shared__ __align__(16) unsigned char smem[];
@@ -240,7 +240,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_two_opt_bound(BoundArgs a) {
   // the longest edges; any rows give a valid threshold, long edges a tight
   // one), and the maximum over the tour
 #pragma unroll
-  for (int o = 1; o < 8; o <<= 1) {
+  constexpr int GL = 32 / SPW;  // lanes per seed group
+  for (int o = 1; o < GL; o <<= 1) {
     const float m2 = __shfl_xor_sync(0xffffffffu, lmax, o);
     const int a2 = __shfl_xor_sync(0xffffffffu, larg, o);
     if (a2 >= 0 && (larg < 0 || m2 > lmax)) {
@@ -248,10 +249,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_two_opt_bound(BoundArgs a) {
       larg = a2;
     }
   }
-  if ((lane & 7) == 0) lpos[warp * 4 + (lane >> 3)] = larg;
+  if (lane % GL == 0) lpos[warp * SPW + lane / GL] = larg;
   float hm = lmax;
 #pragma unroll
-  for (int o = 8; o < 32; o <<= 1)
+  for (int o = GL; o < 32; o <<= 1)
     hm = fmaxf(hm, __shfl_xor_sync(0xffffffffu, hm, o));
   if (lane == 0) s_hmax[warp] = hm;
   __syncthreads();
@@ -264,7 +265,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_two_opt_bound(BoundArgs a) {
   int bi = INT_MAX, bj = INT_MAX;
   int sv = 0;  // seed pairs this thread evaluated
   {
-    constexpr int S = 4 * NW;
+    constexpr int S = SPW * NW;
     constexpr int NP = S * (S - 1) / 2;
     constexpr int KQ = (NP + NT - 1) / NT;
     double A[KQ], B[KQ], di[KQ], dj[KQ];
@@ -585,16 +586,17 @@ cudaError_t launch_two_opt_bound(const TwoOptPlan& pl, int32_t n, int32_t np,
   // small swarms: 256 threads per particle (shorter per-particle latency
   // chains); large swarms: 128 (more particles per SM, fewer seed pairs)
   bool wide = count < 148 * 16;
+  constexpr int SPW_W = 4;  // seed rows per warp (2 measured slower at C2)
   if (const char* e = getenv("DPSO_BOUND_NT")) wide = atoi(e) == 256;
-  const void* kern = wide ? (const void*)k_two_opt_bound<256>
-                          : (const void*)k_two_opt_bound<128>;
+  const void* kern = wide ? (const void*)k_two_opt_bound<256, SPW_W>
+                          : (const void*)k_two_opt_bound<128, 4>;
   e = set_dyn_smem(kern, smem);
   if (e) return e;
   if (count > 0) {
     if (wide)
-      k_two_opt_bound<256><<<count, 256, smem, s>>>(a);
+      k_two_opt_bound<256, SPW_W><<<count, 256, smem, s>>>(a);
     else
-      k_two_opt_bound<128><<<count, 128, smem, s>>>(a);
+      k_two_opt_bound<128, 4><<<count, 128, smem, s>>>(a);
   }
   return cudaGetLastError();
 }
