@@ -90,6 +90,66 @@ def best_exchange(body, cost: np.ndarray):
     return body, 0.0
 
 
+def _f32_up(x):
+    """x (float64 array) rounded up to float32."""
+    f = np.asarray(x, dtype=np.float64).astype(np.float32)
+    low = f.astype(np.float64) < x
+    return np.where(low, np.nextafter(f, np.float32(np.inf)), f)
+
+
+def _f32_down(x):
+    f = np.asarray(x, dtype=np.float64).astype(np.float32)
+    high = f.astype(np.float64) > x
+    return np.where(high, np.nextafter(f, np.float32(-np.inf)), f)
+
+
+def bounded_exchange(body, cost: np.ndarray, seeds: int = 32):
+    """The bounded 2-opt scan's formulation (k_two_opt_bound.cu), restated
+    to check on the CPU that it returns ``best_exchange``'s result.  Test
+    infrastructure, not the reference: delta(i, j) >= -(h_i + h_j) with
+    h_k = d_k - min((r(a_k) + r(s_k)) / 2, (q(a_k) + q(s_k)) / 2), r / q the
+    off-diagonal row / column minima; h rounded up to fp32, the threshold
+    -Tq - 2^-40 max|C| rounded down; Tq from the pairs of the `seeds` rows
+    of largest h.  Only pairs with h_i + h_j >= thr are evaluated, with the
+    reference expression.  Returns (new_body, delta, evaluated_pairs)."""
+    n = len(body)
+    if n < 4:
+        return body, 0.0, 0
+    arr = np.asarray(body)
+    succ = np.roll(arr, -1)
+    d = cost[arr, succ]
+    off = cost + np.diag(np.full(n, np.inf))
+    r = _f32_down(off.min(1)).astype(np.float64)
+    q = _f32_down(off.min(0)).astype(np.float64)
+    f = _f32_down(0.5 * (r[arr] + r[succ])).astype(np.float64)
+    g = _f32_down(0.5 * (q[arr] + q[succ])).astype(np.float64)
+    h = _f32_up(_f32_up(d).astype(np.float64) - np.minimum(f, g))
+    h = h.astype(np.float64)
+
+    def delta_of(i, j):
+        return ((cost[arr[i], arr[j]] + cost[succ[i], succ[j]]) - d[i]) - d[j]
+
+    seed = np.sort(np.argsort(-h, kind="stable")[:min(seeds, n)])
+    si, sj = np.triu_indices(len(seed), 1)
+    t0 = delta_of(seed[si], seed[sj]).min() if len(si) else np.inf
+    tq = min(t0, -1e-12)
+    slack = np.ldexp(np.abs(cost).max(), -40)
+    thr = _f32_down(np.array([-tq - slack]))[0].astype(np.float64)
+    ii, jj = np.triu_indices(n, 1)
+    keep = _f32_up(h[ii] + h[jj]) >= thr
+    ii, jj = ii[keep], jj[keep]
+    if len(ii) == 0:
+        return body, 0.0, 0
+    dv = delta_of(ii, jj)
+    k = np.lexsort((jj, ii, dv))[0]
+    i, j, best = int(ii[k]), int(jj[k]), float(dv[k])
+    if best < -1e-12:
+        new = list(body)
+        new[i + 1:j + 1] = reversed(new[i + 1:j + 1])
+        return new, best, len(ii)
+    return body, 0.0, len(ii)
+
+
 def canonical_tour(sequence) -> tuple[int, ...]:
     """``canonical_tour`` (graph.py:106-115)."""
     body = list(sequence[:-1])
