@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_two_opt_bound(BoundArgs a) {
   const int n = a.n;
   const unsigned below = lanemask_lt();
   uint16_t* tr = reinterpret_cast<uint16_t*>(smem);  // tour, tr[n] = tr[0]
-  double* dd = reinterpret_cast<double*>(smem + a.off_d);
+  const double* dd = a.dcache + (size_t)p * a.np;  // d in fp64 (cached)
   float* hv = reinterpret_cast<float*>(smem + a.off_h);
   float2* cm = reinterpret_cast<float2*>(smem + a.off_c);  // minima of a_i
   int* lpos = reinterpret_cast<int*>(smem + a.off_pos);
@@ -185,9 +185,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_two_opt_bound(BoundArgs a) {
   uint32_t* pr = reinterpret_cast<uint32_t*>(smem + a.off_pairs) +
                  warp * kPairCap;
   const uint16_t* tour = a.tours + (size_t)p * a.np;
-  const double* dg = a.dcache + (size_t)p * a.np;
+  const double* dg = dd;
 
-  // ---- the tour, its edge costs and its cities' minima in shared memory
+  // ---- the tour, its edge costs (rounded up) and its cities' minima in
+  // shared memory
   for (int i0 = 0; i0 < n; i0 += 4 * NT) {
     int t[4];
     double d[4];
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_two_opt_bound(BoundArgs a) {
       const int i = i0 + k * NT + tid;
       if (i < n) {
         tr[i] = (uint16_t)t[k];
-        dd[i] = d[k];
+        hv[i] = __double2float_ru(d[k]);  // d rounded up; h below
         cm[i] = c[k];
       }
     }
@@ -229,18 +230,18 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_two_opt_bound(BoundArgs a) {
     const float2 ca = cm[i], cs = cm[i + 1];
     const float f = __fmul_rd(0.5f, __fadd_rd(ca.x, cs.x));
     const float g = __fmul_rd(0.5f, __fadd_rd(ca.y, cs.y));
-    const float h = __fsub_ru(__double2float_ru(dd[i]), fminf(f, g));
+    const float h = __fsub_ru(hv[i], fminf(f, g));
     hv[i] = h;
     if (larg < 0 || h > lmax) {
       lmax = h;
       larg = i;
     }
   }
-  // seed rows: the largest h of each group of 8 threads (NT / 8 seeds among
+  // seed rows: the largest h of each group of 32 / SPW threads (NT / 8 seeds among
   // the longest edges; any rows give a valid threshold, long edges a tight
   // one), and the maximum over the tour
-#pragma unroll
   constexpr int GL = 32 / SPW;  // lanes per seed group
+#pragma unroll
   for (int o = 1; o < GL; o <<= 1) {
     const float m2 = __shfl_xor_sync(0xffffffffu, lmax, o);
     const int a2 = __shfl_xor_sync(0xffffffffu, larg, o);
@@ -249,12 +250,13 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_two_opt_bound(BoundArgs a) {
       larg = a2;
     }
   }
-  if (lane % GL == 0) lpos[warp * SPW + lane / GL] = larg;
   float hm = lmax;
 #pragma unroll
   for (int o = GL; o < 32; o <<= 1)
     hm = fmaxf(hm, __shfl_xor_sync(0xffffffffu, hm, o));
   if (lane == 0) s_hmax[warp] = hm;
+  __syncthreads();  // the minima (aliased by the row list) are dead now
+  if (lane % GL == 0) lpos[warp * SPW + lane / GL] = larg;
   __syncthreads();
   float hmax = s_hmax[0];
   for (int w = 1; w < NW; ++w) hmax = fmaxf(hmax, s_hmax[w]);
@@ -485,25 +487,26 @@ struct BoundLayout {
   uint32_t off_d, off_h, off_c, off_pos, off_lh, off_pairs, bytes;
 };
 
-// dynamic shared memory of one CTA: tour (u16, n + 1), d (f64, n), h (f32,
-// n), the cities' minima (f32 x 2, n + 1), the row list (positions, h;
-// rmax each), the warps' pair lists
-BoundLayout bound_layout(int n, int rmax) {
+// dynamic shared memory of one CTA: tour (u16, n + 1), h (f32, n), then
+// the cities' minima (f32 x 2, n + 1; the h pass only) aliased with the row
+// list (positions, h; rmax each) and the warps' pair lists
+BoundLayout bound_layout(int n, int rmax, int nt) {
   BoundLayout L;
   int64_t o = round_up(2 * (int64_t)(n + 1), 16);
-  L.off_d = (uint32_t)o;
-  o += 8 * (int64_t)n;
   L.off_h = (uint32_t)o;
   o = round_up(o + 4 * (int64_t)n, 16);
+  const int64_t u0 = o;
   L.off_c = (uint32_t)o;
-  o += 8 * (int64_t)(n + 1);
+  const int64_t cend = o + 8 * (int64_t)(n + 1);
   L.off_pos = (uint32_t)o;
   o = round_up(o + 4 * (int64_t)std::max(rmax, kSeedRows), 16);
   L.off_lh = (uint32_t)o;
   o = round_up(o + 4 * (int64_t)rmax, 16);
   L.off_pairs = (uint32_t)o;
-  o += 4 * (int64_t)kPairCap * (kBoundThreads / 32);
-  L.bytes = (uint32_t)round_up(o, 128);
+  o += 4 * (int64_t)kPairCap * (nt / 32);
+  (void)u0;
+  L.off_d = 0;
+  L.bytes = (uint32_t)round_up(std::max(o, cend), 128);
   return L;
 }
 
@@ -532,7 +535,7 @@ cudaError_t bound_prepare(const double* cost, int64_t ld, int32_t n,
   // finite matrices of moderate magnitude only (h and the threshold stay
   // finite); others keep the full scan
   if (!(maxabs < 1e300)) return cudaSuccess;
-  const BoundLayout L = bound_layout(n, bound_rmax());
+  const BoundLayout L = bound_layout(n, bound_rmax(), kBoundThreads);
   if (L.bytes > kBoundSmem) return cudaSuccess;
   float2* cmn = reinterpret_cast<float2*>(buf);
   k_bound_minima<<<(n + 7) / 8, 256, 0, s>>>(cost, ld, n, cmn);
@@ -573,7 +576,12 @@ cudaError_t launch_two_opt_bound(const TwoOptPlan& pl, int32_t n, int32_t np,
   a.rmax = bound_rmax();
   a.maxpeel = kMaxPeel;
   if (const char* e = getenv("DPSO_BOUND_PEEL")) a.maxpeel = atoi(e);
-  const BoundLayout L = bound_layout(n, a.rmax);
+  // small swarms: 256 threads per particle (shorter per-particle latency
+  // chains); large swarms: 128 (more particles per SM, fewer seed pairs)
+  bool wide = count < 148 * 16;
+  constexpr int SPW_W = 4;  // seed rows per warp (2 measured slower at C2)
+  if (const char* e = getenv("DPSO_BOUND_NT")) wide = atoi(e) == 256;
+  const BoundLayout L = bound_layout(n, a.rmax, wide ? 256 : 128);
   a.off_d = L.off_d;
   a.off_h = L.off_h;
   a.off_c = L.off_c;
@@ -583,11 +591,6 @@ cudaError_t launch_two_opt_bound(const TwoOptPlan& pl, int32_t n, int32_t np,
   const size_t smem = L.bytes;
   cudaError_t e = cudaMemsetAsync(a.fb, 0, 4, s);
   if (e) return e;
-  // small swarms: 256 threads per particle (shorter per-particle latency
-  // chains); large swarms: 128 (more particles per SM, fewer seed pairs)
-  bool wide = count < 148 * 16;
-  constexpr int SPW_W = 4;  // seed rows per warp (2 measured slower at C2)
-  if (const char* e = getenv("DPSO_BOUND_NT")) wide = atoi(e) == 256;
   const void* kern = wide ? (const void*)k_two_opt_bound<256, SPW_W>
                           : (const void*)k_two_opt_bound<128, 4>;
   e = set_dyn_smem(kern, smem);
