@@ -77,20 +77,6 @@ __device__ __forceinline__ bool lex_less(double d1, int i1, int j1, double d2,
   return (i1 < i2) || (i1 == i2 && j1 < j2);
 }
 
-__device__ __forceinline__ void warp_lexmin(double& d, int& i, int& j) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double d2 = __shfl_xor_sync(0xffffffffu, d, o);
-    const int i2 = __shfl_xor_sync(0xffffffffu, i, o);
-    const int j2 = __shfl_xor_sync(0xffffffffu, j, o);
-    if (lex_less(d2, i2, j2, d, i, j)) {
-      d = d2;
-      i = i2;
-      j = j2;
-    }
-  }
-}
-
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -142,24 +128,57 @@ __device__ __forceinline__ void eval_list(const BoundArgs& a, int np,
   }
 }
 
-// CTA-wide lexicographic minimum (every thread gets it).
+// Warp-wide minimum of d (every lane gets it).
+__device__ __forceinline__ double warp_dmin(double d) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+    d = fmin(d, __shfl_xor_sync(0xffffffffu, d, o));
+  return d;
+}
+
+// CTA-wide minimum of d (every thread gets it): the seed threshold needs
+// the value only.
+__device__ __forceinline__ double cta_dmin(double d, double* rd, int lane,
+                                           int warp, int nw) {
+  d = warp_dmin(d);
+  if (lane == 0) rd[warp] = d;
+  __syncthreads();
+  d = rd[0];
+  for (int w = 1; w < nw; ++w) d = fmin(d, rd[w]);
+  __syncthreads();
+  return d;
+}
+
+// Warp-wide lexicographic (delta, i, j) minimum: the minimum delta, then
+// the smallest (i, j) among the lanes holding it (i, j < 2^16), in lane 0.
+__device__ __forceinline__ void warp_lexmin_fast(double& d, int& i, int& j) {
+  const double m = warp_dmin(d);
+  const unsigned key =
+      d == m ? ((unsigned)i << 16) | (unsigned)j : 0xFFFFFFFFu;
+  const unsigned k = __reduce_min_sync(0xffffffffu, key);
+  d = m;
+  i = k == 0xFFFFFFFFu ? INT_MAX : (int)(k >> 16);
+  j = k == 0xFFFFFFFFu ? INT_MAX : (int)(k & 0xFFFFu);
+}
+
+// CTA-wide lexicographic minimum, in thread 0.
 __device__ __forceinline__ void cta_lexmin(double& d, int& i, int& j,
                                            double* rd, int* ri, int* rj,
                                            int lane, int warp, int nw) {
-  warp_lexmin(d, i, j);
+  warp_lexmin_fast(d, i, j);
   if (lane == 0) {
     rd[warp] = d;
     ri[warp] = i;
     rj[warp] = j;
   }
   __syncthreads();
-  for (int w = 0; w < nw; ++w)
-    if (lex_less(rd[w], ri[w], rj[w], d, i, j)) {
-      d = rd[w];
-      i = ri[w];
-      j = rj[w];
-    }
-  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int w = 1; w < nw; ++w)
+      if (lex_less(rd[w], ri[w], rj[w], d, i, j)) {
+        d = rd[w];
+        i = ri[w];
+        j = rj[w];
+      }
 }
 
 template <int NT, int SPW>
@@ -308,9 +327,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_two_opt_bound(BoundArgs a) {
       }
     }
   }
-  double t0 = bd;
-  int ti = bi, tj = bj;
-  cta_lexmin(t0, ti, tj, s_rd, s_ri, s_rj, lane, warp, NW);
+  const double t0 = cta_dmin(bd, s_rd, lane, warp, NW);
   const double tq = fmin(t0, -1e-12);
   // skip a pair iff h_i + h_j < thr <= -tq - slack (exactly: the fp32
   // tests round up)
@@ -577,7 +594,8 @@ cudaError_t launch_two_opt_bound(const TwoOptPlan& pl, int32_t n, int32_t np,
   a.maxpeel = kMaxPeel;
   if (const char* e = getenv("DPSO_BOUND_PEEL")) a.maxpeel = atoi(e);
   // small swarms: 256 threads per particle (shorter per-particle latency
-  // chains); large swarms: 128 (more particles per SM, fewer seed pairs)
+  // chains; 128 and 512 measured slower at C2: 0.066 / 0.055 vs 0.050 ms);
+  // large swarms: 128 (more particles per SM, fewer seed pairs)
   bool wide = count < 148 * 16;
   constexpr int SPW_W = 4;  // seed rows per warp (2 measured slower at C2)
   if (const char* e = getenv("DPSO_BOUND_NT")) wide = atoi(e) == 256;
