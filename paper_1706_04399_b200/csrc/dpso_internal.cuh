@@ -65,6 +65,7 @@ struct CostStats {
   int nonintegral;
   int negmax;                      // some entry equals -max|C|
   unsigned long long second_bits;  // bits of max |C| over |C| < max|C|
+  int asym;                        // some C[a][b] differs bitwise from C[b][a]
 };
 
 struct TwoOptPlan {
@@ -113,6 +114,9 @@ struct TwoOptPlan {
   int32_t* bound_fb;
   unsigned long long* bound_pairs;  // pairs evaluated (cumulative)
   double bound_slack;
+  // the matrix equals its transpose bit for bit: a reversed tour segment
+  // keeps its edge costs (the 2-opt apply moves them instead of gathering)
+  int symmetric;
 };
 
 struct TwoOptRes {

@@ -826,6 +826,7 @@ struct ApplyArgs {
   double* dcache;
   const double* cost64;  // capped plan: re-evaluate the chosen pair in fp64
   const double* dcache_in;  // (with the tour's d values)
+  int sym;  // symmetric matrix: reversed edges keep their costs
 };
 
 __global__ void __launch_bounds__(128) k_two_opt_apply(ApplyArgs a) {
@@ -871,16 +872,42 @@ __global__ void __launch_bounds__(128) k_two_opt_apply(ApplyArgs a) {
   const int i = s_move[1], j = s_move[2];
   uint16_t* t = a.tours + (size_t)p * a.np;
   const int len = j - i;  // reverse t[i+1 .. j]
-  for (int u = tid; u < len / 2; u += blockDim.x) {
-    uint16_t x = t[i + 1 + u];
-    t[i + 1 + u] = t[j - u];
-    t[j - u] = x;
-  }
-  __syncthreads();
-  if (a.cost) {
-    for (int k = i + tid; k <= j && k < a.n; k += blockDim.x) {
-      int u = t[k], w = t[k + 1 == a.n ? 0 : k + 1];
-      a.dcache[(size_t)p * a.np + k] = ld_cost(a.cost + (size_t)u * a.ld + w);
+  if (a.cost && a.sym) {
+    // symmetric matrix: edge k in (i, j) of the new tour is old edge
+    // i + j - k reversed, same cost bits: reverse d[i+1 .. j-1] along with
+    // the tour; only the two new edges i and j are gathered
+    double* dg = a.dcache + (size_t)p * a.np;
+    const int m = len - 1;  // d[i+1 .. j-1]
+    for (int u = tid; u < len / 2 || u < m / 2; u += blockDim.x) {
+      if (u < len / 2) {
+        uint16_t x = t[i + 1 + u];
+        t[i + 1 + u] = t[j - u];
+        t[j - u] = x;
+      }
+      if (u < m / 2) {
+        const double y = dg[i + 1 + u];
+        dg[i + 1 + u] = dg[j - 1 - u];
+        dg[j - 1 - u] = y;
+      }
+    }
+    __syncthreads();
+    if (tid < 2) {
+      const int k = tid == 0 ? i : j;
+      const int u = t[k], w = t[k + 1 == a.n ? 0 : k + 1];
+      dg[k] = ld_cost(a.cost + (size_t)u * a.ld + w);
+    }
+  } else {
+    for (int u = tid; u < len / 2; u += blockDim.x) {
+      uint16_t x = t[i + 1 + u];
+      t[i + 1 + u] = t[j - u];
+      t[j - u] = x;
+    }
+    __syncthreads();
+    if (a.cost) {
+      for (int k = i + tid; k <= j && k < a.n; k += blockDim.x) {
+        int u = t[k], w = t[k + 1 == a.n ? 0 : k + 1];
+        a.dcache[(size_t)p * a.np + k] = ld_cost(a.cost + (size_t)u * a.ld + w);
+      }
     }
   }
   if (a.fit) {
@@ -951,11 +978,14 @@ __global__ void k_cost_second(const double* cost, int64_t ld, int n,
                               CostStats* st) {
   const double mx = __longlong_as_double((long long)st->maxabs_bits);
   unsigned long long m2 = 0;
-  int neg = 0;
+  int neg = 0, asym = 0;
   const int64_t total = (int64_t)n * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const double v = cost[(e / n) * ld + e % n];
+    const int64_t r = e / n, c = e % n;
+    const double v = cost[r * ld + c];
+    if (c > r)
+      asym |= __double_as_longlong(v) != __double_as_longlong(cost[c * ld + r]);
     const double a = fabs(v);
     if (a < mx) {
       const unsigned long long b = (unsigned long long)__double_as_longlong(a);
@@ -969,10 +999,12 @@ __global__ void k_cost_second(const double* cost, int64_t ld, int n,
     const unsigned long long x = __shfl_xor_sync(0xffffffffu, m2, o);
     m2 = x > m2 ? x : m2;
     neg |= __shfl_xor_sync(0xffffffffu, neg, o);
+    asym |= __shfl_xor_sync(0xffffffffu, asym, o);
   }
   if ((threadIdx.x & 31) == 0) {
     atomicMax(&st->second_bits, m2);
     if (neg) atomicOr(&st->negmax, 1);
+    if (asym) atomicOr(&st->asym, 1);
   }
 }
 
@@ -1084,6 +1116,7 @@ cudaError_t two_opt_prepare(const double* cost, int64_t ld, int32_t n,
   if (e) return e;
   double maxabs_raw;
   memcpy(&maxabs_raw, &h.maxabs_bits, sizeof maxabs_raw);
+  pl->symmetric = !h.asym && !getenv("DPSO_NO_SYM");
   {
     // a virtual level (entries equal to max|C|, > 64 x every other |C|):
     // cap it at 5 x the finite maximum in the fp32/fp16 rows (> the spread
@@ -1386,6 +1419,7 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
                                    : pl.vfrom > 0.0 && pl.mode != kScanFP64;
   b.cost64 = capped ? pl.cost : nullptr;
   b.dcache_in = dcache;
+  b.sym = pl.symmetric;
   if (n < 4) {
     // _best_exchange returns (body, 0.0) for n < 4 (solver.py:91-93)
     if (delta_out) cudaMemsetAsync(delta_out, 0, sizeof(double) * count, s);
