@@ -311,13 +311,17 @@ def kernels_per_generation(cfg, band=0, bound=0):
     at entry, but they still launch.  band: dpso_scan_band (1/2: the band
     scan and its column-record kernel).  bound: the bounded scan runs
     first; the band scan launches after it every pass (it exits at once
-    when the bounded scan hands it no particle)."""
+    when the bounded scan hands it no particle), without its column-record
+    kernel."""
     k = 1 + 1 + 1  # gen_begin, update, fitness (with the pbest copy)
     k += 1         # select
     if cfg.get("ee", True):
         # scan kernels (bounded scan, or the band / column scan), apply,
         # finalize
-        k += (1 if bound else 0) + band_kernels(cfg, band)
+        # (with the bounded scan, which writes the column records of the
+        # particles it hands over, the record kernel does not launch: the
+        # bounded scan takes its place in the count)
+        k += band_kernels(cfg, band)
         k += 2
     m = 6          # mutation: hash, rank, dedupe, verify, lists, copy
     if RNG == "philox":

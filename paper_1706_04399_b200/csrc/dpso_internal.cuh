@@ -279,7 +279,8 @@ cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
                                 cudaStream_t s, int reserve_sms = 0,
                                 const int32_t* plist = nullptr,
                                 const int32_t* pcnt = nullptr,
-                                int32_t* runs = nullptr);
+                                int32_t* runs = nullptr,
+                                bool cols_ready = false);
 // bounded scan (k_two_opt_bound.cu): workspace bytes for count particles
 // (0: not available at this n), preparation (needs the band plan), launch
 constexpr int kBoundMaxN = kBandMaxN;
@@ -290,7 +291,8 @@ cudaError_t bound_prepare(const double* cost, int64_t ld, int32_t n,
 cudaError_t launch_two_opt_bound(const TwoOptPlan& pl, int32_t n, int32_t np,
                                  const uint16_t* tours, const double* dcache,
                                  int32_t count, TwoOptRes* res, int32_t chunks,
-                                 const DevCtl* ctl, cudaStream_t s);
+                                 const DevCtl* ctl, cudaStream_t s,
+                                 int32_t* runs = nullptr);
 int two_opt_pick_chunks(int32_t n, int32_t P);
 
 // A random fp64 gather from the cost matrix (edge costs C[a][b]).  sm_100

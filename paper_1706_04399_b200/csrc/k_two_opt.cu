@@ -1338,17 +1338,17 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
       // launch that exits at once when the list is empty: measured as fast
       // as a conditional graph node around it, which ncu cannot profile)
       const bool bound = pl.bound != 0;
-      if (!e && bound)
-        e = launch_two_opt_bound(pl, n, np, tours, dcache, count, res, chunks,
-                                 ctl, s);
       int32_t* runs =
           ctl ? &const_cast<DevCtl*>(ctl)->band_runs : nullptr;
+      if (!e && bound)
+        e = launch_two_opt_bound(pl, n, np, tours, dcache, count, res, chunks,
+                                 ctl, s, runs);
       if (!e && pl.band_mode == 2) e = cudaMemsetAsync(a.ovf, 0, 4, s);
       if (!e)
         e = launch_two_opt_band(pl, n, np, tours, dcache, count, res, chunks,
                                 a.ovf, ctl, s, reserve_sms,
                                 bound ? pl.bound_fb + 1 : nullptr,
-                                bound ? pl.bound_fb : nullptr, runs);
+                                bound ? pl.bound_fb : nullptr, runs, bound);
       if (!e && pl.band_mode == 2) {
         k_two_opt_rescan64<<<2 * 148, 128, 0, s>>>(a);
         e = cudaGetLastError();

@@ -1040,7 +1040,7 @@ cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
                                 int32_t* ovf, const DevCtl* ctl,
                                 cudaStream_t s, int reserve_sms,
                                 const int32_t* plist, const int32_t* pcnt,
-                                int32_t* runs) {
+                                int32_t* runs, bool cols_ready) {
   if (!pl.band_cols || count > pl.band_cols_cap) return cudaErrorInvalidValue;
   BandArgs a;
   memset(&a, 0, sizeof a);
@@ -1067,9 +1067,11 @@ cudaError_t launch_two_opt_band(const TwoOptPlan& pl, int32_t n, int32_t np,
   a.cols = pl.band_cols;
   a.plist = plist;
   a.pcnt = pcnt;
-  k_band_cols<<<count, 256, 0, s>>>(tours, np, dcache, n, a.cw, count,
-                                     a.scale, a.vfrom, a.vto, pl.band_cols,
-                                     ctl, pl.band_es, plist, pcnt, runs);
+  // (the bounded scan writes the records of the particles it lists)
+  if (!cols_ready)
+    k_band_cols<<<count, 256, 0, s>>>(tours, np, dcache, n, a.cw, count,
+                                       a.scale, a.vfrom, a.vto, pl.band_cols,
+                                       ctl, pl.band_es, plist, pcnt, runs);
   cudaError_t e = cudaGetLastError();
   if (e) return e;
   const int rpl = pl.band_rpl;

@@ -67,6 +67,12 @@ struct BoundArgs {
   double slack;
   int rmax;     // row-list capacity
   int maxpeel;  // rows peeled before the band fallback
+  // the band scan's column records of a fallback particle, written here
+  // (k_band_cols' layout: O = es a_c at k = c + 3, D = round(d_c s))
+  int32_t* cols;
+  int cw, es;
+  double scale, vfrom, vto;
+  int32_t* runs;  // passes with a fallback (DevCtl::band_runs), nullable
   uint32_t off_d, off_h, off_c, off_pos, off_lh, off_pairs;  // shared
 };
 
@@ -424,8 +430,27 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_two_opt_bound(BoundArgs a) {
     __syncthreads();
     if (peel >= a.maxpeel || m == INT_MAX || !(hmv > -FLT_MAX)) {
       // weak bound everywhere (a nearly 2-opt-optimal tour): the band
-      // scan takes the particle
-      if (tid == 0) a.fb[1 + atomicAdd(&a.fb[0], 1)] = p;
+      // scan takes the particle; its column records from here
+      int32_t* O = a.cols + (size_t)p * 2 * a.cw;
+      int32_t* D = O + a.cw;
+      for (int k = tid; k < a.cw; k += NT) {
+        const int kk = k - 3;
+        O[k] = (kk >= 0 && kk <= n) ? a.es * (int)tr[kk] : 0;  // tr[n] = a_0
+        if (k < n) {
+          double d = dd[k];
+          if (a.vfrom > 0.0 && d == a.vfrom) d = a.vto;
+          D[k] = __double2int_rn(d * a.scale);
+        } else {
+          D[k] = -0x40000000;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        const int at = atomicAdd(&a.fb[0], 1);
+        a.fb[1 + at] = p;
+        if (at == 0 && a.runs) atomicAdd(a.runs, 1);
+      }
       return;
     }
     // row m against every row it reaches
@@ -573,7 +598,8 @@ cudaError_t bound_prepare(const double* cost, int64_t ld, int32_t n,
 cudaError_t launch_two_opt_bound(const TwoOptPlan& pl, int32_t n, int32_t np,
                                  const uint16_t* tours, const double* dcache,
                                  int32_t count, TwoOptRes* res, int32_t chunks,
-                                 const DevCtl* ctl, cudaStream_t s) {
+                                 const DevCtl* ctl, cudaStream_t s,
+                                 int32_t* runs) {
   BoundArgs a;
   memset(&a, 0, sizeof a);
   a.cost = pl.cost;
@@ -592,6 +618,13 @@ cudaError_t launch_two_opt_bound(const TwoOptPlan& pl, int32_t n, int32_t np,
   a.slack = pl.bound_slack;
   a.rmax = bound_rmax();
   a.maxpeel = kMaxPeel;
+  a.cols = pl.band_cols;
+  a.cw = band_cw(n);
+  a.es = pl.band_es;
+  a.scale = pl.band_scale;
+  a.vfrom = pl.band_vfrom;
+  a.vto = pl.band_vto;
+  a.runs = runs;
   if (const char* e = getenv("DPSO_BOUND_PEEL")) a.maxpeel = atoi(e);
   // small swarms: 256 threads per particle (shorter per-particle latency
   // chains; 128 and 512 measured slower at C2: 0.066 / 0.055 vs 0.050 ms);
