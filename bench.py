@@ -318,10 +318,10 @@ def kernels_per_generation(cfg, band=0, bound=0):
     if cfg.get("ee", True):
         # scan kernels (bounded scan, or the band / column scan), apply,
         # finalize
-        # (with the bounded scan, which writes the column records of the
-        # particles it hands over, the record kernel does not launch: the
-        # bounded scan takes its place in the count)
-        k += band_kernels(cfg, band)
+        # with the bounded scan: bounded scan + band scan (the bounded scan
+        # writes the column records of the particles it hands over, and the
+        # apply re-scans a FILTER overflow itself)
+        k += 2 if bound else band_kernels(cfg, band)
         k += 2
     m = 6          # mutation: hash, rank, dedupe, verify, lists, copy
     if RNG == "philox":

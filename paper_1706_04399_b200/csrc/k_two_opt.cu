@@ -825,8 +825,13 @@ struct ApplyArgs {
   int64_t ld;
   double* dcache;
   const double* cost64;  // capped plan: re-evaluate the chosen pair in fp64
+  const double* cost64r;  // the fp64 matrix (in-apply re-scan)
   const double* dcache_in;  // (with the tour's d values)
   int sym;  // symmetric matrix: reversed edges keep their costs
+  // bounded-scan mode: no separate fp64 re-scan kernel runs; a particle
+  // whose band-scan candidate list overflowed (tagged result, rare) is
+  // re-scanned in fp64 here, by its CTA
+  int ovf_scan;
 };
 
 __global__ void __launch_bounds__(128) k_two_opt_apply(ApplyArgs a) {
@@ -836,17 +841,61 @@ __global__ void __launch_bounds__(128) k_two_opt_apply(ApplyArgs a) {
   __shared__ int s_move[3];
   __shared__ double s_delta;
   __shared__ int s_better;
+  __shared__ double s_wd[4];
+  __shared__ int s_wi[4], s_wj[4];
   const int tid = threadIdx.x;
+  const bool rescan = a.ovf_scan && a.n >= 4 &&
+                      a.res[(size_t)p * a.chunks].i == kOverflowTag;
+  if (rescan) {
+    // every pair in fp64 with the reference expression (solver.py:94-100)
+    const uint16_t* t = a.tours + (size_t)p * a.np;
+    const double* dg = a.dcache_in + (size_t)p * a.np;
+    const int n = a.n, lane = tid & 31, warp = tid >> 5;
+    double bd = __longlong_as_double(0x7ff0000000000000ll);
+    int ei = 0x7fffffff, ej = 0x7fffffff;
+    for (int i = warp; i < n - 1; i += 4) {
+      const int ai = t[i], si = t[i + 1];
+      const double di = dg[i];
+      for (int j = i + 1 + lane; j < n; j += 32) {
+        const int aj = t[j], sj = t[j + 1 == n ? 0 : j + 1];
+        double v = __dadd_rn(ld_cost(a.cost64r + (size_t)ai * a.ld + aj),
+                             ld_cost(a.cost64r + (size_t)si * a.ld + sj));
+        v = __dsub_rn(v, di);
+        v = __dsub_rn(v, dg[j]);
+        if (res_less(v, i, j, bd, ei, ej)) {
+          bd = v;
+          ei = i;
+          ej = j;
+        }
+      }
+    }
+    warp_argmin(bd, ei, ej);
+    if (lane == 0) {
+      s_wd[warp] = bd;
+      s_wi[warp] = ei;
+      s_wj[warp] = ej;
+    }
+    __syncthreads();
+  }
   if (tid == 0) {
     double best = __longlong_as_double(0x7ff0000000000000ll);
     int bi = 0x7fffffff, bj = 0x7fffffff;
     const TwoOptRes* r = a.res + (size_t)p * a.chunks;
-    for (int c = 0; c < a.chunks; ++c)
-      if (res_less(r[c].delta, r[c].i, r[c].j, best, bi, bj)) {
-        best = r[c].delta;
-        bi = r[c].i;
-        bj = r[c].j;
-      }
+    if (rescan) {
+      for (int w = 0; w < 4; ++w)
+        if (res_less(s_wd[w], s_wi[w], s_wj[w], best, bi, bj)) {
+          best = s_wd[w];
+          bi = s_wi[w];
+          bj = s_wj[w];
+        }
+    } else {
+      for (int c = 0; c < a.chunks; ++c)
+        if (res_less(r[c].delta, r[c].i, r[c].j, best, bi, bj)) {
+          best = r[c].delta;
+          bi = r[c].i;
+          bj = r[c].j;
+        }
+    }
     if (a.cost64 && bi != 0x7fffffff && bj != 0x7fffffff &&
         best != __longlong_as_double(0x7ff0000000000000ll)) {
       // the scan compared capped values: the reference's fp64 delta of the
@@ -1349,7 +1398,8 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
                                 a.ovf, ctl, s, reserve_sms,
                                 bound ? pl.bound_fb + 1 : nullptr,
                                 bound ? pl.bound_fb : nullptr, runs, bound);
-      if (!e && pl.band_mode == 2) {
+      // (bounded-scan mode: the apply re-scans a tagged particle itself)
+      if (!e && pl.band_mode == 2 && !bound) {
         k_two_opt_rescan64<<<2 * 148, 128, 0, s>>>(a);
         e = cudaGetLastError();
       }
@@ -1420,6 +1470,8 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
   b.cost64 = capped ? pl.cost : nullptr;
   b.dcache_in = dcache;
   b.sym = pl.symmetric;
+  b.cost64r = pl.cost;
+  b.ovf_scan = pl.band_mode == 2 && pl.bound;
   if (n < 4) {
     // _best_exchange returns (body, 0.0) for n < 4 (solver.py:91-93)
     if (delta_out) cudaMemsetAsync(delta_out, 0, sizeof(double) * count, s);

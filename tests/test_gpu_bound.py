@@ -238,3 +238,22 @@ def test_bound_whole_solves_match_oracle(pkg, rmax, peel, monkeypatch):
         assert gpu.best_tour_ == ref.best_tour_
         assert gpu.convergence_ == ref.convergence_
         assert gpu.n_generations_ == ref.n_generations_
+
+
+def test_bound_fallback_filter_overflow(pkg, monkeypatch):
+    # particles handed to the band scan (peel limit 0, small row list) on a
+    # non-integer lattice: thousands of exactly tied deltas overflow the
+    # FILTER candidate lists, and the apply re-scans those particles in
+    # fp64 itself (no separate re-scan kernel in bounded-scan mode)
+    monkeypatch.setenv("DPSO_BOUND_RMAX", "32")
+    monkeypatch.setenv("DPSO_BOUND_PEEL", "0")
+    rng = np.random.default_rng(13)
+    for n in (144, 400):
+        cost = grid(n) / 3.0
+        check(pkg, cost, perms(rng, 12, n), ("lattice-fallback", n))
+        params = dict(n_particles=16, max_generations=12,
+                      stall_generations=12, random_state=4)
+        gpu = pkg.DiscreteSwarmSolver(**params).fit(cost)
+        ref = O.OracleSolver(**params).fit(cost)
+        assert gpu.best_tour_ == ref.best_tour_
+        assert gpu.convergence_ == ref.convergence_
