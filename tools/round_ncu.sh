@@ -13,8 +13,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none \
 echo "launch list rc=$?"
 for c in c2 c3; do
   timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:k_two_opt_bound -s 2 -c 1 -o gpurun_out/bound_${tag}_$c -f \
-    python bench.py --config $c --steps 3 --warmup 3 --profile-gens 1 \
+    -k regex:k_two_opt_bound -s 8 -c 1 -o gpurun_out/bound_${tag}_$c -f \
+    python bench.py --config $c --steps 12 --warmup 3 --profile-gens 1 \
     --no-cpu-baseline --no-e2e > gpurun_out/ncu_full_${tag}_$c.log 2>&1
   echo "ncu full bound $c rc=$?"
 done
