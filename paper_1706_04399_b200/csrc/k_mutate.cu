@@ -816,7 +816,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample(
   const int64_t cur = (int64_t)b.ev_cursor[e];
   const int D = sample_draws(n, k);
   int rej = 0;
-  if (!tail && vals_cap > 0 && cur - sv.h + D <= sv.cap) {
+  if (!tail && D <= vals_cap && cur - sv.h + D <= sv.cap) {
     for (int d = lane; d < D; d += 32) {
       const uint32_t rng = sample_bound(n, k, d);
       const uint32_t u = sv.buf[cur - sv.h + d];
@@ -1032,11 +1032,15 @@ cudaError_t launch_mutation_post(const SwarmView& v, cudaStream_t s) {
                           kSampleWarps * 32, 0, s>>>(v);
     return cudaGetLastError();
   }
-  // per warp: draw values (<= 2n u32) + Floyd bitmap / tail arange; without
-  // room for the draw buffer the warp samples sequentially
-  const int scratch_words =
-      (int)round_up(std::max<int64_t>((n + 31) / 32, (n + 1) / 2), 4);
-  int vals_cap = (int)round_up(2 * (int64_t)n + 2, 4);
+  // per warp: draw values + Floyd bitmap (n bits) / tail arange (n u16,
+  // n > 10000 only); without room for the draw buffer the warp samples
+  // sequentially.  An event draws D = F + 2k - 1 <= 4k <= n + 4 values
+  // (k <= max(2, n / 4): solver.py:235-236): sizing the buffers by that
+  // instead of 2n, and the bitmap by n bits, doubles the warps per SM at
+  // C3 / C4
+  const int scratch_words = (int)round_up(
+      n > 10000 ? (n + 1) / 2 : (n + 31) / 32, 4);
+  int vals_cap = (int)round_up((int64_t)n + 8, 4);
   const int idx_words = (n + 1) / 2;
   constexpr size_t kBudget = 200 * 1024;
   if ((size_t)(vals_cap + scratch_words + idx_words) * 4 > kBudget)
