@@ -794,8 +794,82 @@ struct PcgNext {  // next32() regenerated from the stream state
 // n-bit Floyd bitmap (or arange(n) for the tail shuffle).
 constexpr int kSampleWarps = 4;
 
+// numpy's choice(n, 2k, replace=False) - Floyd's sampler then the
+// _shuffle_int of the 2k values - from the event's bounded draws vals,
+// data-parallel over one warp (the reference's loops are sequential):
+//  Floyd: step t (value j_t = n - 2k + t) draws v_t; it adds j_t instead
+//    iff v_t is already in the set: iff an earlier step drew v_t (the first
+//    step to draw each value: an atomicMin per value) or v_t = j_s of an
+//    earlier step s that itself collided (s = v_t - (n - 2k) < t):
+//    col(t) = dup(t) or col(s), iterated to the fixpoint (links strictly
+//    decrease).
+//  Shuffle: step i = 2k-1 .. 1 swaps positions i and w_i <= i, and
+//    position i is final after it.  Its value is whatever position w_i held
+//    just before step i: the value written there by the most recent earlier
+//    step (the smallest i' > i with w_i' = w_i), which is what position i'
+//    held just before step i' (the smallest writer of i' above i'), and so
+//    on back to an original value.  Each position's writers form a short
+//    list (atomicExch heads), searched per query.
+// first: max(n, 2k) words; nxt, sidx: 2k u16; col: 2k bytes.
+__device__ void floyd_shuffle_warp(const uint32_t* vals, int n, int size,
+                                   uint32_t* first, uint16_t* nxt,
+                                   uint8_t* col, uint16_t* sidx,
+                                   uint16_t* out, int lane) {
+  const int nmz = n - size;  // j_t = nmz + t
+  const int zero = nmz == 0 ? 1 : 0;  // j_0 == 0 takes no draw
+  const int F = size - zero;         // Floyd draws
+  auto vt = [&](int t) -> uint32_t {
+    return (zero && t == 0) ? 0u : vals[t - zero];
+  };
+  for (int v = lane; v < n; v += 32) first[v] = 0xFFFFFFFFu;
+  __syncwarp();
+  for (int t = lane; t < size; t += 32) atomicMin(&first[vt(t)], (uint32_t)t);
+  __syncwarp();
+  for (int t = lane; t < size; t += 32) col[t] = first[vt(t)] < (uint32_t)t;
+  __syncwarp();
+  for (;;) {
+    int changed = 0;
+    for (int t = lane; t < size; t += 32) {
+      if (col[t]) continue;
+      const int v = (int)vt(t);
+      if (v >= nmz && v - nmz < t && col[v - nmz]) {
+        col[t] = 1;
+        changed = 1;
+      }
+    }
+    __syncwarp();
+    if (!__any_sync(0xffffffffu, changed)) break;
+  }
+  for (int t = lane; t < size; t += 32)
+    sidx[t] = (uint16_t)(col[t] ? (uint32_t)(nmz + t) : vt(t));
+  // the shuffle: step i draws w_i = vals[F + size - 1 - i]; writer lists of
+  // each position (heads in first[], links in nxt[])
+  __syncwarp();
+  for (int x = lane; x < size; x += 32) first[x] = 0xFFFFu;
+  __syncwarp();
+  for (int i = 1 + lane; i < size; i += 32)
+    nxt[i] = (uint16_t)atomicExch(&first[vals[F + size - 1 - i]], (uint32_t)i);
+  __syncwarp();
+  // the smallest writer of position x above y (0xFFFF: none)
+  auto above = [&](uint32_t x, uint32_t y) -> uint32_t {
+    uint32_t best = 0xFFFFu;
+    for (uint32_t w = first[x]; w != 0xFFFFu; w = nxt[w])
+      if (w > y && w < best) best = w;
+    return best;
+  };
+  for (int i = lane; i < size; i += 32) {
+    uint32_t x = i == 0 ? 0u : vals[F + size - 1 - i];
+    uint32_t w = above(x, (uint32_t)i);
+    while (w != 0xFFFFu) {
+      x = w;
+      w = above(x, x);
+    }
+    out[i] = sidx[x];
+  }
+}
+
 __global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample(
-    SwarmView v, int vals_cap, int scratch_words) {
+    SwarmView v, int vals_cap, int scratch_words, int par_m) {
   if (!v.ctl->mutating || v.ctl->done) return;
   const MutBufs b = mut_bufs(v, v.ctl->mut_cur);
   extern __shared__ __align__(16) uint32_t sm[];
@@ -806,7 +880,9 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample(
   if (k < 1) return;
   // per warp: vals[vals_cap] | bits/arr[scratch_words] | sidx[idx_words]
   const int idx_words = (n + 1) / 2;
-  uint32_t* vals = sm + (size_t)warp * (vals_cap + scratch_words + idx_words);
+  const int par_words = par_m ? n + (3 * n + 3) / 4 + 1 : 0;
+  uint32_t* vals =
+      sm + (size_t)warp * (vals_cap + scratch_words + idx_words + par_words);
   uint32_t* bits = vals + vals_cap;
   uint16_t* arr = (uint16_t*)bits;
   uint16_t* idx = v.ev_idx + (size_t)e * v.np;
@@ -824,6 +900,16 @@ __global__ void __launch_bounds__(kSampleWarps * 32) k_mut_sample(
       vals[d] = (uint32_t)(((uint64_t)u * (rng + 1u)) >> 32);
     }
     rej = __any_sync(0xffffffffu, rej);
+    if (!rej && par_m) {
+      // data-parallel Floyd + shuffle (floyd_shuffle_warp)
+      __syncwarp();
+      uint16_t* sidx = (uint16_t*)(bits + scratch_words);
+      uint32_t* first = bits + scratch_words + idx_words;  // n words
+      uint16_t* nxt = reinterpret_cast<uint16_t*>(first + n);
+      uint8_t* col = reinterpret_cast<uint8_t*>(nxt + n);
+      floyd_shuffle_warp(vals, n, size, first, nxt, col, sidx, idx, lane);
+      return;
+    }
     if (!rej) {
       __syncwarp();
       for (int i = lane; i < (n + 31) / 32; i += 32) bits[i] = 0;
@@ -1042,17 +1128,26 @@ cudaError_t launch_mutation_post(const SwarmView& v, cudaStream_t s) {
       n > 10000 ? (n + 1) / 2 : (n + 31) / 32, 4);
   int vals_cap = (int)round_up((int64_t)n + 8, 4);
   const int idx_words = (n + 1) / 2;
+  // the data-parallel sampler's arrays (n u32 + n u16 + n bytes per warp;
+  // par_m = 1: on, 0: the serial lane-0 sampler)
+  int par_m = getenv("DPSO_MUT_SERIAL") ? 0 : 1;
+  const int par_words = par_m ? n + (3 * n + 3) / 4 + 1 : 0;
   constexpr size_t kBudget = 200 * 1024;
-  if ((size_t)(vals_cap + scratch_words + idx_words) * 4 > kBudget)
+  if ((size_t)(vals_cap + scratch_words + idx_words + par_words) * 4 >
+      kBudget) {
     vals_cap = 0;
-  const size_t per_warp = (size_t)(vals_cap + scratch_words + idx_words) * 4;
+    par_m = 0;
+  }
+  const size_t per_warp =
+      (size_t)(vals_cap + scratch_words + idx_words + (par_m ? par_words : 0)) * 4;
   const int warps =
       (int)std::max<size_t>(1, std::min<size_t>(kSampleWarps,
                                                 kBudget / per_warp));
   const size_t smem = (size_t)warps * per_warp;
   set_dyn_smem((const void*)k_mut_sample, smem);
   const unsigned grid = (unsigned)((P + warps - 1) / warps);
-  k_mut_sample<<<grid, warps * 32, smem, s>>>(v, vals_cap, scratch_words);
+  k_mut_sample<<<grid, warps * 32, smem, s>>>(v, vals_cap, scratch_words,
+                                              par_m);
   const size_t scratch =
       std::max<size_t>(round_up((n + 31) / 32 * 4, 16), 2 * (size_t)v.np);
   set_dyn_smem((const void*)k_mut_fix, scratch);
