@@ -288,11 +288,22 @@ int64_t bound_bytes(int n, int64_t count);
 cudaError_t bound_prepare(const double* cost, int64_t ld, int32_t n,
                           void* buf, double maxabs, cudaStream_t s,
                           TwoOptPlan* pl);
+// the move applied by the bounded scan itself (nullable pointers as in
+// k_two_opt_apply)
+struct BoundApply {
+  uint16_t* tours;
+  double* dcache;
+  double* fit;
+  double* pfit;
+  uint16_t* pbest;
+  double* delta_out;
+};
 cudaError_t launch_two_opt_bound(const TwoOptPlan& pl, int32_t n, int32_t np,
                                  const uint16_t* tours, const double* dcache,
                                  int32_t count, TwoOptRes* res, int32_t chunks,
                                  const DevCtl* ctl, cudaStream_t s,
-                                 int32_t* runs = nullptr);
+                                 int32_t* runs = nullptr,
+                                 const BoundApply* ap = nullptr);
 int two_opt_pick_chunks(int32_t n, int32_t P);
 
 // A random fp64 gather from the cost matrix (edge costs C[a][b]).  sm_100

@@ -58,6 +58,7 @@ constexpr int kBufs = 3;      // row ring depth per warp
 constexpr int kGroup = 4;     // column blocks (of 32) per uniform skip test
 constexpr int kCand = 4;      // fp32 candidates kept per lane (FILTER32)
 constexpr int kOverflowTag = -2;
+constexpr int kAppliedTag = -3;  // the bounded scan applied the move itself
 
 struct ScanArgs {
   const double* cost;
@@ -844,6 +845,7 @@ __global__ void __launch_bounds__(128) k_two_opt_apply(ApplyArgs a) {
   __shared__ double s_wd[4];
   __shared__ int s_wi[4], s_wj[4];
   const int tid = threadIdx.x;
+  if (a.res[(size_t)p * a.chunks].i == kAppliedTag) return;
   const bool rescan = a.ovf_scan && a.n >= 4 &&
                       a.res[(size_t)p * a.chunks].i == kOverflowTag;
   if (rescan) {
@@ -1389,9 +1391,13 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
       const bool bound = pl.bound != 0;
       int32_t* runs =
           ctl ? &const_cast<DevCtl*>(ctl)->band_runs : nullptr;
+      // with the apply in this call, the bounded scan applies the moves it
+      // resolves itself (k_two_opt_apply skips them)
+      BoundApply ap{tours, dcache_rw, fit, pfit, pbest, delta_out};
+      const bool ap_here = (parts & 2) && dcache_rw && !getenv("DPSO_BOUND_NOAPPLY");
       if (!e && bound)
         e = launch_two_opt_bound(pl, n, np, tours, dcache, count, res, chunks,
-                                 ctl, s, runs);
+                                 ctl, s, runs, ap_here ? &ap : nullptr);
       if (!e && pl.band_mode == 2) e = cudaMemsetAsync(a.ovf, 0, 4, s);
       if (!e)
         e = launch_two_opt_band(pl, n, np, tours, dcache, count, res, chunks,

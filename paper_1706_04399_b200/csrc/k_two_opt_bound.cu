@@ -48,6 +48,7 @@ namespace dpso {
 namespace {
 
 constexpr int kBoundThreads = 256;  // one CTA per particle (at most)
+constexpr int kAppliedTag = -3;     // as k_two_opt.cu: move already applied
 constexpr int kSeedRows = 32;       // seed rows (one per 8 threads, at most)
 constexpr int kPairCap = 256;       // pair-list entries per warp
 constexpr int kMaxPeel = 64;        // rows peeled before the band fallback
@@ -73,6 +74,16 @@ struct BoundArgs {
   int cw, es;
   double scale, vfrom, vto;
   int32_t* runs;  // passes with a fallback (DevCtl::band_runs), nullable
+  // the move applied here (the 2-opt apply's work for the particles this
+  // kernel resolves; k_two_opt_apply then skips them): tours and dcache
+  // are written, fit / pfit / pbest (nullable) and delta_out (nullable)
+  int apply, sym;
+  uint16_t* tours_rw;
+  double* dcache_rw;
+  double* fit;
+  double* pfit;
+  uint16_t* pbest;
+  double* delta_out;
   uint32_t off_d, off_h, off_c, off_pos, off_lh, off_pairs;  // shared
 };
 
@@ -499,8 +510,71 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_two_opt_bound(BoundArgs a) {
   if (lane == 0 && evals) atomicAdd(a.pairs, (unsigned long long)evals);
   cta_lexmin(bd, bi, bj, s_rd, s_ri, s_rj, lane, warp, NW);
   TwoOptRes* out = a.res + (size_t)p * a.chunks;
-  for (int c = tid; c < a.chunks; c += NT)
-    out[c] = c == 0 ? TwoOptRes{bd, bi, bj} : TwoOptRes{kInf, INT_MAX, INT_MAX};
+  if (!a.apply) {
+    for (int c = tid; c < a.chunks; c += NT)
+      out[c] = c == 0 ? TwoOptRes{bd, bi, bj}
+                      : TwoOptRes{kInf, INT_MAX, INT_MAX};
+    return;
+  }
+  // ---- the apply (k_two_opt_apply's steps, solver.py:101-104, 309-316):
+  // reverse a[i+1 .. j] when delta < -1e-12, refresh the edge costs,
+  // fitness += delta, pbest; the apply kernel skips this particle
+  __shared__ int s_mv[3];
+  __shared__ double s_dl;
+  __shared__ int s_bt;
+  if (tid == 0) {
+    const int move = bd < -1e-12;  // n >= 4 here
+    s_mv[0] = move;
+    s_mv[1] = bi;
+    s_mv[2] = bj;
+    s_dl = move ? bd : 0.0;
+    if (a.delta_out) a.delta_out[p] = s_dl;
+    out[0] = TwoOptRes{kInf, kAppliedTag, kAppliedTag};
+  }
+  __syncthreads();
+  if (!s_mv[0]) return;
+  const int i = s_mv[1], j = s_mv[2], len = j - i;
+  uint16_t* t = a.tours_rw + (size_t)p * a.np;
+  double* dgw = a.dcache_rw + (size_t)p * a.np;
+  // the new tour from the shared copy: positions i+1 .. j reversed
+  for (int u = i + 1 + tid; u <= j; u += NT) t[u] = tr[i + j + 1 - u];
+  if (a.sym) {
+    // symmetric matrix: edge k in (i, j) of the new tour is old edge
+    // i + j - k reversed (same cost bits); edges i and j are new
+    const int m = len - 1;
+    for (int u = tid; u < m / 2; u += NT) {
+      const double y = dgw[i + 1 + u];
+      dgw[i + 1 + u] = dgw[j - 1 - u];
+      dgw[j - 1 - u] = y;
+    }
+    if (tid < 2) {
+      const int k = tid == 0 ? i : j;
+      const int x = tid == 0 ? tr[i] : tr[i + 1];
+      const int y = tid == 0 ? tr[j] : tr[j + 1];  // tr[n] = a_0
+      dgw[k] = ld_cost(a.cost + (size_t)x * a.ld + y);
+    }
+  } else {
+    for (int k = i + tid; k <= j; k += NT) {
+      // new edge k: (new a_k, new a_{k+1}) from the shared old tour
+      const int x = k == i ? tr[i] : tr[i + j + 1 - k];
+      const int y = k == j ? tr[j + 1] : tr[i + j - k];
+      dgw[k] = ld_cost(a.cost + (size_t)x * a.ld + y);
+    }
+  }
+  if (a.fit) {
+    if (tid == 0) {
+      const double f = __dadd_rn(a.fit[p], s_dl);
+      a.fit[p] = f;
+      s_bt = f < a.pfit[p];
+      if (s_bt) a.pfit[p] = f;
+    }
+    __syncthreads();
+    if (s_bt) {
+      uint16_t* pb = a.pbest + (size_t)p * a.np;
+      for (int u = tid; u < n; u += NT)
+        pb[u] = (u > i && u <= j) ? tr[i + j + 1 - u] : tr[u];
+    }
+  }
 }
 
 // Off-diagonal row and column minima {r(c), q(c)}, rounded down to fp32
@@ -599,7 +673,7 @@ cudaError_t launch_two_opt_bound(const TwoOptPlan& pl, int32_t n, int32_t np,
                                  const uint16_t* tours, const double* dcache,
                                  int32_t count, TwoOptRes* res, int32_t chunks,
                                  const DevCtl* ctl, cudaStream_t s,
-                                 int32_t* runs) {
+                                 int32_t* runs, const BoundApply* ap) {
   BoundArgs a;
   memset(&a, 0, sizeof a);
   a.cost = pl.cost;
@@ -625,6 +699,16 @@ cudaError_t launch_two_opt_bound(const TwoOptPlan& pl, int32_t n, int32_t np,
   a.vfrom = pl.band_vfrom;
   a.vto = pl.band_vto;
   a.runs = runs;
+  if (ap) {
+    a.apply = 1;
+    a.sym = pl.symmetric;
+    a.tours_rw = ap->tours;
+    a.dcache_rw = ap->dcache;
+    a.fit = ap->fit;
+    a.pfit = ap->pfit;
+    a.pbest = ap->pbest;
+    a.delta_out = ap->delta_out;
+  }
   if (const char* e = getenv("DPSO_BOUND_PEEL")) a.maxpeel = atoi(e);
   // small swarms: 256 threads per particle (shorter per-particle latency
   // chains; 128 and 512 measured slower at C2: 0.066 / 0.055 vs 0.050 ms);
