@@ -323,7 +323,9 @@ def kernels_per_generation(cfg, band=0, bound=0):
         # apply re-scans a FILTER overflow itself)
         k += 2 if bound else band_kernels(cfg, band)
         k += 2
-    m = 6          # mutation: hash, rank, dedupe, verify, lists, copy
+    # mutation: hash, rank, dedupe, verify, lists, copy (P <= 1024: rank,
+    # dedupe, verify and lists in one single-CTA kernel)
+    m = 3 if cfg["P"] <= 1024 else 6
     if RNG == "philox":
         m += 1     # Philox sampler
     else:

@@ -243,6 +243,117 @@ __global__ void __launch_bounds__(1024) k_mut_lists(SwarmView v) {
   }
 }
 
+// Swarms of P <= 1024: rank, dedupe, verify and lists in one CTA (one
+// launch instead of four).  Rank: a bitonic sort of (fitness key, slot);
+// dedupe: a bitonic sort of (hash, rank), each particle's candidate the
+// first (lowest-ranked) member of its hash group - the values k_mut_rank /
+// k_mut_dedupe compute by counting; then k_mut_verify's exact check by
+// warps and k_mut_lists' scans.
+template <typename K>
+__device__ __forceinline__ void block_bitonic_1024(K* key, int* val) {
+  const int tid = threadIdx.x;
+  for (int k = 2; k <= 1024; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int ixj = tid ^ j;
+      if (ixj > tid) {
+        const K a = key[tid], b = key[ixj];
+        const int va = val[tid], vb = val[ixj];
+        const bool gt = a > b || (a == b && va > vb);
+        if (gt == ((tid & k) == 0)) {
+          key[tid] = b;
+          key[ixj] = a;
+          val[tid] = vb;
+          val[ixj] = va;
+        }
+      }
+      __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_mut_small(SwarmView v,
+                                                   const int32_t* canon) {
+  if (!v.ctl->mutating || v.ctl->done) return;
+  __shared__ unsigned long long s_k[1024];
+  __shared__ int s_v[1024];
+  __shared__ int s_w[32];
+  const int P = v.P, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // ---- rank: (fitness, slot) order (solver.py:223-224)
+  s_k[tid] = tid < P ? fit_key(v.fit[tid]) : ~0ull;
+  s_v[tid] = tid < P ? tid : 0x7fffffff;
+  __syncthreads();
+  block_bitonic_1024(s_k, s_v);
+  if (tid < P) {
+    v.rank[s_v[tid]] = tid;
+    v.order[tid] = s_v[tid];
+  }
+  __syncthreads();
+  // ---- dedupe candidates: the lowest-ranked particle of each hash group
+  s_k[tid] = tid < P ? v.hash[tid] : ~0ull;
+  s_v[tid] = tid < P ? v.rank[tid] : 0x7fffffff;
+  __syncthreads();
+  block_bitonic_1024(s_k, s_v);
+  if (tid < P) {
+    int q0 = tid;
+    while (q0 > 0 && s_k[q0 - 1] == s_k[tid]) --q0;
+    const int r = s_v[tid], r0 = s_v[q0];
+    v.flag[v.order[r]] = r0 < r ? r0 : 0x7fffffff;
+  }
+  __syncthreads();
+  // ---- verify (k_mut_verify): one warp per particle
+  for (int i = warp; i < P; i += 32) {
+    const int crank = v.flag[i];
+    if (crank == 0x7fffffff) {
+      if (lane == 0) v.flag[i] = 0;
+      continue;
+    }
+    const int cand = v.order[crank];
+    int dropped = warp_canon_equal(v, canon, i, cand);
+    if (!dropped) {
+      if (lane == 0) v.ctl->collision = 1;
+      const uint64_t hi = v.hash[i];
+      const int ri = v.rank[i];
+      for (int j = 0; j < P && !dropped; ++j)
+        if (j != cand && v.hash[j] == hi && v.rank[j] < ri)
+          dropped = warp_canon_equal(v, canon, i, j);
+    }
+    if (lane == 0) v.flag[i] = dropped;
+  }
+  __syncthreads();
+  // ---- lists (k_mut_lists, one 1024-block: P <= 1024)
+  {
+    const int r = tid;
+    const int i = r < P ? v.order[r] : 0;
+    const int sv = (r < P) ? !v.flag[i] : 0;
+    int tot;
+    const int ex = block_scan_excl<1024>(sv, s_w, &tot);
+    if (r < P) {
+      if (sv) {
+        v.sidx[i] = ex;
+        v.surv_list[ex] = i;
+      } else {
+        v.sidx[i] = r - ex;  // dropped index in rank order
+      }
+    }
+    const int S = tot;
+    const int nkeep = (S + 2) / 3;  // ceil(S / 3)
+    __syncthreads();
+    int kp = 0;
+    if (tid < P) {
+      kp = !v.flag[tid] && v.sidx[tid] < nkeep;
+      v.keep[tid] = kp;
+    }
+    const int e = (tid < P) && !kp;
+    int tot2;
+    const int ex2 = block_scan_excl<1024>(e, s_w, &tot2);
+    if (e) v.ev_slot[ex2] = tid;
+    if (tid == 0) {
+      v.ctl->n_surv = S;
+      v.ctl->n_drop = P - S;
+      v.ctl->n_events = tot2;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(128) k_mut_copy(SwarmView v) {
   if (!v.ctl->mutating || v.ctl->done) return;
   const int p = blockIdx.x;
@@ -1101,11 +1212,15 @@ cudaError_t launch_mutation_pre(const SwarmView& v, cudaStream_t s) {
   // k_mut_lists rewrites it
   int32_t* canon = v.keep;
   k_mut_hash<<<P, 128, 0, s>>>(v, canon);
-  const dim3 g2((P + 255) / 256, (P + kChunk - 1) / kChunk);
-  k_mut_rank<<<g2, 256, 0, s>>>(v);
-  k_mut_dedupe<<<g2, 256, 0, s>>>(v);
-  k_mut_verify<<<(P + 3) / 4, 128, 0, s>>>(v, canon);
-  k_mut_lists<<<1, 1024, 0, s>>>(v);
+  if (P <= 1024 && !getenv("DPSO_MUT_GRID")) {
+    k_mut_small<<<1, 1024, 0, s>>>(v, canon);
+  } else {
+    const dim3 g2((P + 255) / 256, (P + kChunk - 1) / kChunk);
+    k_mut_rank<<<g2, 256, 0, s>>>(v);
+    k_mut_dedupe<<<g2, 256, 0, s>>>(v);
+    k_mut_verify<<<(P + 3) / 4, 128, 0, s>>>(v, canon);
+    k_mut_lists<<<1, 1024, 0, s>>>(v);
+  }
   k_mut_copy<<<P, 128, 0, s>>>(v);
   return cudaGetLastError();
 }
