@@ -216,6 +216,7 @@ struct dpso_ctx {
   cudaStream_t stream;
   cudaStream_t stream2;  // fork for the mutation-stream walk
   cudaEvent_t ev, ev_fork, ev_join;
+  cudaEvent_t ev_fix;  // the mutating graph's stream state is final
   cudaGraphExec_t graph;        // a generation with the mutation call
   cudaGraphExec_t graph_plain;  // a generation without it (gen % period)
   int64_t gen_next = 1;         // generation the next launch runs
@@ -292,7 +293,8 @@ static cudaError_t enqueue_generation(const SwarmView& v, cudaStream_t s,
                                       cudaStream_t s2, cudaEvent_t fork,
                                       cudaEvent_t join,
                                       bool with_mutation = true,
-                                      int walk = kWalkAfterMutation) {
+                                      int walk = kWalkAfterMutation,
+                                      cudaEvent_t fix = nullptr) {
   cudaError_t e;
 #define STAGE(name, call)      \
   do {                         \
@@ -306,6 +308,12 @@ static cudaError_t enqueue_generation(const SwarmView& v, cudaStream_t s,
   if (mut) {
     STAGE("mutation_pre", launch_mutation_pre(v, s));
     STAGE("mutation_post", launch_mutation_post(v, s));
+    // kWalkNone: the next call's walk (launched by the host after this
+    // graph) may start as soon as the stream state is final - an external
+    // event record node it waits on
+    if (walk == kWalkNone && fix)
+      STAGE("fix_event",
+            cudaEventRecordWithFlags(fix, s, cudaEventRecordExternal));
     if (walk == kWalkAfterMutation) {
       // the next call's stream walk overlaps the rest of this generation
       STAGE("fork", cudaEventRecord(fork, s));
@@ -505,6 +513,7 @@ int dpso_create(const dpso_params* prm, int32_t n, void* dev_workspace,
   cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_fix, cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking);
   c->host_ctl = pinned_ctl_get();
   SwarmView& v = c->v;
@@ -753,12 +762,17 @@ int dpso_init(dpso_ctx* c, const int32_t* seed_body, int32_t n_seed) {
 // not (gen % mutation_period != 0: the mutation kernels would only exit at
 // entry).  The host knows which generation each launch runs (gen_next; a
 // generation after the stall break is a no-op either way).
+static bool walk_early(const dpso_ctx* c);
+
 static int capture_generation(dpso_ctx* c, bool with_mutation, int walk,
                               cudaGraphExec_t* out) {
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-  cudaError_t e = enqueue_generation(c->v, c->stream, c->stream2, c->ev_fork,
-                                     c->ev_join, with_mutation, walk);
+  cudaError_t e = enqueue_generation(
+      c->v, c->stream, c->stream2, c->ev_fork, c->ev_join, with_mutation,
+      walk, with_mutation && walk == kWalkNone && walk_early(c)
+                ? c->ev_fix
+                : nullptr);
   cudaError_t e2 = cudaStreamEndCapture(c->stream, &g);
   if (e) {
     std::string where = std::string("capture generation (") + g_stage + ")";
@@ -769,6 +783,16 @@ static int capture_generation(dpso_ctx* c, bool with_mutation, int walk,
   cudaGraphDestroy(g);
   if (e) return cuda_fail(e, "cudaGraphInstantiate");
   return DPSO_OK;
+}
+
+// The next call's walk starts at the mutating graph's event node right
+// after the call's stream update (large swarms: C3 14.5 -> 14.9 M, C4 5.1
+// -> 5.4 M particle-iter/s) or after the whole mutating generation (small
+// swarms, where the one-SM walk then competes with the 2-opt scan: C2 0.148
+// vs 0.150 ms per step).  DPSO_WALK_LATE=0/1 overrides.
+static bool walk_early(const dpso_ctx* c) {
+  if (const char* e = getenv("DPSO_WALK_LATE")) return atoi(e) == 0;
+  return c->prm.n_particles >= 4096;
 }
 
 static bool walk_eager(const dpso_ctx* c) {
@@ -847,9 +871,14 @@ static cudaError_t launch_generation(dpso_ctx* c) {
   if ((e = cudaGraphLaunch(mut ? c->graph : c->graph_plain, c->stream)))
     return e;
   if (!eager) return cudaSuccess;
-  // the next call's walk, concurrent with the generations until then
-  if ((e = cudaEventRecord(c->ev_fork, c->stream))) return e;
-  if ((e = cudaStreamWaitEvent(c->stream2, c->ev_fork, 0))) return e;
+  // the next call's walk, concurrent with the generations until then: it
+  // starts at the mutating graph's event node right after the call's
+  // stream update (k_mut_fix), overlapping the rest of this generation
+  const bool early = walk_early(c);
+  if (!early && (e = cudaEventRecord(c->ev_fork, c->stream))) return e;
+  if ((e = cudaStreamWaitEvent(c->stream2, early ? c->ev_fix : c->ev_fork,
+                               0)))
+    return e;
   if ((e = launch_mutation_walk(c->v, c->stream2))) return e;
   return cudaEventRecord(c->ev_join, c->stream2);
 }
@@ -1207,6 +1236,7 @@ void dpso_destroy(dpso_ctx* c) {
   if (c->ev) cudaEventDestroy(c->ev);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->ev_fix) cudaEventDestroy(c->ev_fix);
   if (c->stream2) cudaStreamDestroy(c->stream2);
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->vel_owned) cudaFree(c->vel_owned);
