@@ -681,15 +681,19 @@ __global__ void __launch_bounds__(kWalkThreads) k_mut_walk(SwarmView v) {
         uint32_t f = (uint32_t)(p - sv.h);
         const uint32_t fend = (uint32_t)(wend - sv.h);
         if (skips) {
+          // the stores are unconditional (a rejected k-draw's slot is
+          // overwritten by the next event): no branch on the chain
+          int64_t* cur = s.cur;
+          int32_t* off = s.off;
+          const int64_t h1 = sv.h + 1;
           while (f < fend && nb < nev) {
             const uint32_t sk = sring[f & kMask];
-            if (sk != 0) {
-              s.cur[nb] = sv.h + f + 1;
-              s.off[nb] = tot;
-            }
-            tot += sk != 0 ? (int)sk - 1 : 0;
-            nb += sk != 0;
-            f += sk != 0 ? sk : 1u;
+            const int acc = sk != 0u;
+            cur[nb] = h1 + f;
+            off[nb] = tot;
+            tot += acc ? (int)sk - 1 : 0;
+            nb += acc;
+            f += acc ? sk : 1u;
           }
         } else {
           while (f < fend && nb < nev) {
