@@ -833,12 +833,11 @@ struct ApplyArgs {
   // whose band-scan candidate list overflowed (tagged result, rare) is
   // re-scanned in fp64 here, by its CTA
   int ovf_scan;
+  const int32_t* plist;  // nullable: only these particles (count in *pcnt)
+  const int32_t* pcnt;
 };
 
-__global__ void __launch_bounds__(128) k_two_opt_apply(ApplyArgs a) {
-  if (a.ctl && (a.ctl->done || a.ctl->improved)) return;
-  const int p = blockIdx.x;
-  if (p >= a.count) return;
+__device__ void apply_one(const ApplyArgs& a, int p) {
   __shared__ int s_move[3];
   __shared__ double s_delta;
   __shared__ int s_better;
@@ -974,6 +973,25 @@ __global__ void __launch_bounds__(128) k_two_opt_apply(ApplyArgs a) {
       for (int u = tid; u < a.n; u += blockDim.x) pb[u] = t[u];
     }
   }
+}
+
+
+// One CTA per particle; with a particle list (bounded-scan mode: the band
+// scan's fallbacks, the others were applied by the bounded scan) a small
+// grid strides over the list.
+__global__ void __launch_bounds__(128) k_two_opt_apply(ApplyArgs a) {
+  if (a.ctl && (a.ctl->done || a.ctl->improved)) return;
+  if (a.plist) {
+    const int cnt = *a.pcnt;
+    for (int q = blockIdx.x; q < cnt; q += gridDim.x) {
+      apply_one(a, a.plist[q]);
+      __syncthreads();
+    }
+    return;
+  }
+  const int p = blockIdx.x;
+  if (p >= a.count) return;
+  apply_one(a, p);
 }
 
 // ---- cost-matrix preparation ------------------------------------------------
@@ -1483,7 +1501,16 @@ cudaError_t launch_two_opt_core(const TwoOptPlan& pl, int32_t n, int32_t np,
     if (delta_out) cudaMemsetAsync(delta_out, 0, sizeof(double) * count, s);
     return cudaGetLastError();
   }
-  if (count > 0) k_two_opt_apply<<<count, 128, 0, s>>>(b);
+  b.plist = nullptr;
+  b.pcnt = nullptr;
+  int grid = count;
+  if (pl.bound && (parts & 1) && dcache_rw && !getenv("DPSO_BOUND_NOAPPLY")) {
+    // the bounded scan applied every move it resolved: only its fallbacks
+    b.plist = pl.bound_fb + 1;
+    b.pcnt = pl.bound_fb;
+    grid = std::min(count, 148);
+  }
+  if (count > 0) k_two_opt_apply<<<grid, 128, 0, s>>>(b);
   return cudaGetLastError();
 }
 
